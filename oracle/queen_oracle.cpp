@@ -1,0 +1,554 @@
+// QUEEN per-frame decode -> apply -> 3D-GS splat: CPU ORACLE.
+//
+// TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+// cpu_baseline / --impl reference legs may load this library.  The product path
+// (paper_2412_04469_b200/) never links, imports or executes anything under oracle/,
+// and this file shares no code, header, table or constant generator with csrc/.
+//
+// Plain, slow, literal scalar C++17.  Each function cites the passage it follows:
+//   P:n  = /root/reference/PAPER.md line n (section / equation named beside it)
+//   S:n  = /root/reference/SPEC.md line n (interfaces / test ideas only)
+//   R#n  = DESIGN.md reading #n (where the paper is silent)
+//
+// Arithmetic contract: IEEE fp32, round to
+// nearest even, no FMA contraction (compiled with -ffp-contract=off, no fast-math),
+// fmaf() only where written.  The operation order below IS the contract that the
+// GPU path reproduces bit-for-bit for every value that decides an integer (cull,
+// tile rect, skip test, mask, quantised latent).  OpenMP is used only to spread
+// independent elements over host cores for timing; it never changes per-element
+// arithmetic or any result.
+//
+// Parity pins: every function here is pinned by tests/test_oracle_*.py against
+// closed forms, paper/SPEC worked examples, invariants, brute force and double
+// precision.  No function is "parity unpinned".
+
+#pragma STDC FP_CONTRACT OFF
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+#include <tuple>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+extern "C" {
+
+// ---------------------------------------------------------------------------
+// bit helpers
+// ---------------------------------------------------------------------------
+static inline float f_from_bits(uint32_t b) { float f; std::memcpy(&f, &b, 4); return f; }
+static inline uint32_t bits_of(float f) { uint32_t b; std::memcpy(&b, &f, 4); return b; }
+
+// ---------------------------------------------------------------------------
+// det_exp / det_log: deterministic exp / log built only from IEEE + - * / fmaf
+// rintf fminf fmaxf and bit casts (R#8).  The exp / log are
+// the activations of the 3D-GS parameterisation the paper builds on (P:213-215,
+// scale s = exp(log s), opacity = sigmoid(logit)) and of the hard-concrete gate
+// sigmoid.  Pinned against double libm (<= 2 ulp) in tests.
+// ---------------------------------------------------------------------------
+float oracle_det_exp(float x) {
+    const float L2E = f_from_bits(0x3fb8aa3bu);     // log2(e)
+    const float LN2_HI = f_from_bits(0x3f317200u);  // 6.9314575195e-01
+    const float LN2_LO = f_from_bits(0x35bfbe8eu);  // 1.4286067653e-06
+    x = std::fmin(std::fmax(x, -87.0f), 88.0f);
+    float k = std::rint(x * L2E);
+    float r = std::fma(-k, LN2_HI, x);
+    r = std::fma(-k, LN2_LO, r);
+    // Taylor series of e^r, Horner, degree 7
+    float p = 1.0f / 5040.0f;
+    p = std::fma(p, r, 1.0f / 720.0f);
+    p = std::fma(p, r, 1.0f / 120.0f);
+    p = std::fma(p, r, 1.0f / 24.0f);
+    p = std::fma(p, r, 1.0f / 6.0f);
+    p = std::fma(p, r, 0.5f);
+    p = std::fma(p, r, 1.0f);
+    p = std::fma(p, r, 1.0f);
+    int ki = (int)k;
+    float scale = f_from_bits((uint32_t)(ki + 127) << 23);  // 2^k, k in [-126, 127]
+    return p * scale;
+}
+
+float oracle_det_log(float y) {  // y: normal, > 0
+    const float LN2_HI = f_from_bits(0x3f317200u);
+    const float LN2_LO = f_from_bits(0x35bfbe8eu);
+    uint32_t b = bits_of(y);
+    int e = (int)((b >> 23) & 255u) - 127;
+    float m = f_from_bits((b & 0x7fffffu) | 0x3f800000u);  // m in [1, 2)
+    if (m > 1.41421356f) { m = m * 0.5f; e += 1; }
+    float f = m - 1.0f;
+    float s = f / (2.0f + f);
+    float z = s * s;
+    // ln(1+f) = 2 atanh(s) = 2s + s*R(z), R = z*(2/3 + 2/5 z + 2/7 z^2 + 2/9 z^3)
+    float R = std::fma(z, 2.0f / 9.0f, 2.0f / 7.0f);
+    R = std::fma(z, R, 2.0f / 5.0f);
+    R = std::fma(z, R, 2.0f / 3.0f);
+    R = z * R;
+    float hfsq = (0.5f * f) * f;
+    float lnm = f - (hfsq - s * (hfsq + R));
+    float ef = (float)e;
+    return std::fma(ef, LN2_HI, std::fma(ef, LN2_LO, lnm));
+}
+
+// ---------------------------------------------------------------------------
+// a1. Quantise trainer-state latents: l = round(l_hat) (Eq. 5 "rounded
+// to the nearest integer"); tie rule half away from zero (R#5).  Returns the
+// number of entries whose |l| > 127 (wire range, R#4); those are stored clamped.
+// ---------------------------------------------------------------------------
+int64_t oracle_quantize(const float* lhat, int8_t* q, int64_t count) {
+    int64_t bad = 0;
+    for (int64_t j = 0; j < count; ++j) {
+        float r = std::round(lhat[j]);  // C round(): half away from zero
+        if (!(r >= -127.0f && r <= 127.0f)) { ++bad; r = r < 0 ? -127.0f : 127.0f; }
+        q[j] = (int8_t)(int)r;
+    }
+    return bad;
+}
+
+// residual dimension M_c per category (rot, scale, opacity, sh_dc, sh_rest):
+// P:290-292 footnote (categories), P:447 (separate decoders), R#2/R#3.
+static void category_m(int deg, int M[5]) {
+    int B = (deg + 1) * (deg + 1);
+    M[0] = 4; M[1] = 3; M[2] = 1; M[3] = 3; M[4] = 3 * (B - 1);
+}
+
+// ---------------------------------------------------------------------------
+// a2. Latent decode r_i = D . float(l_i) (Eq. 5), one decoder per
+// category per frame.  Accumulation order (R#7): ascending k,
+// from +0.0f, one fmaf per term.  resid: float [sum M_c][n_pad], row m of
+// category c at row (sum_{c'<c} M_c') + m, which is plane 3 + that row.
+// ---------------------------------------------------------------------------
+void oracle_decode(int n, int n_pad, int deg, const int* lat, const int8_t* q,
+                   const float* dec, float* resid) {
+    int M[5];
+    category_m(deg, M);
+    int lat_row = 0, dec_off = 0, out_row = 0;
+    for (int c = 0; c < 5; ++c) {
+        int L = lat[c];
+        if (L == 0) { out_row += M[c]; continue; }  // category absent: residual 0
+        for (int m = 0; m < M[c]; ++m) {
+            for (int i = 0; i < n; ++i) {
+                float r = +0.0f;
+                for (int k = 0; k < L; ++k)
+                    r = std::fma(dec[dec_off + m * L + k], (float)q[(int64_t)(lat_row + k) * n_pad + i], r);
+                resid[(int64_t)(out_row + m) * n_pad + i] = r;
+            }
+        }
+        lat_row += L;
+        dec_off += M[c] * L;
+        out_row += M[c];
+    }
+    // category with L == 0: rows already counted; write zeros for them
+    out_row = 0;
+    for (int c = 0; c < 5; ++c) {
+        if (lat[c] == 0)
+            for (int m = 0; m < M[c]; ++m)
+                for (int i = 0; i < n; ++i) resid[(int64_t)(out_row + m) * n_pad + i] = 0.0f;
+        out_row += M[c];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a3 + a5. Apply A_t = A_{t-1} + R_t (Eq. 4) on the raw non-position
+// planes (R#1), then the COO position residual p[I_k] += E_p[k].
+// planes: float [11+3B][n_pad]; non-position plane 3+row receives resid row.
+// Returns 0, or -3 if a COO index is >= n or indices are not strictly increasing.
+// ---------------------------------------------------------------------------
+int oracle_apply(int n, int n_pad, int deg, const int* lat, const int8_t* q, const float* dec,
+                 float* planes, int k, const uint32_t* idx, const float* val) {
+    int M[5];
+    category_m(deg, M);
+    int Mtot = M[0] + M[1] + M[2] + M[3] + M[4];
+    std::vector<float> resid((size_t)Mtot * n_pad, 0.0f);
+    oracle_decode(n, n_pad, deg, lat, q, dec, resid.data());
+    for (int m = 0; m < Mtot; ++m)
+        for (int i = 0; i < n; ++i)
+            planes[(int64_t)(3 + m) * n_pad + i] = planes[(int64_t)(3 + m) * n_pad + i] + resid[(int64_t)m * n_pad + i];
+    int err = 0;
+    for (int j = 0; j < k; ++j) {
+        if (idx[j] >= (uint32_t)n || (j > 0 && idx[j] <= idx[j - 1])) { err = -3; continue; }
+        for (int d = 0; d < 3; ++d)
+            planes[(int64_t)d * n_pad + idx[j]] = planes[(int64_t)d * n_pad + idx[j]] + val[(int64_t)d * k + j];
+    }
+    return err;
+}
+
+// ---------------------------------------------------------------------------
+// a4. Hard-concrete gate: g_hat = sigmoid(log alpha / tau),
+// g_tilde = g_hat (gamma1 - gamma0) + gamma0, g = min(1, max(0, g_tilde)).
+// Deterministic at inference (R#6).  The sigmoid is 1/(1+det_exp(-x)).
+// ---------------------------------------------------------------------------
+float oracle_gate_value(float log_alpha, float tau, float gamma0, float gamma1) {
+    float ghat = 1.0f / (1.0f + oracle_det_exp((-log_alpha) / tau));
+    float gt = std::fma(ghat, gamma1 - gamma0, gamma0);
+    return std::fmin(1.0f, std::fmax(0.0f, gt));
+}
+
+// Gate -> mask -> COO (P:319-320 dp = g l_p; P:1389 I = {i : g_i != 0}).
+// mask_i = (log alpha_i > theta0), theta0 = tau ln(-gamma0/gamma1) computed in
+// double by the caller and rounded to float (R#6: the exact threshold where
+// g_tilde crosses 0; the same shift as Eq. 8).  Writes ascending indices
+// and values dp = g * l_p ([3][n_pad] layout in, [3][cap] out).  Returns k.
+// ---------------------------------------------------------------------------
+int oracle_gate(int n, int n_pad, const float* log_alpha, const float* lp, float tau, float gamma0,
+                float gamma1, float theta0, uint32_t* idx_out, float* val_out, int cap) {
+    int k = 0;
+    for (int i = 0; i < n; ++i) {
+        if (!(log_alpha[i] > theta0)) continue;
+        float g = oracle_gate_value(log_alpha[i], tau, gamma0, gamma1);
+        if (k < cap) {
+            idx_out[k] = (uint32_t)i;
+            for (int d = 0; d < 3; ++d) val_out[(int64_t)d * cap + k] = g * lp[(int64_t)d * n_pad + i];
+        }
+        ++k;
+    }
+    return k;
+}
+
+// ---------------------------------------------------------------------------
+// Real SH basis, degree <= 3, 3D-GS constants and signs (R#10; "view-
+// dependent RGB value c_i computed from h_i").  Pinned in tests against
+// scipy.special spherical harmonics and quadrature orthonormality.
+// ---------------------------------------------------------------------------
+void oracle_sh_basis(int deg, float x, float y, float z, float* Y) {
+    const float C0 = 0.28209479177387814f;
+    const float C1 = 0.4886025119029199f;
+    const float C2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
+                         -1.0925484305920792f, 0.5462742152960396f};
+    const float C3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f, 0.3731763325901154f,
+                         -0.4570457994644658f, 1.445305721320277f, -0.5900435899266435f};
+    Y[0] = C0;
+    if (deg < 1) return;
+    Y[1] = -C1 * y;
+    Y[2] = C1 * z;
+    Y[3] = -C1 * x;
+    if (deg < 2) return;
+    float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    Y[4] = C2[0] * xy;
+    Y[5] = C2[1] * yz;
+    Y[6] = C2[2] * (2.0f * zz - xx - yy);
+    Y[7] = C2[3] * xz;
+    Y[8] = C2[4] * (xx - yy);
+    if (deg < 3) return;
+    Y[9] = C3[0] * y * (3.0f * xx - yy);
+    Y[10] = C3[1] * xy * z;
+    Y[11] = C3[2] * y * (4.0f * zz - xx - yy);
+    Y[12] = C3[3] * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    Y[13] = C3[4] * x * (4.0f * zz - xx - yy);
+    Y[14] = C3[5] * z * (xx - yy);
+    Y[15] = C3[6] * x * (xx - 3.0f * yy);
+}
+
+// camera record: 24 words  fx fy cx cy R[9] t[3] C[3] limx limy near | width height (int32)
+struct Cam {
+    float fx, fy, cx, cy, R[9], t[3], C[3], limx, limy, near_z;
+    int W, H;
+};
+static Cam load_cam(const float* w) {
+    Cam c;
+    c.fx = w[0]; c.fy = w[1]; c.cx = w[2]; c.cy = w[3];
+    for (int j = 0; j < 9; ++j) c.R[j] = w[4 + j];
+    for (int j = 0; j < 3; ++j) { c.t[j] = w[13 + j]; c.C[j] = w[16 + j]; }
+    c.limx = w[19]; c.limy = w[20]; c.near_z = w[21];
+    std::memcpy(&c.W, &w[22], 4);
+    std::memcpy(&c.H, &w[23], 4);
+    return c;
+}
+
+// ---------------------------------------------------------------------------
+// a6 + a7. Projection of Gaussian i into view v (Eq. 1; colour P:226).
+// Records (R#13, R#14): rec[12] = u, v, A2, B2 | C2, T2, o, 0 | r, g, b, 0
+//   A2,B2,C2 = base-2 conic: p2 = A2 dx^2 + B2 dx dy + C2 dy^2 = -0.5 log2(e) d^T S'^-1 d
+//   T2 = log2(1/(255 o)): alpha < 1/255  <=>  p2 < T2
+// depth = bits(z_c); tiles = #16x16 tiles of the opacity-aware extent; rect = tile
+// rect (tx0, ty0, tx1, ty1) inclusive.  A culled Gaussian gets all zeros.
+// Returns 1 if any Gaussian had a non-finite input (culled + QUEEN_WARN_NONFINITE).
+// ---------------------------------------------------------------------------
+static int project_one(int i, int n_pad, int deg, const float* pl, const Cam& c, float* rec, uint32_t* depth,
+                       uint32_t* tiles, int16_t* rect) {
+    const int B = (deg + 1) * (deg + 1);
+    const int P = 11 + 3 * B;
+    for (int j = 0; j < 12; ++j) rec[j] = 0.0f;
+    *depth = 0; *tiles = 0;
+    rect[0] = rect[1] = rect[2] = rect[3] = 0;
+    // 0. non-finite input -> cull (must precede fminf/fmaxf, which would hide a NaN)
+    for (int p = 0; p < P; ++p)
+        if (!std::isfinite(pl[(int64_t)p * n_pad + i])) return 1;
+    const float px = pl[0 * (int64_t)n_pad + i], py = pl[1 * (int64_t)n_pad + i], pz = pl[2 * (int64_t)n_pad + i];
+    // 1. camera transform x_c = W p (P:220 viewing transform W), near cull (R#11)
+    const float* Rw = c.R;
+    float xc = std::fma(Rw[0], px, std::fma(Rw[1], py, std::fma(Rw[2], pz, c.t[0])));
+    float yc = std::fma(Rw[3], px, std::fma(Rw[4], py, std::fma(Rw[5], pz, c.t[1])));
+    float zc = std::fma(Rw[6], px, std::fma(Rw[7], py, std::fma(Rw[8], pz, c.t[2])));
+    if (!(zc > c.near_z)) return 0;
+    // 2. quaternion normalisation ("rotation matrix parameterized by a quaternion")
+    float qw = pl[3 * (int64_t)n_pad + i], qx = pl[4 * (int64_t)n_pad + i], qy = pl[5 * (int64_t)n_pad + i],
+          qz = pl[6 * (int64_t)n_pad + i];
+    float n2 = std::fma(qw, qw, std::fma(qx, qx, std::fma(qy, qy, qz * qz)));
+    if (!(n2 > 0.0f)) return 0;
+    float inv = 1.0f / std::sqrt(n2);
+    qw = qw * inv; qx = qx * inv; qy = qy * inv; qz = qz * inv;
+    // 3. Sigma = R S S^T R^T, s = exp(log s) (R#8)
+    float s[3];
+    for (int j = 0; j < 3; ++j) s[j] = oracle_det_exp(pl[(int64_t)(7 + j) * n_pad + i]);
+    float Rq[9];
+    Rq[0] = 1.0f - 2.0f * std::fma(qy, qy, qz * qz);
+    Rq[1] = 2.0f * (qx * qy - qw * qz);
+    Rq[2] = 2.0f * (qx * qz + qw * qy);
+    Rq[3] = 2.0f * (qx * qy + qw * qz);
+    Rq[4] = 1.0f - 2.0f * std::fma(qx, qx, qz * qz);
+    Rq[5] = 2.0f * (qy * qz - qw * qx);
+    Rq[6] = 2.0f * (qx * qz - qw * qy);
+    Rq[7] = 2.0f * (qy * qz + qw * qx);
+    Rq[8] = 1.0f - 2.0f * std::fma(qx, qx, qy * qy);
+    float Mm[9];
+    for (int j = 0; j < 3; ++j)
+        for (int m = 0; m < 3; ++m) Mm[j * 3 + m] = Rq[j * 3 + m] * s[m];
+    float S[9];
+    for (int j = 0; j < 3; ++j)
+        for (int k = j; k < 3; ++k) {
+            float v = std::fma(Mm[j * 3 + 0], Mm[k * 3 + 0], std::fma(Mm[j * 3 + 1], Mm[k * 3 + 1], Mm[j * 3 + 2] * Mm[k * 3 + 2]));
+            S[j * 3 + k] = v;
+            S[k * 3 + j] = v;
+        }
+    // 4. Jacobian of the affine approximation of the projective transform,
+    //    with the 3D-GS 1.3x frustum clamp (R#11)
+    float tx = xc / zc, ty = yc / zc;
+    float xcl = std::fmin(c.limx, std::fmax(-c.limx, tx)) * zc;
+    float ycl = std::fmin(c.limy, std::fmax(-c.limy, ty)) * zc;
+    float j00 = c.fx / zc;
+    float j02 = -(c.fx * xcl) / (zc * zc);
+    float j11 = c.fy / zc;
+    float j12 = -(c.fy * ycl) / (zc * zc);
+    // 5. Sigma' = J W Sigma W^T J^T (Eq. 1) + 0.3 px^2 (R#11)
+    float A[6];
+    for (int m = 0; m < 3; ++m) {
+        A[0 * 3 + m] = std::fma(j00, Rw[0 * 3 + m], j02 * Rw[2 * 3 + m]);
+        A[1 * 3 + m] = std::fma(j11, Rw[1 * 3 + m], j12 * Rw[2 * 3 + m]);
+    }
+    float Bm[6];
+    for (int r = 0; r < 2; ++r)
+        for (int m = 0; m < 3; ++m)
+            Bm[r * 3 + m] = std::fma(A[r * 3 + 0], S[0 * 3 + m], std::fma(A[r * 3 + 1], S[1 * 3 + m], A[r * 3 + 2] * S[2 * 3 + m]));
+    float a = std::fma(Bm[0], A[0], std::fma(Bm[1], A[1], Bm[2] * A[2]));
+    float b = std::fma(Bm[0], A[3], std::fma(Bm[1], A[4], Bm[2] * A[5]));
+    float cc2 = std::fma(Bm[3], A[3], std::fma(Bm[4], A[4], Bm[5] * A[5]));
+    a = a + 0.3f;
+    cc2 = cc2 + 0.3f;
+    // 6. conic = Sigma'^-1 (Eq. 2 exponent), largest eigenvalue for the extent
+    float det = std::fma(a, cc2, -(b * b));
+    if (!(det > 0.0f)) return 0;
+    float ca = cc2 / det, cb = -b / det, ccn = a / det;
+    float mid = 0.5f * (a + cc2);
+    float lam1 = mid + std::sqrt(std::fmax(0.1f, mid * mid - det));
+    // 7. opacity o = sigmoid(logit) in [0,1]; alpha can reach 1/255 only if 255 o > 1 (R#14)
+    float o = 1.0f / (1.0f + oracle_det_exp(-pl[10 * (int64_t)n_pad + i]));
+    if (!(255.0f * o > 1.0f)) return 0;
+    float e2 = 2.0f * oracle_det_log(255.0f * o);
+    // 8. opacity-aware radius: Mahalanobis^2 = 2 ln(255 o) along the major axis (R#13)
+    float rad = std::ceil(1.0001f * std::sqrt(e2 * lam1));
+    float u = std::fma(c.fx, tx, c.cx);
+    float v = std::fma(c.fy, ty, c.cy);
+    // 9. 16x16 tile rect (inclusive), clamped in float before the int conversion
+    int gx = (c.W + 15) / 16, gy = (c.H + 15) / 16;
+    float ftx0 = std::fmin(std::fmax(std::ceil(((u - rad) - 15.0f) * 0.0625f), 0.0f), (float)gx);
+    float ftx1 = std::fmin(std::fmax(std::floor((u + rad) * 0.0625f), -1.0f), (float)(gx - 1));
+    float fty0 = std::fmin(std::fmax(std::ceil(((v - rad) - 15.0f) * 0.0625f), 0.0f), (float)gy);
+    float fty1 = std::fmin(std::fmax(std::floor((v + rad) * 0.0625f), -1.0f), (float)(gy - 1));
+    int tx0 = (int)ftx0, tx1 = (int)ftx1, ty0 = (int)fty0, ty1 = (int)fty1;
+    uint32_t nt = (tx0 <= tx1 && ty0 <= ty1) ? (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1)) : 0u;
+    // 10. base-2 blend coefficients
+    const float L2E = 1.4426950408889634f;
+    float A2 = (-0.5f * ca) * L2E;
+    float B2 = (-cb) * L2E;
+    float C2 = (-0.5f * ccn) * L2E;
+    float T2 = -(0.5f * e2) * L2E;
+    // 11. view-dependent colour from SH, +0.5 and clamp at 0 (R#8)
+    float dx = px - c.C[0], dy = py - c.C[1], dz = pz - c.C[2];
+    float dn = std::sqrt(std::fma(dx, dx, std::fma(dy, dy, dz * dz)));
+    dx = dx / dn; dy = dy / dn; dz = dz / dn;
+    float Y[16];
+    oracle_sh_basis(deg, dx, dy, dz, Y);
+    float rgb[3];
+    for (int ch = 0; ch < 3; ++ch) {
+        float acc = Y[0] * pl[(int64_t)(11 + ch) * n_pad + i];
+        for (int bb = 1; bb < B; ++bb) acc = std::fma(Y[bb], pl[(int64_t)(11 + 3 * bb + ch) * n_pad + i], acc);
+        rgb[ch] = std::fmax(0.0f, acc + 0.5f);
+    }
+    rec[0] = u; rec[1] = v; rec[2] = A2; rec[3] = B2;
+    rec[4] = C2; rec[5] = T2; rec[6] = o; rec[7] = 0.0f;
+    rec[8] = rgb[0]; rec[9] = rgb[1]; rec[10] = rgb[2]; rec[11] = 0.0f;
+    *depth = bits_of(zc);  // 12. depth key: z_c > 0 so its bits order like the float (R#15)
+    *tiles = nt;
+    rect[0] = (int16_t)tx0; rect[1] = (int16_t)ty0; rect[2] = (int16_t)tx1; rect[3] = (int16_t)ty1;
+    return 0;
+}
+
+// batch of views: cams [V][24]; rec [V][n_pad][12]; depth/tiles [V][n_pad]; rect [V][n_pad][4]
+int oracle_project(int n, int n_pad, int deg, const float* planes, int V, const float* cams, float* rec,
+                   uint32_t* depth, uint32_t* tiles, int16_t* rect, int threads) {
+    int nonfinite = 0;
+    for (int v = 0; v < V; ++v) {
+        Cam c = load_cam(cams + 24 * v);
+        int nf = 0;
+#pragma omp parallel for num_threads(threads) reduction(| : nf) schedule(static)
+        for (int i = 0; i < n_pad; ++i) {
+            int64_t o = (int64_t)v * n_pad + i;
+            if (i >= n) {
+                for (int j = 0; j < 12; ++j) rec[o * 12 + j] = 0.0f;
+                depth[o] = 0; tiles[o] = 0;
+                rect[o * 4 + 0] = rect[o * 4 + 1] = rect[o * 4 + 2] = rect[o * 4 + 3] = 0;
+                continue;
+            }
+            nf |= project_one(i, n_pad, deg, planes, c, rec + o * 12, depth + o, tiles + o, rect + o * 4);
+        }
+        nonfinite |= nf;
+    }
+    return nonfinite;
+}
+
+// ---------------------------------------------------------------------------
+// a8-a11. Scan / duplicate / sort / ranges over a batch of V views of one size
+// (W x H, T = gx*gy tiles each).  Global tile id gt = v*T + ty*gx + tx.
+//   offsets = exclusive prefix sum of tiles over the flattened [V][n_pad] array
+//   key = (gt << 31) | depth_bits   (depth bits < 2^31: z_c > 0), val = i
+//   emitted for (v, i) ascending, then ty ascending, then tx ascending
+//   sorted ascending by (key, val)  (R#15: depth, ties by index; "depth-sorted")
+//   ranges[gt] = [first, last+1) of gt in the sorted array, [0,0) if empty
+// keys/vals arrays must hold K = offsets total; K is returned (or -1 if > cap).
+// ---------------------------------------------------------------------------
+int64_t oracle_bin(int n_pad, int V, int W, int H, const uint32_t* tiles, const int16_t* rect,
+                   const uint32_t* depth, uint32_t* offsets, uint64_t* keys_emit, uint32_t* vals_emit,
+                   uint64_t* keys_sorted, uint32_t* vals_sorted, uint32_t* ranges, int64_t cap) {
+    const int gx = (W + 15) / 16, gy = (H + 15) / 16;
+    const int64_t T = (int64_t)gx * gy;
+    int64_t total = 0;
+    for (int64_t j = 0; j < (int64_t)V * n_pad; ++j) {
+        offsets[j] = (uint32_t)total;
+        total += tiles[j];
+    }
+    if (total > cap) return -1;
+    for (int v = 0; v < V; ++v)
+        for (int i = 0; i < n_pad; ++i) {
+            int64_t j = (int64_t)v * n_pad + i;
+            if (tiles[j] == 0) continue;
+            int64_t w = offsets[j];
+            const int16_t* r = rect + j * 4;
+            for (int ty = r[1]; ty <= r[3]; ++ty)
+                for (int tx = r[0]; tx <= r[2]; ++tx) {
+                    uint64_t gt = (uint64_t)v * T + (uint64_t)ty * gx + tx;
+                    keys_emit[w] = (gt << 31) | (uint64_t)depth[j];
+                    vals_emit[w] = (uint32_t)i;
+                    ++w;
+                }
+        }
+    std::vector<std::pair<uint64_t, uint32_t>> kv((size_t)total);
+    for (int64_t j = 0; j < total; ++j) kv[j] = {keys_emit[j], vals_emit[j]};
+    std::sort(kv.begin(), kv.end());
+    for (int64_t j = 0; j < total; ++j) { keys_sorted[j] = kv[j].first; vals_sorted[j] = kv[j].second; }
+    for (int64_t t = 0; t < V * T; ++t) { ranges[2 * t] = 0; ranges[2 * t + 1] = 0; }
+    for (int64_t j = 0; j < total; ++j) {
+        uint64_t gt = keys_sorted[j] >> 31;
+        if (j == 0 || (keys_sorted[j - 1] >> 31) != gt) ranges[2 * gt] = (uint32_t)j;
+        if (j == total - 1 || (keys_sorted[j + 1] >> 31) != gt) ranges[2 * gt + 1] = (uint32_t)(j + 1);
+    }
+    return total;
+}
+
+// ---------------------------------------------------------------------------
+// a12. Front-to-back compositing, Eq. 2: c = sum c_i a_i prod_{j<i}(1-a_j),
+// a_i = o_i exp(-1/2 d^T S'^-1 d), over the pixel's tile list in depth order.
+// 3D-GS cut-offs as read in R#14: skip when a_i < 1/255 (exact test p2 < T2, or
+// p2 > 0), a_i clamped at 0.99, composite-then-stop when T < 1e-4.  Pixel (x, y)
+// is sampled at ((float)x, (float)y) (R#12).  Output C + T*bg and T (R#16).
+// ---------------------------------------------------------------------------
+static inline bool blend_step(const float* rc, float fx, float fy, float C[3], float& T) {
+    float dx = rc[0] - fx, dy = rc[1] - fy;
+    float p2 = std::fma(rc[2] * dx, dx, std::fma(rc[4] * dy, dy, (rc[3] * dx) * dy));
+    if (p2 > 0.0f || p2 < rc[5]) return false;
+    float alpha = std::fmin(0.99f, rc[6] * std::exp2(p2));
+    float aT = alpha * T;
+    C[0] = std::fma(rc[8], aT, C[0]);
+    C[1] = std::fma(rc[9], aT, C[1]);
+    C[2] = std::fma(rc[10], aT, C[2]);
+    T = T * (1.0f - alpha);
+    return T < 1e-4f;
+}
+
+void oracle_rasterize(int n_pad, int V, int W, int H, const float* rec, const uint32_t* ranges,
+                      const uint32_t* vals_sorted, const float* bg, float* rgb_out, float* T_out, int threads) {
+    const int gx = (W + 15) / 16, gy = (H + 15) / 16;
+    const int64_t T = (int64_t)gx * gy;
+    for (int v = 0; v < V; ++v) {
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 4)
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x) {
+                int64_t gt = (int64_t)v * T + (int64_t)(y >> 4) * gx + (x >> 4);
+                float C[3] = {0.0f, 0.0f, 0.0f}, Tr = 1.0f;
+                for (uint32_t j = ranges[2 * gt]; j < ranges[2 * gt + 1]; ++j) {
+                    const float* rc = rec + ((int64_t)v * n_pad + vals_sorted[j]) * 12;
+                    if (blend_step(rc, (float)x, (float)y, C, Tr)) break;
+                }
+                int64_t pix = (int64_t)y * W + x;
+                for (int ch = 0; ch < 3; ++ch)
+                    rgb_out[((int64_t)v * 3 + ch) * H * W + pix] = C[ch] + Tr * bg[ch];
+                T_out[(int64_t)v * H * W + pix] = Tr;
+            }
+    }
+}
+
+// Brute force: every non-culled Gaussian of the view (record o > 0), globally
+// sorted by (depth, index), composited at every pixel with the same per-pixel
+// arithmetic.  No tiles, no ranges.  Pins the tiled path bit-for-bit (R#13).
+void oracle_rasterize_bruteforce(int n, int n_pad, int V, int W, int H, const float* rec, const uint32_t* depth,
+                                 const float* bg, float* rgb_out, float* T_out, int threads) {
+    for (int v = 0; v < V; ++v) {
+        std::vector<std::pair<uint32_t, uint32_t>> order;
+        for (int i = 0; i < n; ++i)
+            if (rec[((int64_t)v * n_pad + i) * 12 + 6] > 0.0f) order.push_back({depth[(int64_t)v * n_pad + i], (uint32_t)i});
+        std::sort(order.begin(), order.end());
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 1)
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x) {
+                float C[3] = {0.0f, 0.0f, 0.0f}, Tr = 1.0f;
+                for (auto& di : order) {
+                    const float* rc = rec + ((int64_t)v * n_pad + di.second) * 12;
+                    if (blend_step(rc, (float)x, (float)y, C, Tr)) break;
+                }
+                int64_t pix = (int64_t)y * W + x;
+                for (int ch = 0; ch < 3; ++ch)
+                    rgb_out[((int64_t)v * 3 + ch) * H * W + pix] = C[ch] + Tr * bg[ch];
+                T_out[(int64_t)v * H * W + pix] = Tr;
+            }
+    }
+}
+
+// Work counters for the blend roofline: evaluated (pixel, Gaussian)
+// pairs and composited pairs, per view, for the tiled order.
+void oracle_blend_counts(int n_pad, int V, int W, int H, const float* rec, const uint32_t* ranges,
+                         const uint32_t* vals_sorted, int64_t* evaluated, int64_t* composited, int threads) {
+    const int gx = (W + 15) / 16, gy = (H + 15) / 16;
+    const int64_t T = (int64_t)gx * gy;
+    for (int v = 0; v < V; ++v) {
+        int64_t ev = 0, cp = 0;
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 4) reduction(+ : ev, cp)
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x) {
+                int64_t gt = (int64_t)v * T + (int64_t)(y >> 4) * gx + (x >> 4);
+                float C[3] = {0.0f, 0.0f, 0.0f}, Tr = 1.0f;
+                for (uint32_t j = ranges[2 * gt]; j < ranges[2 * gt + 1]; ++j) {
+                    const float* rc = rec + ((int64_t)v * n_pad + vals_sorted[j]) * 12;
+                    ++ev;
+                    float dx = rc[0] - (float)x, dy = rc[1] - (float)y;
+                    float p2 = std::fma(rc[2] * dx, dx, std::fma(rc[4] * dy, dy, (rc[3] * dx) * dy));
+                    if (!(p2 > 0.0f || p2 < rc[5])) ++cp;
+                    if (blend_step(rc, (float)x, (float)y, C, Tr)) break;
+                }
+            }
+        evaluated[v] = ev;
+        composited[v] = cp;
+    }
+}
+
+}  // extern "C"
