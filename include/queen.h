@@ -1,0 +1,212 @@
+/*
+ * queen.h -- C-ABI of libqueen: QUEEN's per-frame decode -> apply -> 3D-GS splat
+ * hot path (arXiv 2412.04469), hand-written CUDA for sm_100a (B200).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n;
+ * R#n = DESIGN.md reading #n (where the paper is silent).
+ *
+ * Conventions shared by every call
+ * ---------------------------------
+ *  - Every function is extern "C", never throws, and returns a queen_status.
+ *  - Pointers named *_dev, and every array member of the structs below, are DEVICE
+ *    pointers on the ctx's device; camera arrays and queen_* structs themselves are
+ *    HOST memory, read during the call only (cameras are copied into kernel
+ *    parameters), so they may be freed as soon as the call returns.
+ *  - All device buffers are caller-owned (torch tensors in the Python binding):
+ *    contiguous, 16-byte aligned, n_pad % 4 == 0.  The library allocates NO device
+ *    memory; its scratch lives in the caller-provided workspace (queen_set_workspace).
+ *  - `stream` is a cudaStream_t passed as void*.  Calls only ENQUEUE work on it and
+ *    return; nothing synchronises except queen_check.  Every call is capturable in a
+ *    CUDA graph.
+ *  - Host-detectable errors (null pointer, bad shape, bad degree, ...) are returned
+ *    immediately and nothing is enqueued.  Device-detectable errors (bad COO index,
+ *    latent out of range, key-capacity overflow, non-finite Gaussian) set sticky
+ *    flags in the workspace that queen_check reports.
+ *  - A queen_ctx is bound to one device and is not thread-safe.
+ */
+#ifndef QUEEN_H
+#define QUEEN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t queen_status;
+enum {
+    QUEEN_OK = 0,
+    QUEEN_ERR_INVALID_ARG = -1,   /* null pointer, bad enum, degree not in [0,3], ...        */
+    QUEEN_ERR_SHAPE = -2,         /* n > n_pad, n_pad % 4, latent dims, view sizes differ   */
+    QUEEN_ERR_INDEX = -3,         /* COO index >= n or not strictly increasing */
+    QUEEN_ERR_LATENT_RANGE = -4,  /* rounded latent outside [-127, 127] (R#4)               */
+    QUEEN_ERR_CAPACITY = -5,      /* keys needed > keys_cap; queen_check's info = keys needed */
+    QUEEN_ERR_CUDA = -6,          /* a CUDA runtime call failed (see queen_last_error)      */
+    QUEEN_ERR_TIMEOUT = -7,       /* a look-back spin exceeded its bound (should never fire) */
+    QUEEN_WARN_NONFINITE = 1      /* a Gaussian had a non-finite attribute and was culled   */
+};
+
+enum { QUEEN_LAT_INT8 = 0, QUEEN_LAT_F32 = 1 };                 /* latent_kind */
+enum { QUEEN_POS_COO = 0, QUEEN_POS_GATES = 1, QUEEN_POS_NONE = 2 }; /* pos_kind */
+enum { QUEEN_MAX_VIEWS = 64, QUEEN_TILE = 16 };
+
+typedef struct queen_ctx queen_ctx;
+
+/* Gaussian attributes A = {p, q, s, o, h}, fp32 SoA,
+ * planes[P][n_pad], P = 11 + 3B, B = (sh_degree+1)^2:
+ *   rows 0-2 position xyz | 3-6 raw quaternion wxyz | 7-9 log-scale |
+ *   10 opacity logit | 11 + 3b + ch SH coefficient b, channel ch.
+ * Raw (pre-activation) storage: residuals add to raw values (R#1).  Columns
+ * i >= n are padding and are never read or written. */
+typedef struct {
+    int32_t n, n_pad, sh_degree;
+    float* planes;
+} queen_gaussians;
+
+/* One frame's residual packet R_t (Eq. 4).
+ * Non-position categories c = (rot, scale, opacity, sh_dc, sh_rest) (R#2):
+ *   M_c = (4, 3, 1, 3, 3(B-1)) residual rows, L_c = lat_dim[c] latent dims in [0,16]
+ *   (0 = category absent; sh_rest must be 0 at degree 0).
+ *   latents:  [sum L_c][n_pad] category-major, int8 (QUEEN_LAT_INT8, wire form) or
+ *             fp32 trainer-state l_hat (QUEEN_LAT_F32), rounded half away from zero
+ *             in-kernel (R#5).
+ *   decoders: concatenation of row-major D_c (M_c x L_c), fp32 (Eq. 5).
+ * Position:
+ *   QUEEN_POS_COO:   pos_idx[k] strictly increasing u32, pos_val[3][k] fp32 (row stride k).
+ *                    If k_dev != NULL the live count is min(*k_dev, k) read on the device
+ *                    (packets broadcast over NCCL) and k is the capacity.
+ *   QUEEN_POS_GATES: trainer state: log_alpha[n_pad], pos_pregate[3][n_pad] and the
+ *                    hard-concrete hyperparameters (tau, gamma0, gamma1);
+ *                    mask = log_alpha > tau ln(-gamma0/gamma1) (R#6).
+ *   QUEEN_POS_NONE:  no position residual. */
+typedef struct {
+    int32_t n, n_pad, sh_degree;
+    int32_t lat_dim[5];
+    int32_t latent_kind;
+    const void* latents;
+    const float* decoders;
+    int32_t pos_kind;
+    int32_t k;
+    const int32_t* k_dev;
+    const uint32_t* pos_idx;
+    const float* pos_val;
+    const float* log_alpha;
+    const float* pos_pregate;
+    float tau, gamma0, gamma1;
+} queen_packet;
+
+/* Pinhole camera (intrinsics K, viewing transform W).  x_c = R p + t.
+ * C = camera centre (-R^T t), limx/limy = 1.3 * tan(half FoV) (R#11), near_z = 0.2.
+ * Pixel k is sampled at coordinate k (R#12).  96 bytes. */
+typedef struct {
+    float fx, fy, cx, cy;
+    float R[9];
+    float t[3];
+    float C[3];
+    float limx, limy, near_z;
+    int32_t width, height;
+} queen_camera;
+
+/* Per-view projected records, each [n_views][n_pad]:
+ *   rec   [..][12] fp32 = u, v, A2, B2 | C2, T2, o, 0 | r, g, b, 0
+ *         (A2,B2,C2 base-2 conic, T2 = log2(1/(255 o)); all zero if culled)
+ *   depth u32 = bits(z_c) (z_c > 0)          tiles u32 = #16x16 tiles touched
+ *   rect  int16[4] = tx0, ty0, tx1, ty1 (inclusive; zeros if culled) */
+typedef struct {
+    int32_t n_pad;
+    float* rec;
+    uint32_t* depth;
+    uint32_t* tiles;
+    int16_t* rect;
+} queen_proj;
+
+/* Binning buffers for one batch of equally-sized views (gt = view*T + tile, T = gx*gy):
+ *   offsets[n_views][n_pad]  exclusive prefix sum of tiles (u32)
+ *   keys/vals (+ _alt ping-pong) [keys_cap]: key = (gt << 31) | depth, val = Gaussian index
+ *   ranges[n_views*T][2]     [first, last+1) of gt in the sorted keys, [0,0) if empty
+ *   K (device u32[1])        total keys of the batch
+ *   sorted_in_alt            OUT (host): 1 if the sorted result is in keys_alt/vals_alt */
+typedef struct {
+    int64_t keys_cap;
+    uint64_t* keys;
+    uint64_t* keys_alt;
+    uint32_t* vals;
+    uint32_t* vals_alt;
+    uint32_t* offsets;
+    uint32_t* ranges;
+    uint32_t* K;
+    int32_t sorted_in_alt;
+} queen_bins;
+
+/* ---- context / workspace ------------------------------------------------ */
+queen_status queen_create(int device, queen_ctx** out);
+void queen_destroy(queen_ctx* ctx);
+const char* queen_last_error(const queen_ctx* ctx);
+const char* queen_version(void);
+
+/* Bytes of device workspace for up to (n_pad, n_views <= QUEEN_MAX_VIEWS, width x
+ * height, keys_cap < 2^30) -- covers queen_bin_sort's scratch and, for
+ * queen_render_views, the proj / bins buffers it carves. */
+queen_status queen_workspace_size(int32_t n_pad, int32_t n_views, int32_t width, int32_t height,
+                                  int64_t keys_cap, size_t* bytes);
+/* Hands the ctx a caller-owned device buffer (>= queen_workspace_size bytes, 256-B
+ * aligned) and the shape it was sized for.  Zeroes the sticky flags (stream 0 order). */
+queen_status queen_set_workspace(queen_ctx* ctx, void* dev_ptr, size_t bytes, int32_t n_pad, int32_t n_views,
+                                 int32_t width, int32_t height, int64_t keys_cap);
+/* Synchronises `stream`, returns the first sticky device error (or
+ * QUEEN_WARN_NONFINITE, or QUEEN_OK) and clears the flags.  info_out (nullable)
+ * receives the largest key count requested (for QUEEN_ERR_CAPACITY). */
+queen_status queen_check(queen_ctx* ctx, void* stream, int64_t* info_out);
+
+/* ---- the hot path ---------------------------------------------------------
+ * queen_decode_residuals: UNFUSED decode (the test surface).  P:289-298, Eq. 5.
+ *   resid_out  (nullable) fp32 [sum M_c][n_pad]: r_c = D_c float(l_c), row order =
+ *              plane order 3.. (fmaf chain ascending k from +0, R#7)
+ *   q_out      (nullable) int8 [sum L_c][n_pad]: rounded latents (a copy for INT8)
+ *   coo_idx_out/coo_val_out/k_out (nullable together) u32 [n], fp32 [3][n] (row
+ *              stride n), device int32: the position COO (gates -> mask -> ascending
+ *              compaction, dp = g l_p; or a validated copy of the input COO). */
+queen_status queen_decode_residuals(queen_ctx* ctx, const queen_packet* pkt, float* resid_out, int8_t* q_out,
+                                    uint32_t* coo_idx_out, float* coo_val_out, int32_t* k_out, void* stream);
+/* queen_apply_frame: FUSED a1-a5: A_{t-1} -> A_t in place (Eq. 4):
+ * non-position planes += D_c float(round(l_c)); positions += COO / gated residual. */
+queen_status queen_apply_frame(queen_ctx* ctx, queen_gaussians* scene, const queen_packet* pkt, void* stream);
+/* queen_project: a6-a7 for n_views cameras (Eq. 1 + SH colour).
+ * `cams` is a HOST array of n_views cameras.  out arrays hold [n_views][n_pad]. */
+queen_status queen_project(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams, int32_t n_views,
+                           queen_proj* out, void* stream);
+/* queen_bin_sort: a8-a11 for a batch of equally-sized views: scan, duplicate,
+ * LSD onesweep radix sort on (gt, depth) then index (stable), tile ranges.  Uses the
+ * workspace scratch.  Outputs bit-exact. */
+queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_camera* cams, int32_t n_views,
+                            queen_bins* bins, void* stream);
+/* queen_rasterize: a12, Eq. 2: per pixel front-to-back over its tile's
+ * range; skip a < 1/255 (p2 < T2), a = min(0.99, o 2^p2), stop after T < 1e-4.
+ * rgb_out fp32 [n_views][3][H][W] = C + T bg;  T_out (nullable) fp32 [n_views][H][W]. */
+queen_status queen_rasterize(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins, const queen_camera* cams,
+                             int32_t n_views, const float bg[3], float* rgb_out, float* T_out, void* stream);
+/* queen_render_views: project + bin_sort + rasterize with proj/bins carved from the
+ * workspace (sized for >= these n_views/width/height/n_pad). */
+queen_status queen_render_views(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
+                                int32_t n_views, const float bg[3], float* rgb_out, float* T_out, void* stream);
+
+/* Debug / evidence: per-view blend work counters (evaluated and composited
+ * (pixel, Gaussian) pairs, int64 device arrays [n_views]); same semantics as the
+ * rasterizer, used only to compute the blend roofline. */
+queen_status queen_blend_counts(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
+                                const queen_camera* cams, int32_t n_views, int64_t* evaluated, int64_t* composited,
+                                void* stream);
+
+/* Stage profiler (evidence for bench.py): when enabled, every call records CUDA events
+ * on its stream around each stage: 0 apply, 1 project, 2 scan (+resets), 3 duplicate,
+ * 4 histogram, 5 sort (all onesweep passes), 6 ranges, 7 blend.  queen_profile_read
+ * waits for the recorded events and returns per-stage summed milliseconds and kernel
+ * launches (double[8], int64[8]), optionally resetting them.  Not capturable. */
+queen_status queen_profile_enable(queen_ctx* ctx, int32_t enable);
+queen_status queen_profile_read(queen_ctx* ctx, double* ms, int64_t* launches, int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QUEEN_H */

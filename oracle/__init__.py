@@ -53,6 +53,7 @@ def lib():
             "oracle_bin": (i64, [i32, i32, i32, i32, p, p, p, p, p, p, p, p, p, i64]),
             "oracle_rasterize": (None, [i32, i32, i32, i32, p, p, p, p, p, p, i32]),
             "oracle_rasterize_bruteforce": (None, [i32, i32, i32, i32, i32, p, p, p, p, p, i32]),
+            "oracle_rasterize_pixels": (None, [i32, i32, i32, p, p, p, p, i64, p, p, p, i32]),
             "oracle_blend_counts": (None, [i32, i32, i32, i32, p, p, p, p, p, i32]),
         }
         for name, (res, args) in sig.items():
@@ -191,6 +192,21 @@ def rasterize(proj, bins, W: int, H: int, bg=(0.0, 0.0, 0.0), threads: int | Non
     vals = bins["vals"] if bins["K"] else np.zeros(1, np.uint32)
     lib().oracle_rasterize(n_pad, V, W, H, _p(rec), _p(bins["ranges"]), _p(np.ascontiguousarray(vals)), _p(bgv), _p(rgb), _p(T),
                            threads or default_threads())
+    return rgb, T
+
+
+def rasterize_pixels(rec: np.ndarray, ranges: np.ndarray, vals: np.ndarray, W: int, H: int, pix: np.ndarray,
+                     bg=(0.0, 0.0, 0.0), threads: int | None = None):
+    """Composite only the sampled pixels pix[(v, x, y)] (full-size parity checks)."""
+    rec = np.ascontiguousarray(rec, np.float32)
+    n_pad = rec.shape[1]
+    pix = np.ascontiguousarray(pix, np.int32)
+    rgb = np.zeros((pix.shape[0], 3), np.float32)
+    T = np.zeros(pix.shape[0], np.float32)
+    bgv = np.asarray(bg, np.float32)
+    vals = np.ascontiguousarray(vals if vals.size else np.zeros(1, np.uint32), np.uint32)
+    lib().oracle_rasterize_pixels(n_pad, W, H, _p(rec), _p(np.ascontiguousarray(ranges, np.uint32)), _p(vals), _p(bgv),
+                                  pix.shape[0], _p(pix), _p(rgb), _p(T), threads or default_threads())
     return rgb, T
 
 

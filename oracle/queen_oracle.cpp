@@ -498,6 +498,27 @@ void oracle_rasterize(int n_pad, int V, int W, int H, const float* rec, const ui
     }
 }
 
+// Same compositing for a list of sampled pixels (v, x, y) -- used to check full-size
+// configurations pixel by pixel.  out: rgb [npix][3] (C + T*bg), T [npix].
+void oracle_rasterize_pixels(int n_pad, int W, int H, const float* rec, const uint32_t* ranges,
+                             const uint32_t* vals_sorted, const float* bg, int64_t npix, const int32_t* pix,
+                             float* rgb_out, float* T_out, int threads) {
+    const int gx = (W + 15) / 16, gy = (H + 15) / 16;
+    const int64_t T = (int64_t)gx * gy;
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 16)
+    for (int64_t q = 0; q < npix; ++q) {
+        const int v = pix[3 * q], x = pix[3 * q + 1], y = pix[3 * q + 2];
+        int64_t gt = (int64_t)v * T + (int64_t)(y >> 4) * gx + (x >> 4);
+        float C[3] = {0.0f, 0.0f, 0.0f}, Tr = 1.0f;
+        for (uint32_t j = ranges[2 * gt]; j < ranges[2 * gt + 1]; ++j) {
+            const float* rc = rec + ((int64_t)v * n_pad + vals_sorted[j]) * 12;
+            if (blend_step(rc, (float)x, (float)y, C, Tr)) break;
+        }
+        for (int ch = 0; ch < 3; ++ch) rgb_out[3 * q + ch] = C[ch] + Tr * bg[ch];
+        T_out[q] = Tr;
+    }
+}
+
 // Brute force: every non-culled Gaussian of the view (record o > 0), globally
 // sorted by (depth, index), composited at every pixel with the same per-pixel
 // arithmetic.  No tiles, no ranges.  Pins the tiled path bit-for-bit (R#13).

@@ -1,0 +1,330 @@
+// libqueen C-ABI entry points (include/queen.h): argument validation, workspace
+// carve-up, sticky-flag reporting and the per-frame orchestration
+// (queen_render_views = project -> bin_sort -> rasterize, all enqueued, no host sync).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "queen_internal.cuh"
+
+struct queen_ctx {
+    int device = 0;
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    int32_t ws_n_pad = 0, ws_views = 0, ws_w = 0, ws_h = 0;
+    int64_t ws_keys = 0;
+    queen::WsLayout L{};
+    queen::Prof prof;
+    std::string err;
+};
+
+namespace queen {
+float host_theta0(float tau, float g0, float g1) {
+    // exact mask threshold on log alpha: g_tilde > 0 <=> log alpha > tau ln(-g0/g1) (R#6)
+    return (float)((double)tau * std::log(-(double)g0 / (double)g1));
+}
+cudaError_t init_binning_attributes();
+int key_passes(int64_t gtiles);
+}  // namespace queen
+
+using namespace queen;
+
+static queen_status fail(queen_ctx* c, queen_status st, const char* msg) {
+    if (c) c->err = msg;
+    return st;
+}
+static queen_status cuda_fail(queen_ctx* c, cudaError_t e, const char* where) {
+    if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e);
+    return QUEEN_ERR_CUDA;
+}
+
+extern "C" {
+
+const char* queen_version(void) { return "libqueen 0.1 sm_100a"; }
+
+queen_status queen_create(int device, queen_ctx** out) {
+    if (!out) return QUEEN_ERR_INVALID_ARG;
+    *out = nullptr;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return QUEEN_ERR_CUDA;
+    if ((e = init_binning_attributes()) != cudaSuccess) return QUEEN_ERR_CUDA;
+    queen_ctx* c = new queen_ctx();
+    c->device = device;
+    *out = c;
+    return QUEEN_OK;
+}
+
+void queen_destroy(queen_ctx* ctx) { delete ctx; }
+
+const char* queen_last_error(const queen_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+queen_status queen_workspace_size(int32_t n_pad, int32_t n_views, int32_t width, int32_t height, int64_t keys_cap,
+                                  size_t* bytes) {
+    if (!bytes) return QUEEN_ERR_INVALID_ARG;
+    if (n_pad < 0 || n_pad % 4 || n_views < 1 || n_views > QUEEN_MAX_VIEWS || width < 1 || height < 1 ||
+        keys_cap < 1 || keys_cap > MAX_KEYS)
+        return QUEEN_ERR_SHAPE;
+    *bytes = ws_layout(n_pad, n_views, width, height, keys_cap).total;
+    return QUEEN_OK;
+}
+
+queen_status queen_set_workspace(queen_ctx* ctx, void* dev_ptr, size_t bytes, int32_t n_pad, int32_t n_views,
+                                 int32_t width, int32_t height, int64_t keys_cap) {
+    if (!ctx || !dev_ptr) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null ctx/workspace");
+    size_t need = 0;
+    queen_status st = queen_workspace_size(n_pad, n_views, width, height, keys_cap, &need);
+    if (st) return fail(ctx, st, "bad workspace shape");
+    if (bytes < need) return fail(ctx, QUEEN_ERR_SHAPE, "workspace too small");
+    if (reinterpret_cast<uintptr_t>(dev_ptr) % 256) return fail(ctx, QUEEN_ERR_INVALID_ARG, "workspace not 256-B aligned");
+    ctx->ws = dev_ptr;
+    ctx->ws_bytes = bytes;
+    ctx->ws_n_pad = n_pad;
+    ctx->ws_views = n_views;
+    ctx->ws_w = width;
+    ctx->ws_h = height;
+    ctx->ws_keys = keys_cap;
+    ctx->L = ws_layout(n_pad, n_views, width, height, keys_cap);
+    cudaError_t e = cudaMemset(dev_ptr, 0, ctx->L.total_scratch);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "queen_set_workspace");
+    return QUEEN_OK;
+}
+
+static DevFlags* flags_of(queen_ctx* c) { return reinterpret_cast<DevFlags*>(static_cast<unsigned char*>(c->ws) + c->L.flags); }
+
+queen_status queen_check(queen_ctx* ctx, void* stream, int64_t* info_out) {
+    if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no workspace");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "queen_check sync");
+    DevFlags h{};
+    DevFlags* d = flags_of(ctx);
+    e = cudaMemcpy(&h, d, sizeof(DevFlags), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "queen_check copy");
+    if (info_out) *info_out = (int64_t)h.info;
+    uint32_t zero[4] = {0, 0, 0, 0};
+    e = cudaMemcpy(d, zero, 16, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "queen_check reset");
+    if (h.flags & FLAG_INDEX) return fail(ctx, QUEEN_ERR_INDEX, "COO index out of range or not strictly increasing");
+    if (h.flags & FLAG_LATENT_RANGE) return fail(ctx, QUEEN_ERR_LATENT_RANGE, "rounded latent outside [-127,127]");
+    if (h.flags & FLAG_CAPACITY) return fail(ctx, QUEEN_ERR_CAPACITY, "key capacity exceeded (info = keys needed)");
+    if (h.flags & FLAG_TIMEOUT) return fail(ctx, QUEEN_ERR_TIMEOUT, "look-back spin bound exceeded");
+    if (h.flags & FLAG_NONFINITE) return fail(ctx, QUEEN_WARN_NONFINITE, "non-finite Gaussian culled");
+    return QUEEN_OK;
+}
+
+static queen_status check_packet(queen_ctx* ctx, const queen_packet* p) {
+    if (!p || !p->latents || !p->decoders) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null packet/latents/decoders");
+    if (p->sh_degree < 0 || p->sh_degree > 3) return fail(ctx, QUEEN_ERR_INVALID_ARG, "sh_degree not in [0,3]");
+    if (p->n < 0 || p->n > p->n_pad || p->n_pad % 4) return fail(ctx, QUEEN_ERR_SHAPE, "n > n_pad or n_pad % 4");
+    for (int c = 0; c < 5; ++c)
+        if (p->lat_dim[c] < 0 || p->lat_dim[c] > 16) return fail(ctx, QUEEN_ERR_SHAPE, "lat_dim outside [0,16]");
+    if (p->sh_degree == 0 && p->lat_dim[4] != 0) return fail(ctx, QUEEN_ERR_SHAPE, "sh_rest latent dim must be 0 at degree 0");
+    if (p->latent_kind != QUEEN_LAT_INT8 && p->latent_kind != QUEEN_LAT_F32) return fail(ctx, QUEEN_ERR_INVALID_ARG, "latent_kind");
+    if (p->pos_kind == QUEEN_POS_COO) {
+        if (p->k < 0 || (p->k > 0 && (!p->pos_idx || !p->pos_val))) return fail(ctx, QUEEN_ERR_INVALID_ARG, "bad COO");
+    } else if (p->pos_kind == QUEEN_POS_GATES) {
+        if (!p->log_alpha || !p->pos_pregate) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null gates");
+        if (!(p->tau > 0.f) || !(p->gamma0 < 0.f) || !(p->gamma1 > 1.f)) return fail(ctx, QUEEN_ERR_INVALID_ARG, "gate hyperparameters");
+    } else if (p->pos_kind != QUEEN_POS_NONE) {
+        return fail(ctx, QUEEN_ERR_INVALID_ARG, "pos_kind");
+    }
+    return QUEEN_OK;
+}
+
+queen_status queen_decode_residuals(queen_ctx* ctx, const queen_packet* pkt, float* resid_out, int8_t* q_out,
+                                    uint32_t* coo_idx_out, float* coo_val_out, int32_t* k_out, void* stream) {
+    if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
+    if (queen_status st = check_packet(ctx, pkt)) return st;
+    const bool coo_out = coo_idx_out || coo_val_out || k_out;
+    if (coo_out && !(coo_idx_out && coo_val_out && k_out)) return fail(ctx, QUEEN_ERR_INVALID_ARG, "COO outputs go together");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    DevFlags* fl = flags_of(ctx);
+    cudaError_t e = cudaSuccess;
+    if (resid_out || q_out) e = launch_decode_apply(*pkt, nullptr, resid_out, q_out, false, false, fl, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "decode");
+    if (coo_out) {
+        if (pkt->pos_kind == QUEEN_POS_GATES) {
+            // scratch for block counts: the sort look-back region (not in use concurrently)
+            void* scratch = static_cast<unsigned char*>(ctx->ws) + ctx->L.sort_lb;
+            size_t need = sizeof(uint32_t) * ((pkt->n + 1023) / 1024 + 1);
+            if (need > ctx->L.total_scratch - ctx->L.sort_lb) return fail(ctx, QUEEN_ERR_SHAPE, "workspace too small for gate compaction");
+            e = launch_gate_compact(*pkt, coo_idx_out, coo_val_out, k_out, scratch, fl, s);
+        } else if (pkt->pos_kind == QUEEN_POS_COO) {
+            e = launch_coo_copy(*pkt, coo_idx_out, coo_val_out, k_out, fl, s);
+        } else {
+            e = cudaMemsetAsync(k_out, 0, sizeof(int32_t), s);
+        }
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "decode positions");
+    }
+    return QUEEN_OK;
+}
+
+queen_status queen_apply_frame(queen_ctx* ctx, queen_gaussians* scene, const queen_packet* pkt, void* stream) {
+    if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
+    if (!scene || !scene->planes) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null scene");
+    if (queen_status st = check_packet(ctx, pkt)) return st;
+    if (scene->n != pkt->n || scene->n_pad != pkt->n_pad || scene->sh_degree != pkt->sh_degree)
+        return fail(ctx, QUEEN_ERR_SHAPE, "scene / packet shape mismatch");
+    ctx->prof.begin(ST_APPLY, static_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_decode_apply(*pkt, scene->planes, nullptr, nullptr, true, true, flags_of(ctx),
+                                        static_cast<cudaStream_t>(stream));
+    ctx->prof.end(static_cast<cudaStream_t>(stream), pkt->pos_kind == QUEEN_POS_COO && pkt->k > 0 ? 2 : 1);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "apply");
+    return QUEEN_OK;
+}
+
+static queen_status check_cams(queen_ctx* ctx, const queen_camera* cams, int32_t n_views, bool same_size) {
+    if (!cams || n_views < 1) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null cams / n_views < 1");
+    for (int v = 0; v < n_views; ++v) {
+        const queen_camera& c = cams[v];
+        if (!(c.fx > 0.f) || !(c.fy > 0.f) || !(c.near_z > 0.f) || c.width < 1 || c.height < 1)
+            return fail(ctx, QUEEN_ERR_INVALID_ARG, "camera: fx, fy, near must be > 0");
+        if (c.width > 16 * 32767 || c.height > 16 * 32767) return fail(ctx, QUEEN_ERR_SHAPE, "image too large");
+        for (int r = 0; r < 3; ++r)
+            for (int q = 0; q < 3; ++q) {
+                double d = 0;
+                for (int m = 0; m < 3; ++m) d += (double)c.R[r * 3 + m] * c.R[q * 3 + m];
+                if (std::fabs(d - (r == q ? 1.0 : 0.0)) > 1e-6) return fail(ctx, QUEEN_ERR_INVALID_ARG, "camera R not orthonormal (1e-6)");
+            }
+        if (same_size && (c.width != cams[0].width || c.height != cams[0].height))
+            return fail(ctx, QUEEN_ERR_SHAPE, "views of a batch must share width/height");
+    }
+    return QUEEN_OK;
+}
+
+queen_status queen_project(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams, int32_t n_views,
+                           queen_proj* out, void* stream) {
+    if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
+    if (!scene || !scene->planes || !out || !out->rec || !out->depth || !out->tiles || !out->rect)
+        return fail(ctx, QUEEN_ERR_INVALID_ARG, "null scene/proj");
+    if (scene->sh_degree < 0 || scene->sh_degree > 3) return fail(ctx, QUEEN_ERR_INVALID_ARG, "sh_degree");
+    if (scene->n < 0 || scene->n > scene->n_pad || scene->n_pad % 4 || out->n_pad != scene->n_pad)
+        return fail(ctx, QUEEN_ERR_SHAPE, "n / n_pad");
+    if (queen_status st = check_cams(ctx, cams, n_views, false)) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ctx->prof.begin(ST_PROJECT, s);
+    for (int v0 = 0; v0 < n_views; v0 += QUEEN_MAX_VIEWS) {
+        const int nv = n_views - v0 < (int)QUEEN_MAX_VIEWS ? n_views - v0 : (int)QUEEN_MAX_VIEWS;
+        CamBatch cb;
+        std::memset(&cb, 0, sizeof(cb));
+        std::memcpy(cb.cam, cams + v0, sizeof(queen_camera) * nv);
+        const int64_t o = (int64_t)v0 * scene->n_pad;
+        cudaError_t e = launch_project(scene->planes, scene->n, scene->n_pad, scene->sh_degree, cb, nv, out->rec + o * REC_WORDS,
+                                       out->depth + o, out->tiles + o, out->rect + o * 4, flags_of(ctx), s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "project");
+    }
+    ctx->prof.end(s, (n_views + QUEEN_MAX_VIEWS - 1) / QUEEN_MAX_VIEWS);
+    return QUEEN_OK;
+}
+
+queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_camera* cams, int32_t n_views,
+                            queen_bins* bins, void* stream) {
+    if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
+    if (!proj || !bins || !bins->keys || !bins->keys_alt || !bins->vals || !bins->vals_alt || !bins->offsets ||
+        !bins->ranges || !bins->K)
+        return fail(ctx, QUEEN_ERR_INVALID_ARG, "null proj/bins");
+    if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
+    const int W = cams[0].width, H = cams[0].height;
+    const int64_t T = (int64_t)((W + 15) / 16) * ((H + 15) / 16);
+    if (bins->keys_cap < 1 || bins->keys_cap > MAX_KEYS) return fail(ctx, QUEEN_ERR_SHAPE, "keys_cap outside [1, 2^30)");
+    if (T * n_views >= (1ll << 33)) return fail(ctx, QUEEN_ERR_SHAPE, "too many tiles");
+    // scratch must cover this batch
+    WsLayout need = ws_layout(proj->n_pad, n_views, W, H, bins->keys_cap);
+    if (need.total_scratch > ctx->L.total_scratch || need.sort_tiles > ctx->L.sort_tiles || need.scan_tiles > ctx->L.scan_tiles)
+        return fail(ctx, QUEEN_ERR_SHAPE, "workspace scratch too small for this batch");
+    cudaError_t e = launch_bin_sort(*proj, n_views, W, H, *bins, ctx->ws, ctx->L, flags_of(ctx),
+                                    static_cast<cudaStream_t>(stream), &ctx->prof);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "bin_sort");
+    return QUEEN_OK;
+}
+
+queen_status queen_rasterize(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins, const queen_camera* cams,
+                             int32_t n_views, const float bg[3], float* rgb_out, float* T_out, void* stream) {
+    if (!ctx) return QUEEN_ERR_INVALID_ARG;
+    if (!proj || !bins || !rgb_out || !bg) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
+    if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
+    const uint32_t* vals = bins->sorted_in_alt ? bins->vals_alt : bins->vals;
+    ctx->prof.begin(ST_BLEND, static_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_rasterize(proj->rec, proj->n_pad, bins->ranges, vals, n_views, cams[0].width, cams[0].height,
+                                     bg[0], bg[1], bg[2], rgb_out, T_out, static_cast<cudaStream_t>(stream));
+    ctx->prof.end(static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "rasterize");
+    return QUEEN_OK;
+}
+
+queen_status queen_blend_counts(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
+                                const queen_camera* cams, int32_t n_views, int64_t* evaluated, int64_t* composited,
+                                void* stream) {
+    if (!ctx) return QUEEN_ERR_INVALID_ARG;
+    if (!proj || !bins || !evaluated || !composited) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
+    if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
+    const uint32_t* vals = bins->sorted_in_alt ? bins->vals_alt : bins->vals;
+    cudaError_t e = launch_blend_counts(proj->rec, proj->n_pad, bins->ranges, vals, n_views, cams[0].width,
+                                        cams[0].height, reinterpret_cast<long long*>(evaluated),
+                                        reinterpret_cast<long long*>(composited), static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "blend_counts");
+    return QUEEN_OK;
+}
+
+queen_status queen_profile_enable(queen_ctx* ctx, int32_t enable) {
+    if (!ctx) return QUEEN_ERR_INVALID_ARG;
+    ctx->prof.on = enable != 0;
+    return QUEEN_OK;
+}
+
+queen_status queen_profile_read(queen_ctx* ctx, double* ms, int64_t* launches, int32_t reset) {
+    if (!ctx || !ms || !launches) return QUEEN_ERR_INVALID_ARG;
+    Prof& P = ctx->prof;
+    if (!P.pending.empty()) {
+        cudaError_t e = cudaEventSynchronize(P.pool[P.pending.back().e1]);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "queen_profile_read");
+        for (auto& q : P.pending) {
+            float t = 0.f;
+            e = cudaEventElapsedTime(&t, P.pool[q.e0], P.pool[q.e1]);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "queen_profile_read elapsed");
+            P.ms[q.stage] += t;
+            P.launches[q.stage] += q.launches;
+        }
+        P.pending.clear();
+        P.used = 0;
+    }
+    for (int i = 0; i < ST_COUNT; ++i) {
+        ms[i] = P.ms[i];
+        launches[i] = P.launches[i];
+        if (reset) { P.ms[i] = 0; P.launches[i] = 0; }
+    }
+    return QUEEN_OK;
+}
+
+queen_status queen_render_views(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams, int32_t n_views,
+                                const float bg[3], float* rgb_out, float* T_out, void* stream) {
+    if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
+    if (!scene || !rgb_out || !bg) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
+    if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
+    if (scene->n_pad > ctx->ws_n_pad || n_views > ctx->ws_views || cams[0].width > ctx->ws_w || cams[0].height > ctx->ws_h)
+        return fail(ctx, QUEEN_ERR_SHAPE, "workspace was sized for a smaller batch");
+    unsigned char* ws = static_cast<unsigned char*>(ctx->ws);
+    const WsLayout& L = ctx->L;
+    queen_proj pj;
+    pj.n_pad = scene->n_pad;
+    pj.rec = reinterpret_cast<float*>(ws + L.rec);
+    pj.depth = reinterpret_cast<uint32_t*>(ws + L.depth);
+    pj.tiles = reinterpret_cast<uint32_t*>(ws + L.tiles);
+    pj.rect = reinterpret_cast<int16_t*>(ws + L.rect);
+    queen_bins b;
+    b.keys_cap = ctx->ws_keys;
+    b.keys = reinterpret_cast<uint64_t*>(ws + L.keys);
+    b.keys_alt = reinterpret_cast<uint64_t*>(ws + L.keys_alt);
+    b.vals = reinterpret_cast<uint32_t*>(ws + L.vals);
+    b.vals_alt = reinterpret_cast<uint32_t*>(ws + L.vals_alt);
+    b.offsets = reinterpret_cast<uint32_t*>(ws + L.offsets);
+    b.ranges = reinterpret_cast<uint32_t*>(ws + L.ranges);
+    b.K = reinterpret_cast<uint32_t*>(ws + L.K);
+    b.sorted_in_alt = 0;
+    if (queen_status st = queen_project(ctx, scene, cams, n_views, &pj, stream)) return st;
+    if (queen_status st = queen_bin_sort(ctx, &pj, cams, n_views, &b, stream)) return st;
+    return queen_rasterize(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,187 @@
+// Internal definitions of libqueen (sm_100a).  Not part of the C-ABI.
+//
+// Arithmetic contract: this library is compiled with -fmad=false -prec-div=true
+// -prec-sqrt=true -ftz=false, so every `a * b + c` below is two roundings and every
+// fmaf() is one, exactly as DESIGN.md "Arithmetic contract" specifies.  That is what
+// makes projection records, tile rects, keys and skip decisions bit-identical to the
+// CPU oracle (which is written independently from the same text).
+#pragma once
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../../include/queen.h"
+
+namespace queen {
+
+// sticky device flags (bit i <-> error class)
+enum : uint32_t {
+    FLAG_INDEX = 1u << 0,
+    FLAG_LATENT_RANGE = 1u << 1,
+    FLAG_CAPACITY = 1u << 2,
+    FLAG_NONFINITE = 1u << 3,
+    FLAG_TIMEOUT = 1u << 4,
+};
+
+struct DevFlags {
+    uint32_t flags;
+    uint32_t pad;
+    unsigned long long info;     // largest key count requested
+    uint32_t tickets[16];        // per-launch dynamic tile counters (sort passes, scan)
+    uint32_t pad2[12];
+};
+static_assert(sizeof(DevFlags) == 128, "DevFlags layout");
+
+constexpr int MAX_PASSES = 8;
+constexpr int SORT_THREADS = 256;
+constexpr int SORT_ITEMS = 16;
+constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;  // 4096 keys per tile
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+constexpr int REC_WORDS = 12;
+constexpr int64_t MAX_KEYS = (1ll << 30) - 1;  // look-back packs 30-bit counts
+
+struct CamBatch {
+    queen_camera cam[QUEEN_MAX_VIEWS];
+};
+
+// Workspace carve-up (bytes, 256-aligned) for (n_pad, n_views, W, H, keys_cap).
+struct WsLayout {
+    size_t flags, hist, scan_lb, sort_lb, total_scratch;
+    size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, offsets, ranges, K, total;
+    int64_t sort_tiles, scan_tiles, T;
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, int64_t keys_cap) {
+    WsLayout L{};
+    int64_t gx = (W + 15) / 16, gy = (H + 15) / 16;
+    L.T = gx * gy;
+    int64_t elems = (int64_t)n_pad * n_views;
+    L.sort_tiles = (keys_cap + SORT_TILE - 1) / SORT_TILE;
+    L.scan_tiles = (elems + SCAN_TILE - 1) / SCAN_TILE;
+    size_t o = 0;
+    L.flags = o; o += align256(sizeof(DevFlags));
+    L.hist = o; o += align256(sizeof(uint32_t) * MAX_PASSES * 256 * 2);
+    L.scan_lb = o; o += align256(sizeof(unsigned long long) * (L.scan_tiles + 1));
+    L.sort_lb = o; o += align256(sizeof(uint32_t) * MAX_PASSES * 256 * (L.sort_tiles + 1));
+    L.total_scratch = o;
+    L.rec = o; o += align256(sizeof(float) * REC_WORDS * elems);
+    L.depth = o; o += align256(sizeof(uint32_t) * elems);
+    L.tiles = o; o += align256(sizeof(uint32_t) * elems);
+    L.rect = o; o += align256(sizeof(int16_t) * 4 * elems);
+    L.keys = o; o += align256(sizeof(uint64_t) * keys_cap);
+    L.keys_alt = o; o += align256(sizeof(uint64_t) * keys_cap);
+    L.vals = o; o += align256(sizeof(uint32_t) * keys_cap);
+    L.vals_alt = o; o += align256(sizeof(uint32_t) * keys_cap);
+    L.offsets = o; o += align256(sizeof(uint32_t) * elems);
+    L.ranges = o; o += align256(sizeof(uint32_t) * 2 * L.T * n_views);
+    L.K = o; o += align256(sizeof(uint32_t) * 4);
+    L.total = o;
+    return L;
+}
+
+// ---------------------------------------------------------------------------
+// det_exp / det_log:
+// only IEEE + - * / fmaf rintf fminf fmaxf and bit casts, so results are identical
+// on any IEEE-754 binary32 implementation.  Used for s = exp(log s),
+// o = sigmoid(logit) and the gate sigmoid.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float det_exp(float x) {
+    const float L2E = __int_as_float(0x3fb8aa3b);
+    const float LN2_HI = __int_as_float(0x3f317200);
+    const float LN2_LO = __int_as_float(0x35bfbe8e);
+    x = fminf(fmaxf(x, -87.0f), 88.0f);
+    float k = rintf(x * L2E);
+    float r = fmaf(-k, LN2_HI, x);
+    r = fmaf(-k, LN2_LO, r);
+    float p = 1.0f / 5040.0f;
+    p = fmaf(p, r, 1.0f / 720.0f);
+    p = fmaf(p, r, 1.0f / 120.0f);
+    p = fmaf(p, r, 1.0f / 24.0f);
+    p = fmaf(p, r, 1.0f / 6.0f);
+    p = fmaf(p, r, 0.5f);
+    p = fmaf(p, r, 1.0f);
+    p = fmaf(p, r, 1.0f);
+    return p * __int_as_float((int)(k + 127.0f) << 23);
+}
+
+__device__ __forceinline__ float det_log(float y) {
+    const float LN2_HI = __int_as_float(0x3f317200);
+    const float LN2_LO = __int_as_float(0x35bfbe8e);
+    uint32_t b = __float_as_uint(y);
+    int e = (int)((b >> 23) & 255u) - 127;
+    float m = __uint_as_float((b & 0x7fffffu) | 0x3f800000u);
+    if (m > 1.41421356f) { m = m * 0.5f; e += 1; }
+    float f = m - 1.0f;
+    float s = f / (2.0f + f);
+    float z = s * s;
+    float R = fmaf(z, 2.0f / 9.0f, 2.0f / 7.0f);
+    R = fmaf(z, R, 2.0f / 5.0f);
+    R = fmaf(z, R, 2.0f / 3.0f);
+    R = z * R;
+    float hfsq = (0.5f * f) * f;
+    float lnm = f - (hfsq - s * (hfsq + R));
+    float ef = (float)e;
+    return fmaf(ef, LN2_HI, fmaf(ef, LN2_LO, lnm));
+}
+
+__device__ __forceinline__ void raise_flag(DevFlags* fl, uint32_t bit) { atomicOr(&fl->flags, bit); }
+
+// Stage profiler: CUDA events recorded on the launching stream at stage boundaries
+// (enabled by queen_profile_enable; used by bench.py for per-kernel durations).
+enum Stage { ST_APPLY = 0, ST_PROJECT, ST_SCAN, ST_DUPLICATE, ST_HIST, ST_SORT, ST_RANGES, ST_BLEND, ST_COUNT };
+struct Prof {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    struct Pending { int stage; size_t e0, e1; int launches; };
+    std::vector<Pending> pending;
+    double ms[ST_COUNT] = {0};
+    long long launches[ST_COUNT] = {0};
+    size_t open_ev = 0;
+    int open_stage = -1;
+    cudaEvent_t ev() {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        return pool[used++];
+    }
+    void begin(int stage, cudaStream_t s) {
+        if (!on) return;
+        open_ev = used;
+        cudaEventRecord(ev(), s);
+        open_stage = stage;
+    }
+    void end(cudaStream_t s, int n_launches = 1) {
+        if (!on || open_stage < 0) return;
+        size_t e1 = used;
+        cudaEventRecord(ev(), s);
+        pending.push_back({open_stage, open_ev, e1, n_launches});
+        open_stage = -1;
+    }
+};
+
+// host-side launchers (defined in the .cu files)
+cudaError_t launch_decode_apply(const queen_packet& p, float* planes, float* resid_out, int8_t* q_out,
+                                bool apply_attrs, bool apply_pos, DevFlags* fl, cudaStream_t s);
+cudaError_t launch_gate_compact(const queen_packet& p, uint32_t* idx_out, float* val_out, int32_t* k_out,
+                                void* scratch, DevFlags* fl, cudaStream_t s);
+cudaError_t launch_coo_copy(const queen_packet& p, uint32_t* idx_out, float* val_out, int32_t* k_out, DevFlags* fl,
+                            cudaStream_t s);
+cudaError_t launch_project(const float* planes, int n, int n_pad, int deg, const CamBatch& cams, int n_views,
+                           float* rec, uint32_t* depth, uint32_t* tiles, int16_t* rect, DevFlags* fl, cudaStream_t s);
+cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
+                            const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof);
+cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
+                             int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
+                             cudaStream_t s);
+cudaError_t launch_blend_counts(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
+                                int W, int H, long long* evaluated, long long* composited, cudaStream_t s);
+cudaError_t init_kernel_attributes();
+
+}  // namespace queen

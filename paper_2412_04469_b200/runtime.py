@@ -1,0 +1,117 @@
+"""Per-frame player over libqueen: resident Gaussian SoA, A_t = A_{t-1} + R_t, multi-view render.
+
+Everything here is argument marshalling and buffer management (torch memory,
+streams); every step of the path runs in libqueen's kernels.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import (QUEEN_LAT_F32, QUEEN_LAT_INT8, QUEEN_MAX_VIEWS, QUEEN_POS_COO, QUEEN_POS_GATES, Context,
+               QueenError, camera_array, gaussians_struct, packet_struct, queen_apply_frame, queen_render_views)
+from . import packet as wire
+
+
+class DevicePacket:
+    """A frame packet resident on the device (keeps its tensors alive)."""
+
+    def __init__(self, struct, tensors):
+        self.struct = struct
+        self._keep = tensors
+
+
+def device_packet(pkt, device="cuda", *, gates: bool = False, f32_latents: bool = False) -> DevicePacket:
+    """Upload a host packet (harness.synth.Packet-like) in trainer-state or COO form."""
+    t = {}
+    t["lat"] = torch.from_numpy(np.ascontiguousarray(pkt.latents_f32 if f32_latents else pkt.latents)).to(device)
+    t["dec"] = torch.from_numpy(np.ascontiguousarray(pkt.decoders, np.float32)).to(device) if pkt.decoders.size else \
+        torch.zeros(1, dtype=torch.float32, device=device)
+    kw = dict(n=pkt.n, n_pad=pkt.n_pad, sh_degree=pkt.deg, lat_dim=pkt.lat, latents=t["lat"], decoders=t["dec"],
+              latent_kind=QUEEN_LAT_F32 if f32_latents else QUEEN_LAT_INT8, gate=pkt.gate)
+    if gates:
+        t["la"] = torch.from_numpy(np.ascontiguousarray(pkt.log_alpha)).to(device)
+        t["lp"] = torch.from_numpy(np.ascontiguousarray(pkt.pos_pregate)).to(device)
+        s = packet_struct(**kw, pos_kind=QUEEN_POS_GATES, log_alpha=t["la"], pos_pregate=t["lp"])
+    else:
+        k = int(pkt.coo_idx.shape[0])
+        t["idx"] = torch.from_numpy(np.ascontiguousarray(pkt.coo_idx).view(np.int32)).to(device) if k else None
+        t["val"] = torch.from_numpy(np.ascontiguousarray(pkt.coo_val, np.float32)).to(device) if k else None
+        s = packet_struct(**kw, pos_kind=QUEEN_POS_COO, k=k, pos_idx=t["idx"], pos_val=t["val"])
+    return DevicePacket(s, t)
+
+
+def wire_packet(buf: torch.Tensor, hdr: dict) -> DevicePacket:
+    """QueenPacket view of a device-resident wire buffer (packet.py layout).
+
+    The live COO count is read on the device from the header (k_dev), so a buffer
+    filled by an NCCL broadcast needs no host round trip; hdr supplies only the
+    stream-static fields (n, n_pad, degree, latent dims, k_cap, offsets)."""
+    base = buf.data_ptr()
+    s = packet_struct(n=hdr["n"], n_pad=hdr["n_pad"], sh_degree=hdr["deg"], lat_dim=hdr["lat"],
+                      latents=base + hdr["lat_off"], decoders=base + hdr["dec_off"], latent_kind=QUEEN_LAT_INT8,
+                      pos_kind=QUEEN_POS_COO, k=hdr["k_cap"], k_dev=base + wire.K_WORD * 4,
+                      pos_idx=base + hdr["idx_off"], pos_val=base + hdr["val_off"])
+    if hdr["k_cap"] == 0:
+        s.pos_idx = None
+        s.pos_val = None
+    return DevicePacket(s, [buf])
+
+
+class Player:
+    """Resident scene on one GPU; renders a fixed set of equally-sized views per frame."""
+
+    def __init__(self, planes, n: int, deg: int, cams, *, device: int = 0, keys_cap: int | None = None,
+                 views_per_batch: int | None = None, bg=(0.0, 0.0, 0.0), with_T: bool = False):
+        self.dev = torch.device(f"cuda:{device}")
+        self.ctx = Context(device)
+        if isinstance(planes, np.ndarray):
+            planes = torch.from_numpy(np.ascontiguousarray(planes, np.float32))
+        self.planes = planes.to(self.dev).contiguous()
+        self.n, self.deg = n, deg
+        self.cams = list(cams)
+        W, H = self.cams[0].width, self.cams[0].height
+        if any(c.width != W or c.height != H for c in self.cams):
+            raise ValueError("all views of a Player must share width/height")
+        self.W, self.H = W, H
+        V = len(self.cams)
+        self.vpb = min(V, views_per_batch or QUEEN_MAX_VIEWS, QUEEN_MAX_VIEWS)
+        self.batches = [(b, min(b + self.vpb, V)) for b in range(0, V, self.vpb)]
+        self.cam_arrays = [camera_array(self.cams[a:b]) for a, b in self.batches]
+        self.bg = bg
+        self.rgb = torch.empty((V, 3, H, W), dtype=torch.float32, device=self.dev)
+        self.T = torch.empty((V, H, W), dtype=torch.float32, device=self.dev) if with_T else None
+        self.scene = gaussians_struct(self.planes, n, deg)
+        n_pad = self.planes.shape[1]
+        if keys_cap is None:
+            keys_cap = min((1 << 30) - 1, max(1 << 16, 8 * n * self.vpb))
+        self.keys_cap = int(keys_cap)
+        self.ctx.set_workspace(n_pad, self.vpb, W, H, self.keys_cap)
+
+    def apply(self, pkt: DevicePacket, stream=None):
+        queen_apply_frame(self.ctx, self.scene, pkt.struct, stream)
+
+    def render(self, stream=None):
+        for (a, b), arr in zip(self.batches, self.cam_arrays):
+            queen_render_views(self.ctx, self.scene, None, self.rgb[a:b], None if self.T is None else self.T[a:b],
+                               self.bg, stream, cam_array=arr)
+        return self.rgb
+
+    def frame(self, pkt: DevicePacket | None, stream=None):
+        if pkt is not None:
+            self.apply(pkt, stream)
+        return self.render(stream)
+
+    def fit_capacity(self, margin: float = 1.3, stream=None):
+        """Render once, and grow keys_cap (re-carving the workspace) until no capacity error."""
+        for _ in range(4):
+            self.render(stream)
+            st, info = self.ctx.check_status(stream)
+            if st == -5:
+                self.keys_cap = min((1 << 30) - 1, int(info * margin) + 1024)
+                self.ctx.set_workspace(self.planes.shape[1], self.vpb, self.W, self.H, self.keys_cap)
+                continue
+            if st < 0:
+                raise QueenError(st, self.ctx.last_error())
+            return self.keys_cap
+        raise QueenError(-5, "could not fit key capacity")

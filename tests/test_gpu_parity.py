@@ -1,0 +1,318 @@
+"""GPU (libqueen, sm_100a) vs CPU oracle parity, element by element, on seeded inputs.
+
+Bars (BASELINE north_star):
+  bit-exact  : quantised latents, gate mask / COO indices, projection records except
+               rgb (u, v, A2, B2, C2, T2, o, depth, tiles, rect), offsets, K, keys,
+               vals, ranges
+  tolerance  : decoded attributes |d| <= 1e-5 max(|ref|, 1e-6) (bit-exact expected);
+               per-Gaussian rgb 1e-5 relative; image RGB max-abs <= 2e-3 on [0,1],
+               PSNR > 60 dB; T max-abs <= 2e-3
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from harness import synth  # noqa: E402
+from tests.util import planes_from  # noqa: E402
+
+RGB_TOL = 2e-3
+ATTR_REL = 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (run with -m 'not gpu' on CPU)")
+    import paper_2412_04469_b200 as Q
+    Q.lib()  # loud failure if the extension was not built
+
+
+def _attr_close(got, ref):
+    got = got.astype(np.float64)
+    ref = ref.astype(np.float64)
+    return np.all(np.abs(got - ref) <= ATTR_REL * np.maximum(np.abs(ref), 1e-6))
+
+
+def _scene(name, n=None, **over):
+    cfg = synth.get_config(name, **over)
+    return cfg, synth.make_scene(cfg, n)
+
+
+# ------------------------------------------------------------------ decode / apply
+@pytest.mark.parametrize("name,n", [("tiny", 1000), ("n3dv", 20011), ("immersive", 5003)])
+@pytest.mark.parametrize("f32", [False, True])
+def test_decode_residuals_parity(name, n, f32):
+    import paper_2412_04469_b200 as Q
+    from paper_2412_04469_b200.runtime import device_packet
+    cfg, sc = _scene(name, n)
+    pkt = synth.make_packet(sc, 1)
+    ref = oracle.decode(pkt)
+    ctx = Q.Context(0)
+    ctx.set_workspace(sc.n_pad, 1, 16, 16, 1024)
+    dp = device_packet(pkt, "cuda", gates=True, f32_latents=f32)
+    resid = torch.zeros(ref.shape, dtype=torch.float32, device="cuda")
+    q = torch.zeros(pkt.latents.shape, dtype=torch.int8, device="cuda")
+    idx = torch.zeros(max(sc.n, 1), dtype=torch.int32, device="cuda")
+    val = torch.zeros((3, max(sc.n, 1)), dtype=torch.float32, device="cuda")
+    k = torch.zeros(1, dtype=torch.int32, device="cuda")
+    Q.queen_decode_residuals(ctx, dp.struct, resid, q, idx, val, k)
+    st, _ = ctx.check_status()
+    assert st == 0
+    r = resid.cpu().numpy()
+    assert _attr_close(r[:, : sc.n], ref[:, : sc.n])
+    assert np.array_equal(r[:, : sc.n].view(np.uint32), ref[:, : sc.n].view(np.uint32))  # expected bit-identical
+    qref, bad = oracle.quantize(pkt.latents_f32) if f32 else (pkt.latents, 0)
+    assert np.array_equal(q.cpu().numpy()[:, : sc.n], qref[:, : sc.n])
+    oi, ov = oracle.gate(pkt)
+    kk = int(k.item())
+    assert kk == oi.shape[0]
+    assert np.array_equal(idx.cpu().numpy()[:kk].view(np.uint32), oi)
+    gv = val.cpu().numpy()[:, :kk]
+    assert np.array_equal(gv.view(np.uint32), ov.view(np.uint32))
+
+
+@pytest.mark.parametrize("mode", ["coo_int8", "gates_f32"])
+@pytest.mark.parametrize("name,n", [("tiny", 1000), ("n3dv", 30001), ("stress", 4099)])
+def test_apply_frame_parity(mode, name, n):
+    from tests.gpu_helpers import gpu_apply
+    cfg, sc = _scene(name, n)
+    pkt = synth.make_packet(sc, 2)
+    gates = mode.startswith("gates")
+    f32 = mode.endswith("f32")
+    ref, st, _ = oracle.apply(sc.planes, pkt, use_gates=gates, use_f32_latents=f32)
+    got, gst = gpu_apply(sc.planes, pkt, gates=gates, f32=f32)
+    assert st == 0 and gst == 0
+    assert _attr_close(got[:, : sc.n], ref[:, : sc.n])
+    assert np.array_equal(got[:, : sc.n].view(np.uint32), ref[:, : sc.n].view(np.uint32))
+    assert np.array_equal(got[:, sc.n:], sc.planes[:, sc.n:])  # padding untouched
+
+
+def test_dyadic_stream_exact_on_gpu():
+    """Drift-free streaming: 10 frames of dyadic packets, GPU == int64 closed form (exact)."""
+    from tests.gpu_helpers import gpu_apply
+    cfg = synth.get_config("n3dv")
+    sc = synth.make_dyadic_scene(cfg, n=5000)
+    pkts = [synth.make_packet(sc, t, dyadic=True) for t in range(1, 11)]
+    got, st = gpu_apply(sc.planes, pkts[0], frames_pkts=pkts)
+    A = sc.planes.copy()
+    for p in pkts:
+        A, s, _ = oracle.apply(A, p)
+    assert st == 0
+    assert np.array_equal(got, A)
+
+
+def test_zero_residual_keeps_scene():
+    from tests.gpu_helpers import gpu_apply
+    cfg, sc = _scene("n3dv", 10000)
+    pkt = synth.zero_packet(sc)
+    got, st = gpu_apply(sc.planes, pkt)
+    assert st == 0 and np.array_equal(got, sc.planes)
+
+
+def test_device_errors_reported():
+    from tests.gpu_helpers import gpu_apply
+    cfg, sc = _scene("tiny")
+    pkt = synth.make_packet(sc, 1)
+    pkt.coo_idx = pkt.coo_idx.copy()
+    pkt.coo_idx[3] = pkt.coo_idx[2]  # not strictly increasing
+    _, st = gpu_apply(sc.planes, pkt)
+    assert st == -3
+    pkt = synth.make_packet(sc, 1)
+    pkt.coo_idx = pkt.coo_idx.copy()
+    pkt.coo_idx[-1] = sc.n  # out of range
+    _, st = gpu_apply(sc.planes, pkt)
+    assert st == -3
+    pkt = synth.make_packet(sc, 1)
+    pkt.latents_f32[2, 5] = 200.0
+    _, st = gpu_apply(sc.planes, pkt, f32=True)
+    assert st == -4
+
+
+# ------------------------------------------------------------------ render stages
+def _render_case(name, n=None, views=None, **over):
+    cfg, sc = _scene(name, n, **over)
+    cams = synth.make_cameras(cfg, views)
+    return cfg, sc, cams
+
+
+def _check_proj(got, ref, n):
+    for key in ("depth", "tiles", "rect"):
+        assert np.array_equal(got[key][:, :n], ref[key][:, :n]), key
+    g, r = got["rec"][:, :n], ref["rec"][:, :n]
+    assert np.array_equal(g[..., :8].view(np.uint32), r[..., :8].view(np.uint32))  # u v A2 B2 C2 T2 o pad
+    assert np.all(np.abs(g[..., 8:] - r[..., 8:]) <= 1e-5 * np.maximum(np.abs(r[..., 8:]), 1e-6) + 1e-7)
+
+
+def _check_bins(got, ref):
+    assert got["K"] == ref["K"]
+    assert np.array_equal(got["offsets"], ref["offsets"])
+    assert np.array_equal(got["keys"], ref["keys"])
+    assert np.array_equal(got["vals"], ref["vals"])
+    assert np.array_equal(got["ranges"], ref["ranges"])
+
+
+def _check_image(rgb, T, rref, Tref):
+    a, b = np.clip(rgb, 0, 1), np.clip(rref, 0, 1)
+    from tests.gpu_helpers import psnr
+    err = np.abs(a - b).max()
+    assert err <= RGB_TOL, err
+    assert np.abs(T - Tref).max() <= RGB_TOL
+    assert psnr(a, b) > 60.0
+
+
+@pytest.mark.parametrize("case", [("tiny", None, None, {}),
+                                  ("tiny", 337, None, {"index": 7}),
+                                  ("n3dv", 20003, 3, {"width": 333, "height": 250, "focal": 280.0}),
+                                  ("immersive", 12001, 5, {"width": 320, "height": 240, "focal": 160.0}),
+                                  ("meetroom", 8000, 13, {"width": 160, "height": 90, "focal": 125.0})])
+def test_render_stages_parity(case):
+    from tests.gpu_helpers import Stages
+    name, n, views, over = case
+    cfg, sc, cams = _render_case(name, n, views, **over)
+    W, H = cams[0].width, cams[0].height
+    proj, bins, rgb, T = oracle.render(sc.planes, sc.n, sc.deg, cams)
+    st = Stages(sc.planes, sc.n, sc.deg, cams).run()
+    _check_proj(st.proj_np(), proj, sc.n)
+    _check_bins(st.bins_np(), bins)
+    g_rgb, g_T = st.image_np()
+    _check_image(g_rgb, g_T, rgb, T)
+    s, _ = st.ctx.check_status()
+    assert s == 0
+
+
+def test_render_big_gaussians_ragged():
+    """Large, overlapping, off-screen and near-plane Gaussians; ragged 70x45 image; degree 3."""
+    from tests.gpu_helpers import Stages
+    rng = np.random.default_rng(11)
+    n = 2001
+    pos = np.stack([rng.uniform(-3, 3, n), rng.uniform(-2, 2, n), rng.uniform(0.1, 6, n)], 1)
+    pl = planes_from(pos, rng.standard_normal((n, 4)), rng.normal(math.log(0.15), 0.8, (n, 3)), rng.normal(0, 2.5, n),
+                     rng.normal(0, 0.5, (n, 16, 3)), 3)
+    cams = [synth.make_camera(np.eye(3), np.zeros(3), 40.0, 40.0, 70, 45)]
+    proj, bins, rgb, T = oracle.render(pl, n, 3, cams, bg=(0.1, 0.2, 0.3))
+    st = Stages(pl, n, 3, cams).run(bg=(0.1, 0.2, 0.3))
+    _check_proj(st.proj_np(), proj, n)
+    _check_bins(st.bins_np(), bins)
+    _check_image(*st.image_np(), rgb, T)
+
+
+def test_empty_and_all_culled():
+    from tests.gpu_helpers import Stages
+    pl = planes_from([[0, 0, -5.0]] * 8, [[1, 0, 0, 0]] * 8, [[-3] * 3] * 8, [2.0] * 8,
+                     [np.zeros((1, 3))] * 8, 0)
+    cams = [synth.make_camera(np.eye(3), np.zeros(3), 30.0, 30.0, 40, 24)]
+    st = Stages(pl, 8, 0, cams).run(bg=(0.25, 0.5, 1.0))
+    rgb, T = st.image_np()
+    assert st.bins_np()["K"] == 0
+    assert np.all(T == 1.0) and np.all(rgb[0, 0] == 0.25) and np.all(rgb[0, 2] == 1.0)
+
+
+def test_nonfinite_warns_and_culls():
+    from tests.gpu_helpers import Stages
+    cfg, sc, cams = _render_case("tiny")
+    pl = sc.planes.copy()
+    pl[8, 10] = np.inf
+    pl[20 % pl.shape[0], 11] = np.nan
+    proj, bins, rgb, T = oracle.render(pl, sc.n, sc.deg, cams)
+    st = Stages(pl, sc.n, sc.deg, cams).run()
+    s, _ = st.ctx.check_status()
+    assert s == 1  # QUEEN_WARN_NONFINITE
+    _check_proj(st.proj_np(), proj, sc.n)
+    _check_image(*st.image_np(), rgb, T)
+
+
+def test_capacity_error_reports_needed_keys():
+    from tests.gpu_helpers import Stages
+    cfg, sc, cams = _render_case("tiny")
+    proj, bins, rgb, T = oracle.render(sc.planes, sc.n, sc.deg, cams)
+    st = Stages(sc.planes, sc.n, sc.deg, cams, keys_cap=max(1, bins["K"] // 2)).run()
+    s, info = st.ctx.check_status()
+    assert s == -5 and info == bins["K"]
+
+
+def test_render_views_equals_stages_and_deterministic():
+    import paper_2412_04469_b200 as Q
+    from paper_2412_04469_b200.runtime import Player
+    from tests.gpu_helpers import Stages
+    cfg, sc, cams = _render_case("n3dv", 20003, 4, width=200, height=150, focal=170.0)
+    st = Stages(sc.planes, sc.n, sc.deg, cams).run()
+    rgb_s, T_s = st.image_np()
+    pl = Player(sc.planes, sc.n, sc.deg, cams, with_T=True)
+    pl.fit_capacity()
+    a = pl.render().cpu().numpy()
+    b = pl.render().cpu().numpy()
+    assert np.array_equal(a, rgb_s) and np.array_equal(pl.T.cpu().numpy(), T_s)
+    assert np.array_equal(a, b)
+    # 2 batches of 2 views == 1 batch of 4 views (bit-identical)
+    pl2 = Player(sc.planes, sc.n, sc.deg, cams, views_per_batch=2)
+    pl2.fit_capacity()
+    assert np.array_equal(pl2.render().cpu().numpy(), a)
+    assert Q.QUEEN_MAX_VIEWS == 64
+
+
+def test_wire_packet_roundtrip_apply():
+    """Packed wire packet (k read on device) applies exactly like the host-side COO packet."""
+    from paper_2412_04469_b200 import packet as wire
+    import paper_2412_04469_b200 as Q
+    from paper_2412_04469_b200.runtime import wire_packet
+    cfg, sc = _scene("n3dv", 9001)
+    pkt = synth.make_packet(sc, 3)
+    buf = wire.pack(pkt, frame=3, k_cap=pkt.k + 100)
+    hdr = wire.header(buf)
+    dbuf = torch.from_numpy(buf).cuda()
+    dp = wire_packet(dbuf, hdr)
+    ctx = Q.Context(0)
+    ctx.set_workspace(sc.n_pad, 1, 16, 16, 1024)
+    pl = torch.from_numpy(sc.planes.copy()).cuda()
+    Q.queen_apply_frame(ctx, Q.gaussians_struct(pl, sc.n, sc.deg), dp.struct)
+    s, _ = ctx.check_status()
+    ref, _, _ = oracle.apply(sc.planes, pkt)
+    assert s == 0 and np.array_equal(pl.cpu().numpy(), ref)
+
+
+# ------------------------------------------------------------------ full-size configs (sampled)
+@pytest.mark.parametrize("name", ["n3dv", "immersive"])
+def test_full_size_frame_sampled(name):
+    """BASELINE configs at full size, in bench.py's launch configuration (Player, frame 1 applied):
+    SoA after apply bit-exact; projection records for all views bit-exact; bins bit-exact for the
+    first batch; 4096 sampled pixels per view within tolerance."""
+    from paper_2412_04469_b200.runtime import Player, device_packet
+    cfg = synth.get_config(name)
+    sc = synth.make_scene(cfg)
+    cams = synth.make_cameras(cfg)
+    pkt = synth.make_packet(sc, 1)
+    vpb = 10 if name == "n3dv" else 8
+    pl = Player(sc.planes, sc.n, sc.deg, cams, views_per_batch=vpb)
+    pl.apply(device_packet(pkt, pl.dev))
+    A1, st, _ = oracle.apply(sc.planes, pkt)
+    assert np.array_equal(pl.planes.cpu().numpy(), A1)
+    pl.fit_capacity()
+    rgb = pl.render().cpu().numpy()
+    s, _ = pl.ctx.check_status()
+    assert s == 0
+    W, H = cams[0].width, cams[0].height
+    rng = np.random.default_rng(5)
+    for b0 in range(0, len(cams), vpb):
+        bc = cams[b0:b0 + vpb]
+        proj = oracle.project(A1, sc.n, sc.deg, bc)
+        bins = oracle.bin_sort(proj, W, H) if b0 == 0 else None
+        if b0 == 0:
+            from tests.gpu_helpers import Stages
+            stg = Stages(A1, sc.n, sc.deg, bc, keys_cap=pl.keys_cap).project().bin_sort()
+            _check_proj(stg.proj_np(), proj, sc.n)
+            _check_bins(stg.bins_np(), bins)
+            del stg
+        else:
+            bins = oracle.bin_sort(proj, W, H)
+        V = len(bc)
+        pix = np.stack([np.repeat(np.arange(V), 4096), rng.integers(0, W, V * 4096), rng.integers(0, H, V * 4096)], 1)
+        orgb, oT = oracle.rasterize_pixels(proj["rec"], bins["ranges"], bins["vals"], W, H, pix)
+        g = rgb[b0 + pix[:, 0], :, pix[:, 2], pix[:, 1]]
+        assert np.abs(np.clip(g, 0, 1) - np.clip(orgb, 0, 1)).max() <= RGB_TOL
+        del proj, bins
