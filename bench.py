@@ -53,8 +53,7 @@ def parse():
 def default_vpb(cfg):
     # key buffers per batch ~ 24 B/key x ~8 keys/Gaussian/view: keep one batch <= ~6 GB
     per_view = 8 * cfg.n * 24 * 1.5
-    return int(max(1, min(cfg.views, synth.QUEEN_MAX_VIEWS if hasattr(synth, "QUEEN_MAX_VIEWS") else 64,
-                          (6 << 30) // per_view)))
+    return int(max(1, min(cfg.views, 64, (6 << 30) // per_view)))
 
 
 def rank_views(V, rank, world):
@@ -260,7 +259,7 @@ def main():
         kc = torch.tensor([k_cap], device=dev)
         dist.broadcast(kc, 0)
         k_cap = int(kc.item())
-    lay = wire.layout(sc.n_pad, cfg.deg, cfg.lat if cfg.deg else cfg.lat[:4] + (0,), k_cap)
+    lay = wire.layout(sc.n_pad, cfg.deg, cfg.lat, k_cap)
     hdr = dict(n=sc.n, n_pad=sc.n_pad, deg=cfg.deg, lat=tuple(cfg.lat), k_cap=k_cap, **{k: lay[k] for k in
                                                                                           ("dec_off", "lat_off", "idx_off", "val_off")})
     if rank == 0:
@@ -331,7 +330,7 @@ def main():
 
     # ---- evidence (outside the timed region): K per batch, blend work counts
     batches = [cams[a:b] for a, b in player.batches]
-    from tests.gpu_helpers import Stages  # explicit-buffer stage runner over the same C-ABI
+    from paper_2412_04469_b200.stages import Stages  # explicit-buffer stage runner over the same C-ABI
     K_list, ev_pairs, cp_pairs = [], 0, 0
     for bc in batches:
         stg = Stages(player.planes.cpu().numpy(), sc.n, sc.deg, bc, keys_cap=player.keys_cap, device=local)
