@@ -121,19 +121,20 @@ typedef struct {
     int16_t* rect;
 } queen_proj;
 
-/* Binning buffers for one batch of equally-sized views (gt = view*T + tile, T = gx*gy):
- *   offsets[n_views][n_pad]  exclusive prefix sum of tiles (u32)
- *   keys/vals (+ _alt ping-pong) [keys_cap]: key = (gt << 31) | depth, val = Gaussian index
- *   ranges[n_views*T][2]     [first, last+1) of gt in the sorted keys, [0,0) if empty
- *   K (device u32[1])        total keys of the batch
- *   sorted_in_alt            OUT (host): 1 if the sorted result is in keys_alt/vals_alt */
+/* Binning buffers for one batch of equally-sized views (gt = view*T + tile, T = gx*gy).
+ * The entries are the (16x16 tile, Gaussian) pairs, sorted by the composite key
+ * (gt << 31 | depth bits) and then Gaussian index:
+ *   keys/vals (+ _alt ping-pong) [keys_cap] u32: key = gt of the entry, val = Gaussian
+ *            index (the entry's full sort key is (gt << 31) | proj.depth[view][val])
+ *   ranges[n_views*T][2] u32  [first, last+1) of gt in the sorted entries, [0,0) if empty
+ *   K (device u32[2])         [0] = entries K of the batch, [1] = visible (view, Gaussian) pairs
+ *   sorted_in_alt             OUT (host): 1 if the sorted result is in keys_alt/vals_alt */
 typedef struct {
     int64_t keys_cap;
-    uint64_t* keys;
-    uint64_t* keys_alt;
+    uint32_t* keys;
+    uint32_t* keys_alt;
     uint32_t* vals;
     uint32_t* vals_alt;
-    uint32_t* offsets;
     uint32_t* ranges;
     uint32_t* K;
     int32_t sorted_in_alt;

@@ -29,7 +29,7 @@ EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version",
            "queen_set_workspace", "queen_check", "queen_decode_residuals", "queen_apply_frame", "queen_project",
            "queen_bin_sort", "queen_rasterize", "queen_render_views", "queen_blend_counts",
            "queen_profile_enable", "queen_profile_read"]
-STAGES = ["apply", "project", "scan", "duplicate", "hist", "sort", "ranges", "blend"]
+STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend"]
 
 
 class QueenError(RuntimeError):
@@ -64,7 +64,7 @@ class QueenProj(C.Structure):
 
 class QueenBins(C.Structure):
     _fields_ = [("keys_cap", C.c_int64), ("keys", C.c_void_p), ("keys_alt", C.c_void_p), ("vals", C.c_void_p),
-                ("vals_alt", C.c_void_p), ("offsets", C.c_void_p), ("ranges", C.c_void_p), ("K", C.c_void_p),
+                ("vals_alt", C.c_void_p), ("ranges", C.c_void_p), ("K", C.c_void_p),
                 ("sorted_in_alt", C.c_int32)]
 
 
@@ -260,11 +260,11 @@ def proj_struct(rec, depth, tiles, rect) -> QueenProj:
     return pj
 
 
-def bins_struct(keys, keys_alt, vals, vals_alt, offsets, ranges, K) -> QueenBins:
+def bins_struct(keys, keys_alt, vals, vals_alt, ranges, K) -> QueenBins:
     b = QueenBins()
     b.keys_cap = keys.shape[0]
     b.keys, b.keys_alt, b.vals, b.vals_alt = _ptr(keys), _ptr(keys_alt), _ptr(vals), _ptr(vals_alt)
-    b.offsets, b.ranges, b.K = _ptr(offsets), _ptr(ranges), _ptr(K)
+    b.ranges, b.K = _ptr(ranges), _ptr(K)
     b.sorted_in_alt = 0
     return b
 

@@ -1,15 +1,27 @@
-// K3-K6: binning for a batch of equally-sized views (BASELINE north_star: "warp-level
-// scans and a custom onesweep radix sort").
-//   K3 k_scan_tiles   single-pass decoupled look-back exclusive scan of tiles touched
-//   K4 k_duplicate    one (key, val) per touched 16x16 tile, key = (gt << 31) | depth
-//   K5 k_hist + k_onesweep  LSD radix sort, 8-bit digits: one global histogram pass
-//                     for all digits, then one pass per digit that ranks a 4096-key tile
-//                     with warp match_any multisplit (stable), resolves the tile's
-//                     global digit offsets by decoupled look-back, stages the tile in
-//                     shared memory in digit order and writes it out coalesced.
-//   K6 k_ranges       [first, last+1) per global tile from the sorted keys
-// Order = (view, tile, depth, index): the sort is stable and keys are emitted in
-// ascending Gaussian index, so results equal the oracle's std::sort on (key, val).
+// K3-K6: binning for a batch of equally-sized views (BASELINE north_star: "duplication
+// of Gaussians into 16x16 tiles, a radix sort on (tile, depth) keys, per-tile range
+// extraction"; "warp-level scans and a custom onesweep radix sort").
+//
+// The sort is an LSD radix sort on the composite key (gt, depth) with gt = view*T +
+// tile: LSD order processes the depth digits first and the tile digits last.  Every
+// duplicate of a Gaussian carries the same depth, so the depth digits are sorted
+// BEFORE duplication, on the M visible (view, Gaussian) pairs (M << K), and only the
+// tile digits are sorted on the K duplicated entries, with 4-byte keys:
+//   K3a k_vis_compact   decoupled look-back scan: visible pairs (tiles > 0) in (view,
+//                       index) order -> (depth bits, flat index)            [M]
+//   K5a k_onesweep32<8> x4  stable sort of the pairs by depth (31 bits)
+//   K3b/K4 k_scan_dup   decoupled look-back scan of tiles touched in depth order fused
+//                       with duplication: entry = (gt, Gaussian index), emitted for
+//                       each pair ty-major, tx-minor; fused tile-digit histograms
+//   K5b k_onesweep32<8|9> x2..3  stable sort of the entries by gt
+//   K6  k_ranges        [first, last+1) of each gt
+// Stability makes the final order (gt, depth, view, index) -> (gt, depth, index):
+// identical to sorting the 96-bit (gt << 31 | depth, index) tuples (oracle: std::sort).
+//
+// onesweep pass: persistent CTAs take 4096-key tiles by atomic ticket (forward
+// progress for the look-back), rank keys with warp match_any multisplit in key order
+// (stable), publish per-digit tile counts, resolve global digit offsets by decoupled
+// look-back, stage the tile in shared memory in digit order and write it out coalesced.
 #include "queen_internal.cuh"
 
 namespace queen {
@@ -26,262 +38,246 @@ __device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) { *rein
 constexpr unsigned long long SCAN_AGG = 1ull << 62, SCAN_INC = 2ull << 62, SCAN_MASK = (1ull << 62) - 1;
 constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_MASK = (1u << 30) - 1;
 constexpr long long SPIN_LIMIT = 1ll << 24;
+constexpr int SORT_WARPS = SORT_THREADS / 32;
 
-// ---------------------------------------------------------------------------
-// K3: offsets[j] = sum_{j' < j} tiles[j'] over the flattened [V][n_pad] array; K = total
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_tiles(const uint32_t* __restrict__ tiles,
-                                                             uint32_t* __restrict__ offsets, int64_t count,
-                                                             unsigned long long* lb, DevFlags* fl, uint32_t* K_out,
-                                                             int64_t cap) {
-    __shared__ uint32_t s_tile;
-    __shared__ uint32_t s_wsum[SCAN_THREADS / 32];
-    __shared__ unsigned long long s_prefix;
-    if (threadIdx.x == 0) s_tile = atomicAdd(&fl->tickets[8], 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const int64_t ntiles = (count + SCAN_TILE - 1) / SCAN_TILE;
-    const int64_t base = (int64_t)tile * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
-    uint32_t v[SCAN_ITEMS];
-#pragma unroll
-    for (int q = 0; q < SCAN_ITEMS / 4; ++q) {
-        uint4 x = make_uint4(0, 0, 0, 0);
-        if (base + 4 * q < count) x = __ldg(reinterpret_cast<const uint4*>(tiles + base + 4 * q));
-        v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
-    }
-    uint32_t tsum = 0;
-#pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; ++j) tsum += v[j];
+enum : int { TK_DEPTH = 0, TK_TILE = 4, TK_VIS = 8, TK_DUP = 9 };
+
+// Block-wide exclusive scan of one u32 per thread (256 threads); returns the exclusive
+// prefix and the block total.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* s_w, uint32_t& total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t x = tsum;
+    uint32_t inc = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
     }
-    if (lane == 31) s_wsum[w] = x;
+    if (lane == 31) s_w[w] = inc;
     __syncthreads();
-    uint32_t wpre = 0, agg = 0;
+    uint32_t pre = 0, tot = 0;
 #pragma unroll
-    for (int q = 0; q < SCAN_THREADS / 32; ++q) {
-        const uint32_t s = s_wsum[q];
-        if (q < w) wpre += s;
-        agg += s;
+    for (int q = 0; q < SORT_WARPS; ++q) {
+        const uint32_t s = s_w[q];
+        pre += (q < w) ? s : 0u;
+        tot += s;
     }
+    total = tot;
+    return pre + inc - x;
+}
+
+// Decoupled look-back over 64-bit aggregates (called by one thread).
+__device__ unsigned long long lookback64(unsigned long long* lb, uint32_t tile, unsigned long long agg, DevFlags* fl) {
+    unsigned long long prefix = 0;
+    if (tile == 0) {
+        st_volatile_u64(&lb[0], SCAN_INC | agg);
+        return 0;
+    }
+    st_volatile_u64(&lb[tile], SCAN_AGG | agg);
+    int64_t look = (int64_t)tile - 1;
+    long long spins = 0;
+    while (look >= 0) {
+        const unsigned long long e = ld_volatile_u64(&lb[look]);
+        if ((e >> 62) == 0) {
+            if (++spins > SPIN_LIMIT) { raise_flag(fl, FLAG_TIMEOUT); break; }
+            continue;
+        }
+        prefix += e & SCAN_MASK;
+        if ((e >> 62) == 2) break;
+        --look;
+    }
+    st_volatile_u64(&lb[tile], SCAN_INC | (prefix + agg));
+    return prefix;
+}
+
+// ---------------------------------------------------------------------------
+// K3a: visible (view, Gaussian) pairs, in flat-index order -> (depth bits, j)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(SORT_THREADS) k_vis_compact(const uint32_t* __restrict__ tiles,
+                                                              const uint32_t* __restrict__ depth, int64_t count,
+                                                              uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
+                                                              unsigned long long* lb, DevFlags* fl, uint32_t* M_out) {
+    __shared__ uint32_t s_tile, s_w[SORT_WARPS];
+    __shared__ unsigned long long s_prefix;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&fl->tickets[TK_VIS], 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t ntiles = (count + SORT_TILE - 1) / SORT_TILE;
+    const int64_t base = (int64_t)tile * SORT_TILE + (int64_t)threadIdx.x * SORT_ITEMS;
+    uint32_t vis = 0;  // bit e set <=> element base+e is visible
+#pragma unroll
+    for (int q = 0; q < SORT_ITEMS / 4; ++q) {
+        if (base + 4 * q < count) {
+            const uint4 t4 = __ldg(reinterpret_cast<const uint4*>(tiles + base + 4 * q));
+            vis |= (t4.x ? 1u : 0u) << (4 * q) | (t4.y ? 2u : 0u) << (4 * q) | (t4.z ? 4u : 0u) << (4 * q) |
+                   (t4.w ? 8u : 0u) << (4 * q);
+        }
+    }
+    uint32_t total;
+    const uint32_t excl = block_excl_scan(__popc(vis), s_w, total);
     if (threadIdx.x == 0) {
-        unsigned long long prefix = 0;
-        if (tile == 0) {
-            st_volatile_u64(&lb[0], SCAN_INC | agg);
-        } else {
-            st_volatile_u64(&lb[tile], SCAN_AGG | agg);
-            int64_t look = (int64_t)tile - 1;
-            long long spins = 0;
-            while (look >= 0) {
-                const unsigned long long e = ld_volatile_u64(&lb[look]);
-                if ((e >> 62) == 0) {
-                    if (++spins > SPIN_LIMIT) { raise_flag(fl, FLAG_TIMEOUT); break; }
-                    continue;
-                }
-                prefix += e & SCAN_MASK;
-                if ((e >> 62) == 2) break;
-                --look;
-            }
-            st_volatile_u64(&lb[tile], SCAN_INC | (prefix + agg));
-        }
-        s_prefix = prefix;
-        if ((int64_t)tile == ntiles - 1) {
-            const unsigned long long total = prefix + agg;
-            if ((long long)total > cap) {
-                raise_flag(fl, FLAG_CAPACITY);
-                atomicMax(&fl->info, total);
-            }
-            K_out[0] = (uint32_t)(total > (unsigned long long)cap ? cap : total);
-        }
+        s_prefix = lookback64(lb, tile, total, fl);
+        if ((int64_t)tile == ntiles - 1) *M_out = (uint32_t)(s_prefix + total);
     }
     __syncthreads();
-    unsigned long long run = s_prefix + wpre + (x - tsum);
-    uint32_t o[SCAN_ITEMS];
+    uint64_t pos = s_prefix + excl;
+    while (vis) {
+        const int e = __ffs(vis) - 1;
+        vis &= vis - 1;
+        const int64_t j = base + e;
+        dkeys[pos] = __ldg(depth + j);
+        dvals[pos] = (uint32_t)j;
+        ++pos;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5: histograms of the depth digits (4 x 8 bits) of the M visible pairs
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_hist_depth(const uint32_t* __restrict__ keys, const uint32_t* count_ptr,
+                                                    uint32_t* hist) {
+    __shared__ uint32_t sh[DEPTH_PASSES * 256];
+    for (int q = threadIdx.x; q < DEPTH_PASSES * 256; q += blockDim.x) sh[q] = 0;
+    __syncthreads();
+    const uint32_t n = *count_ptr;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t k = keys[j];
 #pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; ++j) {
-        o[j] = (uint32_t)run;
-        run += v[j];
-    }
-#pragma unroll
-    for (int q = 0; q < SCAN_ITEMS / 4; ++q)
-        if (base + 4 * q < count)
-            *reinterpret_cast<uint4*>(offsets + base + 4 * q) = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-}
-
-// ---------------------------------------------------------------------------
-// K4: duplicate.  For (v, i) ascending, ty ascending, tx ascending (R#15).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_duplicate(const uint32_t* __restrict__ tiles, const uint32_t* __restrict__ offsets,
-                                                   const short4* __restrict__ rect, const uint32_t* __restrict__ depth,
-                                                   int64_t count, int n_pad, int gx, int64_t T,
-                                                   uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, int64_t cap) {
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= count) return;
-    const uint32_t nt = tiles[j];
-    if (nt == 0) return;
-    const int64_t v = j / n_pad;
-    const uint32_t i = (uint32_t)(j - v * n_pad);
-    const short4 r = rect[j];
-    const uint64_t d = depth[j];
-    int64_t w = offsets[j];
-    const uint64_t gbase = (uint64_t)v * (uint64_t)T;
-    for (int ty = r.y; ty <= r.w; ++ty) {
-        const uint64_t rowg = gbase + (uint64_t)ty * gx;
-        for (int tx = r.x; tx <= r.z; ++tx) {
-            if (w < cap) {
-                keys[w] = ((rowg + (uint64_t)tx) << 31) | d;
-                vals[w] = i;
-            }
-            ++w;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K5a: histograms of every 8-bit digit of every key (one read of the keys)
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_hist(const uint64_t* __restrict__ keys, const uint32_t* K, int64_t cap,
-                                              int passes, uint32_t* hist) {
-    __shared__ uint32_t sh[MAX_PASSES * 256];
-    for (int q = threadIdx.x; q < MAX_PASSES * 256; q += blockDim.x) sh[q] = 0;
-    __syncthreads();
-    const int64_t Kn = min((int64_t)*K, cap);
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < Kn; j += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = keys[j];
-        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * 256 + ((k >> (8 * p)) & 255u)], 1u);
+        for (int p = 0; p < DEPTH_PASSES; ++p) atomicAdd(&sh[p * 256 + ((k >> (8 * p)) & 255u)], 1u);
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < passes * 256; q += blockDim.x)
-        if (sh[q]) atomicAdd(&hist[q], sh[q]);
+    for (int q = threadIdx.x; q < DEPTH_PASSES * 256; q += blockDim.x)
+        if (sh[q]) atomicAdd(&hist[(q >> 8) * MAX_BINS + (q & 255)], sh[q]);  // per-pass stride MAX_BINS
 }
 
-// K5b: exclusive scan of each pass's 256 digit counts (one block, one warp per pass)
-__global__ void k_hist_scan(const uint32_t* hist, uint32_t* excl, int passes) {
+// exclusive scan of each pass's digit counts (one warp per pass)
+__global__ void k_hist_scan(const uint32_t* hist, uint32_t* excl, int passes, int bins) {
     const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (p >= passes) return;
-    uint32_t v[8], s = 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) { v[q] = hist[p * 256 + lane * 8 + q]; s += v[q]; }
+    const int per = bins / 32;
+    uint32_t s = 0;
+    for (int q = 0; q < per; ++q) s += hist[p * MAX_BINS + lane * per + q];
     uint32_t x = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
     uint32_t run = x - s;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) { excl[p * 256 + lane * 8 + q] = run; run += v[q]; }
+    for (int q = 0; q < per; ++q) {
+        const uint32_t c = hist[p * MAX_BINS + lane * per + q];
+        excl[p * MAX_BINS + lane * per + q] = run;
+        run += c;
+    }
 }
 
 // ---------------------------------------------------------------------------
-// K5c: one onesweep pass (persistent CTAs, dynamic tile tickets => forward progress)
+// K5: one onesweep pass over (u32 key, u32 value) pairs
 // ---------------------------------------------------------------------------
-constexpr int SORT_WARPS = SORT_THREADS / 32;
-constexpr size_t ONESWEEP_SMEM = (size_t)SORT_TILE * 8 + (size_t)SORT_TILE * 4 + (size_t)SORT_WARPS * 256 * 4 + 256 * 4 * 2;
+template <int BITS>
+struct Onesweep {
+    static constexpr int BINS = 1 << BITS;
+    static constexpr int DPT = BINS / SORT_THREADS;
+    static constexpr size_t SMEM = (size_t)SORT_TILE * 4 * 2 + (size_t)SORT_WARPS * BINS * 4 + (size_t)BINS * 4 * 2;
+};
 
-__global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                           uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                           const uint32_t* K, int64_t cap, int shift,
-                                                           const uint32_t* __restrict__ hist_excl, uint32_t* lb,
-                                                           uint32_t* ticket, DevFlags* fl) {
+template <int BITS>
+__global__ void __launch_bounds__(SORT_THREADS) k_onesweep32(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                             uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                             const uint32_t* count_ptr, uint32_t cap, int shift,
+                                                             const uint32_t* __restrict__ hist_excl, uint32_t* lb,
+                                                             uint32_t* ticket, DevFlags* fl) {
+    constexpr int BINS = Onesweep<BITS>::BINS;
+    constexpr int DPT = Onesweep<BITS>::DPT;
+    constexpr uint32_t DMASK = BINS - 1;
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* sk = reinterpret_cast<uint64_t*>(smem);
-    uint32_t* sv = reinterpret_cast<uint32_t*>(sk + SORT_TILE);
-    uint32_t* whist = sv + SORT_TILE;          // [warps][256]
-    uint32_t* dstart = whist + SORT_WARPS * 256;  // [256] tile-local exclusive digit start
-    uint32_t* dbase = dstart + 256;            // [256] global base minus local start
-    __shared__ uint32_t s_tile;
-    __shared__ uint32_t s_wtot[SORT_WARPS];
-    const uint32_t Kn = (uint32_t)min((int64_t)*K, cap);
+    uint32_t* sk = reinterpret_cast<uint32_t*>(smem);
+    uint32_t* sv = sk + SORT_TILE;
+    uint32_t* whist = sv + SORT_TILE;             // [warps][BINS]: counts, then exclusive-over-warps
+    uint32_t* dstart = whist + SORT_WARPS * BINS;  // [BINS] tile-local exclusive digit start
+    uint32_t* dbase = dstart + BINS;              // [BINS] global destination minus local start
+    __shared__ uint32_t s_tile, s_w[SORT_WARPS];
+    const uint32_t Kn = min(*count_ptr, cap);
     const uint32_t ntiles = (Kn + SORT_TILE - 1) / SORT_TILE;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-#pragma unroll
-        for (int q = 0; q < SORT_WARPS; ++q) whist[q * 256 + threadIdx.x] = 0u;
+        for (int q = threadIdx.x; q < SORT_WARPS * BINS; q += SORT_THREADS) whist[q] = 0u;
         __syncthreads();
         const uint32_t tile = s_tile;
         if (tile >= ntiles) break;
         const uint32_t base = tile * SORT_TILE;
-        uint64_t k[SORT_ITEMS];
-        uint32_t val[SORT_ITEMS], rank[SORT_ITEMS], dig[SORT_ITEMS];
+        uint32_t k[SORT_ITEMS], val[SORT_ITEMS], rk[SORT_ITEMS];
 #pragma unroll
         for (int j = 0; j < SORT_ITEMS; ++j) {
             const uint32_t idx = base + w * (32 * SORT_ITEMS) + j * 32 + lane;
             const bool ok = idx < Kn;
-            k[j] = ok ? kin[idx] : 0ull;
+            k[j] = ok ? kin[idx] : 0u;
             val[j] = ok ? vin[idx] : 0u;
-            dig[j] = ok ? (uint32_t)((k[j] >> shift) & 255u) : 256u;
+            rk[j] = ok ? ((k[j] >> shift) & DMASK) : (uint32_t)BINS;
         }
-        // warp multisplit, in key order => stable
+        // warp multisplit in key order (stable): rank among this warp's earlier equal digits
 #pragma unroll
         for (int j = 0; j < SORT_ITEMS; ++j) {
-            const uint32_t d = dig[j];
+            const uint32_t d = rk[j];
             const uint32_t peers = __match_any_sync(0xffffffffu, d);
             const uint32_t below = peers & lt_mask;
             uint32_t prior = 0;
-            if (d < 256u) prior = whist[w * 256 + d];
+            if (d < (uint32_t)BINS) prior = whist[w * BINS + d];
             __syncwarp();
-            if (below == 0 && d < 256u) whist[w * 256 + d] = prior + __popc(peers);
+            if (below == 0 && d < (uint32_t)BINS) whist[w * BINS + d] = prior + __popc(peers);
             __syncwarp();
-            rank[j] = prior + __popc(below);
+            rk[j] = (prior + __popc(below)) | (d << 16);
         }
         __syncthreads();
-        // thread t <-> digit t: exclusive over warps, tile count
-        const uint32_t d = threadIdx.x;
-        uint32_t cnt = 0;
+        uint32_t cnt[DPT];
+        uint32_t tsum = 0;
 #pragma unroll
-        for (int q = 0; q < SORT_WARPS; ++q) {
-            const uint32_t c = whist[q * 256 + d];
-            whist[q * 256 + d] = cnt;
-            cnt += c;
-        }
-        uint32_t* lbt = lb + (size_t)tile * 256;
-        st_volatile_u32(&lbt[d], (tile == 0 ? LB_INC : LB_AGG) | cnt);
-        // tile-local exclusive scan over digits
-        uint32_t x = cnt;
+        for (int e = 0; e < DPT; ++e) {
+            const int d = threadIdx.x * DPT + e;
+            uint32_t run = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_wtot[w] = x;
-        // decoupled look-back for this digit
-        uint32_t prefix = 0;
-        if (tile > 0) {
-            int64_t look = (int64_t)tile - 1;
-            long long spins = 0;
-            while (look >= 0) {
-                const uint32_t e = ld_volatile_u32(&lb[(size_t)look * 256 + d]);
-                const uint32_t f = e >> 30;
-                if (f == 0) {
-                    if (++spins > SPIN_LIMIT) { raise_flag(fl, FLAG_TIMEOUT); break; }
-                    continue;
-                }
-                prefix += e & LB_MASK;
-                if (f == 2) break;
-                --look;
+            for (int q = 0; q < SORT_WARPS; ++q) {
+                const uint32_t c = whist[q * BINS + d];
+                whist[q * BINS + d] = run;
+                run += c;
             }
-            st_volatile_u32(&lbt[d], LB_INC | (prefix + cnt));
+            cnt[e] = run;
+            tsum += run;
+            st_volatile_u32(&lb[(size_t)tile * BINS + d], (tile == 0 ? LB_INC : LB_AGG) | run);
         }
-        __syncthreads();
-        uint32_t wpre = 0;
+        uint32_t total;
+        uint32_t excl = block_excl_scan(tsum, s_w, total);
 #pragma unroll
-        for (int q = 0; q < SORT_WARPS; ++q) wpre += (q < w) ? s_wtot[q] : 0u;
-        const uint32_t excl = wpre + x - cnt;
-        dstart[d] = excl;
-        dbase[d] = hist_excl[d] + prefix - excl;
+        for (int e = 0; e < DPT; ++e) {
+            const int d = threadIdx.x * DPT + e;
+            uint32_t prefix = 0;
+            if (tile > 0) {
+                int64_t look = (int64_t)tile - 1;
+                long long spins = 0;
+                while (look >= 0) {
+                    const uint32_t x = ld_volatile_u32(&lb[(size_t)look * BINS + d]);
+                    const uint32_t f = x >> 30;
+                    if (f == 0) {
+                        if (++spins > SPIN_LIMIT) { raise_flag(fl, FLAG_TIMEOUT); break; }
+                        continue;
+                    }
+                    prefix += x & LB_MASK;
+                    if (f == 2) break;
+                    --look;
+                }
+                st_volatile_u32(&lb[(size_t)tile * BINS + d], LB_INC | (prefix + cnt[e]));
+            }
+            dstart[d] = excl;
+            dbase[d] = hist_excl[d] + prefix - excl;
+            excl += cnt[e];
+        }
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < SORT_ITEMS; ++j) {
-            const uint32_t dj = dig[j];
-            if (dj < 256u) {
-                const uint32_t pos = dstart[dj] + whist[w * 256 + dj] + rank[j];
+            const uint32_t d = rk[j] >> 16;
+            if (d < (uint32_t)BINS) {
+                const uint32_t pos = dstart[d] + whist[w * BINS + d] + (rk[j] & 0xffffu);
                 sk[pos] = k[j];
                 sv[pos] = val[j];
             }
@@ -289,8 +285,8 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __res
         __syncthreads();
         const uint32_t nvalid = min((uint32_t)SORT_TILE, Kn - base);
         for (uint32_t p = threadIdx.x; p < nvalid; p += SORT_THREADS) {
-            const uint64_t key = sk[p];
-            const uint32_t dest = dbase[(uint32_t)((key >> shift) & 255u)] + p;
+            const uint32_t key = sk[p];
+            const uint32_t dest = dbase[(key >> shift) & DMASK] + p;
             kout[dest] = key;
             vout[dest] = sv[p];
         }
@@ -299,15 +295,120 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __res
 }
 
 // ---------------------------------------------------------------------------
-// K6: ranges[gt] = [first, last+1)
+// K3b + K4: offsets of the depth-sorted pairs (decoupled look-back) + duplication.
+// Entry = (gt, Gaussian index).  The block's 4096 pairs and their block-local offsets
+// are staged in shared memory; threads then stride over the block's OUTPUT entries
+// (load-balanced: an entry finds its pair by binary search over the offsets), so the
+// key/value stores are coalesced whatever the per-Gaussian tile counts are.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_ranges(const uint64_t* __restrict__ keys, const uint32_t* K, int64_t cap,
-                                                uint2* __restrict__ ranges) {
-    const uint32_t Kn = (uint32_t)min((int64_t)*K, cap);
+__global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __restrict__ dvals, const uint32_t* count_ptr,
+                                                           const uint32_t* __restrict__ tiles,
+                                                           const short4* __restrict__ rect, int n_pad, int gx,
+                                                           uint32_t T, uint32_t* __restrict__ keys,
+                                                           uint32_t* __restrict__ vals, uint32_t cap,
+                                                           unsigned long long* lb, DevFlags* fl, uint32_t* K_out) {
+    __shared__ uint32_t s_tile, s_w[SORT_WARPS];
+    __shared__ unsigned long long s_prefix;
+    __shared__ uint32_t s_off[SORT_TILE];
+    __shared__ uint32_t s_j[SORT_TILE];
+    const uint32_t M = *count_ptr;
+    const uint32_t ntiles = (M + SORT_TILE - 1) / SORT_TILE;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&fl->tickets[TK_DUP], 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) return;
+    const uint32_t base = tile * SORT_TILE + threadIdx.x * SORT_ITEMS;
+    uint32_t jj[SORT_ITEMS], nt[SORT_ITEMS];
+    uint32_t tsum = 0;
+#pragma unroll
+    for (int e = 0; e < SORT_ITEMS; ++e) {
+        const uint32_t m = base + e;
+        jj[e] = m < M ? __ldg(dvals + m) : 0u;
+        nt[e] = m < M ? __ldg(tiles + jj[e]) : 0u;
+        tsum += nt[e];
+    }
+    uint32_t total;
+    const uint32_t excl = block_excl_scan(tsum, s_w, total);
+    if (threadIdx.x == 0) {
+        s_prefix = lookback64(lb, tile, total, fl);
+        if (tile == ntiles - 1) {
+            const unsigned long long K = s_prefix + total;
+            if (K > cap) {
+                raise_flag(fl, FLAG_CAPACITY);
+                atomicMax(&fl->info, K);
+            }
+            K_out[0] = (uint32_t)(K > cap ? cap : K);
+        }
+    }
+    {
+        uint32_t run = excl;
+#pragma unroll
+        for (int e = 0; e < SORT_ITEMS; ++e) {
+            s_off[threadIdx.x * SORT_ITEMS + e] = run;
+            s_j[threadIdx.x * SORT_ITEMS + e] = jj[e];
+            run += nt[e];
+        }
+    }
+    __syncthreads();
+    const unsigned long long gbase = s_prefix;
+    for (uint32_t p = threadIdx.x; p < total; p += SORT_THREADS) {
+        // last pair whose block-local offset <= p (it owns entry p: pairs with 0 tiles share
+        // their successor's offset and come before it)
+        int lo = 0, hi = SORT_TILE;  // invariant: s_off[lo] <= p < s_off[hi] (s_off[SORT_TILE] := total)
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_off[mid] <= p) lo = mid; else hi = mid;
+        }
+        const uint32_t c = p - s_off[lo];
+        const uint32_t j = s_j[lo];
+        const short4 r = __ldg(rect + j);
+        const uint32_t wx = (uint32_t)(r.z - r.x + 1);
+        const uint32_t row = c / wx;
+        const uint32_t v = j / (uint32_t)n_pad;
+        const uint64_t w = gbase + p;
+        if (w < cap) {
+            keys[w] = v * T + (uint32_t)(r.y + (int)row) * (uint32_t)gx + (uint32_t)(r.x + (int)(c - row * wx));
+            vals[w] = j - v * (uint32_t)n_pad;
+        }
+    }
+}
+
+// K5b: histograms of the tile digits of the K entries (warp-aggregated smem atomics:
+// consecutive entries share their high digits, so peers are merged with match_any)
+__global__ void __launch_bounds__(256) k_hist_tile(const uint32_t* __restrict__ keys, const uint32_t* count_ptr,
+                                                   uint32_t* hist, int tpasses, int tbits) {
+    __shared__ uint32_t sh[MAX_TILE_PASSES * MAX_BINS];
+    for (int q = threadIdx.x; q < tpasses * MAX_BINS; q += blockDim.x) sh[q] = 0;
+    __syncthreads();
+    const uint32_t n = *count_ptr;
+    const uint32_t dmask = (1u << tbits) - 1u;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    // whole warps iterate together so match_any sees full warps
+    for (uint32_t j0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); j0 < n; j0 += stride) {
+        const uint32_t j = j0 + lane;
+        const bool ok = j < n;
+        const uint32_t g = ok ? keys[j] : 0u;
+        for (int p = 0; p < tpasses; ++p) {
+            const uint32_t d = ok ? ((g >> (p * tbits)) & dmask) : 0xffffffffu;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            if (ok && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&sh[p * MAX_BINS + d], __popc(peers));
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < tpasses * MAX_BINS; q += blockDim.x)
+        if (sh[q]) atomicAdd(&hist[q], sh[q]);
+}
+
+// ---------------------------------------------------------------------------
+// K6: ranges[gt] = [first, last+1) in the sorted entries
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, const uint32_t* K, uint2* __restrict__ ranges) {
+    const uint32_t Kn = *K;
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < Kn; j += gridDim.x * blockDim.x) {
-        const uint64_t g = keys[j] >> 31;
-        if (j == 0 || (keys[j - 1] >> 31) != g) ranges[g].x = j;
-        if (j == Kn - 1 || (keys[j + 1] >> 31) != g) ranges[g].y = j + 1;
+        const uint32_t g = keys[j];
+        if (j == 0 || keys[j - 1] != g) ranges[g].x = j;
+        if (j == Kn - 1 || keys[j + 1] != g) ranges[g].y = j + 1;
     }
 }
 
@@ -322,23 +423,28 @@ static int num_sms() {
     return sms;
 }
 
-static int onesweep_blocks_per_sm() {
+template <int BITS>
+static int onesweep_grid() {
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_onesweep, SORT_THREADS, ONESWEEP_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_onesweep32<BITS>, SORT_THREADS, Onesweep<BITS>::SMEM);
         if (occ <= 0) occ = 1;
     }
-    return occ;
+    return occ * num_sms();
 }
 
 cudaError_t init_binning_attributes() {
-    return cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ONESWEEP_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_onesweep32<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Onesweep<8>::SMEM);
+    if (e) return e;
+    return cudaFuncSetAttribute(k_onesweep32<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Onesweep<9>::SMEM);
 }
 
-int key_passes(int64_t gtiles) {
-    int gbits = 1;
-    while ((1ll << gbits) < gtiles) ++gbits;
-    return (31 + gbits + 7) / 8;
+template <int BITS>
+static void onesweep(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout, const uint32_t* count,
+                     uint32_t cap, int shift, const uint32_t* hist_excl, uint32_t* lb, uint32_t* ticket, DevFlags* fl,
+                     cudaStream_t s) {
+    k_onesweep32<BITS><<<onesweep_grid<BITS>(), SORT_THREADS, Onesweep<BITS>::SMEM, s>>>(kin, vin, kout, vout, count, cap,
+                                                                                         shift, hist_excl, lb, ticket, fl);
 }
 
 cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
@@ -346,57 +452,80 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     const int gx = (W + 15) / 16, gy = (H + 15) / 16;
     const int64_t T = (int64_t)gx * gy;
     const int64_t count = (int64_t)n_views * proj.n_pad;
-    const int64_t cap = bins.keys_cap;
-    const int passes = key_passes(T * n_views);
+    const uint32_t cap = (uint32_t)bins.keys_cap;
+    const int gbits = tile_gbits(T * n_views);
+    const int tbits = tile_digit_bits(gbits);
+    const int tpasses = tile_passes(gbits);
     unsigned char* ws = static_cast<unsigned char*>(scratch);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);
-    uint32_t* hist_excl = hist + MAX_PASSES * 256;
-    unsigned long long* scan_lb = reinterpret_cast<unsigned long long*>(ws + L.scan_lb);
-    uint32_t* sort_lb = reinterpret_cast<uint32_t*>(ws + L.sort_lb);
-    const int64_t sort_tiles = (cap + SORT_TILE - 1) / SORT_TILE;
-    const int64_t scan_tiles = (count + SCAN_TILE - 1) / SCAN_TILE;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);  // [depth 4 | tile 4][MAX_BINS] counts, then excl
+    uint32_t* hist_excl = hist + (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS;
+    unsigned long long* vis_lb = reinterpret_cast<unsigned long long*>(ws + L.vis_lb);
+    unsigned long long* dup_lb = reinterpret_cast<unsigned long long*>(ws + L.dup_lb);
+    uint32_t* depth_lb = reinterpret_cast<uint32_t*>(ws + L.depth_lb);
+    uint32_t* tile_lb = reinterpret_cast<uint32_t*>(ws + L.tile_lb);
+    uint32_t* dk[2] = {reinterpret_cast<uint32_t*>(ws + L.dkeys), reinterpret_cast<uint32_t*>(ws + L.dkeys_alt)};
+    uint32_t* dv[2] = {reinterpret_cast<uint32_t*>(ws + L.dvals), reinterpret_cast<uint32_t*>(ws + L.dvals_alt)};
+    const int64_t elem_tiles = (count + SORT_TILE - 1) / SORT_TILE;
+    const int64_t key_tiles = ((int64_t)cap + SORT_TILE - 1) / SORT_TILE;
+    uint32_t* Kd = bins.K;      // [0] = K entries
+    uint32_t* Md = bins.K + 1;  // [1] = M visible pairs
     cudaError_t e;
-    // reset tickets, histograms, look-back state, ranges
-    prof->begin(ST_SCAN, s);
+    prof->begin(ST_COMPACT, s);
     if ((e = cudaMemsetAsync(fl->tickets, 0, sizeof(fl->tickets), s))) return e;
-    if ((e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * MAX_PASSES * 256, s))) return e;
-    if ((e = cudaMemsetAsync(scan_lb, 0, sizeof(unsigned long long) * (scan_tiles + 1), s))) return e;
-    if ((e = cudaMemsetAsync(sort_lb, 0, sizeof(uint32_t) * 256 * (size_t)(sort_tiles + 1) * passes, s))) return e;
+    if ((e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS, s))) return e;
+    if ((e = cudaMemsetAsync(vis_lb, 0, sizeof(unsigned long long) * (elem_tiles + 1), s))) return e;
+    if ((e = cudaMemsetAsync(dup_lb, 0, sizeof(unsigned long long) * (elem_tiles + 1), s))) return e;
+    if ((e = cudaMemsetAsync(depth_lb, 0, sizeof(uint32_t) * DEPTH_PASSES * 256 * (size_t)(elem_tiles + 1), s))) return e;
+    if ((e = cudaMemsetAsync(tile_lb, 0, sizeof(uint32_t) * (size_t)tpasses * (1 << tbits) * (size_t)(key_tiles + 1), s)))
+        return e;
     if ((e = cudaMemsetAsync(bins.ranges, 0, sizeof(uint32_t) * 2 * (size_t)T * n_views, s))) return e;
-    if ((e = cudaMemsetAsync(bins.K, 0, sizeof(uint32_t), s))) return e;
-    if (scan_tiles > 0)
-        k_scan_tiles<<<(unsigned)scan_tiles, SCAN_THREADS, 0, s>>>(proj.tiles, bins.offsets, count, scan_lb, fl, bins.K, cap);
+    if ((e = cudaMemsetAsync(bins.K, 0, sizeof(uint32_t) * 2, s))) return e;
+    if (elem_tiles > 0)
+        k_vis_compact<<<(unsigned)elem_tiles, SORT_THREADS, 0, s>>>(proj.tiles, proj.depth, count, dk[0], dv[0], vis_lb,
+                                                                     fl, Md);
     prof->end(s);
-    prof->begin(ST_DUPLICATE, s);
-    {
-        const int64_t blocks = (count + 255) / 256;
-        if (blocks > 0)
-            k_duplicate<<<(unsigned)blocks, 256, 0, s>>>(proj.tiles, bins.offsets, reinterpret_cast<const short4*>(proj.rect),
-                                                         proj.depth, count, proj.n_pad, gx, T, bins.keys, bins.vals, cap);
-    }
-    prof->end(s);
+    // depth digits (LSD: least significant first) on the visible pairs
+    prof->begin(ST_DEPTH_SORT, s);
     const int sms = num_sms();
-    prof->begin(ST_HIST, s);
-    k_hist<<<sms * 4, 256, 0, s>>>(bins.keys, bins.K, cap, passes, hist);
-    k_hist_scan<<<1, 32 * MAX_PASSES, 0, s>>>(hist, hist_excl, passes);
-    prof->end(s, 2);
-    uint64_t* ka = bins.keys;
-    uint64_t* kb = bins.keys_alt;
+    k_hist_depth<<<sms * 2, 256, 0, s>>>(dk[0], Md, hist);
+    k_hist_scan<<<1, 32 * DEPTH_PASSES, 0, s>>>(hist, hist_excl, DEPTH_PASSES, 256);
+    int cur = 0;
+    for (int p = 0; p < DEPTH_PASSES; ++p) {
+        onesweep<8>(dk[cur], dv[cur], dk[cur ^ 1], dv[cur ^ 1], Md, (uint32_t)count, 8 * p, hist_excl + p * MAX_BINS,
+                    depth_lb + (size_t)p * 256 * (elem_tiles + 1), &fl->tickets[TK_DEPTH + p], fl, s);
+        cur ^= 1;
+    }
+    prof->end(s, DEPTH_PASSES + 2);
+    // offsets in depth order + duplication (+ tile-digit histograms)
+    prof->begin(ST_DUPLICATE, s);
+    uint32_t* thist = hist + DEPTH_PASSES * MAX_BINS;
+    uint32_t* thist_excl = hist_excl + DEPTH_PASSES * MAX_BINS;
+    if (elem_tiles > 0)
+        k_scan_dup<<<(unsigned)elem_tiles, SORT_THREADS, 0, s>>>(dv[cur], Md, proj.tiles,
+                                                                  reinterpret_cast<const short4*>(proj.rect), proj.n_pad,
+                                                                  gx, (uint32_t)T, bins.keys, bins.vals, cap, dup_lb, fl, Kd);
+    prof->end(s);
+    // tile digits on the K entries
+    prof->begin(ST_TILE_SORT, s);
+    k_hist_tile<<<sms * 4, 256, 0, s>>>(bins.keys, Kd, thist, tpasses, tbits);
+    k_hist_scan<<<1, 32 * MAX_TILE_PASSES, 0, s>>>(thist, thist_excl, tpasses, 1 << tbits);
+    uint32_t* ka = bins.keys;
+    uint32_t* kb = bins.keys_alt;
     uint32_t* va = bins.vals;
     uint32_t* vb = bins.vals_alt;
-    const int grid = sms * onesweep_blocks_per_sm();
-    prof->begin(ST_SORT, s);
-    for (int p = 0; p < passes; ++p) {
-        k_onesweep<<<grid, SORT_THREADS, ONESWEEP_SMEM, s>>>(ka, va, kb, vb, bins.K, cap, 8 * p, hist_excl + p * 256,
-                                                             sort_lb + (size_t)p * 256 * (sort_tiles + 1), &fl->tickets[p],
-                                                             fl);
-        uint64_t* tk = ka; ka = kb; kb = tk;
+    for (int p = 0; p < tpasses; ++p) {
+        uint32_t* lbp = tile_lb + (size_t)p * (1 << tbits) * (key_tiles + 1);
+        if (tbits == 9)
+            onesweep<9>(ka, va, kb, vb, Kd, cap, 9 * p, thist_excl + p * MAX_BINS, lbp, &fl->tickets[TK_TILE + p], fl, s);
+        else
+            onesweep<8>(ka, va, kb, vb, Kd, cap, 8 * p, thist_excl + p * MAX_BINS, lbp, &fl->tickets[TK_TILE + p], fl, s);
+        uint32_t* tk = ka; ka = kb; kb = tk;
         uint32_t* tv = va; va = vb; vb = tv;
     }
-    prof->end(s, passes);
-    bins.sorted_in_alt = (passes & 1) ? 1 : 0;
+    prof->end(s, tpasses + 2);
+    bins.sorted_in_alt = (tpasses & 1) ? 1 : 0;
     prof->begin(ST_RANGES, s);
-    k_ranges<<<sms * 8, 256, 0, s>>>(ka, bins.K, cap, reinterpret_cast<uint2*>(bins.ranges));
+    k_ranges<<<sms * 8, 256, 0, s>>>(ka, Kd, reinterpret_cast<uint2*>(bins.ranges));
     prof->end(s);
     return cudaGetLastError();
 }

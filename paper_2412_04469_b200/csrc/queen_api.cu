@@ -146,9 +146,9 @@ queen_status queen_decode_residuals(queen_ctx* ctx, const queen_packet* pkt, flo
     if (coo_out) {
         if (pkt->pos_kind == QUEEN_POS_GATES) {
             // scratch for block counts: the sort look-back region (not in use concurrently)
-            void* scratch = static_cast<unsigned char*>(ctx->ws) + ctx->L.sort_lb;
+            void* scratch = static_cast<unsigned char*>(ctx->ws) + ctx->L.tile_lb;
             size_t need = sizeof(uint32_t) * ((pkt->n + 1023) / 1024 + 1);
-            if (need > ctx->L.total_scratch - ctx->L.sort_lb) return fail(ctx, QUEEN_ERR_SHAPE, "workspace too small for gate compaction");
+            if (need > ctx->L.total_scratch - ctx->L.tile_lb) return fail(ctx, QUEEN_ERR_SHAPE, "workspace too small for gate compaction");
             e = launch_gate_compact(*pkt, coo_idx_out, coo_val_out, k_out, scratch, fl, s);
         } else if (pkt->pos_kind == QUEEN_POS_COO) {
             e = launch_coo_copy(*pkt, coo_idx_out, coo_val_out, k_out, fl, s);
@@ -221,17 +221,16 @@ queen_status queen_project(queen_ctx* ctx, const queen_gaussians* scene, const q
 queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_camera* cams, int32_t n_views,
                             queen_bins* bins, void* stream) {
     if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
-    if (!proj || !bins || !bins->keys || !bins->keys_alt || !bins->vals || !bins->vals_alt || !bins->offsets ||
-        !bins->ranges || !bins->K)
+    if (!proj || !bins || !bins->keys || !bins->keys_alt || !bins->vals || !bins->vals_alt || !bins->ranges || !bins->K)
         return fail(ctx, QUEEN_ERR_INVALID_ARG, "null proj/bins");
     if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
     const int W = cams[0].width, H = cams[0].height;
     const int64_t T = (int64_t)((W + 15) / 16) * ((H + 15) / 16);
     if (bins->keys_cap < 1 || bins->keys_cap > MAX_KEYS) return fail(ctx, QUEEN_ERR_SHAPE, "keys_cap outside [1, 2^30)");
-    if (T * n_views >= (1ll << 33)) return fail(ctx, QUEEN_ERR_SHAPE, "too many tiles");
+    if (T * n_views >= (1ll << 31)) return fail(ctx, QUEEN_ERR_SHAPE, "too many tiles in one batch");
     // scratch must cover this batch
     WsLayout need = ws_layout(proj->n_pad, n_views, W, H, bins->keys_cap);
-    if (need.total_scratch > ctx->L.total_scratch || need.sort_tiles > ctx->L.sort_tiles || need.scan_tiles > ctx->L.scan_tiles)
+    if (need.key_tiles > ctx->L.key_tiles || need.elem_tiles > ctx->L.elem_tiles || need.elems > ctx->L.elems)
         return fail(ctx, QUEEN_ERR_SHAPE, "workspace scratch too small for this batch");
     cudaError_t e = launch_bin_sort(*proj, n_views, W, H, *bins, ctx->ws, ctx->L, flags_of(ctx),
                                     static_cast<cudaStream_t>(stream), &ctx->prof);
@@ -314,11 +313,10 @@ queen_status queen_render_views(queen_ctx* ctx, const queen_gaussians* scene, co
     pj.rect = reinterpret_cast<int16_t*>(ws + L.rect);
     queen_bins b;
     b.keys_cap = ctx->ws_keys;
-    b.keys = reinterpret_cast<uint64_t*>(ws + L.keys);
-    b.keys_alt = reinterpret_cast<uint64_t*>(ws + L.keys_alt);
+    b.keys = reinterpret_cast<uint32_t*>(ws + L.keys);
+    b.keys_alt = reinterpret_cast<uint32_t*>(ws + L.keys_alt);
     b.vals = reinterpret_cast<uint32_t*>(ws + L.vals);
     b.vals_alt = reinterpret_cast<uint32_t*>(ws + L.vals_alt);
-    b.offsets = reinterpret_cast<uint32_t*>(ws + L.offsets);
     b.ranges = reinterpret_cast<uint32_t*>(ws + L.ranges);
     b.K = reinterpret_cast<uint32_t*>(ws + L.K);
     b.sorted_in_alt = 0;

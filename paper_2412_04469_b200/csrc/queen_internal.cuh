@@ -46,11 +46,33 @@ struct CamBatch {
     queen_camera cam[QUEEN_MAX_VIEWS];
 };
 
+// Binning plan: an LSD radix sort on (tile, depth) whose depth
+// digits run BEFORE duplication, on the visible (view, Gaussian) pairs, and whose
+// tile digits run after it on the duplicated entries:
+//   depth passes : 4 x 8 bits over the 31 depth bits of the M visible pairs
+//   tile passes  : ceil(gbits / TILE_DIGIT_BITS) x (8 or 9) bits over the K entries
+constexpr int DEPTH_PASSES = 4;
+constexpr int MAX_TILE_PASSES = 4;
+constexpr int MAX_BINS = 512;
+
+inline int tile_gbits(int64_t gtiles) {
+    int g = 1;
+    while ((1ll << g) < gtiles) ++g;
+    return g;
+}
+inline int tile_digit_bits(int gbits) { return gbits <= 16 ? 8 : (gbits <= 18 ? 9 : 8); }
+inline int tile_passes(int gbits) {
+    const int db = tile_digit_bits(gbits);
+    return (gbits + db - 1) / db;
+}
+
 // Workspace carve-up (bytes, 256-aligned) for (n_pad, n_views, W, H, keys_cap).
 struct WsLayout {
-    size_t flags, hist, scan_lb, sort_lb, total_scratch;
-    size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, offsets, ranges, K, total;
-    int64_t sort_tiles, scan_tiles, T;
+    // scratch (bin_sort)
+    size_t flags, hist, vis_lb, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, total_scratch;
+    // render_views buffers
+    size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, total;
+    int64_t key_tiles, elem_tiles, T, elems;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -59,24 +81,29 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     WsLayout L{};
     int64_t gx = (W + 15) / 16, gy = (H + 15) / 16;
     L.T = gx * gy;
-    int64_t elems = (int64_t)n_pad * n_views;
-    L.sort_tiles = (keys_cap + SORT_TILE - 1) / SORT_TILE;
-    L.scan_tiles = (elems + SCAN_TILE - 1) / SCAN_TILE;
+    L.elems = (int64_t)n_pad * n_views;
+    L.key_tiles = (keys_cap + SORT_TILE - 1) / SORT_TILE;
+    L.elem_tiles = (L.elems + SORT_TILE - 1) / SORT_TILE;
     size_t o = 0;
     L.flags = o; o += align256(sizeof(DevFlags));
-    L.hist = o; o += align256(sizeof(uint32_t) * MAX_PASSES * 256 * 2);
-    L.scan_lb = o; o += align256(sizeof(unsigned long long) * (L.scan_tiles + 1));
-    L.sort_lb = o; o += align256(sizeof(uint32_t) * MAX_PASSES * 256 * (L.sort_tiles + 1));
+    L.hist = o; o += align256(sizeof(uint32_t) * (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS * 2);
+    L.vis_lb = o; o += align256(sizeof(unsigned long long) * (L.elem_tiles + 1));
+    L.dup_lb = o; o += align256(sizeof(unsigned long long) * (L.elem_tiles + 1));
+    L.depth_lb = o; o += align256(sizeof(uint32_t) * DEPTH_PASSES * 256 * (L.elem_tiles + 1));
+    L.tile_lb = o; o += align256(sizeof(uint32_t) * MAX_TILE_PASSES * MAX_BINS * (L.key_tiles + 1));
+    L.dkeys = o; o += align256(sizeof(uint32_t) * L.elems);
+    L.dkeys_alt = o; o += align256(sizeof(uint32_t) * L.elems);
+    L.dvals = o; o += align256(sizeof(uint32_t) * L.elems);
+    L.dvals_alt = o; o += align256(sizeof(uint32_t) * L.elems);
     L.total_scratch = o;
-    L.rec = o; o += align256(sizeof(float) * REC_WORDS * elems);
-    L.depth = o; o += align256(sizeof(uint32_t) * elems);
-    L.tiles = o; o += align256(sizeof(uint32_t) * elems);
-    L.rect = o; o += align256(sizeof(int16_t) * 4 * elems);
-    L.keys = o; o += align256(sizeof(uint64_t) * keys_cap);
-    L.keys_alt = o; o += align256(sizeof(uint64_t) * keys_cap);
+    L.rec = o; o += align256(sizeof(float) * REC_WORDS * L.elems);
+    L.depth = o; o += align256(sizeof(uint32_t) * L.elems);
+    L.tiles = o; o += align256(sizeof(uint32_t) * L.elems);
+    L.rect = o; o += align256(sizeof(int16_t) * 4 * L.elems);
+    L.keys = o; o += align256(sizeof(uint32_t) * keys_cap);
+    L.keys_alt = o; o += align256(sizeof(uint32_t) * keys_cap);
     L.vals = o; o += align256(sizeof(uint32_t) * keys_cap);
     L.vals_alt = o; o += align256(sizeof(uint32_t) * keys_cap);
-    L.offsets = o; o += align256(sizeof(uint32_t) * elems);
     L.ranges = o; o += align256(sizeof(uint32_t) * 2 * L.T * n_views);
     L.K = o; o += align256(sizeof(uint32_t) * 4);
     L.total = o;
@@ -132,7 +159,7 @@ __device__ __forceinline__ void raise_flag(DevFlags* fl, uint32_t bit) { atomicO
 
 // Stage profiler: CUDA events recorded on the launching stream at stage boundaries
 // (enabled by queen_profile_enable; used by bench.py for per-kernel durations).
-enum Stage { ST_APPLY = 0, ST_PROJECT, ST_SCAN, ST_DUPLICATE, ST_HIST, ST_SORT, ST_RANGES, ST_BLEND, ST_COUNT };
+enum Stage { ST_APPLY = 0, ST_PROJECT, ST_COMPACT, ST_DEPTH_SORT, ST_DUPLICATE, ST_TILE_SORT, ST_RANGES, ST_BLEND, ST_COUNT };
 struct Prof {
     bool on = false;
     std::vector<cudaEvent_t> pool;

@@ -37,17 +37,16 @@ class Stages:
         self.depth = torch.zeros((V, self.n_pad), dtype=torch.int32, device=d)
         self.tiles = torch.zeros((V, self.n_pad), dtype=torch.int32, device=d)
         self.rect = torch.zeros((V, self.n_pad, 4), dtype=torch.int16, device=d)
-        self.keys = torch.zeros(self.keys_cap, dtype=torch.int64, device=d)
+        self.keys = torch.zeros(self.keys_cap, dtype=torch.int32, device=d)
         self.keys_alt = torch.zeros_like(self.keys)
         self.vals = torch.zeros(self.keys_cap, dtype=torch.int32, device=d)
         self.vals_alt = torch.zeros_like(self.vals)
-        self.offsets = torch.zeros((V, self.n_pad), dtype=torch.int32, device=d)
         self.ranges = torch.zeros((V * self.T, 2), dtype=torch.int32, device=d)
         self.K = torch.zeros(4, dtype=torch.int32, device=d)
         self.rgb = torch.zeros((V, 3, self.H, self.W), dtype=torch.float32, device=d)
         self.Tout = torch.zeros((V, self.H, self.W), dtype=torch.float32, device=d)
         self.proj = proj_struct(self.rec, self.depth, self.tiles, self.rect)
-        self.bins = bins_struct(self.keys, self.keys_alt, self.vals, self.vals_alt, self.offsets, self.ranges, self.K)
+        self.bins = bins_struct(self.keys, self.keys_alt, self.vals, self.vals_alt, self.ranges, self.K)
         self.scene = gaussians_struct(self.planes_t, n, deg)
 
     def project(self):
@@ -76,7 +75,7 @@ class Stages:
         alt = self.bins.sorted_in_alt
         ks = self.keys_alt if alt else self.keys
         vs = self.vals_alt if alt else self.vals
-        return dict(K=K, offsets=to_np(self.offsets).view(np.uint32), keys=to_np(ks[:K]).view(np.uint64),
+        return dict(K=K, M=int(to_np(self.K)[1]), keys=to_np(ks[:K]).view(np.uint32),
                     vals=to_np(vs[:K]).view(np.uint32), ranges=to_np(self.ranges).view(np.uint32))
 
     def image_np(self):

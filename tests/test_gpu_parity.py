@@ -2,7 +2,7 @@
 
 Bars (BASELINE north_star):
   bit-exact  : quantised latents, gate mask / COO indices, projection records except
-               rgb (u, v, A2, B2, C2, T2, o, depth, tiles, rect), offsets, K, keys,
+               rgb (u, v, A2, B2, C2, T2, o, depth, tiles, rect), K, sorted keys,
                vals, ranges
   tolerance  : decoded attributes |d| <= 1e-5 max(|ref|, 1e-6) (bit-exact expected);
                per-Gaussian rgb 1e-5 relative; image RGB max-abs <= 2e-3 on [0,1],
@@ -149,12 +149,17 @@ def _check_proj(got, ref, n):
     assert np.all(np.abs(g[..., 8:] - r[..., 8:]) <= 1e-5 * np.maximum(np.abs(r[..., 8:]), 1e-6) + 1e-7)
 
 
-def _check_bins(got, ref):
+def _check_bins(got, ref, depth=None, T=None):
+    """Sorted entries bit-exact: gt, Gaussian index, ranges, K; and the full composite key
+    (gt << 31 | depth bits) rebuilt from the entry equals the oracle's sorted key."""
     assert got["K"] == ref["K"]
-    assert np.array_equal(got["offsets"], ref["offsets"])
-    assert np.array_equal(got["keys"], ref["keys"])
+    assert np.array_equal(got["keys"].astype(np.uint64), ref["keys"] >> np.uint64(31))
     assert np.array_equal(got["vals"], ref["vals"])
     assert np.array_equal(got["ranges"], ref["ranges"])
+    if depth is not None:
+        v = got["keys"].astype(np.int64) // T
+        full = (got["keys"].astype(np.uint64) << np.uint64(31)) | depth[v, got["vals"]].astype(np.uint64)
+        assert np.array_equal(full, ref["keys"])
 
 
 def _check_image(rgb, T, rref, Tref):
@@ -178,8 +183,11 @@ def test_render_stages_parity(case):
     W, H = cams[0].width, cams[0].height
     proj, bins, rgb, T = oracle.render(sc.planes, sc.n, sc.deg, cams)
     st = Stages(sc.planes, sc.n, sc.deg, cams).run()
-    _check_proj(st.proj_np(), proj, sc.n)
-    _check_bins(st.bins_np(), bins)
+    gp = st.proj_np()
+    _check_proj(gp, proj, sc.n)
+    gb = st.bins_np()
+    _check_bins(gb, bins, gp["depth"], st.T)
+    assert gb["M"] == int(np.count_nonzero(proj["tiles"]))
     g_rgb, g_T = st.image_np()
     _check_image(g_rgb, g_T, rgb, T)
     s, _ = st.ctx.check_status()
@@ -197,8 +205,9 @@ def test_render_big_gaussians_ragged():
     cams = [synth.make_camera(np.eye(3), np.zeros(3), 40.0, 40.0, 70, 45)]
     proj, bins, rgb, T = oracle.render(pl, n, 3, cams, bg=(0.1, 0.2, 0.3))
     st = Stages(pl, n, 3, cams).run(bg=(0.1, 0.2, 0.3))
-    _check_proj(st.proj_np(), proj, n)
-    _check_bins(st.bins_np(), bins)
+    gp = st.proj_np()
+    _check_proj(gp, proj, n)
+    _check_bins(st.bins_np(), bins, gp["depth"], st.T)
     _check_image(*st.image_np(), rgb, T)
 
 
@@ -305,8 +314,9 @@ def test_full_size_frame_sampled(name):
         if b0 == 0:
             from tests.gpu_helpers import Stages
             stg = Stages(A1, sc.n, sc.deg, bc, keys_cap=pl.keys_cap).project().bin_sort()
-            _check_proj(stg.proj_np(), proj, sc.n)
-            _check_bins(stg.bins_np(), bins)
+            gp = stg.proj_np()
+            _check_proj(gp, proj, sc.n)
+            _check_bins(stg.bins_np(), bins, gp["depth"], stg.T)
             del stg
         else:
             bins = oracle.bin_sort(proj, W, H)
