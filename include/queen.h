@@ -127,7 +127,9 @@ typedef struct {
  *   keys/vals (+ _alt ping-pong) [keys_cap] u32: key = gt of the entry, val = Gaussian
  *            index (the entry's full sort key is (gt << 31) | proj.depth[view][val])
  *   ranges[n_views*T][2] u32  [first, last+1) of gt in the sorted entries, [0,0) if empty
- *   K (device u32[2])         [0] = entries K of the batch, [1] = visible (view, Gaussian) pairs
+ *   K (device u32[4])         [0] = entries K of the batch (0 if K > keys_cap: QUEEN_ERR_CAPACITY,
+ *                             no entries, all ranges [0,0)), [1] = visible (view, Gaussian) pairs,
+ *                             [2] = 1 on capacity overflow
  *   sorted_in_alt             OUT (host): 1 if the sorted result is in keys_alt/vals_alt */
 typedef struct {
     int64_t keys_cap;

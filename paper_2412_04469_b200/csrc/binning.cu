@@ -296,21 +296,30 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep32(const uint32_t* __r
 
 // ---------------------------------------------------------------------------
 // K3b + K4: offsets of the depth-sorted pairs (decoupled look-back) + duplication.
-// Entry = (gt, Gaussian index).  The block's 4096 pairs and their block-local offsets
-// are staged in shared memory; threads then stride over the block's OUTPUT entries
-// (load-balanced: an entry finds its pair by binary search over the offsets), so the
-// key/value stores are coalesced whatever the per-Gaussian tile counts are.
+// Entry = (gt, Gaussian index), emitted for each pair ty-major, tx-minor.
+// Phase 1 stages the block's 4096 pairs in shared memory (block-local offset, gt of the
+// rect's first tile, Gaussian index, rect width) and adds the pair's tile rect to the
+// per-view 2D difference array of tile counts (4 corner increments; k_tile_counts turns
+// it into per-tile entry counts, i.e. the final ranges and the digit histograms).
+// Phase 2: each warp emits a contiguous run of the block's entries, 32 at a time; every
+// pair has >= 1 entry, so the pairs starting inside a 32-entry chunk are the next <= 31
+// pairs: one shared load + redux.or + popc locates each lane's pair.  Stores coalesce.
 // ---------------------------------------------------------------------------
+constexpr size_t DUP_SMEM = (size_t)SORT_TILE * (4 + 4 + 4 + 2) + 16;
+
 __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __restrict__ dvals, const uint32_t* count_ptr,
-                                                           const uint32_t* __restrict__ tiles,
-                                                           const short4* __restrict__ rect, int n_pad, int gx,
+                                                           const short4* __restrict__ rect, int n_pad, int gx, int gy,
                                                            uint32_t T, uint32_t* __restrict__ keys,
                                                            uint32_t* __restrict__ vals, uint32_t cap,
-                                                           unsigned long long* lb, DevFlags* fl, uint32_t* K_out) {
+                                                           unsigned long long* lb, DevFlags* fl, uint32_t* K_out,
+                                                           int* __restrict__ diff) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint32_t* s_off = reinterpret_cast<uint32_t*>(dsm);       // [SORT_TILE + 1]
+    uint32_t* s_base = s_off + SORT_TILE + 4;                // [SORT_TILE]
+    uint32_t* s_i = s_base + SORT_TILE;                      // [SORT_TILE]
+    uint16_t* s_wx = reinterpret_cast<uint16_t*>(s_i + SORT_TILE);
     __shared__ uint32_t s_tile, s_w[SORT_WARPS];
     __shared__ unsigned long long s_prefix;
-    __shared__ uint32_t s_off[SORT_TILE];
-    __shared__ uint32_t s_j[SORT_TILE];
     const uint32_t M = *count_ptr;
     const uint32_t ntiles = (M + SORT_TILE - 1) / SORT_TILE;
     if (threadIdx.x == 0) s_tile = atomicAdd(&fl->tickets[TK_DUP], 1u);
@@ -318,13 +327,29 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
     const uint32_t tile = s_tile;
     if (tile >= ntiles) return;
     const uint32_t base = tile * SORT_TILE + threadIdx.x * SORT_ITEMS;
-    uint32_t jj[SORT_ITEMS], nt[SORT_ITEMS];
+    const int dw = gx + 1, dplane = (gx + 1) * (gy + 1);
+    uint32_t nt[SORT_ITEMS];
     uint32_t tsum = 0;
 #pragma unroll
     for (int e = 0; e < SORT_ITEMS; ++e) {
         const uint32_t m = base + e;
-        jj[e] = m < M ? __ldg(dvals + m) : 0u;
-        nt[e] = m < M ? __ldg(tiles + jj[e]) : 0u;
+        const int q = threadIdx.x * SORT_ITEMS + e;
+        nt[e] = 0;
+        if (m < M) {
+            const uint32_t j = __ldg(dvals + m);
+            const short4 r = __ldg(rect + j);
+            const uint32_t v = j / (uint32_t)n_pad;
+            const uint32_t wx = (uint32_t)(r.z - r.x + 1), wy = (uint32_t)(r.w - r.y + 1);
+            nt[e] = wx * wy;
+            s_base[q] = v * T + (uint32_t)r.y * (uint32_t)gx + (uint32_t)r.x;
+            s_i[q] = j - v * (uint32_t)n_pad;
+            s_wx[q] = (uint16_t)wx;
+            int* d = diff + (int64_t)v * dplane;
+            atomicAdd(d + r.y * dw + r.x, 1);
+            atomicAdd(d + r.y * dw + r.z + 1, -1);
+            atomicAdd(d + (r.w + 1) * dw + r.x, -1);
+            atomicAdd(d + (r.w + 1) * dw + r.z + 1, 1);
+        }
         tsum += nt[e];
     }
     uint32_t total;
@@ -337,78 +362,139 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
                 raise_flag(fl, FLAG_CAPACITY);
                 atomicMax(&fl->info, K);
             }
-            K_out[0] = (uint32_t)(K > cap ? cap : K);
+            // overflow: no entry list is produced (the tile sort sees 0 entries and every range is
+            // [0,0)); QUEEN_ERR_CAPACITY carries the K needed.  K_out[2] = overflow flag.
+            K_out[0] = K > cap ? 0u : (uint32_t)K;
+            K_out[2] = K > cap ? 1u : 0u;
         }
+        s_off[SORT_TILE] = total;
     }
     {
         uint32_t run = excl;
 #pragma unroll
         for (int e = 0; e < SORT_ITEMS; ++e) {
             s_off[threadIdx.x * SORT_ITEMS + e] = run;
-            s_j[threadIdx.x * SORT_ITEMS + e] = jj[e];
             run += nt[e];
         }
     }
     __syncthreads();
     const unsigned long long gbase = s_prefix;
-    for (uint32_t p = threadIdx.x; p < total; p += SORT_THREADS) {
-        // last pair whose block-local offset <= p (it owns entry p: pairs with 0 tiles share
-        // their successor's offset and come before it)
-        int lo = 0, hi = SORT_TILE;  // invariant: s_off[lo] <= p < s_off[hi] (s_off[SORT_TILE] := total)
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t nchunks = (total + 31) / 32;
+    const uint32_t c0 = (uint32_t)(((uint64_t)nchunks * w) / SORT_WARPS);
+    const uint32_t c1 = (uint32_t)(((uint64_t)nchunks * (w + 1)) / SORT_WARPS);
+    if (c0 >= c1) return;
+    // pair owning entry 32*c0 (binary search once; all lanes agree)
+    int lo = 0;
+    {
+        const uint32_t p = 32 * c0;
+        int hi = SORT_TILE;
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
             if (s_off[mid] <= p) lo = mid; else hi = mid;
         }
-        const uint32_t c = p - s_off[lo];
-        const uint32_t j = s_j[lo];
-        const short4 r = __ldg(rect + j);
-        const uint32_t wx = (uint32_t)(r.z - r.x + 1);
-        const uint32_t row = c / wx;
-        const uint32_t v = j / (uint32_t)n_pad;
-        const uint64_t w = gbase + p;
-        if (w < cap) {
-            keys[w] = v * T + (uint32_t)(r.y + (int)row) * (uint32_t)gx + (uint32_t)(r.x + (int)(c - row * wx));
-            vals[w] = j - v * (uint32_t)n_pad;
+    }
+    const uint32_t le_mask = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+    for (uint32_t c = c0; c < c1; ++c) {
+        const uint32_t p0 = 32 * c;
+        const int cand = lo + (int)lane;
+        const uint32_t o = cand <= SORT_TILE ? s_off[cand] : 0xffffffffu;
+        const uint32_t sdel = o - p0;  // start of pair lo+lane relative to p0 (lanes >= 1 start after p0)
+        const uint32_t bit = (lane > 0 && o > p0 && sdel < 32u) ? (1u << sdel) : 0u;
+        const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
+        const int e = lo + __popc(starts & le_mask);
+        const uint32_t p = p0 + lane;
+        if (p < total) {
+            const uint32_t cc = p - s_off[e];
+            const uint32_t wx = s_wx[e];
+            const uint32_t row = cc / wx;
+            const uint64_t dst = gbase + p;
+            if (dst < cap) {
+                keys[dst] = s_base[e] + row * (uint32_t)gx + (cc - row * wx);
+                vals[dst] = s_i[e];
+            }
         }
+        const int e31 = __shfl_sync(0xffffffffu, e, 31);
+        lo = e31 + ((e31 + 1 <= SORT_TILE && s_off[e31 + 1] == p0 + 32) ? 1 : 0);
     }
 }
 
-// K5b: histograms of the tile digits of the K entries (warp-aggregated smem atomics:
-// consecutive entries share their high digits, so peers are merged with match_any)
-__global__ void __launch_bounds__(256) k_hist_tile(const uint32_t* __restrict__ keys, const uint32_t* count_ptr,
-                                                   uint32_t* hist, int tpasses, int tbits) {
+// Per-view 2D prefix sums of the tile-count difference arrays -> entries per global tile,
+// the tile-digit histograms of the coming tile sort, and per-view totals.
+__global__ void __launch_bounds__(1024) k_tile_counts(const int* __restrict__ diff, int gx, int gy, uint32_t* counts,
+                                                      uint32_t* view_tot, uint32_t* hist, int tpasses, int tbits) {
+    extern __shared__ int cs[];  // [(gy+1)][(gx+1)]
     __shared__ uint32_t sh[MAX_TILE_PASSES * MAX_BINS];
+    __shared__ uint32_t s_tot;
+    const int v = blockIdx.x;
+    const int dw = gx + 1, dplane = (gx + 1) * (gy + 1);
+    const int T = gx * gy;
+    for (int q = threadIdx.x; q < dplane; q += blockDim.x) cs[q] = diff[(int64_t)v * dplane + q];
     for (int q = threadIdx.x; q < tpasses * MAX_BINS; q += blockDim.x) sh[q] = 0;
+    if (threadIdx.x == 0) s_tot = 0;
     __syncthreads();
-    const uint32_t n = *count_ptr;
-    const uint32_t dmask = (1u << tbits) - 1u;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    // whole warps iterate together so match_any sees full warps
-    for (uint32_t j0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); j0 < n; j0 += stride) {
-        const uint32_t j = j0 + lane;
-        const bool ok = j < n;
-        const uint32_t g = ok ? keys[j] : 0u;
-        for (int p = 0; p < tpasses; ++p) {
-            const uint32_t d = ok ? ((g >> (p * tbits)) & dmask) : 0xffffffffu;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            if (ok && (peers & ((1u << lane) - 1u)) == 0) atomicAdd(&sh[p * MAX_BINS + d], __popc(peers));
-        }
+    for (int r = threadIdx.x; r < gy; r += blockDim.x) {  // prefix along x
+        int run = 0;
+        for (int x = 0; x < gx; ++x) { run += cs[r * dw + x]; cs[r * dw + x] = run; }
     }
+    __syncthreads();
+    for (int x = threadIdx.x; x < gx; x += blockDim.x) {  // prefix along y
+        int run = 0;
+        for (int r = 0; r < gy; ++r) { run += cs[r * dw + x]; cs[r * dw + x] = run; }
+    }
+    __syncthreads();
+    const uint32_t dmask = (1u << tbits) - 1u;
+    uint32_t tot = 0;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        const uint32_t c = (uint32_t)cs[(t / gx) * dw + (t % gx)];
+        const uint32_t g = (uint32_t)v * (uint32_t)T + (uint32_t)t;
+        counts[g] = c;
+        tot += c;
+        if (c)
+            for (int p = 0; p < tpasses; ++p) atomicAdd(&sh[p * MAX_BINS + ((g >> (p * tbits)) & dmask)], c);
+    }
+    atomicAdd(&s_tot, tot);
     __syncthreads();
     for (int q = threadIdx.x; q < tpasses * MAX_BINS; q += blockDim.x)
         if (sh[q]) atomicAdd(&hist[q], sh[q]);
+    if (threadIdx.x == 0) view_tot[v] = s_tot;
 }
 
-// ---------------------------------------------------------------------------
-// K6: ranges[gt] = [first, last+1) in the sorted entries
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, const uint32_t* K, uint2* __restrict__ ranges) {
-    const uint32_t Kn = *K;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < Kn; j += gridDim.x * blockDim.x) {
-        const uint32_t g = keys[j];
-        if (j == 0 || keys[j - 1] != g) ranges[g].x = j;
-        if (j == Kn - 1 || keys[j + 1] != g) ranges[g].y = j + 1;
+// ranges from the per-tile counts: exclusive scan over all global tiles (one block),
+// clamped to the key capacity (a capacity overflow is already flagged)
+__global__ void __launch_bounds__(1024) k_ranges_from_counts(const uint32_t* __restrict__ counts, int64_t G, uint32_t cap,
+                                                             const uint32_t* Kd, uint2* __restrict__ ranges) {
+    const bool overflow = Kd[2] != 0u;
+    __shared__ uint32_t s_w[32];
+    __shared__ unsigned long long s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t b = 0; b < G; b += 1024) {
+        const int64_t g = b + threadIdx.x;
+        const uint32_t c = g < G ? counts[g] : 0u;
+        uint32_t inc = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_w[w] = inc;
+        __syncthreads();
+        uint32_t pre = 0, tot = 0;
+        for (int q = 0; q < 32; ++q) {
+            const uint32_t sq = s_w[q];
+            pre += q < w ? sq : 0u;
+            tot += sq;
+        }
+        const unsigned long long st = s_carry + pre + inc - c;
+        if (g < G) {
+            const unsigned long long en = st + c;
+            ranges[g] = (c && !overflow) ? make_uint2((uint32_t)(st < cap ? st : cap), (uint32_t)(en < cap ? en : cap))
+                          : make_uint2(0u, 0u);  // empty tile: [0, 0)
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += tot;
+        __syncthreads();
     }
 }
 
@@ -436,7 +522,10 @@ static int onesweep_grid() {
 cudaError_t init_binning_attributes() {
     cudaError_t e = cudaFuncSetAttribute(k_onesweep32<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Onesweep<8>::SMEM);
     if (e) return e;
-    return cudaFuncSetAttribute(k_onesweep32<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Onesweep<9>::SMEM);
+    if ((e = cudaFuncSetAttribute(k_onesweep32<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Onesweep<9>::SMEM)))
+        return e;
+    if ((e = cudaFuncSetAttribute(k_scan_dup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DUP_SMEM))) return e;
+    return cudaFuncSetAttribute(k_tile_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
 template <int BITS>
@@ -478,8 +567,12 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     if ((e = cudaMemsetAsync(depth_lb, 0, sizeof(uint32_t) * DEPTH_PASSES * 256 * (size_t)(elem_tiles + 1), s))) return e;
     if ((e = cudaMemsetAsync(tile_lb, 0, sizeof(uint32_t) * (size_t)tpasses * (1 << tbits) * (size_t)(key_tiles + 1), s)))
         return e;
-    if ((e = cudaMemsetAsync(bins.ranges, 0, sizeof(uint32_t) * 2 * (size_t)T * n_views, s))) return e;
-    if ((e = cudaMemsetAsync(bins.K, 0, sizeof(uint32_t) * 2, s))) return e;
+    int* diff = reinterpret_cast<int*>(ws + L.diff);
+    uint32_t* tcounts = reinterpret_cast<uint32_t*>(ws + L.counts);
+    uint32_t* view_tot = reinterpret_cast<uint32_t*>(ws + L.view_tot);
+    const size_t dplane = (size_t)(gx + 1) * (gy + 1);
+    if ((e = cudaMemsetAsync(diff, 0, sizeof(int) * dplane * n_views, s))) return e;
+    if ((e = cudaMemsetAsync(bins.K, 0, sizeof(uint32_t) * 4, s))) return e;
     if (elem_tiles > 0)
         k_vis_compact<<<(unsigned)elem_tiles, SORT_THREADS, 0, s>>>(proj.tiles, proj.depth, count, dk[0], dv[0], vis_lb,
                                                                      fl, Md);
@@ -501,13 +594,18 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     uint32_t* thist = hist + DEPTH_PASSES * MAX_BINS;
     uint32_t* thist_excl = hist_excl + DEPTH_PASSES * MAX_BINS;
     if (elem_tiles > 0)
-        k_scan_dup<<<(unsigned)elem_tiles, SORT_THREADS, 0, s>>>(dv[cur], Md, proj.tiles,
-                                                                  reinterpret_cast<const short4*>(proj.rect), proj.n_pad,
-                                                                  gx, (uint32_t)T, bins.keys, bins.vals, cap, dup_lb, fl, Kd);
+        k_scan_dup<<<(unsigned)elem_tiles, SORT_THREADS, DUP_SMEM, s>>>(dv[cur], Md,
+                                                                         reinterpret_cast<const short4*>(proj.rect),
+                                                                         proj.n_pad, gx, gy, (uint32_t)T, bins.keys,
+                                                                         bins.vals, cap, dup_lb, fl, Kd, diff);
     prof->end(s);
+    // per-tile entry counts -> ranges and tile-digit histograms
+    prof->begin(ST_RANGES, s);
+    k_tile_counts<<<n_views, 1024, sizeof(int) * dplane, s>>>(diff, gx, gy, tcounts, view_tot, thist, tpasses, tbits);
+    k_ranges_from_counts<<<1, 1024, 0, s>>>(tcounts, T * n_views, cap, Kd, reinterpret_cast<uint2*>(bins.ranges));
+    prof->end(s, 2);
     // tile digits on the K entries
     prof->begin(ST_TILE_SORT, s);
-    k_hist_tile<<<sms * 4, 256, 0, s>>>(bins.keys, Kd, thist, tpasses, tbits);
     k_hist_scan<<<1, 32 * MAX_TILE_PASSES, 0, s>>>(thist, thist_excl, tpasses, 1 << tbits);
     uint32_t* ka = bins.keys;
     uint32_t* kb = bins.keys_alt;
@@ -522,11 +620,8 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
         uint32_t* tk = ka; ka = kb; kb = tk;
         uint32_t* tv = va; va = vb; vb = tv;
     }
-    prof->end(s, tpasses + 2);
+    prof->end(s, tpasses + 1);
     bins.sorted_in_alt = (tpasses & 1) ? 1 : 0;
-    prof->begin(ST_RANGES, s);
-    k_ranges<<<sms * 8, 256, 0, s>>>(ka, Kd, reinterpret_cast<uint2*>(bins.ranges));
-    prof->end(s);
     return cudaGetLastError();
 }
 

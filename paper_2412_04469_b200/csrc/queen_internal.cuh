@@ -69,7 +69,8 @@ inline int tile_passes(int gbits) {
 // Workspace carve-up (bytes, 256-aligned) for (n_pad, n_views, W, H, keys_cap).
 struct WsLayout {
     // scratch (bin_sort)
-    size_t flags, hist, vis_lb, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, total_scratch;
+    size_t flags, hist, vis_lb, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, diff, counts, view_tot,
+        total_scratch;
     // render_views buffers
     size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, total;
     int64_t key_tiles, elem_tiles, T, elems;
@@ -95,6 +96,9 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     L.dkeys_alt = o; o += align256(sizeof(uint32_t) * L.elems);
     L.dvals = o; o += align256(sizeof(uint32_t) * L.elems);
     L.dvals_alt = o; o += align256(sizeof(uint32_t) * L.elems);
+    L.diff = o; o += align256(sizeof(int32_t) * (size_t)n_views * (gx + 1) * (gy + 1));
+    L.counts = o; o += align256(sizeof(uint32_t) * (size_t)n_views * L.T);
+    L.view_tot = o; o += align256(sizeof(uint32_t) * (size_t)n_views);
     L.total_scratch = o;
     L.rec = o; o += align256(sizeof(float) * REC_WORDS * L.elems);
     L.depth = o; o += align256(sizeof(uint32_t) * L.elems);
