@@ -109,10 +109,11 @@ typedef struct {
 } queen_camera;
 
 /* Per-view projected records, each [n_views][n_pad]:
- *   rec   [..][12] fp32 = u, v, A2, B2 | C2, T2, o, 0 | r, g, b, 0
- *         (A2,B2,C2 base-2 conic, T2 = log2(1/(255 o)); all zero if culled)
+ *   rec   [..][12] fp32 = u, v, hx, hy | A2, B2, C2, T2 | o, r, g, b
+ *         (A2,B2,C2 base-2 conic, T2 = log2(1/(255 o)); hx, hy = 1.0001 sqrt(2 ln(255 o) S'_xx|yy),
+ *          the bounding box of the alpha >= 1/255 ellipse (R#13); all zero if culled)
  *   depth u32 = bits(z_c) (z_c > 0)          tiles u32 = #16x16 tiles touched
- *   rect  int16[4] = tx0, ty0, tx1, ty1 (inclusive; zeros if culled) */
+ *   rect  int16[4] = tx0, ty0, tx1, ty1 of [u +- ceil(hx)] x [v +- ceil(hy)] (inclusive) */
 typedef struct {
     int32_t n_pad;
     float* rec;

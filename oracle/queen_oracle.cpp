@@ -258,11 +258,14 @@ static Cam load_cam(const float* w) {
 
 // ---------------------------------------------------------------------------
 // a6 + a7. Projection of Gaussian i into view v (Eq. 1; colour P:226).
-// Records (R#13, R#14): rec[12] = u, v, A2, B2 | C2, T2, o, 0 | r, g, b, 0
+// Records (R#13, R#14): rec[12] = u, v, hx, hy | A2, B2, C2, T2 | o, r, g, b
 //   A2,B2,C2 = base-2 conic: p2 = A2 dx^2 + B2 dx dy + C2 dy^2 = -0.5 log2(e) d^T S'^-1 d
 //   T2 = log2(1/(255 o)): alpha < 1/255  <=>  p2 < T2
-// depth = bits(z_c); tiles = #16x16 tiles of the opacity-aware extent; rect = tile
-// rect (tx0, ty0, tx1, ty1) inclusive.  A culled Gaussian gets all zeros.
+//   hx, hy = 1.0001 sqrt(e2 S'_xx), 1.0001 sqrt(e2 S'_yy): half-extents of the ellipse
+//   d^T S'^-1 d <= e2 = 2 ln(255 o) (where alpha reaches 1/255) -- its tight axis-aligned
+//   bounding box, with 1e-4 relative slack
+// depth = bits(z_c); rect = 16x16 tiles overlapping [u +- ceil(hx)] x [v +- ceil(hy)]
+// (tx0, ty0, tx1, ty1 inclusive); tiles = their number.  A culled Gaussian gets zeros.
 // Returns 1 if any Gaussian had a non-finite input (culled + QUEEN_WARN_NONFINITE).
 // ---------------------------------------------------------------------------
 static int project_one(int i, int n_pad, int deg, const float* pl, const Cam& c, float* rec, uint32_t* depth,
@@ -336,26 +339,27 @@ static int project_one(int i, int n_pad, int deg, const float* pl, const Cam& c,
     float cc2 = std::fma(Bm[3], A[3], std::fma(Bm[4], A[4], Bm[5] * A[5]));
     a = a + 0.3f;
     cc2 = cc2 + 0.3f;
-    // 6. conic = Sigma'^-1 (Eq. 2 exponent), largest eigenvalue for the extent
+    // 6. conic = Sigma'^-1 (Eq. 2 exponent)
     float det = std::fma(a, cc2, -(b * b));
     if (!(det > 0.0f)) return 0;
     float ca = cc2 / det, cb = -b / det, ccn = a / det;
-    float mid = 0.5f * (a + cc2);
-    float lam1 = mid + std::sqrt(std::fmax(0.1f, mid * mid - det));
     // 7. opacity o = sigmoid(logit) in [0,1]; alpha can reach 1/255 only if 255 o > 1 (R#14)
     float o = 1.0f / (1.0f + oracle_det_exp(-pl[10 * (int64_t)n_pad + i]));
     if (!(255.0f * o > 1.0f)) return 0;
     float e2 = 2.0f * oracle_det_log(255.0f * o);
-    // 8. opacity-aware radius: Mahalanobis^2 = 2 ln(255 o) along the major axis (R#13)
-    float rad = std::ceil(1.0001f * std::sqrt(e2 * lam1));
+    // 8. opacity-aware extent (R#13): the ellipse d^T S'^-1 d <= e2 has axis-aligned
+    //    half-extents sqrt(e2 S'_xx), sqrt(e2 S'_yy); 1e-4 relative slack, integer radii
+    float hx = 1.0001f * std::sqrt(e2 * a);
+    float hy = 1.0001f * std::sqrt(e2 * cc2);
+    float rx = std::ceil(hx), ry = std::ceil(hy);
     float u = std::fma(c.fx, tx, c.cx);
     float v = std::fma(c.fy, ty, c.cy);
     // 9. 16x16 tile rect (inclusive), clamped in float before the int conversion
     int gx = (c.W + 15) / 16, gy = (c.H + 15) / 16;
-    float ftx0 = std::fmin(std::fmax(std::ceil(((u - rad) - 15.0f) * 0.0625f), 0.0f), (float)gx);
-    float ftx1 = std::fmin(std::fmax(std::floor((u + rad) * 0.0625f), -1.0f), (float)(gx - 1));
-    float fty0 = std::fmin(std::fmax(std::ceil(((v - rad) - 15.0f) * 0.0625f), 0.0f), (float)gy);
-    float fty1 = std::fmin(std::fmax(std::floor((v + rad) * 0.0625f), -1.0f), (float)(gy - 1));
+    float ftx0 = std::fmin(std::fmax(std::ceil(((u - rx) - 15.0f) * 0.0625f), 0.0f), (float)gx);
+    float ftx1 = std::fmin(std::fmax(std::floor((u + rx) * 0.0625f), -1.0f), (float)(gx - 1));
+    float fty0 = std::fmin(std::fmax(std::ceil(((v - ry) - 15.0f) * 0.0625f), 0.0f), (float)gy);
+    float fty1 = std::fmin(std::fmax(std::floor((v + ry) * 0.0625f), -1.0f), (float)(gy - 1));
     int tx0 = (int)ftx0, tx1 = (int)ftx1, ty0 = (int)fty0, ty1 = (int)fty1;
     uint32_t nt = (tx0 <= tx1 && ty0 <= ty1) ? (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1)) : 0u;
     // 10. base-2 blend coefficients
@@ -376,9 +380,9 @@ static int project_one(int i, int n_pad, int deg, const float* pl, const Cam& c,
         for (int bb = 1; bb < B; ++bb) acc = std::fma(Y[bb], pl[(int64_t)(11 + 3 * bb + ch) * n_pad + i], acc);
         rgb[ch] = std::fmax(0.0f, acc + 0.5f);
     }
-    rec[0] = u; rec[1] = v; rec[2] = A2; rec[3] = B2;
-    rec[4] = C2; rec[5] = T2; rec[6] = o; rec[7] = 0.0f;
-    rec[8] = rgb[0]; rec[9] = rgb[1]; rec[10] = rgb[2]; rec[11] = 0.0f;
+    rec[0] = u; rec[1] = v; rec[2] = hx; rec[3] = hy;
+    rec[4] = A2; rec[5] = B2; rec[6] = C2; rec[7] = T2;
+    rec[8] = o; rec[9] = rgb[0]; rec[10] = rgb[1]; rec[11] = rgb[2];
     *depth = bits_of(zc);  // 12. depth key: z_c > 0 so its bits order like the float (R#15)
     *tiles = nt;
     rect[0] = (int16_t)tx0; rect[1] = (int16_t)ty0; rect[2] = (int16_t)tx1; rect[3] = (int16_t)ty1;
@@ -463,15 +467,20 @@ int64_t oracle_bin(int n_pad, int V, int W, int H, const uint32_t* tiles, const 
 // p2 > 0), a_i clamped at 0.99, composite-then-stop when T < 1e-4.  Pixel (x, y)
 // is sampled at ((float)x, (float)y) (R#12).  Output C + T*bg and T (R#16).
 // ---------------------------------------------------------------------------
-static inline bool blend_step(const float* rc, float fx, float fy, float C[3], float& T) {
+// record words: 0 u, 1 v, 4 A2, 5 B2, 6 C2, 7 T2, 8 o, 9-11 rgb (hx, hy unused here)
+static inline float rec_p2(const float* rc, float fx, float fy) {
     float dx = rc[0] - fx, dy = rc[1] - fy;
-    float p2 = std::fma(rc[2] * dx, dx, std::fma(rc[4] * dy, dy, (rc[3] * dx) * dy));
-    if (p2 > 0.0f || p2 < rc[5]) return false;
-    float alpha = std::fmin(0.99f, rc[6] * std::exp2(p2));
+    return std::fma(rc[4] * dx, dx, std::fma(rc[6] * dy, dy, (rc[5] * dx) * dy));
+}
+
+static inline bool blend_step(const float* rc, float fx, float fy, float C[3], float& T) {
+    float p2 = rec_p2(rc, fx, fy);
+    if (p2 > 0.0f || p2 < rc[7]) return false;
+    float alpha = std::fmin(0.99f, rc[8] * std::exp2(p2));
     float aT = alpha * T;
-    C[0] = std::fma(rc[8], aT, C[0]);
-    C[1] = std::fma(rc[9], aT, C[1]);
-    C[2] = std::fma(rc[10], aT, C[2]);
+    C[0] = std::fma(rc[9], aT, C[0]);
+    C[1] = std::fma(rc[10], aT, C[1]);
+    C[2] = std::fma(rc[11], aT, C[2]);
     T = T * (1.0f - alpha);
     return T < 1e-4f;
 }
@@ -527,7 +536,7 @@ void oracle_rasterize_bruteforce(int n, int n_pad, int V, int W, int H, const fl
     for (int v = 0; v < V; ++v) {
         std::vector<std::pair<uint32_t, uint32_t>> order;
         for (int i = 0; i < n; ++i)
-            if (rec[((int64_t)v * n_pad + i) * 12 + 6] > 0.0f) order.push_back({depth[(int64_t)v * n_pad + i], (uint32_t)i});
+            if (rec[((int64_t)v * n_pad + i) * 12 + 8] > 0.0f) order.push_back({depth[(int64_t)v * n_pad + i], (uint32_t)i});
         std::sort(order.begin(), order.end());
 #pragma omp parallel for num_threads(threads) schedule(dynamic, 1)
         for (int y = 0; y < H; ++y)
@@ -561,9 +570,8 @@ void oracle_blend_counts(int n_pad, int V, int W, int H, const float* rec, const
                 for (uint32_t j = ranges[2 * gt]; j < ranges[2 * gt + 1]; ++j) {
                     const float* rc = rec + ((int64_t)v * n_pad + vals_sorted[j]) * 12;
                     ++ev;
-                    float dx = rc[0] - (float)x, dy = rc[1] - (float)y;
-                    float p2 = std::fma(rc[2] * dx, dx, std::fma(rc[4] * dy, dy, (rc[3] * dx) * dy));
-                    if (!(p2 > 0.0f || p2 < rc[5])) ++cp;
+                    float p2 = rec_p2(rc, (float)x, (float)y);
+                    if (!(p2 > 0.0f || p2 < rc[7])) ++cp;
                     if (blend_step(rc, (float)x, (float)y, C, Tr)) break;
                 }
             }

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(128) k_project(const float* __restrict__ plane
             zc = fmaf(Rw[6], px, fmaf(Rw[7], py, fmaf(Rw[8], pz, c.t[2])));
             ok = zc > c.near_z;
         }
-        float a2 = 0.f, b2 = 0.f, c2 = 0.f, lam1 = 0.f, tx = 0.f, ty = 0.f;
+        float a2 = 0.f, b2 = 0.f, c2 = 0.f, sxx = 0.f, syy = 0.f, tx = 0.f, ty = 0.f;
         if (ok) {
             const float* Rw = c.R;
             tx = xc / zc;
@@ -153,24 +153,27 @@ __global__ void __launch_bounds__(128) k_project(const float* __restrict__ plane
                 a2 = sc / det;    // conic xx
                 b2 = -sb / det;   // conic xy
                 c2 = sa / det;    // conic yy
-                const float mid = 0.5f * (sa + sc);
-                lam1 = mid + sqrtf(fmaxf(0.1f, mid * mid - det));
+                sxx = sa;         // Sigma'_xx (incl. the 0.3 dilation)
+                syy = sc;
             }
         }
         if (ok) {
-            const float rad = ceilf(1.0001f * sqrtf(e2 * lam1));
+            // opacity-aware extent (R#13): tight bounding box of d^T S'^-1 d <= e2, 1e-4 slack
+            const float hx = 1.0001f * sqrtf(e2 * sxx);
+            const float hy = 1.0001f * sqrtf(e2 * syy);
+            const float rx = ceilf(hx), ry = ceilf(hy);
             const float u = fmaf(c.fx, tx, c.cx);
             const float vv = fmaf(c.fy, ty, c.cy);
             const int gx = (c.width + 15) / 16, gy = (c.height + 15) / 16;
-            const float ftx0 = fminf(fmaxf(ceilf(((u - rad) - 15.0f) * 0.0625f), 0.0f), (float)gx);
-            const float ftx1 = fminf(fmaxf(floorf((u + rad) * 0.0625f), -1.0f), (float)(gx - 1));
-            const float fty0 = fminf(fmaxf(ceilf(((vv - rad) - 15.0f) * 0.0625f), 0.0f), (float)gy);
-            const float fty1 = fminf(fmaxf(floorf((vv + rad) * 0.0625f), -1.0f), (float)(gy - 1));
+            const float ftx0 = fminf(fmaxf(ceilf(((u - rx) - 15.0f) * 0.0625f), 0.0f), (float)gx);
+            const float ftx1 = fminf(fmaxf(floorf((u + rx) * 0.0625f), -1.0f), (float)(gx - 1));
+            const float fty0 = fminf(fmaxf(ceilf(((vv - ry) - 15.0f) * 0.0625f), 0.0f), (float)gy);
+            const float fty1 = fminf(fmaxf(floorf((vv + ry) * 0.0625f), -1.0f), (float)(gy - 1));
             const int tx0 = (int)ftx0, tx1 = (int)ftx1, ty0 = (int)fty0, ty1 = (int)fty1;
             nt = (tx0 <= tx1 && ty0 <= ty1) ? (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1)) : 0u;
             const float L2E = 1.4426950408889634f;
-            r0 = make_float4(u, vv, (-0.5f * a2) * L2E, (-b2) * L2E);
-            r1 = make_float4((-0.5f * c2) * L2E, -(0.5f * e2) * L2E, o, 0.f);
+            r0 = make_float4(u, vv, hx, hy);
+            r1 = make_float4((-0.5f * a2) * L2E, (-b2) * L2E, (-0.5f * c2) * L2E, -(0.5f * e2) * L2E);
             // colour: dir = (p - C)/|p - C|, rgb = max(0, sum Y_b h_b + 0.5) (R#8, R#10)
             float dx = px - c.C[0], dy = py - c.C[1], dz = pz - c.C[2];
             const float dn = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
@@ -185,7 +188,7 @@ __global__ void __launch_bounds__(128) k_project(const float* __restrict__ plane
                 for (int b = 1; b < B; ++b) acc = fmaf(Y[b], a[11 + 3 * b + ch], acc);
                 rgb[ch] = fmaxf(0.0f, acc + 0.5f);
             }
-            r2 = make_float4(rgb[0], rgb[1], rgb[2], 0.f);
+            r2 = make_float4(o, rgb[0], rgb[1], rgb[2]);
             dbits = __float_as_uint(zc);
             rc = make_short4((short)tx0, (short)ty0, (short)tx1, (short)ty1);
         }

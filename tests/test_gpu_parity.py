@@ -145,8 +145,8 @@ def _check_proj(got, ref, n):
     for key in ("depth", "tiles", "rect"):
         assert np.array_equal(got[key][:, :n], ref[key][:, :n]), key
     g, r = got["rec"][:, :n], ref["rec"][:, :n]
-    assert np.array_equal(g[..., :8].view(np.uint32), r[..., :8].view(np.uint32))  # u v A2 B2 C2 T2 o pad
-    assert np.all(np.abs(g[..., 8:] - r[..., 8:]) <= 1e-5 * np.maximum(np.abs(r[..., 8:]), 1e-6) + 1e-7)
+    assert np.array_equal(g[..., :9].view(np.uint32), r[..., :9].view(np.uint32))  # u v hx hy A2 B2 C2 T2 o
+    assert np.all(np.abs(g[..., 9:] - r[..., 9:]) <= 1e-5 * np.maximum(np.abs(r[..., 9:]), 1e-6) + 1e-7)
 
 
 def _check_bins(got, ref, depth=None, T=None):

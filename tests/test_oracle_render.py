@@ -24,9 +24,9 @@ L2E = 1.4426950408889634
 
 def _conic_to_sigma(rec):
     """Recover Sigma' (float64) from a record's base-2 conic (A2, B2, C2)."""
-    ca = rec[2] / (-0.5 * L2E)
-    cb = rec[3] / (-L2E)
-    cc = rec[4] / (-0.5 * L2E)
+    ca = rec[4] / (-0.5 * L2E)
+    cb = rec[5] / (-L2E)
+    cc = rec[6] / (-0.5 * L2E)
     return np.linalg.inv(np.array([[ca, cb], [cb, cc]], np.float64))
 
 
@@ -112,8 +112,8 @@ def test_single_and_two_gaussian_compositing():
     pl = planes_from([[0, 0, 3.0]], [[1, 0, 0, 0]], [[math.log(0.01)] * 3], [logit(ex["o"])],
                      [sh_for_rgb(ex["c"], 0)], 0)
     proj, bins, rgb, T = oracle.render(pl, 1, 0, [cam])
-    o = proj["rec"][0, 0, 6]
-    c = proj["rec"][0, 0, 8:11]
+    o = proj["rec"][0, 0, 8]
+    c = proj["rec"][0, 0, 9:12]
     assert np.allclose(rgb[0, :, 16, 16], c * o, rtol=1e-6) and np.allclose(c, ex["c"], atol=1e-6)
     assert T[0, 16, 16] == pytest.approx(1 - o, abs=1e-7) and abs(o - ex["o"]) < 1e-6
     assert np.allclose(rgb[0, :, 16, 16], ex["C"], atol=2e-6)
@@ -204,7 +204,7 @@ def test_transmittance_monotone_and_alpha_bound():
     proj, bins, rgb, T = oracle.render(sc.planes, sc.n, sc.deg, cams)
     # accumulated alpha 1 - T in [0, 1); colour bounded by max rgb * (1 - T)
     assert np.all(T <= 1) and np.all(T > 0)
-    cmax = proj["rec"][0, :, 8:11].max()
+    cmax = proj["rec"][0, :, 9:12].max()
     assert np.all(rgb[0] <= cmax * (1 - T[0]) * (1 + 1e-5) + 1e-7)
     # prefix renders: compositing only the first j entries of every tile list can only lower T
     r2 = dict(bins)
@@ -234,12 +234,42 @@ def test_oracle_vs_float64_textbook_renderer(deg):
     assert np.abs(T[0] - Tref).max() < 2e-2
     # projected footprint vs float64 Eq. 1 for every non-culled Gaussian
     pr = ref64.project64(sc.planes, sc.n, deg, cam)
-    live = proj["rec"][0, : sc.n, 6] > 0
+    live = proj["rec"][0, : sc.n, 8] > 0
     assert np.array_equal(live, pr["valid"])
     rec = proj["rec"][0, : sc.n][live]
     con = pr["conic"][live]
-    assert np.allclose(rec[:, 2], -0.5 * L2E * con[:, 0, 0], rtol=1e-4, atol=1e-7)
-    assert np.allclose(rec[:, 3], -L2E * con[:, 0, 1], rtol=1e-4, atol=1e-6)
-    assert np.allclose(rec[:, 4], -0.5 * L2E * con[:, 1, 1], rtol=1e-4, atol=1e-7)
+    assert np.allclose(rec[:, 4], -0.5 * L2E * con[:, 0, 0], rtol=1e-4, atol=1e-7)
+    assert np.allclose(rec[:, 5], -L2E * con[:, 0, 1], rtol=1e-4, atol=1e-6)
+    assert np.allclose(rec[:, 6], -0.5 * L2E * con[:, 1, 1], rtol=1e-4, atol=1e-7)
     assert np.allclose(rec[:, 0], pr["u"][live], rtol=1e-6, atol=1e-4)
-    assert np.allclose(rec[:, 8:11], pr["rgb"][:, live].T, rtol=1e-5, atol=1e-6)
+    assert np.allclose(rec[:, 9:12], pr["rgb"][:, live].T, rtol=1e-5, atol=1e-6)
+    # extent: hx = sqrt(2 ln(255 o) S'_xx) (tight bounding box of the alpha = 1/255 ellipse), 1e-4 slack
+    e2 = 2 * np.log(255 * pr["o"][live])
+    assert np.allclose(rec[:, 2], 1.0001 * np.sqrt(e2 * pr["S2"][live, 0, 0]), rtol=1e-4)
+    assert np.allclose(rec[:, 3], 1.0001 * np.sqrt(e2 * pr["S2"][live, 1, 1]), rtol=1e-4)
+
+
+def test_extent_contains_every_contributing_pixel():
+    """Every pixel whose (fp32) p2 >= T2 lies within [u +- hx] x [v +- hy] (the blend's cull box)
+    and inside the Gaussian's tile rect: brute force over all pixels of a ragged image."""
+    rng = np.random.default_rng(9)
+    n = 400
+    pos = np.stack([rng.uniform(-2, 2, n), rng.uniform(-1.5, 1.5, n), rng.uniform(1.0, 5, n)], 1)
+    pl = planes_from(pos, rng.standard_normal((n, 4)), rng.normal(math.log(0.08), 0.9, (n, 3)),
+                     rng.normal(1, 2.5, n), rng.normal(0, 0.5, (n, 1, 3)), 0)
+    cam = synth.make_camera(np.eye(3), np.zeros(3), 50.0, 50.0, 90, 61)
+    pr = oracle.project(pl, n, 0, [cam])
+    rec = pr["rec"][0, :n].astype(np.float32)
+    ys, xs = np.mgrid[0:61, 0:90]
+    xs = xs.reshape(-1).astype(np.float32)
+    ys = ys.reshape(-1).astype(np.float32)
+    for i in np.nonzero(rec[:, 8] > 0)[0]:
+        r = rec[i]
+        dx = (r[0] - xs).astype(np.float32)
+        dy = (r[1] - ys).astype(np.float32)
+        p2 = (r[4] * dx).astype(np.float32) * dx + ((r[6] * dy).astype(np.float32) * dy + (r[5] * dx).astype(np.float32) * dy)
+        hit = (p2 >= r[7] - 1e-4) & (p2 <= 1e-6)
+        assert np.all(np.abs(dx[hit]) <= r[2]) and np.all(np.abs(dy[hit]) <= r[3])
+        tx, ty = (xs[hit] // 16).astype(int), (ys[hit] // 16).astype(int)
+        rc = pr["rect"][0, i]
+        assert np.all((tx >= rc[0]) & (tx <= rc[2]) & (ty >= rc[1]) & (ty <= rc[3]))
