@@ -173,59 +173,94 @@ __global__ void k_hist_scan(const uint32_t* hist, uint32_t* excl, int passes, in
 // ---------------------------------------------------------------------------
 // K5: one onesweep pass over (u32 key, u32 value) pairs
 // ---------------------------------------------------------------------------
+// Block of NT threads: exclusive scan of one u32 per thread; returns prefix, sets total.
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_scan_t(uint32_t x, uint32_t* s_w, uint32_t& total) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) {
+        const uint32_t s = s_w[q];
+        pre += (q < w) ? s : 0u;
+        tot += s;
+    }
+    total = tot;
+    return pre + inc - x;
+}
+
+// onesweep configuration: NT threads x IT keys per thread = one 4096-key tile
 template <int BITS>
 struct Onesweep {
+    static constexpr int NT = 512, IT = 8, NW = NT / 32;
+    static constexpr int TILE = NT * IT;
     static constexpr int BINS = 1 << BITS;
-    static constexpr int DPT = BINS / SORT_THREADS;
-    static constexpr size_t SMEM = (size_t)SORT_TILE * 4 * 2 + (size_t)SORT_WARPS * BINS * 4 + (size_t)BINS * 4 * 2;
+    static constexpr int DPT = BINS >= NT ? BINS / NT : 1;  // digits per thread (threads >= BINS idle)
+    static constexpr size_t SMEM = (size_t)TILE * 4 * 2 + (size_t)NW * BINS * 4 + (size_t)BINS * 4 * 2;
 };
 
 template <int BITS>
-__global__ void __launch_bounds__(SORT_THREADS) k_onesweep32(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                             uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                             const uint32_t* count_ptr, uint32_t cap, int shift,
-                                                             const uint32_t* __restrict__ hist_excl, uint32_t* lb,
-                                                             uint32_t* ticket, DevFlags* fl) {
-    constexpr int BINS = Onesweep<BITS>::BINS;
-    constexpr int DPT = Onesweep<BITS>::DPT;
+__global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_t* __restrict__ kin,
+                                                                   const uint32_t* __restrict__ vin,
+                                                                   uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                                   const uint32_t* count_ptr, uint32_t cap, int shift,
+                                                                   const uint32_t* __restrict__ hist_excl, uint32_t* lb,
+                                                                   uint32_t* ticket, DevFlags* fl) {
+    using OS = Onesweep<BITS>;
+    constexpr int NT = OS::NT, IT = OS::IT, NW = OS::NW, TILE = OS::TILE, BINS = OS::BINS, DPT = OS::DPT;
     constexpr uint32_t DMASK = BINS - 1;
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* sk = reinterpret_cast<uint32_t*>(smem);
-    uint32_t* sv = sk + SORT_TILE;
-    uint32_t* whist = sv + SORT_TILE;             // [warps][BINS]: counts, then exclusive-over-warps
-    uint32_t* dstart = whist + SORT_WARPS * BINS;  // [BINS] tile-local exclusive digit start
-    uint32_t* dbase = dstart + BINS;              // [BINS] global destination minus local start
-    __shared__ uint32_t s_tile, s_w[SORT_WARPS];
+    uint32_t* sv = sk + TILE;
+    uint32_t* whist = sv + TILE;             // [warps][BINS]: counts, then exclusive-over-warps
+    uint32_t* dstart = whist + NW * BINS;    // [BINS] tile-local exclusive digit start
+    uint32_t* dbase = dstart + BINS;         // [BINS] global destination minus local start
+    __shared__ uint32_t s_tile, s_w[NW];
     const uint32_t Kn = min(*count_ptr, cap);
-    const uint32_t ntiles = (Kn + SORT_TILE - 1) / SORT_TILE;
+    const uint32_t ntiles = (Kn + TILE - 1) / TILE;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    const bool owns_digits = threadIdx.x * DPT < BINS;
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-        for (int q = threadIdx.x; q < SORT_WARPS * BINS; q += SORT_THREADS) whist[q] = 0u;
+        for (int q = threadIdx.x; q < NW * BINS; q += NT) whist[q] = 0u;
         __syncthreads();
         const uint32_t tile = s_tile;
         if (tile >= ntiles) break;
-        const uint32_t base = tile * SORT_TILE;
-        uint32_t k[SORT_ITEMS], val[SORT_ITEMS], rk[SORT_ITEMS];
+        const uint32_t base = tile * TILE;
+        uint32_t k[IT], val[IT], rk[IT];
 #pragma unroll
-        for (int j = 0; j < SORT_ITEMS; ++j) {
-            const uint32_t idx = base + w * (32 * SORT_ITEMS) + j * 32 + lane;
+        for (int j = 0; j < IT; ++j) {
+            const uint32_t idx = base + w * (32 * IT) + j * 32 + lane;
             const bool ok = idx < Kn;
             k[j] = ok ? kin[idx] : 0u;
             val[j] = ok ? vin[idx] : 0u;
-            rk[j] = ok ? ((k[j] >> shift) & DMASK) : (uint32_t)BINS;
         }
-        // warp multisplit in key order (stable): rank among this warp's earlier equal digits
+        // warp multisplit in key order (stable): rank among this warp's earlier equal digits.
+        // All MATCHes first (independent), then the short shared-memory chain.
+        uint32_t peers[IT];
 #pragma unroll
-        for (int j = 0; j < SORT_ITEMS; ++j) {
+        for (int j = 0; j < IT; ++j) {
+            const uint32_t idx = base + w * (32 * IT) + j * 32 + lane;
+            rk[j] = idx < Kn ? ((k[j] >> shift) & DMASK) : (uint32_t)BINS;
+            peers[j] = __match_any_sync(0xffffffffu, rk[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
             const uint32_t d = rk[j];
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            const uint32_t below = peers & lt_mask;
+            const uint32_t below = peers[j] & lt_mask;
             uint32_t prior = 0;
             if (d < (uint32_t)BINS) prior = whist[w * BINS + d];
             __syncwarp();
-            if (below == 0 && d < (uint32_t)BINS) whist[w * BINS + d] = prior + __popc(peers);
+            if (below == 0 && d < (uint32_t)BINS) whist[w * BINS + d] = prior + __popc(peers[j]);
             __syncwarp();
             rk[j] = (prior + __popc(below)) | (d << 16);
         }
@@ -234,47 +269,52 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep32(const uint32_t* __r
         uint32_t tsum = 0;
 #pragma unroll
         for (int e = 0; e < DPT; ++e) {
-            const int d = threadIdx.x * DPT + e;
-            uint32_t run = 0;
+            cnt[e] = 0;
+            if (owns_digits) {
+                const int d = threadIdx.x * DPT + e;
+                uint32_t run = 0;
 #pragma unroll
-            for (int q = 0; q < SORT_WARPS; ++q) {
-                const uint32_t c = whist[q * BINS + d];
-                whist[q * BINS + d] = run;
-                run += c;
+                for (int q = 0; q < NW; ++q) {
+                    const uint32_t c = whist[q * BINS + d];
+                    whist[q * BINS + d] = run;
+                    run += c;
+                }
+                cnt[e] = run;
+                tsum += run;
+                st_volatile_u32(&lb[(size_t)tile * BINS + d], (tile == 0 ? LB_INC : LB_AGG) | run);
             }
-            cnt[e] = run;
-            tsum += run;
-            st_volatile_u32(&lb[(size_t)tile * BINS + d], (tile == 0 ? LB_INC : LB_AGG) | run);
         }
         uint32_t total;
-        uint32_t excl = block_excl_scan(tsum, s_w, total);
+        uint32_t excl = block_excl_scan_t<NT>(tsum, s_w, total);
+        if (owns_digits) {
 #pragma unroll
-        for (int e = 0; e < DPT; ++e) {
-            const int d = threadIdx.x * DPT + e;
-            uint32_t prefix = 0;
-            if (tile > 0) {
-                int64_t look = (int64_t)tile - 1;
-                long long spins = 0;
-                while (look >= 0) {
-                    const uint32_t x = ld_volatile_u32(&lb[(size_t)look * BINS + d]);
-                    const uint32_t f = x >> 30;
-                    if (f == 0) {
-                        if (++spins > SPIN_LIMIT) { raise_flag(fl, FLAG_TIMEOUT); break; }
-                        continue;
+            for (int e = 0; e < DPT; ++e) {
+                const int d = threadIdx.x * DPT + e;
+                dstart[d] = excl;
+                uint32_t prefix = 0;
+                if (tile > 0) {
+                    int64_t look = (int64_t)tile - 1;
+                    long long spins = 0;
+                    while (look >= 0) {
+                        const uint32_t x = ld_volatile_u32(&lb[(size_t)look * BINS + d]);
+                        const uint32_t f = x >> 30;
+                        if (f == 0) {
+                            if (++spins > SPIN_LIMIT) { raise_flag(fl, FLAG_TIMEOUT); break; }
+                            continue;
+                        }
+                        prefix += x & LB_MASK;
+                        if (f == 2) break;
+                        --look;
                     }
-                    prefix += x & LB_MASK;
-                    if (f == 2) break;
-                    --look;
+                    st_volatile_u32(&lb[(size_t)tile * BINS + d], LB_INC | (prefix + cnt[e]));
                 }
-                st_volatile_u32(&lb[(size_t)tile * BINS + d], LB_INC | (prefix + cnt[e]));
+                dbase[d] = hist_excl[d] + prefix - excl;
+                excl += cnt[e];
             }
-            dstart[d] = excl;
-            dbase[d] = hist_excl[d] + prefix - excl;
-            excl += cnt[e];
         }
         __syncthreads();
 #pragma unroll
-        for (int j = 0; j < SORT_ITEMS; ++j) {
+        for (int j = 0; j < IT; ++j) {
             const uint32_t d = rk[j] >> 16;
             if (d < (uint32_t)BINS) {
                 const uint32_t pos = dstart[d] + whist[w * BINS + d] + (rk[j] & 0xffffu);
@@ -283,8 +323,8 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep32(const uint32_t* __r
             }
         }
         __syncthreads();
-        const uint32_t nvalid = min((uint32_t)SORT_TILE, Kn - base);
-        for (uint32_t p = threadIdx.x; p < nvalid; p += SORT_THREADS) {
+        const uint32_t nvalid = min((uint32_t)TILE, Kn - base);
+        for (uint32_t p = threadIdx.x; p < nvalid; p += NT) {
             const uint32_t key = sk[p];
             const uint32_t dest = dbase[(key >> shift) & DMASK] + p;
             kout[dest] = key;
@@ -330,14 +370,30 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
     const int dw = gx + 1, dplane = (gx + 1) * (gy + 1);
     uint32_t nt[SORT_ITEMS];
     uint32_t tsum = 0;
+    // batch the dependent gathers: all 16 indices (4 x uint4), then all 16 rects, then use them
+    uint32_t jj[SORT_ITEMS];
+#pragma unroll
+    for (int q4 = 0; q4 < SORT_ITEMS / 4; ++q4) {
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (base + 4 * q4 + 3 < M) x = __ldg(reinterpret_cast<const uint4*>(dvals + base + 4 * q4));
+        else {
+            if (base + 4 * q4 + 0 < M) x.x = __ldg(dvals + base + 4 * q4 + 0);
+            if (base + 4 * q4 + 1 < M) x.y = __ldg(dvals + base + 4 * q4 + 1);
+            if (base + 4 * q4 + 2 < M) x.z = __ldg(dvals + base + 4 * q4 + 2);
+        }
+        jj[4 * q4] = x.x; jj[4 * q4 + 1] = x.y; jj[4 * q4 + 2] = x.z; jj[4 * q4 + 3] = x.w;
+    }
+    short4 rr[SORT_ITEMS];
+#pragma unroll
+    for (int e = 0; e < SORT_ITEMS; ++e) rr[e] = base + e < M ? __ldg(rect + jj[e]) : make_short4(0, 0, 0, 0);
 #pragma unroll
     for (int e = 0; e < SORT_ITEMS; ++e) {
         const uint32_t m = base + e;
         const int q = threadIdx.x * SORT_ITEMS + e;
         nt[e] = 0;
         if (m < M) {
-            const uint32_t j = __ldg(dvals + m);
-            const short4 r = __ldg(rect + j);
+            const uint32_t j = jj[e];
+            const short4 r = rr[e];
             const uint32_t v = j / (uint32_t)n_pad;
             const uint32_t wx = (uint32_t)(r.z - r.x + 1), wy = (uint32_t)(r.w - r.y + 1);
             nt[e] = wx * wy;
@@ -420,18 +476,19 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
 }
 
 // Per-view 2D prefix sums of the tile-count difference arrays -> entries per global tile,
-// the tile-digit histograms of the coming tile sort, and per-view totals.
+// their view-local exclusive starts, the tile-digit histograms of the coming tile sort,
+// and per-view totals.  One block per view.
 __global__ void __launch_bounds__(1024) k_tile_counts(const int* __restrict__ diff, int gx, int gy, uint32_t* counts,
-                                                      uint32_t* view_tot, uint32_t* hist, int tpasses, int tbits) {
+                                                      uint32_t* lstart, uint32_t* view_tot, uint32_t* hist, int tpasses,
+                                                      int tbits) {
     extern __shared__ int cs[];  // [(gy+1)][(gx+1)]
     __shared__ uint32_t sh[MAX_TILE_PASSES * MAX_BINS];
-    __shared__ uint32_t s_tot;
+    __shared__ uint32_t s_w[32];
     const int v = blockIdx.x;
     const int dw = gx + 1, dplane = (gx + 1) * (gy + 1);
     const int T = gx * gy;
     for (int q = threadIdx.x; q < dplane; q += blockDim.x) cs[q] = diff[(int64_t)v * dplane + q];
     for (int q = threadIdx.x; q < tpasses * MAX_BINS; q += blockDim.x) sh[q] = 0;
-    if (threadIdx.x == 0) s_tot = 0;
     __syncthreads();
     for (int r = threadIdx.x; r < gy; r += blockDim.x) {  // prefix along x
         int run = 0;
@@ -443,58 +500,60 @@ __global__ void __launch_bounds__(1024) k_tile_counts(const int* __restrict__ di
         for (int r = 0; r < gy; ++r) { run += cs[r * dw + x]; cs[r * dw + x] = run; }
     }
     __syncthreads();
+    // each thread: a contiguous chunk of tiles (row-major t) -> local exclusive starts
+    const int per = (T + blockDim.x - 1) / blockDim.x;
+    const int t0 = threadIdx.x * per, t1 = min(T, t0 + per);
+    uint32_t csum = 0;
+    for (int t = t0; t < t1; ++t) csum += (uint32_t)cs[(t / gx) * dw + (t % gx)];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t inc = csum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+        pre += q < w ? s_w[q] : 0u;
+        tot += s_w[q];
+    }
+    uint32_t run = pre + inc - csum;
     const uint32_t dmask = (1u << tbits) - 1u;
-    uint32_t tot = 0;
-    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    for (int t = t0; t < t1; ++t) {
         const uint32_t c = (uint32_t)cs[(t / gx) * dw + (t % gx)];
         const uint32_t g = (uint32_t)v * (uint32_t)T + (uint32_t)t;
         counts[g] = c;
-        tot += c;
+        lstart[g] = run;
+        run += c;
         if (c)
             for (int p = 0; p < tpasses; ++p) atomicAdd(&sh[p * MAX_BINS + ((g >> (p * tbits)) & dmask)], c);
     }
-    atomicAdd(&s_tot, tot);
     __syncthreads();
     for (int q = threadIdx.x; q < tpasses * MAX_BINS; q += blockDim.x)
         if (sh[q]) atomicAdd(&hist[q], sh[q]);
-    if (threadIdx.x == 0) view_tot[v] = s_tot;
+    if (threadIdx.x == 0) view_tot[v] = tot;
 }
 
-// ranges from the per-tile counts: exclusive scan over all global tiles (one block),
-// clamped to the key capacity (a capacity overflow is already flagged)
-__global__ void __launch_bounds__(1024) k_ranges_from_counts(const uint32_t* __restrict__ counts, int64_t G, uint32_t cap,
-                                                             const uint32_t* Kd, uint2* __restrict__ ranges) {
-    const bool overflow = Kd[2] != 0u;
-    __shared__ uint32_t s_w[32];
-    __shared__ unsigned long long s_carry;
-    if (threadIdx.x == 0) s_carry = 0;
+// ranges[gt] = view base + local start (view bases = exclusive scan of the <= 64 view
+// totals); [0,0) for empty tiles and everywhere on capacity overflow (already flagged)
+__global__ void __launch_bounds__(256) k_ranges_finalize(const uint32_t* __restrict__ counts,
+                                                         const uint32_t* __restrict__ lstart,
+                                                         const uint32_t* __restrict__ view_tot, int n_views, uint32_t T,
+                                                         uint32_t cap, const uint32_t* Kd, uint2* __restrict__ ranges) {
+    __shared__ unsigned long long s_base[QUEEN_MAX_VIEWS + 1];
+    if (threadIdx.x == 0) {
+        unsigned long long r = 0;
+        for (int q = 0; q < n_views; ++q) { s_base[q] = r; r += view_tot[q]; }
+    }
     __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int64_t b = 0; b < G; b += 1024) {
-        const int64_t g = b + threadIdx.x;
-        const uint32_t c = g < G ? counts[g] : 0u;
-        uint32_t inc = c;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        if (lane == 31) s_w[w] = inc;
-        __syncthreads();
-        uint32_t pre = 0, tot = 0;
-        for (int q = 0; q < 32; ++q) {
-            const uint32_t sq = s_w[q];
-            pre += q < w ? sq : 0u;
-            tot += sq;
-        }
-        const unsigned long long st = s_carry + pre + inc - c;
-        if (g < G) {
-            const unsigned long long en = st + c;
-            ranges[g] = (c && !overflow) ? make_uint2((uint32_t)(st < cap ? st : cap), (uint32_t)(en < cap ? en : cap))
-                          : make_uint2(0u, 0u);  // empty tile: [0, 0)
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) s_carry += tot;
-        __syncthreads();
+    const bool overflow = Kd[2] != 0u;
+    const uint64_t G = (uint64_t)n_views * T;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = counts[g];
+        const unsigned long long st = s_base[g / T] + lstart[g], en = st + c;
+        ranges[g] = (c && !overflow) ? make_uint2((uint32_t)(st < cap ? st : cap), (uint32_t)(en < cap ? en : cap))
+                                     : make_uint2(0u, 0u);
     }
 }
 
@@ -513,7 +572,7 @@ template <int BITS>
 static int onesweep_grid() {
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_onesweep32<BITS>, SORT_THREADS, Onesweep<BITS>::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_onesweep32<BITS>, Onesweep<BITS>::NT, Onesweep<BITS>::SMEM);
         if (occ <= 0) occ = 1;
     }
     return occ * num_sms();
@@ -532,7 +591,7 @@ template <int BITS>
 static void onesweep(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout, const uint32_t* count,
                      uint32_t cap, int shift, const uint32_t* hist_excl, uint32_t* lb, uint32_t* ticket, DevFlags* fl,
                      cudaStream_t s) {
-    k_onesweep32<BITS><<<onesweep_grid<BITS>(), SORT_THREADS, Onesweep<BITS>::SMEM, s>>>(kin, vin, kout, vout, count, cap,
+    k_onesweep32<BITS><<<onesweep_grid<BITS>(), Onesweep<BITS>::NT, Onesweep<BITS>::SMEM, s>>>(kin, vin, kout, vout, count, cap,
                                                                                          shift, hist_excl, lb, ticket, fl);
 }
 
@@ -601,8 +660,10 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     prof->end(s);
     // per-tile entry counts -> ranges and tile-digit histograms
     prof->begin(ST_RANGES, s);
-    k_tile_counts<<<n_views, 1024, sizeof(int) * dplane, s>>>(diff, gx, gy, tcounts, view_tot, thist, tpasses, tbits);
-    k_ranges_from_counts<<<1, 1024, 0, s>>>(tcounts, T * n_views, cap, Kd, reinterpret_cast<uint2*>(bins.ranges));
+    k_tile_counts<<<n_views, 1024, sizeof(int) * dplane, s>>>(diff, gx, gy, tcounts, tcounts + T * n_views, view_tot, thist,
+                                                               tpasses, tbits);
+    k_ranges_finalize<<<sms * 2, 256, 0, s>>>(tcounts, tcounts + T * n_views, view_tot, n_views, (uint32_t)T, cap, Kd,
+                                              reinterpret_cast<uint2*>(bins.ranges));
     prof->end(s, 2);
     // tile digits on the K entries
     prof->begin(ST_TILE_SORT, s);
