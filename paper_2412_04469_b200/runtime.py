@@ -75,7 +75,9 @@ class Player:
             raise ValueError("all views of a Player must share width/height")
         self.W, self.H = W, H
         V = len(self.cams)
-        self.vpb = min(V, views_per_batch or QUEEN_MAX_VIEWS, QUEEN_MAX_VIEWS)
+        vmax = min(V, views_per_batch or QUEEN_MAX_VIEWS, QUEEN_MAX_VIEWS)
+        nbatch = (V + vmax - 1) // vmax
+        self.vpb = (V + nbatch - 1) // nbatch  # balanced batches (e.g. 46 views -> 23 + 23)
         self.batches = [(b, min(b + self.vpb, V)) for b in range(0, V, self.vpb)]
         self.cam_arrays = [camera_array(self.cams[a:b]) for a, b in self.batches]
         self.bg = bg
@@ -91,11 +93,13 @@ class Player:
     def apply(self, pkt: DevicePacket, stream=None):
         queen_apply_frame(self.ctx, self.scene, pkt.struct, stream)
 
-    def render(self, stream=None):
+    def render(self, stream=None, out=None):
+        """Render every view into `out` (default self.rgb), fp32 [V][3][H][W]."""
+        rgb = self.rgb if out is None else out
         for (a, b), arr in zip(self.batches, self.cam_arrays):
-            queen_render_views(self.ctx, self.scene, None, self.rgb[a:b], None if self.T is None else self.T[a:b],
+            queen_render_views(self.ctx, self.scene, None, rgb[a:b], None if self.T is None else self.T[a:b],
                                self.bg, stream, cam_array=arr)
-        return self.rgb
+        return rgb
 
     def frame(self, pkt: DevicePacket | None, stream=None):
         if pkt is not None:
