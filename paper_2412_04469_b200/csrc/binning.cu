@@ -32,8 +32,16 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
 __device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v) {
     *reinterpret_cast<volatile unsigned long long*>(p) = v;
 }
-__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) { return *reinterpret_cast<const volatile uint32_t*>(p); }
-__device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) { *reinterpret_cast<volatile uint32_t*>(p) = v; }
+// look-back words: one 32-bit (flag | count) word each, so GPU-scope relaxed accesses suffice
+// (volatile would compile to system-scope .STRONG.SYS accesses)
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 constexpr unsigned long long SCAN_AGG = 1ull << 62, SCAN_INC = 2ull << 62, SCAN_MASK = (1ull << 62) - 1;
 constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_MASK = (1u << 30) - 1;
@@ -286,11 +294,22 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
         }
         uint32_t total;
         uint32_t excl = block_excl_scan_t<NT>(tsum, s_w, total);
+        uint32_t lstart[DPT];
+        if (owns_digits) {
+#pragma unroll
+            for (int e = 0; e < DPT; ++e) {
+                lstart[e] = excl;
+                dstart[threadIdx.x * DPT + e] = excl;
+                excl += cnt[e];
+            }
+        }
+        __syncthreads();
+        // digit owners run the decoupled look-back first (the inclusive chain is the critical
+        // path); meanwhile the other threads already scatter their keys into shared memory
         if (owns_digits) {
 #pragma unroll
             for (int e = 0; e < DPT; ++e) {
                 const int d = threadIdx.x * DPT + e;
-                dstart[d] = excl;
                 uint32_t prefix = 0;
                 if (tile > 0) {
                     int64_t look = (int64_t)tile - 1;
@@ -308,11 +327,9 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
                     }
                     st_volatile_u32(&lb[(size_t)tile * BINS + d], LB_INC | (prefix + cnt[e]));
                 }
-                dbase[d] = hist_excl[d] + prefix - excl;
-                excl += cnt[e];
+                dbase[d] = hist_excl[d] + prefix - lstart[e];
             }
         }
-        __syncthreads();
 #pragma unroll
         for (int j = 0; j < IT; ++j) {
             const uint32_t d = rk[j] >> 16;
