@@ -141,6 +141,15 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
+def lookup_traffic(traffic: dict, prefix: str):
+    """DRAM bytes per launch (ncu --set full capture summarised by tools/ncu_summary.py) of the
+    first kernel whose name starts with `prefix`, or None."""
+    for k in sorted(traffic):
+        if k.startswith(prefix):
+            return traffic[k]
+    return None
+
+
 def load_traffic():
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
@@ -367,7 +376,7 @@ def main():
             achieved = ops / len(batches) / t / 1e12
             peak = SM_COUNT * 128 * f_mhz * 1e6 / 1e12
             roof = {"bound": "alu", "kernel": "k_blend", "achieved": achieved, "peak": peak,
-                    "unit": "T FP32-lane-ops/s", "frac": achieved / peak, "traffic": traffic.get("k_blend"),
+                    "unit": "T FP32-lane-ops/s", "frac": achieved / peak, "traffic": lookup_traffic(traffic, "k_blend<0"),
                     "peak_source": f"148 SMs x 128 FP32 lanes x {f_mhz:.0f} MHz (sampled SM clock)",
                     "work": {"evaluated_pairs": ev_pairs, "composited_pairs": cp_pairs}}
         else:
@@ -378,7 +387,7 @@ def main():
             kname = {"sort": "k_onesweep", "apply": "k_decode_apply", "project": "k_project", "scan": "k_scan_tiles",
                      "duplicate": "k_duplicate", "hist": "k_hist", "ranges": "k_ranges"}[dom]
             roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": traffic.get(kname), "peak_source": f"hbm_gbs ({peak_src})",
+                    "frac": achieved / peak, "traffic": lookup_traffic(traffic, kname), "peak_source": f"hbm_gbs ({peak_src})",
                     "algorithmic_bytes_per_launch": b}
         for name, s in stages.items():
             b = algorithmic_bytes(name, cfg, sc.n, vpb_list, K_list, k_coo)
