@@ -301,17 +301,17 @@ def main():
     player.fit_capacity()
     for t in range(1, args.warmup):
         step(t)
-    st, info = player.ctx.check_status()
+    st, info = player.check_status()
     if st < 0:
-        print(json.dumps({"error": f"libqueen status {st}: {player.ctx.last_error()} info={info}"}))
+        print(json.dumps({"error": f"libqueen status {st}: {player.last_error()} info={info}"}))
         return 3
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if not args.no_profile:
-        player.ctx.profile(True)
-        player.ctx.profile_read(reset=True)
+        player.profile(True)
+        player.profile_read(reset=True)
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
@@ -327,9 +327,9 @@ def main():
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
-    prof = player.ctx.profile_read(reset=True) if not args.no_profile else {}
-    player.ctx.profile(False)
-    st, info = player.ctx.check_status()
+    prof = player.profile_read(reset=True) if not args.no_profile else {}
+    player.profile(False)
+    st, info = player.check_status()
     tot = torch.tensor([sum(step_ms), statistics.median(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -475,7 +475,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": f"{cfg.name}: BASELINE configs[{cfg.index}] ({cfg.n} Gaussians, {V} views "
                                    f"{W}x{H}, SH {cfg.deg}, latents {tuple(cfg.lat)}, {cfg.rho:.0%} gates)",
-                       "gaussians": cfg.n, "views": V, "width": W, "height": H, "views_per_batch": vpb,
+                       "gaussians": cfg.n, "views": V, "width": W, "height": H, "views_per_batch": player.vpb, "render_lanes": player.n_lanes,
                        "parallelism": f"views sharded v mod {world}, Gaussians replicated, packet NCCL-broadcast",
                        "l2": "flushed between timed steps (512 MB write outside the step events)"},
             "mpixel_per_s": mpix, "view_fps": value * V,

@@ -202,6 +202,12 @@ queen_status queen_blend_counts(queen_ctx* ctx, const queen_proj* proj, const qu
                                 const queen_camera* cams, int32_t n_views, int64_t* evaluated, int64_t* composited,
                                 void* stream);
 
+/* Makes `stream` wait until the binning (project + bin_sort) of the most recent
+ * queen_render_views call on `ctx` has completed -- lets a renderer with several contexts
+ * pipeline one batch's binning (memory/latency bound) under another batch's blend (ALU
+ * bound).  Capturable; no host sync. */
+queen_status queen_wait_binned(const queen_ctx* ctx, void* stream);
+
 /* Stage profiler (evidence for bench.py): when enabled, every call records CUDA events
  * on its stream around each stage: 0 apply, 1 project, 2 scan (+resets), 3 duplicate,
  * 4 histogram, 5 sort (all onesweep passes), 6 ranges, 7 blend.  queen_profile_read

@@ -28,7 +28,7 @@ QUEEN_MAX_VIEWS = 64
 EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version", "queen_workspace_size",
            "queen_set_workspace", "queen_check", "queen_decode_residuals", "queen_apply_frame", "queen_project",
            "queen_bin_sort", "queen_rasterize", "queen_render_views", "queen_blend_counts",
-           "queen_profile_enable", "queen_profile_read"]
+           "queen_profile_enable", "queen_profile_read", "queen_wait_binned"]
 STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend"]
 
 
@@ -101,6 +101,7 @@ def lib() -> C.CDLL:
             "queen_blend_counts": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
                                          p, p, p]),
             "queen_profile_enable": (i32, [p, i32]),
+            "queen_wait_binned": (i32, [p, p]),
             "queen_profile_read": (i32, [p, C.POINTER(C.c_double), C.POINTER(C.c_int64), i32]),
         }
         for name, (res, args) in sig.items():
@@ -297,6 +298,11 @@ def queen_render_views(ctx: Context, scene: QueenGaussians, cams, rgb_out, T_out
     st = lib().queen_render_views(ctx.handle, C.byref(scene), arr, len(arr), bgv, _ptr(rgb_out), _ptr(T_out),
                                   C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_render_views")
+
+
+def queen_wait_binned(ctx: Context, stream=None):
+    st = lib().queen_wait_binned(ctx.handle, C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_wait_binned")
 
 
 def queen_blend_counts(ctx: Context, proj: QueenProj, bins: QueenBins, cams, evaluated, composited, stream=None):

@@ -16,6 +16,7 @@ struct queen_ctx {
     int64_t ws_keys = 0;
     queen::WsLayout L{};
     queen::Prof prof;
+    cudaEvent_t binned = nullptr;  // recorded by queen_render_views after binning (queen_wait_binned)
     std::string err;
 };
 
@@ -51,11 +52,26 @@ queen_status queen_create(int device, queen_ctx** out) {
     if ((e = init_binning_attributes()) != cudaSuccess) return QUEEN_ERR_CUDA;
     queen_ctx* c = new queen_ctx();
     c->device = device;
+    if (cudaEventCreateWithFlags(&c->binned, cudaEventDisableTiming) != cudaSuccess) {
+        delete c;
+        return QUEEN_ERR_CUDA;
+    }
     *out = c;
     return QUEEN_OK;
 }
 
-void queen_destroy(queen_ctx* ctx) { delete ctx; }
+void queen_destroy(queen_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->binned) cudaEventDestroy(ctx->binned);
+    for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
+    delete ctx;
+}
+
+queen_status queen_wait_binned(const queen_ctx* ctx, void* stream) {
+    if (!ctx) return QUEEN_ERR_INVALID_ARG;
+    return cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->binned, 0) == cudaSuccess ? QUEEN_OK
+                                                                                                 : QUEEN_ERR_CUDA;
+}
 
 const char* queen_last_error(const queen_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
 
@@ -322,6 +338,8 @@ queen_status queen_render_views(queen_ctx* ctx, const queen_gaussians* scene, co
     b.sorted_in_alt = 0;
     if (queen_status st = queen_project(ctx, scene, cams, n_views, &pj, stream)) return st;
     if (queen_status st = queen_bin_sort(ctx, &pj, cams, n_views, &b, stream)) return st;
+    if (cudaEventRecord(ctx->binned, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return cuda_fail(ctx, cudaGetLastError(), "record binned event");
     return queen_rasterize(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, stream);
 }
 

@@ -303,7 +303,7 @@ def test_full_size_frame_sampled(name):
     assert np.array_equal(pl.planes.cpu().numpy(), A1)
     pl.fit_capacity()
     rgb = pl.render().cpu().numpy()
-    s, _ = pl.ctx.check_status()
+    s, _ = pl.check_status()
     assert s == 0
     W, H = cams[0].width, cams[0].height
     rng = np.random.default_rng(5)
