@@ -208,7 +208,7 @@ __device__ __forceinline__ uint32_t block_excl_scan_t(uint32_t x, uint32_t* s_w,
 // onesweep configuration: NT threads x IT keys per thread = one 4096-key tile
 template <int BITS>
 struct Onesweep {
-    static constexpr int NT = 512, IT = 8, NW = NT / 32;
+    static constexpr int NT = OS_THREADS, IT = OS_ITEMS, NW = NT / 32;
     static constexpr int TILE = NT * IT;
     static constexpr int BINS = 1 << BITS;
     static constexpr int DPT = BINS >= NT ? BINS / NT : 1;  // digits per thread (threads >= BINS idle)
@@ -631,7 +631,8 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     uint32_t* dk[2] = {reinterpret_cast<uint32_t*>(ws + L.dkeys), reinterpret_cast<uint32_t*>(ws + L.dkeys_alt)};
     uint32_t* dv[2] = {reinterpret_cast<uint32_t*>(ws + L.dvals), reinterpret_cast<uint32_t*>(ws + L.dvals_alt)};
     const int64_t elem_tiles = (count + SORT_TILE - 1) / SORT_TILE;
-    const int64_t key_tiles = ((int64_t)cap + SORT_TILE - 1) / SORT_TILE;
+    const int64_t os_elem_tiles = (count + OS_TILE - 1) / OS_TILE;
+    const int64_t os_key_tiles = ((int64_t)cap + OS_TILE - 1) / OS_TILE;
     uint32_t* Kd = bins.K;      // [0] = K entries
     uint32_t* Md = bins.K + 1;  // [1] = M visible pairs
     cudaError_t e;
@@ -640,8 +641,8 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     if ((e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS, s))) return e;
     if ((e = cudaMemsetAsync(vis_lb, 0, sizeof(unsigned long long) * (elem_tiles + 1), s))) return e;
     if ((e = cudaMemsetAsync(dup_lb, 0, sizeof(unsigned long long) * (elem_tiles + 1), s))) return e;
-    if ((e = cudaMemsetAsync(depth_lb, 0, sizeof(uint32_t) * DEPTH_PASSES * 256 * (size_t)(elem_tiles + 1), s))) return e;
-    if ((e = cudaMemsetAsync(tile_lb, 0, sizeof(uint32_t) * (size_t)tpasses * (1 << tbits) * (size_t)(key_tiles + 1), s)))
+    if ((e = cudaMemsetAsync(depth_lb, 0, sizeof(uint32_t) * DEPTH_PASSES * 256 * (size_t)(os_elem_tiles + 1), s))) return e;
+    if ((e = cudaMemsetAsync(tile_lb, 0, sizeof(uint32_t) * (size_t)tpasses * (1 << tbits) * (size_t)(os_key_tiles + 1), s)))
         return e;
     int* diff = reinterpret_cast<int*>(ws + L.diff);
     uint32_t* tcounts = reinterpret_cast<uint32_t*>(ws + L.counts);
@@ -661,7 +662,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     int cur = 0;
     for (int p = 0; p < DEPTH_PASSES; ++p) {
         onesweep<8>(dk[cur], dv[cur], dk[cur ^ 1], dv[cur ^ 1], Md, (uint32_t)count, 8 * p, hist_excl + p * MAX_BINS,
-                    depth_lb + (size_t)p * 256 * (elem_tiles + 1), &fl->tickets[TK_DEPTH + p], fl, s);
+                    depth_lb + (size_t)p * 256 * (os_elem_tiles + 1), &fl->tickets[TK_DEPTH + p], fl, s);
         cur ^= 1;
     }
     prof->end(s, DEPTH_PASSES + 2);
@@ -690,7 +691,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     uint32_t* va = bins.vals;
     uint32_t* vb = bins.vals_alt;
     for (int p = 0; p < tpasses; ++p) {
-        uint32_t* lbp = tile_lb + (size_t)p * (1 << tbits) * (key_tiles + 1);
+        uint32_t* lbp = tile_lb + (size_t)p * (1 << tbits) * (os_key_tiles + 1);
         if (tbits == 9)
             onesweep<9>(ka, va, kb, vb, Kd, cap, 9 * p, thist_excl + p * MAX_BINS, lbp, &fl->tickets[TK_TILE + p], fl, s);
         else

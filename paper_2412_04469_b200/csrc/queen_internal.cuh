@@ -40,6 +40,8 @@ constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 16;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 constexpr int REC_WORDS = 12;
+constexpr int OS_THREADS = 512, OS_ITEMS = 8;         // onesweep pass CTA shape
+constexpr int OS_TILE = OS_THREADS * OS_ITEMS;         // keys per onesweep tile
 constexpr int64_t MAX_KEYS = (1ll << 30) - 1;  // look-back packs 30-bit counts
 
 struct CamBatch {
@@ -73,7 +75,7 @@ struct WsLayout {
         total_scratch;
     // render_views buffers
     size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, total;
-    int64_t key_tiles, elem_tiles, T, elems;
+    int64_t key_tiles, elem_tiles, os_key_tiles, os_elem_tiles, T, elems;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -85,13 +87,15 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     L.elems = (int64_t)n_pad * n_views;
     L.key_tiles = (keys_cap + SORT_TILE - 1) / SORT_TILE;
     L.elem_tiles = (L.elems + SORT_TILE - 1) / SORT_TILE;
+    L.os_key_tiles = (keys_cap + OS_TILE - 1) / OS_TILE;
+    L.os_elem_tiles = (L.elems + OS_TILE - 1) / OS_TILE;
     size_t o = 0;
     L.flags = o; o += align256(sizeof(DevFlags));
     L.hist = o; o += align256(sizeof(uint32_t) * (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS * 2);
     L.vis_lb = o; o += align256(sizeof(unsigned long long) * (L.elem_tiles + 1));
     L.dup_lb = o; o += align256(sizeof(unsigned long long) * (L.elem_tiles + 1));
-    L.depth_lb = o; o += align256(sizeof(uint32_t) * DEPTH_PASSES * 256 * (L.elem_tiles + 1));
-    L.tile_lb = o; o += align256(sizeof(uint32_t) * MAX_TILE_PASSES * MAX_BINS * (L.key_tiles + 1));
+    L.depth_lb = o; o += align256(sizeof(uint32_t) * DEPTH_PASSES * 256 * (L.os_elem_tiles + 1));
+    L.tile_lb = o; o += align256(sizeof(uint32_t) * MAX_TILE_PASSES * MAX_BINS * (L.os_key_tiles + 1));
     L.dkeys = o; o += align256(sizeof(uint32_t) * L.elems);
     L.dkeys_alt = o; o += align256(sizeof(uint32_t) * L.elems);
     L.dvals = o; o += align256(sizeof(uint32_t) * L.elems);
