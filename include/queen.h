@@ -202,6 +202,19 @@ queen_status queen_blend_counts(queen_ctx* ctx, const queen_proj* proj, const qu
                                 const queen_camera* cams, int32_t n_views, int64_t* evaluated, int64_t* composited,
                                 void* stream);
 
+/* ---- NEXT #1: entropy-coded latents ----------
+ * queen_entropy_encode (HOST, producer side): codes one category's latent matrix
+ *   latents[L][n_pad] int8 (host memory; columns >= n ignored), flattened row-major,
+ *   into the chunked 32-way interleaved rANS "QANS" stream written to `out` (host, capacity
+ *   bytes).  *bytes = stream size; QUEEN_ERR_SHAPE if capacity is too small (nothing written).
+ * queen_entropy_decode (DEVICE): decodes such a stream (device memory) back into
+ *   latents_out[L][n_pad] int8 (device; columns >= n untouched), one warp per 16384-symbol
+ *   chunk.  A corrupt stream or one that does not match (L, n) sets QUEEN_ERR_INDEX. */
+queen_status queen_entropy_encode(const int8_t* latents, int32_t L, int32_t n, int32_t n_pad, void* out,
+                                  size_t capacity, size_t* bytes);
+queen_status queen_entropy_decode(queen_ctx* ctx, const void* stream_dev, int32_t L, int32_t n, int32_t n_pad,
+                                  int8_t* latents_out, void* stream);
+
 /* Makes `stream` wait until the binning (project + bin_sort) of the most recent
  * queen_render_views call on `ctx` has completed -- lets a renderer with several contexts
  * pipeline one batch's binning (memory/latency bound) under another batch's blend (ALU
@@ -209,10 +222,10 @@ queen_status queen_blend_counts(queen_ctx* ctx, const queen_proj* proj, const qu
 queen_status queen_wait_binned(const queen_ctx* ctx, void* stream);
 
 /* Stage profiler (evidence for bench.py): when enabled, every call records CUDA events
- * on its stream around each stage: 0 apply, 1 project, 2 scan (+resets), 3 duplicate,
- * 4 histogram, 5 sort (all onesweep passes), 6 ranges, 7 blend.  queen_profile_read
+ * on its stream around each stage: 0 apply, 1 project, 2 compact (+resets), 3 depth sort,
+ * 4 duplicate, 5 tile sort, 6 ranges, 7 blend, 8 entropy decode.  queen_profile_read
  * waits for the recorded events and returns per-stage summed milliseconds and kernel
- * launches (double[8], int64[8]), optionally resetting them.  Not capturable. */
+ * launches (double[9], int64[9]), optionally resetting them.  Not capturable. */
 queen_status queen_profile_enable(queen_ctx* ctx, int32_t enable);
 queen_status queen_profile_read(queen_ctx* ctx, double* ms, int64_t* launches, int32_t reset);
 

@@ -54,6 +54,8 @@ def lib():
             "oracle_rasterize": (None, [i32, i32, i32, i32, p, p, p, p, p, p, i32]),
             "oracle_rasterize_bruteforce": (None, [i32, i32, i32, i32, i32, p, p, p, p, p, i32]),
             "oracle_rasterize_pixels": (None, [i32, i32, i32, p, p, p, p, i64, p, p, p, i32]),
+            "oracle_ans_encode": (i64, [p, i32, i32, i32, p, i64]),
+            "oracle_ans_decode": (i32, [p, i64, i32, i32, i32, p]),
             "oracle_blend_counts": (None, [i32, i32, i32, i32, p, p, p, p, p, i32]),
         }
         for name, (res, args) in sig.items():
@@ -146,6 +148,26 @@ def apply(planes: np.ndarray, pkt, *, use_gates: bool = False, use_f32_latents: 
     if bad:
         st = -4 if st == 0 else st
     return out, st, q
+
+
+# ---------------------------------------------------------------- entropy coding (NEXT #1)
+def ans_encode(latents: np.ndarray, n: int) -> np.ndarray:
+    """Reference QANS encoder of one category's int8 latent matrix [L][n_pad]."""
+    lat = np.ascontiguousarray(latents, np.int8)
+    L, n_pad = lat.shape
+    need = lib().oracle_ans_encode(_p(lat), L, n, n_pad, None, 0)
+    out = np.zeros(max(int(need), 1), np.uint8)
+    got = lib().oracle_ans_encode(_p(lat), L, n, n_pad, _p(out), int(need))
+    assert got == need
+    return out[:need]
+
+
+def ans_decode(stream: np.ndarray, L: int, n: int, n_pad: int):
+    """Reference QANS decoder -> (int8 [L][n_pad], status 0 / -3)."""
+    s = np.ascontiguousarray(stream, np.uint8)
+    lat = np.zeros((max(L, 1), n_pad), np.int8)
+    st = lib().oracle_ans_decode(_p(s), s.size, L, n, n_pad, _p(lat))
+    return lat[:L], int(st)
 
 
 # ---------------------------------------------------------------- render

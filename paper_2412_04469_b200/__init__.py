@@ -28,8 +28,9 @@ QUEEN_MAX_VIEWS = 64
 EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version", "queen_workspace_size",
            "queen_set_workspace", "queen_check", "queen_decode_residuals", "queen_apply_frame", "queen_project",
            "queen_bin_sort", "queen_rasterize", "queen_render_views", "queen_blend_counts",
-           "queen_profile_enable", "queen_profile_read", "queen_wait_binned"]
-STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend"]
+           "queen_profile_enable", "queen_profile_read", "queen_wait_binned", "queen_entropy_encode",
+           "queen_entropy_decode"]
+STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy"]
 
 
 class QueenError(RuntimeError):
@@ -102,6 +103,8 @@ def lib() -> C.CDLL:
                                          p, p, p]),
             "queen_profile_enable": (i32, [p, i32]),
             "queen_wait_binned": (i32, [p, p]),
+            "queen_entropy_encode": (i32, [p, i32, i32, i32, p, C.c_size_t, C.POINTER(C.c_size_t)]),
+            "queen_entropy_decode": (i32, [p, p, i32, i32, i32, p, p]),
             "queen_profile_read": (i32, [p, C.POINTER(C.c_double), C.POINTER(C.c_int64), i32]),
         }
         for name, (res, args) in sig.items():
@@ -206,10 +209,10 @@ class Context:
         self._chk(lib().queen_profile_enable(self._h, 1 if enable else 0), "queen_profile_enable")
 
     def profile_read(self, reset: bool = True) -> dict:
-        ms = (C.c_double * 8)()
-        ln = (C.c_int64 * 8)()
+        ms = (C.c_double * len(STAGES))()
+        ln = (C.c_int64 * len(STAGES))()
         self._chk(lib().queen_profile_read(self._h, ms, ln, 1 if reset else 0), "queen_profile_read")
-        return {STAGES[i]: (float(ms[i]), int(ln[i])) for i in range(8)}
+        return {STAGES[i]: (float(ms[i]), int(ln[i])) for i in range(len(STAGES))}
 
     def __del__(self):
         try:
@@ -298,6 +301,26 @@ def queen_render_views(ctx: Context, scene: QueenGaussians, cams, rgb_out, T_out
     st = lib().queen_render_views(ctx.handle, C.byref(scene), arr, len(arr), bgv, _ptr(rgb_out), _ptr(T_out),
                                   C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_render_views")
+
+
+def queen_entropy_encode(latents: np.ndarray, n: int) -> np.ndarray:
+    """Host rANS encode of one category's int8 latent matrix [L][n_pad] -> uint8 QANS stream."""
+    lat = np.ascontiguousarray(latents, np.int8)
+    L, n_pad = lat.shape
+    nb = C.c_size_t(0)
+    cap = 2 * L * max(n, 1) + 64 * 1024 + 160 * (L * n // 16384 + 2)
+    out = np.zeros(cap, np.uint8)
+    st = lib().queen_entropy_encode(lat.ctypes.data_as(C.c_void_p), L, n, n_pad, out.ctypes.data_as(C.c_void_p), cap,
+                                    C.byref(nb))
+    if st != QUEEN_OK:
+        raise QueenError(st, f"queen_entropy_encode (needs {nb.value} bytes)")
+    return out[: nb.value].copy()
+
+
+def queen_entropy_decode(ctx: Context, stream_dev, L: int, n: int, latents_out, stream=None):
+    st = lib().queen_entropy_decode(ctx.handle, _ptr(stream_dev), L, n, latents_out.shape[-1], _ptr(latents_out),
+                                    C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_entropy_decode")
 
 
 def queen_wait_binned(ctx: Context, stream=None):

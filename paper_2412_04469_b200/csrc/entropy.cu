@@ -1,0 +1,197 @@
+// NEXT #1: entropy coding of the integer latents (PAPER.md:1386-1387:
+// "flattens our integer latent matrix for each attribute ... encoded using standard entropy
+// coding approaches such as arithmetic coding").  The paper's coder is a single sequential
+// arithmetic stream; to decode on the GPU we use the same kind of coder (an order-0
+// static-model range/ANS coder) cut into independently decodable chunks and 32-way
+// interleaved inside each chunk, so one warp decodes a chunk with one rANS state per lane.
+//
+// Stream format ("QANS"), all little-endian:
+//   u32 magic 'QANS' | u32 n_sym | u32 n_chunks | u32 reserved
+//   u16 freq[256]                    normalised to sum 4096 (PROB_BITS = 12); symbol = latent + 128
+//   u32 word_off[n_chunks + 1]       chunk word offsets into words[]
+//   u32 state[n_chunks][32]          initial decoder state of each lane
+//   u16 words[]                      renormalisation words in decoding order (padded to 4 bytes)
+// Symbols are the category's latent matrix flattened row-major (k * n + i, k < L, i < n);
+// chunk j holds symbols [j*CH, (j+1)*CH), CH = 16384; lane l of chunk j decodes symbols
+// j*CH + 32 t + l for t = 0, 1, ...  rANS: 32-bit state in [2^16, 2^32), 16-bit renormalisation.
+#include <cstring>
+#include <vector>
+
+#include "queen_internal.cuh"
+
+namespace queen {
+
+constexpr uint32_t ANS_MAGIC = 0x534e4151u;  // 'QANS'
+constexpr int ANS_PROB_BITS = 12;
+constexpr uint32_t ANS_M = 1u << ANS_PROB_BITS;
+constexpr uint32_t ANS_L = 1u << 16;
+constexpr int ANS_LANES = 32;
+constexpr int ANS_CHUNK = 32 * 512;
+
+struct AnsHeader {
+    uint32_t magic, n_sym, n_chunks, reserved;
+    uint16_t freq[256];
+};
+static_assert(sizeof(AnsHeader) == 528, "AnsHeader layout");
+
+// deterministic normalisation of the symbol counts to a table summing to ANS_M
+static void normalise(const uint64_t cnt[256], uint64_t total, uint16_t f[256]) {
+    int64_t sum = 0;
+    int best = -1;
+    for (int s = 0; s < 256; ++s) {
+        f[s] = 0;
+        if (!cnt[s]) continue;
+        uint64_t v = cnt[s] * ANS_M / total;
+        if (v == 0) v = 1;
+        f[s] = (uint16_t)v;
+        sum += (int64_t)v;
+        if (best < 0 || cnt[s] > cnt[best]) best = s;
+    }
+    if (best < 0) return;
+    if (sum <= (int64_t)ANS_M) {
+        f[best] = (uint16_t)((int64_t)f[best] + ((int64_t)ANS_M - sum));
+        return;
+    }
+    while (sum > (int64_t)ANS_M) {  // too many rare symbols bumped to 1: take from the largest
+        int m = -1;
+        for (int s = 0; s < 256; ++s)
+            if (f[s] > 1 && (m < 0 || f[s] > f[m])) m = s;
+        --f[m];
+        --sum;
+    }
+}
+
+// ---------------------------------------------------------------- device decoder
+// One warp per chunk; the category's tables live in shared memory.
+constexpr int ANS_WARPS = 4;
+
+__global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const unsigned char* __restrict__ stream, int L, int n,
+                                                               int n_pad, int8_t* __restrict__ out, DevFlags* fl) {
+    __shared__ uint8_t s_sym[ANS_M];
+    __shared__ uint16_t s_f[256], s_c[256];
+    const AnsHeader* h = reinterpret_cast<const AnsHeader*>(stream);
+    const uint32_t n_sym = h->n_sym, n_chunks = h->n_chunks;
+    if (threadIdx.x == 0 && (h->magic != ANS_MAGIC || n_sym != (uint32_t)L * (uint32_t)n)) raise_flag(fl, FLAG_INDEX);
+    for (int s = threadIdx.x; s < 256; s += blockDim.x) s_f[s] = h->freq[s];
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the 256 frequencies by one warp
+        uint32_t v[8], sum = 0;
+        for (int q = 0; q < 8; ++q) { v[q] = s_f[threadIdx.x * 8 + q]; sum += v[q]; }
+        uint32_t inc = sum;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (threadIdx.x >= o) inc += y;
+        }
+        uint32_t run = inc - sum;
+        for (int q = 0; q < 8; ++q) { s_c[threadIdx.x * 8 + q] = (uint16_t)run; run += v[q]; }
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < 256; s += blockDim.x)
+        for (uint32_t k = s_c[s]; k < (uint32_t)s_c[s] + s_f[s] && k < ANS_M; ++k) s_sym[k] = (uint8_t)s;
+    __syncthreads();
+    const uint32_t chunk = blockIdx.x * ANS_WARPS + (threadIdx.x >> 5);
+    if (chunk >= n_chunks) return;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t* woff = reinterpret_cast<const uint32_t*>(stream + sizeof(AnsHeader));
+    const uint32_t* states = woff + n_chunks + 1;
+    const uint16_t* words = reinterpret_cast<const uint16_t*>(states + (size_t)n_chunks * ANS_LANES);
+    uint32_t x = states[(size_t)chunk * ANS_LANES + lane];
+    uint32_t ptr = woff[chunk];
+    const uint32_t end = woff[chunk + 1];
+    const uint32_t base = chunk * ANS_CHUNK;
+    const uint32_t len = min((uint32_t)ANS_CHUNK, n_sym - base);
+    const uint32_t steps = (len + 31) / 32;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t k = (base + lane) / (uint32_t)n, i = (base + lane) - k * (uint32_t)n;
+    for (uint32_t t = 0; t < steps; ++t) {
+        const bool active = t * 32 + lane < len;
+        if (active) {
+            const uint32_t slot = x & (ANS_M - 1);
+            const uint32_t s = s_sym[slot];
+            x = (uint32_t)s_f[s] * (x >> ANS_PROB_BITS) + slot - s_c[s];
+            out[(size_t)k * n_pad + i] = (int8_t)((int)s - 128);
+        }
+        const bool need = active && x < ANS_L;
+        const uint32_t m = __ballot_sync(0xffffffffu, need);
+        if (need) {
+            const uint32_t wp = ptr + __popc(m & lt);
+            x = (x << 16) | (wp < end ? (uint32_t)words[wp] : 0u);
+        }
+        ptr += __popc(m);
+        i += 32;  // next symbol of this lane: flat index + 32
+        while (i >= (uint32_t)n) { i -= (uint32_t)n; ++k; }
+    }
+    if (ptr != end || x != ANS_L) raise_flag(fl, FLAG_INDEX);  // corrupt / mismatched stream
+}
+
+cudaError_t launch_ans_decode(const void* stream_dev, int L, int n, int n_pad, int8_t* out, DevFlags* fl,
+                              cudaStream_t s) {
+    const int64_t n_chunks = ((int64_t)L * n + ANS_CHUNK - 1) / ANS_CHUNK;
+    if (n_chunks == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((n_chunks + ANS_WARPS - 1) / ANS_WARPS);
+    k_ans_decode<<<blocks, ANS_WARPS * 32, 0, s>>>(static_cast<const unsigned char*>(stream_dev), L, n, n_pad, out, fl);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- host encoder
+// Produces exactly the stream the decoder consumes: per chunk, the symbols are encoded in
+// the reverse of decoding order (t descending, lane descending); the words emitted by the
+// pre-encode renormalisations are reversed at the end so the decoder reads them forward.
+size_t ans_encode(const int8_t* lat, int L, int n, int n_pad, std::vector<unsigned char>& out) {
+    const uint64_t n_sym = (uint64_t)L * (uint64_t)n;
+    const uint32_t n_chunks = (uint32_t)((n_sym + ANS_CHUNK - 1) / ANS_CHUNK);
+    AnsHeader h{};
+    h.magic = ANS_MAGIC;
+    h.n_sym = (uint32_t)n_sym;
+    h.n_chunks = n_chunks;
+    uint64_t cnt[256] = {0};
+    for (int k = 0; k < L; ++k)
+        for (int i = 0; i < n; ++i) ++cnt[(uint8_t)((int)lat[(size_t)k * n_pad + i] + 128)];
+    normalise(cnt, n_sym ? n_sym : 1, h.freq);
+    uint32_t cum[257];
+    cum[0] = 0;
+    for (int s = 0; s < 256; ++s) cum[s + 1] = cum[s] + h.freq[s];
+    std::vector<uint32_t> woff(n_chunks + 1, 0), states((size_t)n_chunks * ANS_LANES, ANS_L);
+    std::vector<uint16_t> words;
+    std::vector<uint16_t> rev;
+    for (uint32_t c = 0; c < n_chunks; ++c) {
+        const uint64_t base = (uint64_t)c * ANS_CHUNK;
+        const uint32_t len = (uint32_t)std::min<uint64_t>(ANS_CHUNK, n_sym - base);
+        const uint32_t steps = (len + 31) / 32;
+        uint32_t x[ANS_LANES];
+        for (int l = 0; l < ANS_LANES; ++l) x[l] = ANS_L;
+        rev.clear();
+        for (int64_t t = (int64_t)steps - 1; t >= 0; --t)
+            for (int l = ANS_LANES - 1; l >= 0; --l) {
+                const uint64_t p = (uint64_t)t * 32 + l;
+                if (p >= len) continue;
+                const uint64_t flat = base + p;
+                const int k = (int)(flat / (uint64_t)n), i = (int)(flat % (uint64_t)n);
+                const uint32_t s = (uint8_t)((int)lat[(size_t)k * n_pad + i] + 128);
+                const uint32_t f = h.freq[s];
+                const uint64_t xmax = (uint64_t)((ANS_L >> ANS_PROB_BITS) << 16) * f;  // f = 4096 -> 2^32
+                if ((uint64_t)x[l] >= xmax) {
+                    rev.push_back((uint16_t)(x[l] & 0xffffu));
+                    x[l] >>= 16;
+                }
+                x[l] = ((x[l] / f) << ANS_PROB_BITS) + (x[l] % f) + cum[s];
+            }
+        woff[c] = (uint32_t)words.size();
+        for (size_t q = rev.size(); q-- > 0;) words.push_back(rev[q]);
+        for (int l = 0; l < ANS_LANES; ++l) states[(size_t)c * ANS_LANES + l] = x[l];
+    }
+    woff[n_chunks] = (uint32_t)words.size();
+    const size_t bytes = sizeof(AnsHeader) + 4 * woff.size() + 4 * states.size() + ((2 * words.size() + 3) & ~size_t(3));
+    out.assign(bytes, 0);
+    unsigned char* o = out.data();
+    std::memcpy(o, &h, sizeof(h));
+    o += sizeof(h);
+    std::memcpy(o, woff.data(), 4 * woff.size());
+    o += 4 * woff.size();
+    std::memcpy(o, states.data(), 4 * states.size());
+    o += 4 * states.size();
+    if (!words.empty()) std::memcpy(o, words.data(), 2 * words.size());
+    return bytes;
+}
+
+}  // namespace queen

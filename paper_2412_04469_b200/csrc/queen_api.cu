@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "queen_internal.cuh"
 
@@ -27,6 +28,9 @@ float host_theta0(float tau, float g0, float g1) {
 }
 cudaError_t init_binning_attributes();
 int key_passes(int64_t gtiles);
+size_t ans_encode(const int8_t* lat, int L, int n, int n_pad, std::vector<unsigned char>& out);
+cudaError_t launch_ans_decode(const void* stream_dev, int L, int n, int n_pad, int8_t* out, DevFlags* fl,
+                              cudaStream_t s);
 }  // namespace queen
 
 using namespace queen;
@@ -309,6 +313,28 @@ queen_status queen_profile_read(queen_ctx* ctx, double* ms, int64_t* launches, i
         launches[i] = P.launches[i];
         if (reset) { P.ms[i] = 0; P.launches[i] = 0; }
     }
+    return QUEEN_OK;
+}
+
+queen_status queen_entropy_encode(const int8_t* latents, int32_t L, int32_t n, int32_t n_pad, void* out,
+                                  size_t capacity, size_t* bytes) {
+    if (!latents || !bytes || L < 0 || L > 16 || n < 0 || n > n_pad) return QUEEN_ERR_INVALID_ARG;
+    std::vector<unsigned char> buf;
+    const size_t need = ans_encode(latents, L, n, n_pad, buf);
+    *bytes = need;
+    if (!out || capacity < need) return QUEEN_ERR_SHAPE;
+    std::memcpy(out, buf.data(), need);
+    return QUEEN_OK;
+}
+
+queen_status queen_entropy_decode(queen_ctx* ctx, const void* stream_dev, int32_t L, int32_t n, int32_t n_pad,
+                                  int8_t* latents_out, void* stream) {
+    if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
+    if (!stream_dev || !latents_out || L < 0 || L > 16 || n < 0 || n > n_pad) return fail(ctx, QUEEN_ERR_INVALID_ARG, "entropy decode args");
+    ctx->prof.begin(ST_ENTROPY, static_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_ans_decode(stream_dev, L, n, n_pad, latents_out, flags_of(ctx), static_cast<cudaStream_t>(stream));
+    ctx->prof.end(static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "entropy decode");
     return QUEEN_OK;
 }
 

@@ -167,7 +167,7 @@ __device__ __forceinline__ void raise_flag(DevFlags* fl, uint32_t bit) { atomicO
 
 // Stage profiler: CUDA events recorded on the launching stream at stage boundaries
 // (enabled by queen_profile_enable; used by bench.py for per-kernel durations).
-enum Stage { ST_APPLY = 0, ST_PROJECT, ST_COMPACT, ST_DEPTH_SORT, ST_DUPLICATE, ST_TILE_SORT, ST_RANGES, ST_BLEND, ST_COUNT };
+enum Stage { ST_APPLY = 0, ST_PROJECT, ST_COMPACT, ST_DEPTH_SORT, ST_DUPLICATE, ST_TILE_SORT, ST_RANGES, ST_BLEND, ST_ENTROPY, ST_COUNT };
 struct Prof {
     bool on = false;
     std::vector<cudaEvent_t> pool;

@@ -9,8 +9,8 @@ import numpy as np
 import torch
 
 from . import (QUEEN_LAT_F32, QUEEN_LAT_INT8, QUEEN_MAX_VIEWS, QUEEN_POS_COO, QUEEN_POS_GATES, Context,
-               QueenError, camera_array, gaussians_struct, packet_struct, queen_apply_frame, queen_render_views,
-               queen_wait_binned)
+               QueenError, camera_array, gaussians_struct, packet_struct, queen_apply_frame, queen_entropy_decode,
+               queen_render_views, queen_wait_binned)
 from . import packet as wire
 
 
@@ -57,6 +57,38 @@ def wire_packet(buf: torch.Tensor, hdr: dict) -> DevicePacket:
         s.pos_idx = None
         s.pos_val = None
     return DevicePacket(s, [buf])
+
+
+class EntropyPacket:
+    """A device-resident entropy-coded frame packet (packet.py version 2).
+
+    decode(ctx) enqueues the GPU rANS decode of every category (one warp per 16384-symbol
+    chunk) into an int8 latent scratch [sum L][n_pad]; `struct` is the queen_packet that
+    points at that scratch, the decoders and the COO section (k read on the device), so
+    apply = decode(ctx) + queen_apply_frame(struct)."""
+
+    def __init__(self, buf: torch.Tensor, hdr: dict, latents: torch.Tensor | None = None):
+        self.buf, self.hdr = buf, hdr
+        SL = sum(hdr["lat"])
+        self.latents = latents if latents is not None else torch.zeros((max(SL, 1), hdr["n_pad"]), dtype=torch.int8,
+                                                                        device=buf.device)
+        base = buf.data_ptr()
+        self.struct = packet_struct(n=hdr["n"], n_pad=hdr["n_pad"], sh_degree=hdr["deg"], lat_dim=hdr["lat"],
+                                    latents=self.latents, decoders=base + hdr["dec_off"], latent_kind=QUEEN_LAT_INT8,
+                                    pos_kind=QUEEN_POS_COO, k=hdr["k_cap"], k_dev=base + wire.K_WORD * 4,
+                                    pos_idx=base + hdr["idx_off"], pos_val=base + hdr["val_off"])
+        if hdr["k_cap"] == 0:
+            self.struct.pos_idx = None
+            self.struct.pos_val = None
+
+    def decode(self, ctx: Context, stream=None):
+        row = 0
+        for c in range(5):
+            L = self.hdr["lat"][c]
+            if L:
+                queen_entropy_decode(ctx, self.buf.data_ptr() + self.hdr["ans_off"][c], L, self.hdr["n"],
+                                     self.latents[row:row + L], stream)
+            row += L
 
 
 class Player:
@@ -106,7 +138,10 @@ class Player:
         for c in self.ctxs:
             c.set_workspace(self.planes.shape[1], self.vpb, self.W, self.H, self.keys_cap)
 
-    def apply(self, pkt: DevicePacket, stream=None):
+    def apply(self, pkt, stream=None):
+        """A_{t-1} -> A_t: (entropy decode, if the packet is coded) + fused decode/apply."""
+        if isinstance(pkt, EntropyPacket):
+            pkt.decode(self.ctx, stream)
         queen_apply_frame(self.ctx, self.scene, pkt.struct, stream)
 
     def render(self, stream=None, out=None):
