@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--views-per-batch", type=int, default=None)
     ap.add_argument("--packets", type=int, default=8, help="cyclic window of pre-generated frame packets")
+    ap.add_argument("--packet-format", default="entropy", choices=["entropy", "int8"],
+                    help="entropy: rANS-coded latents decoded on the GPU each frame (default); int8: raw latents")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -238,7 +240,7 @@ def main():
 
     import paper_2412_04469_b200 as Q
     from paper_2412_04469_b200 import packet as wire
-    from paper_2412_04469_b200.runtime import Player, wire_packet
+    from paper_2412_04469_b200.runtime import EntropyPacket, Player, wire_packet
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -260,26 +262,47 @@ def main():
     W, H = cfg.width, cfg.height
     vpb = args.views_per_batch or min(len(cams), default_vpb(cfg))
 
-    # frame packets R_1..R_P (wire form), resident in HBM before the timed region
+    # frame packets R_1..R_P (wire form), resident in HBM before the timed region.  Default:
+    # entropy-coded latents (packet v2, the paper's storage form P:1386-1390), decoded on the GPU
+    # inside the step; --packet-format int8 streams raw int8 latents (packet v1).
     P = max(1, args.packets)
+    entropy = args.packet_format == "entropy"
     host_pkts = [synth.make_packet(sc, t) for t in range(1, P + 1)] if rank == 0 else None
     k_cap = max(p.k for p in host_pkts) if rank == 0 else 0
+    if entropy and rank == 0:
+        streams = [wire.ans_streams(p, Q.queen_entropy_encode) for p in host_pkts]
+        ans_cap = [max(st[c].size for st in streams) for c in range(5)]
+    else:
+        ans_cap = [0] * 5
     if world > 1:
-        kc = torch.tensor([k_cap], device=dev)
+        kc = torch.tensor([k_cap] + ans_cap, device=dev, dtype=torch.int64)
         dist.broadcast(kc, 0)
-        k_cap = int(kc.item())
-    lay = wire.layout(sc.n_pad, cfg.deg, cfg.lat, k_cap)
-    hdr = dict(n=sc.n, n_pad=sc.n_pad, deg=cfg.deg, lat=tuple(cfg.lat), k_cap=k_cap, **{k: lay[k] for k in
-                                                                                          ("dec_off", "lat_off", "idx_off", "val_off")})
+        k_cap, ans_cap = int(kc[0]), [int(x) for x in kc[1:]]
+    if entropy:
+        lay = wire.layout_entropy(sc.n_pad, cfg.deg, cfg.lat, k_cap, ans_cap)
+    else:
+        lay = wire.layout(sc.n_pad, cfg.deg, cfg.lat, k_cap)
+    hdr = dict(n=sc.n, n_pad=sc.n_pad, deg=cfg.deg, lat=tuple(cfg.lat), k_cap=k_cap,
+               **{k: lay[k] for k in ("dec_off", "lat_off", "idx_off", "val_off")})
+    if entropy:
+        hdr["ans_off"] = lay["ans_off"]
+    used_bytes = []
     if rank == 0:
-        host_bufs = [wire.pack(p, frame=t + 1, k_cap=k_cap) for t, p in enumerate(host_pkts)]
+        if entropy:
+            host_bufs = [wire.pack_entropy(p, st, frame=t + 1, k_cap=k_cap, ans_cap=ans_cap)
+                         for t, (p, st) in enumerate(zip(host_pkts, streams))]
+            used_bytes = [wire.header_entropy(b)["used"] for b in host_bufs]
+        else:
+            host_bufs = [wire.pack(p, frame=t + 1, k_cap=k_cap) for t, p in enumerate(host_pkts)]
+            used_bytes = [b.size for b in host_bufs]
         src_bufs = [torch.from_numpy(b).to(dev) for b in host_bufs]
     nbytes = lay["total"]
     # every rank decodes from its own copy of the frame packet (the broadcast target)
     slots = [torch.zeros(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
     if rank == 0 and world == 1:
         slots = src_bufs  # N=1: the resident packets are used directly (no collective)
-    dps = [wire_packet(s, hdr) for s in slots]
+    mkpkt = (lambda b: EntropyPacket(b, hdr)) if entropy else (lambda b: wire_packet(b, hdr))
+    dps = [mkpkt(s) for s in slots]
 
     player = Player(sc.planes, sc.n, sc.deg, cams, device=local, views_per_batch=vpb)
     stream = torch.cuda.current_stream()
@@ -406,7 +429,7 @@ def main():
         out_dev = [torch.empty_like(player.rgb) for _ in range(2)]
         out_host = [torch.empty(player.rgb.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
         recv = [torch.zeros(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
-        dp_recv = [wire_packet(r, hdr) for r in recv]
+        dp_recv = [mkpkt(r) for r in recv]
         s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
         ev_h2d = [ev() for _ in range(args.steps)]
@@ -428,7 +451,8 @@ def main():
                 if k >= 2:
                     s_h2d.wait_event(ev_apply[k - 2])  # recv[slot] consumed by frame k-2
                 if rank == 0:
-                    recv[slot].copy_(pin_pk[k % P], non_blocking=True)
+                    ub = used_bytes[k % P]  # only the bytes the packet uses cross PCIe
+                    recv[slot][:ub].copy_(pin_pk[k % P][:ub], non_blocking=True)
                 ev_h2d[k].record(s_h2d)
             stream.wait_event(ev_h2d[k])
             if world > 1:
@@ -452,7 +476,7 @@ def main():
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": args.steps / (float(e_ms[0]) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": nbytes if rank == 0 else 0,
+               "h2d_bytes_per_step": int(statistics.mean(used_bytes)) if rank == 0 else 0,
                "d2h_bytes_per_step": int(out_host[0].numel() * 4),
                "note": "runtime.Player public API: pinned H2D of each frame's wire packet + apply + render + "
                        "D2H of this rank's fp32 RGB images, copies on their own streams (double-buffered), "
@@ -477,7 +501,9 @@ def main():
                                    f"{W}x{H}, SH {cfg.deg}, latents {tuple(cfg.lat)}, {cfg.rho:.0%} gates)",
                        "gaussians": cfg.n, "views": V, "width": W, "height": H, "views_per_batch": player.vpb, "render_lanes": player.n_lanes,
                        "parallelism": f"views sharded v mod {world}, Gaussians replicated, packet NCCL-broadcast",
+                       "packet_format": args.packet_format,
                        "l2": "flushed between timed steps (512 MB write outside the step events)"},
+            "packet_bytes_per_frame": int(statistics.mean(used_bytes)) if used_bytes else None,
             "mpixel_per_s": mpix, "view_fps": value * V,
             "status": Q.STATUS.get(st, st),
             "keys_per_batch": K_list, "stages": stages, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

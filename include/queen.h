@@ -208,12 +208,17 @@ queen_status queen_blend_counts(queen_ctx* ctx, const queen_proj* proj, const qu
  *   into the chunked 32-way interleaved rANS "QANS" stream written to `out` (host, capacity
  *   bytes).  *bytes = stream size; QUEEN_ERR_SHAPE if capacity is too small (nothing written).
  * queen_entropy_decode (DEVICE): decodes such a stream (device memory) back into
- *   latents_out[L][n_pad] int8 (device; columns >= n untouched), one warp per 16384-symbol
+ *   latents_out[L][n_pad] int8 (device; columns >= n untouched), one warp per 8192-symbol
  *   chunk.  A corrupt stream or one that does not match (L, n) sets QUEEN_ERR_INDEX. */
 queen_status queen_entropy_encode(const int8_t* latents, int32_t L, int32_t n, int32_t n_pad, void* out,
                                   size_t capacity, size_t* bytes);
 queen_status queen_entropy_decode(queen_ctx* ctx, const void* stream_dev, int32_t L, int32_t n, int32_t n_pad,
                                   int8_t* latents_out, void* stream);
+/* queen_entropy_decode_frame: all five categories of a frame in ONE launch.  streams_dev
+ * (HOST array of 5 device pointers, NULL where lat_dim[c] = 0), lat_dim[5] (host); output
+ * latents_out[sum L][n_pad] int8 in category-major row order (the queen_packet layout). */
+queen_status queen_entropy_decode_frame(queen_ctx* ctx, const void* const* streams_dev, const int32_t* lat_dim,
+                                        int32_t n, int32_t n_pad, int8_t* latents_out, void* stream);
 
 /* Makes `stream` wait until the binning (project + bin_sort) of the most recent
  * queen_render_views call on `ctx` has completed -- lets a renderer with several contexts

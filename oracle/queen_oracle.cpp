@@ -587,7 +587,7 @@ void oracle_blend_counts(int n_pad, int V, int W, int H, const float* rec, const
 // approaches such as arithmetic coding").  Plain reference codec for the "QANS" stream of
 // order-0 static model, probabilities normalised to 4096,
 // rANS with a 32-bit state in [2^16, 2^32) and 16-bit renormalisation, the flattened
-// matrix (row-major, k*n + i) cut into 16384-symbol chunks, each chunk 32-way interleaved
+// matrix (row-major, k*n + i) cut into 8192-symbol chunks, each chunk 32-way interleaved
 // (symbol p of a chunk belongs to lane p % 32).  Decoding order inside a chunk: for
 // t = 0.. , for lane = 0..31: decode symbol 32 t + lane, then (if the state fell below
 // 2^16) read the next 16-bit word.  Written from that text, independently of csrc/.
@@ -619,7 +619,7 @@ static void oracle_ans_freq(const uint64_t cnt[256], uint64_t total, uint16_t f[
 
 // returns the stream size; writes it to out if out != NULL and cap is large enough
 int64_t oracle_ans_encode(const int8_t* lat, int L, int n, int n_pad, uint8_t* out, int64_t cap) {
-    const int64_t CH = 16384;
+    const int64_t CH = 8192;
     const int64_t nsym = (int64_t)L * n;
     const int64_t nch = (nsym + CH - 1) / CH;
     uint64_t cnt[256] = {0};
@@ -667,7 +667,7 @@ int oracle_ans_decode(const uint8_t* in, int64_t bytes, int L, int n, int n_pad,
     uint32_t hdr[4];
     std::memcpy(hdr, in, 16);
     if (hdr[0] != 0x534e4151u || (int64_t)hdr[1] != (int64_t)L * n) return -3;
-    const int64_t CH = 16384, nsym = hdr[1], nch = hdr[2];
+    const int64_t CH = 8192, nsym = hdr[1], nch = hdr[2];
     if (nch != (nsym + CH - 1) / CH) return -3;
     uint16_t f[256];
     std::memcpy(f, in + 16, 512);

@@ -29,7 +29,7 @@ EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version",
            "queen_set_workspace", "queen_check", "queen_decode_residuals", "queen_apply_frame", "queen_project",
            "queen_bin_sort", "queen_rasterize", "queen_render_views", "queen_blend_counts",
            "queen_profile_enable", "queen_profile_read", "queen_wait_binned", "queen_entropy_encode",
-           "queen_entropy_decode"]
+           "queen_entropy_decode", "queen_entropy_decode_frame"]
 STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy"]
 
 
@@ -105,6 +105,7 @@ def lib() -> C.CDLL:
             "queen_wait_binned": (i32, [p, p]),
             "queen_entropy_encode": (i32, [p, i32, i32, i32, p, C.c_size_t, C.POINTER(C.c_size_t)]),
             "queen_entropy_decode": (i32, [p, p, i32, i32, i32, p, p]),
+            "queen_entropy_decode_frame": (i32, [p, C.POINTER(C.c_void_p), C.POINTER(C.c_int32), i32, i32, p, p]),
             "queen_profile_read": (i32, [p, C.POINTER(C.c_double), C.POINTER(C.c_int64), i32]),
         }
         for name, (res, args) in sig.items():
@@ -321,6 +322,15 @@ def queen_entropy_decode(ctx: Context, stream_dev, L: int, n: int, latents_out, 
     st = lib().queen_entropy_decode(ctx.handle, _ptr(stream_dev), L, n, latents_out.shape[-1], _ptr(latents_out),
                                     C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_entropy_decode")
+
+
+def queen_entropy_decode_frame(ctx: Context, stream_ptrs, lat_dim, n: int, latents_out, stream=None):
+    """Decode every category of a frame in one launch (stream_ptrs: 5 device addresses or None)."""
+    ptrs = (C.c_void_p * 5)(*[C.c_void_p(int(p)) if p else None for p in stream_ptrs])
+    dims = (C.c_int32 * 5)(*[int(x) for x in lat_dim])
+    st = lib().queen_entropy_decode_frame(ctx.handle, ptrs, dims, n, latents_out.shape[-1], _ptr(latents_out),
+                                          C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_entropy_decode_frame")
 
 
 def queen_wait_binned(ctx: Context, stream=None):

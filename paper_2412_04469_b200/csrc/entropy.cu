@@ -12,7 +12,7 @@
 //   u32 state[n_chunks][32]          initial decoder state of each lane
 //   u16 words[]                      renormalisation words in decoding order (padded to 4 bytes)
 // Symbols are the category's latent matrix flattened row-major (k * n + i, k < L, i < n);
-// chunk j holds symbols [j*CH, (j+1)*CH), CH = 16384; lane l of chunk j decodes symbols
+// chunk j holds symbols [j*CH, (j+1)*CH), CH = 8192; lane l of chunk j decodes symbols
 // j*CH + 32 t + l for t = 0, 1, ...  rANS: 32-bit state in [2^16, 2^32), 16-bit renormalisation.
 #include <cstring>
 #include <vector>
@@ -26,7 +26,7 @@ constexpr int ANS_PROB_BITS = 12;
 constexpr uint32_t ANS_M = 1u << ANS_PROB_BITS;
 constexpr uint32_t ANS_L = 1u << 16;
 constexpr int ANS_LANES = 32;
-constexpr int ANS_CHUNK = 32 * 512;
+constexpr int ANS_CHUNK = 32 * 256;  // 8192 symbols: chunk count vs per-chunk state overhead
 
 struct AnsHeader {
     uint32_t magic, n_sym, n_chunks, reserved;
@@ -62,17 +62,30 @@ static void normalise(const uint64_t cnt[256], uint64_t total, uint16_t f[256]) 
 }
 
 // ---------------------------------------------------------------- device decoder
-// One warp per chunk; the category's tables live in shared memory.
+// One launch decodes every category of a frame: block -> (category, 4 chunks), one warp per
+// chunk, one rANS state per lane.  The category's slot -> symbol table is rebuilt per block
+// in shared memory (slot-parallel binary search over the cumulative frequencies).
 constexpr int ANS_WARPS = 4;
 
-__global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const unsigned char* __restrict__ stream, int L, int n,
-                                                               int n_pad, int8_t* __restrict__ out, DevFlags* fl) {
+struct AnsFrame {
+    const unsigned char* stream[5];
+    int L[5];
+    int row0[5];          // first latent row of the category in the [sum L][n_pad] matrix
+    int block0[6];        // first block of each category (prefix), block0[5] = total blocks
+    int n, n_pad;
+};
+
+__global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr, int8_t* __restrict__ out, DevFlags* fl) {
     __shared__ uint8_t s_sym[ANS_M];
-    __shared__ uint16_t s_f[256], s_c[256];
+    __shared__ uint16_t s_f[256], s_c[257];
+    int cat = 0;
+    while (cat < 4 && (int)blockIdx.x >= fr.block0[cat + 1]) ++cat;
+    const unsigned char* stream = fr.stream[cat];
+    const int L = fr.L[cat], n = fr.n, n_pad = fr.n_pad;
     const AnsHeader* h = reinterpret_cast<const AnsHeader*>(stream);
     const uint32_t n_sym = h->n_sym, n_chunks = h->n_chunks;
     if (threadIdx.x == 0 && (h->magic != ANS_MAGIC || n_sym != (uint32_t)L * (uint32_t)n)) raise_flag(fl, FLAG_INDEX);
-    for (int s = threadIdx.x; s < 256; s += blockDim.x) s_f[s] = h->freq[s];
+    for (int q = threadIdx.x; q < 256; q += blockDim.x) s_f[q] = h->freq[q];
     __syncthreads();
     if (threadIdx.x < 32) {  // exclusive scan of the 256 frequencies by one warp
         uint32_t v[8], sum = 0;
@@ -83,18 +96,26 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const unsigned ch
             if (threadIdx.x >= o) inc += y;
         }
         uint32_t run = inc - sum;
-        for (int q = 0; q < 8; ++q) { s_c[threadIdx.x * 8 + q] = (uint16_t)run; run += v[q]; }
+        for (int q = 0; q < 8; ++q) { s_c[threadIdx.x * 8 + q] = (uint16_t)min(run, (uint32_t)0xffff); run += v[q]; }
+        if (threadIdx.x == 31) s_c[256] = (uint16_t)min(run, (uint32_t)0xffff);
     }
     __syncthreads();
-    for (int s = threadIdx.x; s < 256; s += blockDim.x)
-        for (uint32_t k = s_c[s]; k < (uint32_t)s_c[s] + s_f[s] && k < ANS_M; ++k) s_sym[k] = (uint8_t)s;
+    for (uint32_t slot = threadIdx.x; slot < ANS_M; slot += blockDim.x) {  // symbol s with c[s] <= slot < c[s+1]
+        int lo = 0, hi = 256;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_c[mid] <= slot) lo = mid; else hi = mid;
+        }
+        s_sym[slot] = (uint8_t)lo;
+    }
     __syncthreads();
-    const uint32_t chunk = blockIdx.x * ANS_WARPS + (threadIdx.x >> 5);
+    const uint32_t chunk = (blockIdx.x - fr.block0[cat]) * ANS_WARPS + (threadIdx.x >> 5);
     if (chunk >= n_chunks) return;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t* woff = reinterpret_cast<const uint32_t*>(stream + sizeof(AnsHeader));
     const uint32_t* states = woff + n_chunks + 1;
     const uint16_t* words = reinterpret_cast<const uint16_t*>(states + (size_t)n_chunks * ANS_LANES);
+    int8_t* cout = out + (size_t)fr.row0[cat] * n_pad;
     uint32_t x = states[(size_t)chunk * ANS_LANES + lane];
     uint32_t ptr = woff[chunk];
     const uint32_t end = woff[chunk + 1];
@@ -103,34 +124,70 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const unsigned ch
     const uint32_t steps = (len + 31) / 32;
     const uint32_t lt = (1u << lane) - 1u;
     uint32_t k = (base + lane) / (uint32_t)n, i = (base + lane) - k * (uint32_t)n;
+    // The chunk's renormalisation words are consumed in order, ~1 per step for the warp.
+    // Keep a 128-word window in registers (4 words per lane: current 64 + next 64), so a
+    // renormalisation is a shuffle, and the next 64 words load one window ahead.
+    auto ld = [&](uint32_t w) -> uint32_t { return w < end ? (uint32_t)__ldg(words + w) : 0u; };
+    uint32_t wbase = ptr;
+    uint32_t c0 = ld(wbase + lane), c1 = ld(wbase + 32 + lane), n0 = ld(wbase + 64 + lane), n1 = ld(wbase + 96 + lane);
     for (uint32_t t = 0; t < steps; ++t) {
         const bool active = t * 32 + lane < len;
         if (active) {
             const uint32_t slot = x & (ANS_M - 1);
-            const uint32_t s = s_sym[slot];
-            x = (uint32_t)s_f[s] * (x >> ANS_PROB_BITS) + slot - s_c[s];
-            out[(size_t)k * n_pad + i] = (int8_t)((int)s - 128);
+            const uint32_t sy = s_sym[slot];
+            x = (uint32_t)s_f[sy] * (x >> ANS_PROB_BITS) + slot - s_c[sy];
+            cout[(size_t)k * n_pad + i] = (int8_t)((int)sy - 128);
         }
         const bool need = active && x < ANS_L;
         const uint32_t m = __ballot_sync(0xffffffffu, need);
-        if (need) {
-            const uint32_t wp = ptr + __popc(m & lt);
-            x = (x << 16) | (wp < end ? (uint32_t)words[wp] : 0u);
+        if (m) {
+            const uint32_t q = ptr - wbase + __popc(m & lt);  // window position of this lane's word (< 96)
+            const uint32_t src = q & 31u;
+            const uint32_t a0 = __shfl_sync(0xffffffffu, c0, src), a1 = __shfl_sync(0xffffffffu, c1, src);
+            const uint32_t a2 = __shfl_sync(0xffffffffu, n0, src);
+            const uint32_t wv = q < 32 ? a0 : (q < 64 ? a1 : a2);
+            if (need) x = (x << 16) | wv;
+            ptr += __popc(m);
+            if (ptr - wbase >= 64) {  // slide the window by 64 words
+                wbase += 64;
+                c0 = n0;
+                c1 = n1;
+                n0 = ld(wbase + 64 + lane);
+                n1 = ld(wbase + 96 + lane);
+            }
         }
-        ptr += __popc(m);
         i += 32;  // next symbol of this lane: flat index + 32
         while (i >= (uint32_t)n) { i -= (uint32_t)n; ++k; }
     }
     if (ptr != end || x != ANS_L) raise_flag(fl, FLAG_INDEX);  // corrupt / mismatched stream
 }
 
+cudaError_t launch_ans_decode_frame(const void* const streams[5], const int L[5], int n, int n_pad, int8_t* out,
+                                    DevFlags* fl, cudaStream_t s) {
+    AnsFrame fr{};
+    fr.n = n;
+    fr.n_pad = n_pad;
+    int row = 0, blk = 0;
+    for (int c = 0; c < 5; ++c) {
+        fr.stream[c] = static_cast<const unsigned char*>(streams[c]);
+        fr.L[c] = (streams[c] && L[c] > 0) ? L[c] : 0;
+        fr.row0[c] = row;
+        fr.block0[c] = blk;
+        row += L[c] > 0 ? L[c] : 0;
+        const int64_t chunks = ((int64_t)fr.L[c] * n + ANS_CHUNK - 1) / ANS_CHUNK;
+        blk += (int)((chunks + ANS_WARPS - 1) / ANS_WARPS);
+    }
+    fr.block0[5] = blk;
+    if (blk == 0) return cudaSuccess;
+    k_ans_decode<<<blk, ANS_WARPS * 32, 0, s>>>(fr, out, fl);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_ans_decode(const void* stream_dev, int L, int n, int n_pad, int8_t* out, DevFlags* fl,
                               cudaStream_t s) {
-    const int64_t n_chunks = ((int64_t)L * n + ANS_CHUNK - 1) / ANS_CHUNK;
-    if (n_chunks == 0) return cudaSuccess;
-    const unsigned blocks = (unsigned)((n_chunks + ANS_WARPS - 1) / ANS_WARPS);
-    k_ans_decode<<<blocks, ANS_WARPS * 32, 0, s>>>(static_cast<const unsigned char*>(stream_dev), L, n, n_pad, out, fl);
-    return cudaGetLastError();
+    const void* streams[5] = {stream_dev, nullptr, nullptr, nullptr, nullptr};
+    const int Ls[5] = {L, 0, 0, 0, 0};
+    return launch_ans_decode_frame(streams, Ls, n, n_pad, out, fl, s);
 }
 
 // ---------------------------------------------------------------- host encoder

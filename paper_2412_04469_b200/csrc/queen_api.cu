@@ -31,6 +31,8 @@ int key_passes(int64_t gtiles);
 size_t ans_encode(const int8_t* lat, int L, int n, int n_pad, std::vector<unsigned char>& out);
 cudaError_t launch_ans_decode(const void* stream_dev, int L, int n, int n_pad, int8_t* out, DevFlags* fl,
                               cudaStream_t s);
+cudaError_t launch_ans_decode_frame(const void* const streams[5], const int L[5], int n, int n_pad, int8_t* out,
+                                    DevFlags* fl, cudaStream_t s);
 }  // namespace queen
 
 using namespace queen;
@@ -335,6 +337,24 @@ queen_status queen_entropy_decode(queen_ctx* ctx, const void* stream_dev, int32_
     cudaError_t e = launch_ans_decode(stream_dev, L, n, n_pad, latents_out, flags_of(ctx), static_cast<cudaStream_t>(stream));
     ctx->prof.end(static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "entropy decode");
+    return QUEEN_OK;
+}
+
+queen_status queen_entropy_decode_frame(queen_ctx* ctx, const void* const* streams_dev, const int32_t* lat_dim,
+                                        int32_t n, int32_t n_pad, int8_t* latents_out, void* stream) {
+    if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
+    if (!streams_dev || !lat_dim || !latents_out || n < 0 || n > n_pad) return fail(ctx, QUEEN_ERR_INVALID_ARG, "entropy frame args");
+    const void* s5[5];
+    int L5[5];
+    for (int c = 0; c < 5; ++c) {
+        if (lat_dim[c] < 0 || lat_dim[c] > 16 || (lat_dim[c] > 0 && !streams_dev[c])) return fail(ctx, QUEEN_ERR_INVALID_ARG, "entropy frame category");
+        s5[c] = streams_dev[c];
+        L5[c] = lat_dim[c];
+    }
+    ctx->prof.begin(ST_ENTROPY, static_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_ans_decode_frame(s5, L5, n, n_pad, latents_out, flags_of(ctx), static_cast<cudaStream_t>(stream));
+    ctx->prof.end(static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "entropy decode frame");
     return QUEEN_OK;
 }
 

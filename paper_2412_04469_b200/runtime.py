@@ -9,8 +9,8 @@ import numpy as np
 import torch
 
 from . import (QUEEN_LAT_F32, QUEEN_LAT_INT8, QUEEN_MAX_VIEWS, QUEEN_POS_COO, QUEEN_POS_GATES, Context,
-               QueenError, camera_array, gaussians_struct, packet_struct, queen_apply_frame, queen_entropy_decode,
-               queen_render_views, queen_wait_binned)
+               QueenError, camera_array, gaussians_struct, packet_struct, queen_apply_frame,
+               queen_entropy_decode_frame, queen_render_views, queen_wait_binned)
 from . import packet as wire
 
 
@@ -62,7 +62,7 @@ def wire_packet(buf: torch.Tensor, hdr: dict) -> DevicePacket:
 class EntropyPacket:
     """A device-resident entropy-coded frame packet (packet.py version 2).
 
-    decode(ctx) enqueues the GPU rANS decode of every category (one warp per 16384-symbol
+    decode(ctx) enqueues the GPU rANS decode of every category (one warp per 8192-symbol
     chunk) into an int8 latent scratch [sum L][n_pad]; `struct` is the queen_packet that
     points at that scratch, the decoders and the COO section (k read on the device), so
     apply = decode(ctx) + queen_apply_frame(struct)."""
@@ -82,13 +82,9 @@ class EntropyPacket:
             self.struct.pos_val = None
 
     def decode(self, ctx: Context, stream=None):
-        row = 0
-        for c in range(5):
-            L = self.hdr["lat"][c]
-            if L:
-                queen_entropy_decode(ctx, self.buf.data_ptr() + self.hdr["ans_off"][c], L, self.hdr["n"],
-                                     self.latents[row:row + L], stream)
-            row += L
+        base = self.buf.data_ptr()
+        ptrs = [base + self.hdr["ans_off"][c] if self.hdr["lat"][c] else None for c in range(5)]
+        queen_entropy_decode_frame(ctx, ptrs, self.hdr["lat"], self.hdr["n"], self.latents, stream)
 
 
 class Player:

@@ -41,7 +41,7 @@ def test_oracle_roundtrip_and_entropy_bound(L, n, n_pad, beta):
     p = cnt / cnt.sum()
     H = float(-(p * np.log2(p)).sum()) if cnt.sum() else 0.0
     nsym = L * n
-    nch = (nsym + 16383) // 16384
+    nch = (nsym + 8191) // 8192
     overhead_bits = 8 * (528 + 4 * (nch + 1) + 4 * 32 * nch + 4) + 0.01 * nsym + 16 * 32 * nch
     assert 8 * s.size <= nsym * H * 1.01 + overhead_bits
 
