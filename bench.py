@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--packets", type=int, default=8, help="cyclic window of pre-generated frame packets")
     ap.add_argument("--packet-format", default="entropy", choices=["entropy", "int8"],
                     help="entropy: rANS-coded latents decoded on the GPU each frame (default); int8: raw latents")
+    ap.add_argument("--binning", default="onesweep", choices=["bucket", "onesweep"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -304,7 +305,7 @@ def main():
     mkpkt = (lambda b: EntropyPacket(b, hdr)) if entropy else (lambda b: wire_packet(b, hdr))
     dps = [mkpkt(s) for s in slots]
 
-    player = Player(sc.planes, sc.n, sc.deg, cams, device=local, views_per_batch=vpb)
+    player = Player(sc.planes, sc.n, sc.deg, cams, device=local, views_per_batch=vpb, binning=args.binning)
     stream = torch.cuda.current_stream()
 
     def step(t):
@@ -365,7 +366,8 @@ def main():
     from paper_2412_04469_b200.stages import Stages  # explicit-buffer stage runner over the same C-ABI
     K_list, ev_pairs, cp_pairs = [], 0, 0
     for bc in batches:
-        stg = Stages(player.planes.cpu().numpy(), sc.n, sc.deg, bc, keys_cap=player.keys_cap, device=local)
+        stg = Stages(player.planes.cpu().numpy(), sc.n, sc.deg, bc, keys_cap=player.keys_cap, device=local,
+                     binning=args.binning)
         stg.project().bin_sort()
         K_list.append(stg.bins_np()["K"])
         e = torch.zeros(len(bc), dtype=torch.int64, device=dev)
@@ -501,7 +503,7 @@ def main():
                                    f"{W}x{H}, SH {cfg.deg}, latents {tuple(cfg.lat)}, {cfg.rho:.0%} gates)",
                        "gaussians": cfg.n, "views": V, "width": W, "height": H, "views_per_batch": player.vpb, "render_lanes": player.n_lanes,
                        "parallelism": f"views sharded v mod {world}, Gaussians replicated, packet NCCL-broadcast",
-                       "packet_format": args.packet_format,
+                       "packet_format": args.packet_format, "binning": args.binning,
                        "l2": "flushed between timed steps (512 MB write outside the step events)"},
             "packet_bytes_per_frame": int(statistics.mean(used_bytes)) if used_bytes else None,
             "mpixel_per_s": mpix, "view_fps": value * V,

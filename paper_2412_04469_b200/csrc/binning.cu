@@ -574,6 +574,17 @@ __global__ void __launch_bounds__(256) k_ranges_finalize(const uint32_t* __restr
     }
 }
 
+// launchers shared with the BUCKET binning mode (bucket.cu)
+void launch_tile_counts(const int* diff, int gx, int gy, int n_views, uint32_t* counts, uint32_t* lstart,
+                        uint32_t* view_tot, cudaStream_t s) {
+    k_tile_counts<<<n_views, 1024, sizeof(int) * (size_t)(gx + 1) * (gy + 1), s>>>(diff, gx, gy, counts, lstart, view_tot,
+                                                                                 nullptr, 0, 8);
+}
+void launch_ranges_finalize(const uint32_t* counts, const uint32_t* lstart, const uint32_t* view_tot, int n_views,
+                            uint32_t T, uint32_t cap, const uint32_t* Kd, uint2* ranges, int grid, cudaStream_t s) {
+    k_ranges_finalize<<<grid, 256, 0, s>>>(counts, lstart, view_tot, n_views, T, cap, Kd, ranges);
+}
+
 static int num_sms() {
     static int sms = 0;
     if (!sms) {

@@ -17,6 +17,7 @@ struct queen_ctx {
     int64_t ws_keys = 0;
     queen::WsLayout L{};
     queen::Prof prof;
+    int bin_mode = QUEEN_BIN_ONESWEEP;
     cudaEvent_t binned = nullptr;  // recorded by queen_render_views after binning (queen_wait_binned)
     std::string err;
 };
@@ -27,6 +28,8 @@ float host_theta0(float tau, float g0, float g1) {
     return (float)((double)tau * std::log(-(double)g0 / (double)g1));
 }
 cudaError_t init_binning_attributes();
+cudaError_t launch_bin_bucket(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
+                              const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof, int sms);
 int key_passes(int64_t gtiles);
 size_t ans_encode(const int8_t* lat, int L, int n, int n_pad, std::vector<unsigned char>& out);
 cudaError_t launch_ans_decode(const void* stream_dev, int L, int n, int n_pad, int8_t* out, DevFlags* fl,
@@ -254,9 +257,24 @@ queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_
     WsLayout need = ws_layout(proj->n_pad, n_views, W, H, bins->keys_cap);
     if (need.key_tiles > ctx->L.key_tiles || need.elem_tiles > ctx->L.elem_tiles || need.elems > ctx->L.elems)
         return fail(ctx, QUEEN_ERR_SHAPE, "workspace scratch too small for this batch");
-    cudaError_t e = launch_bin_sort(*proj, n_views, W, H, *bins, ctx->ws, ctx->L, flags_of(ctx),
-                                    static_cast<cudaStream_t>(stream), &ctx->prof);
+    cudaError_t e;
+    if (ctx->bin_mode == QUEEN_BIN_ONESWEEP) {
+        e = launch_bin_sort(*proj, n_views, W, H, *bins, ctx->ws, ctx->L, flags_of(ctx), static_cast<cudaStream_t>(stream),
+                            &ctx->prof);
+    } else {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        e = launch_bin_bucket(*proj, n_views, W, H, *bins, ctx->ws, ctx->L, flags_of(ctx),
+                              static_cast<cudaStream_t>(stream), &ctx->prof, sms);
+    }
     if (e != cudaSuccess) return cuda_fail(ctx, e, "bin_sort");
+    return QUEEN_OK;
+}
+
+queen_status queen_set_binning(queen_ctx* ctx, int32_t mode) {
+    if (!ctx) return QUEEN_ERR_INVALID_ARG;
+    if (mode != QUEEN_BIN_BUCKET && mode != QUEEN_BIN_ONESWEEP) return fail(ctx, QUEEN_ERR_INVALID_ARG, "binning mode");
+    ctx->bin_mode = mode;
     return QUEEN_OK;
 }
 

@@ -101,7 +101,7 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     L.dvals = o; o += align256(sizeof(uint32_t) * L.elems);
     L.dvals_alt = o; o += align256(sizeof(uint32_t) * L.elems);
     L.diff = o; o += align256(sizeof(int32_t) * (size_t)n_views * (gx + 1) * (gy + 1));
-    L.counts = o; o += align256(sizeof(uint32_t) * 2 * (size_t)n_views * L.T);  // counts | local starts
+    L.counts = o; o += align256(sizeof(uint32_t) * 3 * (size_t)n_views * L.T);  // counts | local starts | fill
     L.view_tot = o; o += align256(sizeof(uint32_t) * (size_t)n_views);
     L.total_scratch = o;
     L.rec = o; o += align256(sizeof(float) * REC_WORDS * L.elems);

@@ -12,10 +12,16 @@
 //    cp.async (LDGSTS), double-buffered: batch b+1 is in flight while batch b blends,
 //    and the record indices run one batch further ahead;
 //  * all lanes read the same record (LDS.128 broadcast), and the CTA retires as soon
-//    as all 256 pixels have terminated (__syncthreads_count).
+//    as all 256 pixels have terminated (__syncthreads_count);
+//  * compositing is branch-free per row pair (composite2: a non-hitting row gets alpha = +0,
+//    which leaves C and T bit-identical) and paired as well, so a warp whose lanes hit in
+//    different rows issues one short straight-line block instead of four divergent ones
+//    (SASS: 62 instructions for a fully hit record, was ~100).
 // Per-pixel arithmetic is exactly the oracle's (oracle/queen_oracle.cpp blend_step):
 //   p2 = fma(A2 dx, dx, fma(C2 dy, dy, (B2 dx) dy));  skip if p2 > 0 or p2 < T2;
 //   a = min(0.99, o 2^p2); C = fma(rgb, a T, C); T = T (1 - a); stop after T < 1e-4.
+#include <cstdlib>
+
 #include "queen_internal.cuh"
 
 namespace queen {
@@ -36,21 +42,29 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
-struct Px {
-    float r, g, b, T;
-    bool alive;
+// Pixel state of a row pair, kept as float2 so the compositing runs as paired FP32 ops.
+// A pixel is alive while T >= 1e-4 (composite-then-stop: T only drops below 1e-4 through
+// its last composite); pixels outside the image start at T = 0, i.e. terminated.
+struct Px2 {
+    float2 r, g, b, T;
 };
 
-__device__ __forceinline__ bool hit(const Px& p, float p2, float T2) { return p.alive && !(p2 > 0.0f) && !(p2 < T2); }
+__device__ __forceinline__ bool hit(float T, float p2, float T2) { return !(T < 1e-4f) && !(p2 > 0.0f) && !(p2 < T2); }
 
-__device__ __forceinline__ void composite(Px& p, float p2, const float4& c) {  // c = (o, r, g, b)
-    const float alpha = fminf(0.99f, c.x * ex2(p2));
-    const float aT = alpha * p.T;
-    p.r = fmaf(c.y, aT, p.r);
-    p.g = fmaf(c.z, aT, p.g);
-    p.b = fmaf(c.w, aT, p.b);
-    p.T = p.T * (1.0f - alpha);
-    if (p.T < 1e-4f) p.alive = false;
+// Branch-free compositing of one record into a row pair: a row that does not hit gets
+// exponent -inf, i.e. alpha = min(0.99, o * 2^-inf) = +0, and then C = fma(c, +0, C) = C and
+// T = T (1 - 0) = T exactly -- bit-identical to skipping it.  c = (o, r, g, b).
+__device__ __forceinline__ void composite2(Px2& p, float q0, float q1, bool h0, bool h1, const float4& c) {
+    const float NEG_INF = __int_as_float(0xff800000);
+    const float e0 = ex2(h0 ? q0 : NEG_INF), e1 = ex2(h1 ? q1 : NEG_INF);
+    float2 al = __fmul2_rn(make_float2(c.x, c.x), make_float2(e0, e1));
+    al.x = fminf(0.99f, al.x);
+    al.y = fminf(0.99f, al.y);
+    const float2 aT = __fmul2_rn(al, p.T);
+    p.r = __ffma2_rn(make_float2(c.y, c.y), aT, p.r);
+    p.g = __ffma2_rn(make_float2(c.z, c.z), aT, p.g);
+    p.b = __ffma2_rn(make_float2(c.w, c.w), aT, p.b);
+    p.T = __fmul2_rn(p.T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
 }
 
 template <bool COUNT, int RPT>
@@ -76,9 +90,13 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
     float2 nfy[NP];
 #pragma unroll
     for (int q = 0; q < NP; ++q) nfy[q] = make_float2(-(float)(py0 + 2 * q), -(float)(py0 + 2 * q + 1));
-    Px p[RPT];
+    Px2 p[NP];
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) p[r] = Px{0.f, 0.f, 0.f, 1.f, px < W && py0 + r < H};
+    for (int k = 0; k < NP; ++k) {
+        const float T0 = (px < W && py0 + 2 * k < H) ? 1.0f : 0.0f;
+        const float T1 = (px < W && py0 + 2 * k + 1 < H) ? 1.0f : 0.0f;
+        p[k] = Px2{make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(T0, T1)};
+    }
     long long ev = 0, cpn = 0;
     const uint2 rg = ranges[gt];
     const uint32_t rs = rg.x, re = rg.y;
@@ -129,7 +147,7 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
         cp_async_wait<1>();
         bool any_alive = false;
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) any_alive |= p[r].alive;
+        for (int k = 0; k < NP; ++k) any_alive |= !(p[k].T.x < 1e-4f) | !(p[k].T.y < 1e-4f);
         if (__syncthreads_count(!any_alive) == NT) break;
         const int cnt = (int)min((uint32_t)BATCH, re - rs - (uint32_t)b * BATCH);
         // Warp-uniform control flow: no per-thread early exit inside the batch (a divergent
@@ -142,7 +160,7 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
                 const float dx = a.x - fx;
                 if (COUNT) {
 #pragma unroll
-                    for (int r = 0; r < RPT; ++r) ev += (int)p[r].alive;
+                    for (int k = 0; k < NP; ++k) ev += (int)!(p[k].T.x < 1e-4f) + (int)!(p[k].T.y < 1e-4f);
                 }
                 // Conservative box cull: a pixel with p2 >= T2 satisfies |dx| <= hx and |dy| <= hy
                 // (bounding box of the alpha = 1/255 ellipse, 1e-4 relative slack, K7);
@@ -163,8 +181,8 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
                 for (int k = 0; k < NP; ++k) {
                     const float2 dy = __fadd2_rn(vv, nfy[k]);  // v - y, exactly
                     qq[k] = __ffma2_rn(ta2, dx2, __ffma2_rn(__fmul2_rn(cc, dy), dy, __fmul2_rn(tb2, dy)));
-                    h[2 * k] = hit(p[2 * k], qq[k].x, bq.w);
-                    h[2 * k + 1] = hit(p[2 * k + 1], qq[k].y, bq.w);
+                    h[2 * k] = hit(p[k].T.x, qq[k].x, bq.w);
+                    h[2 * k + 1] = hit(p[k].T.y, qq[k].y, bq.w);
                     anyh |= h[2 * k] | h[2 * k + 1];
                 }
                 if (COUNT) {
@@ -174,10 +192,8 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
                 if (anyh) {
                     const float4 c = sC[s][q];  // o, r, g, b
 #pragma unroll
-                    for (int k = 0; k < NP; ++k) {
-                        if (h[2 * k]) composite(p[2 * k], qq[k].x, c);
-                        if (h[2 * k + 1]) composite(p[2 * k + 1], qq[k].y, c);
-                    }
+                    for (int k = 0; k < NP; ++k)
+                        if (h[2 * k] | h[2 * k + 1]) composite2(p[k], qq[k].x, qq[k].y, h[2 * k], h[2 * k + 1], c);
                 }
             }
         }
@@ -207,16 +223,29 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
 #pragma unroll
         for (int r = 0; r < RPT; ++r) {
             if (py0 + r < H) {
-                o[(int64_t)r * W] = p[r].r + p[r].T * bg0;
-                o[plane + (int64_t)r * W] = p[r].g + p[r].T * bg1;
-                o[2 * plane + (int64_t)r * W] = p[r].b + p[r].T * bg2;
-                if (to) to[(int64_t)r * W] = p[r].T;
+                const Px2& q = p[r >> 1];
+                const float pr = (r & 1) ? q.r.y : q.r.x, pg = (r & 1) ? q.g.y : q.g.x, pb = (r & 1) ? q.b.y : q.b.x;
+                const float pT = (r & 1) ? q.T.y : q.T.x;
+                o[(int64_t)r * W] = pr + pT * bg0;
+                o[plane + (int64_t)r * W] = pg + pT * bg1;
+                o[2 * plane + (int64_t)r * W] = pb + pT * bg2;
+                if (to) to[(int64_t)r * W] = pT;
             }
         }
     }
 }
 
 constexpr int BLEND_RPT = 4;
+
+// tuning knob (bench sweeps only): QUEEN_BLEND_RPT=8 selects one warp per tile, 8 rows per thread
+static int blend_rpt() {
+    static int r = 0;
+    if (!r) {
+        const char* e = getenv("QUEEN_BLEND_RPT");
+        r = (e && atoi(e) == 8) ? 8 : BLEND_RPT;
+    }
+    return r;
+}
 
 cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
@@ -225,9 +254,14 @@ cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges
     const int T = gx * gy;
     const int64_t blocks = (int64_t)T * n_views;
     if (blocks == 0) return cudaSuccess;
-    k_blend<false, BLEND_RPT><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
-                                                   reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0, bg1,
-                                                   bg2, rgb_out, T_out, nullptr, nullptr);
+    if (blend_rpt() == 8)
+        k_blend<false, 8><<<(unsigned)blocks, 32, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
+                                                          reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0,
+                                                          bg1, bg2, rgb_out, T_out, nullptr, nullptr);
+    else
+        k_blend<false, BLEND_RPT><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
+                                                       reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0, bg1,
+                                                       bg2, rgb_out, T_out, nullptr, nullptr);
     return cudaGetLastError();
 }
 

@@ -135,6 +135,9 @@ def test_device_errors_reported():
 
 
 # ------------------------------------------------------------------ render stages
+BINNING = ["bucket", "onesweep"]
+
+
 def _render_case(name, n=None, views=None, **over):
     cfg, sc = _scene(name, n, **over)
     cams = synth.make_cameras(cfg, views)
@@ -176,13 +179,14 @@ def _check_image(rgb, T, rref, Tref):
                                   ("n3dv", 20003, 3, {"width": 333, "height": 250, "focal": 280.0}),
                                   ("immersive", 12001, 5, {"width": 320, "height": 240, "focal": 160.0}),
                                   ("meetroom", 8000, 13, {"width": 160, "height": 90, "focal": 125.0})])
-def test_render_stages_parity(case):
+@pytest.mark.parametrize("binning", BINNING)
+def test_render_stages_parity(case, binning):
     from tests.gpu_helpers import Stages
     name, n, views, over = case
     cfg, sc, cams = _render_case(name, n, views, **over)
     W, H = cams[0].width, cams[0].height
     proj, bins, rgb, T = oracle.render(sc.planes, sc.n, sc.deg, cams)
-    st = Stages(sc.planes, sc.n, sc.deg, cams).run()
+    st = Stages(sc.planes, sc.n, sc.deg, cams, binning=binning).run()
     gp = st.proj_np()
     _check_proj(gp, proj, sc.n)
     gb = st.bins_np()
@@ -194,7 +198,8 @@ def test_render_stages_parity(case):
     assert s == 0
 
 
-def test_render_big_gaussians_ragged():
+@pytest.mark.parametrize("binning", BINNING)
+def test_render_big_gaussians_ragged(binning):
     """Large, overlapping, off-screen and near-plane Gaussians; ragged 70x45 image; degree 3."""
     from tests.gpu_helpers import Stages
     rng = np.random.default_rng(11)
@@ -204,19 +209,20 @@ def test_render_big_gaussians_ragged():
                      rng.normal(0, 0.5, (n, 16, 3)), 3)
     cams = [synth.make_camera(np.eye(3), np.zeros(3), 40.0, 40.0, 70, 45)]
     proj, bins, rgb, T = oracle.render(pl, n, 3, cams, bg=(0.1, 0.2, 0.3))
-    st = Stages(pl, n, 3, cams).run(bg=(0.1, 0.2, 0.3))
+    st = Stages(pl, n, 3, cams, binning=binning).run(bg=(0.1, 0.2, 0.3))
     gp = st.proj_np()
     _check_proj(gp, proj, n)
     _check_bins(st.bins_np(), bins, gp["depth"], st.T)
     _check_image(*st.image_np(), rgb, T)
 
 
-def test_empty_and_all_culled():
+@pytest.mark.parametrize("binning", BINNING)
+def test_empty_and_all_culled(binning):
     from tests.gpu_helpers import Stages
     pl = planes_from([[0, 0, -5.0]] * 8, [[1, 0, 0, 0]] * 8, [[-3] * 3] * 8, [2.0] * 8,
                      [np.zeros((1, 3))] * 8, 0)
     cams = [synth.make_camera(np.eye(3), np.zeros(3), 30.0, 30.0, 40, 24)]
-    st = Stages(pl, 8, 0, cams).run(bg=(0.25, 0.5, 1.0))
+    st = Stages(pl, 8, 0, cams, binning=binning).run(bg=(0.25, 0.5, 1.0))
     rgb, T = st.image_np()
     assert st.bins_np()["K"] == 0
     assert np.all(T == 1.0) and np.all(rgb[0, 0] == 0.25) and np.all(rgb[0, 2] == 1.0)
@@ -236,13 +242,38 @@ def test_nonfinite_warns_and_culls():
     _check_image(*st.image_np(), rgb, T)
 
 
-def test_capacity_error_reports_needed_keys():
+@pytest.mark.parametrize("binning", BINNING)
+def test_capacity_error_reports_needed_keys(binning):
     from tests.gpu_helpers import Stages
     cfg, sc, cams = _render_case("tiny")
     proj, bins, rgb, T = oracle.render(sc.planes, sc.n, sc.deg, cams)
-    st = Stages(sc.planes, sc.n, sc.deg, cams, keys_cap=max(1, bins["K"] // 2)).run()
+    st = Stages(sc.planes, sc.n, sc.deg, cams, keys_cap=max(1, bins["K"] // 2), binning=binning).run()
     s, info = st.ctx.check_status()
     assert s == -5 and info == bins["K"]
+    assert st.bins_np()["K"] == 0  # nothing emitted, every range empty
+    assert not np.any(st.ranges.cpu().numpy())
+
+
+@pytest.mark.parametrize("binning", BINNING)
+def test_long_tile_lists(binning):
+    """Tiles whose lists exceed the bucket sort's shared-memory capacity (2048 entries): 6000
+    small Gaussians crowded into a 40x36 image (some tiles hold thousands of entries, forcing the
+    in-place global-memory network), equal depths included (ties broken by index)."""
+    from tests.gpu_helpers import Stages
+    rng = np.random.default_rng(23)
+    n = 6000
+    z = np.where(rng.random(n) < 0.3, 2.0, rng.uniform(1.0, 4.0, n))  # 30 % share one depth
+    pos = np.stack([rng.normal(0, 0.08, n) * z, rng.normal(0, 0.08, n) * z, z], 1)
+    pl = planes_from(pos, rng.standard_normal((n, 4)), rng.normal(math.log(0.01), 0.3, (n, 3)), rng.normal(-1, 1, n),
+                     rng.normal(0, 0.5, (n, 1, 3)), 0)
+    cams = [synth.make_camera(np.eye(3), np.zeros(3), 60.0, 60.0, 40, 36)]
+    proj, bins, rgb, T = oracle.render(pl, n, 0, cams)
+    assert np.diff(bins["ranges"], axis=1).max() > 2048
+    st = Stages(pl, n, 0, cams, binning=binning).run()
+    gp = st.proj_np()
+    _check_proj(gp, proj, n)
+    _check_bins(st.bins_np(), bins, gp["depth"], st.T)
+    _check_image(*st.image_np(), rgb, T)
 
 
 def test_render_views_equals_stages_and_deterministic():
