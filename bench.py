@@ -46,7 +46,6 @@ def parse():
     ap.add_argument("--packets", type=int, default=8, help="cyclic window of pre-generated frame packets")
     ap.add_argument("--packet-format", default="entropy", choices=["entropy", "int8"],
                     help="entropy: rANS-coded latents decoded on the GPU each frame (default); int8: raw latents")
-    ap.add_argument("--binning", default="onesweep", choices=["bucket", "onesweep"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -305,7 +304,7 @@ def main():
     mkpkt = (lambda b: EntropyPacket(b, hdr)) if entropy else (lambda b: wire_packet(b, hdr))
     dps = [mkpkt(s) for s in slots]
 
-    player = Player(sc.planes, sc.n, sc.deg, cams, device=local, views_per_batch=vpb, binning=args.binning)
+    player = Player(sc.planes, sc.n, sc.deg, cams, device=local, views_per_batch=vpb)
     stream = torch.cuda.current_stream()
 
     def step(t):
@@ -366,8 +365,7 @@ def main():
     from paper_2412_04469_b200.stages import Stages  # explicit-buffer stage runner over the same C-ABI
     K_list, ev_pairs, cp_pairs = [], 0, 0
     for bc in batches:
-        stg = Stages(player.planes.cpu().numpy(), sc.n, sc.deg, bc, keys_cap=player.keys_cap, device=local,
-                     binning=args.binning)
+        stg = Stages(player.planes.cpu().numpy(), sc.n, sc.deg, bc, keys_cap=player.keys_cap, device=local)
         stg.project().bin_sort()
         K_list.append(stg.bins_np()["K"])
         e = torch.zeros(len(bc), dtype=torch.int64, device=dev)
@@ -404,6 +402,9 @@ def main():
                     "unit": "T FP32-lane-ops/s", "frac": achieved / peak, "traffic": lookup_traffic(traffic, "k_blend<0"),
                     "peak_source": f"148 SMs x 128 FP32 lanes x {f_mhz:.0f} MHz (sampled SM clock)",
                     "work": {"evaluated_pairs": ev_pairs, "composited_pairs": cp_pairs}}
+        elif algorithmic_bytes(dom, cfg, sc.n, vpb_list, K_list, k_coo) is None:
+            roof = {"bound": None, "kernel": dom, "achieved": None, "peak": None, "unit": None, "frac": None,
+                    "traffic": None, "note": "dominant stage has no roofline model"}
         else:
             b = algorithmic_bytes(dom, cfg, sc.n, vpb_list, K_list, k_coo)
             t = stages[dom]["us_per_launch"] * 1e-6
@@ -503,7 +504,7 @@ def main():
                                    f"{W}x{H}, SH {cfg.deg}, latents {tuple(cfg.lat)}, {cfg.rho:.0%} gates)",
                        "gaussians": cfg.n, "views": V, "width": W, "height": H, "views_per_batch": player.vpb, "render_lanes": player.n_lanes,
                        "parallelism": f"views sharded v mod {world}, Gaussians replicated, packet NCCL-broadcast",
-                       "packet_format": args.packet_format, "binning": args.binning,
+                       "packet_format": args.packet_format,
                        "l2": "flushed between timed steps (512 MB write outside the step events)"},
             "packet_bytes_per_frame": int(statistics.mean(used_bytes)) if used_bytes else None,
             "mpixel_per_s": mpix, "view_fps": value * V,

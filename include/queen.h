@@ -182,18 +182,13 @@ queen_status queen_project(queen_ctx* ctx, const queen_gaussians* scene, const q
                            queen_proj* out, void* stream);
 /* queen_bin_sort: a8-a11 for a batch of equally-sized views: the entries (gt, depth,
  * index) of every visible (view, Gaussian) x overlapped tile, ordered by gt then depth
- * then index, plus tile ranges.  Uses the workspace scratch.  Outputs bit-exact
- * (DESIGN.md "Binning").  Two interchangeable algorithms (queen_set_binning), same
- * output: QUEEN_BIN_ONESWEEP (default) -- LSD onesweep radix sort on (gt, depth); QUEEN_BIN_BUCKET
- * -- per-tile counts, atomic slot placement, per-tile sort in shared memory.
- * The sorted index list is bins->vals (or vals_alt when bins->sorted_in_alt is set on
- * return); keys (same buffer choice) hold gt. */
+ * then index (LSD onesweep radix sort on (gt, depth)), plus tile ranges.  Uses the
+ * workspace scratch.  Outputs bit-exact.  The sorted index list is
+ * bins->vals (or vals_alt when bins->sorted_in_alt is set on return); keys (same buffer
+ * choice) hold gt.  Views whose (ceil(W/16)+1)(ceil(H/16)+1) tile grid exceeds 48K words
+ * (larger than 4K) are rejected with QUEEN_ERR_SHAPE. */
 queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_camera* cams, int32_t n_views,
                             queen_bins* bins, void* stream);
-enum { QUEEN_BIN_BUCKET = 0, QUEEN_BIN_ONESWEEP = 1 };
-/* Selects the binning algorithm of later queen_bin_sort / queen_render_views calls on ctx
- * (QUEEN_ERR_INVALID_ARG for an unknown mode). */
-queen_status queen_set_binning(queen_ctx* ctx, int32_t mode);
 /* queen_rasterize: a12, Eq. 2: per pixel front-to-back over its tile's
  * range; skip a < 1/255 (p2 < T2), a = min(0.99, o 2^p2), stop after T < 1e-4.
  * rgb_out fp32 [n_views][3][H][W] = C + T bg;  T_out (nullable) fp32 [n_views][H][W]. */

@@ -23,14 +23,13 @@ STATUS = {0: "QUEEN_OK", -1: "QUEEN_ERR_INVALID_ARG", -2: "QUEEN_ERR_SHAPE", -3:
 QUEEN_LAT_INT8, QUEEN_LAT_F32 = 0, 1
 QUEEN_POS_COO, QUEEN_POS_GATES, QUEEN_POS_NONE = 0, 1, 2
 QUEEN_MAX_VIEWS = 64
-QUEEN_BIN_BUCKET, QUEEN_BIN_ONESWEEP = 0, 1
 
 # exported C symbols (include/queen.h); tests check the library exports every one
 EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version", "queen_workspace_size",
            "queen_set_workspace", "queen_check", "queen_decode_residuals", "queen_apply_frame", "queen_project",
            "queen_bin_sort", "queen_rasterize", "queen_render_views", "queen_blend_counts",
            "queen_profile_enable", "queen_profile_read", "queen_wait_binned", "queen_entropy_encode",
-           "queen_entropy_decode", "queen_entropy_decode_frame", "queen_set_binning"]
+           "queen_entropy_decode", "queen_entropy_decode_frame"]
 STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy"]
 
 
@@ -103,7 +102,6 @@ def lib() -> C.CDLL:
             "queen_blend_counts": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
                                          p, p, p]),
             "queen_profile_enable": (i32, [p, i32]),
-            "queen_set_binning": (i32, [p, i32]),
             "queen_wait_binned": (i32, [p, p]),
             "queen_entropy_encode": (i32, [p, i32, i32, i32, p, C.c_size_t, C.POINTER(C.c_size_t)]),
             "queen_entropy_decode": (i32, [p, p, i32, i32, i32, p, p]),
@@ -207,11 +205,6 @@ class Context:
         info = C.c_int64(0)
         st = lib().queen_check(self._h, C.c_void_p(_stream(stream)), C.byref(info))
         return st, int(info.value)
-
-    def set_binning(self, mode: str):
-        """'onesweep' (default) or 'bucket': same output, different algorithm (queen.h)."""
-        code = {"bucket": QUEEN_BIN_BUCKET, "onesweep": QUEEN_BIN_ONESWEEP}[mode]
-        self._chk(lib().queen_set_binning(self._h, code), "queen_set_binning")
 
     def profile(self, enable: bool = True):
         self._chk(lib().queen_profile_enable(self._h, 1 if enable else 0), "queen_profile_enable")

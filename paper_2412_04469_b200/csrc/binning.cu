@@ -6,15 +6,21 @@
 // tile: LSD order processes the depth digits first and the tile digits last.  Every
 // duplicate of a Gaussian carries the same depth, so the depth digits are sorted
 // BEFORE duplication, on the M visible (view, Gaussian) pairs (M << K), and only the
-// tile digits are sorted on the K duplicated entries, with 4-byte keys:
-//   K3a k_vis_compact   decoupled look-back scan: visible pairs (tiles > 0) in (view,
-//                       index) order -> (depth bits, flat index)            [M]
+// tile digits are sorted on the K duplicated entries, with 4-byte keys.  Every count the
+// sort needs (visible pairs, entries per tile -> ranges, digit histograms) is known
+// before the first pass, from one read of the projection outputs:
+//   K3a k_slab_count    per slab of S consecutive elements of a view (one CTA): visible
+//                       count, depth-digit histograms, and the slab's entries per tile via
+//                       a shared-memory 2D difference array of tile rects -> counts[slab][t]
+//       k_slab_sum      per view: entries per tile, view-local starts, tile-digit histograms
+//       k_totals        K, M, capacity check; slab offsets of the visible pairs
+//       k_slab_compact  visible pairs in (view, index) order -> (depth bits, flat index) [M]
 //   K5a k_onesweep32<8> x4  stable sort of the pairs by depth (31 bits)
-//   K3b/K4 k_scan_dup   decoupled look-back scan of tiles touched in depth order fused
+//   K4  k_scan_dup      decoupled look-back scan of tiles touched in depth order fused
 //                       with duplication: entry = (gt, Gaussian index), emitted for
-//                       each pair ty-major, tx-minor; fused tile-digit histograms
+//                       each pair ty-major, tx-minor
+//   K6  k_ranges_finalize  [first, last+1) of each gt from the per-tile counts
 //   K5b k_onesweep32<8|9> x2..3  stable sort of the entries by gt
-//   K6  k_ranges        [first, last+1) of each gt
 // Stability makes the final order (gt, depth, view, index) -> (gt, depth, index):
 // identical to sorting the 96-bit (gt << 31 | depth, index) tuples (oracle: std::sort).
 //
@@ -98,63 +104,274 @@ __device__ unsigned long long lookback64(unsigned long long* lb, uint32_t tile, 
 }
 
 // ---------------------------------------------------------------------------
-// K3a: visible (view, Gaussian) pairs, in flat-index order -> (depth bits, j)
+// K3a: per-slab counting.  Each view's elements are cut into slabs of
+// S consecutive indices (bin_plan); one CTA per slab:
+//   * visible elements (tiles > 0) counted -> svis[slab];
+//   * their depth digits (4 x 8 bits) histogrammed in shared memory -> hist (global adds);
+//   * their tile rects added to a private shared-memory 2D difference array of per-tile
+//     entry counts (4 shared atomics per element; measured ~11 lane-ops per clock per SM,
+//     while REDs into one global plane serialise on hot corners), whose 2D prefix sum is
+//     written densely as counts[slab][t].
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(SORT_THREADS) k_vis_compact(const uint32_t* __restrict__ tiles,
-                                                              const uint32_t* __restrict__ depth, int64_t count,
-                                                              uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
-                                                              unsigned long long* lb, DevFlags* fl, uint32_t* M_out) {
-    __shared__ uint32_t s_tile, s_w[SORT_WARPS];
-    __shared__ unsigned long long s_prefix;
-    if (threadIdx.x == 0) s_tile = atomicAdd(&fl->tickets[TK_VIS], 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const int64_t ntiles = (count + SORT_TILE - 1) / SORT_TILE;
-    const int64_t base = (int64_t)tile * SORT_TILE + (int64_t)threadIdx.x * SORT_ITEMS;
-    uint32_t vis = 0;  // bit e set <=> element base+e is visible
+constexpr int SLAB_THREADS = 512;
+constexpr int SLAB_IT = 8;                             // consecutive elements per thread per round
+constexpr int SLAB_ROUND = SLAB_THREADS * SLAB_IT;     // 4096 elements per round
+
+// The 8 elements [i, i+8) of view row jb: tile counts, rects, depth bits (vector loads when
+// the run is whole; n_pad % 4 == 0 keeps them 16-byte aligned), invalid ones get tiles = 0.
+__device__ __forceinline__ void load8(const uint32_t* __restrict__ tiles, const short4* __restrict__ rect,
+                                      const uint32_t* __restrict__ depth, int64_t jb, int i, int b, uint32_t (&nt)[8],
+                                      short4 (&r)[8], uint32_t (&dk)[8], bool want_rect, bool want_depth) {
+    if (i + 8 <= b) {
+        const uint4 t0 = __ldg(reinterpret_cast<const uint4*>(tiles + jb + i));
+        const uint4 t1 = __ldg(reinterpret_cast<const uint4*>(tiles + jb + i + 4));
+        nt[0] = t0.x; nt[1] = t0.y; nt[2] = t0.z; nt[3] = t0.w; nt[4] = t1.x; nt[5] = t1.y; nt[6] = t1.z; nt[7] = t1.w;
+        if (want_rect) {
+            const uint4* rp = reinterpret_cast<const uint4*>(rect + jb + i);
 #pragma unroll
-    for (int q = 0; q < SORT_ITEMS / 4; ++q) {
-        if (base + 4 * q < count) {
-            const uint4 t4 = __ldg(reinterpret_cast<const uint4*>(tiles + base + 4 * q));
-            vis |= (t4.x ? 1u : 0u) << (4 * q) | (t4.y ? 2u : 0u) << (4 * q) | (t4.z ? 4u : 0u) << (4 * q) |
-                   (t4.w ? 8u : 0u) << (4 * q);
+            for (int q = 0; q < 4; ++q) {
+                const uint4 x = __ldg(rp + q);
+                r[2 * q] = *reinterpret_cast<const short4*>(&x.x);
+                r[2 * q + 1] = *reinterpret_cast<const short4*>(&x.z);
+            }
         }
-    }
-    uint32_t total;
-    const uint32_t excl = block_excl_scan(__popc(vis), s_w, total);
-    if (threadIdx.x == 0) {
-        s_prefix = lookback64(lb, tile, total, fl);
-        if ((int64_t)tile == ntiles - 1) *M_out = (uint32_t)(s_prefix + total);
-    }
-    __syncthreads();
-    uint64_t pos = s_prefix + excl;
-    while (vis) {
-        const int e = __ffs(vis) - 1;
-        vis &= vis - 1;
-        const int64_t j = base + e;
-        dkeys[pos] = __ldg(depth + j);
-        dvals[pos] = (uint32_t)j;
-        ++pos;
+        if (want_depth) {
+            const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(depth + jb + i));
+            const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(depth + jb + i + 4));
+            dk[0] = d0.x; dk[1] = d0.y; dk[2] = d0.z; dk[3] = d0.w; dk[4] = d1.x; dk[5] = d1.y; dk[6] = d1.z; dk[7] = d1.w;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const bool ok = i + e < b;
+            nt[e] = ok ? tiles[jb + i + e] : 0u;
+            if (want_rect) r[e] = ok ? rect[jb + i + e] : make_short4(0, 0, 0, 0);
+            if (want_depth) dk[e] = ok ? depth[jb + i + e] : 0u;
+        }
     }
 }
 
-// ---------------------------------------------------------------------------
-// K5: histograms of the depth digits (4 x 8 bits) of the M visible pairs
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_hist_depth(const uint32_t* __restrict__ keys, const uint32_t* count_ptr,
-                                                    uint32_t* hist) {
+__global__ void __launch_bounds__(SLAB_THREADS) k_slab_count(const uint32_t* __restrict__ tiles,
+                                                             const short4* __restrict__ rect,
+                                                             const uint32_t* __restrict__ depth, int n_pad, int S, int spv,
+                                                             int gx, int gy, uint32_t* __restrict__ counts,
+                                                             uint32_t* __restrict__ svis, uint32_t* __restrict__ hist) {
+    extern __shared__ int cs[];  // [(gy+1)][(gx+1)] difference array -> 2D prefix
     __shared__ uint32_t sh[DEPTH_PASSES * 256];
+    __shared__ uint32_t s_vis;
+    const int slab = blockIdx.x;
+    const int v = slab / spv;
+    const int a = (slab - v * spv) * S;
+    const int b = min(a + S, n_pad);
+    const int dw = gx + 1, dplane = (gx + 1) * (gy + 1);
+    const int T = gx * gy;
+    for (int q = threadIdx.x; q < dplane; q += blockDim.x) cs[q] = 0;
     for (int q = threadIdx.x; q < DEPTH_PASSES * 256; q += blockDim.x) sh[q] = 0;
+    if (threadIdx.x == 0) s_vis = 0;
     __syncthreads();
-    const uint32_t n = *count_ptr;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-        const uint32_t k = keys[j];
+    const int64_t jb = (int64_t)v * n_pad;
+    uint32_t vis = 0;
+    for (int i = a + threadIdx.x * SLAB_IT; i < b; i += SLAB_ROUND) {
+        uint32_t nt[8], dk[8];
+        short4 r[8];
+        load8(tiles, rect, depth, jb, i, b, nt, r, dk, true, true);
 #pragma unroll
-        for (int p = 0; p < DEPTH_PASSES; ++p) atomicAdd(&sh[p * 256 + ((k >> (8 * p)) & 255u)], 1u);
+        for (int e = 0; e < 8; ++e) {
+            if (nt[e] == 0) continue;
+            ++vis;
+            atomicAdd(&cs[r[e].y * dw + r[e].x], 1);
+            atomicAdd(&cs[r[e].y * dw + r[e].z + 1], -1);
+            atomicAdd(&cs[(r[e].w + 1) * dw + r[e].x], -1);
+            atomicAdd(&cs[(r[e].w + 1) * dw + r[e].z + 1], 1);
+#pragma unroll
+            for (int p = 0; p < DEPTH_PASSES; ++p) atomicAdd(&sh[p * 256 + ((dk[e] >> (8 * p)) & 255u)], 1u);
+        }
     }
+    for (int o = 16; o > 0; o >>= 1) vis += __shfl_down_sync(0xffffffffu, vis, o);
+    if ((threadIdx.x & 31) == 0 && vis) atomicAdd(&s_vis, vis);
     __syncthreads();
     for (int q = threadIdx.x; q < DEPTH_PASSES * 256; q += blockDim.x)
         if (sh[q]) atomicAdd(&hist[(q >> 8) * MAX_BINS + (q & 255)], sh[q]);  // per-pass stride MAX_BINS
+    if (threadIdx.x == 0) svis[slab] = s_vis;
+    for (int r = threadIdx.x; r < gy; r += blockDim.x) {  // prefix along x
+        int run = 0;
+        for (int x = 0; x < gx; ++x) { run += cs[r * dw + x]; cs[r * dw + x] = run; }
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < gx; x += blockDim.x) {  // prefix along y
+        int run = 0;
+        for (int r = 0; r < gy; ++r) { run += cs[r * dw + x]; cs[r * dw + x] = run; }
+    }
+    __syncthreads();
+    uint32_t* out = counts + (int64_t)slab * T;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) out[t] = (uint32_t)cs[(t / gx) * dw + (t % gx)];
+}
+
+// Entries per tile = column sums of counts[slab][t] over the view's slabs (one thread per
+// tile, grid = views x tile chunks).
+__global__ void __launch_bounds__(256) k_slab_sum(const uint32_t* __restrict__ counts, int spv, int T,
+                                                  uint32_t* __restrict__ tcounts) {
+    const int v = blockIdx.y;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    const uint32_t* c0 = counts + (int64_t)v * spv * T + t;
+    uint32_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    int q = 0;
+    for (; q + 4 <= spv; q += 4) {
+        s0 += c0[(int64_t)q * T];
+        s1 += c0[(int64_t)(q + 1) * T];
+        s2 += c0[(int64_t)(q + 2) * T];
+        s3 += c0[(int64_t)(q + 3) * T];
+    }
+    for (; q < spv; ++q) s0 += c0[(int64_t)q * T];
+    tcounts[(int64_t)v * T + t] = s0 + s1 + s2 + s3;
+}
+
+// Per-view block (1024 threads): view-local exclusive starts of the tile totals, view total,
+// and the tile-digit histograms of the coming tile sort.
+__global__ void __launch_bounds__(1024) k_view_scan(const uint32_t* __restrict__ tcounts, int T, uint32_t* lstart,
+                                                    uint32_t* view_tot, uint32_t* hist, int tpasses, int tbits) {
+    __shared__ uint32_t sh[MAX_TILE_PASSES * MAX_BINS];
+    __shared__ uint32_t s_w[32];
+    const int v = blockIdx.x;
+    for (int q = threadIdx.x; q < tpasses * MAX_BINS; q += blockDim.x) sh[q] = 0;
+    __syncthreads();
+    const uint32_t* tc = tcounts + (int64_t)v * T;
+    const int per = (T + blockDim.x - 1) / blockDim.x;
+    const int t0 = threadIdx.x * per, t1 = min(T, t0 + per);
+    uint32_t csum = 0;
+    for (int t = t0; t < t1; ++t) csum += tc[t];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t inc = csum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+        pre += q < w ? s_w[q] : 0u;
+        tot += s_w[q];
+    }
+    uint32_t run = pre + inc - csum;
+    const uint32_t dmask = (1u << tbits) - 1u;
+    for (int t = t0; t < t1; ++t) {
+        const uint32_t c = tc[t];
+        const uint32_t g = (uint32_t)v * (uint32_t)T + (uint32_t)t;
+        lstart[g] = run;
+        run += c;
+        if (c)
+            for (int p = 0; p < tpasses; ++p) atomicAdd(&sh[p * MAX_BINS + ((g >> (p * tbits)) & dmask)], c);
+    }
+    if (threadIdx.x == 0) view_tot[v] = tot;
+    __syncthreads();
+    for (int q = threadIdx.x; q < tpasses * MAX_BINS; q += blockDim.x)
+        if (sh[q]) atomicAdd(&hist[q], sh[q]);
+}
+
+// K, M, overflow flag; slab visible counts -> global exclusive offsets (in place).  One block.
+__global__ void __launch_bounds__(1024) k_totals(const uint32_t* __restrict__ view_tot, int n_views, uint32_t* svis,
+                                                 int slabs, uint32_t cap, uint32_t* Kd, DevFlags* fl) {
+    __shared__ uint32_t s_w[32];
+    __shared__ uint32_t s_carry;
+    if (threadIdx.x == 0) {
+        unsigned long long K = 0;
+        for (int v = 0; v < n_views; ++v) K += view_tot[v];
+        const bool over = K > cap;
+        if (over) {
+            raise_flag(fl, FLAG_CAPACITY);
+            atomicMax(&fl->info, K);
+        }
+        // overflow: no entry list is produced (every range is [0,0)); QUEEN_ERR_CAPACITY
+        // carries the K needed.  Kd[2] = overflow flag.
+        Kd[0] = over ? 0u : (uint32_t)K;
+        Kd[2] = over ? 1u : 0u;
+        s_carry = 0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < slabs; b0 += blockDim.x) {
+        const int q = b0 + threadIdx.x;
+        const uint32_t x = q < slabs ? svis[q] : 0u;
+        uint32_t inc = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_w[w] = inc;
+        __syncthreads();
+        uint32_t pre = 0, tot = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+            pre += k < w ? s_w[k] : 0u;
+            tot += s_w[k];
+        }
+        const uint32_t carry = s_carry;
+        if (q < slabs) svis[q] = carry + pre + inc - x;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = carry + tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) Kd[1] = s_carry;  // M visible pairs
+}
+
+// K3b: per slab, its visible elements in index order -> (depth bits, flat index) pairs at the
+// slab's global offset.  Rounds of 4096 elements, 8 consecutive per thread (vector loads);
+// block scan of the per-thread visible counts; pairs staged in shared memory in order and
+// written out coalesced.
+__global__ void __launch_bounds__(SLAB_THREADS) k_slab_compact(const uint32_t* __restrict__ tiles,
+                                                               const uint32_t* __restrict__ depth, int n_pad, int S,
+                                                               int spv, const uint32_t* __restrict__ soff,
+                                                               uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dvals) {
+    constexpr int NW = SLAB_THREADS / 32;
+    __shared__ uint32_t s_w[NW];
+    __shared__ uint32_t s_k[SLAB_ROUND], s_j[SLAB_ROUND];
+    const int slab = blockIdx.x;
+    const int v = slab / spv;
+    const int a = (slab - v * spv) * S;
+    const int b = min(a + S, n_pad);
+    const int64_t jb = (int64_t)v * n_pad;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t base = soff[slab];
+    for (int i0 = a; i0 < b; i0 += SLAB_ROUND) {
+        const int i = i0 + threadIdx.x * SLAB_IT;
+        uint32_t nt[8], dk[8];
+        short4 r[8];
+        load8(tiles, nullptr, depth, jb, i, b, nt, r, dk, false, true);
+        uint32_t c = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) c += nt[e] ? 1u : 0u;
+        uint32_t inc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_w[w] = inc;
+        __syncthreads();
+        uint32_t pre = 0, tot = 0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+            pre += q < w ? s_w[q] : 0u;
+            tot += s_w[q];
+        }
+        uint32_t o = pre + inc - c;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            if (nt[e]) {
+                s_k[o] = dk[e];
+                s_j[o] = (uint32_t)(jb + i + e);
+                ++o;
+            }
+        }
+        __syncthreads();
+        for (uint32_t q = threadIdx.x; q < tot; q += SLAB_THREADS) {
+            dkeys[base + q] = s_k[q];
+            dvals[base + q] = s_j[q];
+        }
+        base += tot;
+        __syncthreads();
+    }
 }
 
 // exclusive scan of each pass's digit counts (one warp per pass)
@@ -355,9 +572,7 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
 // K3b + K4: offsets of the depth-sorted pairs (decoupled look-back) + duplication.
 // Entry = (gt, Gaussian index), emitted for each pair ty-major, tx-minor.
 // Phase 1 stages the block's 4096 pairs in shared memory (block-local offset, gt of the
-// rect's first tile, Gaussian index, rect width) and adds the pair's tile rect to the
-// per-view 2D difference array of tile counts (4 corner increments; k_tile_counts turns
-// it into per-tile entry counts, i.e. the final ranges and the digit histograms).
+// rect's first tile, Gaussian index, rect width).
 // Phase 2: each warp emits a contiguous run of the block's entries, 32 at a time; every
 // pair has >= 1 entry, so the pairs starting inside a 32-entry chunk are the next <= 31
 // pairs: one shared load + redux.or + popc locates each lane's pair.  Stores coalesce.
@@ -368,8 +583,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
                                                            const short4* __restrict__ rect, int n_pad, int gx, int gy,
                                                            uint32_t T, uint32_t* __restrict__ keys,
                                                            uint32_t* __restrict__ vals, uint32_t cap,
-                                                           unsigned long long* lb, DevFlags* fl, uint32_t* K_out,
-                                                           int* __restrict__ diff) {
+                                                           unsigned long long* lb, DevFlags* fl, uint32_t* K_out) {
     extern __shared__ __align__(16) unsigned char dsm[];
     uint32_t* s_off = reinterpret_cast<uint32_t*>(dsm);       // [SORT_TILE + 1]
     uint32_t* s_base = s_off + SORT_TILE + 4;                // [SORT_TILE]
@@ -384,7 +598,6 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
     const uint32_t tile = s_tile;
     if (tile >= ntiles) return;
     const uint32_t base = tile * SORT_TILE + threadIdx.x * SORT_ITEMS;
-    const int dw = gx + 1, dplane = (gx + 1) * (gy + 1);
     uint32_t nt[SORT_ITEMS];
     uint32_t tsum = 0;
     // batch the dependent gathers: all 16 indices (4 x uint4), then all 16 rects, then use them
@@ -417,11 +630,6 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
             s_base[q] = v * T + (uint32_t)r.y * (uint32_t)gx + (uint32_t)r.x;
             s_i[q] = j - v * (uint32_t)n_pad;
             s_wx[q] = (uint16_t)wx;
-            int* d = diff + (int64_t)v * dplane;
-            atomicAdd(d + r.y * dw + r.x, 1);
-            atomicAdd(d + r.y * dw + r.z + 1, -1);
-            atomicAdd(d + (r.w + 1) * dw + r.x, -1);
-            atomicAdd(d + (r.w + 1) * dw + r.z + 1, 1);
         }
         tsum += nt[e];
     }
@@ -492,66 +700,6 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
     }
 }
 
-// Per-view 2D prefix sums of the tile-count difference arrays -> entries per global tile,
-// their view-local exclusive starts, the tile-digit histograms of the coming tile sort,
-// and per-view totals.  One block per view.
-__global__ void __launch_bounds__(1024) k_tile_counts(const int* __restrict__ diff, int gx, int gy, uint32_t* counts,
-                                                      uint32_t* lstart, uint32_t* view_tot, uint32_t* hist, int tpasses,
-                                                      int tbits) {
-    extern __shared__ int cs[];  // [(gy+1)][(gx+1)]
-    __shared__ uint32_t sh[MAX_TILE_PASSES * MAX_BINS];
-    __shared__ uint32_t s_w[32];
-    const int v = blockIdx.x;
-    const int dw = gx + 1, dplane = (gx + 1) * (gy + 1);
-    const int T = gx * gy;
-    for (int q = threadIdx.x; q < dplane; q += blockDim.x) cs[q] = diff[(int64_t)v * dplane + q];
-    for (int q = threadIdx.x; q < tpasses * MAX_BINS; q += blockDim.x) sh[q] = 0;
-    __syncthreads();
-    for (int r = threadIdx.x; r < gy; r += blockDim.x) {  // prefix along x
-        int run = 0;
-        for (int x = 0; x < gx; ++x) { run += cs[r * dw + x]; cs[r * dw + x] = run; }
-    }
-    __syncthreads();
-    for (int x = threadIdx.x; x < gx; x += blockDim.x) {  // prefix along y
-        int run = 0;
-        for (int r = 0; r < gy; ++r) { run += cs[r * dw + x]; cs[r * dw + x] = run; }
-    }
-    __syncthreads();
-    // each thread: a contiguous chunk of tiles (row-major t) -> local exclusive starts
-    const int per = (T + blockDim.x - 1) / blockDim.x;
-    const int t0 = threadIdx.x * per, t1 = min(T, t0 + per);
-    uint32_t csum = 0;
-    for (int t = t0; t < t1; ++t) csum += (uint32_t)cs[(t / gx) * dw + (t % gx)];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t inc = csum;
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-    }
-    if (lane == 31) s_w[w] = inc;
-    __syncthreads();
-    uint32_t pre = 0, tot = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
-        pre += q < w ? s_w[q] : 0u;
-        tot += s_w[q];
-    }
-    uint32_t run = pre + inc - csum;
-    const uint32_t dmask = (1u << tbits) - 1u;
-    for (int t = t0; t < t1; ++t) {
-        const uint32_t c = (uint32_t)cs[(t / gx) * dw + (t % gx)];
-        const uint32_t g = (uint32_t)v * (uint32_t)T + (uint32_t)t;
-        counts[g] = c;
-        lstart[g] = run;
-        run += c;
-        if (c)
-            for (int p = 0; p < tpasses; ++p) atomicAdd(&sh[p * MAX_BINS + ((g >> (p * tbits)) & dmask)], c);
-    }
-    __syncthreads();
-    for (int q = threadIdx.x; q < tpasses * MAX_BINS; q += blockDim.x)
-        if (sh[q]) atomicAdd(&hist[q], sh[q]);
-    if (threadIdx.x == 0) view_tot[v] = tot;
-}
-
 // ranges[gt] = view base + local start (view bases = exclusive scan of the <= 64 view
 // totals); [0,0) for empty tiles and everywhere on capacity overflow (already flagged)
 __global__ void __launch_bounds__(256) k_ranges_finalize(const uint32_t* __restrict__ counts,
@@ -574,16 +722,6 @@ __global__ void __launch_bounds__(256) k_ranges_finalize(const uint32_t* __restr
     }
 }
 
-// launchers shared with the BUCKET binning mode (bucket.cu)
-void launch_tile_counts(const int* diff, int gx, int gy, int n_views, uint32_t* counts, uint32_t* lstart,
-                        uint32_t* view_tot, cudaStream_t s) {
-    k_tile_counts<<<n_views, 1024, sizeof(int) * (size_t)(gx + 1) * (gy + 1), s>>>(diff, gx, gy, counts, lstart, view_tot,
-                                                                                 nullptr, 0, 8);
-}
-void launch_ranges_finalize(const uint32_t* counts, const uint32_t* lstart, const uint32_t* view_tot, int n_views,
-                            uint32_t T, uint32_t cap, const uint32_t* Kd, uint2* ranges, int grid, cudaStream_t s) {
-    k_ranges_finalize<<<grid, 256, 0, s>>>(counts, lstart, view_tot, n_views, T, cap, Kd, ranges);
-}
 
 static int num_sms() {
     static int sms = 0;
@@ -612,7 +750,10 @@ cudaError_t init_binning_attributes() {
     if ((e = cudaFuncSetAttribute(k_onesweep32<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Onesweep<9>::SMEM)))
         return e;
     if ((e = cudaFuncSetAttribute(k_scan_dup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DUP_SMEM))) return e;
-    return cudaFuncSetAttribute(k_tile_counts, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if ((e = cudaFuncSetAttribute(k_slab_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(int) * BIN_MAX_SMEM_WORDS))))
+        return e;
+    return cudaSuccess;
 }
 
 template <int BITS>
@@ -632,43 +773,55 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     const int gbits = tile_gbits(T * n_views);
     const int tbits = tile_digit_bits(gbits);
     const int tpasses = tile_passes(gbits);
+    const BinPlan bp = bin_plan(proj.n_pad, n_views, W, H);
     unsigned char* ws = static_cast<unsigned char*>(scratch);
     uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);  // [depth 4 | tile 4][MAX_BINS] counts, then excl
     uint32_t* hist_excl = hist + (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS;
-    unsigned long long* vis_lb = reinterpret_cast<unsigned long long*>(ws + L.vis_lb);
     unsigned long long* dup_lb = reinterpret_cast<unsigned long long*>(ws + L.dup_lb);
     uint32_t* depth_lb = reinterpret_cast<uint32_t*>(ws + L.depth_lb);
     uint32_t* tile_lb = reinterpret_cast<uint32_t*>(ws + L.tile_lb);
     uint32_t* dk[2] = {reinterpret_cast<uint32_t*>(ws + L.dkeys), reinterpret_cast<uint32_t*>(ws + L.dkeys_alt)};
     uint32_t* dv[2] = {reinterpret_cast<uint32_t*>(ws + L.dvals), reinterpret_cast<uint32_t*>(ws + L.dvals_alt)};
+    uint32_t* tcounts = reinterpret_cast<uint32_t*>(ws + L.counts);  // per-tile totals | view-local starts
+    uint32_t* lstart = tcounts + T * n_views;
+    uint32_t* view_tot = reinterpret_cast<uint32_t*>(ws + L.view_tot);
+    uint32_t* scount = reinterpret_cast<uint32_t*>(ws + L.slab_counts);
+    uint32_t* svis = reinterpret_cast<uint32_t*>(ws + L.slab_vis);
     const int64_t elem_tiles = (count + SORT_TILE - 1) / SORT_TILE;
     const int64_t os_elem_tiles = (count + OS_TILE - 1) / OS_TILE;
     const int64_t os_key_tiles = ((int64_t)cap + OS_TILE - 1) / OS_TILE;
     uint32_t* Kd = bins.K;      // [0] = K entries
     uint32_t* Md = bins.K + 1;  // [1] = M visible pairs
+    const int sms = num_sms();
+    const size_t dplane = (size_t)(gx + 1) * (gy + 1);
     cudaError_t e;
     prof->begin(ST_COMPACT, s);
     if ((e = cudaMemsetAsync(fl->tickets, 0, sizeof(fl->tickets), s))) return e;
     if ((e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS, s))) return e;
-    if ((e = cudaMemsetAsync(vis_lb, 0, sizeof(unsigned long long) * (elem_tiles + 1), s))) return e;
     if ((e = cudaMemsetAsync(dup_lb, 0, sizeof(unsigned long long) * (elem_tiles + 1), s))) return e;
     if ((e = cudaMemsetAsync(depth_lb, 0, sizeof(uint32_t) * DEPTH_PASSES * 256 * (size_t)(os_elem_tiles + 1), s))) return e;
     if ((e = cudaMemsetAsync(tile_lb, 0, sizeof(uint32_t) * (size_t)tpasses * (1 << tbits) * (size_t)(os_key_tiles + 1), s)))
         return e;
-    int* diff = reinterpret_cast<int*>(ws + L.diff);
-    uint32_t* tcounts = reinterpret_cast<uint32_t*>(ws + L.counts);
-    uint32_t* view_tot = reinterpret_cast<uint32_t*>(ws + L.view_tot);
-    const size_t dplane = (size_t)(gx + 1) * (gy + 1);
-    if ((e = cudaMemsetAsync(diff, 0, sizeof(int) * dplane * n_views, s))) return e;
     if ((e = cudaMemsetAsync(bins.K, 0, sizeof(uint32_t) * 4, s))) return e;
-    if (elem_tiles > 0)
-        k_vis_compact<<<(unsigned)elem_tiles, SORT_THREADS, 0, s>>>(proj.tiles, proj.depth, count, dk[0], dv[0], vis_lb,
-                                                                     fl, Md);
-    prof->end(s);
+    if (bp.slabs > 0) {
+        k_slab_count<<<(unsigned)bp.slabs, SLAB_THREADS, sizeof(int) * dplane, s>>>(
+            proj.tiles, reinterpret_cast<const short4*>(proj.rect), proj.depth, proj.n_pad, (int)bp.S, (int)bp.spv, gx, gy,
+            scount, svis, hist);
+        k_slab_sum<<<dim3((unsigned)((T + 255) / 256), (unsigned)n_views), 256, 0, s>>>(scount, (int)bp.spv, (int)T,
+                                                                                        tcounts);
+        k_view_scan<<<n_views, 1024, 0, s>>>(tcounts, (int)T, lstart, view_tot, hist + DEPTH_PASSES * MAX_BINS, tpasses,
+                                             tbits);
+    } else {
+        if ((e = cudaMemsetAsync(tcounts, 0, sizeof(uint32_t) * 2 * T * n_views, s))) return e;
+        if ((e = cudaMemsetAsync(view_tot, 0, sizeof(uint32_t) * n_views, s))) return e;
+    }
+    k_totals<<<1, 1024, 0, s>>>(view_tot, n_views, svis, (int)bp.slabs, cap, Kd, fl);
+    if (bp.slabs > 0)
+        k_slab_compact<<<(unsigned)bp.slabs, SLAB_THREADS, 0, s>>>(proj.tiles, proj.depth, proj.n_pad, (int)bp.S,
+                                                                  (int)bp.spv, svis, dk[0], dv[0]);
+    prof->end(s, bp.slabs > 0 ? 5 : 1);
     // depth digits (LSD: least significant first) on the visible pairs
     prof->begin(ST_DEPTH_SORT, s);
-    const int sms = num_sms();
-    k_hist_depth<<<sms * 2, 256, 0, s>>>(dk[0], Md, hist);
     k_hist_scan<<<1, 32 * DEPTH_PASSES, 0, s>>>(hist, hist_excl, DEPTH_PASSES, 256);
     int cur = 0;
     for (int p = 0; p < DEPTH_PASSES; ++p) {
@@ -676,26 +829,24 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
                     depth_lb + (size_t)p * 256 * (os_elem_tiles + 1), &fl->tickets[TK_DEPTH + p], fl, s);
         cur ^= 1;
     }
-    prof->end(s, DEPTH_PASSES + 2);
-    // offsets in depth order + duplication (+ tile-digit histograms)
+    prof->end(s, DEPTH_PASSES + 1);
+    // offsets in depth order + duplication
     prof->begin(ST_DUPLICATE, s);
-    uint32_t* thist = hist + DEPTH_PASSES * MAX_BINS;
-    uint32_t* thist_excl = hist_excl + DEPTH_PASSES * MAX_BINS;
     if (elem_tiles > 0)
         k_scan_dup<<<(unsigned)elem_tiles, SORT_THREADS, DUP_SMEM, s>>>(dv[cur], Md,
                                                                          reinterpret_cast<const short4*>(proj.rect),
                                                                          proj.n_pad, gx, gy, (uint32_t)T, bins.keys,
-                                                                         bins.vals, cap, dup_lb, fl, Kd, diff);
+                                                                         bins.vals, cap, dup_lb, fl, Kd);
     prof->end(s);
-    // per-tile entry counts -> ranges and tile-digit histograms
+    // per-tile entry counts -> ranges
     prof->begin(ST_RANGES, s);
-    k_tile_counts<<<n_views, 1024, sizeof(int) * dplane, s>>>(diff, gx, gy, tcounts, tcounts + T * n_views, view_tot, thist,
-                                                               tpasses, tbits);
-    k_ranges_finalize<<<sms * 2, 256, 0, s>>>(tcounts, tcounts + T * n_views, view_tot, n_views, (uint32_t)T, cap, Kd,
+    k_ranges_finalize<<<sms * 2, 256, 0, s>>>(tcounts, lstart, view_tot, n_views, (uint32_t)T, cap, Kd,
                                               reinterpret_cast<uint2*>(bins.ranges));
-    prof->end(s, 2);
+    prof->end(s);
     // tile digits on the K entries
     prof->begin(ST_TILE_SORT, s);
+    uint32_t* thist = hist + DEPTH_PASSES * MAX_BINS;
+    uint32_t* thist_excl = hist_excl + DEPTH_PASSES * MAX_BINS;
     k_hist_scan<<<1, 32 * MAX_TILE_PASSES, 0, s>>>(thist, thist_excl, tpasses, 1 << tbits);
     uint32_t* ka = bins.keys;
     uint32_t* kb = bins.keys_alt;

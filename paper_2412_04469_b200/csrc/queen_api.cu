@@ -17,7 +17,6 @@ struct queen_ctx {
     int64_t ws_keys = 0;
     queen::WsLayout L{};
     queen::Prof prof;
-    int bin_mode = QUEEN_BIN_ONESWEEP;
     cudaEvent_t binned = nullptr;  // recorded by queen_render_views after binning (queen_wait_binned)
     std::string err;
 };
@@ -28,8 +27,6 @@ float host_theta0(float tau, float g0, float g1) {
     return (float)((double)tau * std::log(-(double)g0 / (double)g1));
 }
 cudaError_t init_binning_attributes();
-cudaError_t launch_bin_bucket(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
-                              const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof, int sms);
 int key_passes(int64_t gtiles);
 size_t ans_encode(const int8_t* lat, int L, int n, int n_pad, std::vector<unsigned char>& out);
 cudaError_t launch_ans_decode(const void* stream_dev, int L, int n, int n_pad, int8_t* out, DevFlags* fl,
@@ -253,28 +250,16 @@ queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_
     const int64_t T = (int64_t)((W + 15) / 16) * ((H + 15) / 16);
     if (bins->keys_cap < 1 || bins->keys_cap > MAX_KEYS) return fail(ctx, QUEEN_ERR_SHAPE, "keys_cap outside [1, 2^30)");
     if (T * n_views >= (1ll << 31)) return fail(ctx, QUEEN_ERR_SHAPE, "too many tiles in one batch");
+    if (!bin_plan(proj->n_pad, n_views, W, H).ok)
+        return fail(ctx, QUEEN_ERR_SHAPE, "view too large: its (gx+1)(gy+1) tile grid exceeds 48K words (> 4K views)");
     // scratch must cover this batch
     WsLayout need = ws_layout(proj->n_pad, n_views, W, H, bins->keys_cap);
-    if (need.key_tiles > ctx->L.key_tiles || need.elem_tiles > ctx->L.elem_tiles || need.elems > ctx->L.elems)
+    if (need.key_tiles > ctx->L.key_tiles || need.elem_tiles > ctx->L.elem_tiles || need.elems > ctx->L.elems ||
+        !scratch_fits(need, ctx->L))
         return fail(ctx, QUEEN_ERR_SHAPE, "workspace scratch too small for this batch");
-    cudaError_t e;
-    if (ctx->bin_mode == QUEEN_BIN_ONESWEEP) {
-        e = launch_bin_sort(*proj, n_views, W, H, *bins, ctx->ws, ctx->L, flags_of(ctx), static_cast<cudaStream_t>(stream),
-                            &ctx->prof);
-    } else {
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-        e = launch_bin_bucket(*proj, n_views, W, H, *bins, ctx->ws, ctx->L, flags_of(ctx),
-                              static_cast<cudaStream_t>(stream), &ctx->prof, sms);
-    }
+    cudaError_t e = launch_bin_sort(*proj, n_views, W, H, *bins, ctx->ws, ctx->L, flags_of(ctx),
+                                    static_cast<cudaStream_t>(stream), &ctx->prof);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "bin_sort");
-    return QUEEN_OK;
-}
-
-queen_status queen_set_binning(queen_ctx* ctx, int32_t mode) {
-    if (!ctx) return QUEEN_ERR_INVALID_ARG;
-    if (mode != QUEEN_BIN_BUCKET && mode != QUEEN_BIN_ONESWEEP) return fail(ctx, QUEEN_ERR_INVALID_ARG, "binning mode");
-    ctx->bin_mode = mode;
     return QUEEN_OK;
 }
 

@@ -68,11 +68,37 @@ inline int tile_passes(int gbits) {
     return (gbits + db - 1) / db;
 }
 
+// Binning counts (binning.cu K3a): each view's elements are cut into slabs of S consecutive
+// indices; one CTA per slab keeps the view's tile grid in shared memory as a difference
+// array, and one CTA per view sums the slabs' tile counts in shared memory, so a view's tile
+// grid must fit in BIN_MAX_SMEM_WORDS words: views up to 4K (241 x 136) qualify; larger
+// ones are rejected with QUEEN_ERR_SHAPE.
+constexpr int BIN_MAX_SMEM_WORDS = 48 * 1024;
+struct BinPlan {
+    bool ok;
+    int64_t S, spv, slabs;  // slab size, slabs per view, slabs in the batch
+};
+inline BinPlan bin_plan(int64_t n_pad, int64_t n_views, int W, int H) {
+    const int64_t gx = (W + 15) / 16, gy = (H + 15) / 16;
+    BinPlan p{};
+    p.ok = (gx + 1) * (gy + 1) <= BIN_MAX_SMEM_WORDS;
+    // ~32 slabs per view (S depends on n_pad only, so a smaller batch never needs more
+    // slab-count space than the workspace was carved for), multiples of 1024 in [2048, 65536]
+    (void)n_views;
+    int64_t S = (n_pad + 31) / 32;
+    S = (S + 1023) / 1024 * 1024;
+    S = S < 2048 ? 2048 : (S > 65536 ? 65536 : S);
+    p.S = S;
+    p.spv = n_pad > 0 ? (n_pad + S - 1) / S : 0;
+    p.slabs = p.spv * n_views;
+    return p;
+}
+
 // Workspace carve-up (bytes, 256-aligned) for (n_pad, n_views, W, H, keys_cap).
 struct WsLayout {
     // scratch (bin_sort)
-    size_t flags, hist, vis_lb, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, diff, counts, view_tot,
-        total_scratch;
+    size_t flags, hist, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, counts, view_tot, slab_counts,
+        slab_vis, total_scratch;
     // render_views buffers
     size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, total;
     int64_t key_tiles, elem_tiles, os_key_tiles, os_elem_tiles, T, elems;
@@ -92,7 +118,6 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     size_t o = 0;
     L.flags = o; o += align256(sizeof(DevFlags));
     L.hist = o; o += align256(sizeof(uint32_t) * (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS * 2);
-    L.vis_lb = o; o += align256(sizeof(unsigned long long) * (L.elem_tiles + 1));
     L.dup_lb = o; o += align256(sizeof(unsigned long long) * (L.elem_tiles + 1));
     L.depth_lb = o; o += align256(sizeof(uint32_t) * DEPTH_PASSES * 256 * (L.os_elem_tiles + 1));
     L.tile_lb = o; o += align256(sizeof(uint32_t) * MAX_TILE_PASSES * MAX_BINS * (L.os_key_tiles + 1));
@@ -100,9 +125,11 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     L.dkeys_alt = o; o += align256(sizeof(uint32_t) * L.elems);
     L.dvals = o; o += align256(sizeof(uint32_t) * L.elems);
     L.dvals_alt = o; o += align256(sizeof(uint32_t) * L.elems);
-    L.diff = o; o += align256(sizeof(int32_t) * (size_t)n_views * (gx + 1) * (gy + 1));
-    L.counts = o; o += align256(sizeof(uint32_t) * 3 * (size_t)n_views * L.T);  // counts | local starts | fill
+    L.counts = o; o += align256(sizeof(uint32_t) * 2 * (size_t)n_views * L.T);  // counts | local starts
     L.view_tot = o; o += align256(sizeof(uint32_t) * (size_t)n_views);
+    const BinPlan bp = bin_plan(n_pad, n_views, W, H);
+    L.slab_counts = o; o += align256(sizeof(uint32_t) * (size_t)(bp.ok ? bp.slabs : 0) * L.T);
+    L.slab_vis = o; o += align256(sizeof(uint32_t) * (size_t)(bp.slabs + 1));
     L.total_scratch = o;
     L.rec = o; o += align256(sizeof(float) * REC_WORDS * L.elems);
     L.depth = o; o += align256(sizeof(uint32_t) * L.elems);
@@ -116,6 +143,18 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     L.K = o; o += align256(sizeof(uint32_t) * 4);
     L.total = o;
     return L;
+}
+
+// every scratch region of `need` fits in the corresponding region of `have`
+inline bool scratch_fits(const WsLayout& need, const WsLayout& have) {
+    const size_t WsLayout::*r[] = {&WsLayout::flags,      &WsLayout::hist,        &WsLayout::dup_lb,
+                                   &WsLayout::depth_lb,   &WsLayout::tile_lb,     &WsLayout::dkeys,
+                                   &WsLayout::dkeys_alt,  &WsLayout::dvals,       &WsLayout::dvals_alt,
+                                   &WsLayout::counts,     &WsLayout::view_tot,    &WsLayout::slab_counts,
+                                   &WsLayout::slab_vis,   &WsLayout::total_scratch};
+    for (size_t q = 0; q + 1 < sizeof(r) / sizeof(r[0]); ++q)
+        if (need.*r[q + 1] - need.*r[q] > have.*r[q + 1] - have.*r[q]) return false;
+    return true;
 }
 
 // ---------------------------------------------------------------------------

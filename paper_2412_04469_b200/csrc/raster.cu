@@ -67,7 +67,34 @@ __device__ __forceinline__ void composite2(Px2& p, float q0, float q1, bool h0, 
     p.T = __fmul2_rn(p.T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
 }
 
-template <bool COUNT, int RPT>
+// Can the record's alpha >= 1/255 region {p2 >= T2} reach a pixel centre of [x0,x1] x [y0,y1]?
+// Conservative (false positives only cost time): p2 is a concave quadratic in (x, y), so its
+// maximum over the rectangle is 0 if the centre (u, v) lies inside, else it sits on an edge,
+// at the edge's 1D maximiser clamped to the edge.  The maximum is compared with T2 minus a
+// slack of 1e-5 of the quadratic's magnitude over the bounding box (>> the few-ulp rounding
+// of either evaluation).  Approximate division only moves the maximiser slightly, which
+// lowers the edge value by a second-order amount (covered by the slack).
+__device__ __forceinline__ bool touches(const float4& a, const float4& q, float x0, float x1, float y0, float y1) {
+    if (a.x + a.z < x0 || a.x - a.z > x1 || a.y + a.w < y0 || a.y - a.w > y1) return false;
+    if (a.x >= x0 && a.x <= x1 && a.y >= y0 && a.y <= y1) return true;
+    const float A = q.x, B = q.y, C = q.z;
+    const float iA = __fdividef(-0.5f * B, A), iC = __fdividef(-0.5f * B, C);
+    const float dxl = a.x - x1, dxh = a.x - x0, dyl = a.y - y1, dyh = a.y - y0;
+    float best = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const float dy = e ? dyl : dyh;  // edge y = y0 (dy = v - y0) or y = y1
+        const float dx = fminf(fmaxf(iA * dy, dxl), dxh);
+        best = fmaxf(best, fmaf(A * dx, dx, fmaf(C * dy, dy, B * dx * dy)));
+        const float ex = e ? dxl : dxh;  // edge x = x0 or x = x1
+        const float ey = fminf(fmaxf(iC * ex, dyl), dyh);
+        best = fmaxf(best, fmaf(A * ex, ex, fmaf(C * ey, ey, B * ex * ey)));
+    }
+    const float S = fabsf(A) * a.z * a.z + fabsf(B) * a.z * a.w + fabsf(C) * a.w * a.w;
+    return best >= q.w - (1e-5f * S + 1e-6f);
+}
+
+template <bool COUNT, int RPT, bool WMASK>
 __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ rec, int n_pad, const uint2* __restrict__ ranges,
                                                     const uint32_t* __restrict__ vals, int W, int H, int gx, int T, float bg0,
                                                     float bg1, float bg2, float* __restrict__ rgb_out, float* __restrict__ T_out,
@@ -79,6 +106,7 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
     __shared__ __align__(16) float4 sA[2][BATCH];  // u, v, hx, hy
     __shared__ __align__(16) float4 sB[2][BATCH];  // A2, B2, C2, T2
     __shared__ __align__(16) float4 sC[2][BATCH];  // o, r, g, b
+    __shared__ uint8_t s_list[NT / 32][BATCH];         // per-warp record list of the batch
     const int gt = blockIdx.x;
     const int v = gt / T;
     const int t = gt - v * T;
@@ -154,18 +182,38 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
         // break would leave the warp split for the rest of the batch); terminated pixels simply
         // never hit again, and fully-terminated warps skip the batch.
         if (__any_sync(0xffffffffu, any_alive)) {
+            // Records this warp must visit, as a 64-bit mask over the batch.  WMASK: only those
+            // whose alpha >= 1/255 ellipse can reach a pixel centre of the warp's 16 x (32/16*RPT)
+            // sub-tile (touches(), conservative); otherwise every record.  Skipping a record no
+            // pixel of the warp hits changes nothing, so the output is bit-identical either way
+            // (test_gpu_parity::test_blend_warp_mask_is_exact).
+            const float wx0 = (float)((t % gx) * 16), wy0 = (float)((t / gx) * 16 + (threadIdx.x >> 5) * (32 / 16) * RPT);
+            // the warp's record list (batch order) in shared memory
+            uint8_t* lst = s_list[threadIdx.x >> 5];
+            int nq = 0;
+#pragma unroll
+            for (int e = 0; e < BATCH / 32; ++e) {
+                const int q = (threadIdx.x & 31) + 32 * e;
+                bool want = q < cnt;
+                if (WMASK && want) want = touches(sA[s][q], sB[s][q], wx0, wx0 + 15.0f, wy0, wy0 + (float)((32 / 16) * RPT - 1));
+                const uint32_t bal = __ballot_sync(0xffffffffu, want);
+                if (want) lst[nq + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = (uint8_t)q;
+                nq += __popc(bal);
+            }
+            __syncwarp();
 #pragma unroll 2
-            for (int q = 0; q < cnt; ++q) {
+            for (int i = 0; i < nq; ++i) {
+                const int q = lst[i];
                 const float4 a = sA[s][q];  // u, v, hx, hy
                 const float dx = a.x - fx;
                 if (COUNT) {
 #pragma unroll
                     for (int k = 0; k < NP; ++k) ev += (int)!(p[k].T.x < 1e-4f) + (int)!(p[k].T.y < 1e-4f);
                 }
-                // Conservative box cull: a pixel with p2 >= T2 satisfies |dx| <= hx and |dy| <= hy
-                // (bounding box of the alpha = 1/255 ellipse, 1e-4 relative slack, K7);
-                // this thread's rows are fyc +- hspan.  Skips never change a decision.
-                if (!COUNT && (fabsf(dx) > a.z || fabsf(a.y - fyc) > a.w + hspan)) continue;
+                // Without the warp mask: conservative per-thread box cull (a pixel with p2 >= T2
+                // satisfies |dx| <= hx and |dy| <= hy, K7; this thread's rows are
+                // fyc +- hspan).  Skips never change a decision.
+                if (!COUNT && !WMASK && (fabsf(dx) > a.z || fabsf(a.y - fyc) > a.w + hspan)) continue;
                 const float4 bq = sB[s][q];  // A2, B2, C2, T2
                 const float tA = bq.x * dx;
                 const float tB = bq.y * dx;
@@ -255,11 +303,15 @@ cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges
     const int64_t blocks = (int64_t)T * n_views;
     if (blocks == 0) return cudaSuccess;
     if (blend_rpt() == 8)
-        k_blend<false, 8><<<(unsigned)blocks, 32, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
+        k_blend<false, 8, true><<<(unsigned)blocks, 32, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
                                                           reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0,
                                                           bg1, bg2, rgb_out, T_out, nullptr, nullptr);
+    else if (getenv("QUEEN_BLEND_NOMASK"))  // test hook: per-thread box cull only
+        k_blend<false, BLEND_RPT, false><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(
+            reinterpret_cast<const float4*>(rec), n_pad, reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0, bg1,
+            bg2, rgb_out, T_out, nullptr, nullptr);
     else
-        k_blend<false, BLEND_RPT><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
+        k_blend<false, BLEND_RPT, true><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
                                                        reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0, bg1,
                                                        bg2, rgb_out, T_out, nullptr, nullptr);
     return cudaGetLastError();
@@ -273,7 +325,7 @@ cudaError_t launch_blend_counts(const float* rec, int n_pad, const uint32_t* ran
     cudaMemsetAsync(evaluated, 0, sizeof(long long) * n_views, s);
     cudaMemsetAsync(composited, 0, sizeof(long long) * n_views, s);
     if (blocks == 0) return cudaSuccess;
-    k_blend<true, BLEND_RPT><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
+    k_blend<true, BLEND_RPT, false><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
                                                   reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, 0.f, 0.f, 0.f,
                                                   nullptr, nullptr, evaluated, composited);
     return cudaGetLastError();

@@ -97,8 +97,7 @@ class Player:
     lane's kernels wait for free slots: 2 lanes 3.77 ms vs 1 lane 3.55 ms), hence lanes=1."""
 
     def __init__(self, planes, n: int, deg: int, cams, *, device: int = 0, keys_cap: int | None = None,
-                 views_per_batch: int | None = None, bg=(0.0, 0.0, 0.0), with_T: bool = False, lanes: int = 1,
-                 binning: str = "onesweep"):
+                 views_per_batch: int | None = None, bg=(0.0, 0.0, 0.0), with_T: bool = False, lanes: int = 1):
         self.dev = torch.device(f"cuda:{device}")
         self.device = device
         if isinstance(planes, np.ndarray):
@@ -120,8 +119,6 @@ class Player:
         self.cam_arrays = [camera_array(self.cams[a:b]) for a, b in self.batches]
         self.n_lanes = max(1, min(lanes, len(self.batches)))
         self.ctxs = [Context(device) for _ in range(self.n_lanes)]
-        for c in self.ctxs:
-            c.set_binning(binning)
         self.ctx = self.ctxs[0]
         self.streams = [None] + [torch.cuda.Stream(device=self.dev) for _ in range(self.n_lanes - 1)]
         self.bg = bg

@@ -18,11 +18,9 @@ def to_np(t):
 class Stages:
     """Explicit project / bin_sort / rasterize buffers for one batch of views."""
 
-    def __init__(self, planes: np.ndarray, n: int, deg: int, cams, keys_cap: int | None = None, device=0,
-                 binning: str = "onesweep"):
+    def __init__(self, planes: np.ndarray, n: int, deg: int, cams, keys_cap: int | None = None, device=0):
         self.dev = torch.device(f"cuda:{device}")
         self.ctx = Context(device)
-        self.ctx.set_binning(binning)
         self.planes_t = torch.from_numpy(np.ascontiguousarray(planes, np.float32)).to(self.dev)
         self.n, self.deg, self.cams = n, deg, list(cams)
         self.n_pad = planes.shape[1]

@@ -135,9 +135,6 @@ def test_device_errors_reported():
 
 
 # ------------------------------------------------------------------ render stages
-BINNING = ["bucket", "onesweep"]
-
-
 def _render_case(name, n=None, views=None, **over):
     cfg, sc = _scene(name, n, **over)
     cams = synth.make_cameras(cfg, views)
@@ -179,14 +176,13 @@ def _check_image(rgb, T, rref, Tref):
                                   ("n3dv", 20003, 3, {"width": 333, "height": 250, "focal": 280.0}),
                                   ("immersive", 12001, 5, {"width": 320, "height": 240, "focal": 160.0}),
                                   ("meetroom", 8000, 13, {"width": 160, "height": 90, "focal": 125.0})])
-@pytest.mark.parametrize("binning", BINNING)
-def test_render_stages_parity(case, binning):
+def test_render_stages_parity(case):
     from tests.gpu_helpers import Stages
     name, n, views, over = case
     cfg, sc, cams = _render_case(name, n, views, **over)
     W, H = cams[0].width, cams[0].height
     proj, bins, rgb, T = oracle.render(sc.planes, sc.n, sc.deg, cams)
-    st = Stages(sc.planes, sc.n, sc.deg, cams, binning=binning).run()
+    st = Stages(sc.planes, sc.n, sc.deg, cams).run()
     gp = st.proj_np()
     _check_proj(gp, proj, sc.n)
     gb = st.bins_np()
@@ -198,8 +194,7 @@ def test_render_stages_parity(case, binning):
     assert s == 0
 
 
-@pytest.mark.parametrize("binning", BINNING)
-def test_render_big_gaussians_ragged(binning):
+def test_render_big_gaussians_ragged():
     """Large, overlapping, off-screen and near-plane Gaussians; ragged 70x45 image; degree 3."""
     from tests.gpu_helpers import Stages
     rng = np.random.default_rng(11)
@@ -209,20 +204,19 @@ def test_render_big_gaussians_ragged(binning):
                      rng.normal(0, 0.5, (n, 16, 3)), 3)
     cams = [synth.make_camera(np.eye(3), np.zeros(3), 40.0, 40.0, 70, 45)]
     proj, bins, rgb, T = oracle.render(pl, n, 3, cams, bg=(0.1, 0.2, 0.3))
-    st = Stages(pl, n, 3, cams, binning=binning).run(bg=(0.1, 0.2, 0.3))
+    st = Stages(pl, n, 3, cams).run(bg=(0.1, 0.2, 0.3))
     gp = st.proj_np()
     _check_proj(gp, proj, n)
     _check_bins(st.bins_np(), bins, gp["depth"], st.T)
     _check_image(*st.image_np(), rgb, T)
 
 
-@pytest.mark.parametrize("binning", BINNING)
-def test_empty_and_all_culled(binning):
+def test_empty_and_all_culled():
     from tests.gpu_helpers import Stages
     pl = planes_from([[0, 0, -5.0]] * 8, [[1, 0, 0, 0]] * 8, [[-3] * 3] * 8, [2.0] * 8,
                      [np.zeros((1, 3))] * 8, 0)
     cams = [synth.make_camera(np.eye(3), np.zeros(3), 30.0, 30.0, 40, 24)]
-    st = Stages(pl, 8, 0, cams, binning=binning).run(bg=(0.25, 0.5, 1.0))
+    st = Stages(pl, 8, 0, cams).run(bg=(0.25, 0.5, 1.0))
     rgb, T = st.image_np()
     assert st.bins_np()["K"] == 0
     assert np.all(T == 1.0) and np.all(rgb[0, 0] == 0.25) and np.all(rgb[0, 2] == 1.0)
@@ -242,34 +236,33 @@ def test_nonfinite_warns_and_culls():
     _check_image(*st.image_np(), rgb, T)
 
 
-@pytest.mark.parametrize("binning", BINNING)
-def test_capacity_error_reports_needed_keys(binning):
+def test_capacity_error_reports_needed_keys():
     from tests.gpu_helpers import Stages
     cfg, sc, cams = _render_case("tiny")
     proj, bins, rgb, T = oracle.render(sc.planes, sc.n, sc.deg, cams)
-    st = Stages(sc.planes, sc.n, sc.deg, cams, keys_cap=max(1, bins["K"] // 2), binning=binning).run()
+    st = Stages(sc.planes, sc.n, sc.deg, cams, keys_cap=max(1, bins["K"] // 2)).run()
     s, info = st.ctx.check_status()
     assert s == -5 and info == bins["K"]
     assert st.bins_np()["K"] == 0  # nothing emitted, every range empty
     assert not np.any(st.ranges.cpu().numpy())
 
 
-@pytest.mark.parametrize("binning", BINNING)
-def test_long_tile_lists(binning):
-    """Tiles whose lists exceed the bucket sort's shared-memory capacity (2048 entries): 6000
-    small Gaussians crowded into a 40x36 image (some tiles hold thousands of entries, forcing the
-    in-place global-memory network), equal depths included (ties broken by index)."""
+def test_long_tile_lists():
+    """Very long tile lists (thousands of entries; several onesweep tiles per gt): 12000 small
+    Gaussians crowded into a 40x36 image, 30 % of them at one shared depth (ties broken by
+    index)."""
     from tests.gpu_helpers import Stages
     rng = np.random.default_rng(23)
-    n = 6000
+    n = 12000
     z = np.where(rng.random(n) < 0.3, 2.0, rng.uniform(1.0, 4.0, n))  # 30 % share one depth
     pos = np.stack([rng.normal(0, 0.08, n) * z, rng.normal(0, 0.08, n) * z, z], 1)
     pl = planes_from(pos, rng.standard_normal((n, 4)), rng.normal(math.log(0.01), 0.3, (n, 3)), rng.normal(-1, 1, n),
                      rng.normal(0, 0.5, (n, 1, 3)), 0)
     cams = [synth.make_camera(np.eye(3), np.zeros(3), 60.0, 60.0, 40, 36)]
     proj, bins, rgb, T = oracle.render(pl, n, 0, cams)
-    assert np.diff(bins["ranges"], axis=1).max() > 2048
-    st = Stages(pl, n, 0, cams, binning=binning).run()
+    lens = np.diff(bins["ranges"].astype(np.int64), axis=1)
+    assert lens.max() > 4096 and np.any((lens > 256) & (lens <= 4096))
+    st = Stages(pl, n, 0, cams).run()
     gp = st.proj_np()
     _check_proj(gp, proj, n)
     _check_bins(st.bins_np(), bins, gp["depth"], st.T)
@@ -357,3 +350,62 @@ def test_full_size_frame_sampled(name):
         g = rgb[b0 + pix[:, 0], :, pix[:, 2], pix[:, 1]]
         assert np.abs(np.clip(g, 0, 1) - np.clip(orgb, 0, 1)).max() <= RGB_TOL
         del proj, bins
+
+
+# ------------------------------------------------------------------ blend work (culling is exact)
+def test_blend_warp_mask_is_exact(monkeypatch):
+    """The blend's per-warp record mask (touches(): conservative ellipse-vs-sub-tile test) only
+    skips records no pixel of the warp hits: the image is bit-identical to the unmasked kernel
+    (per-thread box cull only), on a scene with thin, rotated and large Gaussians."""
+    from tests.gpu_helpers import Stages
+    rng = np.random.default_rng(31)
+    n = 6001
+    pos = np.stack([rng.uniform(-2, 2, n), rng.uniform(-1.5, 1.5, n), rng.uniform(0.5, 6, n)], 1)
+    scale = np.stack([rng.normal(-4.5, 1.2, n), rng.normal(-2.5, 1.0, n), rng.normal(-3, 1, n)], 1)
+    pl = planes_from(pos, rng.standard_normal((n, 4)), scale, rng.normal(0.5, 2.0, n), rng.normal(0, 0.5, (n, 4, 3)), 1)
+    cams = [synth.make_camera(np.eye(3), np.zeros(3), 300.0, 300.0, 333, 250)]
+    st = Stages(pl, n, 1, cams).project().bin_sort().rasterize()
+    rgb_a, T_a = st.image_np()
+    monkeypatch.setenv("QUEEN_BLEND_NOMASK", "1")
+    st.rasterize()
+    rgb_b, T_b = st.image_np()
+    assert np.array_equal(rgb_a.view(np.uint32), rgb_b.view(np.uint32))
+    assert np.array_equal(T_a.view(np.uint32), T_b.view(np.uint32))
+    proj, bins, rgb, T = oracle.render(pl, n, 1, cams)
+    _check_image(rgb_a, T_a, rgb, T)
+
+
+def test_blend_counts_match_oracle():
+    """queen_blend_counts (the bench's roofline work counters) == the oracle's counts: evaluated
+    (alive pixel x record) and composited pairs; equal up to the rare pixel whose T crosses 1e-4
+    one record apart (GPU ex2.approx vs the oracle's exp2)."""
+    import paper_2412_04469_b200 as Q
+    from tests.gpu_helpers import Stages
+    cfg, sc, cams = _render_case("n3dv", 20003, 3, width=333, height=250, focal=280.0)
+    W, H = cams[0].width, cams[0].height
+    proj = oracle.project(sc.planes, sc.n, sc.deg, cams)
+    bins = oracle.bin_sort(proj, W, H)
+    ev_o, cp_o = oracle.blend_counts(proj, bins, W, H)
+    st = Stages(sc.planes, sc.n, sc.deg, cams).project().bin_sort()
+    e = torch.zeros(len(cams), dtype=torch.int64, device="cuda")
+    c = torch.zeros_like(e)
+    Q.queen_blend_counts(st.ctx, st.proj, st.bins, cams, e, c)
+    e, c = e.cpu().numpy(), c.cpu().numpy()
+    assert np.all(np.abs(e - ev_o) <= 1e-4 * ev_o + 50), (e, ev_o)
+    assert np.all(np.abs(c - cp_o) <= 1e-4 * cp_o + 5), (c, cp_o)
+
+
+def test_view_larger_than_4k_rejected():
+    """Binning keeps a view's tile grid in shared memory: an 8K view is refused with
+    QUEEN_ERR_SHAPE (no silent fallback), a 4K view is accepted."""
+    import paper_2412_04469_b200 as Q
+    from tests.gpu_helpers import Stages
+    pl = planes_from([[0, 0, 3.0]] * 4, [[1, 0, 0, 0]] * 4, [[-2] * 3] * 4, [2.0] * 4, [np.zeros((1, 3))] * 4, 0)
+    big = [synth.make_camera(np.eye(3), np.zeros(3), 3000.0, 3000.0, 7680, 4320)]
+    st = Stages(pl, 4, 0, big, keys_cap=4096).project()
+    with pytest.raises(Q.QueenError) as ei:
+        st.bin_sort()
+    assert ei.value.status == -2  # QUEEN_ERR_SHAPE
+    ok = [synth.make_camera(np.eye(3), np.zeros(3), 3000.0, 3000.0, 3840, 2160)]
+    st = Stages(pl, 4, 0, ok, keys_cap=1 << 20).run()
+    assert st.bins_np()["K"] > 0

@@ -1,0 +1,3 @@
+python -m pytest tests/ -x -q -m gpu 2>&1 | tail -2
+python tools/stage_times.py n3dv 10
+python tools/stage_times.py immersive 5

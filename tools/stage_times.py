@@ -1,0 +1,28 @@
+"""Per-stage device milliseconds of one N3DV-shaped frame (libqueen's stage profiler), for
+quick A/B experiments: python tools/stage_times.py [config] [frames]."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from harness import synth
+from paper_2412_04469_b200.runtime import Player, device_packet
+
+name = sys.argv[1] if len(sys.argv) > 1 else "n3dv"
+frames = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+cfg = synth.get_config(name)
+sc = synth.make_scene(cfg)
+cams = synth.make_cameras(cfg)
+pl = Player(sc.planes, sc.n, sc.deg, cams)
+pkt = device_packet(synth.make_packet(sc, 1), pl.dev)
+pl.fit_capacity()
+for _ in range(3):
+    pl.frame(pkt)
+torch.cuda.synchronize()
+pl.profile(True)
+for _ in range(frames):
+    pl.frame(pkt)
+prof = pl.profile_read()
+print(name, {k: round(ms / frames, 4) for k, (ms, n) in prof.items()}, "total", round(sum(ms for ms, _ in prof.values()) / frames, 4))
