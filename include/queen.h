@@ -125,13 +125,14 @@ typedef struct {
 /* Binning buffers for one batch of equally-sized views (gt = view*T + tile, T = gx*gy).
  * The entries are the (16x16 tile, Gaussian) pairs, sorted by the composite key
  * (gt << 31 | depth bits) and then Gaussian index:
- *   keys/vals (+ _alt ping-pong) [keys_cap] u32: key = gt of the entry, val = Gaussian
- *            index (the entry's full sort key is (gt << 31) | proj.depth[view][val])
+ *   vals (+ vals_alt ping-pong) [keys_cap] u32: the Gaussian index of each sorted entry
+ *            (the entry's full sort key is (gt << 31) | proj.depth[view][val], gt = the
+ *            range holding it); keys / keys_alt [keys_cap] u32: sort scratch
  *   ranges[n_views*T][2] u32  [first, last+1) of gt in the sorted entries, [0,0) if empty
  *   K (device u32[4])         [0] = entries K of the batch (0 if K > keys_cap: QUEEN_ERR_CAPACITY,
  *                             no entries, all ranges [0,0)), [1] = visible (view, Gaussian) pairs,
  *                             [2] = 1 on capacity overflow
- *   sorted_in_alt             OUT (host): 1 if the sorted result is in keys_alt/vals_alt */
+ *   sorted_in_alt             OUT (host): 1 if the sorted result is in vals_alt */
 typedef struct {
     int64_t keys_cap;
     uint32_t* keys;
@@ -184,8 +185,9 @@ queen_status queen_project(queen_ctx* ctx, const queen_gaussians* scene, const q
  * index) of every visible (view, Gaussian) x overlapped tile, ordered by gt then depth
  * then index (LSD onesweep radix sort on (gt, depth)), plus tile ranges.  Uses the
  * workspace scratch.  Outputs bit-exact.  The sorted index list is
- * bins->vals (or vals_alt when bins->sorted_in_alt is set on return); keys (same buffer
- * choice) hold gt.  Views whose (ceil(W/16)+1)(ceil(H/16)+1) tile grid exceeds 48K words
+ * bins->vals (or vals_alt when bins->sorted_in_alt is set on return); entry e belongs to
+ * the gt whose range holds e.  keys / keys_alt are scratch (their content is unspecified on
+ * return).  Views whose (ceil(W/16)+1)(ceil(H/16)+1) tile grid exceeds 48K words
  * (larger than 4K) are rejected with QUEEN_ERR_SHAPE. */
 queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_camera* cams, int32_t n_views,
                             queen_bins* bins, void* stream);

@@ -52,6 +52,7 @@ __device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
 constexpr unsigned long long SCAN_AGG = 1ull << 62, SCAN_INC = 2ull << 62, SCAN_MASK = (1ull << 62) - 1;
 constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_MASK = (1u << 30) - 1;
 constexpr long long SPIN_LIMIT = 1ll << 24;
+constexpr int LB_BATCH = 8;  // onesweep look-back predecessors loaded per round trip
 constexpr int SORT_WARPS = SORT_THREADS / 32;
 
 enum : int { TK_DEPTH = 0, TK_TILE = 4, TK_VIS = 8, TK_DUP = 9 };
@@ -432,11 +433,19 @@ struct Onesweep {
     static constexpr size_t SMEM = (size_t)TILE * 4 * 2 + (size_t)NW * BINS * 4 + (size_t)BINS * 4 * 2;
 };
 
-template <int BITS>
+// Pass modes (which words travel): OS_KV key + value in, key + value out;
+// OS_PACK key + value in, one packed word out = (key >> pshift) << ibits | value (the key's
+// digits still to come above the value); OS_PACKED packed word in (digit = word >> shift),
+// value = low ibits out; OS_V key + value in, value out (last pass: the keys are not needed
+// after it -- the tile ranges are known from the counts).
+enum : int { OS_KV = 0, OS_PACK = 1, OS_PACKED = 2, OS_V = 3 };
+
+template <int BITS, int MODE>
 __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_t* __restrict__ kin,
                                                                    const uint32_t* __restrict__ vin,
                                                                    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                                    const uint32_t* count_ptr, uint32_t cap, int shift,
+                                                                   int pshift, int ibits,
                                                                    const uint32_t* __restrict__ hist_excl, uint32_t* lb,
                                                                    uint32_t* ticket, DevFlags* fl) {
     using OS = Onesweep<BITS>;
@@ -467,7 +476,7 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
             const uint32_t idx = base + w * (32 * IT) + j * 32 + lane;
             const bool ok = idx < Kn;
             k[j] = ok ? kin[idx] : 0u;
-            val[j] = ok ? vin[idx] : 0u;
+            val[j] = (ok && MODE != OS_PACKED) ? vin[idx] : 0u;
         }
         // warp multisplit in key order (stable): rank among this warp's earlier equal digits.
         // All MATCHes first (independent), then the short shared-memory chain.
@@ -529,18 +538,30 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
                 const int d = threadIdx.x * DPT + e;
                 uint32_t prefix = 0;
                 if (tile > 0) {
+                    // batched look-back: LB_BATCH predecessors per round trip (independent
+                    // loads), consumed in order until an inclusive prefix or an unpublished
+                    // tile (retried) -- the serial L2 latency chain shrinks ~LB_BATCH-fold
                     int64_t look = (int64_t)tile - 1;
                     long long spins = 0;
-                    while (look >= 0) {
-                        const uint32_t x = ld_volatile_u32(&lb[(size_t)look * BINS + d]);
-                        const uint32_t f = x >> 30;
-                        if (f == 0) {
-                            if (++spins > SPIN_LIMIT) { raise_flag(fl, FLAG_TIMEOUT); break; }
-                            continue;
+                    for (;;) {
+                        uint32_t x[LB_BATCH];
+#pragma unroll
+                        for (int q = 0; q < LB_BATCH; ++q)
+                            x[q] = look - q >= 0 ? ld_volatile_u32(&lb[(size_t)(look - q) * BINS + d]) : LB_INC;
+                        int used = 0;
+                        bool done = false, stall = false;
+#pragma unroll
+                        for (int q = 0; q < LB_BATCH; ++q) {
+                            if (done || stall) continue;
+                            const uint32_t f = x[q] >> 30;
+                            if (f == 0) { stall = true; continue; }
+                            prefix += x[q] & LB_MASK;
+                            ++used;
+                            if (f == 2) done = true;
                         }
-                        prefix += x & LB_MASK;
-                        if (f == 2) break;
-                        --look;
+                        if (done) break;
+                        look -= used;
+                        if (stall && ++spins > SPIN_LIMIT) { raise_flag(fl, FLAG_TIMEOUT); break; }
                     }
                     st_volatile_u32(&lb[(size_t)tile * BINS + d], LB_INC | (prefix + cnt[e]));
                 }
@@ -553,16 +574,19 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
             if (d < (uint32_t)BINS) {
                 const uint32_t pos = dstart[d] + whist[w * BINS + d] + (rk[j] & 0xffffu);
                 sk[pos] = k[j];
-                sv[pos] = val[j];
+                if (MODE != OS_PACKED) sv[pos] = val[j];
             }
         }
         __syncthreads();
         const uint32_t nvalid = min((uint32_t)TILE, Kn - base);
+        const uint32_t imask = ibits >= 32 ? 0xffffffffu : (1u << ibits) - 1u;
         for (uint32_t p = threadIdx.x; p < nvalid; p += NT) {
             const uint32_t key = sk[p];
             const uint32_t dest = dbase[(key >> shift) & DMASK] + p;
-            kout[dest] = key;
-            vout[dest] = sv[p];
+            if (MODE == OS_KV) { kout[dest] = key; vout[dest] = sv[p]; }
+            if (MODE == OS_PACK) kout[dest] = ((key >> pshift) << ibits) | sv[p];
+            if (MODE == OS_PACKED) vout[dest] = key & imask;
+            if (MODE == OS_V) vout[dest] = sv[p];
         }
         __syncthreads();
     }
@@ -734,34 +758,52 @@ static int num_sms() {
     return sms;
 }
 
-template <int BITS>
+template <int BITS, int MODE>
 static int onesweep_grid() {
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_onesweep32<BITS>, Onesweep<BITS>::NT, Onesweep<BITS>::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_onesweep32<BITS, MODE>, Onesweep<BITS>::NT,
+                                                      Onesweep<BITS>::SMEM);
         if (occ <= 0) occ = 1;
     }
     return occ * num_sms();
 }
 
+template <int BITS, int MODE>
+static cudaError_t onesweep_attr() {
+    return cudaFuncSetAttribute(k_onesweep32<BITS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)Onesweep<BITS>::SMEM);
+}
+
 cudaError_t init_binning_attributes() {
-    cudaError_t e = cudaFuncSetAttribute(k_onesweep32<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Onesweep<8>::SMEM);
-    if (e) return e;
-    if ((e = cudaFuncSetAttribute(k_onesweep32<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Onesweep<9>::SMEM)))
+    cudaError_t e;
+    if ((e = onesweep_attr<8, OS_KV>()) || (e = onesweep_attr<8, OS_PACK>()) || (e = onesweep_attr<8, OS_PACKED>()) ||
+        (e = onesweep_attr<8, OS_V>()) || (e = onesweep_attr<9, OS_KV>()) || (e = onesweep_attr<9, OS_PACK>()) ||
+        (e = onesweep_attr<9, OS_PACKED>()) || (e = onesweep_attr<9, OS_V>()))
         return e;
     if ((e = cudaFuncSetAttribute(k_scan_dup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DUP_SMEM))) return e;
-    if ((e = cudaFuncSetAttribute(k_slab_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(int) * BIN_MAX_SMEM_WORDS))))
-        return e;
-    return cudaSuccess;
+    return cudaFuncSetAttribute(k_slab_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(int) * BIN_MAX_SMEM_WORDS));
+}
+
+template <int BITS, int MODE>
+static void onesweep(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout, const uint32_t* count,
+                     uint32_t cap, int shift, int pshift, int ibits, const uint32_t* hist_excl, uint32_t* lb,
+                     uint32_t* ticket, DevFlags* fl, cudaStream_t s) {
+    k_onesweep32<BITS, MODE><<<onesweep_grid<BITS, MODE>(), Onesweep<BITS>::NT, Onesweep<BITS>::SMEM, s>>>(
+        kin, vin, kout, vout, count, cap, shift, pshift, ibits, hist_excl, lb, ticket, fl);
 }
 
 template <int BITS>
-static void onesweep(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout, const uint32_t* count,
-                     uint32_t cap, int shift, const uint32_t* hist_excl, uint32_t* lb, uint32_t* ticket, DevFlags* fl,
-                     cudaStream_t s) {
-    k_onesweep32<BITS><<<onesweep_grid<BITS>(), Onesweep<BITS>::NT, Onesweep<BITS>::SMEM, s>>>(kin, vin, kout, vout, count, cap,
-                                                                                         shift, hist_excl, lb, ticket, fl);
+static void onesweep_mode(int mode, const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                          const uint32_t* count, uint32_t cap, int shift, int pshift, int ibits, const uint32_t* hist_excl,
+                          uint32_t* lb, uint32_t* ticket, DevFlags* fl, cudaStream_t s) {
+    switch (mode) {
+        case OS_KV: onesweep<BITS, OS_KV>(kin, vin, kout, vout, count, cap, shift, pshift, ibits, hist_excl, lb, ticket, fl, s); break;
+        case OS_PACK: onesweep<BITS, OS_PACK>(kin, vin, kout, vout, count, cap, shift, pshift, ibits, hist_excl, lb, ticket, fl, s); break;
+        case OS_PACKED: onesweep<BITS, OS_PACKED>(kin, vin, kout, vout, count, cap, shift, pshift, ibits, hist_excl, lb, ticket, fl, s); break;
+        default: onesweep<BITS, OS_V>(kin, vin, kout, vout, count, cap, shift, pshift, ibits, hist_excl, lb, ticket, fl, s); break;
+    }
 }
 
 cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
@@ -825,8 +867,9 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     k_hist_scan<<<1, 32 * DEPTH_PASSES, 0, s>>>(hist, hist_excl, DEPTH_PASSES, 256);
     int cur = 0;
     for (int p = 0; p < DEPTH_PASSES; ++p) {
-        onesweep<8>(dk[cur], dv[cur], dk[cur ^ 1], dv[cur ^ 1], Md, (uint32_t)count, 8 * p, hist_excl + p * MAX_BINS,
-                    depth_lb + (size_t)p * 256 * (os_elem_tiles + 1), &fl->tickets[TK_DEPTH + p], fl, s);
+        onesweep<8, OS_KV>(dk[cur], dv[cur], dk[cur ^ 1], dv[cur ^ 1], Md, (uint32_t)count, 8 * p, 0, 32,
+                           hist_excl + p * MAX_BINS, depth_lb + (size_t)p * 256 * (os_elem_tiles + 1),
+                           &fl->tickets[TK_DEPTH + p], fl, s);
         cur ^= 1;
     }
     prof->end(s, DEPTH_PASSES + 1);
@@ -848,21 +891,31 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     uint32_t* thist = hist + DEPTH_PASSES * MAX_BINS;
     uint32_t* thist_excl = hist_excl + DEPTH_PASSES * MAX_BINS;
     k_hist_scan<<<1, 32 * MAX_TILE_PASSES, 0, s>>>(thist, thist_excl, tpasses, 1 << tbits);
+    // The keys are not needed after the last pass (ranges come from the counts), so the last
+    // pass writes values only; with two passes whose remaining digit fits beside the
+    // Gaussian index, the first pass writes one packed word and the second reads only it.
+    int ibits = 1;
+    while ((1ll << ibits) < (int64_t)proj.n_pad) ++ibits;
+    const bool packed = tpasses == 2 && (gbits - tbits) + ibits <= 32;
     uint32_t* ka = bins.keys;
     uint32_t* kb = bins.keys_alt;
     uint32_t* va = bins.vals;
     uint32_t* vb = bins.vals_alt;
     for (int p = 0; p < tpasses; ++p) {
         uint32_t* lbp = tile_lb + (size_t)p * (1 << tbits) * (os_key_tiles + 1);
+        const int mode = packed ? (p == 0 ? OS_PACK : OS_PACKED) : (p == tpasses - 1 ? OS_V : OS_KV);
+        const int shift = mode == OS_PACKED ? ibits : tbits * p;
         if (tbits == 9)
-            onesweep<9>(ka, va, kb, vb, Kd, cap, 9 * p, thist_excl + p * MAX_BINS, lbp, &fl->tickets[TK_TILE + p], fl, s);
+            onesweep_mode<9>(mode, ka, va, kb, vb, Kd, cap, shift, tbits, ibits, thist_excl + p * MAX_BINS, lbp,
+                             &fl->tickets[TK_TILE + p], fl, s);
         else
-            onesweep<8>(ka, va, kb, vb, Kd, cap, 8 * p, thist_excl + p * MAX_BINS, lbp, &fl->tickets[TK_TILE + p], fl, s);
+            onesweep_mode<8>(mode, ka, va, kb, vb, Kd, cap, shift, tbits, ibits, thist_excl + p * MAX_BINS, lbp,
+                             &fl->tickets[TK_TILE + p], fl, s);
         uint32_t* tk = ka; ka = kb; kb = tk;
         uint32_t* tv = va; va = vb; vb = tv;
     }
     prof->end(s, tpasses + 1);
-    bins.sorted_in_alt = (tpasses & 1) ? 1 : 0;
+    bins.sorted_in_alt = va == bins.vals_alt ? 1 : 0;
     return cudaGetLastError();
 }
 
