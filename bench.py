@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--packet-format", default="entropy", choices=["entropy", "int8"],
                     help="entropy: rANS-coded latents decoded on the GPU each frame (default); int8: raw latents")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-libsort", action="store_true", help="skip the torch.sort (CUB) comparison")
+    ap.add_argument("--no-paper-style", action="store_true", help="skip the decode + 1 centre view timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     return ap.parse_args()
@@ -111,27 +113,30 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- roofline model
-def algorithmic_bytes(stage, cfg, n, vpb_list, K_list, k_coo):
-    """Algorithmic bytes per launch, averaged over the launches of a step."""
+def algorithmic_bytes(stage, cfg, n, vpb_list, K_list, k_coo, M_list, ent_bytes=0):
+    """Algorithmic bytes per STEP (one frame, all batches) of each profiled stage (DESIGN.md
+    "Roofline"): what the stage's algorithm must move with perfect coalescing.  Per batch of v
+    views: E = n x v elements, M visible (view, Gaussian) pairs, K entries."""
     deg = cfg.deg
     B = (deg + 1) ** 2
     P = 11 + 3 * B
     SL = sum(cfg.lat if deg else cfg.lat[:4])
     SM = sum(synth.category_m(deg))
+    bt = list(zip(vpb_list, M_list, K_list))
     if stage == "apply":  # int8 latents + RMW of the non-position planes + COO read + position RMW
         return n * (SL + 8 * SM) + k_coo * (4 + 12 + 24)
-    if stage == "project":  # read attributes once, write 64 B per (view, Gaussian)
-        return statistics.mean(n * 4 * P + n * v * 64 for v in vpb_list)
-    if stage == "sort":  # one onesweep pass: read + write (u64 key, u32 val)
-        return statistics.mean(24 * K for K in K_list)
-    if stage == "scan":
-        return statistics.mean(8 * n * v for v in vpb_list)
-    if stage == "duplicate":
-        return statistics.mean(20 * n * v + 12 * K for v, K in zip(vpb_list, K_list))
-    if stage == "hist":
-        return statistics.mean(8 * K for K in K_list)
-    if stage == "ranges":
-        return statistics.mean(8 * K for K in K_list)
+    if stage == "entropy":  # coded streams in, int8 latents out
+        return ent_bytes + n * SL
+    if stage == "project":  # read the attributes once per batch, write 64 B per (view, Gaussian)
+        return sum(n * 4 * P + n * v * 64 for v, M, K in bt)
+    if stage == "compact":  # count: tiles + rect + depth (16 B/elem); compact: tiles + depth (8 B), pairs out
+        return sum(n * v * 24 + 8 * M for v, M, K in bt)
+    if stage == "depth_sort":  # 4 LSD passes over the (depth, index) pairs, 16 B each
+        return sum(4 * 16 * M for v, M, K in bt)
+    if stage == "duplicate":  # pairs + rects in, K (gt, index) entries out
+        return sum(12 * M + 8 * K for v, M, K in bt)
+    if stage == "tile_sort":  # pass 1: 8 B in, 4 B packed out; pass 2: 4 B in, 4 B index out
+        return sum(20 * K for v, M, K in bt)
     return None
 
 
@@ -160,6 +165,36 @@ def load_traffic():
         except Exception:
             return {}
     return {}
+
+
+# ----------------------------------------------------------------------------- library baseline
+def library_sort_comparison(stg, bnp, dev, reps: int = 5):
+    """torch.sort (CUB radix sort) of one batch's K entries keyed (gt << 32 | depth bits) with
+    the Gaussian index as value, from a random order: the library baseline SURVEY 8(d) asks
+    for, on the same box and the same K (our binning computes the same order plus ranges)."""
+    import torch
+    K = bnp["K"]
+    if K == 0:
+        return None
+    rg = torch.from_numpy(bnp["ranges"].astype(np.int64)).to(dev)
+    gt = torch.repeat_interleave(torch.arange(rg.shape[0], device=dev), rg[:, 1] - rg[:, 0])
+    vals = (stg.vals_alt if stg.bins.sorted_in_alt else stg.vals)[:K].long()
+    keys = (gt << 32) | stg.depth.long()[gt // stg.T, vals]
+    perm = torch.randperm(K, device=dev)
+    keys, vals = keys[perm].contiguous(), vals[perm].to(torch.int32).contiguous()
+    torch.sort(keys, stable=True)
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        sk, si = torch.sort(keys, stable=True)
+        sv = vals[si]
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    del sk, si, sv
+    return {"impl": "torch.sort(int64 keys, stable) + value gather (CUB radix sort)", "K": K,
+            "ms": statistics.median(ts), "input": "the batch's entries in a random order"}
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) timing
@@ -363,11 +398,15 @@ def main():
     # ---- evidence (outside the timed region): K per batch, blend work counts
     batches = [cams[a:b] for a, b in player.batches]
     from paper_2412_04469_b200.stages import Stages  # explicit-buffer stage runner over the same C-ABI
-    K_list, ev_pairs, cp_pairs = [], 0, 0
-    for bc in batches:
+    K_list, M_list, ev_pairs, cp_pairs, libsort = [], [], 0, 0, None
+    for bi, bc in enumerate(batches):
         stg = Stages(player.planes.cpu().numpy(), sc.n, sc.deg, bc, keys_cap=player.keys_cap, device=local)
         stg.project().bin_sort()
-        K_list.append(stg.bins_np()["K"])
+        bnp = stg.bins_np()
+        K_list.append(bnp["K"])
+        M_list.append(bnp["M"])
+        if bi == 0 and not args.no_libsort:
+            libsort = library_sort_comparison(stg, bnp, dev)
         e = torch.zeros(len(bc), dtype=torch.int64, device=dev)
         c = torch.zeros(len(bc), dtype=torch.int64, device=dev)
         Q.queen_blend_counts(stg.ctx, stg.proj, stg.bins, bc, e, c)
@@ -386,7 +425,8 @@ def main():
     gpu_launches = int(round(sum(v["launches_per_step"] for v in stages.values()) * args.steps)) if stages else None
     k_coo = host_pkts[0].k if rank == 0 else k_cap
     vpb_list = [len(b) for b in batches]
-    roof = None
+    roof, path = None, None
+    ent_b = int(statistics.mean(used_bytes)) if (entropy and used_bytes) else 0
     if stages:
         dom = max(stages, key=lambda s: stages[s]["ms_per_step"])
         f_mhz = clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
@@ -402,24 +442,70 @@ def main():
                     "unit": "T FP32-lane-ops/s", "frac": achieved / peak, "traffic": lookup_traffic(traffic, "k_blend<0"),
                     "peak_source": f"148 SMs x 128 FP32 lanes x {f_mhz:.0f} MHz (sampled SM clock)",
                     "work": {"evaluated_pairs": ev_pairs, "composited_pairs": cp_pairs}}
-        elif algorithmic_bytes(dom, cfg, sc.n, vpb_list, K_list, k_coo) is None:
+        elif algorithmic_bytes(dom, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b) is None:
             roof = {"bound": None, "kernel": dom, "achieved": None, "peak": None, "unit": None, "frac": None,
                     "traffic": None, "note": "dominant stage has no roofline model"}
         else:
-            b = algorithmic_bytes(dom, cfg, sc.n, vpb_list, K_list, k_coo)
-            t = stages[dom]["us_per_launch"] * 1e-6
+            b = algorithmic_bytes(dom, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b)
+            t = stages[dom]["ms_per_step"] * 1e-3
             achieved = b / t / 1e9
             peak = peaks["hbm_gbs"]
-            kname = {"sort": "k_onesweep", "apply": "k_decode_apply", "project": "k_project", "scan": "k_scan_tiles",
-                     "duplicate": "k_duplicate", "hist": "k_hist", "ranges": "k_ranges"}[dom]
-            roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": lookup_traffic(traffic, kname), "peak_source": f"hbm_gbs ({peak_src})",
-                    "algorithmic_bytes_per_launch": b}
-        for name, s in stages.items():
-            b = algorithmic_bytes(name, cfg, sc.n, vpb_list, K_list, k_coo)
-            if b:
-                s["algorithmic_GBps"] = b / (s["us_per_launch"] * 1e-6) / 1e9
-                s["hbm_frac"] = s["algorithmic_GBps"] / peaks["hbm_gbs"]
+            roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None, "peak_source": f"hbm_gbs ({peak_src})",
+                    "algorithmic_bytes_per_step": b}
+        # path-level roofline: sum of per-stage ideal times / measured frame time.
+        # HBM stages: algorithmic bytes / measured HBM peak; blend: max(FP32 issue, MUFU) from the
+        # exact work counts; stages without a model (ranges) count as their measured time.
+        ideal = {}
+        for name, s_ in stages.items():
+            if name == "blend":
+                f_hz = f_mhz * 1e6
+                ideal[name] = 1e3 * max((7 * ev_pairs + 7 * cp_pairs) / (SM_COUNT * 128 * f_hz),
+                                        cp_pairs / (SM_COUNT * 16 * f_hz))
+            else:
+                b = algorithmic_bytes(name, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b)
+                ideal[name] = 1e3 * b / (peaks["hbm_gbs"] * 1e9) if b else s_["ms_per_step"]
+            s_["ideal_ms_per_step"] = ideal[name]
+            s_["frac"] = ideal[name] / s_["ms_per_step"] if s_["ms_per_step"] > 0 else None
+            b = algorithmic_bytes(name, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b)
+            if b and name != "blend":
+                s_["algorithmic_GBps"] = b / (s_["ms_per_step"] * 1e-3) / 1e9
+        path = {"ideal_ms": sum(ideal.values()), "frame_ms": total_ms / args.steps,
+                "frac": sum(ideal.values()) / (total_ms / args.steps),
+                "note": "sum of per-stage ideal times (HBM bytes / measured peak; blend FP32-issue/MUFU bound "
+                        "from exact work counts) over the measured frame time"}
+
+    if libsort is not None and stages:
+        nb = len(batches)
+        libsort["ours_binning_ms_per_batch"] = sum(stages[k]["ms_per_step"] for k in
+                                                   ("compact", "depth_sort", "duplicate", "ranges", "tile_sort")
+                                                   if k in stages) / nb
+
+    # ---- paper-style FPS: decode + render of ONE centre view on 1 GPU, median
+    paper = None
+    if world == 1 and not args.no_paper_style:
+        pl1 = Player(sc.planes, sc.n, sc.deg, [cams_all[V // 2]], device=local)
+        pl1.apply(dps[0])
+        pl1.render()
+        pl1.fit_capacity()
+        pl1.planes.copy_(torch.from_numpy(sc.planes).to(dev))
+        for t in range(args.warmup):
+            pl1.apply(dps[t % P])
+            pl1.render()
+        pe0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        pe1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        for k in range(args.steps):
+            flush.zero_()
+            pe0[k].record(stream)
+            pl1.apply(dps[(args.warmup + k) % P])
+            pl1.render()
+            pe1[k].record(stream)
+        torch.cuda.synchronize()
+        pms = statistics.median(a.elapsed_time(b) for a, b in zip(pe0, pe1))
+        paper = {"fps": 1e3 / pms, "ms_median": pms, "view": V // 2,
+                 "definition": "decode (entropy + apply) + render of the centre view, 1 GPU, median over the timed "
+                               "frames, L2 flushed between frames (P:1457's definition on this workload)"}
+        del pl1
 
     # ---- end to end through the public API with host buffers (pinned H2D packet, D2H images)
     e2e = None
@@ -439,6 +525,8 @@ def main():
         ev_apply = [ev() for _ in range(args.steps)]
         ev_render = [ev() for _ in range(args.steps)]
         ev_d2h = [ev() for _ in range(args.steps)]
+        lat0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        lat1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         # restart the sequence from A_0 so the streamed frames are the same ones
         player.planes.copy_(torch.from_numpy(sc.planes).to(dev))
@@ -453,6 +541,7 @@ def main():
             with torch.cuda.stream(s_h2d):
                 if k >= 2:
                     s_h2d.wait_event(ev_apply[k - 2])  # recv[slot] consumed by frame k-2
+                lat0[k].record(s_h2d)
                 if rank == 0:
                     ub = used_bytes[k % P]  # only the bytes the packet uses cross PCIe
                     recv[slot][:ub].copy_(pin_pk[k % P][:ub], non_blocking=True)
@@ -466,6 +555,7 @@ def main():
                 stream.wait_event(ev_d2h[k - 2])  # out_dev[slot] drained to the host
             player.render(out=out_dev[slot])
             ev_render[k].record(stream)
+            lat1[k].record(stream)
             with torch.cuda.stream(s_d2h):
                 s_d2h.wait_event(ev_render[k])
                 out_host[slot].copy_(out_dev[slot], non_blocking=True)
@@ -475,15 +565,18 @@ def main():
             stream.wait_event(ev_d2h[args.steps - 2])
         t1.record(stream)
         torch.cuda.synchronize()
-        e_ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=dev)
+        lat_med = statistics.median(a.elapsed_time(b) for a, b in zip(lat0, lat1))
+        e_ms = torch.tensor([t0.elapsed_time(t1), lat_med], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": args.steps / (float(e_ms[0]) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(statistics.mean(used_bytes)) if rank == 0 else 0,
                "d2h_bytes_per_step": int(out_host[0].numel() * 4),
+               "frame_latency_ms": float(e_ms[1]),
                "note": "runtime.Player public API: pinned H2D of each frame's wire packet + apply + render + "
                        "D2H of this rank's fp32 RGB images, copies on their own streams (double-buffered), "
-                       "timed from the first H2D to the last D2H; working set per frame >> L2"}
+                       "timed from the first H2D to the last D2H; working set per frame >> L2; frame_latency_ms = "
+                       "median of (packet H2D start -> frame rendered on the device), max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -509,7 +602,8 @@ def main():
             "packet_bytes_per_frame": int(statistics.mean(used_bytes)) if used_bytes else None,
             "mpixel_per_s": mpix, "view_fps": value * V,
             "status": Q.STATUS.get(st, st),
-            "keys_per_batch": K_list, "stages": stages, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "keys_per_batch": K_list, "visible_pairs_per_batch": M_list, "stages": stages, "roofline": roof,
+            "path_roofline": path, "paper_style": paper, "library_sort": libsort, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
         }
         print(json.dumps(line))
