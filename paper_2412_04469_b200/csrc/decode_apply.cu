@@ -11,6 +11,8 @@
 
 namespace queen {
 
+constexpr int DA_CHUNK = 4;  // attribute rows per batch of loads (rows in flight per warp)
+
 struct DecodeParams {
     int n, n_pad;
     int lat[5], M[5], lat_row0[5], dec_off[5], out_row0[5];
@@ -81,32 +83,46 @@ __global__ void __launch_bounds__(256) k_decode_apply(DecodeParams p) {
                 }
             }
         }
+        // rows in chunks of DA_CHUNK: the chunk's attribute loads are issued together (memory-
+        // level parallelism: DA_CHUNK x 512 B in flight per warp instead of one row at a time)
 #pragma unroll 1
-        for (int m = 0; m < M; ++m) {
-            // a2: r = D_c[m] . float(l), fmaf chain ascending k from +0 (R#7)
-            const float* d = sdec + p.dec_off[c] + m * L;
-            float r0 = +0.0f, r1 = +0.0f, r2 = +0.0f, r3 = +0.0f;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                if (k < L) {
-                    const float w = d[k];
-                    r0 = fmaf(w, ql[k][0], r0);
-                    r1 = fmaf(w, ql[k][1], r1);
-                    r2 = fmaf(w, ql[k][2], r2);
-                    r3 = fmaf(w, ql[k][3], r3);
-                }
-            }
-            const int row = p.out_row0[c] + m;
-            if (p.resid_out) *reinterpret_cast<float4*>(p.resid_out + (int64_t)row * np + i0) = make_float4(r0, r1, r2, r3);
+        for (int m0 = 0; m0 < M; m0 += DA_CHUNK) {
+            float4 av[DA_CHUNK];
             if (APPLY) {
-                // a3: A_t = A_{t-1} + r, separate add (R#7)
-                float4* a = reinterpret_cast<float4*>(p.planes + (int64_t)(3 + row) * np + i0);
-                float4 v = *a;
-                v.x = v.x + r0;
-                if (l1) v.y = v.y + r1;
-                if (l2) v.z = v.z + r2;
-                if (l3) v.w = v.w + r3;
-                *a = v;
+#pragma unroll
+                for (int u = 0; u < DA_CHUNK; ++u)
+                    if (m0 + u < M)
+                        av[u] = *reinterpret_cast<const float4*>(p.planes + (int64_t)(3 + p.out_row0[c] + m0 + u) * np + i0);
+            }
+#pragma unroll
+            for (int u = 0; u < DA_CHUNK; ++u) {
+                const int m = m0 + u;
+                if (m >= M) break;
+                // a2: r = D_c[m] . float(l), fmaf chain ascending k from +0 (R#7)
+                const float* d = sdec + p.dec_off[c] + m * L;
+                float r0 = +0.0f, r1 = +0.0f, r2 = +0.0f, r3 = +0.0f;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    if (k < L) {
+                        const float w = d[k];
+                        r0 = fmaf(w, ql[k][0], r0);
+                        r1 = fmaf(w, ql[k][1], r1);
+                        r2 = fmaf(w, ql[k][2], r2);
+                        r3 = fmaf(w, ql[k][3], r3);
+                    }
+                }
+                const int row = p.out_row0[c] + m;
+                if (p.resid_out)
+                    *reinterpret_cast<float4*>(p.resid_out + (int64_t)row * np + i0) = make_float4(r0, r1, r2, r3);
+                if (APPLY) {
+                    // a3: A_t = A_{t-1} + r, separate add (R#7)
+                    float4 v = av[u];
+                    v.x = v.x + r0;
+                    if (l1) v.y = v.y + r1;
+                    if (l2) v.z = v.z + r2;
+                    if (l3) v.w = v.w + r3;
+                    *reinterpret_cast<float4*>(p.planes + (int64_t)(3 + row) * np + i0) = v;
+                }
             }
         }
     }
