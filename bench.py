@@ -580,7 +580,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        nview = 1 if cfg.n * cfg.width * cfg.height > 1e11 else 2
+        nview = min(V, 1 if cfg.n * cfg.width * cfg.height > 1e11 else 2)
         frame_s, det = time_oracle_frame(cfg, sc.planes, sc.n, sc.deg, cams_all, host_pkts[0], nview)
         cpu = {"value": 1.0 / frame_s, "unit": UNIT, "cores": det["threads"], "kind": "oracle",
                "sample": f"apply of frame 1 (all {sc.n} Gaussians) + render of {nview} of {V} views at "
