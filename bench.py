@@ -507,6 +507,23 @@ def main():
                                "frames, L2 flushed between frames (P:1457's definition on this workload)"}
         del pl1
 
+    # ---- NEXT #3: masked / dynamic-subset rendering of the frame's gated set
+    masked = None
+    if rank == 0 and not args.no_paper_style:
+        idx = torch.from_numpy(np.ascontiguousarray(host_pkts[0].coo_idx, np.uint32)).to(dev)
+        mk = player.render_mask(idx)
+        torch.cuda.synchronize()
+        me0, me1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        me0.record(stream)
+        for _ in range(5):
+            player.render_mask(idx, out=mk)
+        me1.record(stream)
+        torch.cuda.synchronize()
+        masked = {"ms": me0.elapsed_time(me1) / 5, "dynamic_gaussians": int(idx.numel()),
+                  "marked_fraction": float(mk.float().mean()), "views": len(cams), "dilation": 48,
+                  "alpha_thresh": 1e-3, "note": "queen_render_mask of frame 1's gated COO set, all views (L2 warm)"}
+        del mk
+
     # ---- end to end through the public API with host buffers (pinned H2D packet, D2H images)
     e2e = None
     if not args.no_e2e:
@@ -603,7 +620,7 @@ def main():
             "mpixel_per_s": mpix, "view_fps": value * V,
             "status": Q.STATUS.get(st, st),
             "keys_per_batch": K_list, "visible_pairs_per_batch": M_list, "stages": stages, "roofline": roof,
-            "path_roofline": path, "paper_style": paper, "library_sort": libsort, "cpu_baseline": cpu, "e2e": e2e,
+            "path_roofline": path, "paper_style": paper, "library_sort": libsort, "masked_render": masked, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
         }
         print(json.dumps(line))

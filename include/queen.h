@@ -226,6 +226,23 @@ queen_status queen_entropy_decode(queen_ctx* ctx, const void* stream_dev, int32_
 queen_status queen_entropy_decode_frame(queen_ctx* ctx, const void* const* streams_dev, const int32_t* lat_dim,
                                         int32_t n, int32_t n_pad, int8_t* latents_out, void* stream);
 
+/* ---- NEXT #3: masked / dynamic-subset rendering -----
+ * queen_render_mask: renders ONLY the Gaussians listed in subset_idx (device u32 [k], strictly
+ *   increasing, each < scene->n; when k_dev (device int32) is non-NULL the live count is
+ *   min(*k_dev, k) -- e.g. a frame packet's gated COO indices, the "dynamic" set) for n_views
+ *   equally-sized cameras; marks every pixel whose accumulated alpha 1 - T exceeds alpha_thresh
+ *   (S:322-326 uses 1e-3; T by the same compositing rules as queen_rasterize, so with
+ *   alpha_thresh < 1/255 a pixel is marked iff a subset Gaussian passes the 1/255 test there);
+ *   then dilates the marks with a dilation x dilation square (48 in P:1262-1263): output pixel
+ *   (x, y) is 1 iff a mark lies in [x - d/2, x - d/2 + d - 1] x [y - d/2, y - d/2 + d - 1],
+ *   clipped at the borders (d = 1: no dilation).
+ *   mask_out: device u8 [n_views][H][W], values 0/1.  Uses the workspace like
+ *   queen_render_views (same sizing).  Invalid subset indices -> QUEEN_ERR_INDEX (sticky);
+ *   dilation < 1, alpha_thresh outside [0,1), W > 12000 -> immediate error. */
+queen_status queen_render_mask(queen_ctx* ctx, const queen_gaussians* scene, const uint32_t* subset_idx, int32_t k,
+                               const int32_t* k_dev, const queen_camera* cams, int32_t n_views, float alpha_thresh,
+                               int32_t dilation, uint8_t* mask_out, void* stream);
+
 /* Makes `stream` wait until the binning (project + bin_sort) of the most recent
  * queen_render_views call on `ctx` has completed -- lets a renderer with several contexts
  * pipeline one batch's binning (memory/latency bound) under another batch's blend (ALU

@@ -261,3 +261,44 @@ def render(planes, n: int, deg: int, cams, bg=(0.0, 0.0, 0.0), threads: int | No
     bins = bin_sort(proj, W, H)
     rgb, T = rasterize(proj, bins, W, H, bg, threads)
     return proj, bins, rgb, T
+
+
+# ----------------------------------------------------------------------------- NEXT #3
+def dilate(marks: np.ndarray, d: int) -> np.ndarray:
+    """Square d x d dilation of boolean marks [..., H, W], clipped at the borders: output (x, y)
+    is set iff a mark lies in [x - d//2, x - d//2 + d - 1] x [y - d//2, y - d//2 + d - 1]
+    ("dilate the image mask by a 48x48 kernel"; anchor = centre of the kernel, the
+    convention of a centred structuring element).  Window sums of a 2D prefix-sum table."""
+    m = np.asarray(marks, bool)
+    H, W = m.shape[-2:]
+    a = d // 2
+    S = np.zeros(m.shape[:-2] + (H + 1, W + 1), np.int64)
+    S[..., 1:, 1:] = m.astype(np.int64).cumsum(-2).cumsum(-1)
+    y = np.arange(H)
+    x = np.arange(W)
+    y0, y1 = np.clip(y - a, 0, H), np.clip(y - a + d, 0, H)
+    x0, x1 = np.clip(x - a, 0, W), np.clip(x - a + d, 0, W)
+    tot = (S[..., y1[:, None], x1[None, :]] - S[..., y0[:, None], x1[None, :]]
+           - S[..., y1[:, None], x0[None, :]] + S[..., y0[:, None], x0[None, :]])
+    return tot > 0
+
+
+def render_mask(planes: np.ndarray, n: int, deg: int, cams, subset, alpha_thresh: float = 1e-3, dilation: int = 48,
+                threads: int | None = None) -> np.ndarray:
+    """Masked / dynamic-subset rendering: render only the
+    Gaussians in `subset` (ascending indices), mark pixels with accumulated alpha 1 - T >
+    alpha_thresh, dilate.  Rendering the subset alone = rendering the scene restricted to those
+    columns (same per-Gaussian arithmetic; the index order, hence the depth tie-break, is
+    preserved).  Returns uint8 [V][H][W]."""
+    subset = np.asarray(subset, np.int64)
+    W, H = cams[0].width, cams[0].height
+    V = len(cams)
+    if subset.size == 0:
+        return np.zeros((V, H, W), np.uint8)
+    k = subset.size
+    kp = max(4, (k + 3) // 4 * 4)
+    sub = np.zeros((planes.shape[0], kp), np.float32)
+    sub[:, :k] = planes[:, subset]
+    _, _, _, T = render(sub, k, deg, cams, threads=threads)
+    marks = (np.float32(1.0) - T) > np.float32(alpha_thresh)
+    return dilate(marks, dilation).astype(np.uint8)

@@ -29,7 +29,7 @@ EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version",
            "queen_set_workspace", "queen_check", "queen_decode_residuals", "queen_apply_frame", "queen_project",
            "queen_bin_sort", "queen_rasterize", "queen_render_views", "queen_blend_counts",
            "queen_profile_enable", "queen_profile_read", "queen_wait_binned", "queen_entropy_encode",
-           "queen_entropy_decode", "queen_entropy_decode_frame"]
+           "queen_entropy_decode", "queen_entropy_decode_frame", "queen_render_mask"]
 STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy"]
 
 
@@ -102,6 +102,8 @@ def lib() -> C.CDLL:
             "queen_blend_counts": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
                                          p, p, p]),
             "queen_profile_enable": (i32, [p, i32]),
+            "queen_render_mask": (i32, [p, C.POINTER(QueenGaussians), p, i32, p, C.POINTER(QueenCamera), i32, C.c_float,
+                                        i32, p, p]),
             "queen_wait_binned": (i32, [p, p]),
             "queen_entropy_encode": (i32, [p, i32, i32, i32, p, C.c_size_t, C.POINTER(C.c_size_t)]),
             "queen_entropy_decode": (i32, [p, p, i32, i32, i32, p, p]),
@@ -302,6 +304,15 @@ def queen_render_views(ctx: Context, scene: QueenGaussians, cams, rgb_out, T_out
     st = lib().queen_render_views(ctx.handle, C.byref(scene), arr, len(arr), bgv, _ptr(rgb_out), _ptr(T_out),
                                   C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_render_views")
+
+
+def queen_render_mask(ctx: Context, scene: QueenGaussians, subset_idx, k: int, cams, mask_out, alpha_thresh=1e-3,
+                      dilation: int = 48, k_dev=None, stream=None, cam_array=None):
+    """NEXT #3: dilated alpha mask of the subset's rendering (queen.h queen_render_mask)."""
+    arr = cam_array if cam_array is not None else camera_array(cams)
+    st = lib().queen_render_mask(ctx.handle, C.byref(scene), _ptr(subset_idx), int(k), _ptr(k_dev), arr, len(arr),
+                                 float(alpha_thresh), int(dilation), _ptr(mask_out), C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_render_mask")
 
 
 def queen_entropy_encode(latents: np.ndarray, n: int) -> np.ndarray:

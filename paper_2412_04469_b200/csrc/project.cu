@@ -41,7 +41,8 @@ __device__ __forceinline__ void sh_basis(int deg, float x, float y, float z, flo
 template <int DEG>
 __global__ void __launch_bounds__(128) k_project(const float* __restrict__ planes, int n, int n_pad, const CamBatch cams,
                                                  int n_views, float4* __restrict__ rec, uint32_t* __restrict__ depth,
-                                                 uint32_t* __restrict__ tiles, short4* __restrict__ rect, DevFlags* fl) {
+                                                 uint32_t* __restrict__ tiles, short4* __restrict__ rect,
+                                                 const uint8_t* __restrict__ select, DevFlags* fl) {
     constexpr int B = (DEG + 1) * (DEG + 1);
     constexpr int P = 11 + 3 * B;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -66,7 +67,8 @@ __global__ void __launch_bounds__(128) k_project(const float* __restrict__ plane
     for (int p = 0; p < P; ++p) finite = finite && isfinite(a[p]);
     // view-independent part: normalised quaternion, R(q) S, Sigma, opacity
     float S[9], o = 0.f, e2 = 0.f;
-    bool live = finite;
+    // render_mask: Gaussians outside the requested subset are culled like invisible ones
+    bool live = finite && (select == nullptr || select[i] != 0);
     if (live) {
         float qw = a[3], qx = a[4], qy = a[5], qz = a[6];
         const float n2 = fmaf(qw, qw, fmaf(qx, qx, fmaf(qy, qy, qz * qz)));
@@ -203,17 +205,18 @@ __global__ void __launch_bounds__(128) k_project(const float* __restrict__ plane
 }
 
 cudaError_t launch_project(const float* planes, int n, int n_pad, int deg, const CamBatch& cams, int n_views,
-                           float* rec, uint32_t* depth, uint32_t* tiles, int16_t* rect, DevFlags* fl, cudaStream_t s) {
+                           float* rec, uint32_t* depth, uint32_t* tiles, int16_t* rect, const uint8_t* select,
+                           DevFlags* fl, cudaStream_t s) {
     const int threads = 128;
     const int blocks = (n_pad + threads - 1) / threads;
     if (blocks == 0) return cudaSuccess;
     float4* r = reinterpret_cast<float4*>(rec);
     short4* rc = reinterpret_cast<short4*>(rect);
     switch (deg) {
-        case 0: k_project<0><<<blocks, threads, 0, s>>>(planes, n, n_pad, cams, n_views, r, depth, tiles, rc, fl); break;
-        case 1: k_project<1><<<blocks, threads, 0, s>>>(planes, n, n_pad, cams, n_views, r, depth, tiles, rc, fl); break;
-        case 2: k_project<2><<<blocks, threads, 0, s>>>(planes, n, n_pad, cams, n_views, r, depth, tiles, rc, fl); break;
-        default: k_project<3><<<blocks, threads, 0, s>>>(planes, n, n_pad, cams, n_views, r, depth, tiles, rc, fl); break;
+        case 0: k_project<0><<<blocks, threads, 0, s>>>(planes, n, n_pad, cams, n_views, r, depth, tiles, rc, select, fl); break;
+        case 1: k_project<1><<<blocks, threads, 0, s>>>(planes, n, n_pad, cams, n_views, r, depth, tiles, rc, select, fl); break;
+        case 2: k_project<2><<<blocks, threads, 0, s>>>(planes, n, n_pad, cams, n_views, r, depth, tiles, rc, select, fl); break;
+        default: k_project<3><<<blocks, threads, 0, s>>>(planes, n, n_pad, cams, n_views, r, depth, tiles, rc, select, fl); break;
     }
     return cudaGetLastError();
 }

@@ -14,6 +14,7 @@ struct queen_ctx {
     void* ws = nullptr;
     size_t ws_bytes = 0;
     int32_t ws_n_pad = 0, ws_views = 0, ws_w = 0, ws_h = 0;
+    const uint8_t* select = nullptr;  // set only while queen_render_mask projects its subset
     int64_t ws_keys = 0;
     queen::WsLayout L{};
     queen::Prof prof;
@@ -233,7 +234,7 @@ queen_status queen_project(queen_ctx* ctx, const queen_gaussians* scene, const q
         std::memcpy(cb.cam, cams + v0, sizeof(queen_camera) * nv);
         const int64_t o = (int64_t)v0 * scene->n_pad;
         cudaError_t e = launch_project(scene->planes, scene->n, scene->n_pad, scene->sh_degree, cb, nv, out->rec + o * REC_WORDS,
-                                       out->depth + o, out->tiles + o, out->rect + o * 4, flags_of(ctx), s);
+                                       out->depth + o, out->tiles + o, out->rect + o * 4, ctx->select, flags_of(ctx), s);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "project");
     }
     ctx->prof.end(s, (n_views + QUEEN_MAX_VIEWS - 1) / QUEEN_MAX_VIEWS);
@@ -271,7 +272,7 @@ queen_status queen_rasterize(queen_ctx* ctx, const queen_proj* proj, const queen
     const uint32_t* vals = bins->sorted_in_alt ? bins->vals_alt : bins->vals;
     ctx->prof.begin(ST_BLEND, static_cast<cudaStream_t>(stream));
     cudaError_t e = launch_rasterize(proj->rec, proj->n_pad, bins->ranges, vals, n_views, cams[0].width, cams[0].height,
-                                     bg[0], bg[1], bg[2], rgb_out, T_out, static_cast<cudaStream_t>(stream));
+                                     bg[0], bg[1], bg[2], rgb_out, T_out, nullptr, 0.f, static_cast<cudaStream_t>(stream));
     ctx->prof.end(static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "rasterize");
     return QUEEN_OK;
@@ -390,6 +391,55 @@ queen_status queen_render_views(queen_ctx* ctx, const queen_gaussians* scene, co
     if (cudaEventRecord(ctx->binned, static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return cuda_fail(ctx, cudaGetLastError(), "record binned event");
     return queen_rasterize(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, stream);
+}
+
+queen_status queen_render_mask(queen_ctx* ctx, const queen_gaussians* scene, const uint32_t* subset_idx, int32_t k,
+                               const int32_t* k_dev, const queen_camera* cams, int32_t n_views, float alpha_thresh,
+                               int32_t dilation, uint8_t* mask_out, void* stream) {
+    if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
+    if (!scene || !scene->planes || !mask_out) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null scene/mask_out");
+    if (k < 0 || (k > 0 && !subset_idx)) return fail(ctx, QUEEN_ERR_INVALID_ARG, "bad subset");
+    if (dilation < 1 || !(alpha_thresh >= 0.f && alpha_thresh < 1.f))
+        return fail(ctx, QUEEN_ERR_INVALID_ARG, "dilation >= 1 and alpha_thresh in [0,1) required");
+    if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
+    const int W = cams[0].width, H = cams[0].height;
+    if (scene->n_pad > ctx->ws_n_pad || n_views > ctx->ws_views || W > ctx->ws_w || H > ctx->ws_h)
+        return fail(ctx, QUEEN_ERR_SHAPE, "workspace was sized for a smaller batch");
+    if (W > 12000) return fail(ctx, QUEEN_ERR_SHAPE, "mask rows wider than 12000 pixels");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    unsigned char* ws = static_cast<unsigned char*>(ctx->ws);
+    const WsLayout& L = ctx->L;
+    uint8_t* sel = reinterpret_cast<uint8_t*>(ws + L.select);
+    cudaError_t e = launch_select(subset_idx, k, k_dev, scene->n, scene->n_pad, sel, flags_of(ctx), s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "render_mask select");
+    queen_proj pj;
+    pj.n_pad = scene->n_pad;
+    pj.rec = reinterpret_cast<float*>(ws + L.rec);
+    pj.depth = reinterpret_cast<uint32_t*>(ws + L.depth);
+    pj.tiles = reinterpret_cast<uint32_t*>(ws + L.tiles);
+    pj.rect = reinterpret_cast<int16_t*>(ws + L.rect);
+    queen_bins b;
+    b.keys_cap = ctx->ws_keys;
+    b.keys = reinterpret_cast<uint32_t*>(ws + L.keys);
+    b.keys_alt = reinterpret_cast<uint32_t*>(ws + L.keys_alt);
+    b.vals = reinterpret_cast<uint32_t*>(ws + L.vals);
+    b.vals_alt = reinterpret_cast<uint32_t*>(ws + L.vals_alt);
+    b.ranges = reinterpret_cast<uint32_t*>(ws + L.ranges);
+    b.K = reinterpret_cast<uint32_t*>(ws + L.K);
+    b.sorted_in_alt = 0;
+    ctx->select = sel;
+    queen_status st = queen_project(ctx, scene, cams, n_views, &pj, stream);
+    ctx->select = nullptr;
+    if (st) return st;
+    if ((st = queen_bin_sort(ctx, &pj, cams, n_views, &b, stream))) return st;
+    const uint32_t* vals = b.sorted_in_alt ? b.vals_alt : b.vals;
+    ctx->prof.begin(ST_BLEND, s);
+    e = launch_rasterize(pj.rec, pj.n_pad, b.ranges, vals, n_views, W, H, 0.f, 0.f, 0.f, nullptr, nullptr, mask_out,
+                         alpha_thresh, s);
+    if (e == cudaSuccess) e = launch_dilate(mask_out, reinterpret_cast<uint8_t*>(ws + L.mask_tmp), n_views, W, H, dilation, s);
+    ctx->prof.end(s, dilation > 1 ? 3 : 1);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "render_mask");
+    return QUEEN_OK;
 }
 
 }  // extern "C"

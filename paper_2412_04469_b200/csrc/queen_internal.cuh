@@ -98,9 +98,9 @@ inline BinPlan bin_plan(int64_t n_pad, int64_t n_views, int W, int H) {
 struct WsLayout {
     // scratch (bin_sort)
     size_t flags, hist, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, counts, view_tot, slab_counts,
-        slab_vis, total_scratch;
-    // render_views buffers
-    size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, total;
+        slab_vis, select, total_scratch;
+    // render_views / render_mask buffers
+    size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, mask_tmp, total;
     int64_t key_tiles, elem_tiles, os_key_tiles, os_elem_tiles, T, elems;
 };
 
@@ -130,6 +130,7 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     const BinPlan bp = bin_plan(n_pad, n_views, W, H);
     L.slab_counts = o; o += align256(sizeof(uint32_t) * (size_t)(bp.ok ? bp.slabs : 0) * L.T);
     L.slab_vis = o; o += align256(sizeof(uint32_t) * (size_t)(bp.slabs + 1));
+    L.select = o; o += align256((size_t)n_pad);  // render_mask: per-Gaussian subset flags
     L.total_scratch = o;
     L.rec = o; o += align256(sizeof(float) * REC_WORDS * L.elems);
     L.depth = o; o += align256(sizeof(uint32_t) * L.elems);
@@ -141,6 +142,7 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     L.vals_alt = o; o += align256(sizeof(uint32_t) * keys_cap);
     L.ranges = o; o += align256(sizeof(uint32_t) * 2 * L.T * n_views);
     L.K = o; o += align256(sizeof(uint32_t) * 4);
+    L.mask_tmp = o; o += align256((size_t)n_views * W * H);  // render_mask: row-dilated marks
     L.total = o;
     return L;
 }
@@ -151,7 +153,7 @@ inline bool scratch_fits(const WsLayout& need, const WsLayout& have) {
                                    &WsLayout::depth_lb,   &WsLayout::tile_lb,     &WsLayout::dkeys,
                                    &WsLayout::dkeys_alt,  &WsLayout::dvals,       &WsLayout::dvals_alt,
                                    &WsLayout::counts,     &WsLayout::view_tot,    &WsLayout::slab_counts,
-                                   &WsLayout::slab_vis,   &WsLayout::total_scratch};
+                                   &WsLayout::slab_vis,   &WsLayout::select,      &WsLayout::total_scratch};
     for (size_t q = 0; q + 1 < sizeof(r) / sizeof(r[0]); ++q)
         if (need.*r[q + 1] - need.*r[q] > have.*r[q + 1] - have.*r[q]) return false;
     return true;
@@ -248,12 +250,16 @@ cudaError_t launch_gate_compact(const queen_packet& p, uint32_t* idx_out, float*
 cudaError_t launch_coo_copy(const queen_packet& p, uint32_t* idx_out, float* val_out, int32_t* k_out, DevFlags* fl,
                             cudaStream_t s);
 cudaError_t launch_project(const float* planes, int n, int n_pad, int deg, const CamBatch& cams, int n_views,
-                           float* rec, uint32_t* depth, uint32_t* tiles, int16_t* rect, DevFlags* fl, cudaStream_t s);
+                           float* rec, uint32_t* depth, uint32_t* tiles, int16_t* rect, const uint8_t* select,
+                           DevFlags* fl, cudaStream_t s);
 cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
                             const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof);
 cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
-                             cudaStream_t s);
+                             uint8_t* mask_out, float mask_thresh, cudaStream_t s);
+cudaError_t launch_select(const uint32_t* idx, int k, const int32_t* k_dev, int n, int n_pad, uint8_t* select,
+                          DevFlags* fl, cudaStream_t s);
+cudaError_t launch_dilate(uint8_t* marks, uint8_t* tmp, int n_views, int W, int H, int d, cudaStream_t s);
 cudaError_t launch_blend_counts(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                                 int W, int H, long long* evaluated, long long* composited, cudaStream_t s);
 cudaError_t init_kernel_attributes();

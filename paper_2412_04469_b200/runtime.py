@@ -10,7 +10,7 @@ import torch
 
 from . import (QUEEN_LAT_F32, QUEEN_LAT_INT8, QUEEN_MAX_VIEWS, QUEEN_POS_COO, QUEEN_POS_GATES, Context,
                QueenError, camera_array, gaussians_struct, packet_struct, queen_apply_frame,
-               queen_entropy_decode_frame, queen_render_views, queen_wait_binned)
+               queen_entropy_decode_frame, queen_render_mask, queen_render_views, queen_wait_binned)
 from . import packet as wire
 
 
@@ -163,6 +163,19 @@ class Player:
         for s in self.streams[1:]:
             main.wait_stream(s)
         return rgb
+
+    def render_mask(self, subset_idx, k: int | None = None, k_dev=None, out=None, alpha_thresh: float = 1e-3,
+                    dilation: int = 48, stream=None):
+        """NEXT #3: u8 [V][H][W] masks of the pixels the Gaussian subset
+        (device u32 indices, strictly increasing; e.g. a packet's gated COO) reaches with
+        accumulated alpha > alpha_thresh, dilated by a dilation x dilation square."""
+        k = int(subset_idx.numel()) if k is None else int(k)
+        if out is None:
+            out = torch.empty((len(self.cams), self.H, self.W), dtype=torch.uint8, device=self.dev)
+        for (a, b), arr in zip(self.batches, self.cam_arrays):
+            queen_render_mask(self.ctx, self.scene, subset_idx, k, None, out[a:b], alpha_thresh, dilation, k_dev=k_dev,
+                              stream=stream, cam_array=arr)
+        return out
 
     def frame(self, pkt: DevicePacket | None, stream=None):
         if pkt is not None:
