@@ -524,6 +524,36 @@ def main():
                   "alpha_thresh": 1e-3, "note": "queen_render_mask of frame 1's gated COO set, all views (L2 warm)"}
         del mk
 
+    # ---- NEXT #2: densification delta of a frame (0.5 % removed, 1 % added; DESIGN R21)
+    densify = None
+    if rank == 0 and not args.no_paper_style:
+        from paper_2412_04469_b200 import gaussians_struct, queen_densify
+        stt = synth.Scene(sc.cfg, sc.n, sc.n_pad, sc.deg, sc.planes, sc.dynamic)
+        dl = synth.make_delta(stt, 1)
+        n_new = sc.n - dl.rem.size + dl.add.shape[1]
+        cap = (max(sc.n_pad, n_new) + 3) // 4 * 4
+        srcb = torch.zeros((sc.planes.shape[0], cap), dtype=torch.float32, device=dev)
+        srcb[:, :sc.n_pad] = player.planes[:, :sc.n_pad]
+        dstb = torch.empty_like(srcb)
+        rem_d = torch.from_numpy(dl.rem.view(np.int32)).to(dev)
+        add_d = torch.from_numpy(dl.add.view(np.int16)).to(dev)
+        s_src, s_dst = gaussians_struct(srcb, sc.n, sc.deg), gaussians_struct(dstb, n_new, sc.deg)
+        queen_densify(player.ctx, s_src, rem_d, dl.rem.size, add_d, dl.add.shape[1], s_dst)
+        de0, de1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.zero_()
+        de0.record(stream)
+        queen_densify(player.ctx, s_src, rem_d, dl.rem.size, add_d, dl.add.shape[1], s_dst)
+        de1.record(stream)
+        torch.cuda.synchronize()
+        dms = de0.elapsed_time(de1)
+        P_ = sc.planes.shape[0]
+        dbytes = 4 * P_ * (2 * (sc.n - dl.rem.size) + (cap - (sc.n - dl.rem.size))) + 2 * P_ * dl.add.shape[1]
+        densify = {"ms": dms, "n_before": sc.n, "n_removed": int(dl.rem.size), "n_added": int(dl.add.shape[1]),
+                   "algorithmic_GBps": dbytes / (dms * 1e-3) / 1e9,
+                   "note": "queen_densify of a synthetic delta (P:457, DESIGN R21), L2 flushed; bytes = kept columns "
+                           "read + written, additions (binary16) read, tail written"}
+        del srcb, dstb
+
     # ---- end to end through the public API with host buffers (pinned H2D packet, D2H images)
     e2e = None
     if not args.no_e2e:
@@ -620,7 +650,7 @@ def main():
             "mpixel_per_s": mpix, "view_fps": value * V,
             "status": Q.STATUS.get(st, st),
             "keys_per_batch": K_list, "visible_pairs_per_batch": M_list, "stages": stages, "roofline": roof,
-            "path_roofline": path, "paper_style": paper, "library_sort": libsort, "masked_render": masked, "cpu_baseline": cpu, "e2e": e2e,
+            "path_roofline": path, "paper_style": paper, "library_sort": libsort, "masked_render": masked, "densify": densify, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
         }
         print(json.dumps(line))

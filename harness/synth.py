@@ -334,6 +334,62 @@ def make_packet(scene: Scene, t: int, *, gates: bool = True, beta: float | None 
                   log_alpha, pregate, (tau, g0, g1))
 
 
+# ----------------------------------------------------------------------------- NEXT #2
+@dataclass
+class Delta:
+    """Densification delta of frame t (DESIGN reading R21): removals (sorted indices into the
+    current set) then additions (raw parameters as IEEE binary16, SoA [P][n_add])."""
+    rem: np.ndarray   # uint32 [n_rem], strictly increasing
+    add: np.ndarray   # float16 [P][n_add]
+
+
+def make_delta(state: Scene, t: int, rem_frac: float = 0.005, add_frac: float = 0.01) -> Delta:
+    """Synthetic densification of frame t: ~rem_frac of the current Gaussians pruned (uniform),
+    ~add_frac cloned from random dynamic Gaussians (3D-GS clone: same attributes, position
+    jittered by 5 mm, log-scales shrunk by ln 1.6), stored as binary16."""
+    cfg = state.cfg
+    rng = np.random.Generator(np.random.PCG64([cfg.seed, 0xD3, t]))
+    n = state.n
+    n_rem = int(round(rem_frac * n))
+    rem = np.sort(rng.choice(n, n_rem, replace=False)).astype(np.uint32) if n_rem else np.zeros(0, np.uint32)
+    n_add = int(round(add_frac * n))
+    P = 11 + 3 * (state.deg + 1) ** 2
+    pool = state.dynamic if len(state.dynamic) else np.arange(n)
+    src = rng.choice(pool, n_add, replace=True) if n_add else np.zeros(0, np.int64)
+    add = np.zeros((P, n_add), np.float32)
+    if state.planes is not None and n_add:
+        add[:] = state.planes[:, src]
+    else:  # attribute-free state: fresh Gaussians drawn like the scene
+        add[0:3] = rng.uniform(-1, 1, (3, n_add))
+        add[0:3, :] += np.array([[0.0], [0.0], [3.5]])
+        add[3:7] = _rotations(rng, n_add)
+        add[7:10] = np.log(0.01)
+        add[10] = 2.0
+        add[11:14] = rng.uniform(-1.5, 1.5, (3, n_add))
+    add[0:3] += rng.normal(0.0, 5e-3, (3, n_add))
+    add[7:10] -= np.log(1.6)
+    return Delta(rem, add.astype(np.float16))
+
+
+def advance_state(state: Scene, delta: Delta, n_pad: int | None = None) -> Scene:
+    """Bookkeeping of the synthetic stream after a delta (no method arithmetic): new count, the
+    dynamic pool re-indexed after the removals, additions counted as dynamic.  The returned
+    state carries no planes (the stream's attributes live on the renderer / oracle side)."""
+    n = state.n
+    keep = np.ones(n, bool)
+    keep[delta.rem.astype(np.int64)] = False
+    new_index = np.cumsum(keep) - 1
+    pool = state.dynamic[keep[state.dynamic]] if len(state.dynamic) else state.dynamic
+    pool = new_index[pool]
+    n_kept = int(keep.sum())
+    n_new = n_kept + delta.add.shape[1]
+    pool = np.concatenate([pool, np.arange(n_kept, n_new)]).astype(np.int64)
+    n_pad = state.n_pad if n_pad is None else n_pad
+    if n_new > n_pad:
+        raise ValueError("stream outgrew the capacity n_pad")
+    return Scene(state.cfg, n_new, n_pad, state.deg, None, pool)
+
+
 def make_dyadic_scene(cfg: Config, n: int | None = None) -> Scene:
     """A_0 on the 2^-10 grid with |A_0| <= 256, so dyadic decode/apply is exact in fp32."""
     s = make_scene(cfg, n)

@@ -226,6 +226,18 @@ queen_status queen_entropy_decode(queen_ctx* ctx, const void* stream_dev, int32_
 queen_status queen_entropy_decode_frame(queen_ctx* ctx, const void* const* streams_dev, const int32_t* lat_dim,
                                         int32_t n, int32_t n_pad, int8_t* latents_out, void* stream);
 
+/* ---- NEXT #2: densification deltas (DESIGN reading R21) --------------------
+ * queen_densify: dst = src without the Gaussians rem_idx (surviving columns keep their order)
+ *   followed by n_add added Gaussians in order, whose attributes come as IEEE binary16 SoA
+ *   add_attrs [11+3B][n_add] (host layout of the raw parameters, converted exactly to fp32).
+ *   rem_idx: device u32 [n_rem], strictly increasing, each < src->n (else QUEEN_ERR_INDEX,
+ *   sticky; dst contents undefined).  src and dst: same sh_degree, DISTINCT buffers (ping-pong);
+ *   dst->n must equal src->n - n_rem + n_add <= dst->n_pad; dst padding columns are zeroed.
+ *   Call after queen_apply_frame of the same frame (residuals refer to the pre-densification
+ *   set). */
+queen_status queen_densify(queen_ctx* ctx, const queen_gaussians* src, const uint32_t* rem_idx, int32_t n_rem,
+                           const uint16_t* add_attrs, int32_t n_add, queen_gaussians* dst, void* stream);
+
 /* ---- NEXT #3: masked / dynamic-subset rendering -----
  * queen_render_mask: renders ONLY the Gaussians listed in subset_idx (device u32 [k], strictly
  *   increasing, each < scene->n; when k_dev (device int32) is non-NULL the live count is

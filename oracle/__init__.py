@@ -302,3 +302,24 @@ def render_mask(planes: np.ndarray, n: int, deg: int, cams, subset, alpha_thresh
     _, _, _, T = render(sub, k, deg, cams, threads=threads)
     marks = (np.float32(1.0) - T) > np.float32(alpha_thresh)
     return dilate(marks, dilation).astype(np.uint8)
+
+
+# ----------------------------------------------------------------------------- NEXT #2
+def densify(planes: np.ndarray, n: int, rem, add16, n_pad_out: int | None = None):
+    """Densification delta (DESIGN reading R21): the set without the removed columns
+    (survivors in order) followed by the additions (binary16 raw parameters -> float32, exact).
+    Returns (planes_out [P][n_pad_out], n_out, status) with status -3 for a removal list that is
+    not strictly increasing or out of range (planes_out then None)."""
+    rem = np.asarray(rem, np.int64)
+    add = np.asarray(add16, np.float16)
+    if rem.size and (rem.min() < 0 or rem.max() >= n or np.any(np.diff(rem) <= 0)):
+        return None, 0, -3
+    keep = np.ones(n, bool)
+    keep[rem] = False
+    cols = [planes[:, :n][:, keep], add.astype(np.float32)]
+    body = np.concatenate(cols, axis=1)
+    n_out = body.shape[1]
+    n_pad_out = max(4, (n_out + 3) // 4 * 4) if n_pad_out is None else n_pad_out
+    out = np.zeros((planes.shape[0], n_pad_out), np.float32)
+    out[:, :n_out] = body
+    return out, n_out, 0

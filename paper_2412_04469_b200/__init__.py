@@ -29,7 +29,8 @@ EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version",
            "queen_set_workspace", "queen_check", "queen_decode_residuals", "queen_apply_frame", "queen_project",
            "queen_bin_sort", "queen_rasterize", "queen_render_views", "queen_blend_counts",
            "queen_profile_enable", "queen_profile_read", "queen_wait_binned", "queen_entropy_encode",
-           "queen_entropy_decode", "queen_entropy_decode_frame", "queen_render_mask"]
+           "queen_entropy_decode", "queen_entropy_decode_frame", "queen_render_mask",
+           "queen_densify"]
 STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy"]
 
 
@@ -102,6 +103,7 @@ def lib() -> C.CDLL:
             "queen_blend_counts": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
                                          p, p, p]),
             "queen_profile_enable": (i32, [p, i32]),
+            "queen_densify": (i32, [p, C.POINTER(QueenGaussians), p, i32, p, i32, C.POINTER(QueenGaussians), p]),
             "queen_render_mask": (i32, [p, C.POINTER(QueenGaussians), p, i32, p, C.POINTER(QueenCamera), i32, C.c_float,
                                         i32, p, p]),
             "queen_wait_binned": (i32, [p, p]),
@@ -313,6 +315,14 @@ def queen_render_mask(ctx: Context, scene: QueenGaussians, subset_idx, k: int, c
     st = lib().queen_render_mask(ctx.handle, C.byref(scene), _ptr(subset_idx), int(k), _ptr(k_dev), arr, len(arr),
                                  float(alpha_thresh), int(dilation), _ptr(mask_out), C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_render_mask")
+
+
+def queen_densify(ctx: Context, src: QueenGaussians, rem_idx, n_rem: int, add_attrs, n_add: int, dst: QueenGaussians,
+                  stream=None):
+    """NEXT #2: dst = src minus the removed columns, plus the binary16 additions (queen.h)."""
+    st = lib().queen_densify(ctx.handle, C.byref(src), _ptr(rem_idx), int(n_rem), _ptr(add_attrs), int(n_add),
+                             C.byref(dst), C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_densify")
 
 
 def queen_entropy_encode(latents: np.ndarray, n: int) -> np.ndarray:

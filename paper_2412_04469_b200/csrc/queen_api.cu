@@ -393,6 +393,25 @@ queen_status queen_render_views(queen_ctx* ctx, const queen_gaussians* scene, co
     return queen_rasterize(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, stream);
 }
 
+queen_status queen_densify(queen_ctx* ctx, const queen_gaussians* src, const uint32_t* rem_idx, int32_t n_rem,
+                           const uint16_t* add_attrs, int32_t n_add, queen_gaussians* dst, void* stream) {
+    if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
+    if (!src || !dst || !src->planes || !dst->planes) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null scene");
+    if (src->planes == dst->planes) return fail(ctx, QUEEN_ERR_INVALID_ARG, "src and dst must be distinct buffers");
+    if (n_rem < 0 || n_add < 0 || (n_rem > 0 && !rem_idx) || (n_add > 0 && !add_attrs))
+        return fail(ctx, QUEEN_ERR_INVALID_ARG, "bad removal / addition lists");
+    if (src->sh_degree != dst->sh_degree || src->sh_degree < 0 || src->sh_degree > 3)
+        return fail(ctx, QUEEN_ERR_INVALID_ARG, "sh_degree");
+    if (src->n < 0 || src->n > src->n_pad || n_rem > src->n) return fail(ctx, QUEEN_ERR_SHAPE, "src n / n_rem");
+    if (dst->n != src->n - n_rem + n_add || dst->n > dst->n_pad || dst->n_pad % 4)
+        return fail(ctx, QUEEN_ERR_SHAPE, "dst n must be src n - n_rem + n_add <= dst n_pad (n_pad % 4 == 0)");
+    const int B = (src->sh_degree + 1) * (src->sh_degree + 1);
+    cudaError_t e = launch_densify(src->planes, src->n, src->n_pad, rem_idx, n_rem, add_attrs, n_add, 11 + 3 * B,
+                                   dst->planes, dst->n_pad, flags_of(ctx), static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "densify");
+    return QUEEN_OK;
+}
+
 queen_status queen_render_mask(queen_ctx* ctx, const queen_gaussians* scene, const uint32_t* subset_idx, int32_t k,
                                const int32_t* k_dev, const queen_camera* cams, int32_t n_views, float alpha_thresh,
                                int32_t dilation, uint8_t* mask_out, void* stream) {

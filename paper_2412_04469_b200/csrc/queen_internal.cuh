@@ -260,6 +260,8 @@ cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges
 cudaError_t launch_select(const uint32_t* idx, int k, const int32_t* k_dev, int n, int n_pad, uint8_t* select,
                           DevFlags* fl, cudaStream_t s);
 cudaError_t launch_dilate(uint8_t* marks, uint8_t* tmp, int n_views, int W, int H, int d, cudaStream_t s);
+cudaError_t launch_densify(const float* src, int n_old, int np_src, const uint32_t* rem, int n_rem, const void* add,
+                           int n_add, int P, float* dst, int np_dst, DevFlags* fl, cudaStream_t s);
 cudaError_t launch_blend_counts(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                                 int W, int H, long long* evaluated, long long* composited, cudaStream_t s);
 cudaError_t init_kernel_attributes();

@@ -10,7 +10,8 @@ import torch
 
 from . import (QUEEN_LAT_F32, QUEEN_LAT_INT8, QUEEN_MAX_VIEWS, QUEEN_POS_COO, QUEEN_POS_GATES, Context,
                QueenError, camera_array, gaussians_struct, packet_struct, queen_apply_frame,
-               queen_entropy_decode_frame, queen_render_mask, queen_render_views, queen_wait_binned)
+               queen_densify, queen_entropy_decode_frame, queen_render_mask, queen_render_views,
+               queen_wait_binned)
 from . import packet as wire
 
 
@@ -97,12 +98,19 @@ class Player:
     lane's kernels wait for free slots: 2 lanes 3.77 ms vs 1 lane 3.55 ms), hence lanes=1."""
 
     def __init__(self, planes, n: int, deg: int, cams, *, device: int = 0, keys_cap: int | None = None,
-                 views_per_batch: int | None = None, bg=(0.0, 0.0, 0.0), with_T: bool = False, lanes: int = 1):
+                 views_per_batch: int | None = None, bg=(0.0, 0.0, 0.0), with_T: bool = False, lanes: int = 1,
+                 n_cap: int | None = None):
         self.dev = torch.device(f"cuda:{device}")
         self.device = device
         if isinstance(planes, np.ndarray):
             planes = torch.from_numpy(np.ascontiguousarray(planes, np.float32))
         self.planes = planes.to(self.dev).contiguous()
+        if n_cap is not None and n_cap > self.planes.shape[1]:  # room for densification growth
+            cap = (int(n_cap) + 3) // 4 * 4
+            grown = torch.zeros((self.planes.shape[0], cap), dtype=torch.float32, device=self.dev)
+            grown[:, :self.planes.shape[1]] = self.planes
+            self.planes = grown
+        self._planes_b = None  # densification ping-pong buffer (allocated on first use)
         self.n, self.deg = n, deg
         self.cams = list(cams)
         W, H = self.cams[0].width, self.cams[0].height
@@ -163,6 +171,21 @@ class Player:
         for s in self.streams[1:]:
             main.wait_stream(s)
         return rgb
+
+    def densify(self, rem_idx, n_rem: int, add_attrs, n_add: int, stream=None):
+        """NEXT #2: apply a densification delta after the frame's residuals (queen_densify):
+        drop the removed Gaussians (device u32, strictly increasing), append the binary16
+        additions (device [P][n_add]); the set is rebuilt in the second buffer, then swapped."""
+        n_new = self.n - int(n_rem) + int(n_add)
+        if n_new > self.planes.shape[1]:
+            raise QueenError(-2, f"densify: {n_new} Gaussians exceed the capacity {self.planes.shape[1]}")
+        if self._planes_b is None:
+            self._planes_b = torch.empty_like(self.planes)
+        dst = gaussians_struct(self._planes_b, n_new, self.deg)
+        queen_densify(self.ctx, self.scene, rem_idx, n_rem, add_attrs, n_add, dst, stream)
+        self.planes, self._planes_b = self._planes_b, self.planes
+        self.n = n_new
+        self.scene = dst
 
     def render_mask(self, subset_idx, k: int | None = None, k_dev=None, out=None, alpha_thresh: float = 1e-3,
                     dilation: int = 48, stream=None):
