@@ -555,15 +555,15 @@ def main():
         del srcb, dstb
 
     # ---- end to end through the public API with host buffers (pinned H2D packet, D2H images)
-    e2e = None
-    if not args.no_e2e:
+    def run_e2e(rgb8: bool):
         # Streaming player through the public API: per frame a pinned H2D of the wire packet
-        # (own stream, double-buffered), [NCCL broadcast], apply + render on the compute stream,
-        # and a D2H of the fp32 images of this rank's views (own stream, double-buffered), so
+        # (own stream, double-buffered), [NCCL broadcast], decode + apply + render on the compute
+        # stream, and a D2H of the images of this rank's views (own stream, double-buffered), so
         # the copies of frame k overlap the compute of frames k +- 1 like a real player.
         pin_pk = [torch.from_numpy(b).pin_memory() for b in host_bufs] if rank == 0 else None
-        out_dev = [torch.empty_like(player.rgb) for _ in range(2)]
-        out_host = [torch.empty(player.rgb.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
+        odt = torch.uint8 if rgb8 else torch.float32
+        out_dev = [torch.empty(player.rgb.shape, dtype=odt, device=dev) for _ in range(2)]
+        out_host = [torch.empty(player.rgb.shape, dtype=odt).pin_memory() for _ in range(2)]
         recv = [torch.zeros(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
         dp_recv = [mkpkt(r) for r in recv]
         s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
@@ -600,7 +600,7 @@ def main():
             ev_apply[k].record(stream)
             if k >= 2:
                 stream.wait_event(ev_d2h[k - 2])  # out_dev[slot] drained to the host
-            player.render(out=out_dev[slot])
+            player.render(out=out_dev[slot], rgb8=rgb8)
             ev_render[k].record(stream)
             lat1[k].record(stream)
             with torch.cuda.stream(s_d2h):
@@ -616,14 +616,21 @@ def main():
         e_ms = torch.tensor([t0.elapsed_time(t1), lat_med], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-        e2e = {"value": args.steps / (float(e_ms[0]) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(statistics.mean(used_bytes)) if rank == 0 else 0,
-               "d2h_bytes_per_step": int(out_host[0].numel() * 4),
-               "frame_latency_ms": float(e_ms[1]),
-               "note": "runtime.Player public API: pinned H2D of each frame's wire packet + apply + render + "
-                       "D2H of this rank's fp32 RGB images, copies on their own streams (double-buffered), "
-                       "timed from the first H2D to the last D2H; working set per frame >> L2; frame_latency_ms = "
-                       "median of (packet H2D start -> frame rendered on the device), max over ranks"}
+        return {"value": args.steps / (float(e_ms[0]) / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": int(statistics.mean(used_bytes)) if rank == 0 else 0,
+                "d2h_bytes_per_step": int(out_host[0].numel() * out_host[0].element_size()),
+                "frame_latency_ms": float(e_ms[1]),
+                "output": "rgb8: u8 [V][3][H][W] display format (queen_render_views_rgb8)" if rgb8 else
+                          "fp32 [V][3][H][W] (queen_render_views)",
+                "note": "runtime.Player public API: pinned H2D of each frame's wire packet + entropy decode + apply + "
+                        "render + D2H of this rank's images, copies on their own streams (double-buffered), timed "
+                        "from the first H2D to the last D2H; working set per frame >> L2; frame_latency_ms = median "
+                        "of (packet H2D start -> frame rendered on the device), max over ranks"}
+
+    e2e = e2e_f32 = None
+    if not args.no_e2e:
+        e2e = run_e2e(rgb8=True)
+        e2e_f32 = run_e2e(rgb8=False)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -650,7 +657,8 @@ def main():
             "mpixel_per_s": mpix, "view_fps": value * V,
             "status": Q.STATUS.get(st, st),
             "keys_per_batch": K_list, "visible_pairs_per_batch": M_list, "stages": stages, "roofline": roof,
-            "path_roofline": path, "paper_style": paper, "library_sort": libsort, "masked_render": masked, "densify": densify, "cpu_baseline": cpu, "e2e": e2e,
+            "path_roofline": path, "paper_style": paper, "library_sort": libsort, "masked_render": masked, "densify": densify,
+            "e2e_f32": e2e_f32, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
         }
         print(json.dumps(line))

@@ -201,6 +201,15 @@ queen_status queen_rasterize(queen_ctx* ctx, const queen_proj* proj, const queen
 queen_status queen_render_views(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
                                 int32_t n_views, const float bg[3], float* rgb_out, float* T_out, void* stream);
 
+/* Display-format variants (the streaming viewer's output): identical compositing, then
+ * rgb8_out u8 [n_views][3][H][W] = round-half-even(clamp(C + T bg, 0, 1) * 255) in fp32;
+ * T_out as above (nullable). */
+queen_status queen_rasterize_rgb8(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
+                                  const queen_camera* cams, int32_t n_views, const float bg[3], uint8_t* rgb8_out,
+                                  float* T_out, void* stream);
+queen_status queen_render_views_rgb8(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
+                                     int32_t n_views, const float bg[3], uint8_t* rgb8_out, float* T_out, void* stream);
+
 /* Debug / evidence: per-view blend work counters (evaluated and composited
  * (pixel, Gaussian) pairs, int64 device arrays [n_views]); same semantics as the
  * rasterizer, used only to compute the blend roofline. */

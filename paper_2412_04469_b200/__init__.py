@@ -30,7 +30,7 @@ EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version",
            "queen_bin_sort", "queen_rasterize", "queen_render_views", "queen_blend_counts",
            "queen_profile_enable", "queen_profile_read", "queen_wait_binned", "queen_entropy_encode",
            "queen_entropy_decode", "queen_entropy_decode_frame", "queen_render_mask",
-           "queen_densify"]
+           "queen_densify", "queen_rasterize_rgb8", "queen_render_views_rgb8"]
 STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy"]
 
 
@@ -103,6 +103,10 @@ def lib() -> C.CDLL:
             "queen_blend_counts": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
                                          p, p, p]),
             "queen_profile_enable": (i32, [p, i32]),
+            "queen_rasterize_rgb8": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
+                                           C.POINTER(C.c_float), p, p, p]),
+            "queen_render_views_rgb8": (i32, [p, C.POINTER(QueenGaussians), C.POINTER(QueenCamera), i32,
+                                              C.POINTER(C.c_float), p, p, p]),
             "queen_densify": (i32, [p, C.POINTER(QueenGaussians), p, i32, p, i32, C.POINTER(QueenGaussians), p]),
             "queen_render_mask": (i32, [p, C.POINTER(QueenGaussians), p, i32, p, C.POINTER(QueenCamera), i32, C.c_float,
                                         i32, p, p]),
@@ -323,6 +327,24 @@ def queen_densify(ctx: Context, src: QueenGaussians, rem_idx, n_rem: int, add_at
     st = lib().queen_densify(ctx.handle, C.byref(src), _ptr(rem_idx), int(n_rem), _ptr(add_attrs), int(n_add),
                              C.byref(dst), C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_densify")
+
+
+def queen_rasterize_rgb8(ctx: Context, proj: QueenProj, bins: QueenBins, cams, rgb8_out, T_out=None,
+                         bg=(0.0, 0.0, 0.0), stream=None):
+    arr = camera_array(cams)
+    bgv = (C.c_float * 3)(*[float(x) for x in bg])
+    st = lib().queen_rasterize_rgb8(ctx.handle, C.byref(proj), C.byref(bins), arr, len(arr), bgv, _ptr(rgb8_out),
+                                    _ptr(T_out), C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_rasterize_rgb8")
+
+
+def queen_render_views_rgb8(ctx: Context, scene: QueenGaussians, cams, rgb8_out, T_out=None, bg=(0.0, 0.0, 0.0),
+                            stream=None, cam_array=None):
+    arr = cam_array if cam_array is not None else camera_array(cams)
+    bgv = (C.c_float * 3)(*[float(x) for x in bg])
+    st = lib().queen_render_views_rgb8(ctx.handle, C.byref(scene), arr, len(arr), bgv, _ptr(rgb8_out), _ptr(T_out),
+                                       C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_render_views_rgb8")
 
 
 def queen_entropy_encode(latents: np.ndarray, n: int) -> np.ndarray:

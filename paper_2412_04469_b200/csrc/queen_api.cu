@@ -264,18 +264,33 @@ queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_
     return QUEEN_OK;
 }
 
-queen_status queen_rasterize(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins, const queen_camera* cams,
-                             int32_t n_views, const float bg[3], float* rgb_out, float* T_out, void* stream) {
+static queen_status rasterize_impl(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
+                                   const queen_camera* cams, int32_t n_views, const float bg[3], float* rgb_out,
+                                   float* T_out, uint8_t* rgb8_out, void* stream) {
     if (!ctx) return QUEEN_ERR_INVALID_ARG;
-    if (!proj || !bins || !rgb_out || !bg) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
+    if (!proj || !bins || !(rgb_out || rgb8_out) || !bg) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
     if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
     const uint32_t* vals = bins->sorted_in_alt ? bins->vals_alt : bins->vals;
     ctx->prof.begin(ST_BLEND, static_cast<cudaStream_t>(stream));
     cudaError_t e = launch_rasterize(proj->rec, proj->n_pad, bins->ranges, vals, n_views, cams[0].width, cams[0].height,
-                                     bg[0], bg[1], bg[2], rgb_out, T_out, nullptr, 0.f, static_cast<cudaStream_t>(stream));
+                                     bg[0], bg[1], bg[2], rgb_out, T_out, rgb8_out, rgb8_out ? OUT_RGB8 : OUT_F32, 0.f,
+                                     static_cast<cudaStream_t>(stream));
     ctx->prof.end(static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "rasterize");
     return QUEEN_OK;
+}
+
+queen_status queen_rasterize(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins, const queen_camera* cams,
+                             int32_t n_views, const float bg[3], float* rgb_out, float* T_out, void* stream) {
+    if (ctx && !rgb_out) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null rgb_out");
+    return rasterize_impl(ctx, proj, bins, cams, n_views, bg, rgb_out, T_out, nullptr, stream);
+}
+
+queen_status queen_rasterize_rgb8(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
+                                  const queen_camera* cams, int32_t n_views, const float bg[3], uint8_t* rgb8_out,
+                                  float* T_out, void* stream) {
+    if (ctx && !rgb8_out) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null rgb8_out");
+    return rasterize_impl(ctx, proj, bins, cams, n_views, bg, nullptr, T_out, rgb8_out, stream);
 }
 
 queen_status queen_blend_counts(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
@@ -362,10 +377,10 @@ queen_status queen_entropy_decode_frame(queen_ctx* ctx, const void* const* strea
     return QUEEN_OK;
 }
 
-queen_status queen_render_views(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams, int32_t n_views,
-                                const float bg[3], float* rgb_out, float* T_out, void* stream) {
+static queen_status render_impl(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams, int32_t n_views,
+                                const float bg[3], float* rgb_out, float* T_out, uint8_t* rgb8_out, void* stream) {
     if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
-    if (!scene || !rgb_out || !bg) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
+    if (!scene || !(rgb_out || rgb8_out) || !bg) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
     if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
     if (scene->n_pad > ctx->ws_n_pad || n_views > ctx->ws_views || cams[0].width > ctx->ws_w || cams[0].height > ctx->ws_h)
         return fail(ctx, QUEEN_ERR_SHAPE, "workspace was sized for a smaller batch");
@@ -390,7 +405,19 @@ queen_status queen_render_views(queen_ctx* ctx, const queen_gaussians* scene, co
     if (queen_status st = queen_bin_sort(ctx, &pj, cams, n_views, &b, stream)) return st;
     if (cudaEventRecord(ctx->binned, static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return cuda_fail(ctx, cudaGetLastError(), "record binned event");
-    return queen_rasterize(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, stream);
+    return rasterize_impl(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, rgb8_out, stream);
+}
+
+queen_status queen_render_views(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams, int32_t n_views,
+                                const float bg[3], float* rgb_out, float* T_out, void* stream) {
+    if (ctx && !rgb_out) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null rgb_out");
+    return render_impl(ctx, scene, cams, n_views, bg, rgb_out, T_out, nullptr, stream);
+}
+
+queen_status queen_render_views_rgb8(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
+                                     int32_t n_views, const float bg[3], uint8_t* rgb8_out, float* T_out, void* stream) {
+    if (ctx && !rgb8_out) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null rgb8_out");
+    return render_impl(ctx, scene, cams, n_views, bg, nullptr, T_out, rgb8_out, stream);
 }
 
 queen_status queen_densify(queen_ctx* ctx, const queen_gaussians* src, const uint32_t* rem_idx, int32_t n_rem,
@@ -454,7 +481,7 @@ queen_status queen_render_mask(queen_ctx* ctx, const queen_gaussians* scene, con
     const uint32_t* vals = b.sorted_in_alt ? b.vals_alt : b.vals;
     ctx->prof.begin(ST_BLEND, s);
     e = launch_rasterize(pj.rec, pj.n_pad, b.ranges, vals, n_views, W, H, 0.f, 0.f, 0.f, nullptr, nullptr, mask_out,
-                         alpha_thresh, s);
+                         OUT_MASK, alpha_thresh, s);
     if (e == cudaSuccess) e = launch_dilate(mask_out, reinterpret_cast<uint8_t*>(ws + L.mask_tmp), n_views, W, H, dilation, s);
     ctx->prof.end(s, dilation > 1 ? 3 : 1);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "render_mask");

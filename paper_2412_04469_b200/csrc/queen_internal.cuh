@@ -254,9 +254,10 @@ cudaError_t launch_project(const float* planes, int n, int n_pad, int deg, const
                            DevFlags* fl, cudaStream_t s);
 cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
                             const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof);
+enum : int { OUT_F32 = 0, OUT_MASK = 1, OUT_RGB8 = 2 };  // k_blend epilogues
 cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
-                             uint8_t* mask_out, float mask_thresh, cudaStream_t s);
+                             uint8_t* out8, int out_mode, float mask_thresh, cudaStream_t s);
 cudaError_t launch_select(const uint32_t* idx, int k, const int32_t* k_dev, int n, int n_pad, uint8_t* select,
                           DevFlags* fl, cudaStream_t s);
 cudaError_t launch_dilate(uint8_t* marks, uint8_t* tmp, int n_views, int W, int H, int d, cudaStream_t s);

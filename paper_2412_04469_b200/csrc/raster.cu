@@ -98,7 +98,7 @@ template <bool COUNT, int RPT, bool WMASK>
 __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ rec, int n_pad, const uint2* __restrict__ ranges,
                                                     const uint32_t* __restrict__ vals, int W, int H, int gx, int T, float bg0,
                                                     float bg1, float bg2, float* __restrict__ rgb_out, float* __restrict__ T_out,
-                                                    uint8_t* __restrict__ mask_out, float mask_thresh, long long* ev_out,
+                                                    uint8_t* __restrict__ out8, int out_mode, float mask_thresh, long long* ev_out,
                                                     long long* cp_out) {
     constexpr int NT = 256 / RPT;          // threads per tile CTA: one column x RPT rows each
     constexpr int BATCH = NT > 64 ? NT : 64;  // records staged per batch
@@ -265,13 +265,33 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
         }
         return;
     }
-    if (mask_out) {  // render_mask: mark pixels whose accumulated alpha 1 - T exceeds the threshold
+    if (out_mode == OUT_MASK) {  // render_mask: mark pixels whose accumulated alpha 1 - T exceeds the threshold
         if (px < W) {
-            uint8_t* mo = mask_out + (int64_t)v * H * W + (int64_t)py0 * W + px;
+            uint8_t* mo = out8 + (int64_t)v * H * W + (int64_t)py0 * W + px;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
                 const float pT = (r & 1) ? p[r >> 1].T.y : p[r >> 1].T.x;
                 if (py0 + r < H) mo[(int64_t)r * W] = (1.0f - pT > mask_thresh) ? 1 : 0;
+            }
+        }
+        return;
+    }
+    if (out_mode == OUT_RGB8) {  // display format: round(clamp(C + T bg, 0, 1) * 255), planar u8
+        if (px < W) {
+            const int64_t plane = (int64_t)H * W;
+            uint8_t* o8 = out8 + (int64_t)v * 3 * plane + (int64_t)py0 * W + px;
+            float* to = T_out ? T_out + (int64_t)v * plane + (int64_t)py0 * W + px : nullptr;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                if (py0 + r < H) {
+                    const Px2& q = p[r >> 1];
+                    const float pr = (r & 1) ? q.r.y : q.r.x, pg = (r & 1) ? q.g.y : q.g.x, pb = (r & 1) ? q.b.y : q.b.x;
+                    const float pT = (r & 1) ? q.T.y : q.T.x;
+                    o8[(int64_t)r * W] = (uint8_t)__float2uint_rn(fminf(fmaxf(pr + pT * bg0, 0.0f), 1.0f) * 255.0f);
+                    o8[plane + (int64_t)r * W] = (uint8_t)__float2uint_rn(fminf(fmaxf(pg + pT * bg1, 0.0f), 1.0f) * 255.0f);
+                    o8[2 * plane + (int64_t)r * W] = (uint8_t)__float2uint_rn(fminf(fmaxf(pb + pT * bg2, 0.0f), 1.0f) * 255.0f);
+                    if (to) to[(int64_t)r * W] = pT;
+                }
             }
         }
         return;
@@ -299,7 +319,7 @@ constexpr int BLEND_RPT = 4;
 
 cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
-                             uint8_t* mask_out, float mask_thresh, cudaStream_t s) {
+                             uint8_t* out8, int out_mode, float mask_thresh, cudaStream_t s) {
     const int gx = (W + 15) / 16, gy = (H + 15) / 16;
     const int T = gx * gy;
     const int64_t blocks = (int64_t)T * n_views;
@@ -307,11 +327,11 @@ cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges
     if (getenv("QUEEN_BLEND_NOMASK"))  // test hook: per-thread box cull only (no warp record lists)
         k_blend<false, BLEND_RPT, false><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(
             reinterpret_cast<const float4*>(rec), n_pad, reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0, bg1,
-            bg2, rgb_out, T_out, mask_out, mask_thresh, nullptr, nullptr);
+            bg2, rgb_out, T_out, out8, out_mode, mask_thresh, nullptr, nullptr);
     else
         k_blend<false, BLEND_RPT, true><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(
             reinterpret_cast<const float4*>(rec), n_pad, reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0, bg1,
-            bg2, rgb_out, T_out, mask_out, mask_thresh, nullptr, nullptr);
+            bg2, rgb_out, T_out, out8, out_mode, mask_thresh, nullptr, nullptr);
     return cudaGetLastError();
 }
 
@@ -325,7 +345,7 @@ cudaError_t launch_blend_counts(const float* rec, int n_pad, const uint32_t* ran
     if (blocks == 0) return cudaSuccess;
     k_blend<true, BLEND_RPT, false><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
                                                   reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, 0.f, 0.f, 0.f,
-                                                  nullptr, nullptr, nullptr, 0.f, evaluated, composited);
+                                                  nullptr, nullptr, nullptr, OUT_F32, 0.f, evaluated, composited);
     return cudaGetLastError();
 }
 

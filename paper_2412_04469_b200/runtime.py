@@ -11,7 +11,7 @@ import torch
 from . import (QUEEN_LAT_F32, QUEEN_LAT_INT8, QUEEN_MAX_VIEWS, QUEEN_POS_COO, QUEEN_POS_GATES, Context,
                QueenError, camera_array, gaussians_struct, packet_struct, queen_apply_frame,
                queen_densify, queen_entropy_decode_frame, queen_render_mask, queen_render_views,
-               queen_wait_binned)
+               queen_render_views_rgb8, queen_wait_binned)
 from . import packet as wire
 
 
@@ -148,9 +148,13 @@ class Player:
             pkt.decode(self.ctx, stream)
         queen_apply_frame(self.ctx, self.scene, pkt.struct, stream)
 
-    def render(self, stream=None, out=None):
-        """Render every view into `out` (default self.rgb), fp32 [V][3][H][W]."""
+    def render(self, stream=None, out=None, rgb8: bool = False):
+        """Render every view into `out` (default self.rgb): fp32 [V][3][H][W], or with rgb8=True the
+        display format u8 [V][3][H][W] (queen_render_views_rgb8; `out` then required)."""
         rgb = self.rgb if out is None else out
+        if rgb8 and (out is None or out.dtype != torch.uint8):
+            raise ValueError("rgb8 rendering needs a uint8 out tensor [V][3][H][W]")
+        fn = queen_render_views_rgb8 if rgb8 else queen_render_views
         main = stream if stream is not None else torch.cuda.current_stream(self.dev)
         if self.n_lanes > 1:
             start = torch.cuda.Event()
@@ -166,8 +170,8 @@ class Player:
                 # so it runs under the previous batch's blend on the other lane
                 queen_wait_binned(prev, s)
             prev = self.ctxs[k]
-            queen_render_views(self.ctxs[k], self.scene, None, rgb[a:b], None if self.T is None else self.T[a:b],
-                               self.bg, s, cam_array=arr)
+            fn(self.ctxs[k], self.scene, None, rgb[a:b], None if self.T is None else self.T[a:b], self.bg, s,
+               cam_array=arr)
         for s in self.streams[1:]:
             main.wait_stream(s)
         return rgb

@@ -409,3 +409,20 @@ def test_view_larger_than_4k_rejected():
     ok = [synth.make_camera(np.eye(3), np.zeros(3), 3000.0, 3000.0, 3840, 2160)]
     st = Stages(pl, 4, 0, ok, keys_cap=1 << 20).run()
     assert st.bins_np()["K"] > 0
+
+
+def test_render_views_rgb8_display_format():
+    """queen_render_views_rgb8 = the fp32 render quantised round-half-even(clamp(c, 0, 1) * 255)
+    (GPU vs GPU: identical compositing, so bit-exact), and within 1 LSB of the oracle."""
+    from paper_2412_04469_b200.runtime import Player
+    cfg, sc, cams = _render_case("n3dv", 20003, 3, width=333, height=250, focal=280.0)
+    pl = Player(sc.planes, sc.n, sc.deg, cams, bg=(0.2, 0.4, 0.6))
+    pl.fit_capacity()
+    f32 = pl.render().clone()
+    u8 = torch.empty(f32.shape, dtype=torch.uint8, device="cuda")
+    pl.render(out=u8, rgb8=True)
+    q = torch.round(torch.clamp(f32, 0, 1) * 255.0).to(torch.uint8)  # torch.round: half to even
+    assert torch.equal(u8, q)
+    _, _, ref, _ = oracle.render(sc.planes, sc.n, sc.deg, cams, bg=(0.2, 0.4, 0.6))
+    ref8 = np.rint(np.clip(ref, 0, 1) * np.float32(255)).astype(np.int16)
+    assert np.abs(u8.cpu().numpy().astype(np.int16) - ref8).max() <= 1
