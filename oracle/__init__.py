@@ -57,6 +57,7 @@ def lib():
             "oracle_ans_encode": (i64, [p, i32, i32, i32, p, i64]),
             "oracle_ans_decode": (i32, [p, i64, i32, i32, i32, p]),
             "oracle_blend_counts": (None, [i32, i32, i32, i32, p, p, p, p, p, i32]),
+            "oracle_contrib": (None, [i32, i32, i32, i32, p, p, p, p, p, p, p, i32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -323,3 +324,23 @@ def densify(planes: np.ndarray, n: int, rem, add16, n_pad_out: int | None = None
     out = np.zeros((planes.shape[0], n_pad_out), np.float32)
     out[:, :n_out] = body
     return out, n_out, 0
+
+
+# ----------------------------------------------------------------------------- NEXT #4 support
+def contributors(proj, bins, W: int, H: int, threads: int | None = None):
+    """Per-pixel contributor lists of the forward compositing (fp32 decisions, exactly a12's):
+    CSR (offsets [V*H*W+1] int64, gid int32, clamped uint8), pixel index = (v*H + y)*W + x."""
+    rec = proj["rec"]
+    V, n_pad, _ = rec.shape
+    th = threads or default_threads()
+    vals = bins["vals"] if bins["K"] else np.zeros(1, np.uint32)
+    vals = np.ascontiguousarray(vals)
+    counts = np.zeros(V * H * W, np.int32)
+    lib().oracle_contrib(n_pad, V, W, H, _p(rec), _p(bins["ranges"]), _p(vals), _p(counts), None, None, None, th)
+    offsets = np.zeros(V * H * W + 1, np.int64)
+    offsets[1:] = np.cumsum(counts)
+    gid = np.zeros(max(1, int(offsets[-1])), np.int32)
+    clamp = np.zeros(max(1, int(offsets[-1])), np.uint8)
+    lib().oracle_contrib(n_pad, V, W, H, _p(rec), _p(bins["ranges"]), _p(vals), _p(counts), _p(offsets), _p(gid),
+                         _p(clamp), th)
+    return offsets, gid[:offsets[-1]], clamp[:offsets[-1]]

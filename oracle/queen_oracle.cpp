@@ -582,6 +582,40 @@ void oracle_blend_counts(int n_pad, int V, int W, int H, const float* rec, const
 
 
 // ---------------------------------------------------------------------------
+// NEXT #4 support: the contributor list of every pixel -- the records a12 composites, in
+// order, up to and including the one after which T < 1e-4 -- with the 0.99-clamp decision,
+// taken in the forward pass's fp32 arithmetic (blend_step).  The gradient oracle
+// (oracle/grad.py) differentiates Eq. 2 in float64 on exactly these lists.
+// counts[V*H*W]; then lists at offsets[pix]: gid (Gaussian index), clamped (0/1).
+void oracle_contrib(int n_pad, int V, int W, int H, const float* rec, const uint32_t* ranges, const uint32_t* vals_sorted,
+                    int32_t* counts, const int64_t* offsets, int32_t* gid_out, uint8_t* clamp_out, int threads) {
+    const int gx = (W + 15) / 16, gy = (H + 15) / 16;
+    const int64_t T = (int64_t)gx * gy;
+    for (int v = 0; v < V; ++v) {
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 4)
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x) {
+                const int64_t pix = ((int64_t)v * H + y) * W + x;
+                int64_t gt = (int64_t)v * T + (int64_t)(y >> 4) * gx + (x >> 4);
+                float C[3] = {0.0f, 0.0f, 0.0f}, Tr = 1.0f;
+                int32_t c = 0;
+                for (uint32_t j = ranges[2 * gt]; j < ranges[2 * gt + 1]; ++j) {
+                    const float* rc = rec + ((int64_t)v * n_pad + vals_sorted[j]) * 12;
+                    const float p2 = rec_p2(rc, (float)x, (float)y);
+                    if (p2 > 0.0f || p2 < rc[7]) continue;
+                    if (offsets) {
+                        gid_out[offsets[pix] + c] = (int32_t)vals_sorted[j];
+                        clamp_out[offsets[pix] + c] = rc[8] * std::exp2(p2) > 0.99f ? 1 : 0;
+                    }
+                    ++c;
+                    if (blend_step(rc, (float)x, (float)y, C, Tr)) break;
+                }
+                counts[pix] = c;
+            }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // NEXT #1: entropy coding of the integer latents ("flattens our integer
 // latent matrix for each attribute ... then encoded using standard entropy coding
 // approaches such as arithmetic coding").  Plain reference codec for the "QANS" stream of
