@@ -235,6 +235,25 @@ queen_status queen_entropy_decode(queen_ctx* ctx, const void* stream_dev, int32_
 queen_status queen_entropy_decode_frame(queen_ctx* ctx, const void* const* streams_dev, const int32_t* lat_dim,
                                         int32_t n, int32_t n_pad, int8_t* latents_out, void* stream);
 
+/* ---- NEXT #4: backward rasterizer (P:239-251 trains through Eq. 1-2) -----------------------
+ * Gradients of L with respect to the inputs of the forward, holding its discrete decisions
+ * (skip test, 0.99 clamp, composite-then-stop, culls, Jacobian clamp, max(0, .) on colour) at
+ * the values the forward took (the derivative of the piece the input lies in).
+ * queen_rasterize_backward: dL_drgb device fp32 [n_views][3][H][W] (gradient of L w.r.t. the
+ *   queen_rasterize output C + T bg) -> grad_rec device fp32 [n_views][n_pad][9], per record:
+ *   dL/du, dL/dv, dL/dA2, dL/dB2, dL/dC2, dL/do, dL/dr, dL/dg, dL/db (the queen_proj record
+ *   words; A2/B2/C2 the base-2 conic of p2).  Overwritten (zeroed first).  Accumulated with
+ *   float atomics: run-to-run differences at the rounding level.
+ * queen_project_backward: grad_rec (as above, for the same cameras) -> grad_planes device fp32
+ *   [11+3B][n_pad] = dL/d(raw attributes): position, raw quaternion (through its
+ *   normalisation), log-scale, opacity logit, SH coefficients; views summed in order
+ *   (deterministic); padding columns 0.  Overwritten.  cams: host array, <= QUEEN_MAX_VIEWS. */
+queen_status queen_rasterize_backward(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
+                                      const queen_camera* cams, int32_t n_views, const float bg[3], const float* dL_drgb,
+                                      float* grad_rec, void* stream);
+queen_status queen_project_backward(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
+                                    int32_t n_views, const float* grad_rec, float* grad_planes, void* stream);
+
 /* ---- NEXT #2: densification deltas (DESIGN reading R21) --------------------
  * queen_densify: dst = src without the Gaussians rem_idx (surviving columns keep their order)
  *   followed by n_add added Gaussians in order, whose attributes come as IEEE binary16 SoA

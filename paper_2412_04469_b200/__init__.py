@@ -30,7 +30,8 @@ EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version",
            "queen_bin_sort", "queen_rasterize", "queen_render_views", "queen_blend_counts",
            "queen_profile_enable", "queen_profile_read", "queen_wait_binned", "queen_entropy_encode",
            "queen_entropy_decode", "queen_entropy_decode_frame", "queen_render_mask",
-           "queen_densify", "queen_rasterize_rgb8", "queen_render_views_rgb8"]
+           "queen_densify", "queen_rasterize_rgb8", "queen_render_views_rgb8",
+           "queen_rasterize_backward", "queen_project_backward"]
 STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy"]
 
 
@@ -103,6 +104,9 @@ def lib() -> C.CDLL:
             "queen_blend_counts": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
                                          p, p, p]),
             "queen_profile_enable": (i32, [p, i32]),
+            "queen_rasterize_backward": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera),
+                                               i32, C.POINTER(C.c_float), p, p, p]),
+            "queen_project_backward": (i32, [p, C.POINTER(QueenGaussians), C.POINTER(QueenCamera), i32, p, p, p]),
             "queen_rasterize_rgb8": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
                                            C.POINTER(C.c_float), p, p, p]),
             "queen_render_views_rgb8": (i32, [p, C.POINTER(QueenGaussians), C.POINTER(QueenCamera), i32,
@@ -345,6 +349,24 @@ def queen_render_views_rgb8(ctx: Context, scene: QueenGaussians, cams, rgb8_out,
     st = lib().queen_render_views_rgb8(ctx.handle, C.byref(scene), arr, len(arr), bgv, _ptr(rgb8_out), _ptr(T_out),
                                        C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_render_views_rgb8")
+
+
+def queen_rasterize_backward(ctx: Context, proj: QueenProj, bins: QueenBins, cams, dL_drgb, grad_rec,
+                             bg=(0.0, 0.0, 0.0), stream=None):
+    """NEXT #4: dL/d(record) [V][n_pad][9] from dL/d(image) [V][3][H][W] (queen.h)."""
+    arr = camera_array(cams)
+    bgv = (C.c_float * 3)(*[float(x) for x in bg])
+    st = lib().queen_rasterize_backward(ctx.handle, C.byref(proj), C.byref(bins), arr, len(arr), bgv, _ptr(dL_drgb),
+                                        _ptr(grad_rec), C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_rasterize_backward")
+
+
+def queen_project_backward(ctx: Context, scene: QueenGaussians, cams, grad_rec, grad_planes, stream=None):
+    """NEXT #4: dL/d(raw attributes) [P][n_pad] from dL/d(record) (queen.h)."""
+    arr = camera_array(cams)
+    st = lib().queen_project_backward(ctx.handle, C.byref(scene), arr, len(arr), _ptr(grad_rec), _ptr(grad_planes),
+                                      C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_project_backward")
 
 
 def queen_entropy_encode(latents: np.ndarray, n: int) -> np.ndarray:

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libqueen.so")
-SOURCES = ["queen_api.cu", "decode_apply.cu", "project.cu", "binning.cu", "raster.cu", "mask.cu", "densify.cu", "entropy.cu"]
+SOURCES = ["queen_api.cu", "decode_apply.cu", "project.cu", "binning.cu", "raster.cu", "mask.cu", "densify.cu", "backward.cu", "entropy.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # Arithmetic contract: no FMA contraction, IEEE div/sqrt, denormals kept.
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

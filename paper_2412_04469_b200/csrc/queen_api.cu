@@ -420,6 +420,36 @@ queen_status queen_render_views_rgb8(queen_ctx* ctx, const queen_gaussians* scen
     return render_impl(ctx, scene, cams, n_views, bg, nullptr, T_out, rgb8_out, stream);
 }
 
+queen_status queen_rasterize_backward(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
+                                      const queen_camera* cams, int32_t n_views, const float bg[3], const float* dL_drgb,
+                                      float* grad_rec, void* stream) {
+    if (!ctx) return QUEEN_ERR_INVALID_ARG;
+    if (!proj || !bins || !bg || !dL_drgb || !grad_rec) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
+    if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
+    const uint32_t* vals = bins->sorted_in_alt ? bins->vals_alt : bins->vals;
+    cudaError_t e = launch_blend_bwd(proj->rec, proj->n_pad, bins->ranges, vals, n_views, cams[0].width, cams[0].height,
+                                     bg[0], bg[1], bg[2], dL_drgb, grad_rec, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "rasterize_backward");
+    return QUEEN_OK;
+}
+
+queen_status queen_project_backward(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
+                                    int32_t n_views, const float* grad_rec, float* grad_planes, void* stream) {
+    if (!ctx) return QUEEN_ERR_INVALID_ARG;
+    if (!scene || !scene->planes || !grad_rec || !grad_planes) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
+    if (scene->sh_degree < 0 || scene->sh_degree > 3) return fail(ctx, QUEEN_ERR_INVALID_ARG, "sh_degree");
+    if (scene->n < 0 || scene->n > scene->n_pad || scene->n_pad % 4) return fail(ctx, QUEEN_ERR_SHAPE, "n / n_pad");
+    if (n_views > (int32_t)QUEEN_MAX_VIEWS) return fail(ctx, QUEEN_ERR_SHAPE, "n_views > QUEEN_MAX_VIEWS");
+    if (queen_status st = check_cams(ctx, cams, n_views, false)) return st;
+    CamBatch cb;
+    std::memset(&cb, 0, sizeof(cb));
+    std::memcpy(cb.cam, cams, sizeof(queen_camera) * n_views);
+    cudaError_t e = launch_project_bwd(scene->planes, scene->n, scene->n_pad, scene->sh_degree, cb, n_views, grad_rec,
+                                       grad_planes, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "project_backward");
+    return QUEEN_OK;
+}
+
 queen_status queen_densify(queen_ctx* ctx, const queen_gaussians* src, const uint32_t* rem_idx, int32_t n_rem,
                            const uint16_t* add_attrs, int32_t n_add, queen_gaussians* dst, void* stream) {
     if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");

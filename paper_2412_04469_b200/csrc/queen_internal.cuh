@@ -261,6 +261,11 @@ cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges
 cudaError_t launch_select(const uint32_t* idx, int k, const int32_t* k_dev, int n, int n_pad, uint8_t* select,
                           DevFlags* fl, cudaStream_t s);
 cudaError_t launch_dilate(uint8_t* marks, uint8_t* tmp, int n_views, int W, int H, int d, cudaStream_t s);
+cudaError_t launch_blend_bwd(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
+                             int W, int H, float bg0, float bg1, float bg2, const float* gout, float* grec,
+                             cudaStream_t s);
+cudaError_t launch_project_bwd(const float* planes, int n, int n_pad, int deg, const CamBatch& cams, int n_views,
+                               const float* grec, float* gpl, cudaStream_t s);
 cudaError_t launch_densify(const float* src, int n_old, int np_src, const uint32_t* rem, int n_rem, const void* add,
                            int n_add, int P, float* dst, int np_dst, DevFlags* fl, cudaStream_t s);
 cudaError_t launch_blend_counts(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
