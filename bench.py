@@ -275,7 +275,7 @@ def main():
 
     import paper_2412_04469_b200 as Q
     from paper_2412_04469_b200 import packet as wire
-    from paper_2412_04469_b200.runtime import EntropyPacket, Player, wire_packet
+    from paper_2412_04469_b200.runtime import EntropyPacket, Player, device_packet, wire_packet
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -554,6 +554,46 @@ def main():
                            "read + written, additions (binary16) read, tail written"}
         del srcb, dstb
 
+    # ---- NEXT #4: backward pass of the frame (image gradient -> records -> raw attributes ->
+    # decoders / straight-through latents / gates), all views of the first batch
+    backward = None
+    if rank == 0 and world == 1 and not args.no_paper_style:
+        from paper_2412_04469_b200 import (queen_decode_backward, queen_project_backward,
+                                           queen_rasterize_backward)
+        bc = batches[0]
+        stg = Stages(player.planes.cpu().numpy(), sc.n, sc.deg, bc, keys_cap=player.keys_cap, device=local)
+        stg.project().bin_sort()
+        gimg = torch.randn((len(bc), 3, H, W), dtype=torch.float32, device=dev)
+        grec = torch.empty((len(bc), stg.n_pad, 9), dtype=torch.float32, device=dev)
+        gpl = torch.empty((sc.planes.shape[0], stg.n_pad), dtype=torch.float32, device=dev)
+        pk_tr = device_packet(host_pkts[0], dev, gates=True, f32_latents=True)
+        gdec = torch.empty(host_pkts[0].decoders.size, dtype=torch.float32, device=dev)
+        glat = torch.empty((sum(host_pkts[0].lat), stg.n_pad), dtype=torch.float32, device=dev)
+        gla = torch.empty(stg.n_pad, dtype=torch.float32, device=dev)
+        gpre = torch.empty((3, stg.n_pad), dtype=torch.float32, device=dev)
+
+        def bwd():
+            queen_rasterize_backward(stg.ctx, stg.proj, stg.bins, bc, gimg, grec)
+            e1.record(stream)
+            queen_project_backward(stg.ctx, stg.scene, bc, grec, gpl)
+            e2.record(stream)
+            queen_decode_backward(stg.ctx, pk_tr.struct, gpl, gdec, glat, gla, gpre)
+
+        e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+        bwd()
+        torch.cuda.synchronize()
+        flush.zero_()
+        e0.record(stream)
+        bwd()
+        e3.record(stream)
+        torch.cuda.synchronize()
+        backward = {"ms": e0.elapsed_time(e3), "rasterize_backward_ms": e0.elapsed_time(e1),
+                    "project_backward_ms": e1.elapsed_time(e2), "decode_backward_ms": e2.elapsed_time(e3),
+                    "views": len(bc), "status": Q.STATUS.get(stg.ctx.check_status()[0]),
+                    "note": "random image gradient -> dL/d(records) -> dL/d(raw attributes) -> dL/d(decoders, "
+                            "straight-through latents, gates); L2 flushed; forward binning not included"}
+        del stg, gimg, grec, gpl
+
     # ---- end to end through the public API with host buffers (pinned H2D packet, D2H images)
     def run_e2e(rgb8: bool):
         # Streaming player through the public API: per frame a pinned H2D of the wire packet
@@ -657,7 +697,7 @@ def main():
             "mpixel_per_s": mpix, "view_fps": value * V,
             "status": Q.STATUS.get(st, st),
             "keys_per_batch": K_list, "visible_pairs_per_batch": M_list, "stages": stages, "roofline": roof,
-            "path_roofline": path, "paper_style": paper, "library_sort": libsort, "masked_render": masked, "densify": densify,
+            "path_roofline": path, "paper_style": paper, "library_sort": libsort, "masked_render": masked, "densify": densify, "backward": backward,
             "e2e_f32": e2e_f32, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
         }

@@ -253,6 +253,19 @@ queen_status queen_rasterize_backward(queen_ctx* ctx, const queen_proj* proj, co
                                       float* grad_rec, void* stream);
 queen_status queen_project_backward(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
                                     int32_t n_views, const float* grad_rec, float* grad_planes, void* stream);
+/* queen_decode_backward: the encode side of Eq. 4-5 and the gates.  grad_planes =
+ *   dL/dA_t [11+3B][n_pad] (e.g. from queen_project_backward); outputs (each nullable, device fp32,
+ *   overwritten):
+ *   grad_decoders [ndec] (the packet's concatenated D_c layout): sum_i dL/dA[row][i] l[k][i],
+ *     summed in a fixed order (deterministic);
+ *   grad_latents [sum L][n_pad]: straight-through round: D_c^T dL/dr_c;
+ *   grad_log_alpha [n_pad], grad_pregate [3][n_pad] (pos_kind GATES; zeros otherwise): on the
+ *     forward's mask, dL/dl_p = g dL/dp and dL/dlog alpha = (l_p . dL/dp) dg/dlog alpha, 0 where
+ *     g is clamped to 0 or 1 (deterministic gate, R#6).
+ *   Uses the workspace's sort scratch for the decoder partial sums. */
+queen_status queen_decode_backward(queen_ctx* ctx, const queen_packet* pkt, const float* grad_planes,
+                                   float* grad_decoders, float* grad_latents, float* grad_log_alpha, float* grad_pregate,
+                                   void* stream);
 
 /* ---- NEXT #2: densification deltas (DESIGN reading R21) --------------------
  * queen_densify: dst = src without the Gaussians rem_idx (surviving columns keep their order)

@@ -199,3 +199,59 @@ def project_grad(planes: np.ndarray, n: int, deg: int, cams, proj, G_rec: np.nda
             L = L + (outs[j] * G[:, j]).sum()
     L.backward()
     return pt.grad[:, :n].numpy()
+
+
+# ----------------------------------------------------------------------------- decode / gates
+def decode_forward64(pkt, lhat_t, dec_t, la_t, pre_t, planes0: np.ndarray, use_gates: bool = True):
+    """A_t = A_{t-1} + R_t in float64 (Eq. 4-5; gates P:319-338): attribute rows get
+    D_c round(l_hat_c) with the straight-through estimator (round acts as the identity in the
+    backward pass, "straight-through estimator"), positions get g * l_p on the
+    gate's mask (log alpha > theta0, decided in fp32 as the forward does); g's clamp to [0, 1]
+    is held at the forward's decision.  Returns the float64 planes [P][n]."""
+    from oracle import theta0
+    n, deg = pkt.n, pkt.deg
+    B = (deg + 1) ** 2
+    M = (4, 3, 1, 3, 3 * (B - 1))  # rot, scale, opacity, SH-DC, SH-rest rows (R2, R3)
+    lat = pkt.lat
+    rows = []
+    r0 = 0
+    d0 = 0
+    l_st = lhat_t + (torch.round(lhat_t) - lhat_t).detach()  # STE
+    for c in range(5):
+        L = lat[c]
+        Mc = M[c]
+        if L == 0:
+            rows.append(torch.zeros((Mc, n), dtype=torch.float64))
+            continue
+        D = dec_t[d0:d0 + Mc * L].reshape(Mc, L)
+        rows.append(D @ l_st[r0:r0 + L, :n])
+        r0 += L
+        d0 += Mc * L
+    R = torch.cat(rows, 0)
+    A0 = torch.from_numpy(planes0[:, :n].astype(np.float64))
+    pos = A0[0:3]
+    if use_gates:
+        tau, g0, g1 = pkt.gate
+        th0 = float(theta0(*pkt.gate))
+        mask = torch.from_numpy(pkt.log_alpha[:n].astype(np.float32) > np.float32(th0))
+        gt = torch.sigmoid(la_t[:n] / tau) * (g1 - g0) + g0
+        clamp_lo = (gt.detach() <= 0)
+        clamp_hi = (gt.detach() >= 1)
+        g = torch.where(clamp_hi, torch.ones_like(gt), torch.where(clamp_lo, torch.zeros_like(gt), gt))
+        g = torch.where(mask, g, torch.zeros_like(g))
+        pos = pos + g[None, :] * pre_t[:, :n]
+    return torch.cat([pos, A0[3:] + R], 0)
+
+
+def decode_grad(pkt, planes0: np.ndarray, gA: np.ndarray, use_gates: bool = True):
+    """dL/d(decoders [ndec], l_hat [sum L][n], log_alpha [n], pregate [3][n]) for
+    L = sum(gA * A_t), float64 autograd of decode_forward64."""
+    n = pkt.n
+    lhat = torch.from_numpy(np.ascontiguousarray(pkt.latents_f32[:, :n], np.float64)).requires_grad_(True)
+    dec = torch.from_numpy(np.asarray(pkt.decoders, np.float64)).requires_grad_(True)
+    la = torch.from_numpy(np.asarray(pkt.log_alpha[:n], np.float64)).requires_grad_(True)
+    pre = torch.from_numpy(np.ascontiguousarray(pkt.pos_pregate[:, :n], np.float64)).requires_grad_(True)
+    A = decode_forward64(pkt, lhat, dec, la, pre, planes0, use_gates)
+    (A * torch.from_numpy(gA[:, :n].astype(np.float64))).sum().backward()
+    z = lambda t: t.grad.numpy() if t.grad is not None else np.zeros(t.shape)  # noqa: E731
+    return z(dec), z(lhat), z(la), z(pre)

@@ -31,7 +31,7 @@ EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version",
            "queen_profile_enable", "queen_profile_read", "queen_wait_binned", "queen_entropy_encode",
            "queen_entropy_decode", "queen_entropy_decode_frame", "queen_render_mask",
            "queen_densify", "queen_rasterize_rgb8", "queen_render_views_rgb8",
-           "queen_rasterize_backward", "queen_project_backward"]
+           "queen_rasterize_backward", "queen_project_backward", "queen_decode_backward"]
 STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy"]
 
 
@@ -104,6 +104,7 @@ def lib() -> C.CDLL:
             "queen_blend_counts": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
                                          p, p, p]),
             "queen_profile_enable": (i32, [p, i32]),
+            "queen_decode_backward": (i32, [p, C.POINTER(QueenPacket), p, p, p, p, p, p]),
             "queen_rasterize_backward": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera),
                                                i32, C.POINTER(C.c_float), p, p, p]),
             "queen_project_backward": (i32, [p, C.POINTER(QueenGaussians), C.POINTER(QueenCamera), i32, p, p, p]),
@@ -367,6 +368,15 @@ def queen_project_backward(ctx: Context, scene: QueenGaussians, cams, grad_rec, 
     st = lib().queen_project_backward(ctx.handle, C.byref(scene), arr, len(arr), _ptr(grad_rec), _ptr(grad_planes),
                                       C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_project_backward")
+
+
+def queen_decode_backward(ctx: Context, pkt: QueenPacket, grad_planes, grad_decoders=None, grad_latents=None,
+                          grad_log_alpha=None, grad_pregate=None, stream=None):
+    """NEXT #4: decoder / straight-through latent / gate gradients from dL/dA_t (queen.h)."""
+    st = lib().queen_decode_backward(ctx.handle, C.byref(pkt), _ptr(grad_planes), _ptr(grad_decoders),
+                                     _ptr(grad_latents), _ptr(grad_log_alpha), _ptr(grad_pregate),
+                                     C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_decode_backward")
 
 
 def queen_entropy_encode(latents: np.ndarray, n: int) -> np.ndarray:

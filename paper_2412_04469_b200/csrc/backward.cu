@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
     const int px = (t % gx) * 16 + (threadIdx.x & 15);
     const int py0 = (t / gx) * 16 + (threadIdx.x >> 4) * BW_RPT;
     const float fx = (float)px;
+    const float wx0 = (float)((t % gx) * 16), wy0 = (float)((t / gx) * 16 + (threadIdx.x >> 5) * 8);
     const uint2 rg = ranges[gt];
     const int rs = (int)rg.x, re = (int)rg.y;
     const float4* vrec = rec + (int64_t)v * n_pad * 3;
@@ -118,7 +119,18 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
             sI[q] = gi;
         }
         __syncthreads();
-        for (int q = cnt - 1; q >= 0; --q) {
+        // this warp's records of the batch: those whose alpha >= 1/255 ellipse can reach its 16 x 8
+        // sub-tile (touches(), lane q tests record q; the others have no hit in the warp)
+        unsigned long long wmask = 0ull;
+#pragma unroll
+        for (int e2 = 0; e2 < BW_BATCH / 32; ++e2) {
+            const int q = (int)(threadIdx.x & 31) + 32 * e2;
+            const bool want = q < cnt && touches(sA[q], sB[q], wx0, wx0 + 15.0f, wy0, wy0 + 7.0f);
+            wmask |= (unsigned long long)__ballot_sync(0xffffffffu, want) << (32 * e2);
+        }
+        while (wmask) {
+            const int q = 63 - __clzll((long long)wmask);  // descending order
+            wmask &= ~(1ull << q);
             const int j = b0 + q;
             const float4 a = sA[q], bq = sB[q], c = sC[q];
             const float dx = a.x - fx;
@@ -135,39 +147,77 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
                 const float e = ex2b(p2);
                 const float raw = c.x * e;
                 const float alpha = fminf(0.99f, raw);
-                const float om = 1.0f - alpha;
-                const float Ti = Tc[r] / om;
+                const float iom = __fdividef(1.0f, 1.0f - alpha);  // 1 - alpha >= 0.01
+                const float Ti = Tc[r] * iom;
                 const float w = alpha * Ti;
                 const float col[3] = {c.y, c.z, c.w};
                 float dal = 0.f;
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
-                    acc[6 + ch] += w * g[r][ch];
-                    dal += g[r][ch] * (col[ch] * Ti - (S[r][ch] + Tf[r] * bgc[ch]) / om);
-                    S[r][ch] += col[ch] * w;
+                    acc[6 + ch] = fmaf(w, g[r][ch], acc[6 + ch]);
+                    dal = fmaf(g[r][ch], fmaf(col[ch], Ti, -(S[r][ch] + Tf[r] * bgc[ch]) * iom), dal);
+                    S[r][ch] = fmaf(col[ch], w, S[r][ch]);
                 }
                 Tc[r] = Ti;
                 if (raw <= 0.99f) {  // unclamped: a = o 2^p2
-                    acc[5] += dal * e;
+                    acc[5] = fmaf(dal, e, acc[5]);
                     const float dp2 = dal * alpha * LN2;
-                    acc[0] += dp2 * (2.0f * bq.x * dx + bq.y * dy);
-                    acc[1] += dp2 * (bq.y * dx + 2.0f * bq.z * dy);
-                    acc[2] += dp2 * dx * dx;
-                    acc[3] += dp2 * dx * dy;
-                    acc[4] += dp2 * dy * dy;
+                    // moments of dp2; (u, v, A2, B2, C2) gradients are formed from them per record
+                    acc[0] += dp2;            // sum dp2          (x dx: dx is this lane's constant)
+                    acc[1] += dp2 * dy;       // sum dp2 dy
+                    acc[2] += dp2 * dy * dy;  // sum dp2 dy^2
                 }
             }
-            if (__any_sync(0xffffffffu, any)) {
+            if (!__any_sync(0xffffffffu, any)) continue;
+            {  // per lane: u, v, A2, B2, C2 from the moments (dx constant over the lane's rows)
+                const float s0 = acc[0], s1 = acc[1], s2 = acc[2];
+                acc[0] = 2.0f * bq.x * dx * s0 + bq.y * s1;  // d/du = sum dp2 (2 A2 dx + B2 dy)
+                acc[1] = bq.y * dx * s0 + 2.0f * bq.z * s1;  // d/dv = sum dp2 (B2 dx + 2 C2 dy)
+                acc[2] = dx * dx * s0;                        // d/dA2
+                acc[3] = dx * s1;                             // d/dB2
+                acc[4] = s2;                                  // d/dC2
+            }
+            // warp reduce-scatter of the 9 (padded to 16) sums: 8 + 4 + 2 + 1 + 1 shuffles; lane l
+            // ends with the total of value l >> 1, and lanes 0, 2, .., 16 add them (one atomic each)
+            float v8[8];
+            const uint32_t lane = threadIdx.x & 31;
+            {
+                const bool b = (lane >> 4) & 1;
 #pragma unroll
-                for (int k = 0; k < 9; ++k)
-                    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-                if ((threadIdx.x & 31) == 0) {
-                    float* gr = grec + ((int64_t)v * n_pad + sI[q]) * 9;
-#pragma unroll
-                    for (int k = 0; k < 9; ++k)
-                        if (acc[k] != 0.f) atomicAdd(gr + k, acc[k]);
+                for (int k = 0; k < 8; ++k) {
+                    const float lo = acc[k], hi = k + 8 < 9 ? acc[k + 8] : 0.f;
+                    const float send = b ? lo : hi, keep = b ? hi : lo;
+                    v8[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
                 }
             }
+            float v4[4];
+            {
+                const bool b = (lane >> 3) & 1;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float send = b ? v8[k] : v8[k + 4], keep = b ? v8[k + 4] : v8[k];
+                    v4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                }
+            }
+            float v2[2];
+            {
+                const bool b = (lane >> 2) & 1;
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    const float send = b ? v4[k] : v4[k + 2], keep = b ? v4[k + 2] : v4[k];
+                    v2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+                }
+            }
+            float v1;
+            {
+                const bool b = (lane >> 1) & 1;
+                const float send = b ? v2[0] : v2[1], keep = b ? v2[1] : v2[0];
+                v1 = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+            }
+            v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+            const int idx = (int)(lane >> 1);  // = 8 b4 + 4 b3 + 2 b2 + b1
+            if ((lane & 1) == 0 && idx < 9 && v1 != 0.f)
+                atomicAdd(grec + ((int64_t)v * n_pad + sI[q]) * 9 + idx, v1);
         }
     }
 }
@@ -405,6 +455,173 @@ cudaError_t launch_project_bwd(const float* planes, int n, int n_pad, int deg, c
         case 1: k_project_bwd<1><<<blocks, 128, 0, s>>>(planes, n, n_pad, cams, n_views, grec, gpl); break;
         case 2: k_project_bwd<2><<<blocks, 128, 0, s>>>(planes, n, n_pad, cams, n_views, grec, gpl); break;
         default: k_project_bwd<3><<<blocks, 128, 0, s>>>(planes, n, n_pad, cams, n_views, grec, gpl); break;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace queen
+
+// ---------------------------------------------------------------------------
+// decode backward (the encode side of Eq. 4-5 and the gates): given dL/dA_t,
+//   dL/dD_c[m][k] = sum_i dL/dA[row(c,m)][i] round(l)_c[k][i]        (k_dec_grad_partial/_sum,
+//                                                                     deterministic 2-stage sum)
+//   dL/dl_hat_c[k][i] = sum_m D_c[m][k] dL/dA[row(c,m)][i]            (straight-through round)
+//   dL/dl_p,i = g_i dL/dp_i ;  dL/dlog alpha_i = (l_p,i . dL/dp_i) dg/dlog alpha (k_gate_grad)
+namespace queen {
+
+struct DecBwdParams {
+    int n, n_pad;
+    int lat[5], M[5], lat_row0[5], dec_off[5], out_row0[5];
+    int ndec, chunks, f32;
+    const void* latents;
+    const float* decoders;
+    const float* gA;
+};
+
+__device__ __forceinline__ float latent_value(const DecBwdParams& p, int row, int i) {
+    if (p.f32) return roundf(static_cast<const float*>(p.latents)[(int64_t)row * p.n_pad + i]);
+    return (float)static_cast<const int8_t*>(p.latents)[(int64_t)row * p.n_pad + i];
+}
+
+// block (r, chunk): attribute row r = out_row0[c] + m; partial sums over the chunk's Gaussians
+__global__ void __launch_bounds__(256) k_dec_grad_partial(DecBwdParams p, float* __restrict__ part) {
+    __shared__ float s_w[8][16];
+    const int r = blockIdx.x, chunk = blockIdx.y;
+    int c = 0;
+    while (c < 4 && r >= p.out_row0[c] + p.M[c]) ++c;
+    const int m = r - p.out_row0[c];
+    const int L = p.lat[c];
+    if (L == 0) return;
+    const int64_t per = ((int64_t)p.n + p.chunks - 1) / p.chunks;
+    const int i0 = (int)(chunk * per), i1 = (int)min((int64_t)p.n, (chunk + 1) * per);
+    float acc[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = 0.f;
+    const float* g = p.gA + (int64_t)(3 + r) * p.n_pad;
+    for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+        const float gi = g[i];
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k < L) acc[k] = fmaf(gi, latent_value(p, p.lat_row0[c] + k, i), acc[k]);
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        if (k >= L) break;
+        float x = acc[k];
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) s_w[w][k] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < L) {
+        float x = 0.f;
+        for (int q = 0; q < 8; ++q) x += s_w[q][threadIdx.x];
+        part[(int64_t)chunk * p.ndec + p.dec_off[c] + m * L + threadIdx.x] = x;
+    }
+}
+
+__global__ void k_dec_grad_sum(const float* __restrict__ part, int ndec, int chunks, float* __restrict__ gdec) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= ndec) return;
+    float x = 0.f;
+    for (int q = 0; q < chunks; ++q) x += part[(int64_t)q * ndec + j];
+    gdec[j] = x;
+}
+
+__global__ void __launch_bounds__(256) k_lat_grad(DecBwdParams p, float* __restrict__ glat) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n_pad) return;
+    for (int c = 0; c < 5; ++c) {
+        const int L = p.lat[c];
+        if (L == 0) continue;
+        float acc[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = 0.f;
+        if (i < p.n) {
+            for (int m = 0; m < p.M[c]; ++m) {
+                const float gi = p.gA[(int64_t)(3 + p.out_row0[c] + m) * p.n_pad + i];
+                const float* d = p.decoders + p.dec_off[c] + m * L;
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    if (k < L) acc[k] = fmaf(__ldg(d + k), gi, acc[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k < L) glat[(int64_t)(p.lat_row0[c] + k) * p.n_pad + i] = acc[k];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_gate_grad(const float* __restrict__ gA, const float* __restrict__ la,
+                                                   const float* __restrict__ pre, int n, int n_pad, float tau, float g0,
+                                                   float g1, float theta0, float* __restrict__ gla,
+                                                   float* __restrict__ gpre) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_pad) return;
+    float dla = 0.f, dpre[3] = {0.f, 0.f, 0.f};
+    if (i < n && la[i] > theta0) {  // the forward's mask (R#6)
+        const float ghat = 1.0f / (1.0f + det_exp((-la[i]) / tau));
+        const float gt = fmaf(ghat, g1 - g0, g0);
+        const float g = fminf(1.0f, fmaxf(0.0f, gt));
+        float dg = 0.f;
+        for (int d = 0; d < 3; ++d) {
+            const float gp = gA[(int64_t)d * n_pad + i];
+            dpre[d] = g * gp;
+            dg = fmaf(pre[(int64_t)d * n_pad + i], gp, dg);
+        }
+        if (gt > 0.0f && gt < 1.0f) dla = dg * (g1 - g0) * ghat * (1.0f - ghat) / tau;
+    }
+    if (gla) gla[i] = dla;
+    if (gpre)
+        for (int d = 0; d < 3; ++d) gpre[(int64_t)d * n_pad + i] = dpre[d];
+}
+
+float host_theta0(float tau, float g0, float g1);
+
+cudaError_t launch_decode_bwd(const queen_packet& pk, const float* gA, float* gdec, float* glat, float* gla, float* gpre,
+                              float* scratch, size_t scratch_floats, cudaStream_t s) {
+    DecBwdParams p{};
+    const int B = (pk.sh_degree + 1) * (pk.sh_degree + 1);
+    const int Mc[5] = {4, 3, 1, 3, 3 * (B - 1)};
+    int lr = 0, dof = 0, orow = 0;
+    for (int c = 0; c < 5; ++c) {
+        p.lat[c] = pk.lat_dim[c];
+        p.M[c] = Mc[c];
+        p.lat_row0[c] = lr;
+        p.dec_off[c] = dof;
+        p.out_row0[c] = orow;
+        lr += pk.lat_dim[c];
+        dof += Mc[c] * pk.lat_dim[c];
+        orow += Mc[c];
+    }
+    p.ndec = dof;
+    p.n = pk.n;
+    p.n_pad = pk.n_pad;
+    p.f32 = pk.latent_kind == QUEEN_LAT_F32;
+    p.latents = pk.latents;
+    p.decoders = pk.decoders;
+    p.gA = gA;
+    cudaError_t e;
+    if (gdec && p.ndec > 0) {
+        int chunks = (pk.n + 8191) / 8192;
+        chunks = chunks < 1 ? 1 : (chunks > 64 ? 64 : chunks);
+        while (chunks > 1 && (size_t)chunks * p.ndec > scratch_floats) --chunks;
+        if ((size_t)chunks * p.ndec > scratch_floats) return cudaErrorInvalidValue;
+        p.chunks = chunks;
+        if ((e = cudaMemsetAsync(scratch, 0, sizeof(float) * chunks * p.ndec, s))) return e;
+        k_dec_grad_partial<<<dim3((unsigned)orow, (unsigned)chunks), 256, 0, s>>>(p, scratch);
+        k_dec_grad_sum<<<(p.ndec + 255) / 256, 256, 0, s>>>(scratch, p.ndec, chunks, gdec);
+    }
+    if (glat) k_lat_grad<<<(pk.n_pad + 255) / 256, 256, 0, s>>>(p, glat);
+    if (gla || gpre) {
+        if (pk.pos_kind == QUEEN_POS_GATES) {
+            k_gate_grad<<<(pk.n_pad + 255) / 256, 256, 0, s>>>(gA, pk.log_alpha, pk.pos_pregate, pk.n, pk.n_pad, pk.tau,
+                                                              pk.gamma0, pk.gamma1, host_theta0(pk.tau, pk.gamma0, pk.gamma1),
+                                                              gla, gpre);
+        } else {
+            if (gla && (e = cudaMemsetAsync(gla, 0, sizeof(float) * pk.n_pad, s))) return e;
+            if (gpre && (e = cudaMemsetAsync(gpre, 0, sizeof(float) * 3 * (size_t)pk.n_pad, s))) return e;
+        }
     }
     return cudaGetLastError();
 }

@@ -450,6 +450,23 @@ queen_status queen_project_backward(queen_ctx* ctx, const queen_gaussians* scene
     return QUEEN_OK;
 }
 
+queen_status queen_decode_backward(queen_ctx* ctx, const queen_packet* pkt, const float* grad_planes,
+                                   float* grad_decoders, float* grad_latents, float* grad_log_alpha, float* grad_pregate,
+                                   void* stream) {
+    if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
+    if (queen_status st = check_packet(ctx, pkt)) return st;
+    if (!grad_planes) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null grad_planes");
+    if ((grad_log_alpha || grad_pregate) && pkt->pos_kind == QUEEN_POS_GATES && (!pkt->log_alpha || !pkt->pos_pregate))
+        return fail(ctx, QUEEN_ERR_INVALID_ARG, "gate gradients need log_alpha and pos_pregate");
+    float* scratch = reinterpret_cast<float*>(static_cast<unsigned char*>(ctx->ws) + ctx->L.dkeys);
+    const size_t sfloats = (ctx->L.counts - ctx->L.dkeys) / sizeof(float);
+    cudaError_t e = launch_decode_bwd(*pkt, grad_planes, grad_decoders, grad_latents, grad_log_alpha, grad_pregate,
+                                      scratch, sfloats, static_cast<cudaStream_t>(stream));
+    if (e == cudaErrorInvalidValue) return fail(ctx, QUEEN_ERR_SHAPE, "workspace too small for the decoder gradient");
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "decode_backward");
+    return QUEEN_OK;
+}
+
 queen_status queen_densify(queen_ctx* ctx, const queen_gaussians* src, const uint32_t* rem_idx, int32_t n_rem,
                            const uint16_t* add_attrs, int32_t n_add, queen_gaussians* dst, void* stream) {
     if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");

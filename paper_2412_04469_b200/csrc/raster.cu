@@ -67,33 +67,6 @@ __device__ __forceinline__ void composite2(Px2& p, float q0, float q1, bool h0, 
     p.T = __fmul2_rn(p.T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
 }
 
-// Can the record's alpha >= 1/255 region {p2 >= T2} reach a pixel centre of [x0,x1] x [y0,y1]?
-// Conservative (false positives only cost time): p2 is a concave quadratic in (x, y), so its
-// maximum over the rectangle is 0 if the centre (u, v) lies inside, else it sits on an edge,
-// at the edge's 1D maximiser clamped to the edge.  The maximum is compared with T2 minus a
-// slack of 1e-5 of the quadratic's magnitude over the bounding box (>> the few-ulp rounding
-// of either evaluation).  Approximate division only moves the maximiser slightly, which
-// lowers the edge value by a second-order amount (covered by the slack).
-__device__ __forceinline__ bool touches(const float4& a, const float4& q, float x0, float x1, float y0, float y1) {
-    if (a.x + a.z < x0 || a.x - a.z > x1 || a.y + a.w < y0 || a.y - a.w > y1) return false;
-    if (a.x >= x0 && a.x <= x1 && a.y >= y0 && a.y <= y1) return true;
-    const float A = q.x, B = q.y, C = q.z;
-    const float iA = __fdividef(-0.5f * B, A), iC = __fdividef(-0.5f * B, C);
-    const float dxl = a.x - x1, dxh = a.x - x0, dyl = a.y - y1, dyh = a.y - y0;
-    float best = -INFINITY;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const float dy = e ? dyl : dyh;  // edge y = y0 (dy = v - y0) or y = y1
-        const float dx = fminf(fmaxf(iA * dy, dxl), dxh);
-        best = fmaxf(best, fmaf(A * dx, dx, fmaf(C * dy, dy, B * dx * dy)));
-        const float ex = e ? dxl : dxh;  // edge x = x0 or x = x1
-        const float ey = fminf(fmaxf(iC * ex, dyl), dyh);
-        best = fmaxf(best, fmaf(A * ex, ex, fmaf(C * ey, ey, B * ex * ey)));
-    }
-    const float S = fabsf(A) * a.z * a.z + fabsf(B) * a.z * a.w + fabsf(C) * a.w * a.w;
-    return best >= q.w - (1e-5f * S + 1e-6f);
-}
-
 template <bool COUNT, int RPT, bool WMASK>
 __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ rec, int n_pad, const uint2* __restrict__ ranges,
                                                     const uint32_t* __restrict__ vals, int W, int H, int gx, int T, float bg0,

@@ -121,3 +121,33 @@ def test_full_backward_chain_matches_oracle():
     ref_rec = G.blend_grad(proj["rec"], contrib, W, H, (0, 0, 0), gout.astype(np.float64))
     ref = G.project_grad(sc.planes, sc.n, sc.deg, cams, proj, ref_rec)
     _close(gpl.cpu().numpy()[:, :sc.n].T, ref.T, tol=3e-3)
+
+
+@pytest.mark.parametrize("f32", [True, False])
+def test_decode_backward_matches_oracle(f32):
+    """Decoder / straight-through latent / gate gradients vs the float64 oracle (decode_grad)."""
+    import paper_2412_04469_b200 as Q
+    from paper_2412_04469_b200.runtime import device_packet
+    cfg = synth.get_config("n3dv")
+    sc = synth.make_scene(cfg, n=30001)
+    pkt = synth.make_packet(sc, 2)
+    rng = np.random.default_rng(5)
+    gA = rng.standard_normal(sc.planes.shape).astype(np.float32)
+    gA[:, sc.n:] = 0
+    ctx = Q.Context(0)
+    ctx.set_workspace(sc.n_pad, 1, 16, 16, 1024)
+    dp = device_packet(pkt, "cuda", gates=True, f32_latents=f32)
+    ndec = pkt.decoders.size
+    gdec = torch.empty(ndec, dtype=torch.float32, device="cuda")
+    glat = torch.empty((sum(pkt.lat), sc.n_pad), dtype=torch.float32, device="cuda")
+    gla = torch.empty(sc.n_pad, dtype=torch.float32, device="cuda")
+    gpre = torch.empty((3, sc.n_pad), dtype=torch.float32, device="cuda")
+    Q.queen_decode_backward(ctx, dp.struct, torch.from_numpy(gA).cuda(), gdec, glat, gla, gpre)
+    assert ctx.check_status()[0] == 0
+    rdec, rlat, rla, rpre = G.decode_grad(pkt, sc.planes, gA.astype(np.float64))
+    n = sc.n
+    assert np.abs(gdec.cpu().numpy() - rdec).max() <= 1e-4 * np.abs(rdec).max()
+    assert np.abs(glat.cpu().numpy()[:, :n] - rlat).max() <= 1e-5 * np.abs(rlat).max()
+    assert np.abs(gla.cpu().numpy()[:n] - rla).max() <= 1e-5 * max(np.abs(rla).max(), 1e-12)
+    assert np.abs(gpre.cpu().numpy()[:, :n] - rpre).max() <= 1e-5 * np.abs(rpre).max()
+    assert np.count_nonzero(rla) > 100

@@ -114,3 +114,39 @@ def test_project_grad_matches_finite_differences():
             b[r, i] -= h
             fd = (L(a) - L(b)) / (2 * h)
             assert abs(fd - g[r, i]) <= 2e-5 * max(1.0, abs(fd)), (i, r, fd, g[r, i])
+
+
+def test_decode_grad_finite_differences_and_ste():
+    """Decoder and gate gradients equal central differences of the float64 decode; latent
+    gradients are the straight-through ones, D_c^T dL/dr_c."""
+    cfg = synth.get_config("tiny", deg=1)
+    sc = synth.make_scene(cfg, n=200)
+    pkt = synth.make_packet(sc, 1)
+    rng = np.random.default_rng(2)
+    gA = rng.standard_normal(sc.planes.shape)
+    gdec, glat, gla, gpre = G.decode_grad(pkt, sc.planes, gA)
+
+    def L(dec=None, la=None, pre=None):
+        t = lambda a: torch.from_numpy(np.asarray(a, np.float64))  # noqa: E731
+        A = G.decode_forward64(pkt, t(pkt.latents_f32[:, :sc.n]), t(pkt.decoders if dec is None else dec),
+                               t(pkt.log_alpha[:sc.n] if la is None else la),
+                               t(pkt.pos_pregate[:, :sc.n] if pre is None else pre), sc.planes)
+        return float((A.numpy() * gA[:, :sc.n]).sum())
+
+    h = 1e-6
+    for j in rng.choice(pkt.decoders.size, 5, replace=False):
+        a, b = pkt.decoders.astype(np.float64), pkt.decoders.astype(np.float64)
+        a[j] += h
+        b[j] -= h
+        assert abs((L(dec=a) - L(dec=b)) / (2 * h) - gdec[j]) < 1e-6 * max(1, abs(gdec[j]))
+    on = np.nonzero(np.abs(gla) > 0)[0]
+    assert on.size > 3
+    for i in on[:5]:
+        a, b = pkt.log_alpha[:sc.n].astype(np.float64), pkt.log_alpha[:sc.n].astype(np.float64)
+        a[i] += h
+        b[i] -= h
+        assert abs((L(la=a) - L(la=b)) / (2 * h) - gla[i]) < 1e-5 * max(1, abs(gla[i]))
+    # STE: dL/dl_hat for category 0 (rotation, rows 3-6) = D_0^T gA[3:7]
+    L0, M0 = pkt.lat[0], 4
+    D0 = pkt.decoders[:M0 * L0].reshape(M0, L0).astype(np.float64)
+    assert np.allclose(glat[:L0], D0.T @ gA[3:7, :sc.n], rtol=1e-12, atol=1e-12)
