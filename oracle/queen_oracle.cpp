@@ -469,8 +469,9 @@ int64_t oracle_bin(int n_pad, int V, int W, int H, const uint32_t* tiles, const 
 // ---------------------------------------------------------------------------
 // record words: 0 u, 1 v, 4 A2, 5 B2, 6 C2, 7 T2, 8 o, 9-11 rgb (hx, hy unused here)
 static inline float rec_p2(const float* rc, float fx, float fy) {
+    // Horner in dy (DESIGN "Arithmetic contract"): p2 = (C2 dy + B2 dx) dy + (A2 dx) dx
     float dx = rc[0] - fx, dy = rc[1] - fy;
-    return std::fma(rc[4] * dx, dx, std::fma(rc[6] * dy, dy, (rc[5] * dx) * dy));
+    return std::fma(std::fma(rc[6], dy, rc[5] * dx), dy, (rc[4] * dx) * dx);
 }
 
 static inline bool blend_step(const float* rc, float fx, float fy, float C[3], float& T) {

@@ -71,12 +71,12 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
         for (int q = 0; q < cnt; ++q) {
             const float4 a = sA[q], bq = sB[q];
             const float dx = a.x - fx;
-            const float tA = bq.x * dx, tB = bq.y * dx;
+            const float tAdx = (bq.x * dx) * dx, tB = bq.y * dx;
 #pragma unroll
             for (int r = 0; r < BW_RPT; ++r) {
                 if (Tf[r] < 1e-4f) continue;
                 const float dy = a.y - (float)(py0 + r);
-                const float p2 = fmaf(tA, dx, fmaf(bq.z * dy, dy, tB * dy));
+                const float p2 = fmaf(fmaf(bq.z, dy, tB), dy, tAdx);
                 if (p2 > 0.0f || p2 < bq.w) continue;
                 const float alpha = fminf(0.99f, sC[q].x * ex2b(p2));
                 Tf[r] = Tf[r] * (1.0f - alpha);
@@ -134,14 +134,14 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
             const int j = b0 + q;
             const float4 a = sA[q], bq = sB[q], c = sC[q];
             const float dx = a.x - fx;
-            const float tA = bq.x * dx, tB = bq.y * dx;
+            const float tAdx = (bq.x * dx) * dx, tB = bq.y * dx;
             float acc[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // u v A2 B2 C2 o r g b
             bool any = false;
 #pragma unroll
             for (int r = 0; r < BW_RPT; ++r) {
                 if (j > last[r]) continue;
                 const float dy = a.y - (float)(py0 + r);
-                const float p2 = fmaf(tA, dx, fmaf(bq.z * dy, dy, tB * dy));
+                const float p2 = fmaf(fmaf(bq.z, dy, tB), dy, tAdx);
                 if (p2 > 0.0f || p2 < bq.w) continue;
                 any = true;
                 const float e = ex2b(p2);

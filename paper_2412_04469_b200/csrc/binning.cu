@@ -712,7 +712,11 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
         if (p < total) {
             const uint32_t cc = p - s_off[e];
             const uint32_t wx = s_wx[e];
-            const uint32_t row = cc / wx;
+            // row = cc / wx by a float estimate + integer fix-ups (cc < 2^24: the estimate is
+            // within one of the quotient)
+            uint32_t row = __float2uint_rz(__uint2float_rn(cc) * __fdividef(1.0f, (float)wx));
+            if (row * wx > cc) --row;
+            if ((row + 1) * wx <= cc) ++row;
             const uint64_t dst = gbase + p;
             if (dst < cap) {
                 keys[dst] = s_base[e] + row * (uint32_t)gx + (cc - row * wx);

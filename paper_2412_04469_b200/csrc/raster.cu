@@ -18,7 +18,7 @@
 //    different rows issues one short straight-line block instead of four divergent ones
 //    (SASS: 62 instructions for a fully hit record, was ~100).
 // Per-pixel arithmetic is exactly the oracle's (oracle/queen_oracle.cpp blend_step):
-//   p2 = fma(A2 dx, dx, fma(C2 dy, dy, (B2 dx) dy));  skip if p2 > 0 or p2 < T2;
+//   p2 = fma(fma(C2, dy, B2 dx), dy, (A2 dx) dx);  skip if p2 > 0 or p2 < T2;
 //   a = min(0.99, o 2^p2); C = fma(rgb, a T, C); T = T (1 - a); stop after T < 1e-4.
 #include <cstdlib>
 
@@ -54,12 +54,18 @@ __device__ __forceinline__ bool hit(float T, float p2, float T2) { return !(T < 
 // Branch-free compositing of one record into a row pair: a row that does not hit gets
 // exponent -inf, i.e. alpha = min(0.99, o * 2^-inf) = +0, and then C = fma(c, +0, C) = C and
 // T = T (1 - 0) = T exactly -- bit-identical to skipping it.  c = (o, r, g, b).
+// CLAMP = false for records with o <= 0.98: there o 2^p2 <= 0.98 (1 + 2^-22) < 0.99 for every
+// p2 <= 0 (ex2.approx is within 2 ulp of 2^p2 <= 1), so min(0.99, .) is the identity and is
+// skipped -- bit-identical again.
+template <bool CLAMP>
 __device__ __forceinline__ void composite2(Px2& p, float q0, float q1, bool h0, bool h1, const float4& c) {
     const float NEG_INF = __int_as_float(0xff800000);
     const float e0 = ex2(h0 ? q0 : NEG_INF), e1 = ex2(h1 ? q1 : NEG_INF);
     float2 al = __fmul2_rn(make_float2(c.x, c.x), make_float2(e0, e1));
-    al.x = fminf(0.99f, al.x);
-    al.y = fminf(0.99f, al.y);
+    if (CLAMP) {
+        al.x = fminf(0.99f, al.x);
+        al.y = fminf(0.99f, al.y);
+    }
     const float2 aT = __fmul2_rn(al, p.T);
     p.r = __ffma2_rn(make_float2(c.y, c.y), aT, p.r);
     p.g = __ffma2_rn(make_float2(c.z, c.z), aT, p.g);
@@ -189,20 +195,19 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
                 // fyc +- hspan).  Skips never change a decision.
                 if (!COUNT && !WMASK && (fabsf(dx) > a.z || fabsf(a.y - fyc) > a.w + hspan)) continue;
                 const float4 bq = sB[s][q];  // A2, B2, C2, T2
-                const float tA = bq.x * dx;
+                const float tAdx = (bq.x * dx) * dx;
                 const float tB = bq.y * dx;
                 const float2 vv = make_float2(a.y, a.y);
                 const float2 cc = make_float2(bq.z, bq.z);
                 const float2 tb2 = make_float2(tB, tB);
-                const float2 ta2 = make_float2(tA, tA);
-                const float2 dx2 = make_float2(dx, dx);
+                const float2 ta2 = make_float2(tAdx, tAdx);
                 float2 qq[NP];
                 bool h[RPT];
                 bool anyh = false;
 #pragma unroll
                 for (int k = 0; k < NP; ++k) {
                     const float2 dy = __fadd2_rn(vv, nfy[k]);  // v - y, exactly
-                    qq[k] = __ffma2_rn(ta2, dx2, __ffma2_rn(__fmul2_rn(cc, dy), dy, __fmul2_rn(tb2, dy)));
+                    qq[k] = __ffma2_rn(__ffma2_rn(cc, dy, tb2), dy, ta2);  // Horner in dy
                     h[2 * k] = hit(p[k].T.x, qq[k].x, bq.w);
                     h[2 * k + 1] = hit(p[k].T.y, qq[k].y, bq.w);
                     anyh |= h[2 * k] | h[2 * k + 1];
@@ -213,9 +218,17 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
                 }
                 if (anyh) {
                     const float4 c = sC[s][q];  // o, r, g, b
+                    if (c.x > 0.98f) {
 #pragma unroll
-                    for (int k = 0; k < NP; ++k)
-                        if (h[2 * k] | h[2 * k + 1]) composite2(p[k], qq[k].x, qq[k].y, h[2 * k], h[2 * k + 1], c);
+                        for (int k = 0; k < NP; ++k)
+                            if (h[2 * k] | h[2 * k + 1])
+                                composite2<true>(p[k], qq[k].x, qq[k].y, h[2 * k], h[2 * k + 1], c);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < NP; ++k)
+                            if (h[2 * k] | h[2 * k + 1])
+                                composite2<false>(p[k], qq[k].x, qq[k].y, h[2 * k], h[2 * k + 1], c);
+                    }
                 }
             }
         }
