@@ -48,6 +48,7 @@ def parse():
                     help="entropy: rANS-coded latents decoded on the GPU each frame (default); int8: raw latents")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-libsort", action="store_true", help="skip the torch.sort (CUB) comparison")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
     ap.add_argument("--no-paper-style", action="store_true", help="skip the decode + 1 centre view timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -365,33 +366,74 @@ def main():
         return 3
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if not args.no_profile:
-        player.profile(True)
-        player.profile_read(reset=True)
+    use_graph = not args.no_graph
+
+    def bcast(t):  # N > 1: packet t into its slot on every rank (NCCL, outside any graph)
+        if world > 1:
+            if rank == 0:
+                slots[t % 2].copy_(src_bufs[t % P])  # stands for "packet t arrived in HBM on rank 0"
+            dist.broadcast(slots[t % 2], 0)
+
+    def timed_loop(run_step, sampler=None):
+        e0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        e1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.start()
+        for k in range(args.steps):
+            flush.zero_()  # L2 flushed between timed steps (outside the step's events)
+            e0[k].record(stream)
+            run_step(args.warmup + k)
+            e1[k].record(stream)
+        torch.cuda.synchronize()
+        c = sampler.stop() if sampler else None
+        if world > 1:
+            dist.barrier()
+        ms = [a.elapsed_time(b) for a, b in zip(e0, e1)]
+        tot = torch.tensor([sum(ms), statistics.median(ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        return float(tot[0]), float(tot[1]), c
+
+    # Headline: the frame step replayed from CUDA graphs (runtime.Player.capture: one graph per
+    # packet slot; entropy decode + apply + render; the NCCL broadcast, N > 1, outside the graph),
+    # with the stage profiler's events captured inside the graphs (stage times = each graph's
+    # last replay, live in the timed region).  --no-graph: eager launches, profiled per step.
+    prof, n_prof_frames = {}, args.steps
+    eager = None
     clocks = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    for k in range(args.steps):
-        flush.zero_()  # L2 flushed between timed steps (outside the step's events)
-        ev0[k].record(stream)
-        step(args.warmup + k)
-        ev1[k].record(stream)
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    if world > 1:
-        dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
-    prof = player.profile_read(reset=True) if not args.no_profile else {}
-    player.profile(False)
-    st, info = player.check_status()
-    tot = torch.tensor([sum(step_ms), statistics.median(step_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    total_ms, med_ms = float(tot[0]), float(tot[1])
+    if use_graph:
+        player.profile_read(reset=True)
+        graphs = [player.capture(d, profile=not args.no_profile) for d in dps]  # N = 1: per packet
+        player.planes.copy_(torch.from_numpy(sc.planes).to(dev))
+        for t in range(args.warmup):
+            bcast(t)
+            graphs[t % len(graphs)].replay()
+
+        def gstep(t):
+            bcast(t)
+            graphs[t % len(graphs)].replay()
+        total_ms, med_ms, clk = timed_loop(gstep, clocks)
+        if not args.no_profile:
+            prof = player.profile_read(reset=True)
+            n_prof_frames = len(graphs)
+        del graphs
+        st, info = player.check_status()
+        # eager launches of the same frames, for comparison (no profiler)
+        player.planes.copy_(torch.from_numpy(sc.planes).to(dev))
+        e_tot, e_med, _ = timed_loop(step)
+        eager = {"value": args.steps / (e_tot / 1e3), "unit": UNIT, "ms_per_step": e_tot / args.steps,
+                 "note": "the same frames with eager (non-graph) launches"}
+    else:
+        if not args.no_profile:
+            player.profile(True)
+            player.profile_read(reset=True)
+        total_ms, med_ms, clk = timed_loop(step, clocks)
+        prof = player.profile_read(reset=True) if not args.no_profile else {}
+        player.profile(False)
+        st, info = player.check_status()
     value = args.steps / (total_ms / 1e3)  # frames/s, whole job (all V views per frame)
     mpix = value * V * W * H / 1e6
 
@@ -420,7 +462,7 @@ def main():
     stages = {}
     for name, (ms, launches) in prof.items():
         if launches:
-            stages[name] = {"ms_per_step": ms / args.steps, "launches_per_step": launches / args.steps,
+            stages[name] = {"ms_per_step": ms / n_prof_frames, "launches_per_step": launches / n_prof_frames,
                             "us_per_launch": 1e3 * ms / launches}
     gpu_launches = int(round(sum(v["launches_per_step"] for v in stages.values()) * args.steps)) if stages else None
     k_coo = host_pkts[0].k if rank == 0 else k_cap
@@ -692,12 +734,14 @@ def main():
                        "gaussians": cfg.n, "views": V, "width": W, "height": H, "views_per_batch": player.vpb, "render_lanes": player.n_lanes,
                        "parallelism": f"views sharded v mod {world}, Gaussians replicated, packet NCCL-broadcast",
                        "packet_format": args.packet_format,
+                       "launch": "CUDA-graph replay (one graph per packet slot)" if use_graph else "eager",
                        "l2": "flushed between timed steps (512 MB write outside the step events)"},
             "packet_bytes_per_frame": int(statistics.mean(used_bytes)) if used_bytes else None,
             "mpixel_per_s": mpix, "view_fps": value * V,
             "status": Q.STATUS.get(st, st),
             "keys_per_batch": K_list, "visible_pairs_per_batch": M_list, "stages": stages, "roofline": roof,
             "path_roofline": path, "paper_style": paper, "library_sort": libsort, "masked_render": masked, "densify": densify, "backward": backward,
+            "eager": eager,
             "e2e_f32": e2e_f32, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
         }

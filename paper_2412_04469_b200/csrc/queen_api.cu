@@ -310,6 +310,7 @@ queen_status queen_blend_counts(queen_ctx* ctx, const queen_proj* proj, const qu
 queen_status queen_profile_enable(queen_ctx* ctx, int32_t enable) {
     if (!ctx) return QUEEN_ERR_INVALID_ARG;
     ctx->prof.on = enable != 0;
+    ctx->prof.reset_chain();
     return QUEEN_OK;
 }
 
@@ -328,6 +329,7 @@ queen_status queen_profile_read(queen_ctx* ctx, double* ms, int64_t* launches, i
         }
         P.pending.clear();
         P.used = 0;
+        P.reset_chain();
     }
     for (int i = 0; i < ST_COUNT; ++i) {
         ms[i] = P.ms[i];

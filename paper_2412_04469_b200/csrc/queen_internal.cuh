@@ -7,6 +7,7 @@
 // CPU oracle (which is written independently from the same text).
 #pragma once
 #include <cstdint>
+#include <cstddef>
 #include <vector>
 #include <cuda_runtime.h>
 
@@ -255,18 +256,45 @@ struct Prof {
         }
         return pool[used++];
     }
+    // inside a stream capture the record must be an EXTERNAL event-record node, so every graph
+    // replay re-records it (a plain record would only become a capture-internal dependency)
+    static void record(cudaEvent_t e, cudaStream_t s) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cs);
+        if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+        else cudaEventRecord(e, s);
+    }
+    // consecutive stages share their boundary event: begin() reuses the previous end() event
+    // when nothing was profiled in between (halves the events, e.g. the nodes in a graph)
+    // (a frame starts at the entropy decode, or at apply for uncoded packets: the chain breaks
+    // there, so work enqueued between frames is never attributed to a stage)
+    size_t last_end = SIZE_MAX;
+    cudaStream_t last_stream = nullptr;
+    int last_stage = -1;
     void begin(int stage, cudaStream_t s) {
         if (!on) return;
-        open_ev = used;
-        cudaEventRecord(ev(), s);
+        const bool frame_start = stage == ST_ENTROPY || (stage == ST_APPLY && last_stage != ST_ENTROPY);
+        if (!frame_start && last_end != SIZE_MAX && last_stream == s) {
+            open_ev = last_end;
+        } else {
+            open_ev = used;
+            record(ev(), s);
+        }
         open_stage = stage;
     }
     void end(cudaStream_t s, int n_launches = 1) {
         if (!on || open_stage < 0) return;
         size_t e1 = used;
-        cudaEventRecord(ev(), s);
+        record(ev(), s);
         pending.push_back({open_stage, open_ev, e1, n_launches});
+        last_stage = open_stage;
         open_stage = -1;
+        last_end = e1;
+        last_stream = s;
+    }
+    void reset_chain() {
+        last_end = SIZE_MAX;
+        last_stage = -1;
     }
 };
 

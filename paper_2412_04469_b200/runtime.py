@@ -176,6 +176,31 @@ class Player:
             main.wait_stream(s)
         return rgb
 
+    def capture(self, pkt, out=None, rgb8: bool = False, profile: bool = False):
+        """Capture one frame step -- (entropy decode +) apply of `pkt` + render of every view --
+        into a CUDA graph and return it (torch.cuda.CUDAGraph; .replay() runs the frame with one
+        launch).  The packet's buffers, the output and the workspaces are baked in: replay it
+        after refilling the same packet buffer (fixed-capacity wire layout, k read on device).
+        Call fit_capacity() first (no host sync may happen inside).  profile=True bakes the
+        stage profiler's events into the graph: profile_read() after replays returns the stage
+        times of each graph's LAST replay."""
+        g = torch.cuda.CUDAGraph()
+        self.profile(False)
+        side = torch.cuda.Stream(device=self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(side):  # warm-up outside capture (allocator, lazy init)
+            self.apply(pkt)
+            self.render(out=out, rgb8=rgb8)
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        torch.cuda.synchronize(self.dev)
+        if profile:
+            self.profile(True)
+        with torch.cuda.graph(g):
+            self.apply(pkt)
+            self.render(out=out, rgb8=rgb8)
+        self.profile(False)
+        return g
+
     def densify(self, rem_idx, n_rem: int, add_attrs, n_add: int, stream=None):
         """NEXT #2: apply a densification delta after the frame's residuals (queen_densify):
         drop the removed Gaussians (device u32, strictly increasing), append the binary16
