@@ -62,9 +62,10 @@ static void normalise(const uint64_t cnt[256], uint64_t total, uint16_t f[256]) 
 }
 
 // ---------------------------------------------------------------- device decoder
-// One launch decodes every category of a frame: block -> (category, 4 chunks), one warp per
-// chunk, one rANS state per lane.  The category's slot -> symbol table is rebuilt per block
-// in shared memory (slot-parallel binary search over the cumulative frequencies).
+// Two launches per frame: k_ans_table builds every category's slot table once (slot ->
+// packed (symbol | (f - 1) << 8 | (slot - c) << 20), 4096 x u32 = 16 KB per category, in the
+// workspace); k_ans_decode copies its category's table to shared memory and decodes, one warp
+// per chunk, one rANS state per lane: a decode step is ONE shared load + a multiply-add.
 constexpr int ANS_WARPS = 4;
 
 struct AnsFrame {
@@ -73,18 +74,15 @@ struct AnsFrame {
     int row0[5];          // first latent row of the category in the [sum L][n_pad] matrix
     int block0[6];        // first block of each category (prefix), block0[5] = total blocks
     int n, n_pad;
+    const uint32_t* table;  // [5][ANS_M] packed slot tables (k_ans_table)
 };
 
-__global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr, int8_t* __restrict__ out, DevFlags* fl) {
-    __shared__ uint8_t s_sym[ANS_M];
-    __shared__ uint16_t s_f[256], s_c[257];
-    int cat = 0;
-    while (cat < 4 && (int)blockIdx.x >= fr.block0[cat + 1]) ++cat;
-    const unsigned char* stream = fr.stream[cat];
-    const int L = fr.L[cat], n = fr.n, n_pad = fr.n_pad;
-    const AnsHeader* h = reinterpret_cast<const AnsHeader*>(stream);
-    const uint32_t n_sym = h->n_sym, n_chunks = h->n_chunks;
-    if (threadIdx.x == 0 && (h->magic != ANS_MAGIC || n_sym != (uint32_t)L * (uint32_t)n)) raise_flag(fl, FLAG_INDEX);
+__global__ void __launch_bounds__(256) k_ans_table(const AnsFrame fr, uint32_t* __restrict__ table, DevFlags* fl) {
+    __shared__ uint16_t s_f[256];
+    __shared__ uint32_t s_c[257];
+    const int cat = blockIdx.y;
+    if (fr.L[cat] == 0) return;
+    const AnsHeader* h = reinterpret_cast<const AnsHeader*>(fr.stream[cat]);
     for (int q = threadIdx.x; q < 256; q += blockDim.x) s_f[q] = h->freq[q];
     __syncthreads();
     if (threadIdx.x < 32) {  // exclusive scan of the 256 frequencies by one warp
@@ -96,17 +94,35 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
             if (threadIdx.x >= o) inc += y;
         }
         uint32_t run = inc - sum;
-        for (int q = 0; q < 8; ++q) { s_c[threadIdx.x * 8 + q] = (uint16_t)min(run, (uint32_t)0xffff); run += v[q]; }
-        if (threadIdx.x == 31) s_c[256] = (uint16_t)min(run, (uint32_t)0xffff);
+        for (int q = 0; q < 8; ++q) { s_c[threadIdx.x * 8 + q] = run; run += v[q]; }
+        if (threadIdx.x == 31) s_c[256] = run;
     }
     __syncthreads();
-    for (uint32_t slot = threadIdx.x; slot < ANS_M; slot += blockDim.x) {  // symbol s with c[s] <= slot < c[s+1]
-        int lo = 0, hi = 256;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (s_c[mid] <= slot) lo = mid; else hi = mid;
-        }
-        s_sym[slot] = (uint8_t)lo;
+    if (threadIdx.x == 0 && blockIdx.x == 0 && s_c[256] != ANS_M) raise_flag(fl, FLAG_INDEX);  // corrupt table
+    const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;  // symbol s with c[s] <= slot < c[s+1]
+    if (slot >= ANS_M) return;
+    int lo = 0, hi = 256;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_c[mid] <= slot) lo = mid; else hi = mid;
+    }
+    const uint32_t f = s_f[lo];
+    table[(size_t)cat * ANS_M + slot] = (uint32_t)lo | ((f ? f - 1 : 0) << 8) | ((slot - s_c[lo]) << 20);
+}
+
+__global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr, int8_t* __restrict__ out, DevFlags* fl) {
+    __shared__ uint32_t s_tab[ANS_M];
+    int cat = 0;
+    while (cat < 4 && (int)blockIdx.x >= fr.block0[cat + 1]) ++cat;
+    const unsigned char* stream = fr.stream[cat];
+    const int L = fr.L[cat], n = fr.n, n_pad = fr.n_pad;
+    const AnsHeader* h = reinterpret_cast<const AnsHeader*>(stream);
+    const uint32_t n_sym = h->n_sym, n_chunks = h->n_chunks;
+    if (threadIdx.x == 0 && (h->magic != ANS_MAGIC || n_sym != (uint32_t)L * (uint32_t)n)) raise_flag(fl, FLAG_INDEX);
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(fr.table + (size_t)cat * ANS_M);
+        uint4* dst = reinterpret_cast<uint4*>(s_tab);
+        for (int q = threadIdx.x; q < ANS_M / 4; q += blockDim.x) dst[q] = __ldg(src + q);
     }
     __syncthreads();
     const uint32_t chunk = (blockIdx.x - fr.block0[cat]) * ANS_WARPS + (threadIdx.x >> 5);
@@ -133,10 +149,9 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
     for (uint32_t t = 0; t < steps; ++t) {
         const bool active = t * 32 + lane < len;
         if (active) {
-            const uint32_t slot = x & (ANS_M - 1);
-            const uint32_t sy = s_sym[slot];
-            x = (uint32_t)s_f[sy] * (x >> ANS_PROB_BITS) + slot - s_c[sy];
-            cout[(size_t)k * n_pad + i] = (int8_t)((int)sy - 128);
+            const uint32_t e = s_tab[x & (ANS_M - 1)];
+            x = ((e >> 8 & 0xfffu) + 1u) * (x >> ANS_PROB_BITS) + (e >> 20);
+            cout[(size_t)k * n_pad + i] = (int8_t)((int)(e & 0xffu) - 128);
         }
         const bool need = active && x < ANS_L;
         const uint32_t m = __ballot_sync(0xffffffffu, need);
@@ -163,10 +178,11 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
 }
 
 cudaError_t launch_ans_decode_frame(const void* const streams[5], const int L[5], int n, int n_pad, int8_t* out,
-                                    DevFlags* fl, cudaStream_t s) {
+                                    uint32_t* table, DevFlags* fl, cudaStream_t s) {
     AnsFrame fr{};
     fr.n = n;
     fr.n_pad = n_pad;
+    fr.table = table;
     int row = 0, blk = 0;
     for (int c = 0; c < 5; ++c) {
         fr.stream[c] = static_cast<const unsigned char*>(streams[c]);
@@ -179,15 +195,16 @@ cudaError_t launch_ans_decode_frame(const void* const streams[5], const int L[5]
     }
     fr.block0[5] = blk;
     if (blk == 0) return cudaSuccess;
+    k_ans_table<<<dim3(ANS_M / 256, 5), 256, 0, s>>>(fr, table, fl);
     k_ans_decode<<<blk, ANS_WARPS * 32, 0, s>>>(fr, out, fl);
     return cudaGetLastError();
 }
 
-cudaError_t launch_ans_decode(const void* stream_dev, int L, int n, int n_pad, int8_t* out, DevFlags* fl,
-                              cudaStream_t s) {
+cudaError_t launch_ans_decode(const void* stream_dev, int L, int n, int n_pad, int8_t* out, uint32_t* table,
+                              DevFlags* fl, cudaStream_t s) {
     const void* streams[5] = {stream_dev, nullptr, nullptr, nullptr, nullptr};
     const int Ls[5] = {L, 0, 0, 0, 0};
-    return launch_ans_decode_frame(streams, Ls, n, n_pad, out, fl, s);
+    return launch_ans_decode_frame(streams, Ls, n, n_pad, out, table, fl, s);
 }
 
 // ---------------------------------------------------------------- host encoder

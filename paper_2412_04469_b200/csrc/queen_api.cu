@@ -30,10 +30,10 @@ float host_theta0(float tau, float g0, float g1) {
 cudaError_t init_binning_attributes();
 int key_passes(int64_t gtiles);
 size_t ans_encode(const int8_t* lat, int L, int n, int n_pad, std::vector<unsigned char>& out);
-cudaError_t launch_ans_decode(const void* stream_dev, int L, int n, int n_pad, int8_t* out, DevFlags* fl,
-                              cudaStream_t s);
+cudaError_t launch_ans_decode(const void* stream_dev, int L, int n, int n_pad, int8_t* out, uint32_t* table,
+                              DevFlags* fl, cudaStream_t s);
 cudaError_t launch_ans_decode_frame(const void* const streams[5], const int L[5], int n, int n_pad, int8_t* out,
-                                    DevFlags* fl, cudaStream_t s);
+                                    uint32_t* table, DevFlags* fl, cudaStream_t s);
 }  // namespace queen
 
 using namespace queen;
@@ -355,8 +355,10 @@ queen_status queen_entropy_decode(queen_ctx* ctx, const void* stream_dev, int32_
     if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
     if (!stream_dev || !latents_out || L < 0 || L > 16 || n < 0 || n > n_pad) return fail(ctx, QUEEN_ERR_INVALID_ARG, "entropy decode args");
     ctx->prof.begin(ST_ENTROPY, static_cast<cudaStream_t>(stream));
-    cudaError_t e = launch_ans_decode(stream_dev, L, n, n_pad, latents_out, flags_of(ctx), static_cast<cudaStream_t>(stream));
-    ctx->prof.end(static_cast<cudaStream_t>(stream));
+    uint32_t* tab = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(ctx->ws) + ctx->L.ans_table);
+    cudaError_t e = launch_ans_decode(stream_dev, L, n, n_pad, latents_out, tab, flags_of(ctx),
+                                      static_cast<cudaStream_t>(stream));
+    ctx->prof.end(static_cast<cudaStream_t>(stream), 2);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "entropy decode");
     return QUEEN_OK;
 }
@@ -373,8 +375,10 @@ queen_status queen_entropy_decode_frame(queen_ctx* ctx, const void* const* strea
         L5[c] = lat_dim[c];
     }
     ctx->prof.begin(ST_ENTROPY, static_cast<cudaStream_t>(stream));
-    cudaError_t e = launch_ans_decode_frame(s5, L5, n, n_pad, latents_out, flags_of(ctx), static_cast<cudaStream_t>(stream));
-    ctx->prof.end(static_cast<cudaStream_t>(stream));
+    uint32_t* tab = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(ctx->ws) + ctx->L.ans_table);
+    cudaError_t e = launch_ans_decode_frame(s5, L5, n, n_pad, latents_out, tab, flags_of(ctx),
+                                            static_cast<cudaStream_t>(stream));
+    ctx->prof.end(static_cast<cudaStream_t>(stream), 2);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "entropy decode frame");
     return QUEEN_OK;
 }

@@ -99,7 +99,7 @@ inline BinPlan bin_plan(int64_t n_pad, int64_t n_views, int W, int H) {
 struct WsLayout {
     // scratch (bin_sort)
     size_t flags, hist, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, counts, view_tot, slab_counts,
-        slab_vis, select, total_scratch;
+        slab_vis, select, ans_table, total_scratch;
     // render_views / render_mask buffers
     size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, mask_tmp, total;
     int64_t key_tiles, elem_tiles, os_key_tiles, os_elem_tiles, T, elems;
@@ -132,6 +132,7 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     L.slab_counts = o; o += align256(sizeof(uint32_t) * (size_t)(bp.ok ? bp.slabs : 0) * L.T);
     L.slab_vis = o; o += align256(sizeof(uint32_t) * (size_t)(bp.slabs + 1));
     L.select = o; o += align256((size_t)n_pad);  // render_mask: per-Gaussian subset flags
+    L.ans_table = o; o += align256(sizeof(uint32_t) * 5 * 4096);  // entropy decode slot tables
     L.total_scratch = o;
     L.rec = o; o += align256(sizeof(float) * REC_WORDS * L.elems);
     L.depth = o; o += align256(sizeof(uint32_t) * L.elems);
@@ -154,7 +155,8 @@ inline bool scratch_fits(const WsLayout& need, const WsLayout& have) {
                                    &WsLayout::depth_lb,   &WsLayout::tile_lb,     &WsLayout::dkeys,
                                    &WsLayout::dkeys_alt,  &WsLayout::dvals,       &WsLayout::dvals_alt,
                                    &WsLayout::counts,     &WsLayout::view_tot,    &WsLayout::slab_counts,
-                                   &WsLayout::slab_vis,   &WsLayout::select,      &WsLayout::total_scratch};
+                                   &WsLayout::slab_vis,   &WsLayout::select,      &WsLayout::ans_table,
+                                   &WsLayout::total_scratch};
     for (size_t q = 0; q + 1 < sizeof(r) / sizeof(r[0]); ++q)
         if (need.*r[q + 1] - need.*r[q] > have.*r[q + 1] - have.*r[q]) return false;
     return true;
