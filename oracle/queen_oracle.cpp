@@ -317,13 +317,13 @@ static int project_one(int i, int n_pad, int deg, const float* pl, const Cam& c,
         }
     // 4. Jacobian of the affine approximation of the projective transform,
     //    with the 3D-GS 1.3x frustum clamp (R#11)
-    float tx = xc / zc, ty = yc / zc;
-    float xcl = std::fmin(c.limx, std::fmax(-c.limx, tx)) * zc;
-    float ycl = std::fmin(c.limy, std::fmax(-c.limy, ty)) * zc;
-    float j00 = c.fx / zc;
-    float j02 = -(c.fx * xcl) / (zc * zc);
-    float j11 = c.fy / zc;
-    float j12 = -(c.fy * ycl) / (zc * zc);
+    //    (one reciprocal of z_c; DESIGN "Arithmetic contract")
+    float iz = 1.0f / zc;
+    float tx = xc * iz, ty = yc * iz;
+    float j00 = c.fx * iz;
+    float j02 = -(c.fx * std::fmin(c.limx, std::fmax(-c.limx, tx))) * iz;
+    float j11 = c.fy * iz;
+    float j12 = -(c.fy * std::fmin(c.limy, std::fmax(-c.limy, ty))) * iz;
     // 5. Sigma' = J W Sigma W^T J^T (Eq. 1) + 0.3 px^2 (R#11)
     float A[6];
     for (int m = 0; m < 3; ++m) {
@@ -342,7 +342,8 @@ static int project_one(int i, int n_pad, int deg, const float* pl, const Cam& c,
     // 6. conic = Sigma'^-1 (Eq. 2 exponent)
     float det = std::fma(a, cc2, -(b * b));
     if (!(det > 0.0f)) return 0;
-    float ca = cc2 / det, cb = -b / det, ccn = a / det;
+    float idet = 1.0f / det;
+    float ca = cc2 * idet, cb = -b * idet, ccn = a * idet;
     // 7. opacity o = sigmoid(logit) in [0,1]; alpha can reach 1/255 only if 255 o > 1 (R#14)
     float o = 1.0f / (1.0f + oracle_det_exp(-pl[10 * (int64_t)n_pad + i]));
     if (!(255.0f * o > 1.0f)) return 0;
@@ -371,7 +372,8 @@ static int project_one(int i, int n_pad, int deg, const float* pl, const Cam& c,
     // 11. view-dependent colour from SH, +0.5 and clamp at 0 (R#8)
     float dx = px - c.C[0], dy = py - c.C[1], dz = pz - c.C[2];
     float dn = std::sqrt(std::fma(dx, dx, std::fma(dy, dy, dz * dz)));
-    dx = dx / dn; dy = dy / dn; dz = dz / dn;
+    float idn = 1.0f / dn;
+    dx = dx * idn; dy = dy * idn; dz = dz * idn;
     float Y[16];
     oracle_sh_basis(deg, dx, dy, dz, Y);
     float rgb[3];

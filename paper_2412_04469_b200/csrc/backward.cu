@@ -310,10 +310,11 @@ __global__ void __launch_bounds__(128) k_project_bwd(const float* __restrict__ p
             const float X = fmaf(Rw[0], a[0], fmaf(Rw[1], a[1], fmaf(Rw[2], a[2], c.t[0])));
             const float Y = fmaf(Rw[3], a[0], fmaf(Rw[4], a[1], fmaf(Rw[5], a[2], c.t[1])));
             const float Z = fmaf(Rw[6], a[0], fmaf(Rw[7], a[1], fmaf(Rw[8], a[2], c.t[2])));
-            const float tx = X / Z, ty = Y / Z;
+            const float izf = 1.0f / Z;  // the forward's operations (k_project)
+            const float tx = X * izf, ty = Y * izf;
             const bool clx = fabsf(tx) > c.limx, cly = fabsf(ty) > c.limy;
             const float txc = fminf(c.limx, fmaxf(-c.limx, tx)), tyc = fminf(c.limy, fmaxf(-c.limy, ty));
-            const float J00 = c.fx / Z, J02 = -(c.fx * txc) / Z, J11 = c.fy / Z, J12 = -(c.fy * tyc) / Z;
+            const float J00 = c.fx * izf, J02 = -(c.fx * txc) * izf, J11 = c.fy * izf, J12 = -(c.fy * tyc) * izf;
             float Tm[6];
             for (int m = 0; m < 3; ++m) {
                 Tm[m] = fmaf(J00, Rw[m], J02 * Rw[6 + m]);

@@ -124,14 +124,13 @@ __global__ void __launch_bounds__(128) k_project(const float* __restrict__ plane
         float a2 = 0.f, b2 = 0.f, c2 = 0.f, sxx = 0.f, syy = 0.f, tx = 0.f, ty = 0.f;
         if (ok) {
             const float* Rw = c.R;
-            tx = xc / zc;
-            ty = yc / zc;
-            const float xcl = fminf(c.limx, fmaxf(-c.limx, tx)) * zc;
-            const float ycl = fminf(c.limy, fmaxf(-c.limy, ty)) * zc;
-            const float j00 = c.fx / zc;
-            const float j02 = -(c.fx * xcl) / (zc * zc);
-            const float j11 = c.fy / zc;
-            const float j12 = -(c.fy * ycl) / (zc * zc);
+            const float iz = 1.0f / zc;  // one reciprocal of z_c (DESIGN "Arithmetic contract")
+            tx = xc * iz;
+            ty = yc * iz;
+            const float j00 = c.fx * iz;
+            const float j02 = -(c.fx * fminf(c.limx, fmaxf(-c.limx, tx))) * iz;
+            const float j11 = c.fy * iz;
+            const float j12 = -(c.fy * fminf(c.limy, fmaxf(-c.limy, ty))) * iz;
             float A[6];
 #pragma unroll
             for (int m = 0; m < 3; ++m) {
@@ -152,9 +151,10 @@ __global__ void __launch_bounds__(128) k_project(const float* __restrict__ plane
             const float det = fmaf(sa, sc, -(sb * sb));
             ok = det > 0.0f;
             if (ok) {
-                a2 = sc / det;    // conic xx
-                b2 = -sb / det;   // conic xy
-                c2 = sa / det;    // conic yy
+                const float idet = 1.0f / det;
+                a2 = sc * idet;   // conic xx
+                b2 = -sb * idet;  // conic xy
+                c2 = sa * idet;   // conic yy
                 sxx = sa;         // Sigma'_xx (incl. the 0.3 dilation)
                 syy = sc;
             }
@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(128) k_project(const float* __restrict__ plane
             // colour: dir = (p - C)/|p - C|, rgb = max(0, sum Y_b h_b + 0.5) (R#8, R#10)
             float dx = px - c.C[0], dy = py - c.C[1], dz = pz - c.C[2];
             const float dn = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-            dx = dx / dn; dy = dy / dn; dz = dz / dn;
+            const float idn = 1.0f / dn;
+            dx = dx * idn; dy = dy * idn; dz = dz * idn;
             float Y[16];
             sh_basis(DEG, dx, dy, dz, Y);
             float rgb[3];
