@@ -156,10 +156,9 @@ __global__ void __launch_bounds__(SLAB_THREADS) k_slab_count(const uint32_t* __r
                                                              const short4* __restrict__ rect,
                                                              const uint32_t* __restrict__ depth, int n_pad, int S, int spv,
                                                              int gx, int gy, uint32_t* __restrict__ counts,
-                                                             uint32_t* __restrict__ svis, uint32_t* __restrict__ hist) {
+                                                             uint32_t* __restrict__ svis, uint32_t* __restrict__ dminmax) {
     extern __shared__ int cs[];  // [(gy+1)][(gx+1)] difference array -> 2D prefix
-    __shared__ uint32_t sh[DEPTH_PASSES * 256];
-    __shared__ uint32_t s_vis;
+    __shared__ uint32_t s_vis, s_min, s_max;
     const int slab = blockIdx.x;
     const int v = slab / spv;
     const int a = (slab - v * spv) * S;
@@ -167,11 +166,10 @@ __global__ void __launch_bounds__(SLAB_THREADS) k_slab_count(const uint32_t* __r
     const int dw = gx + 1, dplane = (gx + 1) * (gy + 1);
     const int T = gx * gy;
     for (int q = threadIdx.x; q < dplane; q += blockDim.x) cs[q] = 0;
-    for (int q = threadIdx.x; q < DEPTH_PASSES * 256; q += blockDim.x) sh[q] = 0;
-    if (threadIdx.x == 0) s_vis = 0;
+    if (threadIdx.x == 0) { s_vis = 0; s_min = 0xffffffffu; s_max = 0u; }
     __syncthreads();
     const int64_t jb = (int64_t)v * n_pad;
-    uint32_t vis = 0;
+    uint32_t vis = 0, kmin = 0xffffffffu, kmax = 0u;
     for (int i = a + threadIdx.x * SLAB_IT; i < b; i += SLAB_ROUND) {
         uint32_t nt[8], dk[8];
         short4 r[8];
@@ -180,20 +178,32 @@ __global__ void __launch_bounds__(SLAB_THREADS) k_slab_count(const uint32_t* __r
         for (int e = 0; e < 8; ++e) {
             if (nt[e] == 0) continue;
             ++vis;
+            kmin = min(kmin, dk[e]);
+            kmax = max(kmax, dk[e]);
             atomicAdd(&cs[r[e].y * dw + r[e].x], 1);
             atomicAdd(&cs[r[e].y * dw + r[e].z + 1], -1);
             atomicAdd(&cs[(r[e].w + 1) * dw + r[e].x], -1);
             atomicAdd(&cs[(r[e].w + 1) * dw + r[e].z + 1], 1);
-#pragma unroll
-            for (int p = 0; p < DEPTH_PASSES; ++p) atomicAdd(&sh[p * 256 + ((dk[e] >> (8 * p)) & 255u)], 1u);
         }
     }
-    for (int o = 16; o > 0; o >>= 1) vis += __shfl_down_sync(0xffffffffu, vis, o);
-    if ((threadIdx.x & 31) == 0 && vis) atomicAdd(&s_vis, vis);
+    for (int o = 16; o > 0; o >>= 1) {
+        vis += __shfl_down_sync(0xffffffffu, vis, o);
+        kmin = min(kmin, __shfl_down_sync(0xffffffffu, kmin, o));
+        kmax = max(kmax, __shfl_down_sync(0xffffffffu, kmax, o));
+    }
+    if ((threadIdx.x & 31) == 0 && vis) {
+        atomicAdd(&s_vis, vis);
+        atomicMin(&s_min, kmin);
+        atomicMax(&s_max, kmax);
+    }
     __syncthreads();
-    for (int q = threadIdx.x; q < DEPTH_PASSES * 256; q += blockDim.x)
-        if (sh[q]) atomicAdd(&hist[(q >> 8) * MAX_BINS + (q & 255)], sh[q]);  // per-pass stride MAX_BINS
-    if (threadIdx.x == 0) svis[slab] = s_vis;
+    if (threadIdx.x == 0) {
+        svis[slab] = s_vis;
+        if (s_vis) {
+            atomicMin(&dminmax[0], s_min);
+            atomicMax(&dminmax[1], s_max);
+        }
+    }
     for (int r = threadIdx.x; r < gy; r += blockDim.x) {  // prefix along x
         int run = 0;
         for (int x = 0; x < gx; ++x) { run += cs[r * dw + x]; cs[r * dw + x] = run; }
@@ -323,16 +333,21 @@ __global__ void __launch_bounds__(1024) k_totals(const uint32_t* __restrict__ vi
 __global__ void __launch_bounds__(SLAB_THREADS) k_slab_compact(const uint32_t* __restrict__ tiles,
                                                                const uint32_t* __restrict__ depth, int n_pad, int S,
                                                                int spv, const uint32_t* __restrict__ soff,
-                                                               uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dvals) {
+                                                               const uint32_t* __restrict__ dminmax,
+                                                               uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
+                                                               uint32_t* __restrict__ hist) {
     constexpr int NW = SLAB_THREADS / 32;
     __shared__ uint32_t s_w[NW];
     __shared__ uint32_t s_k[SLAB_ROUND], s_j[SLAB_ROUND];
+    __shared__ uint32_t sh[DEPTH_PASSES * MAX_BINS];
     const int slab = blockIdx.x;
     const int v = slab / spv;
     const int a = (slab - v * spv) * S;
     const int b = min(a + S, n_pad);
     const int64_t jb = (int64_t)v * n_pad;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t kmin = dminmax[0];
+    for (int q = threadIdx.x; q < DEPTH_PASSES * MAX_BINS; q += SLAB_THREADS) sh[q] = 0;
     uint32_t base = soff[slab];
     for (int i0 = a; i0 < b; i0 += SLAB_ROUND) {
         const int i = i0 + threadIdx.x * SLAB_IT;
@@ -360,9 +375,13 @@ __global__ void __launch_bounds__(SLAB_THREADS) k_slab_compact(const uint32_t* _
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             if (nt[e]) {
-                s_k[o] = dk[e];
+                const uint32_t rk = dk[e] - kmin;  // relative depth key (order-preserving: keys >= kmin)
+                s_k[o] = rk;
                 s_j[o] = (uint32_t)(jb + i + e);
                 ++o;
+#pragma unroll
+                for (int p = 0; p < DEPTH_PASSES; ++p)
+                    atomicAdd(&sh[p * MAX_BINS + ((rk >> (DEPTH_BITS * p)) & (MAX_BINS - 1))], 1u);
             }
         }
         __syncthreads();
@@ -373,6 +392,8 @@ __global__ void __launch_bounds__(SLAB_THREADS) k_slab_compact(const uint32_t* _
         base += tot;
         __syncthreads();
     }
+    for (int q = threadIdx.x; q < DEPTH_PASSES * MAX_BINS; q += SLAB_THREADS)
+        if (sh[q]) atomicAdd(&hist[q], sh[q]);
 }
 
 // exclusive scan of each pass's digit counts (one warp per pass)
@@ -447,7 +468,8 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
                                                                    const uint32_t* count_ptr, uint32_t cap, int shift,
                                                                    int pshift, int ibits,
                                                                    const uint32_t* __restrict__ hist_excl, uint32_t* lb,
-                                                                   uint32_t* ticket, DevFlags* fl) {
+                                                                   uint32_t* ticket, DevFlags* fl,
+                                                                   const uint32_t* __restrict__ triv) {
     using OS = Onesweep<BITS>;
     constexpr int NT = OS::NT, IT = OS::IT, NW = OS::NW, TILE = OS::TILE, BINS = OS::BINS, DPT = OS::DPT;
     constexpr uint32_t DMASK = BINS - 1;
@@ -462,6 +484,13 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
     const uint32_t ntiles = (Kn + TILE - 1) / TILE;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    if (triv && triv[0] == Kn) {  // every key has digit 0: the stable pass is the identity -- copy
+        for (uint64_t q = (uint64_t)blockIdx.x * NT + threadIdx.x; q < Kn; q += (uint64_t)gridDim.x * NT) {
+            if (MODE == OS_KV) { kout[q] = kin[q]; vout[q] = vin[q]; }
+            if (MODE == OS_V) vout[q] = vin[q];
+        }
+        return;
+    }
     const bool owns_digits = threadIdx.x * DPT < BINS;
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
@@ -793,9 +822,9 @@ cudaError_t init_binning_attributes() {
 template <int BITS, int MODE>
 static void onesweep(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout, const uint32_t* count,
                      uint32_t cap, int shift, int pshift, int ibits, const uint32_t* hist_excl, uint32_t* lb,
-                     uint32_t* ticket, DevFlags* fl, cudaStream_t s) {
+                     uint32_t* ticket, DevFlags* fl, cudaStream_t s, const uint32_t* triv = nullptr) {
     k_onesweep32<BITS, MODE><<<onesweep_grid<BITS, MODE>(), Onesweep<BITS>::NT, Onesweep<BITS>::SMEM, s>>>(
-        kin, vin, kout, vout, count, cap, shift, pshift, ibits, hist_excl, lb, ticket, fl);
+        kin, vin, kout, vout, count, cap, shift, pshift, ibits, hist_excl, lb, ticket, fl, triv);
 }
 
 template <int BITS>
@@ -845,14 +874,18 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     if ((e = cudaMemsetAsync(fl->tickets, 0, sizeof(fl->tickets), s))) return e;
     if ((e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS, s))) return e;
     if ((e = cudaMemsetAsync(dup_lb, 0, sizeof(unsigned long long) * (elem_tiles + 1), s))) return e;
-    if ((e = cudaMemsetAsync(depth_lb, 0, sizeof(uint32_t) * DEPTH_PASSES * 256 * (size_t)(os_elem_tiles + 1), s))) return e;
+    if ((e = cudaMemsetAsync(depth_lb, 0, sizeof(uint32_t) * DEPTH_PASSES * MAX_BINS * (size_t)(os_elem_tiles + 1), s)))
+        return e;
+    uint32_t* dminmax = reinterpret_cast<uint32_t*>(ws + L.dminmax);
+    if ((e = cudaMemsetAsync(dminmax, 0xff, sizeof(uint32_t), s))) return e;       // min <- 0xffffffff
+    if ((e = cudaMemsetAsync(dminmax + 1, 0, sizeof(uint32_t), s))) return e;      // max <- 0
     if ((e = cudaMemsetAsync(tile_lb, 0, sizeof(uint32_t) * (size_t)tpasses * (1 << tbits) * (size_t)(os_key_tiles + 1), s)))
         return e;
     if ((e = cudaMemsetAsync(bins.K, 0, sizeof(uint32_t) * 4, s))) return e;
     if (bp.slabs > 0) {
         k_slab_count<<<(unsigned)bp.slabs, SLAB_THREADS, sizeof(int) * dplane, s>>>(
             proj.tiles, reinterpret_cast<const short4*>(proj.rect), proj.depth, proj.n_pad, (int)bp.S, (int)bp.spv, gx, gy,
-            scount, svis, hist);
+            scount, svis, dminmax);
         k_slab_sum<<<dim3((unsigned)((T + 255) / 256), (unsigned)n_views), 256, 0, s>>>(scount, (int)bp.spv, (int)T,
                                                                                         tcounts);
         k_view_scan<<<n_views, 1024, 0, s>>>(tcounts, (int)T, lstart, view_tot, hist + DEPTH_PASSES * MAX_BINS, tpasses,
@@ -864,16 +897,23 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     k_totals<<<1, 1024, 0, s>>>(view_tot, n_views, svis, (int)bp.slabs, cap, Kd, fl);
     if (bp.slabs > 0)
         k_slab_compact<<<(unsigned)bp.slabs, SLAB_THREADS, 0, s>>>(proj.tiles, proj.depth, proj.n_pad, (int)bp.S,
-                                                                  (int)bp.spv, svis, dk[0], dv[0]);
+                                                                  (int)bp.spv, svis, dminmax, dk[0], dv[0], hist);
     prof->end(s, bp.slabs > 0 ? 5 : 1);
     // depth digits (LSD: least significant first) on the visible pairs
     prof->begin(ST_DEPTH_SORT, s);
-    k_hist_scan<<<1, 32 * DEPTH_PASSES, 0, s>>>(hist, hist_excl, DEPTH_PASSES, 256);
+    // depth keys are relative to the batch's smallest visible depth (order-preserving, and the
+    // range of a scene's depths fits 27 bits unless it spans > 2^27 ulps): three 9-bit passes,
+    // then bits 27..31, which is a copy (triv) whenever that digit is 0 for every key
+    k_hist_scan<<<1, 32 * DEPTH_PASSES, 0, s>>>(hist, hist_excl, DEPTH_PASSES, MAX_BINS);
     int cur = 0;
     for (int p = 0; p < DEPTH_PASSES; ++p) {
-        onesweep<8, OS_KV>(dk[cur], dv[cur], dk[cur ^ 1], dv[cur ^ 1], Md, (uint32_t)count, 8 * p, 0, 32,
-                           hist_excl + p * MAX_BINS, depth_lb + (size_t)p * 256 * (os_elem_tiles + 1),
-                           &fl->tickets[TK_DEPTH + p], fl, s);
+        uint32_t* lbp = depth_lb + (size_t)p * MAX_BINS * (os_elem_tiles + 1);
+        if (p < DEPTH_PASSES - 1)
+            onesweep<9, OS_KV>(dk[cur], dv[cur], dk[cur ^ 1], dv[cur ^ 1], Md, (uint32_t)count, DEPTH_BITS * p, 0, 32,
+                               hist_excl + p * MAX_BINS, lbp, &fl->tickets[TK_DEPTH + p], fl, s);
+        else
+            onesweep<8, OS_KV>(dk[cur], dv[cur], dk[cur ^ 1], dv[cur ^ 1], Md, (uint32_t)count, DEPTH_BITS * p, 0, 32,
+                               hist_excl + p * MAX_BINS, lbp, &fl->tickets[TK_DEPTH + p], fl, s, hist + p * MAX_BINS);
         cur ^= 1;
     }
     prof->end(s, DEPTH_PASSES + 1);

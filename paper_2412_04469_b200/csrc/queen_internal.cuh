@@ -54,7 +54,8 @@ struct CamBatch {
 // tile digits run after it on the duplicated entries:
 //   depth passes : 4 x 8 bits over the 31 depth bits of the M visible pairs
 //   tile passes  : ceil(gbits / TILE_DIGIT_BITS) x (8 or 9) bits over the K entries
-constexpr int DEPTH_PASSES = 4;
+constexpr int DEPTH_PASSES = 4;    // 3 x 9-bit digits of (depth - min depth), + bits 27..31
+constexpr int DEPTH_BITS = 9;
 constexpr int MAX_TILE_PASSES = 4;
 constexpr int MAX_BINS = 512;
 
@@ -98,7 +99,7 @@ inline BinPlan bin_plan(int64_t n_pad, int64_t n_views, int W, int H) {
 // Workspace carve-up (bytes, 256-aligned) for (n_pad, n_views, W, H, keys_cap).
 struct WsLayout {
     // scratch (bin_sort)
-    size_t flags, hist, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, counts, view_tot, slab_counts,
+    size_t flags, hist, dminmax, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, counts, view_tot, slab_counts,
         slab_vis, select, ans_table, total_scratch;
     // render_views / render_mask buffers
     size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, mask_tmp, total;
@@ -119,8 +120,9 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     size_t o = 0;
     L.flags = o; o += align256(sizeof(DevFlags));
     L.hist = o; o += align256(sizeof(uint32_t) * (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS * 2);
+    L.dminmax = o; o += align256(sizeof(uint32_t) * 2);
     L.dup_lb = o; o += align256(sizeof(unsigned long long) * (L.elem_tiles + 1));
-    L.depth_lb = o; o += align256(sizeof(uint32_t) * DEPTH_PASSES * 256 * (L.os_elem_tiles + 1));
+    L.depth_lb = o; o += align256(sizeof(uint32_t) * DEPTH_PASSES * MAX_BINS * (L.os_elem_tiles + 1));
     L.tile_lb = o; o += align256(sizeof(uint32_t) * MAX_TILE_PASSES * MAX_BINS * (L.os_key_tiles + 1));
     L.dkeys = o; o += align256(sizeof(uint32_t) * L.elems);
     L.dkeys_alt = o; o += align256(sizeof(uint32_t) * L.elems);
@@ -151,7 +153,8 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
 
 // every scratch region of `need` fits in the corresponding region of `have`
 inline bool scratch_fits(const WsLayout& need, const WsLayout& have) {
-    const size_t WsLayout::*r[] = {&WsLayout::flags,      &WsLayout::hist,        &WsLayout::dup_lb,
+    const size_t WsLayout::*r[] = {&WsLayout::flags,      &WsLayout::hist,        &WsLayout::dminmax,
+                                   &WsLayout::dup_lb,
                                    &WsLayout::depth_lb,   &WsLayout::tile_lb,     &WsLayout::dkeys,
                                    &WsLayout::dkeys_alt,  &WsLayout::dvals,       &WsLayout::dvals_alt,
                                    &WsLayout::counts,     &WsLayout::view_tot,    &WsLayout::slab_counts,

@@ -457,3 +457,25 @@ def test_cuda_graph_frame_equals_eager():
         assert torch.equal(graphed.planes, eager.planes)
         assert torch.equal(graphed.rgb, ref)
     assert graphed.check_status()[0] == 0
+
+
+def test_depth_keys_spanning_more_than_27_bits():
+    """Depth keys relative to the smallest depth: when the scene's depths span more than 2^27
+    float ulps (z from 0.3 to 1e6) the 4th depth pass (bits 27..31) is a real pass, otherwise a
+    copy; the sorted entries are bit-exact either way."""
+    from tests.gpu_helpers import Stages
+    rng = np.random.default_rng(17)
+    n = 3001
+    z = np.exp(rng.uniform(np.log(0.3), np.log(1e6), n))
+    pos = np.stack([rng.uniform(-0.5, 0.5, n) * z, rng.uniform(-0.4, 0.4, n) * z, z], 1)
+    scale = np.log(np.maximum(0.02 * z, 1e-3))[:, None].repeat(3, 1)
+    pl = planes_from(pos, rng.standard_normal((n, 4)), scale, rng.normal(1.0, 1.0, n), rng.normal(0, 0.5, (n, 1, 3)), 0)
+    cams = [synth.make_camera(np.eye(3), np.zeros(3), 200.0, 200.0, 320, 240)]
+    proj, bins, rgb, T = oracle.render(pl, n, 0, cams)
+    d = proj["depth"][0][proj["tiles"][0] > 0].astype(np.int64)
+    assert d.max() - d.min() >= (1 << 27)
+    st = Stages(pl, n, 0, cams).run()
+    gp = st.proj_np()
+    _check_proj(gp, proj, n)
+    _check_bins(st.bins_np(), bins, gp["depth"], st.T)
+    _check_image(*st.image_np(), rgb, T)
