@@ -406,7 +406,13 @@ def main():
     clocks = ClockSampler(local)
     if use_graph:
         player.profile_read(reset=True)
-        graphs = [player.capture(d, profile=not args.no_profile) for d in dps]  # N = 1: per packet
+        # N = 1: one graph per resident packet (at most one per timed step, so every graph's
+        # profiler events are last recorded inside the timed region); N > 1: one per slot
+        ng = len(dps) if world > 1 else max(1, min(len(dps), args.steps))
+        graphs = [player.capture(d, profile=not args.no_profile) for d in dps[:ng]]
+        player.planes.copy_(torch.from_numpy(sc.planes).to(dev))
+        for g in graphs:  # every graph replayed once before the warm-up proper
+            g.replay()
         player.planes.copy_(torch.from_numpy(sc.planes).to(dev))
         for t in range(args.warmup):
             bcast(t)
