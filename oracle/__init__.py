@@ -58,6 +58,7 @@ def lib():
             "oracle_ans_decode": (i32, [p, i64, i32, i32, i32, p]),
             "oracle_blend_counts": (None, [i32, i32, i32, i32, p, p, p, p, p, i32]),
             "oracle_contrib": (None, [i32, i32, i32, i32, p, p, p, p, p, p, p, i32]),
+            "oracle_rasterize_pixels_direct": (None, [i32, i32, i32, i32, p, p, p, p, p, i64, p, p, p, i32]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -344,3 +345,18 @@ def contributors(proj, bins, W: int, H: int, threads: int | None = None):
     lib().oracle_contrib(n_pad, V, W, H, _p(rec), _p(bins["ranges"]), _p(vals), _p(counts), _p(offsets), _p(gid),
                          _p(clamp), th)
     return offsets, gid[:offsets[-1]], clamp[:offsets[-1]]
+
+
+def rasterize_pixels_direct(proj, n: int, W: int, H: int, pix: np.ndarray, bg=(0.0, 0.0, 0.0),
+                            threads: int | None = None):
+    """Sampled pixels from the projection records alone (no binning; R13: tiled == brute
+    force).  pix int32 [npix][3] = (view, x, y).  Returns rgb [npix][3], T [npix]."""
+    rec = proj["rec"]
+    V, n_pad, _ = rec.shape
+    pix = np.ascontiguousarray(pix, np.int32)
+    rgb = np.zeros((pix.shape[0], 3), np.float32)
+    T = np.zeros(pix.shape[0], np.float32)
+    lib().oracle_rasterize_pixels_direct(n, n_pad, W, H, _p(rec), _p(proj["depth"]), _p(proj["tiles"]),
+                                         _p(proj["rect"]), _p(np.asarray(bg, np.float32)), pix.shape[0], _p(pix),
+                                         _p(rgb), _p(T), threads or default_threads())
+    return rgb, T

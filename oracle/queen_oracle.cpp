@@ -584,6 +584,38 @@ void oracle_blend_counts(int n_pad, int V, int W, int H, const float* rec, const
 }
 
 
+// Sampled pixels straight from the projection records, no binning: for pixel (v, x, y) every
+// Gaussian of view v whose tile rect contains the pixel's tile, ordered by (depth, index), then
+// the same compositing (blend_step).  By R#13 (tiled == brute force) this equals the tiled
+// rasterizer; it lets full-size configurations whose key lists are too large for oracle_bin be
+// checked pixel by pixel.  out: rgb [npix][3] (C + T bg), T [npix].
+void oracle_rasterize_pixels_direct(int n, int n_pad, int W, int H, const float* rec, const uint32_t* depth,
+                                    const uint32_t* tiles, const int16_t* rect, const float* bg, int64_t npix,
+                                    const int32_t* pix, float* rgb_out, float* T_out, int threads) {
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 1)
+    for (int64_t q = 0; q < npix; ++q) {
+        const int v = pix[3 * q], x = pix[3 * q + 1], y = pix[3 * q + 2];
+        const int tx = x >> 4, ty = y >> 4;
+        std::vector<std::pair<uint32_t, uint32_t>> list;
+        for (int i = 0; i < n; ++i) {
+            const int64_t o = (int64_t)v * n_pad + i;
+            if (!tiles[o]) continue;
+            const int16_t* r = rect + o * 4;
+            if (tx < r[0] || tx > r[2] || ty < r[1] || ty > r[3]) continue;
+            list.push_back({depth[o], (uint32_t)i});
+        }
+        std::sort(list.begin(), list.end());
+        float C[3] = {0.0f, 0.0f, 0.0f}, Tr = 1.0f;
+        for (auto& di : list) {
+            const float* rc = rec + ((int64_t)v * n_pad + di.second) * 12;
+            if (blend_step(rc, (float)x, (float)y, C, Tr)) break;
+        }
+        (void)W; (void)H;
+        for (int ch = 0; ch < 3; ++ch) rgb_out[3 * q + ch] = C[ch] + Tr * bg[ch];
+        T_out[q] = Tr;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // NEXT #4 support: the contributor list of every pixel -- the records a12 composites, in
 // order, up to and including the one after which T < 1e-4 -- with the 0.99-clamp decision,

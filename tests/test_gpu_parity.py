@@ -310,18 +310,19 @@ def test_wire_packet_roundtrip_apply():
 
 
 # ------------------------------------------------------------------ full-size configs (sampled)
-@pytest.mark.parametrize("name", ["n3dv", "immersive"])
+@pytest.mark.parametrize("name", ["n3dv", "immersive", "meetroom"])
 def test_full_size_frame_sampled(name):
-    """BASELINE configs at full size, in bench.py's launch configuration (Player, frame 1 applied):
-    SoA after apply bit-exact; projection records for all views bit-exact; bins bit-exact for the
-    first batch; 4096 sampled pixels per view within tolerance."""
+    """BASELINE configs at full size, in bench.py's launch configuration (Player with bench's
+    views per batch, frame 1 applied): SoA after apply bit-exact; projection records for all
+    views bit-exact; bins bit-exact for the first batch; 4096 sampled pixels per view within
+    tolerance."""
+    import bench
     from paper_2412_04469_b200.runtime import Player, device_packet
     cfg = synth.get_config(name)
     sc = synth.make_scene(cfg)
     cams = synth.make_cameras(cfg)
     pkt = synth.make_packet(sc, 1)
-    vpb = 10 if name == "n3dv" else 8
-    pl = Player(sc.planes, sc.n, sc.deg, cams, views_per_batch=vpb)
+    pl = Player(sc.planes, sc.n, sc.deg, cams, views_per_batch=min(len(cams), bench.default_vpb(cfg)))
     pl.apply(device_packet(pkt, pl.dev))
     A1, st, _ = oracle.apply(sc.planes, pkt)
     assert np.array_equal(pl.planes.cpu().numpy(), A1)
@@ -331,25 +332,81 @@ def test_full_size_frame_sampled(name):
     assert s == 0
     W, H = cams[0].width, cams[0].height
     rng = np.random.default_rng(5)
-    for b0 in range(0, len(cams), vpb):
-        bc = cams[b0:b0 + vpb]
+    for bi, (a, b) in enumerate(pl.batches):
+        bc = cams[a:b]
         proj = oracle.project(A1, sc.n, sc.deg, bc)
-        bins = oracle.bin_sort(proj, W, H) if b0 == 0 else None
-        if b0 == 0:
+        bins = oracle.bin_sort(proj, W, H)
+        if bi == 0:
             from tests.gpu_helpers import Stages
             stg = Stages(A1, sc.n, sc.deg, bc, keys_cap=pl.keys_cap).project().bin_sort()
             gp = stg.proj_np()
             _check_proj(gp, proj, sc.n)
             _check_bins(stg.bins_np(), bins, gp["depth"], stg.T)
             del stg
-        else:
-            bins = oracle.bin_sort(proj, W, H)
         V = len(bc)
         pix = np.stack([np.repeat(np.arange(V), 4096), rng.integers(0, W, V * 4096), rng.integers(0, H, V * 4096)], 1)
         orgb, oT = oracle.rasterize_pixels(proj["rec"], bins["ranges"], bins["vals"], W, H, pix)
-        g = rgb[b0 + pix[:, 0], :, pix[:, 2], pix[:, 1]]
+        g = rgb[a + pix[:, 0], :, pix[:, 2], pix[:, 1]]
         assert np.abs(np.clip(g, 0, 1) - np.clip(orgb, 0, 1)).max() <= RGB_TOL
         del proj, bins
+
+
+def test_full_size_stress_sampled():
+    """BASELINE configs[4] (3 M Gaussians, 64 views at 3840x2160) at full size in bench.py's
+    launch configuration: SoA after apply bit-exact; the first batch's projection records
+    bit-exact; its binning checked by properties (K = sum of tiles touched, ranges tile the
+    entries, every entry's Gaussian touches its tile, per-tile lists in (depth, index) order);
+    256 sampled pixels of each of the batch's views against the oracle composited straight from
+    the records (no binning, R13)."""
+    import bench
+    from paper_2412_04469_b200.runtime import Player, device_packet
+    from tests.gpu_helpers import Stages
+    cfg = synth.get_config("stress")
+    sc = synth.make_scene(cfg)
+    cams = synth.make_cameras(cfg)
+    pkt = synth.make_packet(sc, 1)
+    vpb = min(len(cams), bench.default_vpb(cfg))
+    pl = Player(sc.planes, sc.n, sc.deg, cams, views_per_batch=vpb)
+    pl.apply(device_packet(pkt, pl.dev))
+    A1, st, _ = oracle.apply(sc.planes, pkt)
+    assert np.array_equal(pl.planes.cpu().numpy(), A1)
+    pl.fit_capacity()
+    rgb = pl.render()
+    s, _ = pl.check_status()
+    assert s == 0
+    W, H = cams[0].width, cams[0].height
+    a, b = pl.batches[0]
+    bc = cams[a:b]
+    proj = oracle.project(A1, sc.n, sc.deg, bc)
+    stg = Stages(A1, sc.n, sc.deg, bc, keys_cap=pl.keys_cap).project().bin_sort()
+    gp = stg.proj_np()
+    _check_proj(gp, proj, sc.n)
+    gb = stg.bins_np()
+    tiles = proj["tiles"].astype(np.int64)
+    assert gb["K"] == int(tiles.sum())
+    lens = gb["ranges"][:, 1].astype(np.int64) - gb["ranges"][:, 0].astype(np.int64)
+    assert lens.sum() == gb["K"] and np.all(gb["ranges"][1:, 0][lens[1:] > 0] >= gb["ranges"][:-1, 1][lens[1:] > 0])
+    gt = gb["keys"].astype(np.int64)
+    v = gt // stg.T
+    t = gt % stg.T
+    gx = (W + 15) // 16
+    r = proj["rect"][v, gb["vals"]]
+    tx, ty = t % gx, t // gx
+    assert np.all((tx >= r[:, 0]) & (tx <= r[:, 2]) & (ty >= r[:, 1]) & (ty <= r[:, 3]))
+    full = (gt.astype(np.uint64) << np.uint64(32)) | (proj["depth"][v, gb["vals"]].astype(np.uint64) << np.uint64(0))
+    same = gt[1:] == gt[:-1]
+    k2 = full * np.uint64(1)  # (gt, depth) then index: check non-decreasing (gt, depth, index)
+    prev, nxt = k2[:-1], k2[1:]
+    ordered = (nxt > prev) | ((nxt == prev) & (gb["vals"][1:] > gb["vals"][:-1]))
+    assert np.all(ordered | ~same)
+    del stg, gb, full, k2, prev, nxt, ordered, same
+    rng = np.random.default_rng(8)
+    V = len(bc)
+    pix = np.stack([np.repeat(np.arange(V), 256), rng.integers(0, W, V * 256), rng.integers(0, H, V * 256)], 1)
+    orgb, oT = oracle.rasterize_pixels_direct(proj, sc.n, W, H, pix)
+    g = rgb[a + torch.from_numpy(pix[:, 0]).cuda(), :, torch.from_numpy(pix[:, 2]).cuda(),
+            torch.from_numpy(pix[:, 1]).cuda()].cpu().numpy()
+    assert np.abs(np.clip(g, 0, 1) - np.clip(orgb, 0, 1)).max() <= RGB_TOL
 
 
 # ------------------------------------------------------------------ blend work (culling is exact)
