@@ -199,15 +199,29 @@ def library_sort_comparison(stg, bnp, dev, reps: int = 5):
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) timing
-def time_oracle_frame(cfg, scene_planes, n, deg, cams, pkt, views_sample: int):
-    """The oracle as it stands (test infrastructure), on the host cores: apply + render of a
-    bounded sample of views; returns (seconds per full frame, detail)."""
+def time_oracle_frame(cfg, scene_planes, n, deg, cams, pkt, views_sample: int, entropy: bool = True):
+    """The oracle as it stands (test infrastructure), on the host cores: (entropy decode of the
+    latents +) apply + render of a bounded sample of views; returns (seconds per full frame,
+    detail)."""
+    import dataclasses
+
     import oracle
     oracle.build()
     threads = os.cpu_count() or 1
+    t_dec = 0.0
+    if entropy:
+        row, streams = 0, []
+        for c in range(5):
+            L = pkt.lat[c]
+            streams.append((oracle.ans_encode(pkt.latents[row:row + L], pkt.n), L) if L else None)
+            row += L
+        t0 = time.perf_counter()
+        rows = [oracle.ans_decode(st_, L, pkt.n, pkt.n_pad)[0] for st_, L in (x for x in streams if x)]
+        t_dec = time.perf_counter() - t0
+        pkt = dataclasses.replace(pkt, latents=np.concatenate(rows, 0))
     t0 = time.perf_counter()
     A1, st, _ = oracle.apply(scene_planes, pkt)
-    t_apply = time.perf_counter() - t0
+    t_apply = time.perf_counter() - t0 + t_dec
     ts = []
     for v in range(views_sample):
         t0 = time.perf_counter()
@@ -232,10 +246,36 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     planes = sc.planes
     times = []
+    entropy = args.packet_format == "entropy"
+    npk = max(1, args.packets)
+    pkts = [synth.make_packet(sc, 1 + j) for j in range(min(npk, args.warmup + args.steps))]
+    streams = []
+    if entropy:  # the arm decodes the same entropy-coded latents the GPU arm decodes (outside: encoding)
+        for p in pkts:
+            row, st_ = 0, []
+            for c in range(5):
+                L = p.lat[c]
+                st_.append(oracle.ans_encode(p.latents[row:row + L], p.n) if L else None)
+                row += L
+            streams.append(st_)
+
+    def decode(j):
+        p = pkts[j]
+        if not entropy:
+            return p
+        rows = []
+        for c in range(5):
+            if streams[j][c] is not None:
+                lat, s_ = oracle.ans_decode(streams[j][c], p.lat[c], p.n, p.n_pad)
+                rows.append(lat)
+        import dataclasses
+        return dataclasses.replace(p, latents=np.concatenate(rows, 0) if rows else p.latents)
+
     for step in range(args.warmup + args.steps):
-        pkt = synth.make_packet(sc, 1 + step % max(1, args.packets))
+        j = step % len(pkts)
         v = step % V
         t0 = time.perf_counter()
+        pkt = decode(j)
         planes, st, _ = oracle.apply(planes, pkt)
         oracle.render(planes, sc.n, sc.deg, [cams[v]], threads=threads)
         dt = time.perf_counter() - t0
@@ -244,7 +284,7 @@ def run_reference(args):
             times.append(dt)
     # apply share measured separately once to scale views correctly
     t0 = time.perf_counter()
-    oracle.apply(planes, synth.make_packet(sc, 1))
+    oracle.apply(planes, decode(0))
     t_apply = time.perf_counter() - t0
     frame_s = [t_apply + V * max(t - t_apply, 1e-9) for t in times]
     value = 1.0 / statistics.mean(frame_s)
@@ -256,8 +296,8 @@ def run_reference(args):
                    "width": W, "height": H, "sh_degree": cfg.deg},
         "mpixel_per_s": value * V * W * H / 1e6,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": f"per step: apply of one frame packet + render of 1 of {V} views on the host "
-                                   f"cores; frame time = apply + {V} x view time"},
+                         "sample": f"per step: {'entropy decode + ' if entropy else ''}apply of one frame packet + render "
+                                   f"of 1 of {V} views on the host cores; frame time = decode + apply + {V} x view time"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -723,9 +763,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nview = min(V, 1 if cfg.n * cfg.width * cfg.height > 1e11 else 2)
-        frame_s, det = time_oracle_frame(cfg, sc.planes, sc.n, sc.deg, cams_all, host_pkts[0], nview)
+        frame_s, det = time_oracle_frame(cfg, sc.planes, sc.n, sc.deg, cams_all, host_pkts[0], nview,
+                                         entropy=args.packet_format == "entropy")
         cpu = {"value": 1.0 / frame_s, "unit": UNIT, "cores": det["threads"], "kind": "oracle",
-               "sample": f"apply of frame 1 (all {sc.n} Gaussians) + render of {nview} of {V} views at "
+               "sample": f"{'entropy decode + ' if args.packet_format == 'entropy' else ''}apply of frame 1 "
+                         f"(all {sc.n} Gaussians) + render of {nview} of {V} views at "
                          f"{W}x{H} on {det['threads']} host threads; frame time = apply ({det['t_apply']:.2f} s) "
                          f"+ {V} x mean view time ({det['t_view']:.2f} s)"}
 
