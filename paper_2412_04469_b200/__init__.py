@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqueen.so")
+# QUEEN_LIB_PATH: load an experiment build (tools/variants.py) instead of the in-tree library
+LIB_PATH = os.environ.get("QUEEN_LIB_PATH") or os.path.join(_HERE, "libqueen.so")
 
 QUEEN_OK = 0
 QUEEN_WARN_NONFINITE = 1

@@ -52,7 +52,10 @@ __device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
 constexpr unsigned long long SCAN_AGG = 1ull << 62, SCAN_INC = 2ull << 62, SCAN_MASK = (1ull << 62) - 1;
 constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_MASK = (1u << 30) - 1;
 constexpr long long SPIN_LIMIT = 1ll << 24;
-constexpr int LB_BATCH = 8;  // onesweep look-back predecessors loaded per round trip
+#ifndef QUEEN_LB_BATCH
+#define QUEEN_LB_BATCH 8
+#endif
+constexpr int LB_BATCH = QUEEN_LB_BATCH;  // onesweep look-back predecessors loaded per round trip
 constexpr int SORT_WARPS = SORT_THREADS / 32;
 
 enum : int { TK_DEPTH = 0, TK_TILE = 4, TK_VIS = 8, TK_DUP = 9 };

@@ -41,7 +41,13 @@ constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 16;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 constexpr int REC_WORDS = 12;
-constexpr int OS_THREADS = 512, OS_ITEMS = 8;         // onesweep pass CTA shape
+#ifndef QUEEN_OS_THREADS
+#define QUEEN_OS_THREADS 512
+#endif
+#ifndef QUEEN_OS_ITEMS
+#define QUEEN_OS_ITEMS 8
+#endif
+constexpr int OS_THREADS = QUEEN_OS_THREADS, OS_ITEMS = QUEEN_OS_ITEMS;  // onesweep pass CTA shape
 constexpr int OS_TILE = OS_THREADS * OS_ITEMS;         // keys per onesweep tile
 constexpr int64_t MAX_KEYS = (1ll << 30) - 1;  // look-back packs 30-bit counts
 

@@ -329,7 +329,10 @@ cudaError_t launch_blend_counts(const float* rec, int n_pad, const uint32_t* ran
     cudaMemsetAsync(evaluated, 0, sizeof(long long) * n_views, s);
     cudaMemsetAsync(composited, 0, sizeof(long long) * n_views, s);
     if (blocks == 0) return cudaSuccess;
-    k_blend<true, BLEND_RPT, false><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
+#ifndef QUEEN_COUNT_WMASK
+#define QUEEN_COUNT_WMASK false  // experiment knob: count only the records on the warp lists
+#endif
+    k_blend<true, BLEND_RPT, QUEEN_COUNT_WMASK><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
                                                   reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, 0.f, 0.f, 0.f,
                                                   nullptr, nullptr, nullptr, OUT_F32, 0.f, evaluated, composited);
     return cudaGetLastError();
