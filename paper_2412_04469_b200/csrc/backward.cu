@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
     __shared__ float4 sA[BW_BATCH], sB[BW_BATCH], sC[BW_BATCH];
     __shared__ uint32_t sI[BW_BATCH];
     __shared__ int s_jmax[BW_NT / 32];
+    __shared__ uint8_t s_list[BW_NT / 32][BW_BATCH];
     const int gt = blockIdx.x;
     const int v = gt / T;
     const int t = gt - v * T;
@@ -57,10 +58,17 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
         Tf[r] = (px < W && py0 + r < H) ? 1.0f : 0.0f;  // off-image pixels start terminated
         last[r] = -1;
     }
-    // ---- phase A: replay the forward (same fp32 operations as k_blend / the oracle)
+    // ---- phase A: replay the forward (same fp32 operations as k_blend / the oracle), with the
+    // forward's skips: the CTA stops once every pixel has terminated, and each warp visits only
+    // the batch records whose alpha >= 1/255 ellipse reaches its 16 x 8 sub-tile (touches());
+    // skipped records hit none of the warp's pixels, so T and the last contributor are unchanged
+    const unsigned lane_lt = (1u << (threadIdx.x & 31)) - 1u;
     for (int b0 = rs; b0 < re; b0 += BW_BATCH) {
         const int cnt = min(BW_BATCH, re - b0);
-        __syncthreads();
+        bool alive = false;
+#pragma unroll
+        for (int r = 0; r < BW_RPT; ++r) alive |= !(Tf[r] < 1e-4f);
+        if (__syncthreads_count(alive) == 0) break;
         for (int q = threadIdx.x; q < cnt; q += BW_NT) {
             const float4* g = vrec + (int64_t)vals[b0 + q] * 3;
             sA[q] = g[0];
@@ -68,7 +76,20 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
             sC[q] = g[2];
         }
         __syncthreads();
-        for (int q = 0; q < cnt; ++q) {
+        if (!__any_sync(0xffffffffu, alive)) continue;
+        uint8_t* lst = s_list[threadIdx.x >> 5];
+        int nq = 0;
+#pragma unroll
+        for (int e2 = 0; e2 < BW_BATCH / 32; ++e2) {
+            const int q = (int)(threadIdx.x & 31) + 32 * e2;
+            const bool want = q < cnt && touches(sA[q], sB[q], wx0, wx0 + 15.0f, wy0, wy0 + 7.0f);
+            const unsigned bal = __ballot_sync(0xffffffffu, want);
+            if (want) lst[nq + __popc(bal & lane_lt)] = (uint8_t)q;
+            nq += __popc(bal);
+        }
+        __syncwarp();
+        for (int i = 0; i < nq; ++i) {
+            const int q = lst[i];
             const float4 a = sA[q], bq = sB[q];
             const float dx = a.x - fx;
             const float tAdx = (bq.x * dx) * dx, tB = bq.y * dx;
@@ -89,6 +110,7 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
 #pragma unroll
     for (int r = 0; r < BW_RPT; ++r) jmax = max(jmax, last[r]);
     for (int o = 16; o > 0; o >>= 1) jmax = max(jmax, __shfl_xor_sync(0xffffffffu, jmax, o));
+    const int wjmax = jmax;  // this warp's last contributor: later records hit none of its pixels
     if ((threadIdx.x & 31) == 0) s_jmax[threadIdx.x >> 5] = jmax;
     __syncthreads();
     jmax = max(s_jmax[0], s_jmax[1]);
@@ -125,7 +147,7 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
 #pragma unroll
         for (int e2 = 0; e2 < BW_BATCH / 32; ++e2) {
             const int q = (int)(threadIdx.x & 31) + 32 * e2;
-            const bool want = q < cnt && touches(sA[q], sB[q], wx0, wx0 + 15.0f, wy0, wy0 + 7.0f);
+            const bool want = q < cnt && b0 + q <= wjmax && touches(sA[q], sB[q], wx0, wx0 + 15.0f, wy0, wy0 + 7.0f);
             wmask |= (unsigned long long)__ballot_sync(0xffffffffu, want) << (32 * e2);
         }
         while (wmask) {

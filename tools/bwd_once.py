@@ -19,3 +19,10 @@ for _ in range(2):
     Q.queen_rasterize_backward(st.ctx, st.proj, st.bins, cams, g, grec)
 torch.cuda.synchronize()
 print("status", st.ctx.check_status())
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(3):
+    Q.queen_rasterize_backward(st.ctx, st.proj, st.bins, cams, g, grec)
+e1.record()
+torch.cuda.synchronize()
+print("rasterize_backward ms", e0.elapsed_time(e1) / 3)
