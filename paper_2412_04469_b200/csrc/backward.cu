@@ -23,6 +23,12 @@
 
 namespace queen {
 
+__device__ __forceinline__ float rcpa(float x) {  // MUFU.RCP without the denormal fix-up (|x| >= 0.01 here)
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float ex2b(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -115,19 +121,33 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
     __syncthreads();
     jmax = max(s_jmax[0], s_jmax[1]);
     const int64_t plane = (int64_t)H * W;
-    float g[BW_RPT][3], S[BW_RPT][3], Tc[BW_RPT];
-#pragma unroll
-    for (int r = 0; r < BW_RPT; ++r) {
-        const bool in = px < W && py0 + r < H;
-        const int64_t pix = (int64_t)v * 3 * plane + (int64_t)(py0 + r) * W + px;
-        g[r][0] = in ? gout[pix] : 0.f;
-        g[r][1] = in ? gout[pix + plane] : 0.f;
-        g[r][2] = in ? gout[pix + 2 * plane] : 0.f;
-        S[r][0] = S[r][1] = S[r][2] = 0.f;
-        Tc[r] = Tf[r];
-    }
+    // Per row pair (paired FP32 ops, as in the forward): the image gradient g, the colour behind
+    // each record plus the background term Sb = S_i + T_N bg (S_i = colour composited after i),
+    // and the running transmittance Tc (T_i = T_{i+1} / (1 - a_i)).
+    constexpr int NP = BW_RPT / 2;
+    float2 g2[NP][3], Sb[NP][3], Tc[NP], nfy[NP];
     const float bgc[3] = {bg0, bg1, bg2};
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        float gg[2][3];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int r = 2 * k + h;
+            const bool in = px < W && py0 + r < H;
+            const int64_t pix = (int64_t)v * 3 * plane + (int64_t)(py0 + r) * W + px;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) gg[h][ch] = in ? gout[pix + ch * plane] : 0.f;
+        }
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+            g2[k][ch] = make_float2(gg[0][ch], gg[1][ch]);
+            Sb[k][ch] = make_float2(Tf[2 * k] * bgc[ch], Tf[2 * k + 1] * bgc[ch]);
+        }
+        Tc[k] = make_float2(Tf[2 * k], Tf[2 * k + 1]);
+        nfy[k] = make_float2(-(float)(py0 + 2 * k), -(float)(py0 + 2 * k + 1));
+    }
     const float LN2 = 0.69314718055994531f;
+    const float NEG_INF = __int_as_float(0xff800000);
     for (int bend = jmax + 1; bend > rs; bend -= BW_BATCH) {
         const int b0 = max(rs, bend - BW_BATCH);
         const int cnt = bend - b0;
@@ -157,47 +177,62 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
             const float4 a = sA[q], bq = sB[q], c = sC[q];
             const float dx = a.x - fx;
             const float tAdx = (bq.x * dx) * dx, tB = bq.y * dx;
-            float acc[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // u v A2 B2 C2 o r g b
+            const float2 vv = make_float2(a.y, a.y), cc = make_float2(bq.z, bq.z);
+            const float2 ta2 = make_float2(tAdx, tAdx), tb2 = make_float2(tB, tB);
+            const float2 o2 = make_float2(c.x, c.x);
+            const float2 col[3] = {make_float2(c.y, c.y), make_float2(c.z, c.z), make_float2(c.w, c.w)};
+            // pair accumulators: colour r g b, opacity, and the moments of dp2 (1, dy, dy^2)
+            float2 aC[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            float2 aO = make_float2(0.f, 0.f), m0 = aO, m1 = aO, m2 = aO;
             bool any = false;
 #pragma unroll
-            for (int r = 0; r < BW_RPT; ++r) {
-                if (j > last[r]) continue;
-                const float dy = a.y - (float)(py0 + r);
-                const float p2 = fmaf(fmaf(bq.z, dy, tB), dy, tAdx);
-                if (p2 > 0.0f || p2 < bq.w) continue;
+            for (int k = 0; k < NP; ++k) {
+                const bool l0 = j <= last[2 * k], l1 = j <= last[2 * k + 1];
+                if (!(l0 | l1)) continue;
+                const float2 dy = __fadd2_rn(vv, nfy[k]);
+                const float2 p2 = __ffma2_rn(__ffma2_rn(cc, dy, tb2), dy, ta2);
+                const bool h0 = l0 && !(p2.x > 0.0f || p2.x < bq.w);
+                const bool h1 = l1 && !(p2.y > 0.0f || p2.y < bq.w);
+                if (!(h0 | h1)) continue;
                 any = true;
-                const float e = ex2b(p2);
-                const float raw = c.x * e;
-                const float alpha = fminf(0.99f, raw);
-                const float iom = __fdividef(1.0f, 1.0f - alpha);  // 1 - alpha >= 0.01
-                const float Ti = Tc[r] * iom;
-                const float w = alpha * Ti;
-                const float col[3] = {c.y, c.z, c.w};
-                float dal = 0.f;
+                // a non-hit lane of the pair runs with a = 0: T, Sb and every sum stay unchanged
+                const float2 e = make_float2(ex2b(h0 ? p2.x : NEG_INF), ex2b(h1 ? p2.y : NEG_INF));
+                const float2 raw = __fmul2_rn(o2, e);
+                const float2 al = make_float2(fminf(0.99f, raw.x), fminf(0.99f, raw.y));
+                const float2 om = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y));
+                const float2 niom = make_float2(-rcpa(om.x), -rcpa(om.y));  // 1 - a >= 0.01
+                const float2 Ti = __fmul2_rn(Tc[k], make_float2(-niom.x, -niom.y));
+                const float2 w = __fmul2_rn(al, Ti);
+                float2 dal = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) {
-                    acc[6 + ch] = fmaf(w, g[r][ch], acc[6 + ch]);
-                    dal = fmaf(g[r][ch], fmaf(col[ch], Ti, -(S[r][ch] + Tf[r] * bgc[ch]) * iom), dal);
-                    S[r][ch] = fmaf(col[ch], w, S[r][ch]);
+                    // dL/da = sum_ch g (c T_i - Sb / (1 - a))
+                    dal = __ffma2_rn(g2[k][ch], __ffma2_rn(col[ch], Ti, __fmul2_rn(Sb[k][ch], niom)), dal);
+                    Sb[k][ch] = __ffma2_rn(col[ch], w, Sb[k][ch]);
+                    aC[ch] = __ffma2_rn(w, g2[k][ch], aC[ch]);
                 }
-                Tc[r] = Ti;
-                if (raw <= 0.99f) {  // unclamped: a = o 2^p2
-                    acc[5] = fmaf(dal, e, acc[5]);
-                    const float dp2 = dal * alpha * LN2;
-                    // moments of dp2; (u, v, A2, B2, C2) gradients are formed from them per record
-                    acc[0] += dp2;            // sum dp2          (x dx: dx is this lane's constant)
-                    acc[1] += dp2 * dy;       // sum dp2 dy
-                    acc[2] += dp2 * dy * dy;  // sum dp2 dy^2
-                }
+                Tc[k] = Ti;
+                // unclamped hits only: a = o 2^p2
+                const float2 dm = make_float2(h0 && raw.x <= 0.99f ? dal.x : 0.f, h1 && raw.y <= 0.99f ? dal.y : 0.f);
+                aO = __ffma2_rn(dm, e, aO);
+                const float2 dp2 = __fmul2_rn(__fmul2_rn(dm, al), make_float2(LN2, LN2));
+                m0 = __fadd2_rn(m0, dp2);
+                const float2 t = __fmul2_rn(dp2, dy);
+                m1 = __fadd2_rn(m1, t);
+                m2 = __ffma2_rn(t, dy, m2);
             }
             if (!__any_sync(0xffffffffu, any)) continue;
+            float acc[9];
             {  // per lane: u, v, A2, B2, C2 from the moments (dx constant over the lane's rows)
-                const float s0 = acc[0], s1 = acc[1], s2 = acc[2];
+                const float s0 = m0.x + m0.y, s1 = m1.x + m1.y, s2 = m2.x + m2.y;
                 acc[0] = 2.0f * bq.x * dx * s0 + bq.y * s1;  // d/du = sum dp2 (2 A2 dx + B2 dy)
                 acc[1] = bq.y * dx * s0 + 2.0f * bq.z * s1;  // d/dv = sum dp2 (B2 dx + 2 C2 dy)
                 acc[2] = dx * dx * s0;                        // d/dA2
                 acc[3] = dx * s1;                             // d/dB2
                 acc[4] = s2;                                  // d/dC2
+                acc[5] = aO.x + aO.y;
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) acc[6 + ch] = aC[ch].x + aC[ch].y;
             }
             // warp reduce-scatter of the 9 (padded to 16) sums: 8 + 4 + 2 + 1 + 1 shuffles; lane l
             // ends with the total of value l >> 1, and lanes 0, 2, .., 16 add them (one atomic each)
