@@ -64,6 +64,14 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
         Tf[r] = (px < W && py0 + r < H) ? 1.0f : 0.0f;  // off-image pixels start terminated
         last[r] = -1;
     }
+    constexpr int NP = BW_RPT / 2;
+    const float NEG_INF = __int_as_float(0xff800000);
+    float2 TA[NP], nfy[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        TA[k] = make_float2(Tf[2 * k], Tf[2 * k + 1]);
+        nfy[k] = make_float2(-(float)(py0 + 2 * k), -(float)(py0 + 2 * k + 1));
+    }
     // ---- phase A: replay the forward (same fp32 operations as k_blend / the oracle), with the
     // forward's skips: the CTA stops once every pixel has terminated, and each warp visits only
     // the batch records whose alpha >= 1/255 ellipse reaches its 16 x 8 sub-tile (touches());
@@ -73,7 +81,7 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
         const int cnt = min(BW_BATCH, re - b0);
         bool alive = false;
 #pragma unroll
-        for (int r = 0; r < BW_RPT; ++r) alive |= !(Tf[r] < 1e-4f);
+        for (int k = 0; k < NP; ++k) alive |= !(TA[k].x < 1e-4f) | !(TA[k].y < 1e-4f);
         if (__syncthreads_count(alive) == 0) break;
         for (int q = threadIdx.x; q < cnt; q += BW_NT) {
             const float4* g = vrec + (int64_t)vals[b0 + q] * 3;
@@ -94,22 +102,34 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
             nq += __popc(bal);
         }
         __syncwarp();
-        for (int i = 0; i < nq; ++i) {
+        for (int i = 0; i < nq; ++i) {  // the forward's paired row arithmetic, lane for lane
             const int q = lst[i];
             const float4 a = sA[q], bq = sB[q];
             const float dx = a.x - fx;
             const float tAdx = (bq.x * dx) * dx, tB = bq.y * dx;
+            const float2 vv = make_float2(a.y, a.y), cc = make_float2(bq.z, bq.z);
+            const float2 ta2 = make_float2(tAdx, tAdx), tb2 = make_float2(tB, tB);
 #pragma unroll
-            for (int r = 0; r < BW_RPT; ++r) {
-                if (Tf[r] < 1e-4f) continue;
-                const float dy = a.y - (float)(py0 + r);
-                const float p2 = fmaf(fmaf(bq.z, dy, tB), dy, tAdx);
-                if (p2 > 0.0f || p2 < bq.w) continue;
-                const float alpha = fminf(0.99f, sC[q].x * ex2b(p2));
-                Tf[r] = Tf[r] * (1.0f - alpha);
-                last[r] = b0 + q;
+            for (int k = 0; k < NP; ++k) {
+                const float2 dy = __fadd2_rn(vv, nfy[k]);
+                const float2 p2 = __ffma2_rn(__ffma2_rn(cc, dy, tb2), dy, ta2);
+                const bool h0 = !(TA[k].x < 1e-4f) && !(p2.x > 0.0f) && !(p2.x < bq.w);
+                const bool h1 = !(TA[k].y < 1e-4f) && !(p2.y > 0.0f) && !(p2.y < bq.w);
+                if (!(h0 | h1)) continue;
+                const float o = sC[q].x;
+                const float2 e = make_float2(ex2b(h0 ? p2.x : NEG_INF), ex2b(h1 ? p2.y : NEG_INF));
+                float2 al = __fmul2_rn(make_float2(o, o), e);
+                al = make_float2(fminf(0.99f, al.x), fminf(0.99f, al.y));
+                TA[k] = __fmul2_rn(TA[k], __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
+                if (h0) last[2 * k] = b0 + q;
+                if (h1) last[2 * k + 1] = b0 + q;
             }
         }
+    }
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        Tf[2 * k] = TA[k].x;
+        Tf[2 * k + 1] = TA[k].y;
     }
     // ---- phase B: reverse walk
     int jmax = -1;
@@ -124,8 +144,7 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
     // Per row pair (paired FP32 ops, as in the forward): the image gradient g, the colour behind
     // each record plus the background term Sb = S_i + T_N bg (S_i = colour composited after i),
     // and the running transmittance Tc (T_i = T_{i+1} / (1 - a_i)).
-    constexpr int NP = BW_RPT / 2;
-    float2 g2[NP][3], Sb[NP][3], Tc[NP], nfy[NP];
+    float2 g2[NP][3], Sb[NP][3], Tc[NP];
     const float bgc[3] = {bg0, bg1, bg2};
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
@@ -144,10 +163,8 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
             Sb[k][ch] = make_float2(Tf[2 * k] * bgc[ch], Tf[2 * k + 1] * bgc[ch]);
         }
         Tc[k] = make_float2(Tf[2 * k], Tf[2 * k + 1]);
-        nfy[k] = make_float2(-(float)(py0 + 2 * k), -(float)(py0 + 2 * k + 1));
     }
     const float LN2 = 0.69314718055994531f;
-    const float NEG_INF = __int_as_float(0xff800000);
     for (int bend = jmax + 1; bend > rs; bend -= BW_BATCH) {
         const int b0 = max(rs, bend - BW_BATCH);
         const int cnt = bend - b0;
