@@ -193,7 +193,10 @@ queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_
                             queen_bins* bins, void* stream);
 /* queen_rasterize: a12, Eq. 2: per pixel front-to-back over its tile's
  * range; skip a < 1/255 (p2 < T2), a = min(0.99, o 2^p2), stop after T < 1e-4.
- * rgb_out fp32 [n_views][3][H][W] = C + T bg;  T_out (nullable) fp32 [n_views][H][W]. */
+ * rgb_out fp32 [n_views][3][H][W] = C + T bg;  T_out (nullable) fp32 [n_views][H][W].
+ * When the context's workspace covers n_views x tiles, its scratch holds the blend schedule
+ * (tiles launched longest list first; also used by queen_render_mask and
+ * queen_rasterize_backward); otherwise tiles run in grid order.  Output is identical. */
 queen_status queen_rasterize(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins, const queen_camera* cams,
                              int32_t n_views, const float bg[3], float* rgb_out, float* T_out, void* stream);
 /* queen_render_views: project + bin_sort + rasterize with proj/bins carved from the

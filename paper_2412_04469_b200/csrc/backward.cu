@@ -42,12 +42,13 @@ constexpr int BW_BATCH = 64;
 __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ rec, int n_pad,
                                                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
                                                      int W, int H, int gx, int T, float bg0, float bg1, float bg2,
-                                                     const float* __restrict__ gout, float* __restrict__ grec) {
+                                                     const float* __restrict__ gout, float* __restrict__ grec,
+                                                     const uint32_t* __restrict__ order) {
     __shared__ float4 sA[BW_BATCH], sB[BW_BATCH], sC[BW_BATCH];
     __shared__ uint32_t sI[BW_BATCH];
     __shared__ int s_jmax[BW_NT / 32];
     __shared__ uint8_t s_list[BW_NT / 32][BW_BATCH];
-    const int gt = blockIdx.x;
+    const int gt = order ? (int)order[blockIdx.x] : (int)blockIdx.x;
     const int v = gt / T;
     const int t = gt - v * T;
     const int px = (t % gx) * 16 + (threadIdx.x & 15);
@@ -508,16 +509,18 @@ __global__ void __launch_bounds__(128) k_project_bwd(const float* __restrict__ p
 
 cudaError_t launch_blend_bwd(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, const float* gout, float* grec,
-                             cudaStream_t s) {
+                             uint32_t* order_ws, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(grec, 0, sizeof(float) * 9 * (size_t)n_views * n_pad, s);
     if (e) return e;
     const int gx = (W + 15) / 16, gy = (H + 15) / 16;
     const int T = gx * gy;
     const int64_t blocks = (int64_t)T * n_views;
     if (blocks == 0) return cudaSuccess;
+    const uint32_t* order = nullptr;  // longest tile lists first (the forward's schedule)
+    if ((e = launch_tile_order(ranges, blocks, order_ws, s, &order))) return e;
     k_blend_bwd<<<(unsigned)blocks, BW_NT, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
                                                    reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0, bg1,
-                                                   bg2, gout, grec);
+                                                   bg2, gout, grec, order);
     return cudaGetLastError();
 }
 

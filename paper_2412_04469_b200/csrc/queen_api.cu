@@ -264,6 +264,14 @@ queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_
     return QUEEN_OK;
 }
 
+// workspace scratch for the blend schedule (tile order), if the workspace covers this call
+static uint32_t* order_scratch(queen_ctx* ctx, int32_t n_views, int W, int H) {
+    if (!ctx->ws) return nullptr;
+    const int64_t T = (int64_t)((W + 15) / 16) * ((H + 15) / 16);
+    if ((int64_t)n_views * T > (int64_t)ctx->ws_views * ctx->L.T) return nullptr;
+    return reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(ctx->ws) + ctx->L.order);
+}
+
 static queen_status rasterize_impl(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
                                    const queen_camera* cams, int32_t n_views, const float bg[3], float* rgb_out,
                                    float* T_out, uint8_t* rgb8_out, void* stream) {
@@ -272,10 +280,12 @@ static queen_status rasterize_impl(queen_ctx* ctx, const queen_proj* proj, const
     if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
     const uint32_t* vals = bins->sorted_in_alt ? bins->vals_alt : bins->vals;
     ctx->prof.begin(ST_BLEND, static_cast<cudaStream_t>(stream));
+    int nl = 1;
     cudaError_t e = launch_rasterize(proj->rec, proj->n_pad, bins->ranges, vals, n_views, cams[0].width, cams[0].height,
                                      bg[0], bg[1], bg[2], rgb_out, T_out, rgb8_out, rgb8_out ? OUT_RGB8 : OUT_F32, 0.f,
-                                     static_cast<cudaStream_t>(stream));
-    ctx->prof.end(static_cast<cudaStream_t>(stream));
+                                     order_scratch(ctx, n_views, cams[0].width, cams[0].height),
+                                     static_cast<cudaStream_t>(stream), &nl);
+    ctx->prof.end(static_cast<cudaStream_t>(stream), nl);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "rasterize");
     return QUEEN_OK;
 }
@@ -434,7 +444,9 @@ queen_status queen_rasterize_backward(queen_ctx* ctx, const queen_proj* proj, co
     if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
     const uint32_t* vals = bins->sorted_in_alt ? bins->vals_alt : bins->vals;
     cudaError_t e = launch_blend_bwd(proj->rec, proj->n_pad, bins->ranges, vals, n_views, cams[0].width, cams[0].height,
-                                     bg[0], bg[1], bg[2], dL_drgb, grad_rec, static_cast<cudaStream_t>(stream));
+                                     bg[0], bg[1], bg[2], dL_drgb, grad_rec,
+                                     order_scratch(ctx, n_views, cams[0].width, cams[0].height),
+                                     static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "rasterize_backward");
     return QUEEN_OK;
 }
@@ -533,10 +545,11 @@ queen_status queen_render_mask(queen_ctx* ctx, const queen_gaussians* scene, con
     if ((st = queen_bin_sort(ctx, &pj, cams, n_views, &b, stream))) return st;
     const uint32_t* vals = b.sorted_in_alt ? b.vals_alt : b.vals;
     ctx->prof.begin(ST_BLEND, s);
+    int nl = 1;
     e = launch_rasterize(pj.rec, pj.n_pad, b.ranges, vals, n_views, W, H, 0.f, 0.f, 0.f, nullptr, nullptr, mask_out,
-                         OUT_MASK, alpha_thresh, s);
+                         OUT_MASK, alpha_thresh, order_scratch(ctx, n_views, W, H), s, &nl);
     if (e == cudaSuccess) e = launch_dilate(mask_out, reinterpret_cast<uint8_t*>(ws + L.mask_tmp), n_views, W, H, dilation, s);
-    ctx->prof.end(s, dilation > 1 ? 3 : 1);
+    ctx->prof.end(s, nl + (dilation > 1 ? 2 : 0));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "render_mask");
     return QUEEN_OK;
 }

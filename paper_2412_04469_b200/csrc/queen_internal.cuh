@@ -102,11 +102,15 @@ inline BinPlan bin_plan(int64_t n_pad, int64_t n_views, int W, int H) {
     return p;
 }
 
+// Blend schedule (raster.cu): tiles launched longest list first, by list length classes of
+// 32 entries (ORDER_BINS classes, the last open-ended), so the grid's tail holds short tiles.
+constexpr int ORDER_BINS = 64;
+
 // Workspace carve-up (bytes, 256-aligned) for (n_pad, n_views, W, H, keys_cap).
 struct WsLayout {
     // scratch (bin_sort)
     size_t flags, hist, dminmax, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, counts, view_tot, slab_counts,
-        slab_vis, select, ans_table, total_scratch;
+        slab_vis, select, ans_table, order, total_scratch;
     // render_views / render_mask buffers
     size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, mask_tmp, total;
     int64_t key_tiles, elem_tiles, os_key_tiles, os_elem_tiles, T, elems;
@@ -141,6 +145,7 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     L.slab_vis = o; o += align256(sizeof(uint32_t) * (size_t)(bp.slabs + 1));
     L.select = o; o += align256((size_t)n_pad);  // render_mask: per-Gaussian subset flags
     L.ans_table = o; o += align256(sizeof(uint32_t) * 5 * 4096);  // entropy decode slot tables
+    L.order = o; o += align256(sizeof(uint32_t) * (2 * ORDER_BINS + (size_t)n_views * L.T));  // blend tile order
     L.total_scratch = o;
     L.rec = o; o += align256(sizeof(float) * REC_WORDS * L.elems);
     L.depth = o; o += align256(sizeof(uint32_t) * L.elems);
@@ -324,13 +329,18 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
 enum : int { OUT_F32 = 0, OUT_MASK = 1, OUT_RGB8 = 2 };  // k_blend epilogues
 cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
-                             uint8_t* out8, int out_mode, float mask_thresh, cudaStream_t s);
+                             uint8_t* out8, int out_mode, float mask_thresh, uint32_t* order_ws, cudaStream_t s,
+                             int* n_launch = nullptr);
+// blend schedule: *order = longest-list-first permutation of the blocks gt tiles (in order_ws),
+// or nullptr (grid order) when there is no scratch
+cudaError_t launch_tile_order(const uint32_t* ranges, int64_t blocks, uint32_t* order_ws, cudaStream_t s,
+                              const uint32_t** order);
 cudaError_t launch_select(const uint32_t* idx, int k, const int32_t* k_dev, int n, int n_pad, uint8_t* select,
                           DevFlags* fl, cudaStream_t s);
 cudaError_t launch_dilate(uint8_t* marks, uint8_t* tmp, int n_views, int W, int H, int d, cudaStream_t s);
 cudaError_t launch_blend_bwd(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, const float* gout, float* grec,
-                             cudaStream_t s);
+                             uint32_t* order_ws, cudaStream_t s);
 cudaError_t launch_project_bwd(const float* planes, int n, int n_pad, int deg, const CamBatch& cams, int n_views,
                                const float* grec, float* gpl, cudaStream_t s);
 cudaError_t launch_decode_bwd(const queen_packet& pk, const float* gA, float* gdec, float* glat, float* gla, float* gpre,

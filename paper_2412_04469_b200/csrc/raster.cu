@@ -24,6 +24,8 @@
 
 #include "queen_internal.cuh"
 
+#include <algorithm>
+
 namespace queen {
 
 
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
                                                     const uint32_t* __restrict__ vals, int W, int H, int gx, int T, float bg0,
                                                     float bg1, float bg2, float* __restrict__ rgb_out, float* __restrict__ T_out,
                                                     uint8_t* __restrict__ out8, int out_mode, float mask_thresh, long long* ev_out,
-                                                    long long* cp_out) {
+                                                    long long* cp_out, const uint32_t* __restrict__ order) {
     constexpr int NT = 256 / RPT;          // threads per tile CTA: one column x RPT rows each
     constexpr int BATCH = NT > 64 ? NT : 64;  // records staged per batch
     constexpr int PER = BATCH / NT;        // records each thread stages per batch
@@ -87,7 +89,7 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
     __shared__ __align__(16) float4 sB[2][BATCH];  // A2, B2, C2, T2
     __shared__ __align__(16) float4 sC[2][BATCH];  // o, r, g, b
     __shared__ uint8_t s_list[NT / 32][BATCH];         // per-warp record list of the batch
-    const int gt = blockIdx.x;
+    const int gt = order ? (int)order[blockIdx.x] : (int)blockIdx.x;
     const int v = gt / T;
     const int t = gt - v * T;
     const int px = (t % gx) * 16 + (threadIdx.x & 15);
@@ -303,21 +305,95 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
 
 constexpr int BLEND_RPT = 4;
 
+// Blend schedule: a permutation of the gt tiles, longest list first (list-length classes of
+// 32 entries; order inside a class arbitrary).  Tiles are independent, so the schedule never
+// changes a pixel; it only moves the long tiles away from the grid's tail.
+__device__ __forceinline__ int order_class(uint2 r) {
+    const uint32_t c = (r.y - r.x) >> 5;
+    return ORDER_BINS - 1 - (int)(c < (uint32_t)(ORDER_BINS - 1) ? c : (uint32_t)(ORDER_BINS - 1));
+}
+
+__global__ void __launch_bounds__(256) k_order_hist(const uint2* __restrict__ ranges, int n, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t sh[ORDER_BINS];
+    for (int q = threadIdx.x; q < ORDER_BINS; q += blockDim.x) sh[q] = 0u;
+    __syncthreads();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        atomicAdd(&sh[order_class(ranges[i])], 1u);
+    __syncthreads();
+    for (int q = threadIdx.x; q < ORDER_BINS; q += blockDim.x)
+        if (sh[q]) atomicAdd(&hist[q], sh[q]);
+}
+
+__global__ void __launch_bounds__(256) k_order_scatter(const uint2* __restrict__ ranges, int n,
+                                                       const uint32_t* __restrict__ hist, uint32_t* __restrict__ cursor,
+                                                       uint32_t* __restrict__ order) {
+    __shared__ uint32_t s_start[ORDER_BINS], s_cnt[ORDER_BINS], s_base[ORDER_BINS];
+    if (threadIdx.x < 32) {  // exclusive scan of the class counts, two per lane
+        const int l = threadIdx.x;
+        const uint32_t a = hist[2 * l], b = hist[2 * l + 1];
+        uint32_t x = a + b;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (l >= o) x += y;
+        }
+        s_start[2 * l] = x - a - b;
+        s_start[2 * l + 1] = x - b;
+    }
+    for (int c0 = blockIdx.x * blockDim.x; c0 < n; c0 += gridDim.x * blockDim.x) {
+        for (int q = threadIdx.x; q < ORDER_BINS; q += blockDim.x) s_cnt[q] = 0u;
+        __syncthreads();
+        const int i = c0 + threadIdx.x;
+        int cl = 0;
+        uint32_t rank = 0;
+        if (i < n) {
+            cl = order_class(ranges[i]);
+            rank = atomicAdd(&s_cnt[cl], 1u);
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < ORDER_BINS; q += blockDim.x)
+            if (s_cnt[q]) s_base[q] = s_start[q] + atomicAdd(&cursor[q], s_cnt[q]);
+        __syncthreads();
+        if (i < n) order[s_base[cl] + rank] = (uint32_t)i;
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_tile_order(const uint32_t* ranges, int64_t blocks, uint32_t* order_ws, cudaStream_t s,
+                              const uint32_t** order) {
+    *order = nullptr;
+    if (!order_ws || blocks == 0 || getenv("QUEEN_BLEND_GRID_ORDER")) return cudaSuccess;  // env: test hook
+    uint32_t* hist = order_ws;
+    uint32_t* cursor = order_ws + ORDER_BINS;
+    uint32_t* ord = order_ws + 2 * ORDER_BINS;
+    cudaError_t e = cudaMemsetAsync(order_ws, 0, sizeof(uint32_t) * 2 * ORDER_BINS, s);
+    if (e) return e;
+    const int grid = (int)std::min<int64_t>((blocks + 255) / 256, 296);
+    k_order_hist<<<grid, 256, 0, s>>>(reinterpret_cast<const uint2*>(ranges), (int)blocks, hist);
+    k_order_scatter<<<grid, 256, 0, s>>>(reinterpret_cast<const uint2*>(ranges), (int)blocks, hist, cursor, ord);
+    *order = ord;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
-                             uint8_t* out8, int out_mode, float mask_thresh, cudaStream_t s) {
+                             uint8_t* out8, int out_mode, float mask_thresh, uint32_t* order_ws, cudaStream_t s,
+                             int* n_launch) {
     const int gx = (W + 15) / 16, gy = (H + 15) / 16;
     const int T = gx * gy;
     const int64_t blocks = (int64_t)T * n_views;
     if (blocks == 0) return cudaSuccess;
+    const uint32_t* order = nullptr;
+    if (cudaError_t e = launch_tile_order(ranges, blocks, order_ws, s, &order)) return e;
+    if (n_launch) *n_launch = order ? 3 : 1;
     if (getenv("QUEEN_BLEND_NOMASK"))  // test hook: per-thread box cull only (no warp record lists)
         k_blend<false, BLEND_RPT, false><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(
             reinterpret_cast<const float4*>(rec), n_pad, reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0, bg1,
-            bg2, rgb_out, T_out, out8, out_mode, mask_thresh, nullptr, nullptr);
+            bg2, rgb_out, T_out, out8, out_mode, mask_thresh, nullptr, nullptr, order);
     else
         k_blend<false, BLEND_RPT, true><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(
             reinterpret_cast<const float4*>(rec), n_pad, reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0, bg1,
-            bg2, rgb_out, T_out, out8, out_mode, mask_thresh, nullptr, nullptr);
+            bg2, rgb_out, T_out, out8, out_mode, mask_thresh, nullptr, nullptr, order);
     return cudaGetLastError();
 }
 
@@ -334,7 +410,7 @@ cudaError_t launch_blend_counts(const float* rec, int n_pad, const uint32_t* ran
 #endif
     k_blend<true, BLEND_RPT, QUEEN_COUNT_WMASK><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(reinterpret_cast<const float4*>(rec), n_pad,
                                                   reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, 0.f, 0.f, 0.f,
-                                                  nullptr, nullptr, nullptr, OUT_F32, 0.f, evaluated, composited);
+                                                  nullptr, nullptr, nullptr, OUT_F32, 0.f, evaluated, composited, nullptr);
     return cudaGetLastError();
 }
 
