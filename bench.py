@@ -138,6 +138,9 @@ def algorithmic_bytes(stage, cfg, n, vpb_list, K_list, k_coo, M_list, ent_bytes=
         return sum(12 * M + 8 * K for v, M, K in bt)
     if stage == "tile_sort":  # pass 1: 8 B in, 4 B packed out; pass 2: 4 B in, 4 B index out
         return sum(20 * K for v, M, K in bt)
+    if stage == "blend_order":  # ranges read by the histogram and by the scatter, 4 B order out per tile
+        T = ((cfg.width + 15) // 16) * ((cfg.height + 15) // 16)
+        return sum(20 * v * T for v, M, K in bt)
     return None
 
 

@@ -307,9 +307,10 @@ queen_status queen_wait_binned(const queen_ctx* ctx, void* stream);
 
 /* Stage profiler (evidence for bench.py): when enabled, every call records CUDA events
  * on its stream around each stage: 0 apply, 1 project, 2 compact (+resets), 3 depth sort,
- * 4 duplicate, 5 tile sort, 6 ranges, 7 blend, 8 entropy decode.  queen_profile_read
+ * 4 duplicate, 5 tile sort, 6 ranges, 7 blend (k_blend alone), 8 entropy decode, 9 blend
+ * order (the longest-list-first tile schedule built before the blend).  queen_profile_read
  * waits for the recorded events and returns per-stage summed milliseconds and kernel
- * launches (double[9], int64[9]), optionally resetting them.  Not capturable. */
+ * launches (double[10], int64[10]), optionally resetting them.  Not capturable. */
 queen_status queen_profile_enable(queen_ctx* ctx, int32_t enable);
 queen_status queen_profile_read(queen_ctx* ctx, double* ms, int64_t* launches, int32_t reset);
 

@@ -33,7 +33,7 @@ EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version",
            "queen_entropy_decode", "queen_entropy_decode_frame", "queen_render_mask",
            "queen_densify", "queen_rasterize_rgb8", "queen_render_views_rgb8",
            "queen_rasterize_backward", "queen_project_backward", "queen_decode_backward"]
-STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy"]
+STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy", "blend_order"]
 
 
 class QueenError(RuntimeError):

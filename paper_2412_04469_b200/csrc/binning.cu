@@ -55,7 +55,10 @@ constexpr long long SPIN_LIMIT = 1ll << 24;
 #ifndef QUEEN_LB_BATCH
 #define QUEEN_LB_BATCH 8
 #endif
-constexpr int LB_BATCH = QUEEN_LB_BATCH;  // onesweep look-back predecessors loaded per round trip
+constexpr int LB_BATCH = QUEEN_LB_BATCH;
+#ifndef QUEEN_OS_MATCH_OR
+#define QUEEN_OS_MATCH_OR 1  // warp match by shared atomicOr (measured: tile sort 488 -> 417 us vs match.any)
+#endif  // onesweep look-back predecessors loaded per round trip
 constexpr int SORT_WARPS = SORT_THREADS / 32;
 
 enum : int { TK_DEPTH = 0, TK_TILE = 4, TK_VIS = 8, TK_DUP = 9 };
@@ -495,9 +498,20 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
         return;
     }
     const bool owns_digits = threadIdx.x * DPT < BINS;
+#if QUEEN_OS_MATCH_OR
+    // warp match by shared-memory atomicOr (experiment knob): the per-warp match words live in
+    // the staging buffer (free until the scatter), re-zeroed at the start of every tile
+    static_assert(NW * BINS <= 2 * TILE, "match words must fit the staging buffer");
+    uint32_t* wmatch = sk + w * BINS;
+#endif
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-        for (int q = threadIdx.x; q < NW * BINS; q += NT) whist[q] = 0u;
+        for (int q = threadIdx.x; q < NW * BINS; q += NT) {
+            whist[q] = 0u;
+#if QUEEN_OS_MATCH_OR
+            sk[q] = 0u;
+#endif
+        }
         __syncthreads();
         const uint32_t tile = s_tile;
         if (tile >= ntiles) break;
@@ -513,12 +527,28 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
         // warp multisplit in key order (stable): rank among this warp's earlier equal digits.
         // All MATCHes first (independent), then the short shared-memory chain.
         uint32_t peers[IT];
+#if QUEEN_OS_MATCH_OR
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
+            const uint32_t idx = base + w * (32 * IT) + j * 32 + lane;
+            rk[j] = idx < Kn ? ((k[j] >> shift) & DMASK) : (uint32_t)BINS;
+            const bool ok = rk[j] < (uint32_t)BINS;
+            const uint32_t inv = __ballot_sync(0xffffffffu, !ok);
+            if (ok) atomicOr(&wmatch[rk[j]], 1u << lane);
+            __syncwarp();
+            peers[j] = ok ? wmatch[rk[j]] : inv;
+            __syncwarp();
+            if (ok && (peers[j] & lt_mask) == 0) wmatch[rk[j]] = 0u;
+            __syncwarp();
+        }
+#else
 #pragma unroll
         for (int j = 0; j < IT; ++j) {
             const uint32_t idx = base + w * (32 * IT) + j * 32 + lane;
             rk[j] = idx < Kn ? ((k[j] >> shift) & DMASK) : (uint32_t)BINS;
             peers[j] = __match_any_sync(0xffffffffu, rk[j]);
         }
+#endif
 #pragma unroll
         for (int j = 0; j < IT; ++j) {
             const uint32_t d = rk[j];

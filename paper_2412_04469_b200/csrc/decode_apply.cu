@@ -1,22 +1,42 @@
 // K1 / K1b: fused residual decode + apply (Eq. 4-5) and the
 // position step (hard-concrete gate P:329-336, COO P:1389-1390).
 //
-// One coalesced, vectorised pass over the Gaussian SoA: each thread owns 4
-// consecutive Gaussians, so every latent row is one 4-byte char4 load and every
-// attribute row one 16-byte float4 load + store per thread (a warp moves 128 B of
-// latents and 512 B of attributes per row).  The decoders (<= 896 floats) sit in
-// shared memory and are read as warp-uniform broadcasts.  HBM-bound: bytes per
-// Gaussian = sum L_c (int8) + 2*4*sum M_c (fp32 read+write), K1.
+// One coalesced, vectorised pass over the Gaussian SoA, split into work groups of rows so
+// that every thread has all of its loads in flight at once (below).  The decoders sit in
+// shared memory and are read as warp-uniform broadcasts.  HBM-bound: bytes per Gaussian =
+// sum L_c (int8) + 2*4*sum M_c (fp32 read+write), K1.
 #include "queen_internal.cuh"
 
 namespace queen {
 
-constexpr int DA_CHUNK = 4;  // attribute rows per batch of loads (rows in flight per warp)
+#ifndef QUEEN_DA_MINB
+#define QUEEN_DA_MINB 4  // min resident blocks per SM (register cap: 64)
+#endif
+#ifndef QUEEN_DA_ROWS
+#define QUEEN_DA_ROWS 4  // measured N3DV apply (L2 flushed): 8 rows x 2 blocks 57 us, 6 x 3 45 us, 4 x 4 41 us
+#endif
+constexpr int DA_ROWS = QUEEN_DA_ROWS;      // attribute rows per work group (all loads in flight at once)
+constexpr int DA_MAX_GROUPS = 5 + (4 + 3 + 1 + 3 + 45 + DA_ROWS - 1) / DA_ROWS + 1;  // worst case at degree 3, + gates
 
+// One work group = rows [m0, m1) of category c (m1 - m0 <= DA_ROWS, balanced runs), or the gated position
+// rows (c = 5).  The grid is (Gaussian blocks) x (groups) (+ the fused COO scatter blocks).
+// A thread owns 4 consecutive Gaussians of one group (16-byte attribute accesses, 512 B per
+// warp and row) and issues ALL of its loads -- the category's latent rows (<= 16 char4) and
+// its <= DA_ROWS attribute rows -- before using any: one memory round trip per thread.
+// Latents stay packed (one register per 4 Gaussians) and the decode runs k-outermost, so 64
+// registers suffice for 4 resident blocks per SM.  (One thread walking all 56 rows was a chain of ~20
+// dependent round trips in a single wave at 24 % occupancy: latency-bound at ~25 % of HBM.)
 struct DecodeParams {
     int n, n_pad;
     int lat[5], M[5], lat_row0[5], dec_off[5], out_row0[5];
     int ndec;
+    int ngroups;
+    int g_c[DA_MAX_GROUPS], g_m0[DA_MAX_GROUPS], g_m1[DA_MAX_GROUPS];
+    int xblocks;                 // Gaussian blocks per group
+    int coo_k;                   // COO capacity (entries); 0 = no fused scatter
+    const int32_t* coo_kdev;
+    const uint32_t* coo_idx;
+    const float* coo_val;
     const void* latents;
     const float* decoders;
     float* planes;
@@ -35,100 +55,47 @@ __device__ __forceinline__ float gate_value(float la, float tau, float g0, float
     return fminf(1.0f, fmaxf(0.0f, gt));
 }
 
-template <bool F32, bool APPLY, bool GATES>
-__global__ void __launch_bounds__(256) k_decode_apply(DecodeParams p) {
-    extern __shared__ float sdec[];
-    for (int j = threadIdx.x; j < p.ndec; j += blockDim.x) sdec[j] = p.decoders[j];
-    __syncthreads();
-    const int i0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-    if (i0 >= p.n) return;
-    const bool l1 = i0 + 1 < p.n, l2 = i0 + 2 < p.n, l3 = i0 + 3 < p.n;
-    const int64_t np = p.n_pad;
-    bool bad = false;
-#pragma unroll 1
-    for (int c = 0; c < 5; ++c) {
-        const int L = p.lat[c], M = p.M[c];
-        if (L == 0) {
-            if (p.resid_out)
-                for (int m = 0; m < M; ++m)
-                    *reinterpret_cast<float4*>(p.resid_out + (int64_t)(p.out_row0[c] + m) * np + i0) =
-                        make_float4(0.f, 0.f, 0.f, 0.f);
-            continue;
-        }
-        float ql[16][4];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            if (k < L) {
-                const int64_t off = (int64_t)(p.lat_row0[c] + k) * np + i0;
-                if (F32) {
-                    // a1: l = round(l_hat), half away from zero (R#5); |l| <= 127 (R#4)
-                    float4 lh = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(p.latents) + off));
-                    float r0 = roundf(lh.x), r1 = roundf(lh.y), r2 = roundf(lh.z), r3 = roundf(lh.w);
-                    if (!(r0 >= -127.f && r0 <= 127.f)) { bad = true; r0 = r0 < 0.f ? -127.f : 127.f; }
-                    if (l1 && !(r1 >= -127.f && r1 <= 127.f)) { bad = true; r1 = r1 < 0.f ? -127.f : 127.f; }
-                    if (l2 && !(r2 >= -127.f && r2 <= 127.f)) { bad = true; r2 = r2 < 0.f ? -127.f : 127.f; }
-                    if (l3 && !(r3 >= -127.f && r3 <= 127.f)) { bad = true; r3 = r3 < 0.f ? -127.f : 127.f; }
-                    r1 = fminf(fmaxf(r1, -127.f), 127.f);
-                    r2 = fminf(fmaxf(r2, -127.f), 127.f);
-                    r3 = fminf(fmaxf(r3, -127.f), 127.f);
-                    ql[k][0] = r0; ql[k][1] = r1; ql[k][2] = r2; ql[k][3] = r3;
-                    if (p.q_out)
-                        *reinterpret_cast<char4*>(p.q_out + off) =
-                            make_char4((signed char)(int)r0, (signed char)(int)r1, (signed char)(int)r2,
-                                       (signed char)(int)r3);
-                } else {
-                    char4 q4 = __ldg(reinterpret_cast<const char4*>(static_cast<const int8_t*>(p.latents) + off));
-                    ql[k][0] = (float)q4.x; ql[k][1] = (float)q4.y; ql[k][2] = (float)q4.z; ql[k][3] = (float)q4.w;
-                    if (p.q_out) *reinterpret_cast<char4*>(p.q_out + off) = q4;
-                }
-            }
-        }
-        // rows in chunks of DA_CHUNK: the chunk's attribute loads are issued together (memory-
-        // level parallelism: DA_CHUNK x 512 B in flight per warp instead of one row at a time)
-#pragma unroll 1
-        for (int m0 = 0; m0 < M; m0 += DA_CHUNK) {
-            float4 av[DA_CHUNK];
-            if (APPLY) {
-#pragma unroll
-                for (int u = 0; u < DA_CHUNK; ++u)
-                    if (m0 + u < M)
-                        av[u] = *reinterpret_cast<const float4*>(p.planes + (int64_t)(3 + p.out_row0[c] + m0 + u) * np + i0);
-            }
-#pragma unroll
-            for (int u = 0; u < DA_CHUNK; ++u) {
-                const int m = m0 + u;
-                if (m >= M) break;
-                // a2: r = D_c[m] . float(l), fmaf chain ascending k from +0 (R#7)
-                const float* d = sdec + p.dec_off[c] + m * L;
-                float r0 = +0.0f, r1 = +0.0f, r2 = +0.0f, r3 = +0.0f;
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    if (k < L) {
-                        const float w = d[k];
-                        r0 = fmaf(w, ql[k][0], r0);
-                        r1 = fmaf(w, ql[k][1], r1);
-                        r2 = fmaf(w, ql[k][2], r2);
-                        r3 = fmaf(w, ql[k][3], r3);
-                    }
-                }
-                const int row = p.out_row0[c] + m;
-                if (p.resid_out)
-                    *reinterpret_cast<float4*>(p.resid_out + (int64_t)row * np + i0) = make_float4(r0, r1, r2, r3);
-                if (APPLY) {
-                    // a3: A_t = A_{t-1} + r, separate add (R#7)
-                    float4 v = av[u];
-                    v.x = v.x + r0;
-                    if (l1) v.y = v.y + r1;
-                    if (l2) v.z = v.z + r2;
-                    if (l3) v.w = v.w + r3;
-                    *reinterpret_cast<float4*>(p.planes + (int64_t)(3 + row) * np + i0) = v;
-                }
-            }
-        }
+// a5: p[I_k] += E_p[k] for entry j of the COO position residual; validates
+// the index: idx < n and strictly increasing, else QUEEN_ERR_INDEX and skip.
+__device__ __forceinline__ void coo_entry(float* planes, int n, int64_t n_pad, const uint32_t* idx, const float* val,
+                                          int kcap, int j, DevFlags* fl) {
+    const uint32_t i = idx[j];
+    if (i >= (uint32_t)n || (j > 0 && i <= idx[j - 1])) {
+        raise_flag(fl, FLAG_INDEX);
+        return;
     }
-    if (GATES && APPLY) {
+    const float v0 = val[j], v1 = val[(int64_t)kcap + j], v2 = val[2 * (int64_t)kcap + j];
+    planes[i] = planes[i] + v0;
+    planes[n_pad + i] = planes[n_pad + i] + v1;
+    planes[2 * n_pad + i] = planes[2 * n_pad + i] + v2;
+}
+
+template <bool F32, bool APPLY, bool GATES>
+__global__ void __launch_bounds__(256, QUEEN_DA_MINB) k_decode_apply(DecodeParams p) {
+    extern __shared__ float sdec[];
+    const int gid = blockIdx.x / p.xblocks;
+    if (gid >= p.ngroups) {
+        // fused COO scatter blocks (COO mode: the decode groups never touch position rows)
+        int k = p.coo_k;
+        if (p.coo_kdev) k = min(max(*p.coo_kdev, 0), p.coo_k);
+        const int j = (blockIdx.x - p.ngroups * p.xblocks) * blockDim.x + threadIdx.x;
+        if (j < k) coo_entry(p.planes, p.n, p.n_pad, p.coo_idx, p.coo_val, p.coo_k, j, p.fl);
+        return;
+    }
+    const int c = p.g_c[gid];
+    const int64_t np = p.n_pad;
+    const int i0 = ((blockIdx.x - gid * p.xblocks) * blockDim.x + threadIdx.x) * 4;
+    if (c == 5) {
+        if (!(GATES && APPLY) || i0 >= p.n) return;
         // a4 fused: dp = g l_p for log alpha > theta0 (R#6), p += dp
+        const bool l1 = i0 + 1 < p.n, l2 = i0 + 2 < p.n, l3 = i0 + 3 < p.n;
         const float4 la = __ldg(reinterpret_cast<const float4*>(p.log_alpha + i0));
+        float4 lp[3], pv[3];
+#pragma unroll
+        for (int dd = 0; dd < 3; ++dd) {
+            lp[dd] = __ldg(reinterpret_cast<const float4*>(p.pregate + (int64_t)dd * np + i0));
+            pv[dd] = *reinterpret_cast<const float4*>(p.planes + (int64_t)dd * np + i0);
+        }
         const float lav[4] = {la.x, la.y, la.z, la.w};
         const bool live[4] = {true, l1, l2, l3};
         float g[4];
@@ -140,14 +107,100 @@ __global__ void __launch_bounds__(256) k_decode_apply(DecodeParams p) {
         }
 #pragma unroll
         for (int dd = 0; dd < 3; ++dd) {
-            const float4 lp = __ldg(reinterpret_cast<const float4*>(p.pregate + (int64_t)dd * np + i0));
-            float4* a = reinterpret_cast<float4*>(p.planes + (int64_t)dd * np + i0);
-            float4 v = *a;
-            if (on[0]) v.x = v.x + g[0] * lp.x;
-            if (on[1]) v.y = v.y + g[1] * lp.y;
-            if (on[2]) v.z = v.z + g[2] * lp.z;
-            if (on[3]) v.w = v.w + g[3] * lp.w;
-            *a = v;
+            float4 v = pv[dd];
+            if (on[0]) v.x = v.x + g[0] * lp[dd].x;
+            if (on[1]) v.y = v.y + g[1] * lp[dd].y;
+            if (on[2]) v.z = v.z + g[2] * lp[dd].z;
+            if (on[3]) v.w = v.w + g[3] * lp[dd].w;
+            *reinterpret_cast<float4*>(p.planes + (int64_t)dd * np + i0) = v;
+        }
+        return;
+    }
+    const int L = p.lat[c];
+    const int m0 = p.g_m0[gid], R = p.g_m1[gid] - m0;
+    const int dbase = p.dec_off[c] + m0 * L;
+    for (int j = threadIdx.x; j < R * L; j += blockDim.x) sdec[j] = p.decoders[dbase + j];
+    __syncthreads();
+    if (i0 >= p.n) return;
+    const bool l1 = i0 + 1 < p.n, l2 = i0 + 2 < p.n, l3 = i0 + 3 < p.n;
+    const int row0 = p.out_row0[c] + m0;
+    if (L == 0) {
+        if (p.resid_out)
+            for (int m = 0; m < R; ++m)
+                *reinterpret_cast<float4*>(p.resid_out + (int64_t)(row0 + m) * np + i0) = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    const bool write_q = p.q_out && m0 == 0;  // one group per category writes the rounded latents
+    bool bad = false;
+    // the group's latents (4 Gaussians packed per register) and attribute rows, all loads issued
+    // before any is used: one memory round trip per thread
+    uint32_t q4[16];
+    float4 av[DA_ROWS];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        if (k < L) {
+            const int64_t off = (int64_t)(p.lat_row0[c] + k) * np + i0;
+            if (F32) {
+                // a1: l = round(l_hat), half away from zero (R#5); |l| <= 127 (R#4)
+                float4 lh = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(p.latents) + off));
+                float r0 = roundf(lh.x), r1 = roundf(lh.y), r2 = roundf(lh.z), r3 = roundf(lh.w);
+                if (!(r0 >= -127.f && r0 <= 127.f)) { bad = true; r0 = r0 < 0.f ? -127.f : 127.f; }
+                if (l1 && !(r1 >= -127.f && r1 <= 127.f)) { bad = true; r1 = r1 < 0.f ? -127.f : 127.f; }
+                if (l2 && !(r2 >= -127.f && r2 <= 127.f)) { bad = true; r2 = r2 < 0.f ? -127.f : 127.f; }
+                if (l3 && !(r3 >= -127.f && r3 <= 127.f)) { bad = true; r3 = r3 < 0.f ? -127.f : 127.f; }
+                r1 = fminf(fmaxf(r1, -127.f), 127.f);
+                r2 = fminf(fmaxf(r2, -127.f), 127.f);
+                r3 = fminf(fmaxf(r3, -127.f), 127.f);
+                const char4 c4 = make_char4((signed char)(int)r0, (signed char)(int)r1, (signed char)(int)r2,
+                                            (signed char)(int)r3);
+                q4[k] = *reinterpret_cast<const uint32_t*>(&c4);
+            } else {
+                q4[k] = __ldg(reinterpret_cast<const uint32_t*>(static_cast<const int8_t*>(p.latents) + off));
+            }
+            if (write_q) *reinterpret_cast<uint32_t*>(p.q_out + off) = q4[k];
+        }
+    }
+    if (APPLY) {
+#pragma unroll
+        for (int u = 0; u < DA_ROWS; ++u)
+            if (u < R) av[u] = *reinterpret_cast<const float4*>(p.planes + (int64_t)(3 + row0 + u) * np + i0);
+    }
+    // a2: r = D_c[m] . float(l), fmaf chain ascending k from +0 (R#7); k outermost, so
+    // only one latent column is unpacked at a time
+    float4 r[DA_ROWS];
+#pragma unroll
+    for (int u = 0; u < DA_ROWS; ++u) r[u] = make_float4(+0.0f, +0.0f, +0.0f, +0.0f);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        if (k < L) {
+            const uint32_t w4 = q4[k];
+            const float f0 = (float)(int8_t)(w4 & 0xffu), f1 = (float)(int8_t)((w4 >> 8) & 0xffu);
+            const float f2 = (float)(int8_t)((w4 >> 16) & 0xffu), f3 = (float)(int8_t)(w4 >> 24);
+#pragma unroll
+            for (int u = 0; u < DA_ROWS; ++u) {
+                if (u < R) {
+                    const float w = sdec[u * L + k];
+                    r[u].x = fmaf(w, f0, r[u].x);
+                    r[u].y = fmaf(w, f1, r[u].y);
+                    r[u].z = fmaf(w, f2, r[u].z);
+                    r[u].w = fmaf(w, f3, r[u].w);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < DA_ROWS; ++u) {
+        if (u >= R) break;
+        const int row = row0 + u;
+        if (p.resid_out) *reinterpret_cast<float4*>(p.resid_out + (int64_t)row * np + i0) = r[u];
+        if (APPLY) {
+            // a3: A_t = A_{t-1} + r, separate add (R#7)
+            float4 v = av[u];
+            v.x = v.x + r[u].x;
+            if (l1) v.y = v.y + r[u].y;
+            if (l2) v.z = v.z + r[u].z;
+            if (l3) v.w = v.w + r[u].w;
+            *reinterpret_cast<float4*>(p.planes + (int64_t)(3 + row) * np + i0) = v;
         }
     }
     if (bad) raise_flag(p.fl, FLAG_LATENT_RANGE);
@@ -308,25 +361,51 @@ cudaError_t launch_decode_apply(const queen_packet& pk, float* planes, float* re
     p.theta0 = host_theta0(pk.tau, pk.gamma0, pk.gamma1);
     const bool f32 = pk.latent_kind == QUEEN_LAT_F32;
     const bool gates = apply_pos && pk.pos_kind == QUEEN_POS_GATES;
-    const int groups = (pk.n + 3) / 4;
+    // work groups: each category's rows in balanced runs of <= DA_ROWS, then the gated positions
+    int ng = 0, max_dec = 1;
+    for (int c = 0; c < 5; ++c) {
+        const int M = p.M[c], parts = (M + DA_ROWS - 1) / DA_ROWS;
+        for (int q = 0; q < parts; ++q) {
+            p.g_c[ng] = c;
+            p.g_m0[ng] = (int)((int64_t)M * q / parts);
+            p.g_m1[ng] = (int)((int64_t)M * (q + 1) / parts);
+            max_dec = max(max_dec, (p.g_m1[ng] - p.g_m0[ng]) * p.lat[c]);
+            ++ng;
+        }
+    }
+    if (gates && apply_attrs) {
+        p.g_c[ng] = 5; p.g_m0[ng] = 0; p.g_m1[ng] = 3;
+        ++ng;
+    }
+    p.ngroups = ng;
     const int threads = 256;
-    const int blocks = (groups + threads - 1) / threads;
-    const size_t smem = sizeof(float) * (size_t)(p.ndec > 0 ? p.ndec : 1);
+    p.xblocks = (pk.n + 4 * threads - 1) / (4 * threads);
+    const bool coo = apply_attrs && apply_pos && pk.pos_kind == QUEEN_POS_COO && pk.k > 0;
+    int coo_blocks = 0;
+    if (coo) {
+        p.coo_k = pk.k;
+        p.coo_kdev = pk.k_dev;
+        p.coo_idx = pk.pos_idx;
+        p.coo_val = pk.pos_val;
+        coo_blocks = (pk.k + threads - 1) / threads;
+    }
+    const int64_t blocks = (int64_t)p.xblocks * ng + coo_blocks;
+    const size_t smem = sizeof(float) * (size_t)max_dec;
     if (blocks > 0) {
         if (apply_attrs) {
             if (f32) {
-                if (gates) k_decode_apply<true, true, true><<<blocks, threads, smem, s>>>(p);
-                else k_decode_apply<true, true, false><<<blocks, threads, smem, s>>>(p);
+                if (gates) k_decode_apply<true, true, true><<<(unsigned)blocks, threads, smem, s>>>(p);
+                else k_decode_apply<true, true, false><<<(unsigned)blocks, threads, smem, s>>>(p);
             } else {
-                if (gates) k_decode_apply<false, true, true><<<blocks, threads, smem, s>>>(p);
-                else k_decode_apply<false, true, false><<<blocks, threads, smem, s>>>(p);
+                if (gates) k_decode_apply<false, true, true><<<(unsigned)blocks, threads, smem, s>>>(p);
+                else k_decode_apply<false, true, false><<<(unsigned)blocks, threads, smem, s>>>(p);
             }
         } else {
-            if (f32) k_decode_apply<true, false, false><<<blocks, threads, smem, s>>>(p);
-            else k_decode_apply<false, false, false><<<blocks, threads, smem, s>>>(p);
+            if (f32) k_decode_apply<true, false, false><<<(unsigned)blocks, threads, smem, s>>>(p);
+            else k_decode_apply<false, false, false><<<(unsigned)blocks, threads, smem, s>>>(p);
         }
     }
-    if (apply_pos && pk.pos_kind == QUEEN_POS_COO && pk.k > 0) {
+    if (apply_pos && !apply_attrs && pk.pos_kind == QUEEN_POS_COO && pk.k > 0) {
         const int kb = (pk.k + 255) / 256;
         k_coo_scatter<<<kb, 256, 0, s>>>(planes, pk.n, pk.n_pad, pk.pos_idx, pk.pos_val, pk.k, pk.k_dev, fl, nullptr,
                                          nullptr, nullptr, 0, true);

@@ -192,7 +192,7 @@ queen_status queen_apply_frame(queen_ctx* ctx, queen_gaussians* scene, const que
     ctx->prof.begin(ST_APPLY, static_cast<cudaStream_t>(stream));
     cudaError_t e = launch_decode_apply(*pkt, scene->planes, nullptr, nullptr, true, true, flags_of(ctx),
                                         static_cast<cudaStream_t>(stream));
-    ctx->prof.end(static_cast<cudaStream_t>(stream), pkt->pos_kind == QUEEN_POS_COO && pkt->k > 0 ? 2 : 1);
+    ctx->prof.end(static_cast<cudaStream_t>(stream), 1);  // decode + apply + gates / COO scatter: one launch
     if (e != cudaSuccess) return cuda_fail(ctx, e, "apply");
     return QUEEN_OK;
 }
@@ -279,13 +279,11 @@ static queen_status rasterize_impl(queen_ctx* ctx, const queen_proj* proj, const
     if (!proj || !bins || !(rgb_out || rgb8_out) || !bg) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
     if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
     const uint32_t* vals = bins->sorted_in_alt ? bins->vals_alt : bins->vals;
-    ctx->prof.begin(ST_BLEND, static_cast<cudaStream_t>(stream));
     int nl = 1;
     cudaError_t e = launch_rasterize(proj->rec, proj->n_pad, bins->ranges, vals, n_views, cams[0].width, cams[0].height,
                                      bg[0], bg[1], bg[2], rgb_out, T_out, rgb8_out, rgb8_out ? OUT_RGB8 : OUT_F32, 0.f,
                                      order_scratch(ctx, n_views, cams[0].width, cams[0].height),
-                                     static_cast<cudaStream_t>(stream), &nl);
-    ctx->prof.end(static_cast<cudaStream_t>(stream), nl);
+                                     static_cast<cudaStream_t>(stream), &nl, &ctx->prof);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "rasterize");
     return QUEEN_OK;
 }
@@ -547,7 +545,7 @@ queen_status queen_render_mask(queen_ctx* ctx, const queen_gaussians* scene, con
     ctx->prof.begin(ST_BLEND, s);
     int nl = 1;
     e = launch_rasterize(pj.rec, pj.n_pad, b.ranges, vals, n_views, W, H, 0.f, 0.f, 0.f, nullptr, nullptr, mask_out,
-                         OUT_MASK, alpha_thresh, order_scratch(ctx, n_views, W, H), s, &nl);
+                         OUT_MASK, alpha_thresh, order_scratch(ctx, n_views, W, H), s, &nl, nullptr);
     if (e == cudaSuccess) e = launch_dilate(mask_out, reinterpret_cast<uint8_t*>(ws + L.mask_tmp), n_views, W, H, dilation, s);
     ctx->prof.end(s, nl + (dilation > 1 ? 2 : 0));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "render_mask");

@@ -253,7 +253,7 @@ __device__ __forceinline__ bool touches(const float4& a, const float4& q, float 
 
 // Stage profiler: CUDA events recorded on the launching stream at stage boundaries
 // (enabled by queen_profile_enable; used by bench.py for per-kernel durations).
-enum Stage { ST_APPLY = 0, ST_PROJECT, ST_COMPACT, ST_DEPTH_SORT, ST_DUPLICATE, ST_TILE_SORT, ST_RANGES, ST_BLEND, ST_ENTROPY, ST_COUNT };
+enum Stage { ST_APPLY = 0, ST_PROJECT, ST_COMPACT, ST_DEPTH_SORT, ST_DUPLICATE, ST_TILE_SORT, ST_RANGES, ST_BLEND, ST_ENTROPY, ST_BLEND_ORDER, ST_COUNT };
 struct Prof {
     bool on = false;
     std::vector<cudaEvent_t> pool;
@@ -330,7 +330,7 @@ enum : int { OUT_F32 = 0, OUT_MASK = 1, OUT_RGB8 = 2 };  // k_blend epilogues
 cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
                              uint8_t* out8, int out_mode, float mask_thresh, uint32_t* order_ws, cudaStream_t s,
-                             int* n_launch = nullptr);
+                             int* n_launch = nullptr, Prof* prof = nullptr);
 // blend schedule: *order = longest-list-first permutation of the blocks gt tiles (in order_ws),
 // or nullptr (grid order) when there is no scratch
 cudaError_t launch_tile_order(const uint32_t* ranges, int64_t blocks, uint32_t* order_ws, cudaStream_t s,
