@@ -75,6 +75,11 @@ __device__ __forceinline__ void composite2(Px2& p, float q0, float q1, bool h0, 
     p.T = __fmul2_rn(p.T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
 }
 
+#ifndef QUEEN_BLEND_UNCOND
+#define QUEEN_BLEND_UNCOND 1
+#endif
+constexpr bool BLEND_UNCOND = QUEEN_BLEND_UNCOND;
+
 template <bool COUNT, int RPT, bool WMASK>
 __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ rec, int n_pad, const uint2* __restrict__ ranges,
                                                     const uint32_t* __restrict__ vals, int W, int H, int gx, int T, float bg0,
@@ -88,7 +93,7 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
     __shared__ __align__(16) float4 sA[2][BATCH];  // u, v, hx, hy
     __shared__ __align__(16) float4 sB[2][BATCH];  // A2, B2, C2, T2
     __shared__ __align__(16) float4 sC[2][BATCH];  // o, r, g, b
-    __shared__ uint8_t s_list[NT / 32][BATCH];         // per-warp record list of the batch
+    __shared__ uint16_t s_list[NT / 32][BATCH];        // per-warp record list of the batch (byte offsets q * 16)
     const int gt = order ? (int)order[blockIdx.x] : (int)blockIdx.x;
     const int v = gt / T;
     const int t = gt - v * T;
@@ -171,7 +176,7 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
             // (test_gpu_parity::test_blend_warp_mask_is_exact).
             const float wx0 = (float)((t % gx) * 16), wy0 = (float)((t / gx) * 16 + (threadIdx.x >> 5) * (32 / 16) * RPT);
             // the warp's record list (batch order) in shared memory
-            uint8_t* lst = s_list[threadIdx.x >> 5];
+            uint16_t* lst = s_list[threadIdx.x >> 5];
             int nq = 0;
 #pragma unroll
             for (int e = 0; e < BATCH / 32; ++e) {
@@ -179,14 +184,16 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
                 bool want = q < cnt;
                 if (WMASK && want) want = touches(sA[s][q], sB[s][q], wx0, wx0 + 15.0f, wy0, wy0 + (float)((32 / 16) * RPT - 1));
                 const uint32_t bal = __ballot_sync(0xffffffffu, want);
-                if (want) lst[nq + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = (uint8_t)q;
+                if (want) lst[nq + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = (uint16_t)(q * 16);
                 nq += __popc(bal);
             }
             __syncwarp();
 #pragma unroll 2
             for (int i = 0; i < nq; ++i) {
-                const int q = lst[i];
-                const float4 a = sA[s][q];  // u, v, hx, hy
+                // records addressed by byte offset (no per-record index scaling)
+                const uint32_t qo = lst[i];
+#define QREC(arr) (*reinterpret_cast<const float4*>(reinterpret_cast<const char*>(arr[s]) + qo))
+                const float4 a = QREC(sA);  // u, v, hx, hy
                 const float dx = a.x - fx;
                 if (COUNT) {
 #pragma unroll
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
                 // satisfies |dx| <= hx and |dy| <= hy, K7; this thread's rows are
                 // fyc +- hspan).  Skips never change a decision.
                 if (!COUNT && !WMASK && (fabsf(dx) > a.z || fabsf(a.y - fyc) > a.w + hspan)) continue;
-                const float4 bq = sB[s][q];  // A2, B2, C2, T2
+                const float4 bq = QREC(sB);  // A2, B2, C2, T2
                 const float tAdx = (bq.x * dx) * dx;
                 const float tB = bq.y * dx;
                 const float2 vv = make_float2(a.y, a.y);
@@ -219,19 +226,22 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
                     for (int r = 0; r < RPT; ++r) cpn += (int)h[r];
                 }
                 if (anyh) {
-                    const float4 c = sC[s][q];  // o, r, g, b
+                    const float4 c = QREC(sC);  // o, r, g, b
+                    // BLEND_UNCOND: every row pair composites once any lane hits (a non-hitting
+                    // row gets alpha = +0, bit-identical); otherwise branch per row pair
                     if (c.x > 0.98f) {
 #pragma unroll
                         for (int k = 0; k < NP; ++k)
-                            if (h[2 * k] | h[2 * k + 1])
+                            if (BLEND_UNCOND || (h[2 * k] | h[2 * k + 1]))
                                 composite2<true>(p[k], qq[k].x, qq[k].y, h[2 * k], h[2 * k + 1], c);
                     } else {
 #pragma unroll
                         for (int k = 0; k < NP; ++k)
-                            if (h[2 * k] | h[2 * k + 1])
+                            if (BLEND_UNCOND || (h[2 * k] | h[2 * k + 1]))
                                 composite2<false>(p[k], qq[k].x, qq[k].y, h[2 * k], h[2 * k + 1], c);
                     }
                 }
+#undef QREC
             }
         }
         __syncthreads();

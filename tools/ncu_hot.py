@@ -20,7 +20,7 @@ src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 h = rows[1]
-data = rows[2:]
+data = [r for r in rows[2:] if len(r) == len(h)]
 iS, iE, iW = h.index("Source"), h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
 tw = sum(int(r[iW]) for r in data if r[iW].isdigit()) or 1
 te = sum(int(r[iE]) for r in data if r[iE].isdigit()) or 1
