@@ -62,10 +62,11 @@ static void normalise(const uint64_t cnt[256], uint64_t total, uint16_t f[256]) 
 }
 
 // ---------------------------------------------------------------- device decoder
-// Two launches per frame: k_ans_table builds every category's slot table once (slot ->
-// packed (symbol | (f - 1) << 8 | (slot - c) << 20), 4096 x u32 = 16 KB per category, in the
-// workspace); k_ans_decode copies its category's table to shared memory and decodes, one warp
-// per chunk, one rANS state per lane: a decode step is ONE shared load + a multiply-add.
+// Two launches per frame: k_ans_table builds every category's slot tables once (slot ->
+// f | (slot - c) << 16 as u32, and slot -> the decoded int8 latent, 20 KB per category, in the
+// workspace); k_ans_decode copies its category's tables to shared memory and decodes, one warp
+// per chunk, one rANS state per lane: a decode step is ONE shared load + a multiply-add on the
+// state's critical path (the symbol byte is looked up beside it).
 constexpr int ANS_WARPS = 4;
 
 struct AnsFrame {
@@ -74,7 +75,7 @@ struct AnsFrame {
     int row0[5];          // first latent row of the category in the [sum L][n_pad] matrix
     int block0[6];        // first block of each category (prefix), block0[5] = total blocks
     int n, n_pad;
-    const uint32_t* table;  // [5][ANS_M] packed slot tables (k_ans_table)
+    const uint32_t* table;  // [5][ANS_M] (f | (slot - c) << 16), then [5][ANS_M] int8 symbols (k_ans_table)
 };
 
 __global__ void __launch_bounds__(256) k_ans_table(const AnsFrame fr, uint32_t* __restrict__ table, DevFlags* fl) {
@@ -107,11 +108,13 @@ __global__ void __launch_bounds__(256) k_ans_table(const AnsFrame fr, uint32_t* 
         if (s_c[mid] <= slot) lo = mid; else hi = mid;
     }
     const uint32_t f = s_f[lo];
-    table[(size_t)cat * ANS_M + slot] = (uint32_t)lo | ((f ? f - 1 : 0) << 8) | ((slot - s_c[lo]) << 20);
+    table[(size_t)cat * ANS_M + slot] = f | ((slot - s_c[lo]) << 16);
+    reinterpret_cast<int8_t*>(table + 5 * ANS_M)[(size_t)cat * ANS_M + slot] = (int8_t)(lo - 128);
 }
 
 __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr, int8_t* __restrict__ out, DevFlags* fl) {
     __shared__ uint32_t s_tab[ANS_M];
+    __shared__ int8_t s_sym[ANS_M];
     int cat = 0;
     while (cat < 4 && (int)blockIdx.x >= fr.block0[cat + 1]) ++cat;
     const unsigned char* stream = fr.stream[cat];
@@ -123,6 +126,9 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
         const uint4* src = reinterpret_cast<const uint4*>(fr.table + (size_t)cat * ANS_M);
         uint4* dst = reinterpret_cast<uint4*>(s_tab);
         for (int q = threadIdx.x; q < ANS_M / 4; q += blockDim.x) dst[q] = __ldg(src + q);
+        const uint4* ssrc = reinterpret_cast<const uint4*>(reinterpret_cast<const int8_t*>(fr.table + 5 * ANS_M) +
+                                                           (size_t)cat * ANS_M);
+        for (int q = threadIdx.x; q < ANS_M / 16; q += blockDim.x) reinterpret_cast<uint4*>(s_sym)[q] = __ldg(ssrc + q);
     }
     __syncthreads();
     const uint32_t chunk = (blockIdx.x - fr.block0[cat]) * ANS_WARPS + (threadIdx.x >> 5);
@@ -139,7 +145,9 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
     const uint32_t len = min((uint32_t)ANS_CHUNK, n_sym - base);
     const uint32_t steps = (len + 31) / 32;
     const uint32_t lt = (1u << lane) - 1u;
-    uint32_t k = (base + lane) / (uint32_t)n, i = (base + lane) - k * (uint32_t)n;
+    const uint32_t k = (base + lane) / (uint32_t)n;
+    uint32_t i = (base + lane) - k * (uint32_t)n;
+    int8_t* op = cout + (size_t)k * n_pad + i;  // this lane's next output byte (row k, column i)
     // The chunk's renormalisation words are consumed in order, ~1 per step for the warp.
     // Keep a 128-word window in registers (4 words per lane: current 64 + next 64), so a
     // renormalisation is a shuffle, and the next 64 words load one window ahead.
@@ -148,10 +156,12 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
     uint32_t c0 = ld(wbase + lane), c1 = ld(wbase + 32 + lane), n0 = ld(wbase + 64 + lane), n1 = ld(wbase + 96 + lane);
     for (uint32_t t = 0; t < steps; ++t) {
         const bool active = t * 32 + lane < len;
+        const uint32_t slot = x & (ANS_M - 1);
+        const uint32_t e = s_tab[slot];
+        const uint32_t xn = (e & 0xffffu) * (x >> ANS_PROB_BITS) + (e >> 16);
         if (active) {
-            const uint32_t e = s_tab[x & (ANS_M - 1)];
-            x = ((e >> 8 & 0xfffu) + 1u) * (x >> ANS_PROB_BITS) + (e >> 20);
-            cout[(size_t)k * n_pad + i] = (int8_t)((int)(e & 0xffu) - 128);
+            x = xn;
+            *op = s_sym[slot];
         }
         const bool need = active && x < ANS_L;
         const uint32_t m = __ballot_sync(0xffffffffu, need);
@@ -172,7 +182,8 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
             }
         }
         i += 32;  // next symbol of this lane: flat index + 32
-        while (i >= (uint32_t)n) { i -= (uint32_t)n; ++k; }
+        op += 32;
+        while (i >= (uint32_t)n) { i -= (uint32_t)n; op += n_pad - n; }
     }
     if (ptr != end || x != ANS_L) raise_flag(fl, FLAG_INDEX);  // corrupt / mismatched stream
 }
