@@ -75,6 +75,10 @@ __device__ __forceinline__ void composite2(Px2& p, float q0, float q1, bool h0, 
     p.T = __fmul2_rn(p.T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
 }
 
+#ifndef QUEEN_BLEND_UNROLL
+#define QUEEN_BLEND_UNROLL 4  // measured n3dv blend: 1 -> 1.423 ms, 2 -> 1.410, 4 -> 1.399
+#endif
+constexpr int BLEND_UNROLL = QUEEN_BLEND_UNROLL;  // record-loop unroll
 #ifndef QUEEN_BLEND_UNCOND
 #define QUEEN_BLEND_UNCOND 1
 #endif
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ 
                 nq += __popc(bal);
             }
             __syncwarp();
-#pragma unroll 2
+#pragma unroll BLEND_UNROLL
             for (int i = 0; i < nq; ++i) {
                 // records addressed by byte offset (no per-record index scaling)
                 const uint32_t qo = lst[i];
