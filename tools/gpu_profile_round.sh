@@ -13,3 +13,5 @@ echo "launches rc=$?"
 timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_" -s 60 -c 22 -f -o gpurun_out/${R}_full_n3dv \
   python tools/stage_times.py n3dv 1 > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:k_ans -c 2 -f -o gpurun_out/${R}_full_ans python tools/ans_time.py n3dv 1 > gpurun_out/ncu_ans.log 2>&1
+echo "ans rc=$?"
