@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-libsort", action="store_true", help="skip the torch.sort (CUB) comparison")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="serial frame steps (decode + apply, then render) instead of decoding/applying frame "
+                         "t+1 under the blend of frame t")
     ap.add_argument("--no-paper-style", action="store_true", help="skip the decode + 1 centre view timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -447,23 +450,44 @@ def main():
     prof, n_prof_frames = {}, args.steps
     eager = None
     clocks = ClockSampler(local)
+    pipeline = not args.no_pipeline and player.n_lanes == 1
     if use_graph:
         player.profile_read(reset=True)
         # N = 1: one graph per resident packet (at most one per timed step, so every graph's
         # profiler events are last recorded inside the timed region); N > 1: one per slot
         ng = len(dps) if world > 1 else max(1, min(len(dps), args.steps))
-        graphs = [player.capture(d, profile=not args.no_profile) for d in dps[:ng]]
-        player.planes.copy_(torch.from_numpy(sc.planes).to(dev))
-        for g in graphs:  # every graph replayed once before the warm-up proper
-            g.replay()
-        player.planes.copy_(torch.from_numpy(sc.planes).to(dev))
-        for t in range(args.warmup):
-            bcast(t)
-            graphs[t % len(graphs)].replay()
+        A0 = torch.from_numpy(sc.planes).to(dev)
+        if pipeline:
+            # pipelined step t (runtime.Player.capture_step): render frame t, and decode + apply
+            # packet t+1 under its blend; graph j applies packet slot j.  Frame 0 = A_0 + packet 0
+            # (serial, before the warm-up), so step t always renders a fully applied frame t.
+            graphs = [player.capture_step(d, profile=not args.no_profile) for d in dps[:ng]]
+            player.planes.copy_(A0)
+            for g in graphs:  # every graph replayed once before the warm-up proper
+                g.replay()
+            player.planes.copy_(A0)
+            bcast(0)
+            player.apply(dps[0])
+            for t in range(args.warmup):
+                bcast(t + 1)
+                graphs[(t + 1) % len(graphs)].replay()
 
-        def gstep(t):
-            bcast(t)
-            graphs[t % len(graphs)].replay()
+            def gstep(t):
+                bcast(t + 1)
+                graphs[(t + 1) % len(graphs)].replay()
+        else:
+            graphs = [player.capture(d, profile=not args.no_profile) for d in dps[:ng]]
+            player.planes.copy_(A0)
+            for g in graphs:  # every graph replayed once before the warm-up proper
+                g.replay()
+            player.planes.copy_(A0)
+            for t in range(args.warmup):
+                bcast(t)
+                graphs[t % len(graphs)].replay()
+
+            def gstep(t):
+                bcast(t)
+                graphs[t % len(graphs)].replay()
         total_ms, med_ms, clk = timed_loop(gstep, clocks)
         if not args.no_profile:
             prof = player.profile_read(reset=True)
@@ -700,13 +724,17 @@ def main():
         s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
 
-        def stream_frames(k0: int, n: int):
-            """Frames k0 .. k0+n-1 through the pipeline; returns (t0, t1, lat0, lat1) events."""
-            ev_h2d = [ev() for _ in range(n)]
-            ev_apply = [ev() for _ in range(n)]
+        def stream_frames(k0: int, n: int, first: bool):
+            """Frames k0 .. k0+n-1 through the pipeline; returns (t0, t1, lat0, lat1) events.
+            Pipelined (default): step q renders frame k = k0+q and, on the player's side stream,
+            decodes + applies packet k+1 under that frame's blend (runtime.Player.step); the H2D of
+            packet k+1 into its slot waits until the packet two frames back has been applied.
+            first: frame k0 = A_0 + packet k0, uploaded and applied before the first step."""
+            ev_h2d = [ev() for _ in range(n + 1)]   # packet k0 + i uploaded
+            ev_step = [ev() for _ in range(n)]      # step q done (incl. the apply of packet k+1)
             ev_render = [ev() for _ in range(n)]
             ev_d2h = [ev() for _ in range(n)]
-            lat0 = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+            lat0 = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
             lat1 = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if world > 1:
@@ -715,27 +743,42 @@ def main():
             t0.record(stream)
             s_h2d.wait_stream(stream)
             s_d2h.wait_stream(stream)
+
+            def upload(i):  # packet k0 + i into slot (k0 + i) % 2
+                k = k0 + i
+                with torch.cuda.stream(s_h2d):
+                    if i >= 2:
+                        s_h2d.wait_event(ev_step[i - 2])  # the slot's previous packet (k - 2) is applied
+                    lat0[i].record(s_h2d)
+                    if rank == 0:
+                        ub = used_bytes[k % P]  # only the bytes the packet uses cross PCIe
+                        recv[k % 2][:ub].copy_(pin_pk[k % P][:ub], non_blocking=True)
+                    ev_h2d[i].record(s_h2d)
+                if world > 1 or not pipeline or i == 0:
+                    stream.wait_event(ev_h2d[i])  # else only the decoding side stream waits (step(ready=))
+                if world > 1:
+                    dist.broadcast(recv[k % 2], 0)
+
+            if first or not pipeline:
+                upload(0)
+                player.apply(dp_recv[k0 % 2])
             for q in range(n):
                 k = k0 + q
                 slot = k % 2
-                with torch.cuda.stream(s_h2d):
-                    if q >= 2:
-                        s_h2d.wait_event(ev_apply[q - 2])  # recv[slot] consumed by frame k-2
-                    lat0[q].record(s_h2d)
-                    if rank == 0:
-                        ub = used_bytes[k % P]  # only the bytes the packet uses cross PCIe
-                        recv[slot][:ub].copy_(pin_pk[k % P][:ub], non_blocking=True)
-                    ev_h2d[q].record(s_h2d)
-                stream.wait_event(ev_h2d[q])
-                if world > 1:
-                    dist.broadcast(recv[slot], 0)
-                player.apply(dp_recv[slot])
-                ev_apply[q].record(stream)
                 if q >= 2:
                     stream.wait_event(ev_d2h[q - 2])  # out_dev[slot] drained to the host
-                player.render(out=out_dev[slot], rgb8=rgb8)
-                ev_render[q].record(stream)
+                if pipeline:
+                    upload(q + 1)
+                    player.step(dp_recv[(k + 1) % 2], out=out_dev[slot], rgb8=rgb8, rendered=ev_render[q],
+                                ready=ev_h2d[q + 1] if world == 1 else None)
+                else:
+                    if q >= 1:
+                        upload(q)
+                        player.apply(dp_recv[slot])
+                    player.render(out=out_dev[slot], rgb8=rgb8)
+                    ev_render[q].record(stream)
                 lat1[q].record(stream)
+                ev_step[q].record(stream)
                 with torch.cuda.stream(s_d2h):
                     s_d2h.wait_event(ev_render[q])
                     out_host[slot].copy_(out_dev[slot], non_blocking=True)
@@ -745,13 +788,16 @@ def main():
                 stream.wait_event(ev_d2h[n - 2])
             t1.record(stream)
             torch.cuda.synchronize()
-            return t0, t1, lat0, lat1
+            # latency of frame k0+q: its packet's upload start -> rendered (frame k0 is only
+            # uploaded when first / serial)
+            pairs = [(lat0[q], lat1[q]) for q in range(n) if q > 0 or first or not pipeline]
+            return t0, t1, [a for a, _ in pairs], [b for _, b in pairs]
 
         # restart the sequence from A_0 so the streamed frames are the same ones; W untimed
         # warm-up frames (first launches, lazy module loading), then the K timed frames
         player.planes.copy_(torch.from_numpy(sc.planes).to(dev))
-        stream_frames(0, args.warmup)
-        t0, t1, lat0, lat1 = stream_frames(args.warmup, args.steps)
+        stream_frames(0, args.warmup, first=True)
+        t0, t1, lat0, lat1 = stream_frames(args.warmup, args.steps, first=False)
         lat_med = statistics.median(a.elapsed_time(b) for a, b in zip(lat0, lat1))
         e_ms = torch.tensor([t0.elapsed_time(t1), lat_med], dtype=torch.float64, device=dev)
         if world > 1:
@@ -794,7 +840,9 @@ def main():
                        "gaussians": cfg.n, "views": V, "width": W, "height": H, "views_per_batch": player.vpb, "render_lanes": player.n_lanes,
                        "parallelism": f"views sharded v mod {world}, Gaussians replicated, packet NCCL-broadcast",
                        "packet_format": args.packet_format,
-                       "launch": "CUDA-graph replay (one graph per packet slot)" if use_graph else "eager",
+                       "launch": ("CUDA-graph replay (one graph per packet slot)" if use_graph else "eager") +
+                                 ("; pipelined: decode + apply of frame t+1 under the blend of frame t"
+                                  if use_graph and pipeline else "; serial frame steps"),
                        "l2": "flushed between timed steps (512 MB write outside the step events)"},
             "packet_bytes_per_frame": int(statistics.mean(used_bytes)) if used_bytes else None,
             "mpixel_per_s": mpix, "view_fps": value * V,

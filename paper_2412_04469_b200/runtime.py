@@ -229,6 +229,61 @@ class Player:
                               stream=stream, cam_array=arr)
         return out
 
+    def step(self, next_pkt, out=None, rgb8: bool = False, rendered: torch.cuda.Event | None = None,
+             ready: torch.cuda.Event | None = None):
+        """Pipelined frame step: render the current scene A_t on the current stream and, on a side
+        stream, (entropy-)decode next_pkt and apply it (A_t -> A_{t+1}) once this render's
+        binning -- the last read of A_t -- is done (queen_wait_binned), i.e. under the blend of
+        frame t.  The current stream then waits for the apply, so the next step renders A_{t+1}.
+        `rendered` (optional) is recorded on the current stream right after the render; the side
+        stream waits for `ready` (optional, e.g. the packet's H2D on a copy stream) before decoding.
+        The images are bit-identical to apply(next) after render() (tested)."""
+        if self.n_lanes != 1:
+            raise ValueError("pipelined steps need a single render lane")
+        main = torch.cuda.current_stream(self.dev)
+        if not hasattr(self, "_side"):
+            # high priority: the decode/apply blocks are dispatched ahead of the blend's queued
+            # blocks as SM slots free up, instead of after the whole blend grid
+            self._side = torch.cuda.Stream(device=self.dev, priority=-1)
+        side = self._side
+        side.wait_stream(main)  # the packet (H2D / broadcast) and the previous step are ordered first
+        rgb = self.render(out=out, rgb8=rgb8)
+        if rendered is not None:
+            rendered.record(main)
+        if next_pkt is not None:
+            with torch.cuda.stream(side):
+                if ready is not None:
+                    side.wait_event(ready)
+                # decode + apply run under the blend only (the binning stages are latency-bound
+                # and slow down when shared; measured: decoding from the step's start cost the
+                # binning ~60 us per N3DV frame)
+                queen_wait_binned(self.ctx, side)
+                if isinstance(next_pkt, EntropyPacket):
+                    next_pkt.decode(self.ctx, side)
+                queen_apply_frame(self.ctx, self.scene, next_pkt.struct, side)
+            main.wait_stream(side)
+        return rgb
+
+    def capture_step(self, next_pkt, out=None, rgb8: bool = False, profile: bool = False):
+        """CUDA graph of one pipelined step (see step()): render of the current scene + decode and
+        apply of next_pkt under its blend.  Replaying it advances the scene by one frame."""
+        g = torch.cuda.CUDAGraph()
+        self.profile(False)
+        side = torch.cuda.Stream(device=self.dev)
+        side.wait_stream(torch.cuda.current_stream(self.dev))
+        saved = self.planes.clone()
+        with torch.cuda.stream(side):  # warm-up outside capture (allocator, lazy init)
+            self.step(next_pkt, out=out, rgb8=rgb8)
+        torch.cuda.current_stream(self.dev).wait_stream(side)
+        torch.cuda.synchronize(self.dev)
+        self.planes.copy_(saved)  # the warm-up advanced the scene: restore it
+        if profile:
+            self.profile(True)
+        with torch.cuda.graph(g):
+            self.step(next_pkt, out=out, rgb8=rgb8)
+        self.profile(False)
+        return g
+
     def frame(self, pkt: DevicePacket | None, stream=None):
         if pkt is not None:
             self.apply(pkt, stream)

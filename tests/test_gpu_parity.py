@@ -516,6 +516,53 @@ def test_cuda_graph_frame_equals_eager():
     assert graphed.check_status()[0] == 0
 
 
+def test_pipelined_steps_equal_serial_frames():
+    """Pipelined steps (Player.step / capture_step: frame t rendered while packet t+1 is decoded
+    and applied on a side stream after the render's binning) give, frame by frame, the same
+    images and final SoA, bit for bit, as serial apply-then-render; also with two view batches
+    (the apply waits for the LAST batch's binning)."""
+    import paper_2412_04469_b200 as Q
+    from paper_2412_04469_b200 import packet as wire
+    from paper_2412_04469_b200.runtime import EntropyPacket, Player
+    cfg, sc, cams = _render_case("n3dv", 20003, 3, width=333, height=250, focal=280.0)
+    pkts = [synth.make_packet(sc, t) for t in (1, 2, 3, 4)]
+    streams = [wire.ans_streams(p, Q.queen_entropy_encode) for p in pkts]
+    cap = [max(s[c].size for s in streams) for c in range(5)]
+    kc = max(p.k for p in pkts)
+    bufs = [wire.pack_entropy(p, s, frame=t + 1, k_cap=kc, ans_cap=cap) for t, (p, s) in enumerate(zip(pkts, streams))]
+    hdr = wire.header_entropy(bufs[0])
+    eps = [EntropyPacket(torch.from_numpy(b).cuda(), hdr) for b in bufs]
+    for vpb in (None, 2):
+        serial = Player(sc.planes, sc.n, sc.deg, cams, views_per_batch=vpb)
+        serial.fit_capacity()
+        refs = []
+        for ep in eps:
+            serial.apply(ep)
+            refs.append(serial.render().clone())
+        # eager pipelined steps
+        pipe = Player(sc.planes, sc.n, sc.deg, cams, keys_cap=serial.keys_cap, views_per_batch=vpb)
+        pipe.apply(eps[0])
+        for t in range(len(eps)):
+            out = pipe.step(eps[t + 1] if t + 1 < len(eps) else None, out=torch.empty_like(pipe.rgb))
+            torch.cuda.synchronize()
+            assert torch.equal(out, refs[t]), (vpb, t)
+        assert torch.equal(pipe.planes, serial.planes)
+        assert pipe.check_status()[0] == 0
+        # graph replays of the pipelined step (graph j applies packet j)
+        gp = Player(sc.planes, sc.n, sc.deg, cams, keys_cap=serial.keys_cap, views_per_batch=vpb)
+        graphs = [gp.capture_step(ep) for ep in eps]
+        gp.planes.copy_(torch.from_numpy(sc.planes).cuda())
+        gp.apply(eps[0])
+        for t in range(len(eps) - 1):
+            graphs[t + 1].replay()
+            torch.cuda.synchronize()
+            assert torch.equal(gp.rgb, refs[t]), (vpb, t)
+        gp.render()
+        torch.cuda.synchronize()
+        assert torch.equal(gp.rgb, refs[-1])
+        assert gp.check_status()[0] == 0
+
+
 def test_depth_keys_spanning_more_than_27_bits():
     """Depth keys relative to the smallest depth: when the scene's depths span more than 2^27
     float ulps (z from 0.3 to 1e6) the 4th depth pass (bits 27..31) is a real pass, otherwise a
