@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-libsort", action="store_true", help="skip the torch.sort (CUB) comparison")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
+    ap.add_argument("--as-rank", default=None, metavar="R/N",
+                    help="diagnostic: one process renders rank R's views of an N-GPU run (no NCCL); "
+                         "predicts the per-rank frame time of the scaling run")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="serial frame steps (decode + apply, then render) instead of decoding/applying frame "
                          "t+1 under the blend of frame t")
@@ -339,7 +342,11 @@ def main():
     sc = synth.make_scene(cfg)
     cams_all = synth.make_cameras(cfg)
     V = len(cams_all)
-    mine = rank_views(V, rank, world)
+    if args.as_rank:
+        r_, n_ = (int(x) for x in args.as_rank.split("/"))
+        mine = rank_views(V, r_, n_)
+    else:
+        mine = rank_views(V, rank, world)
     cams = [cams_all[v] for v in mine]
     W, H = cfg.width, cfg.height
     vpb = args.views_per_batch or min(len(cams), default_vpb(cfg))
@@ -843,7 +850,8 @@ def main():
                        "launch": ("CUDA-graph replay (one graph per packet slot)" if use_graph else "eager") +
                                  ("; pipelined: decode + apply of frame t+1 under the blend of frame t"
                                   if use_graph and pipeline else "; serial frame steps"),
-                       "l2": "flushed between timed steps (512 MB write outside the step events)"},
+                       "l2": "flushed between timed steps (512 MB write outside the step events)",
+                       **({"as_rank": f"{args.as_rank}: diagnostic, this rank's views only, no NCCL"} if args.as_rank else {})},
             "packet_bytes_per_frame": int(statistics.mean(used_bytes)) if used_bytes else None,
             "mpixel_per_s": mpix, "view_fps": value * V,
             "status": Q.STATUS.get(st, st),
