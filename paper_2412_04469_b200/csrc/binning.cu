@@ -490,13 +490,9 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
     const uint32_t ntiles = (Kn + TILE - 1) / TILE;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    if (triv && triv[0] == Kn) {  // every key has digit 0: the stable pass is the identity -- copy
-        for (uint64_t q = (uint64_t)blockIdx.x * NT + threadIdx.x; q < Kn; q += (uint64_t)gridDim.x * NT) {
-            if (MODE == OS_KV) { kout[q] = kin[q]; vout[q] = vin[q]; }
-            if (MODE == OS_V) vout[q] = vin[q];
-        }
-        return;
-    }
+    // every key has digit 0: the stable pass is the identity -- nothing is written, and the
+    // consumer (k_scan_dup) reads the pass's input buffer instead (same test on the device)
+    if (triv && triv[0] == Kn) return;
     const bool owns_digits = threadIdx.x * DPT < BINS;
 #if QUEEN_OS_MATCH_OR
     // warp match by shared-memory atomicOr (experiment knob): the per-warp match words live in
@@ -665,7 +661,9 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
 // ---------------------------------------------------------------------------
 constexpr size_t DUP_SMEM = (size_t)SORT_TILE * (4 + 4 + 4 + 2) + 16;
 
-__global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __restrict__ dvals, const uint32_t* count_ptr,
+__global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __restrict__ dvals_a,
+                                                           const uint32_t* __restrict__ dvals_b,
+                                                           const uint32_t* __restrict__ triv, const uint32_t* count_ptr,
                                                            const short4* __restrict__ rect, int n_pad, int gx, int gy,
                                                            uint32_t T, uint32_t* __restrict__ keys,
                                                            uint32_t* __restrict__ vals, uint32_t cap,
@@ -679,6 +677,8 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
     __shared__ unsigned long long s_prefix;
     const uint32_t M = *count_ptr;
     const uint32_t ntiles = (M + SORT_TILE - 1) / SORT_TILE;
+    // the last depth pass skipped (identity) when its digit histogram says so: its input holds the order
+    const uint32_t* __restrict__ dvals = triv[0] == M ? dvals_a : dvals_b;
     if (threadIdx.x == 0) s_tile = atomicAdd(&fl->tickets[TK_DUP], 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
@@ -936,7 +936,8 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     prof->begin(ST_DEPTH_SORT, s);
     // depth keys are relative to the batch's smallest visible depth (order-preserving, and the
     // range of a scene's depths fits 27 bits unless it spans > 2^27 ulps): three 9-bit passes,
-    // then bits 27..31, which is a copy (triv) whenever that digit is 0 for every key
+    // then bits 27..31, which is skipped (no copy; the duplication reads the previous buffer)
+    // whenever that digit is 0 for every key
     k_hist_scan<<<1, 32 * DEPTH_PASSES, 0, s>>>(hist, hist_excl, DEPTH_PASSES, MAX_BINS);
     int cur = 0;
     for (int p = 0; p < DEPTH_PASSES; ++p) {
@@ -953,7 +954,8 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     // offsets in depth order + duplication
     prof->begin(ST_DUPLICATE, s);
     if (elem_tiles > 0)
-        k_scan_dup<<<(unsigned)elem_tiles, SORT_THREADS, DUP_SMEM, s>>>(dv[cur], Md,
+        k_scan_dup<<<(unsigned)elem_tiles, SORT_THREADS, DUP_SMEM, s>>>(dv[cur ^ 1], dv[cur],
+                                                                         hist + (DEPTH_PASSES - 1) * MAX_BINS, Md,
                                                                          reinterpret_cast<const short4*>(proj.rect),
                                                                          proj.n_pad, gx, gy, (uint32_t)T, bins.keys,
                                                                          bins.vals, cap, dup_lb, fl, Kd);

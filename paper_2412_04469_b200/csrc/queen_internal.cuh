@@ -89,6 +89,9 @@ struct BinPlan {
     bool ok;
     int64_t S, spv, slabs;  // slab size, slabs per view, slabs in the batch
 };
+#ifndef QUEEN_SLABS_PER_VIEW
+#define QUEEN_SLABS_PER_VIEW 32
+#endif
 inline BinPlan bin_plan(int64_t n_pad, int64_t n_views, int W, int H) {
     const int64_t gx = (W + 15) / 16, gy = (H + 15) / 16;
     BinPlan p{};
@@ -96,7 +99,7 @@ inline BinPlan bin_plan(int64_t n_pad, int64_t n_views, int W, int H) {
     // ~32 slabs per view (S depends on n_pad only, so a smaller batch never needs more
     // slab-count space than the workspace was carved for), multiples of 1024 in [2048, 65536]
     (void)n_views;
-    int64_t S = (n_pad + 31) / 32;
+    int64_t S = (n_pad + QUEEN_SLABS_PER_VIEW - 1) / QUEEN_SLABS_PER_VIEW;
     S = (S + 1023) / 1024 * 1024;
     S = S < 2048 ? 2048 : (S > 65536 ? 65536 : S);
     p.S = S;
