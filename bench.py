@@ -455,6 +455,7 @@ def main():
     # with the stage profiler's events captured inside the graphs (stage times = each graph's
     # last replay, live in the timed region).  --no-graph: eager launches, profiled per step.
     prof, n_prof_frames = {}, args.steps
+    prof_serial = {}
     eager = None
     clocks = ClockSampler(local)
     pipeline = not args.no_pipeline and player.n_lanes == 1
@@ -501,11 +502,19 @@ def main():
             n_prof_frames = len(graphs)
         del graphs
         st, info = player.check_status()
-        # eager launches of the same frames, for comparison (no profiler)
+        # eager SERIAL launches of the same frames (decode + apply, then render), for comparison;
+        # profiled, so each stage's time is also measured with the stage alone on the GPU
+        # (pipelined, the side-stream stages share the GPU with the blend)
         player.planes.copy_(torch.from_numpy(sc.planes).to(dev))
+        if not args.no_profile:
+            player.profile(True)
+            player.profile_read(reset=True)
         e_tot, e_med, _ = timed_loop(step)
+        if not args.no_profile:
+            prof_serial = player.profile_read(reset=True)
+            player.profile(False)
         eager = {"value": args.steps / (e_tot / 1e3), "unit": UNIT, "ms_per_step": e_tot / args.steps,
-                 "note": "the same frames with eager (non-graph) launches"}
+                 "note": "the same frames with eager (non-graph) launches, serial steps (no pipelining)"}
     else:
         if not args.no_profile:
             player.profile(True)
@@ -539,11 +548,15 @@ def main():
 
     peaks, peak_src = load_peaks()
     traffic = load_traffic()
-    stages = {}
-    for name, (ms, launches) in prof.items():
-        if launches:
-            stages[name] = {"ms_per_step": ms / n_prof_frames, "launches_per_step": launches / n_prof_frames,
-                            "us_per_launch": 1e3 * ms / launches}
+    def stage_dict(pr, frames):
+        out = {}
+        for name, (ms, launches) in pr.items():
+            if launches:
+                out[name] = {"ms_per_step": ms / frames, "launches_per_step": launches / frames,
+                             "us_per_launch": 1e3 * ms / launches}
+        return out
+    stages = stage_dict(prof, n_prof_frames)
+    stages_serial = stage_dict(prof_serial, args.steps) if (pipeline and prof_serial) else None
     gpu_launches = int(round(sum(v["launches_per_step"] for v in stages.values()) * args.steps)) if stages else None
     k_coo = host_pkts[0].k if rank == 0 else k_cap
     vpb_list = [len(b) for b in batches]
@@ -579,19 +592,22 @@ def main():
         # HBM stages: algorithmic bytes / measured HBM peak; blend: max(FP32 issue, MUFU) from the
         # exact work counts; stages without a model (ranges) count as their measured time.
         ideal = {}
-        for name, s_ in stages.items():
-            if name == "blend":
-                f_hz = f_mhz * 1e6
-                ideal[name] = 1e3 * max((7 * ev_pairs + 7 * cp_pairs) / (SM_COUNT * 128 * f_hz),
-                                        cp_pairs / (SM_COUNT * 16 * f_hz))
-            else:
+        for table in ([stages, stages_serial] if stages_serial else [stages]):
+            for name, s_ in table.items():
+                if name == "blend":
+                    f_hz = f_mhz * 1e6
+                    idl = 1e3 * max((7 * ev_pairs + 7 * cp_pairs) / (SM_COUNT * 128 * f_hz),
+                                    cp_pairs / (SM_COUNT * 16 * f_hz))
+                else:
+                    b = algorithmic_bytes(name, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b)
+                    idl = 1e3 * b / (peaks["hbm_gbs"] * 1e9) if b else s_["ms_per_step"]
+                if table is stages:
+                    ideal[name] = idl
+                s_["ideal_ms_per_step"] = idl
+                s_["frac"] = idl / s_["ms_per_step"] if s_["ms_per_step"] > 0 else None
                 b = algorithmic_bytes(name, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b)
-                ideal[name] = 1e3 * b / (peaks["hbm_gbs"] * 1e9) if b else s_["ms_per_step"]
-            s_["ideal_ms_per_step"] = ideal[name]
-            s_["frac"] = ideal[name] / s_["ms_per_step"] if s_["ms_per_step"] > 0 else None
-            b = algorithmic_bytes(name, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b)
-            if b and name != "blend":
-                s_["algorithmic_GBps"] = b / (s_["ms_per_step"] * 1e-3) / 1e9
+                if b and name != "blend":
+                    s_["algorithmic_GBps"] = b / (s_["ms_per_step"] * 1e-3) / 1e9
         path = {"ideal_ms": sum(ideal.values()), "frame_ms": total_ms / args.steps,
                 "frac": sum(ideal.values()) / (total_ms / args.steps),
                 "note": "sum of per-stage ideal times (HBM bytes / measured peak; blend FP32-issue/MUFU bound "
@@ -855,7 +871,11 @@ def main():
             "packet_bytes_per_frame": int(statistics.mean(used_bytes)) if used_bytes else None,
             "mpixel_per_s": mpix, "view_fps": value * V,
             "status": Q.STATUS.get(st, st),
-            "keys_per_batch": K_list, "visible_pairs_per_batch": M_list, "stages": stages, "roofline": roof,
+            "keys_per_batch": K_list, "visible_pairs_per_batch": M_list, "stages": stages,
+            **({"stages_serial": {"note": "the same stages in serial eager steps (each stage alone on the GPU); "
+                                          "`stages` is the pipelined headline region, where entropy/apply run on a "
+                                          "side stream under the blend", **stages_serial}} if stages_serial else {}),
+            "roofline": roof,
             "path_roofline": path, "paper_style": paper, "library_sort": libsort, "masked_render": masked, "densify": densify, "backward": backward,
             "eager": eager,
             "e2e_f32": e2e_f32, "cpu_baseline": cpu, "e2e": e2e,
