@@ -35,6 +35,11 @@ __device__ __forceinline__ float ex2b(float x) {
     return y;
 }
 
+__device__ __forceinline__ void bw_cp16(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
 constexpr int BW_RPT = 4;
 constexpr int BW_NT = 256 / BW_RPT;  // 64 threads per tile
 constexpr int BW_BATCH = 64;
@@ -44,7 +49,7 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
                                                      int W, int H, int gx, int T, float bg0, float bg1, float bg2,
                                                      const float* __restrict__ gout, float* __restrict__ grec,
                                                      const uint32_t* __restrict__ order) {
-    __shared__ float4 sA[BW_BATCH], sB[BW_BATCH], sC[BW_BATCH];
+    __shared__ __align__(16) float4 sA[2][BW_BATCH], sB[2][BW_BATCH], sC[2][BW_BATCH];
     __shared__ uint32_t sI[BW_BATCH];
     __shared__ int s_jmax[BW_NT / 32];
     __shared__ uint8_t s_list[BW_NT / 32][BW_BATCH];
@@ -78,18 +83,32 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
     // the batch records whose alpha >= 1/255 ellipse reaches its 16 x 8 sub-tile (touches());
     // skipped records hit none of the warp's pixels, so T and the last contributor are unchanged
     const unsigned lane_lt = (1u << (threadIdx.x & 31)) - 1u;
-    for (int b0 = rs; b0 < re; b0 += BW_BATCH) {
+    // records staged by cp.async, double-buffered (batch b+1 in flight while batch b replays),
+    // as in k_blend; one record per thread per batch (BW_NT == BW_BATCH)
+    static_assert(BW_NT == BW_BATCH, "one staged record per thread");
+    const int nbA = (re - rs + BW_BATCH - 1) / BW_BATCH;
+    auto stageA = [&](int b, int buf) {
+        const int j = rs + b * BW_BATCH + (int)threadIdx.x;
+        if (j < re) {
+            const float4* g = vrec + (int64_t)vals[j] * 3;
+            bw_cp16(&sA[buf][threadIdx.x], g);
+            bw_cp16(&sB[buf][threadIdx.x], g + 1);
+            bw_cp16(&sC[buf][threadIdx.x], g + 2);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    if (nbA > 0) stageA(0, 0);
+    for (int b = 0; b < nbA; ++b) {
+        const int buf = b & 1;
+        const int b0 = rs + b * BW_BATCH;
         const int cnt = min(BW_BATCH, re - b0);
         bool alive = false;
 #pragma unroll
         for (int k = 0; k < NP; ++k) alive |= !(TA[k].x < 1e-4f) | !(TA[k].y < 1e-4f);
-        if (__syncthreads_count(alive) == 0) break;
-        for (int q = threadIdx.x; q < cnt; q += BW_NT) {
-            const float4* g = vrec + (int64_t)vals[b0 + q] * 3;
-            sA[q] = g[0];
-            sB[q] = g[1];
-            sC[q] = g[2];
-        }
+        if (__syncthreads_count(alive) == 0) break;  // (also: every warp is done with buffer buf ^ 1)
+        if (b + 1 < nbA) stageA(b + 1, buf ^ 1);
+        else asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         __syncthreads();
         if (!__any_sync(0xffffffffu, alive)) continue;
         uint8_t* lst = s_list[threadIdx.x >> 5];
@@ -97,7 +116,7 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
 #pragma unroll
         for (int e2 = 0; e2 < BW_BATCH / 32; ++e2) {
             const int q = (int)(threadIdx.x & 31) + 32 * e2;
-            const bool want = q < cnt && touches(sA[q], sB[q], wx0, wx0 + 15.0f, wy0, wy0 + 7.0f);
+            const bool want = q < cnt && touches(sA[buf][q], sB[buf][q], wx0, wx0 + 15.0f, wy0, wy0 + 7.0f);
             const unsigned bal = __ballot_sync(0xffffffffu, want);
             if (want) lst[nq + __popc(bal & lane_lt)] = (uint8_t)q;
             nq += __popc(bal);
@@ -105,28 +124,38 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
         __syncwarp();
         for (int i = 0; i < nq; ++i) {  // the forward's paired row arithmetic, lane for lane
             const int q = lst[i];
-            const float4 a = sA[q], bq = sB[q];
+            const float4 a = sA[buf][q], bq = sB[buf][q];
             const float dx = a.x - fx;
             const float tAdx = (bq.x * dx) * dx, tB = bq.y * dx;
             const float2 vv = make_float2(a.y, a.y), cc = make_float2(bq.z, bq.z);
             const float2 ta2 = make_float2(tAdx, tAdx), tb2 = make_float2(tB, tB);
+            float2 p2[NP];
+            bool h[2 * NP];
+            bool anyh = false;
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
                 const float2 dy = __fadd2_rn(vv, nfy[k]);
-                const float2 p2 = __ffma2_rn(__ffma2_rn(cc, dy, tb2), dy, ta2);
-                const bool h0 = !(TA[k].x < 1e-4f) && !(p2.x > 0.0f) && !(p2.x < bq.w);
-                const bool h1 = !(TA[k].y < 1e-4f) && !(p2.y > 0.0f) && !(p2.y < bq.w);
-                if (!(h0 | h1)) continue;
-                const float o = sC[q].x;
-                const float2 e = make_float2(ex2b(h0 ? p2.x : NEG_INF), ex2b(h1 ? p2.y : NEG_INF));
+                p2[k] = __ffma2_rn(__ffma2_rn(cc, dy, tb2), dy, ta2);
+                h[2 * k] = !(TA[k].x < 1e-4f) && !(p2[k].x > 0.0f) && !(p2[k].x < bq.w);
+                h[2 * k + 1] = !(TA[k].y < 1e-4f) && !(p2[k].y > 0.0f) && !(p2[k].y < bq.w);
+                anyh |= h[2 * k] | h[2 * k + 1];
+            }
+            if (!anyh) continue;
+            // branch-free over the row pairs (a non-hitting row gets alpha = +0: T unchanged)
+            const float o = sC[buf][q].x;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                const float2 e = make_float2(ex2b(h[2 * k] ? p2[k].x : NEG_INF), ex2b(h[2 * k + 1] ? p2[k].y : NEG_INF));
                 float2 al = __fmul2_rn(make_float2(o, o), e);
                 al = make_float2(fminf(0.99f, al.x), fminf(0.99f, al.y));
                 TA[k] = __fmul2_rn(TA[k], __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
-                if (h0) last[2 * k] = b0 + q;
-                if (h1) last[2 * k + 1] = b0 + q;
+                last[2 * k] = h[2 * k] ? b0 + q : last[2 * k];
+                last[2 * k + 1] = h[2 * k + 1] ? b0 + q : last[2 * k + 1];
             }
         }
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
         Tf[2 * k] = TA[k].x;
@@ -173,9 +202,9 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
         for (int q = threadIdx.x; q < cnt; q += BW_NT) {
             const uint32_t gi = vals[b0 + q];
             const float4* gp = vrec + (int64_t)gi * 3;
-            sA[q] = gp[0];
-            sB[q] = gp[1];
-            sC[q] = gp[2];
+            sA[0][q] = gp[0];
+            sB[0][q] = gp[1];
+            sC[0][q] = gp[2];
             sI[q] = gi;
         }
         __syncthreads();
@@ -185,14 +214,14 @@ __global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ 
 #pragma unroll
         for (int e2 = 0; e2 < BW_BATCH / 32; ++e2) {
             const int q = (int)(threadIdx.x & 31) + 32 * e2;
-            const bool want = q < cnt && b0 + q <= wjmax && touches(sA[q], sB[q], wx0, wx0 + 15.0f, wy0, wy0 + 7.0f);
+            const bool want = q < cnt && b0 + q <= wjmax && touches(sA[0][q], sB[0][q], wx0, wx0 + 15.0f, wy0, wy0 + 7.0f);
             wmask |= (unsigned long long)__ballot_sync(0xffffffffu, want) << (32 * e2);
         }
         while (wmask) {
             const int q = 63 - __clzll((long long)wmask);  // descending order
             wmask &= ~(1ull << q);
             const int j = b0 + q;
-            const float4 a = sA[q], bq = sB[q], c = sC[q];
+            const float4 a = sA[0][q], bq = sB[0][q], c = sC[0][q];
             const float dx = a.x - fx;
             const float tAdx = (bq.x * dx) * dx, tB = bq.y * dx;
             const float2 vv = make_float2(a.y, a.y), cc = make_float2(bq.z, bq.z);
