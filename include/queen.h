@@ -305,6 +305,16 @@ queen_status queen_render_mask(queen_ctx* ctx, const queen_gaussians* scene, con
  * bound).  Capturable; no host sync. */
 queen_status queen_wait_binned(const queen_ctx* ctx, void* stream);
 
+/* Optional separate stream for the blend of queen_render_views[_rgb8] on `ctx` (NULL: the
+ * call's stream, the default).  When set, the projection + binning run on the call's stream
+ * and the blend on `stream` after them, so a renderer can give the (latency-bound) binning a
+ * higher stream priority than the (ALU-bound) blend of another context; the next
+ * queen_render_views on `ctx` waits for this blend before reusing the workspace.
+ * queen_wait_rendered makes `stream` wait for the most recent blend that ran on a blend
+ * stream of `ctx`.  Not for stream capture (the plain single-stream path is capturable). */
+queen_status queen_set_blend_stream(queen_ctx* ctx, void* stream);
+queen_status queen_wait_rendered(const queen_ctx* ctx, void* stream);
+
 /* Stage profiler (evidence for bench.py): when enabled, every call records CUDA events
  * on its stream around each stage: 0 apply, 1 project, 2 compact (+resets), 3 depth sort,
  * 4 duplicate, 5 tile sort, 6 ranges, 7 blend (k_blend alone), 8 entropy decode, 9 blend

@@ -29,7 +29,8 @@ QUEEN_MAX_VIEWS = 64
 EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version", "queen_workspace_size",
            "queen_set_workspace", "queen_check", "queen_decode_residuals", "queen_apply_frame", "queen_project",
            "queen_bin_sort", "queen_rasterize", "queen_render_views", "queen_blend_counts",
-           "queen_profile_enable", "queen_profile_read", "queen_wait_binned", "queen_entropy_encode",
+           "queen_profile_enable", "queen_profile_read", "queen_wait_binned", "queen_set_blend_stream",
+           "queen_wait_rendered", "queen_entropy_encode",
            "queen_entropy_decode", "queen_entropy_decode_frame", "queen_render_mask",
            "queen_densify", "queen_rasterize_rgb8", "queen_render_views_rgb8",
            "queen_rasterize_backward", "queen_project_backward", "queen_decode_backward"]
@@ -117,6 +118,8 @@ def lib() -> C.CDLL:
             "queen_render_mask": (i32, [p, C.POINTER(QueenGaussians), p, i32, p, C.POINTER(QueenCamera), i32, C.c_float,
                                         i32, p, p]),
             "queen_wait_binned": (i32, [p, p]),
+            "queen_set_blend_stream": (i32, [p, p]),
+            "queen_wait_rendered": (i32, [p, p]),
             "queen_entropy_encode": (i32, [p, i32, i32, i32, p, C.c_size_t, C.POINTER(C.c_size_t)]),
             "queen_entropy_decode": (i32, [p, p, i32, i32, i32, p, p]),
             "queen_entropy_decode_frame": (i32, [p, C.POINTER(C.c_void_p), C.POINTER(C.c_int32), i32, i32, p, p]),
@@ -412,6 +415,17 @@ def queen_entropy_decode_frame(ctx: Context, stream_ptrs, lat_dim, n: int, laten
 def queen_wait_binned(ctx: Context, stream=None):
     st = lib().queen_wait_binned(ctx.handle, C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_wait_binned")
+
+
+def queen_set_blend_stream(ctx: Context, stream=None):
+    """None: the blend runs on each render call's stream (default)."""
+    st = lib().queen_set_blend_stream(ctx.handle, C.c_void_p(None if stream is None else stream.cuda_stream))
+    ctx._chk(st, "queen_set_blend_stream")
+
+
+def queen_wait_rendered(ctx: Context, stream=None):
+    st = lib().queen_wait_rendered(ctx.handle, C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_wait_rendered")
 
 
 def queen_blend_counts(ctx: Context, proj: QueenProj, bins: QueenBins, cams, evaluated, composited, stream=None):

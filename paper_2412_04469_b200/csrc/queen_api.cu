@@ -19,6 +19,9 @@ struct queen_ctx {
     queen::WsLayout L{};
     queen::Prof prof;
     cudaEvent_t binned = nullptr;  // recorded by queen_render_views after binning (queen_wait_binned)
+    cudaEvent_t rendered = nullptr;     // recorded by queen_render_views after the blend
+    cudaStream_t blend_stream = nullptr;  // queen_set_blend_stream: the blend's own stream
+    bool blend_elsewhere = false;         // the most recent blend ran on blend_stream
     std::string err;
 };
 
@@ -59,7 +62,8 @@ queen_status queen_create(int device, queen_ctx** out) {
     if ((e = init_binning_attributes()) != cudaSuccess) return QUEEN_ERR_CUDA;
     queen_ctx* c = new queen_ctx();
     c->device = device;
-    if (cudaEventCreateWithFlags(&c->binned, cudaEventDisableTiming) != cudaSuccess) {
+    if (cudaEventCreateWithFlags(&c->binned, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->rendered, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
         return QUEEN_ERR_CUDA;
     }
@@ -70,6 +74,7 @@ queen_status queen_create(int device, queen_ctx** out) {
 void queen_destroy(queen_ctx* ctx) {
     if (!ctx) return;
     if (ctx->binned) cudaEventDestroy(ctx->binned);
+    if (ctx->rendered) cudaEventDestroy(ctx->rendered);
     for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
     delete ctx;
 }
@@ -78,6 +83,18 @@ queen_status queen_wait_binned(const queen_ctx* ctx, void* stream) {
     if (!ctx) return QUEEN_ERR_INVALID_ARG;
     return cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->binned, 0) == cudaSuccess ? QUEEN_OK
                                                                                                  : QUEEN_ERR_CUDA;
+}
+
+queen_status queen_set_blend_stream(queen_ctx* ctx, void* stream) {
+    if (!ctx) return QUEEN_ERR_INVALID_ARG;
+    ctx->blend_stream = static_cast<cudaStream_t>(stream);
+    return QUEEN_OK;
+}
+
+queen_status queen_wait_rendered(const queen_ctx* ctx, void* stream) {
+    if (!ctx) return QUEEN_ERR_INVALID_ARG;
+    return cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->rendered, 0) == cudaSuccess ? QUEEN_OK
+                                                                                                   : QUEEN_ERR_CUDA;
 }
 
 const char* queen_last_error(const queen_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
@@ -415,11 +432,23 @@ static queen_status render_impl(queen_ctx* ctx, const queen_gaussians* scene, co
     b.ranges = reinterpret_cast<uint32_t*>(ws + L.ranges);
     b.K = reinterpret_cast<uint32_t*>(ws + L.K);
     b.sorted_in_alt = 0;
+    cudaStream_t bs = ctx->blend_stream;
+    // after a blend on a separate stream, that blend must be done before the binning overwrites
+    // the workspace (the rendered event is only ever recorded on a separate blend stream, never
+    // inside a capture of the plain path)
+    if (ctx->blend_elsewhere && cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->rendered, 0) != cudaSuccess)
+        return cuda_fail(ctx, cudaGetLastError(), "wait rendered event");
+    ctx->blend_elsewhere = bs != nullptr;
     if (queen_status st = queen_project(ctx, scene, cams, n_views, &pj, stream)) return st;
     if (queen_status st = queen_bin_sort(ctx, &pj, cams, n_views, &b, stream)) return st;
     if (cudaEventRecord(ctx->binned, static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return cuda_fail(ctx, cudaGetLastError(), "record binned event");
-    return rasterize_impl(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, rgb8_out, stream);
+    if (!bs) return rasterize_impl(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, rgb8_out, stream);
+    if (cudaStreamWaitEvent(bs, ctx->binned, 0) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "blend wait");
+    queen_status st = rasterize_impl(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, rgb8_out, bs);
+    if (!st && cudaEventRecord(ctx->rendered, bs) != cudaSuccess)
+        return cuda_fail(ctx, cudaGetLastError(), "record rendered event");
+    return st;
 }
 
 queen_status queen_render_views(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams, int32_t n_views,

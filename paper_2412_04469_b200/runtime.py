@@ -11,7 +11,7 @@ import torch
 from . import (QUEEN_LAT_F32, QUEEN_LAT_INT8, QUEEN_MAX_VIEWS, QUEEN_POS_COO, QUEEN_POS_GATES, Context,
                QueenError, camera_array, gaussians_struct, packet_struct, queen_apply_frame,
                queen_densify, queen_entropy_decode_frame, queen_render_mask, queen_render_views,
-               queen_render_views_rgb8, queen_wait_binned)
+               queen_render_views_rgb8, queen_set_blend_stream, queen_wait_binned)
 from . import packet as wire
 
 
@@ -263,6 +263,63 @@ class Player:
                 queen_apply_frame(self.ctx, self.scene, next_pkt.struct, side)
             main.wait_stream(side)
         return rgb
+
+    def step2(self, next_pkt, out=None, rgb8: bool = False, rendered: torch.cuda.Event | None = None,
+              ready: torch.cuda.Event | None = None):
+        """Two-lane pipelined frame step (eager): like step(), but frame t renders on lane t % 2 --
+        its own libqueen context (workspace) and high-priority stream -- and the current stream
+        does NOT wait for it, so frame t+1's projection and binning (on the other lane) run under
+        frame t's blend.  Frame t+1 starts once packet t+1 is applied (after frame t's binning).
+        `rendered` is recorded on the lane stream when frame t's image is complete; `out` must not
+        be reused before that.  Call sync_lanes() before reading results on the current stream."""
+        if self.n_lanes != 1:
+            raise ValueError("two-lane frame steps need a single view-batch lane")
+        main = torch.cuda.current_stream(self.dev)
+        if not hasattr(self, "_lanes2"):
+            # per lane: context, high-priority binning stream, normal-priority blend stream
+            lo, hi = torch.cuda.Stream.priority_range()  # (lowest, highest) priority
+            self._lanes2 = []
+            for k in range(2):
+                ctx = self.ctx if k == 0 else Context(self.device)
+                if k:  # joins self.ctxs: profiled, status-checked and re-carved with the others
+                    ctx.set_workspace(self.planes.shape[1], self.vpb, self.W, self.H, self.keys_cap)
+                    self.ctxs.append(ctx)
+                bs = torch.cuda.Stream(device=self.dev, priority=lo)
+                self._lanes2.append((ctx, torch.cuda.Stream(device=self.dev, priority=hi), bs))
+            self._lane_t = 0
+            self._side = getattr(self, "_side", None) or torch.cuda.Stream(device=self.dev, priority=hi)
+        ctx, ls, bs = self._lanes2[self._lane_t & 1]
+        self._lane_t += 1
+        ls.wait_stream(main)  # the frame's apply (and the caller's ordering) first
+        rgb = self.rgb if out is None else out
+        fn = queen_render_views_rgb8 if rgb8 else queen_render_views
+        queen_set_blend_stream(ctx, bs)  # only for these calls: render() / step() keep one stream
+        try:
+            for (a, b), arr in zip(self.batches, self.cam_arrays):
+                fn(ctx, self.scene, None, rgb[a:b], None if self.T is None else self.T[a:b], self.bg, ls, cam_array=arr)
+        finally:
+            queen_set_blend_stream(ctx, None)
+        if rendered is not None:
+            rendered.record(bs)
+        if next_pkt is not None:
+            side = self._side
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                if ready is not None:
+                    side.wait_event(ready)
+                queen_wait_binned(ctx, side)
+                if isinstance(next_pkt, EntropyPacket):
+                    next_pkt.decode(ctx, side)
+                queen_apply_frame(ctx, self.scene, next_pkt.struct, side)
+            main.wait_stream(side)
+        return rgb
+
+    def sync_lanes(self):
+        """The current stream waits for both two-lane render streams (step2)."""
+        main = torch.cuda.current_stream(self.dev)
+        for _, ls, bs in getattr(self, "_lanes2", []):
+            main.wait_stream(ls)
+            main.wait_stream(bs)
 
     def capture_step(self, next_pkt, out=None, rgb8: bool = False, profile: bool = False):
         """CUDA graph of one pipelined step (see step()): render of the current scene + decode and

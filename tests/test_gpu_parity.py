@@ -518,9 +518,10 @@ def test_cuda_graph_frame_equals_eager():
 
 def test_pipelined_steps_equal_serial_frames():
     """Pipelined steps (Player.step / capture_step: frame t rendered while packet t+1 is decoded
-    and applied on a side stream after the render's binning) give, frame by frame, the same
-    images and final SoA, bit for bit, as serial apply-then-render; also with two view batches
-    (the apply waits for the LAST batch's binning)."""
+    and applied on a side stream after the render's binning; Player.step2: in addition frame t+1
+    binned on a second context under frame t's blend) give, frame by frame, the same images and
+    final SoA, bit for bit, as serial apply-then-render; also with two view batches (the apply
+    waits for the LAST batch's binning)."""
     import paper_2412_04469_b200 as Q
     from paper_2412_04469_b200 import packet as wire
     from paper_2412_04469_b200.runtime import EntropyPacket, Player
@@ -561,6 +562,23 @@ def test_pipelined_steps_equal_serial_frames():
         torch.cuda.synchronize()
         assert torch.equal(gp.rgb, refs[-1])
         assert gp.check_status()[0] == 0
+        # two-lane steps (Player.step2): frame t+1's binning under frame t's blend, 2 contexts
+        tl = Player(sc.planes, sc.n, sc.deg, cams, keys_cap=serial.keys_cap, views_per_batch=vpb)
+        tl.apply(eps[0])
+        outs = [torch.empty_like(tl.rgb) for _ in range(len(eps))]
+        evs = [torch.cuda.Event() for _ in range(len(eps))]
+        for t in range(len(eps)):
+            tl.step2(eps[t + 1] if t + 1 < len(eps) else None, out=outs[t], rendered=evs[t])
+        tl.sync_lanes()
+        torch.cuda.synchronize()
+        for t in range(len(eps)):
+            assert torch.equal(outs[t], refs[t]), ("two-lane", vpb, t)
+        assert torch.equal(tl.planes, serial.planes)
+        # a plain render after two-lane steps (the lane-0 blend ran on its own stream)
+        again = tl.render().clone()
+        torch.cuda.synchronize()
+        assert torch.equal(again, refs[-1])
+        assert tl.check_status()[0] == 0
 
 
 def test_depth_keys_spanning_more_than_27_bits():
