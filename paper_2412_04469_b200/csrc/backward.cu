@@ -44,7 +44,11 @@ constexpr int BW_RPT = 4;
 constexpr int BW_NT = 256 / BW_RPT;  // 64 threads per tile
 constexpr int BW_BATCH = 64;
 
-__global__ void __launch_bounds__(BW_NT) k_blend_bwd(const float4* __restrict__ rec, int n_pad,
+#ifndef QUEEN_BWD_MINB
+#define QUEEN_BWD_MINB 12  // 80 registers (a few spilled words): rasterize_backward 7.27 -> 7.00 ms (92 regs uncapped)
+#endif
+#define BWD_BOUNDS __launch_bounds__(BW_NT, QUEEN_BWD_MINB)
+__global__ void BWD_BOUNDS k_blend_bwd(const float4* __restrict__ rec, int n_pad,
                                                      const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
                                                      int W, int H, int gx, int T, float bg0, float bg1, float bg2,
                                                      const float* __restrict__ gout, float* __restrict__ grec,

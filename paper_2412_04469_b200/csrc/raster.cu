@@ -75,6 +75,9 @@ __device__ __forceinline__ void composite2(Px2& p, float q0, float q1, bool h0, 
     p.T = __fmul2_rn(p.T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
 }
 
+#ifndef QUEEN_BLEND_MINB
+#define QUEEN_BLEND_MINB 20  // 48 registers: 20 CTAs (40 warps) per SM; measured n3dv blend 64 regs 1.399 ms, 48 regs 1.378, 40 regs (spills) 1.401
+#endif
 #ifndef QUEEN_BLEND_UNROLL
 #define QUEEN_BLEND_UNROLL 4  // measured n3dv blend: 1 -> 1.423 ms, 2 -> 1.410, 4 -> 1.399
 #endif
@@ -85,7 +88,7 @@ constexpr int BLEND_UNROLL = QUEEN_BLEND_UNROLL;  // record-loop unroll
 constexpr bool BLEND_UNCOND = QUEEN_BLEND_UNCOND;
 
 template <bool COUNT, int RPT, bool WMASK>
-__global__ void __launch_bounds__(256 / RPT) k_blend(const float4* __restrict__ rec, int n_pad, const uint2* __restrict__ ranges,
+__global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const float4* __restrict__ rec, int n_pad, const uint2* __restrict__ ranges,
                                                     const uint32_t* __restrict__ vals, int W, int H, int gx, int T, float bg0,
                                                     float bg1, float bg2, float* __restrict__ rgb_out, float* __restrict__ T_out,
                                                     uint8_t* __restrict__ out8, int out_mode, float mask_thresh, long long* ev_out,
