@@ -671,9 +671,10 @@ def main():
 
     if libsort is not None and stages:
         nb = len(batches)
-        libsort["ours_binning_ms_per_batch"] = sum(stages[k]["ms_per_step"] for k in
+        kst = stages_serial if stages_serial else stages  # stages alone on the GPU (not overlapped)
+        libsort["ours_binning_ms_per_batch"] = sum(kst[k]["ms_per_step"] for k in
                                                    ("compact", "depth_sort", "duplicate", "ranges", "tile_sort")
-                                                   if k in stages) / nb
+                                                   if k in kst) / nb
 
     # ---- paper-style FPS: decode + render of ONE centre view on 1 GPU, median
     paper = None
