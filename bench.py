@@ -65,9 +65,13 @@ def parse():
 
 
 def default_vpb(cfg):
-    # key buffers per batch ~ 24 B/key x ~8 keys/Gaussian/view: keep one batch <= ~6 GB
+    """Views per batch: as many as fit (a) two 9-bit tile-sort passes (batch tiles <= 2^18: a
+    third pass costs more than a second batch; measured stress 8 -> 14 views: 14.4 -> 12.9
+    frames/s) and (b) ~12 GB of key buffers (~24 B/key x ~8 keys/Gaussian/view).  Immersive's 46
+    views then render as one batch (298 vs 278 frames/s as 23 + 23)."""
+    tiles = ((cfg.width + 15) // 16) * ((cfg.height + 15) // 16)
     per_view = 8 * cfg.n * 24 * 1.5
-    return int(max(1, min(cfg.views, 64, (6 << 30) // per_view)))
+    return int(max(1, min(cfg.views, 64, (12 << 30) // per_view, (1 << 18) // tiles)))
 
 
 def rank_views(V, rank, world):
