@@ -502,10 +502,11 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
 #endif
     for (;;) {
         if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-        for (int q = threadIdx.x; q < NW * BINS; q += NT) {
-            whist[q] = 0u;
+        // zero the per-warp histograms (and match words) with 16-byte stores
+        for (int q = threadIdx.x; q < NW * BINS / 4; q += NT) {
+            reinterpret_cast<uint4*>(whist)[q] = make_uint4(0u, 0u, 0u, 0u);
 #if QUEEN_OS_MATCH_OR
-            sk[q] = 0u;
+            reinterpret_cast<uint4*>(sk)[q] = make_uint4(0u, 0u, 0u, 0u);
 #endif
         }
         __syncthreads();
