@@ -466,6 +466,9 @@ def main():
     eager = graph_pipelined = None
     clocks = ClockSampler(local)
     pipeline = not args.no_pipeline and player.n_lanes == 1
+    # two-lane eager steps pay when a frame has work to overlap; tiny frames are launch-bound and
+    # run faster as one-lane graph replays (tiny: ~5.4 k vs ~5.1 k frames/s)
+    two_lane = pipeline and not args.one_lane and len(cams) * W * H >= (1 << 20)
     if use_graph:
         player.profile_read(reset=True)
         # N = 1: one graph per resident packet (at most one per timed step, so every graph's
@@ -509,7 +512,7 @@ def main():
             n_prof_frames = len(graphs)
         del graphs
         st, info = player.check_status()
-        if pipeline and not args.one_lane:
+        if two_lane:
             # Headline: two-lane eager steps (runtime.Player.step2): frame t renders on lane t % 2
             # (own context; binning on a high-priority stream, blend on a normal-priority one), so
             # frame t+1's projection + binning overlap frame t's blend, and packet t+1 is decoded +
@@ -928,13 +931,13 @@ def main():
                        "packet_format": args.packet_format,
                        "launch": ("eager two-lane steps: frame t+1's binning (own context, high-priority "
                                   "stream) and decode + apply under frame t's blend"
-                                  if (use_graph and pipeline and not args.one_lane) else
+                                  if (use_graph and two_lane) else
                                   ("CUDA-graph replay (one graph per packet slot)" if use_graph else "eager") +
                                   ("; pipelined: decode + apply of frame t+1 under the blend of frame t"
                                    if use_graph and pipeline else "; serial frame steps")),
                        "l2": ("not flushed: the K overlapped two-lane steps are one timed interval; a frame's "
                               "working set (SoA, records, keys, images) is several times the 126 MB L2"
-                              if (use_graph and pipeline and not args.one_lane) else
+                              if (use_graph and two_lane) else
                               "flushed between timed steps (512 MB write outside the step events)"),
                        **({"as_rank": f"{args.as_rank}: diagnostic, this rank's views only, no NCCL"} if args.as_rank else {})},
             "packet_bytes_per_frame": int(statistics.mean(used_bytes)) if used_bytes else None,
