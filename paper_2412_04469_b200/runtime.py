@@ -267,11 +267,14 @@ class Player:
     def step2(self, next_pkt, out=None, rgb8: bool = False, rendered: torch.cuda.Event | None = None,
               ready: torch.cuda.Event | None = None):
         """Two-lane pipelined frame step (eager): like step(), but frame t renders on lane t % 2 --
-        its own libqueen context (workspace) and high-priority stream -- and the current stream
+        its own libqueen context (workspace), a high-priority stream for projection + binning and
+        a normal-priority stream for the blend (queen_set_blend_stream) -- and the current stream
         does NOT wait for it, so frame t+1's projection and binning (on the other lane) run under
         frame t's blend.  Frame t+1 starts once packet t+1 is applied (after frame t's binning).
-        `rendered` is recorded on the lane stream when frame t's image is complete; `out` must not
-        be reused before that.  Call sync_lanes() before reading results on the current stream."""
+        `rendered` is recorded on the blend stream when frame t's image is complete; `out` must
+        not be reused before that (out=None: one of two per-lane image buffers, returned; with_T:
+        per-lane T buffers, self.T_lanes).  Call sync_lanes() before reading results on the
+        current stream."""
         if self.n_lanes != 1:
             raise ValueError("two-lane frame steps need a single view-batch lane")
         main = torch.cuda.current_stream(self.dev)
@@ -288,15 +291,21 @@ class Player:
                 self._lanes2.append((ctx, torch.cuda.Stream(device=self.dev, priority=hi), bs))
             self._lane_t = 0
             self._side = getattr(self, "_side", None) or torch.cuda.Stream(device=self.dev, priority=hi)
-        ctx, ls, bs = self._lanes2[self._lane_t & 1]
+        lane = self._lane_t & 1
+        ctx, ls, bs = self._lanes2[lane]
         self._lane_t += 1
         ls.wait_stream(main)  # the frame's apply (and the caller's ordering) first
-        rgb = self.rgb if out is None else out
+        if out is None or self.T is not None:  # the two lanes' blends overlap: per-lane buffers
+            if not hasattr(self, "rgb_lanes"):
+                self.rgb_lanes = [self.rgb, torch.empty_like(self.rgb)]
+                self.T_lanes = [self.T, torch.empty_like(self.T)] if self.T is not None else [None, None]
+        rgb = self.rgb_lanes[lane] if out is None else out
+        T = self.T_lanes[lane] if self.T is not None else None
         fn = queen_render_views_rgb8 if rgb8 else queen_render_views
         queen_set_blend_stream(ctx, bs)  # only for these calls: render() / step() keep one stream
         try:
             for (a, b), arr in zip(self.batches, self.cam_arrays):
-                fn(ctx, self.scene, None, rgb[a:b], None if self.T is None else self.T[a:b], self.bg, ls, cam_array=arr)
+                fn(ctx, self.scene, None, rgb[a:b], None if T is None else T[a:b], self.bg, ls, cam_array=arr)
         finally:
             queen_set_blend_stream(ctx, None)
         if rendered is not None:

@@ -574,6 +574,15 @@ def test_pipelined_steps_equal_serial_frames():
         for t in range(len(eps)):
             assert torch.equal(outs[t], refs[t]), ("two-lane", vpb, t)
         assert torch.equal(tl.planes, serial.planes)
+        # out=None: the per-lane image buffers (frame t's is valid once `rendered` fires)
+        tl2 = Player(sc.planes, sc.n, sc.deg, cams, keys_cap=serial.keys_cap, views_per_batch=vpb)
+        tl2.apply(eps[0])
+        for t in range(len(eps)):
+            ev = torch.cuda.Event()
+            img = tl2.step2(eps[t + 1] if t + 1 < len(eps) else None, rendered=ev)
+            torch.cuda.current_stream().wait_event(ev)
+            assert torch.equal(img.clone(), refs[t]), ("two-lane, own buffers", vpb, t)
+        tl2.sync_lanes()
         # a plain render after two-lane steps (the lane-0 blend ran on its own stream)
         again = tl.render().clone()
         torch.cuda.synchronize()
