@@ -804,8 +804,11 @@ def main():
         # the copies of frame k overlap the compute of frames k +- 1 like a real player.
         pin_pk = [torch.from_numpy(b).pin_memory() for b in host_bufs] if rank == 0 else None
         odt = torch.uint8 if rgb8 else torch.float32
-        out_dev = [torch.empty(player.rgb.shape, dtype=odt, device=dev) for _ in range(2)]
-        out_host = [torch.empty(player.rgb.shape, dtype=odt).pin_memory() for _ in range(2)]
+        # three image slots: with two-lane steps frame k+2's binning may start while frame k's D2H
+        # is still running, so a slot is reused three frames later
+        NB = 3
+        out_dev = [torch.empty(player.rgb.shape, dtype=odt, device=dev) for _ in range(NB)]
+        out_host = [torch.empty(player.rgb.shape, dtype=odt).pin_memory() for _ in range(NB)]
         recv = [torch.zeros(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
         dp_recv = [mkpkt(r) for r in recv]
         s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
@@ -851,29 +854,28 @@ def main():
                 player.apply(dp_recv[k0 % 2])
             for q in range(n):
                 k = k0 + q
-                slot = k % 2
-                if q >= 2:
-                    stream.wait_event(ev_d2h[q - 2])  # out_dev[slot] drained to the host
+                islot = k % NB
+                if q >= NB:
+                    stream.wait_event(ev_d2h[q - NB])  # out_dev[islot] drained to the host
                 if pipeline:
                     upload(q + 1)
                     stepper = player.step if args.one_lane else player.step2
-                    stepper(dp_recv[(k + 1) % 2], out=out_dev[slot], rgb8=rgb8, rendered=ev_render[q],
+                    stepper(dp_recv[(k + 1) % 2], out=out_dev[islot], rgb8=rgb8, rendered=ev_render[q],
                             ready=ev_h2d[q + 1] if world == 1 else None)
                 else:
                     if q >= 1:
                         upload(q)
-                        player.apply(dp_recv[slot])
-                    player.render(out=out_dev[slot], rgb8=rgb8)
+                        player.apply(dp_recv[k % 2])
+                    player.render(out=out_dev[islot], rgb8=rgb8)
                     ev_render[q].record(stream)
-                lat1[q].record(stream)
                 ev_step[q].record(stream)
                 with torch.cuda.stream(s_d2h):
                     s_d2h.wait_event(ev_render[q])
-                    out_host[slot].copy_(out_dev[slot], non_blocking=True)
+                    lat1[q].record(s_d2h)  # frame k rendered (its blend may run on a lane stream)
+                    out_host[islot].copy_(out_dev[islot], non_blocking=True)
                     ev_d2h[q].record(s_d2h)
-            stream.wait_event(ev_d2h[n - 1])
-            if n > 1:
-                stream.wait_event(ev_d2h[n - 2])
+            for q in range(max(0, n - NB), n):
+                stream.wait_event(ev_d2h[q])
             player.sync_lanes()
             t1.record(stream)
             torch.cuda.synchronize()
