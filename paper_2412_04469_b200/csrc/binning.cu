@@ -53,7 +53,7 @@ constexpr unsigned long long SCAN_AGG = 1ull << 62, SCAN_INC = 2ull << 62, SCAN_
 constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_MASK = (1u << 30) - 1;
 constexpr long long SPIN_LIMIT = 1ll << 24;
 #ifndef QUEEN_LB_BATCH
-#define QUEEN_LB_BATCH 8
+#define QUEEN_LB_BATCH 4  // measured (tile sort, N3DV): 1 -> 420 us, 2 -> 388, 4 -> 390, 8 -> 408, 16 -> 450
 #endif
 constexpr int LB_BATCH = QUEEN_LB_BATCH;
 #ifndef QUEEN_OS_MATCH_OR
