@@ -34,7 +34,10 @@ struct DevFlags {
 static_assert(sizeof(DevFlags) == 128, "DevFlags layout");
 
 constexpr int MAX_PASSES = 8;
-constexpr int SORT_THREADS = 256;
+#ifndef QUEEN_SORT_THREADS
+#define QUEEN_SORT_THREADS 256
+#endif
+constexpr int SORT_THREADS = QUEEN_SORT_THREADS;  // duplication block size
 #ifndef QUEEN_SORT_ITEMS
 #define QUEEN_SORT_ITEMS 4  // measured N3DV duplication: 16 -> 173 us, 8 -> 139 us, 4 -> 129 us
 #endif
