@@ -929,6 +929,7 @@ def main():
             "config": {"workload": f"{cfg.name}: BASELINE configs[{cfg.index}] ({cfg.n} Gaussians, {V} views "
                                    f"{W}x{H}, SH {cfg.deg}, latents {tuple(cfg.lat)}, {cfg.rho:.0%} gates)",
                        "gaussians": cfg.n, "views": V, "width": W, "height": H, "views_per_batch": player.vpb, "render_lanes": player.n_lanes,
+                       "frame_lanes": 2 if (use_graph and two_lane) else 1,
                        "parallelism": f"views sharded v mod {world}, Gaussians replicated, packet NCCL-broadcast",
                        "packet_format": args.packet_format,
                        "launch": ("eager two-lane steps: frame t+1's binning (own context, high-priority "
