@@ -273,3 +273,155 @@ def test_extent_contains_every_contributing_pixel():
         tx, ty = (xs[hit] // 16).astype(int), (ys[hit] // 16).astype(int)
         rc = pr["rect"][0, i]
         assert np.all((tx >= rc[0]) & (tx <= rc[2]) & (ty >= rc[1]) & (ty <= rc[3]))
+
+
+# ---------------------------------------------------------------------------------------------
+# Pins for the sampled-pixel rasterizers and the blend work counters (VERDICT r1 "What's
+# missing" 3).  rasterize_pixels / rasterize_pixels_direct must equal the full tiled rasterizer
+# bit for bit at every pixel they are asked for; blend_counts must be 0 on an empty scene, equal
+# hand-counted values on one-tile scenes, and agree with a recount from the contributor lists.
+# ---------------------------------------------------------------------------------------------
+def _ragged_scene(seed, n=300, W=70, H=45, needle=False):
+    rng = np.random.default_rng(seed)
+    pos = np.stack([rng.uniform(-3, 3, n), rng.uniform(-2, 2, n), rng.uniform(0.1, 6, n)], 1)
+    quat = rng.standard_normal((n, 4))
+    if needle:
+        # needle ellipses: one long axis, two ~100x shorter ones
+        ls = np.stack([rng.normal(math.log(0.4), 0.3, n), rng.normal(math.log(0.003), 0.3, n),
+                       rng.normal(math.log(0.003), 0.3, n)], 1)
+        ls = ls[np.arange(n)[:, None], np.argsort(rng.random((n, 3)), 1)]  # long axis in any slot
+    else:
+        ls = rng.normal(math.log(0.15), 0.8, (n, 3))
+    opl = rng.normal(1.0, 2.5, n)
+    sh = rng.normal(0, 0.5, (n, 16, 3))
+    pl = planes_from(pos, quat, ls, opl, sh, 3)
+    cam = synth.make_camera(np.eye(3), np.zeros(3), 40.0, 40.0, W, H)
+    return pl, n, cam
+
+
+def _all_pixels(V, W, H):
+    v, y, x = np.meshgrid(np.arange(V), np.arange(H), np.arange(W), indexing="ij")
+    return np.stack([v.reshape(-1), x.reshape(-1), y.reshape(-1)], 1).astype(np.int32)
+
+
+@pytest.mark.parametrize("case", ["tiny", "ragged", "needle"])
+def test_rasterize_pixels_and_direct_equal_full_rasterizer(case):
+    if case == "tiny":
+        cfg = synth.get_config("tiny")
+        sc = synth.make_scene(cfg, n=337)
+        cams = synth.make_cameras(cfg)
+        pl, n, deg = sc.planes, sc.n, sc.deg
+    else:
+        pl, n, cam = _ragged_scene(11, needle=(case == "needle"))
+        cams, deg = [cam, synth.make_camera(np.eye(3), np.array([0.3, -0.1, 0.5]), 40.0, 40.0, 70, 45)], 3
+    W, H = cams[0].width, cams[0].height
+    proj, bins, rgb, T = oracle.render(pl, n, deg, cams, bg=(0.1, 0.2, 0.3))
+    pix = _all_pixels(len(cams), W, H)
+    r1, T1 = oracle.rasterize_pixels(proj["rec"], bins["ranges"], bins["vals"], W, H, pix, bg=(0.1, 0.2, 0.3))
+    r2, T2 = oracle.rasterize_pixels_direct(proj, n, W, H, pix, bg=(0.1, 0.2, 0.3))
+    full_rgb = rgb[pix[:, 0], :, pix[:, 2], pix[:, 1]]
+    full_T = T[pix[:, 0], pix[:, 2], pix[:, 1]]
+    for r, t in ((r1, T1), (r2, T2)):
+        assert np.array_equal(r.view(np.uint32), full_rgb.view(np.uint32))
+        assert np.array_equal(t.view(np.uint32), full_T.view(np.uint32))
+    assert T.min() < 0.5  # the scene covers pixels non-trivially
+    # a random subset in a shuffled order gives the same values (no state between pixels)
+    sel = np.random.default_rng(3).permutation(pix.shape[0])[:500]
+    r3, T3 = oracle.rasterize_pixels_direct(proj, n, W, H, pix[sel], bg=(0.1, 0.2, 0.3))
+    assert np.array_equal(r3, full_rgb[sel]) and np.array_equal(T3, full_T[sel])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_needle_ellipses_tiled_equals_bruteforce(seed):
+    """R13 (opacity-aware bounding box) must hold for needle-shaped footprints too: the tiled
+    result equals brute force over all Gaussians bit for bit (VERDICT r1 weak 1 probe)."""
+    pl, n, cam = _ragged_scene(100 + seed, n=250, W=83, H=57, needle=True)
+    proj, bins, rgb, T = oracle.render(pl, n, 3, [cam])
+    _check_bins(proj, bins, 83, 57)
+    rgb_b, T_b = oracle.rasterize_bruteforce(proj, n, 83, 57)
+    assert np.array_equal(rgb, rgb_b) and np.array_equal(T, T_b)
+    assert T.min() < 0.9
+
+
+def test_blend_counts_empty_scene():
+    cam = identity_camera(40, 24, 30.0)
+    pl = planes_from([[0, 0, -5.0]], [[1, 0, 0, 0]], [[-3] * 3], [2.0], [sh_for_rgb((1, 1, 1), 0)], 0)
+    proj, bins, _, _ = oracle.render(pl, 1, 0, [cam])
+    ev, cp = oracle.blend_counts(proj, bins, 40, 24)
+    assert ev.tolist() == [0] and cp.tolist() == [0]
+
+
+def test_blend_counts_one_tile_hand_counted():
+    """16x16 image = one tile.  (a) One small isotropic Gaussian: every pixel evaluates its single
+    entry (E = 256); the composited pixels are those with alpha >= 1/255, counted in float64 from
+    the textbook projection (tests/ref64.py) on a scene whose pixels all sit far from the
+    threshold.  (b) Three coincident, near-opaque, very wide Gaussians: alpha clamps to 0.99 at
+    every pixel, T = 0.01 after the first and 0.01^2 < 1e-4 after the second, so every pixel
+    stops there: E = Cp = 2 x 256."""
+    cam = identity_camera(16, 16, 40.0, cx=7.3, cy=8.6)
+    pl = planes_from([[0.0, 0.0, 4.0]], [[1, 0, 0, 0]], [[math.log(0.25)] * 3], [logit(0.8)],
+                     [sh_for_rgb((0.5, 0.5, 0.5), 0)], 0)
+    proj, bins, _, _ = oracle.render(pl, 1, 0, [cam])
+    ev, cp = oracle.blend_counts(proj, bins, 16, 16)
+    pr = ref64.project64(pl, 1, 0, cam)
+    ys, xs = np.mgrid[0:16, 0:16]
+    dx, dy = xs - pr["u"][0], ys - pr["v"][0]
+    cn = pr["conic"][0]
+    alpha = pr["o"][0] * np.exp(-0.5 * (cn[0, 0] * dx * dx + 2 * cn[0, 1] * dx * dy + cn[1, 1] * dy * dy))
+    assert np.abs(np.log(alpha * 255.0)).min() > 0.01  # no pixel near the skip threshold
+    n_hit = int((alpha >= 1 / 255).sum())
+    assert 0 < n_hit < 256
+    assert ev.tolist() == [256] and cp.tolist() == [n_hit]
+    pl3 = planes_from([[0.0, 0.0, 4.0]] * 3, [[1, 0, 0, 0]] * 3, [[math.log(500.0)] * 3] * 3,
+                      [logit(0.9999)] * 3, [sh_for_rgb((0.5, 0.5, 0.5), 0)] * 3, 0)
+    proj, bins, _, T = oracle.render(pl3, 3, 0, [cam])
+    ev, cp = oracle.blend_counts(proj, bins, 16, 16)
+    assert bins["K"] == 3 and np.all(T < 1e-4)
+    assert ev.tolist() == [512] and cp.tolist() == [512]
+
+
+@pytest.mark.parametrize("case", ["tiny", "ragged"])
+def test_blend_counts_equal_contributor_recount(case):
+    """Cp = number of contributors of every pixel; E = per pixel the tile-list length, or, where
+    compositing stopped (T < 1e-4), the list position of the last contributor + 1."""
+    if case == "tiny":
+        cfg = synth.get_config("tiny")
+        sc = synth.make_scene(cfg)
+        cams = synth.make_cameras(cfg)
+        pl, n, deg = sc.planes, sc.n, sc.deg
+    else:
+        pl, n, cam = _ragged_scene(21, n=400)
+        # a wall of opaque Gaussians makes many pixels terminate early
+        wall = planes_from([[0.0, 0.0, 0.5]] * 4, [[1, 0, 0, 0]] * 4, [[math.log(3.0)] * 3] * 4, [logit(0.999)] * 4,
+                           [sh_for_rgb((0.2, 0.4, 0.6), 3)] * 4, 3)
+        pl = np.concatenate([pl[:, :n], wall[:, :4]], 1)
+        n += 4
+        cams, deg = [cam, synth.make_camera(np.eye(3), np.array([0.2, 0.1, 0.0]), 40.0, 40.0, 70, 45)], 3
+    W, H = cams[0].width, cams[0].height
+    proj, bins, rgb, T = oracle.render(pl, n, deg, cams)
+    ev, cp = oracle.blend_counts(proj, bins, W, H)
+    off, gid, _ = oracle.contributors(proj, bins, W, H)
+    cnt = np.diff(off)
+    V = len(cams)
+    gx = (W + 15) // 16
+    Tt = gx * ((H + 15) // 16)
+    ev_re = np.zeros(V, np.int64)
+    stopped_any = False
+    for v in range(V):
+        for y in range(H):
+            for x in range(W):
+                p = (v * H + y) * W + x
+                a, b = bins["ranges"][v * Tt + (y >> 4) * gx + (x >> 4)]
+                if T[v, y, x] < 1e-4:
+                    stopped_any = True
+                    last = gid[off[p + 1] - 1]
+                    pos = np.nonzero(bins["vals"][a:b] == last)[0]
+                    assert pos.size == 1
+                    ev_re[v] += int(pos[0]) + 1
+                else:
+                    ev_re[v] += int(b) - int(a)
+    assert cp.tolist() == cnt.reshape(V, -1).sum(1).tolist()
+    assert ev.tolist() == ev_re.tolist()
+    assert np.all(cp <= ev) and cp.sum() > 0
+    if case == "ragged":
+        assert stopped_any
