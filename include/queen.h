@@ -225,18 +225,23 @@ queen_status queen_blend_counts(queen_ctx* ctx, const queen_proj* proj, const qu
  *   latents[L][n_pad] int8 (host memory; columns >= n ignored), flattened row-major,
  *   into the chunked 32-way interleaved rANS "QANS" stream written to `out` (host, capacity
  *   bytes).  *bytes = stream size; QUEEN_ERR_SHAPE if capacity is too small (nothing written).
- * queen_entropy_decode (DEVICE): decodes such a stream (device memory) back into
- *   latents_out[L][n_pad] int8 (device; columns >= n untouched), one warp per 8192-symbol
- *   chunk.  A corrupt stream or one that does not match (L, n) sets QUEEN_ERR_INDEX. */
+ * queen_entropy_decode (DEVICE): decodes such a stream (device memory, stream_bytes long) back
+ *   into latents_out[L][n_pad] int8 (device; columns >= n untouched), one warp per 8192-symbol
+ *   chunk.  A stream too small for the header and chunk tables that (L, n) imply returns
+ *   QUEEN_ERR_SHAPE.  A corrupt stream, one that does not match (L, n), or a chunk whose words
+ *   lie outside stream_bytes sets QUEEN_ERR_INDEX (sticky; the mismatched category or chunk
+ *   writes nothing, and no read or write leaves the stream or latents_out). */
 queen_status queen_entropy_encode(const int8_t* latents, int32_t L, int32_t n, int32_t n_pad, void* out,
                                   size_t capacity, size_t* bytes);
-queen_status queen_entropy_decode(queen_ctx* ctx, const void* stream_dev, int32_t L, int32_t n, int32_t n_pad,
-                                  int8_t* latents_out, void* stream);
+queen_status queen_entropy_decode(queen_ctx* ctx, const void* stream_dev, int64_t stream_bytes, int32_t L, int32_t n,
+                                  int32_t n_pad, int8_t* latents_out, void* stream);
 /* queen_entropy_decode_frame: all five categories of a frame in ONE launch.  streams_dev
- * (HOST array of 5 device pointers, NULL where lat_dim[c] = 0), lat_dim[5] (host); output
- * latents_out[sum L][n_pad] int8 in category-major row order (the queen_packet layout). */
-queen_status queen_entropy_decode_frame(queen_ctx* ctx, const void* const* streams_dev, const int32_t* lat_dim,
-                                        int32_t n, int32_t n_pad, int8_t* latents_out, void* stream);
+ * (HOST array of 5 device pointers, NULL where lat_dim[c] = 0), stream_bytes[5] (host; each
+ * stream's size, the packet's ans_bytes), lat_dim[5] (host); output latents_out[sum L][n_pad]
+ * int8 in category-major row order (the queen_packet layout).  Errors as queen_entropy_decode. */
+queen_status queen_entropy_decode_frame(queen_ctx* ctx, const void* const* streams_dev, const int64_t* stream_bytes,
+                                        const int32_t* lat_dim, int32_t n, int32_t n_pad, int8_t* latents_out,
+                                        void* stream);
 
 /* ---- NEXT #4: backward rasterizer (P:239-251 trains through Eq. 1-2) -----------------------
  * Gradients of L with respect to the inputs of the forward, holding its discrete decisions
@@ -322,6 +327,14 @@ queen_status queen_wait_rendered(const queen_ctx* ctx, void* stream);
  * waits for the recorded events and returns per-stage summed milliseconds and kernel
  * launches (double[10], int64[10]), optionally resetting them.  Not capturable. */
 queen_status queen_profile_enable(queen_ctx* ctx, int32_t enable);
+
+/* Context options (test / experiment switches, set once per context, default 0):
+ *   QUEEN_OPT_BLEND_NOMASK      k_blend without the per-warp record lists (per-thread box cull
+ *                               only) -- the reference the exactness test of the lists compares to;
+ *   QUEEN_OPT_BLEND_GRID_ORDER  blend tiles in grid order instead of longest-list-first.
+ * Neither changes any output bit (both are tested).  Unknown bits -> QUEEN_ERR_INVALID_ARG. */
+enum { QUEEN_OPT_BLEND_NOMASK = 1, QUEEN_OPT_BLEND_GRID_ORDER = 2 };
+queen_status queen_set_options(queen_ctx* ctx, int32_t opts);
 queen_status queen_profile_read(queen_ctx* ctx, double* ms, int64_t* launches, int32_t reset);
 
 #ifdef __cplusplus

@@ -24,6 +24,7 @@ STATUS = {0: "QUEEN_OK", -1: "QUEEN_ERR_INVALID_ARG", -2: "QUEEN_ERR_SHAPE", -3:
 QUEEN_LAT_INT8, QUEEN_LAT_F32 = 0, 1
 QUEEN_POS_COO, QUEEN_POS_GATES, QUEEN_POS_NONE = 0, 1, 2
 QUEEN_MAX_VIEWS = 64
+QUEEN_OPT_BLEND_NOMASK, QUEEN_OPT_BLEND_GRID_ORDER = 1, 2
 
 # exported C symbols (include/queen.h); tests check the library exports every one
 EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version", "queen_workspace_size",
@@ -33,7 +34,7 @@ EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version",
            "queen_wait_rendered", "queen_entropy_encode",
            "queen_entropy_decode", "queen_entropy_decode_frame", "queen_render_mask",
            "queen_densify", "queen_rasterize_rgb8", "queen_render_views_rgb8",
-           "queen_rasterize_backward", "queen_project_backward", "queen_decode_backward"]
+           "queen_rasterize_backward", "queen_project_backward", "queen_decode_backward", "queen_set_options"]
 STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy", "blend_order"]
 
 
@@ -106,6 +107,7 @@ def lib() -> C.CDLL:
             "queen_blend_counts": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
                                          p, p, p]),
             "queen_profile_enable": (i32, [p, i32]),
+            "queen_set_options": (i32, [p, i32]),
             "queen_decode_backward": (i32, [p, C.POINTER(QueenPacket), p, p, p, p, p, p]),
             "queen_rasterize_backward": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera),
                                                i32, C.POINTER(C.c_float), p, p, p]),
@@ -121,8 +123,9 @@ def lib() -> C.CDLL:
             "queen_set_blend_stream": (i32, [p, p]),
             "queen_wait_rendered": (i32, [p, p]),
             "queen_entropy_encode": (i32, [p, i32, i32, i32, p, C.c_size_t, C.POINTER(C.c_size_t)]),
-            "queen_entropy_decode": (i32, [p, p, i32, i32, i32, p, p]),
-            "queen_entropy_decode_frame": (i32, [p, C.POINTER(C.c_void_p), C.POINTER(C.c_int32), i32, i32, p, p]),
+            "queen_entropy_decode": (i32, [p, p, C.c_int64, i32, i32, i32, p, p]),
+            "queen_entropy_decode_frame": (i32, [p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                                 i32, i32, p, p]),
             "queen_profile_read": (i32, [p, C.POINTER(C.c_double), C.POINTER(C.c_int64), i32]),
         }
         for name, (res, args) in sig.items():
@@ -222,6 +225,9 @@ class Context:
         info = C.c_int64(0)
         st = lib().queen_check(self._h, C.c_void_p(_stream(stream)), C.byref(info))
         return st, int(info.value)
+
+    def set_options(self, opts: int):
+        self._chk(lib().queen_set_options(self._h, int(opts)), "queen_set_options")
 
     def profile(self, enable: bool = True):
         self._chk(lib().queen_profile_enable(self._h, 1 if enable else 0), "queen_profile_enable")
@@ -397,17 +403,21 @@ def queen_entropy_encode(latents: np.ndarray, n: int) -> np.ndarray:
     return out[: nb.value].copy()
 
 
-def queen_entropy_decode(ctx: Context, stream_dev, L: int, n: int, latents_out, stream=None):
-    st = lib().queen_entropy_decode(ctx.handle, _ptr(stream_dev), L, n, latents_out.shape[-1], _ptr(latents_out),
+def queen_entropy_decode(ctx: Context, stream_dev, L: int, n: int, latents_out, stream=None, nbytes: int | None = None):
+    """stream_dev: device uint8 tensor holding one QANS stream (nbytes defaults to its size)."""
+    nb = int(stream_dev.numel() * stream_dev.element_size()) if nbytes is None else int(nbytes)
+    st = lib().queen_entropy_decode(ctx.handle, _ptr(stream_dev), nb, L, n, latents_out.shape[-1], _ptr(latents_out),
                                     C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_entropy_decode")
 
 
-def queen_entropy_decode_frame(ctx: Context, stream_ptrs, lat_dim, n: int, latents_out, stream=None):
-    """Decode every category of a frame in one launch (stream_ptrs: 5 device addresses or None)."""
+def queen_entropy_decode_frame(ctx: Context, stream_ptrs, stream_bytes, lat_dim, n: int, latents_out, stream=None):
+    """Decode every category of a frame in one launch (stream_ptrs: 5 device addresses or None;
+    stream_bytes: the 5 stream sizes)."""
     ptrs = (C.c_void_p * 5)(*[C.c_void_p(int(p)) if p else None for p in stream_ptrs])
+    nbs = (C.c_int64 * 5)(*[int(x) for x in stream_bytes])
     dims = (C.c_int32 * 5)(*[int(x) for x in lat_dim])
-    st = lib().queen_entropy_decode_frame(ctx.handle, ptrs, dims, n, latents_out.shape[-1], _ptr(latents_out),
+    st = lib().queen_entropy_decode_frame(ctx.handle, ptrs, nbs, dims, n, latents_out.shape[-1], _ptr(latents_out),
                                           C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_entropy_decode_frame")
 

@@ -28,6 +28,10 @@ __global__ void __launch_bounds__(256) k_densify_keep(const float* __restrict__ 
     }
     if (lo < n_rem && rem[lo] == (uint32_t)i) return;  // removed
     const int j = i - lo;
+    // a valid list puts every kept column below n_old - n_rem; a bad one (duplicate, unsorted or
+    // out-of-range entries, already flagged above) must not write into the additions or past
+    // the destination's n_pad
+    if (j >= n_old - n_rem) return;
     for (int p = 0; p < P; ++p) dst[(int64_t)p * np_dst + j] = src[(int64_t)p * np_src + i];
 }
 

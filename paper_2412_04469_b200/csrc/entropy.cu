@@ -14,6 +14,7 @@
 // Symbols are the category's latent matrix flattened row-major (k * n + i, k < L, i < n);
 // chunk j holds symbols [j*CH, (j+1)*CH), CH = 8192; lane l of chunk j decodes symbols
 // j*CH + 32 t + l for t = 0, 1, ...  rANS: 32-bit state in [2^16, 2^32), 16-bit renormalisation.
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -62,123 +63,134 @@ static void normalise(const uint64_t cnt[256], uint64_t total, uint16_t f[256]) 
 }
 
 // ---------------------------------------------------------------- device decoder
-// Two launches per frame: k_ans_table builds every category's slot tables once (slot ->
-// f | (slot - c) << 16 as u32, and slot -> the decoded int8 latent, 20 KB per category, in the
-// workspace); k_ans_decode copies its category's tables to shared memory and decodes, one warp
-// per chunk, one rANS state per lane: a decode step is ONE shared load + a multiply-add on the
-// state's critical path (the symbol byte is looked up beside it).
-constexpr int ANS_WARPS = 4;
+// One launch per frame (every category).  A block builds its category's slot table in shared
+// memory straight from the stream's 256 frequencies: slot -> (f - 1) | (slot - c) << 12 |
+// latent byte << 24, one 32-bit word, so a decode step is ONE shared load + a multiply-add on
+// the state's critical path.  Each warp then decodes chunks with one rANS state per lane; the
+// chunk's renormalisation words pass through a 128-word shared-memory window per warp (refilled
+// 64 words at a time from a register prefetch issued one refill ahead), so a renormalisation is
+// a ballot + one shared load.
+//
+// Bounds (every stream is wire input): the host passes each category's expected symbol and
+// chunk counts (L * n, from the packet shape) and the stream's byte size.  A block whose
+// header does not match (magic, n_sym, n_chunks, frequency sum) raises QUEEN_ERR_INDEX and
+// writes nothing; a chunk whose word range lies outside the stream raises it and writes
+// nothing; every decoded symbol index stays below the host n_sym.
+constexpr int ANS_WARPS = 8;
+constexpr int ANS_WIN = 128;  // words in a warp's shared-memory window
 
 struct AnsFrame {
     const unsigned char* stream[5];
     int L[5];
     int row0[5];          // first latent row of the category in the [sum L][n_pad] matrix
     int block0[6];        // first block of each category (prefix), block0[5] = total blocks
+    uint32_t n_sym[5];    // host-expected symbols (L * n) and chunks of each category
+    uint32_t n_chunks[5];
+    uint32_t n_words[5];  // 16-bit renormalisation words the stream's byte size can hold
     int n, n_pad;
-    const uint32_t* table;  // [5][ANS_M] (f | (slot - c) << 16), then [5][ANS_M] int8 symbols (k_ans_table)
 };
 
-__global__ void __launch_bounds__(256) k_ans_table(const AnsFrame fr, uint32_t* __restrict__ table, DevFlags* fl) {
-    __shared__ uint16_t s_f[256];
-    __shared__ uint32_t s_c[257];
-    const int cat = blockIdx.y;
-    if (fr.L[cat] == 0) return;
-    const AnsHeader* h = reinterpret_cast<const AnsHeader*>(fr.stream[cat]);
-    for (int q = threadIdx.x; q < 256; q += blockDim.x) s_f[q] = h->freq[q];
-    __syncthreads();
-    if (threadIdx.x < 32) {  // exclusive scan of the 256 frequencies by one warp
-        uint32_t v[8], sum = 0;
-        for (int q = 0; q < 8; ++q) { v[q] = s_f[threadIdx.x * 8 + q]; sum += v[q]; }
-        uint32_t inc = sum;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (threadIdx.x >= o) inc += y;
-        }
-        uint32_t run = inc - sum;
-        for (int q = 0; q < 8; ++q) { s_c[threadIdx.x * 8 + q] = run; run += v[q]; }
-        if (threadIdx.x == 31) s_c[256] = run;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && blockIdx.x == 0 && s_c[256] != ANS_M) raise_flag(fl, FLAG_INDEX);  // corrupt table
-    const uint32_t slot = blockIdx.x * blockDim.x + threadIdx.x;  // symbol s with c[s] <= slot < c[s+1]
-    if (slot >= ANS_M) return;
-    int lo = 0, hi = 256;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (s_c[mid] <= slot) lo = mid; else hi = mid;
-    }
-    const uint32_t f = s_f[lo];
-    table[(size_t)cat * ANS_M + slot] = f | ((slot - s_c[lo]) << 16);
-    reinterpret_cast<int8_t*>(table + 5 * ANS_M)[(size_t)cat * ANS_M + slot] = (int8_t)(lo - 128);
-}
-
-__global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr, int8_t* __restrict__ out, DevFlags* fl) {
+__global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr, int8_t* __restrict__ out,
+                                                               DevFlags* fl) {
     __shared__ uint32_t s_tab[ANS_M];
-    __shared__ int8_t s_sym[ANS_M];
+    __shared__ uint32_t s_c[257];
+    __shared__ uint32_t s_win[ANS_WARPS][ANS_WIN];
     int cat = 0;
     while (cat < 4 && (int)blockIdx.x >= fr.block0[cat + 1]) ++cat;
     const unsigned char* stream = fr.stream[cat];
-    const int L = fr.L[cat], n = fr.n, n_pad = fr.n_pad;
+    const int n = fr.n, n_pad = fr.n_pad;
     const AnsHeader* h = reinterpret_cast<const AnsHeader*>(stream);
-    const uint32_t n_sym = h->n_sym, n_chunks = h->n_chunks;
-    if (threadIdx.x == 0 && (h->magic != ANS_MAGIC || n_sym != (uint32_t)L * (uint32_t)n)) raise_flag(fl, FLAG_INDEX);
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(fr.table + (size_t)cat * ANS_M);
-        uint4* dst = reinterpret_cast<uint4*>(s_tab);
-        for (int q = threadIdx.x; q < ANS_M / 4; q += blockDim.x) dst[q] = __ldg(src + q);
-        const uint4* ssrc = reinterpret_cast<const uint4*>(reinterpret_cast<const int8_t*>(fr.table + 5 * ANS_M) +
-                                                           (size_t)cat * ANS_M);
-        for (int q = threadIdx.x; q < ANS_M / 16; q += blockDim.x) reinterpret_cast<uint4*>(s_sym)[q] = __ldg(ssrc + q);
+    const uint32_t n_sym = fr.n_sym[cat], n_chunks = fr.n_chunks[cat];
+    if (h->magic != ANS_MAGIC || h->n_sym != n_sym || h->n_chunks != n_chunks) {  // block-uniform
+        if (threadIdx.x == 0) raise_flag(fl, FLAG_INDEX);
+        return;
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (wid == 0) {  // exclusive scan of the 256 frequencies by one warp
+        uint32_t v[8], sum = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { v[q] = h->freq[lane * 8 + q]; sum += v[q]; }
+        uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        uint32_t run = inc - sum;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { s_c[lane * 8 + q] = run; run += v[q]; }
+        if (lane == 31) s_c[256] = run;
     }
     __syncthreads();
-    const uint32_t chunk = (blockIdx.x - fr.block0[cat]) * ANS_WARPS + (threadIdx.x >> 5);
+    if (s_c[256] != ANS_M) {  // corrupt frequency table (block-uniform)
+        if (threadIdx.x == 0) raise_flag(fl, FLAG_INDEX);
+        return;
+    }
+    {  // slot table: thread t fills slots [t*SPT, (t+1)*SPT): binary search once, then walk
+        constexpr int SPT = ANS_M / (ANS_WARPS * 32);
+        const uint32_t s0 = threadIdx.x * SPT;
+        int lo = 0, hi = 256;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_c[mid] <= s0) lo = mid; else hi = mid;
+        }
+        uint32_t c_lo = s_c[lo], c_hi = s_c[lo + 1];
+        for (uint32_t slot = s0; slot < s0 + SPT; ++slot) {
+            while (slot >= c_hi) { ++lo; c_lo = c_hi; c_hi = s_c[lo + 1]; }
+            s_tab[slot] = (c_hi - c_lo - 1u) | ((slot - c_lo) << 12) | ((uint32_t)(uint8_t)(lo - 128) << 24);
+        }
+    }
+    __syncthreads();
+    const uint32_t chunk = (blockIdx.x - fr.block0[cat]) * ANS_WARPS + wid;
     if (chunk >= n_chunks) return;
-    const uint32_t lane = threadIdx.x & 31;
     const uint32_t* woff = reinterpret_cast<const uint32_t*>(stream + sizeof(AnsHeader));
     const uint32_t* states = woff + n_chunks + 1;
     const uint16_t* words = reinterpret_cast<const uint16_t*>(states + (size_t)n_chunks * ANS_LANES);
-    int8_t* cout = out + (size_t)fr.row0[cat] * n_pad;
-    uint32_t x = states[(size_t)chunk * ANS_LANES + lane];
     uint32_t ptr = woff[chunk];
     const uint32_t end = woff[chunk + 1];
+    if (ptr > end || end > fr.n_words[cat]) {  // warp-uniform
+        if (lane == 0) raise_flag(fl, FLAG_INDEX);
+        return;
+    }
+    int8_t* cout = out + (size_t)fr.row0[cat] * n_pad;
+    uint32_t x = states[(size_t)chunk * ANS_LANES + lane];
     const uint32_t base = chunk * ANS_CHUNK;
     const uint32_t len = min((uint32_t)ANS_CHUNK, n_sym - base);
-    const uint32_t steps = (len + 31) / 32;
     const uint32_t lt = (1u << lane) - 1u;
     const uint32_t k = (base + lane) / (uint32_t)n;
     uint32_t i = (base + lane) - k * (uint32_t)n;
     int8_t* op = cout + (size_t)k * n_pad + i;  // this lane's next output byte (row k, column i)
-    // The chunk's renormalisation words are consumed in order, ~1 per step for the warp.
-    // Keep a 128-word window in registers (4 words per lane: current 64 + next 64), so a
-    // renormalisation is a shuffle, and the next 64 words load one window ahead.
+    uint32_t* win = s_win[wid];
     auto ld = [&](uint32_t w) -> uint32_t { return w < end ? (uint32_t)__ldg(words + w) : 0u; };
-    uint32_t wbase = ptr;
-    uint32_t c0 = ld(wbase + lane), c1 = ld(wbase + 32 + lane), n0 = ld(wbase + 64 + lane), n1 = ld(wbase + 96 + lane);
+    uint32_t wbase = ptr;  // window = words [wbase, wbase + 128) at win[(w - wbase0) & 127]
+#pragma unroll
+    for (int q = 0; q < 4; ++q) win[q * 32 + lane] = ld(wbase + q * 32 + lane);
+    uint32_t pre0 = ld(wbase + 128 + lane), pre1 = ld(wbase + 160 + lane);  // next refill
+    uint32_t wpos = 0;  // window slot of word wbase
+    __syncwarp();
+    const uint32_t steps = (len + 31) / 32;
     for (uint32_t t = 0; t < steps; ++t) {
         const bool active = t * 32 + lane < len;
-        const uint32_t slot = x & (ANS_M - 1);
-        const uint32_t e = s_tab[slot];
-        const uint32_t xn = (e & 0xffffu) * (x >> ANS_PROB_BITS) + (e >> 16);
+        const uint32_t e = s_tab[x & (ANS_M - 1)];
         if (active) {
-            x = xn;
-            *op = s_sym[slot];
+            x = ((e & 0xfffu) + 1u) * (x >> ANS_PROB_BITS) + ((e >> 12) & 0xfffu);
+            *op = (int8_t)(e >> 24);
         }
         const bool need = active && x < ANS_L;
         const uint32_t m = __ballot_sync(0xffffffffu, need);
         if (m) {
-            const uint32_t q = ptr - wbase + __popc(m & lt);  // window position of this lane's word (< 96)
-            const uint32_t src = q & 31u;
-            const uint32_t a0 = __shfl_sync(0xffffffffu, c0, src), a1 = __shfl_sync(0xffffffffu, c1, src);
-            const uint32_t a2 = __shfl_sync(0xffffffffu, n0, src);
-            const uint32_t wv = q < 32 ? a0 : (q < 64 ? a1 : a2);
-            if (need) x = (x << 16) | wv;
+            const uint32_t q = ptr - wbase + __popc(m & lt);  // < 96: inside the window
+            if (need) x = (x << 16) | win[(wpos + q) & (ANS_WIN - 1)];
             ptr += __popc(m);
-            if (ptr - wbase >= 64) {  // slide the window by 64 words
+            if (ptr - wbase >= 64) {  // the oldest 64 words are consumed: refill them
+                __syncwarp();
+                win[(wpos + lane) & (ANS_WIN - 1)] = pre0;
+                win[(wpos + 32 + lane) & (ANS_WIN - 1)] = pre1;
+                wpos = (wpos + 64) & (ANS_WIN - 1);
                 wbase += 64;
-                c0 = n0;
-                c1 = n1;
-                n0 = ld(wbase + 64 + lane);
-                n1 = ld(wbase + 96 + lane);
+                pre0 = ld(wbase + 128 + lane);
+                pre1 = ld(wbase + 160 + lane);
+                __syncwarp();
             }
         }
         i += 32;  // next symbol of this lane: flat index + 32
@@ -188,12 +200,26 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
     if (ptr != end || x != ANS_L) raise_flag(fl, FLAG_INDEX);  // corrupt / mismatched stream
 }
 
-cudaError_t launch_ans_decode_frame(const void* const streams[5], const int L[5], int n, int n_pad, int8_t* out,
-                                    uint32_t* table, DevFlags* fl, cudaStream_t s) {
+// host: expected counts of one category's stream (L * n symbols), and the renormalisation
+// words its byte size can hold; false if the stream cannot even hold its header and tables
+static bool ans_expect(int L, int n, int64_t bytes, uint32_t& n_sym, uint32_t& n_chunks, uint32_t& n_words) {
+    const uint64_t ns = (uint64_t)L * (uint64_t)n;
+    if (ns > 0xffffffffull) return false;
+    n_sym = (uint32_t)ns;
+    n_chunks = (uint32_t)((ns + ANS_CHUNK - 1) / ANS_CHUNK);
+    const int64_t fixed = (int64_t)sizeof(AnsHeader) + 4 * ((int64_t)n_chunks + 1) + 4 * (int64_t)ANS_LANES * n_chunks;
+    if (bytes < fixed) return false;
+    const int64_t nw = (bytes - fixed) / 2;
+    n_words = (uint32_t)std::min<int64_t>(nw, 0xffffffffll);
+    return true;
+}
+
+// returns cudaErrorInvalidValue when a stream is too small for its (L, n) (host-detectable)
+cudaError_t launch_ans_decode_frame(const void* const streams[5], const int64_t bytes[5], const int L[5], int n,
+                                    int n_pad, int8_t* out, DevFlags* fl, cudaStream_t s) {
     AnsFrame fr{};
     fr.n = n;
     fr.n_pad = n_pad;
-    fr.table = table;
     int row = 0, blk = 0;
     for (int c = 0; c < 5; ++c) {
         fr.stream[c] = static_cast<const unsigned char*>(streams[c]);
@@ -201,21 +227,22 @@ cudaError_t launch_ans_decode_frame(const void* const streams[5], const int L[5]
         fr.row0[c] = row;
         fr.block0[c] = blk;
         row += L[c] > 0 ? L[c] : 0;
-        const int64_t chunks = ((int64_t)fr.L[c] * n + ANS_CHUNK - 1) / ANS_CHUNK;
-        blk += (int)((chunks + ANS_WARPS - 1) / ANS_WARPS);
+        if (fr.L[c] == 0 || n == 0) continue;
+        if (!ans_expect(fr.L[c], n, bytes[c], fr.n_sym[c], fr.n_chunks[c], fr.n_words[c])) return cudaErrorInvalidValue;
+        blk += (int)((fr.n_chunks[c] + ANS_WARPS - 1) / ANS_WARPS);
     }
     fr.block0[5] = blk;
     if (blk == 0) return cudaSuccess;
-    k_ans_table<<<dim3(ANS_M / 256, 5), 256, 0, s>>>(fr, table, fl);
     k_ans_decode<<<blk, ANS_WARPS * 32, 0, s>>>(fr, out, fl);
     return cudaGetLastError();
 }
 
-cudaError_t launch_ans_decode(const void* stream_dev, int L, int n, int n_pad, int8_t* out, uint32_t* table,
+cudaError_t launch_ans_decode(const void* stream_dev, int64_t bytes, int L, int n, int n_pad, int8_t* out,
                               DevFlags* fl, cudaStream_t s) {
     const void* streams[5] = {stream_dev, nullptr, nullptr, nullptr, nullptr};
+    const int64_t b5[5] = {bytes, 0, 0, 0, 0};
     const int Ls[5] = {L, 0, 0, 0, 0};
-    return launch_ans_decode_frame(streams, Ls, n, n_pad, out, table, fl, s);
+    return launch_ans_decode_frame(streams, b5, Ls, n, n_pad, out, fl, s);
 }
 
 // ---------------------------------------------------------------- host encoder

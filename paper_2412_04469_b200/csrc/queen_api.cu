@@ -22,6 +22,7 @@ struct queen_ctx {
     cudaEvent_t rendered = nullptr;     // recorded by queen_render_views after the blend
     cudaStream_t blend_stream = nullptr;  // queen_set_blend_stream: the blend's own stream
     bool blend_elsewhere = false;         // the most recent blend ran on blend_stream
+    int32_t opts = 0;                     // queen_set_options (test / experiment switches)
     std::string err;
 };
 
@@ -33,10 +34,10 @@ float host_theta0(float tau, float g0, float g1) {
 cudaError_t init_binning_attributes();
 int key_passes(int64_t gtiles);
 size_t ans_encode(const int8_t* lat, int L, int n, int n_pad, std::vector<unsigned char>& out);
-cudaError_t launch_ans_decode(const void* stream_dev, int L, int n, int n_pad, int8_t* out, uint32_t* table,
+cudaError_t launch_ans_decode(const void* stream_dev, int64_t bytes, int L, int n, int n_pad, int8_t* out,
                               DevFlags* fl, cudaStream_t s);
-cudaError_t launch_ans_decode_frame(const void* const streams[5], const int L[5], int n, int n_pad, int8_t* out,
-                                    uint32_t* table, DevFlags* fl, cudaStream_t s);
+cudaError_t launch_ans_decode_frame(const void* const streams[5], const int64_t bytes[5], const int L[5], int n,
+                                    int n_pad, int8_t* out, DevFlags* fl, cudaStream_t s);
 }  // namespace queen
 
 using namespace queen;
@@ -300,7 +301,7 @@ static queen_status rasterize_impl(queen_ctx* ctx, const queen_proj* proj, const
     cudaError_t e = launch_rasterize(proj->rec, proj->n_pad, bins->ranges, vals, n_views, cams[0].width, cams[0].height,
                                      bg[0], bg[1], bg[2], rgb_out, T_out, rgb8_out, rgb8_out ? OUT_RGB8 : OUT_F32, 0.f,
                                      order_scratch(ctx, n_views, cams[0].width, cams[0].height),
-                                     static_cast<cudaStream_t>(stream), &nl, &ctx->prof);
+                                     static_cast<cudaStream_t>(stream), &nl, &ctx->prof, ctx->opts);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "rasterize");
     return QUEEN_OK;
 }
@@ -329,6 +330,13 @@ queen_status queen_blend_counts(queen_ctx* ctx, const queen_proj* proj, const qu
                                         cams[0].height, reinterpret_cast<long long*>(evaluated),
                                         reinterpret_cast<long long*>(composited), static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "blend_counts");
+    return QUEEN_OK;
+}
+
+queen_status queen_set_options(queen_ctx* ctx, int32_t opts) {
+    if (!ctx) return QUEEN_ERR_INVALID_ARG;
+    if (opts & ~(QUEEN_OPT_BLEND_NOMASK | QUEEN_OPT_BLEND_GRID_ORDER)) return fail(ctx, QUEEN_ERR_INVALID_ARG, "unknown option bits");
+    ctx->opts = opts;
     return QUEEN_OK;
 }
 
@@ -375,35 +383,39 @@ queen_status queen_entropy_encode(const int8_t* latents, int32_t L, int32_t n, i
     return QUEEN_OK;
 }
 
-queen_status queen_entropy_decode(queen_ctx* ctx, const void* stream_dev, int32_t L, int32_t n, int32_t n_pad,
-                                  int8_t* latents_out, void* stream) {
+queen_status queen_entropy_decode(queen_ctx* ctx, const void* stream_dev, int64_t stream_bytes, int32_t L, int32_t n,
+                                  int32_t n_pad, int8_t* latents_out, void* stream) {
     if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
     if (!stream_dev || !latents_out || L < 0 || L > 16 || n < 0 || n > n_pad) return fail(ctx, QUEEN_ERR_INVALID_ARG, "entropy decode args");
     ctx->prof.begin(ST_ENTROPY, static_cast<cudaStream_t>(stream));
-    uint32_t* tab = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(ctx->ws) + ctx->L.ans_table);
-    cudaError_t e = launch_ans_decode(stream_dev, L, n, n_pad, latents_out, tab, flags_of(ctx),
+    cudaError_t e = launch_ans_decode(stream_dev, stream_bytes, L, n, n_pad, latents_out, flags_of(ctx),
                                       static_cast<cudaStream_t>(stream));
-    ctx->prof.end(static_cast<cudaStream_t>(stream), 2);
+    ctx->prof.end(static_cast<cudaStream_t>(stream), 1);
+    if (e == cudaErrorInvalidValue) return fail(ctx, QUEEN_ERR_SHAPE, "entropy stream smaller than its header and chunk tables");
     if (e != cudaSuccess) return cuda_fail(ctx, e, "entropy decode");
     return QUEEN_OK;
 }
 
-queen_status queen_entropy_decode_frame(queen_ctx* ctx, const void* const* streams_dev, const int32_t* lat_dim,
-                                        int32_t n, int32_t n_pad, int8_t* latents_out, void* stream) {
+queen_status queen_entropy_decode_frame(queen_ctx* ctx, const void* const* streams_dev, const int64_t* stream_bytes,
+                                        const int32_t* lat_dim, int32_t n, int32_t n_pad, int8_t* latents_out,
+                                        void* stream) {
     if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
-    if (!streams_dev || !lat_dim || !latents_out || n < 0 || n > n_pad) return fail(ctx, QUEEN_ERR_INVALID_ARG, "entropy frame args");
+    if (!streams_dev || !stream_bytes || !lat_dim || !latents_out || n < 0 || n > n_pad)
+        return fail(ctx, QUEEN_ERR_INVALID_ARG, "entropy frame args");
     const void* s5[5];
     int L5[5];
+    int64_t b5[5];
     for (int c = 0; c < 5; ++c) {
         if (lat_dim[c] < 0 || lat_dim[c] > 16 || (lat_dim[c] > 0 && !streams_dev[c])) return fail(ctx, QUEEN_ERR_INVALID_ARG, "entropy frame category");
         s5[c] = streams_dev[c];
         L5[c] = lat_dim[c];
+        b5[c] = stream_bytes[c];
     }
     ctx->prof.begin(ST_ENTROPY, static_cast<cudaStream_t>(stream));
-    uint32_t* tab = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(ctx->ws) + ctx->L.ans_table);
-    cudaError_t e = launch_ans_decode_frame(s5, L5, n, n_pad, latents_out, tab, flags_of(ctx),
+    cudaError_t e = launch_ans_decode_frame(s5, b5, L5, n, n_pad, latents_out, flags_of(ctx),
                                             static_cast<cudaStream_t>(stream));
-    ctx->prof.end(static_cast<cudaStream_t>(stream), 2);
+    ctx->prof.end(static_cast<cudaStream_t>(stream), 1);
+    if (e == cudaErrorInvalidValue) return fail(ctx, QUEEN_ERR_SHAPE, "entropy stream smaller than its header and chunk tables");
     if (e != cudaSuccess) return cuda_fail(ctx, e, "entropy decode frame");
     return QUEEN_OK;
 }
@@ -574,7 +586,7 @@ queen_status queen_render_mask(queen_ctx* ctx, const queen_gaussians* scene, con
     ctx->prof.begin(ST_BLEND, s);
     int nl = 1;
     e = launch_rasterize(pj.rec, pj.n_pad, b.ranges, vals, n_views, W, H, 0.f, 0.f, 0.f, nullptr, nullptr, mask_out,
-                         OUT_MASK, alpha_thresh, order_scratch(ctx, n_views, W, H), s, &nl, nullptr);
+                         OUT_MASK, alpha_thresh, order_scratch(ctx, n_views, W, H), s, &nl, nullptr, ctx->opts);
     if (e == cudaSuccess) e = launch_dilate(mask_out, reinterpret_cast<uint8_t*>(ws + L.mask_tmp), n_views, W, H, dilation, s);
     ctx->prof.end(s, nl + (dilation > 1 ? 2 : 0));
     if (e != cudaSuccess) return cuda_fail(ctx, e, "render_mask");

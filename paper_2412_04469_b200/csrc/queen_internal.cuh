@@ -119,7 +119,7 @@ constexpr int ORDER_BINS = 64;
 struct WsLayout {
     // scratch (bin_sort)
     size_t flags, hist, dminmax, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, counts, view_tot, slab_counts,
-        slab_vis, select, ans_table, order, total_scratch;
+        slab_vis, select, order, total_scratch;
     // render_views / render_mask buffers
     size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, mask_tmp, total;
     int64_t key_tiles, elem_tiles, os_key_tiles, os_elem_tiles, T, elems;
@@ -153,7 +153,6 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     L.slab_counts = o; o += align256(sizeof(uint32_t) * (size_t)(bp.ok ? bp.slabs : 0) * L.T);
     L.slab_vis = o; o += align256(sizeof(uint32_t) * (size_t)(bp.slabs + 1));
     L.select = o; o += align256((size_t)n_pad);  // render_mask: per-Gaussian subset flags
-    L.ans_table = o; o += align256((sizeof(uint32_t) + 1) * 5 * 4096);  // entropy decode slot + symbol tables
     L.order = o; o += align256(sizeof(uint32_t) * (2 * ORDER_BINS + (size_t)n_views * L.T));  // blend tile order
     L.total_scratch = o;
     L.rec = o; o += align256(sizeof(float) * REC_WORDS * L.elems);
@@ -178,7 +177,7 @@ inline bool scratch_fits(const WsLayout& need, const WsLayout& have) {
                                    &WsLayout::depth_lb,   &WsLayout::tile_lb,     &WsLayout::dkeys,
                                    &WsLayout::dkeys_alt,  &WsLayout::dvals,       &WsLayout::dvals_alt,
                                    &WsLayout::counts,     &WsLayout::view_tot,    &WsLayout::slab_counts,
-                                   &WsLayout::slab_vis,   &WsLayout::select,      &WsLayout::ans_table,
+                                   &WsLayout::slab_vis,   &WsLayout::select,      &WsLayout::order,
                                    &WsLayout::total_scratch};
     for (size_t q = 0; q + 1 < sizeof(r) / sizeof(r[0]); ++q)
         if (need.*r[q + 1] - need.*r[q] > have.*r[q + 1] - have.*r[q]) return false;
@@ -339,11 +338,11 @@ enum : int { OUT_F32 = 0, OUT_MASK = 1, OUT_RGB8 = 2 };  // k_blend epilogues
 cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
                              uint8_t* out8, int out_mode, float mask_thresh, uint32_t* order_ws, cudaStream_t s,
-                             int* n_launch = nullptr, Prof* prof = nullptr);
+                             int* n_launch = nullptr, Prof* prof = nullptr, int opts = 0);
 // blend schedule: *order = longest-list-first permutation of the blocks gt tiles (in order_ws),
 // or nullptr (grid order) when there is no scratch
 cudaError_t launch_tile_order(const uint32_t* ranges, int64_t blocks, uint32_t* order_ws, cudaStream_t s,
-                              const uint32_t** order);
+                              const uint32_t** order, int opts = 0);
 cudaError_t launch_select(const uint32_t* idx, int k, const int32_t* k_dev, int n, int n_pad, uint8_t* select,
                           DevFlags* fl, cudaStream_t s);
 cudaError_t launch_dilate(uint8_t* marks, uint8_t* tmp, int n_views, int W, int H, int d, cudaStream_t s);

@@ -377,9 +377,9 @@ __global__ void __launch_bounds__(256) k_order_scatter(const uint2* __restrict__
 }
 
 cudaError_t launch_tile_order(const uint32_t* ranges, int64_t blocks, uint32_t* order_ws, cudaStream_t s,
-                              const uint32_t** order) {
+                              const uint32_t** order, int opts) {
     *order = nullptr;
-    if (!order_ws || blocks == 0 || getenv("QUEEN_BLEND_GRID_ORDER")) return cudaSuccess;  // env: test hook
+    if (!order_ws || blocks == 0 || (opts & QUEEN_OPT_BLEND_GRID_ORDER)) return cudaSuccess;
     uint32_t* hist = order_ws;
     uint32_t* cursor = order_ws + ORDER_BINS;
     uint32_t* ord = order_ws + 2 * ORDER_BINS;
@@ -395,7 +395,7 @@ cudaError_t launch_tile_order(const uint32_t* ranges, int64_t blocks, uint32_t* 
 cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
                              uint8_t* out8, int out_mode, float mask_thresh, uint32_t* order_ws, cudaStream_t s,
-                             int* n_launch, Prof* prof) {
+                             int* n_launch, Prof* prof, int opts) {
     const int gx = (W + 15) / 16, gy = (H + 15) / 16;
     const int T = gx * gy;
     const int64_t blocks = (int64_t)T * n_views;
@@ -404,13 +404,13 @@ cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges
     // stage profiler (when given): the tile schedule and the blend are separate stages, so the
     // blend stage times k_blend alone (bench.py's roofline divides its work by that time)
     if (prof) prof->begin(ST_BLEND_ORDER, s);
-    if (cudaError_t e = launch_tile_order(ranges, blocks, order_ws, s, &order)) return e;
+    if (cudaError_t e = launch_tile_order(ranges, blocks, order_ws, s, &order, opts)) return e;
     if (prof) {
         prof->end(s, order ? 2 : 0);
         prof->begin(ST_BLEND, s);
     }
     if (n_launch) *n_launch = order ? 3 : 1;
-    if (getenv("QUEEN_BLEND_NOMASK"))  // test hook: per-thread box cull only (no warp record lists)
+    if (opts & QUEEN_OPT_BLEND_NOMASK)  // test option: per-thread box cull only (no warp record lists)
         k_blend<false, BLEND_RPT, false><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(
             reinterpret_cast<const float4*>(rec), n_pad, reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0, bg1,
             bg2, rgb_out, T_out, out8, out_mode, mask_thresh, nullptr, nullptr, order);

@@ -1,8 +1,9 @@
 """Frame-packet wire format (one contiguous byte buffer per frame, NCCL-broadcastable).
 
 Carries what the paper stores per frame: the decoders D_c (fp32), the
-integer latents L_c (int8 here; entropy coding is out of scope) and the
-COO position residual (u32 indices + fp32 vectors).  Sections are 256-B aligned.
+integer latents L_c and the COO position residual (u32 indices + fp32 vectors).  Version 1
+holds the latents as raw int8; version 2 (below) holds them entropy-coded as one QANS stream
+per category, decoded on the GPU.  Sections are 256-B aligned.
 
   header: 32 x int32 little-endian
     0 magic 'QNFP'  1 version  2 frame  3 n  4 n_pad  5 sh_degree  6-10 lat_dim[5]

@@ -64,7 +64,7 @@ class EntropyPacket:
     """A device-resident entropy-coded frame packet (packet.py version 2).
 
     decode(ctx) enqueues the GPU rANS decode of every category (one warp per 8192-symbol
-    chunk) into an int8 latent scratch [sum L][n_pad]; `struct` is the queen_packet that
+    chunk, bounded by each stream's byte size from the header) into an int8 latent scratch [sum L][n_pad]; `struct` is the queen_packet that
     points at that scratch, the decoders and the COO section (k read on the device), so
     apply = decode(ctx) + queen_apply_frame(struct)."""
 
@@ -85,7 +85,7 @@ class EntropyPacket:
     def decode(self, ctx: Context, stream=None):
         base = self.buf.data_ptr()
         ptrs = [base + self.hdr["ans_off"][c] if self.hdr["lat"][c] else None for c in range(5)]
-        queen_entropy_decode_frame(ctx, ptrs, self.hdr["lat"], self.hdr["n"], self.latents, stream)
+        queen_entropy_decode_frame(ctx, ptrs, self.hdr["ans_bytes"], self.hdr["lat"], self.hdr["n"], self.latents, stream)
 
 
 class Player:
@@ -265,7 +265,7 @@ class Player:
         return rgb
 
     def step2(self, next_pkt, out=None, rgb8: bool = False, rendered: torch.cuda.Event | None = None,
-              ready: torch.cuda.Event | None = None):
+              ready: torch.cuda.Event | None = None, consumed: torch.cuda.Event | None = None):
         """Two-lane pipelined frame step (eager): like step(), but frame t renders on lane t % 2 --
         its own libqueen context (workspace), a high-priority stream for projection + binning and
         a normal-priority stream for the blend (queen_set_blend_stream) -- and the current stream
@@ -273,8 +273,11 @@ class Player:
         frame t's blend.  Frame t+1 starts once packet t+1 is applied (after frame t's binning).
         `rendered` is recorded on the blend stream when frame t's image is complete; `out` must
         not be reused before that (out=None: one of two per-lane image buffers, returned; with_T:
-        per-lane T buffers, self.T_lanes).  Call sync_lanes() before reading results on the
-        current stream."""
+        per-lane T buffers, self.T_lanes).  With out=None the returned buffer is rendered into
+        again two frames later: a caller that reads it on another stream passes `consumed`, an
+        event it records after its last read of THIS call's image (before the step two frames
+        on); that later step's blend waits for it before overwriting the buffer.  Call
+        sync_lanes() before reading results on the current stream."""
         if self.n_lanes != 1:
             raise ValueError("two-lane frame steps need a single view-batch lane")
         main = torch.cuda.current_stream(self.dev)
@@ -301,6 +304,11 @@ class Player:
                 self.T_lanes = [self.T, torch.empty_like(self.T)] if self.T is not None else [None, None]
         rgb = self.rgb_lanes[lane] if out is None else out
         T = self.T_lanes[lane] if self.T is not None else None
+        if not hasattr(self, "_consumed"):
+            self._consumed = [None, None]
+        if self._consumed[lane] is not None:  # the reader of this lane's previous image is done
+            bs.wait_event(self._consumed[lane])
+        self._consumed[lane] = consumed if out is None else None
         fn = queen_render_views_rgb8 if rgb8 else queen_render_views
         queen_set_blend_stream(ctx, bs)  # only for these calls: render() / step() keep one stream
         try:

@@ -52,6 +52,28 @@ def test_densify_errors():
     assert e2.value.status == -2
 
 
+def test_densify_bad_removals_stay_in_bounds():
+    """a removal list with duplicates / out-of-range entries is flagged (-3) and must
+    not write past the kept columns (into the additions) or past the destination's n_pad."""
+    import paper_2412_04469_b200 as Q
+    ctx = Q.Context(0)
+    ctx.set_workspace(64, 1, 16, 16, 1024)
+    a = torch.arange(14 * 64, dtype=torch.float32, device="cuda").reshape(14, 64)
+    # destination [14][48] at the start of a larger buffer: the 64 floats after it are a guard
+    big = torch.full((14 * 48 + 64,), -7.0, dtype=torch.float32, device="cuda")
+    dst = big[:14 * 48].view(14, 48)
+    add = torch.zeros((14, 1), dtype=torch.int16, device="cuda")  # binary16 +0.0
+    # 4 "removals" of which only one is real (duplicates + out of range): 50 - 4 + 1 = 47 <= 48
+    bad = torch.tensor([3, 3, 3, 999], dtype=torch.int32, device="cuda")
+    g_dst = Q.gaussians_struct(dst, 47, 0)
+    Q.queen_densify(ctx, Q.gaussians_struct(a, 50, 0), bad, 4, add, 1, g_dst)
+    assert ctx.check_status()[0] == -3
+    b = big.cpu().numpy()
+    # the addition (column 46 = n_old - n_rem) is intact and nothing crossed it or n_pad
+    assert np.all(b[:14 * 48].reshape(14, 48)[:, 46] == 0.0)
+    assert np.all(b[14 * 48:] == -7.0)
+
+
 def test_densifying_stream_matches_oracle():
     from paper_2412_04469_b200.runtime import Player, device_packet
     cfg = synth.get_config("n3dv", width=333, height=250, focal=280.0)

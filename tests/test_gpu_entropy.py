@@ -53,6 +53,42 @@ def test_gpu_ans_corrupt_stream_flags():
     assert ctx.check_status()[0] == -3
 
 
+def test_gpu_ans_hostile_headers_stay_in_bounds():
+    """the stream header is wire input.  A header claiming more symbols or chunks than
+    (L, n) imply, chunk word offsets past the stream's byte size, or a stream too small for its
+    tables must never read or write out of bounds: the mismatched category writes nothing and
+    QUEEN_ERR_INDEX is raised (or QUEEN_ERR_SHAPE on the host for a truncated stream)."""
+    import paper_2412_04469_b200 as Q
+    L, n = 3, 20000
+    lat = _laplace(L, n, n, 0.3, seed=5)
+    s = Q.queen_entropy_encode(lat, n)
+    hdr = np.frombuffer(s[:16].tobytes(), np.uint32)
+    n_chunks = int(hdr[2])
+    ctx = _ctx()
+    # guard bytes after the output: an out-of-bounds write would change them
+    out = torch.full((L + 1, n), 55, dtype=torch.int8, device="cuda")
+    for word, val in ((1, 10 ** 9), (1, 8191), (2, n_chunks + 5), (2, 0)):
+        bad = s.copy()
+        bad[4 * word:4 * word + 4] = np.array([val], np.uint32).view(np.uint8)
+        Q.queen_entropy_decode(ctx, torch.from_numpy(bad).cuda(), L, n, out[:L])
+        assert ctx.check_status()[0] == -3, (word, val)
+        assert np.all(out.cpu().numpy() == 55), (word, val)  # mismatched header: nothing written
+    # a chunk's end offset far past the stream
+    bad = s.copy()
+    woff = 528 + 4 * 1
+    bad[woff:woff + 4] = np.array([1 << 30], np.uint32).view(np.uint8)
+    Q.queen_entropy_decode(ctx, torch.from_numpy(bad).cuda(), L, n, out[:L])
+    assert ctx.check_status()[0] == -3
+    assert np.all(out[L].cpu().numpy() == 55)
+    # truncated stream (the byte size cannot hold the chunk tables): host error, nothing enqueued
+    with pytest.raises(Q.QueenError):
+        Q.queen_entropy_decode(ctx, torch.from_numpy(s[:600].copy()).cuda(), L, n, out[:L])
+    # the intact stream still decodes exactly afterwards
+    Q.queen_entropy_decode(ctx, torch.from_numpy(s).cuda(), L, n, out[:L])
+    assert ctx.check_status()[0] == 0
+    assert np.array_equal(out[:L].cpu().numpy(), lat)
+
+
 def test_entropy_packet_apply_matches_oracle():
     import paper_2412_04469_b200 as Q
     from harness import synth

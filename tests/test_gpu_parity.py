@@ -410,7 +410,7 @@ def test_full_size_stress_sampled():
 
 
 # ------------------------------------------------------------------ blend work (culling is exact)
-def test_blend_warp_mask_is_exact(monkeypatch):
+def test_blend_warp_mask_is_exact():
     """The blend's per-warp record mask (touches(): conservative ellipse-vs-sub-tile test) only
     skips records no pixel of the warp hits: the image is bit-identical to the unmasked kernel
     (per-thread box cull only), on a scene with thin, rotated and large Gaussians."""
@@ -423,9 +423,11 @@ def test_blend_warp_mask_is_exact(monkeypatch):
     cams = [synth.make_camera(np.eye(3), np.zeros(3), 300.0, 300.0, 333, 250)]
     st = Stages(pl, n, 1, cams).project().bin_sort().rasterize()
     rgb_a, T_a = st.image_np()
-    monkeypatch.setenv("QUEEN_BLEND_NOMASK", "1")
+    import paper_2412_04469_b200 as Q
+    st.ctx.set_options(Q.QUEEN_OPT_BLEND_NOMASK | Q.QUEEN_OPT_BLEND_GRID_ORDER)
     st.rasterize()
     rgb_b, T_b = st.image_np()
+    st.ctx.set_options(0)
     assert np.array_equal(rgb_a.view(np.uint32), rgb_b.view(np.uint32))
     assert np.array_equal(T_a.view(np.uint32), T_b.view(np.uint32))
     proj, bins, rgb, T = oracle.render(pl, n, 1, cams)
@@ -583,6 +585,23 @@ def test_pipelined_steps_equal_serial_frames():
             torch.cuda.current_stream().wait_event(ev)
             assert torch.equal(img.clone(), refs[t]), ("two-lane, own buffers", vpb, t)
         tl2.sync_lanes()
+        # out=None read on a consumer stream without host syncs: `consumed` fences the reuse of
+        # each lane's buffer two frames later
+        tl3 = Player(sc.planes, sc.n, sc.deg, cams, keys_cap=serial.keys_cap, views_per_batch=vpb)
+        tl3.apply(eps[0])
+        reader = torch.cuda.Stream()
+        copies = []
+        for t in range(len(eps)):
+            ev, done = torch.cuda.Event(), torch.cuda.Event()
+            img = tl3.step2(eps[t + 1] if t + 1 < len(eps) else None, rendered=ev, consumed=done)
+            reader.wait_event(ev)
+            with torch.cuda.stream(reader):
+                copies.append(img.clone())
+                done.record(reader)
+        tl3.sync_lanes()
+        torch.cuda.synchronize()
+        for t in range(len(eps)):
+            assert torch.equal(copies[t], refs[t]), ("two-lane, consumer stream", vpb, t)
         # a plain render after two-lane steps (the lane-0 blend ran on its own stream)
         again = tl.render().clone()
         torch.cuda.synchronize()
