@@ -653,13 +653,15 @@ void oracle_contrib(int n_pad, int V, int W, int H, const float* rec, const uint
 // ---------------------------------------------------------------------------
 // NEXT #1: entropy coding of the integer latents ("flattens our integer
 // latent matrix for each attribute ... then encoded using standard entropy coding
-// approaches such as arithmetic coding").  Plain reference codec for the "QANS" stream of
-// order-0 static model, probabilities normalised to 4096,
-// rANS with a 32-bit state in [2^16, 2^32) and 16-bit renormalisation, the flattened
-// matrix (row-major, k*n + i) cut into 8192-symbol chunks, each chunk 32-way interleaved
-// (symbol p of a chunk belongs to lane p % 32).  Decoding order inside a chunk: for
-// t = 0.. , for lane = 0..31: decode symbol 32 t + lane, then (if the state fell below
-// 2^16) read the next 16-bit word.  Written from that text, independently of csrc/.
+// approaches such as arithmetic coding").  Plain reference codec for the "QAN2" stream of
+// order-0 static model, probabilities normalised to 4096, rANS with a
+// 32-bit state in [2^16, 2^32) and 16-bit renormalisation, the flattened matrix
+// (row-major, k*n + i) cut into 8192-symbol chunks, each chunk split over 32 lanes
+// (symbol p of a chunk belongs to lane p % 32), every lane an independent rANS coder with
+// its own word sequence.  Decoding a lane: for t = 0.. : decode symbol 32 t + lane, then
+// (if the state fell below 2^16) read the lane's next 16-bit word.  A chunk's words are
+// lane 0's sequence, then lane 1's, ... (lane_count[c][l] words each).  Written from that
+// text, independently of csrc/.
 // ---------------------------------------------------------------------------
 static void oracle_ans_freq(const uint64_t cnt[256], uint64_t total, uint16_t f[256]) {
     // deterministic normalisation: floor(count * 4096 / total), at least 1 for present
@@ -699,34 +701,38 @@ int64_t oracle_ans_encode(const int8_t* lat, int L, int n, int n_pad, uint8_t* o
     uint32_t run = 0;
     for (int s = 0; s < 256; ++s) { cum[s] = run; run += f[s]; }
     std::vector<uint32_t> off(nch + 1, 0), st(nch * 32, 1u << 16);
+    std::vector<uint16_t> lcount(nch * 32, 0);
     std::vector<uint16_t> words;
     for (int64_t c = 0; c < nch; ++c) {
         const int64_t len = std::min(CH, nsym - c * CH);
-        std::vector<uint16_t> emitted;  // in encoding order (reverse of decoding)
-        uint32_t x[32];
-        for (int l = 0; l < 32; ++l) x[l] = 1u << 16;
-        for (int64_t p = ((len + 31) / 32) * 32 - 1; p >= 0; --p) {  // (t, lane) descending
-            if (p >= len) continue;
-            const int l = (int)(p % 32);
-            const int64_t q = c * CH + p;
-            const uint32_t s = (uint8_t)(lat[(q / n) * (int64_t)n_pad + q % n] + 128);
-            if ((uint64_t)x[l] >= ((uint64_t)f[s] << 20)) { emitted.push_back((uint16_t)(x[l] & 0xffff)); x[l] >>= 16; }
-            x[l] = (x[l] / f[s]) * 4096u + x[l] % f[s] + cum[s];
-        }
         off[c] = (uint32_t)words.size();
-        for (int64_t q = (int64_t)emitted.size() - 1; q >= 0; --q) words.push_back(emitted[q]);
-        for (int l = 0; l < 32; ++l) st[c * 32 + l] = x[l];
+        for (int l = 0; l < 32; ++l) {
+            uint32_t x = 1u << 16;
+            std::vector<uint16_t> emitted;  // in encoding order (reverse of decoding)
+            for (int64_t p = ((len + 31) / 32) * 32 - 32 + l; p >= 0; p -= 32) {  // t descending
+                if (p >= len) continue;
+                const int64_t q = c * CH + p;
+                const uint32_t s = (uint8_t)(lat[(q / n) * (int64_t)n_pad + q % n] + 128);
+                if ((uint64_t)x >= ((uint64_t)f[s] << 20)) { emitted.push_back((uint16_t)(x & 0xffff)); x >>= 16; }
+                x = (x / f[s]) * 4096u + x % f[s] + cum[s];
+            }
+            st[c * 32 + l] = x;
+            lcount[c * 32 + l] = (uint16_t)emitted.size();
+            for (int64_t q = (int64_t)emitted.size() - 1; q >= 0; --q) words.push_back(emitted[q]);
+        }
     }
     off[nch] = (uint32_t)words.size();
-    const int64_t bytes = 528 + 4 * (nch + 1) + 4 * 32 * nch + ((2 * (int64_t)words.size() + 3) / 4) * 4;
+    const int64_t fixed = 528 + 4 * (nch + 1) + 4 * 32 * nch + 2 * 32 * nch;
+    const int64_t bytes = fixed + ((2 * (int64_t)words.size() + 3) / 4) * 4;
     if (!out || cap < bytes) return bytes;
     std::memset(out, 0, bytes);
-    const uint32_t hdr[4] = {0x534e4151u, (uint32_t)nsym, (uint32_t)nch, 0u};
+    const uint32_t hdr[4] = {0x324e4151u, (uint32_t)nsym, (uint32_t)nch, 0u};
     std::memcpy(out, hdr, 16);
     std::memcpy(out + 16, f, 512);
     std::memcpy(out + 528, off.data(), 4 * (nch + 1));
     std::memcpy(out + 528 + 4 * (nch + 1), st.data(), 4 * 32 * nch);
-    if (!words.empty()) std::memcpy(out + 528 + 4 * (nch + 1) + 4 * 32 * nch, words.data(), 2 * words.size());
+    std::memcpy(out + 528 + 4 * (nch + 1) + 4 * 32 * nch, lcount.data(), 2 * 32 * nch);
+    if (!words.empty()) std::memcpy(out + fixed, words.data(), 2 * words.size());
     return bytes;
 }
 
@@ -735,7 +741,7 @@ int oracle_ans_decode(const uint8_t* in, int64_t bytes, int L, int n, int n_pad,
     if (bytes < 528) return -3;
     uint32_t hdr[4];
     std::memcpy(hdr, in, 16);
-    if (hdr[0] != 0x534e4151u || (int64_t)hdr[1] != (int64_t)L * n) return -3;
+    if (hdr[0] != 0x324e4151u || (int64_t)hdr[1] != (int64_t)L * n) return -3;
     const int64_t CH = 8192, nsym = hdr[1], nch = hdr[2];
     if (nch != (nsym + CH - 1) / CH) return -3;
     uint16_t f[256];
@@ -748,38 +754,40 @@ int oracle_ans_decode(const uint8_t* in, int64_t bytes, int L, int n, int n_pad,
         run += f[s];
     }
     if (run != 4096) return -3;
+    const int64_t fixed = 528 + 4 * (nch + 1) + 4 * 32 * nch + 2 * 32 * nch;
+    if (bytes < fixed) return -3;
     std::vector<uint32_t> off(nch + 1), st(nch * 32);
-    if (bytes < 528 + 4 * (nch + 1) + 4 * 32 * nch) return -3;
+    std::vector<uint16_t> lcount(nch * 32);
     std::memcpy(off.data(), in + 528, 4 * (nch + 1));
     std::memcpy(st.data(), in + 528 + 4 * (nch + 1), 4 * 32 * nch);
-    const uint8_t* wbase = in + 528 + 4 * (nch + 1) + 4 * 32 * nch;
-    const int64_t nwords = (bytes - (528 + 4 * (nch + 1) + 4 * 32 * nch)) / 2;
+    std::memcpy(lcount.data(), in + 528 + 4 * (nch + 1) + 4 * 32 * nch, 2 * 32 * nch);
+    const uint8_t* wbase = in + fixed;
+    const int64_t nwords = (bytes - fixed) / 2;
     int err = 0;
     for (int64_t c = 0; c < nch; ++c) {
         const int64_t len = std::min(CH, nsym - c * CH);
-        uint32_t x[32];
-        for (int l = 0; l < 32; ++l) x[l] = st[c * 32 + l];
         int64_t ptr = off[c];
-        for (int64_t t = 0; t * 32 < len; ++t)
-            for (int l = 0; l < 32; ++l) {
-                const int64_t p = t * 32 + l;
-                if (p >= len) continue;
-                const uint32_t slot = x[l] & 4095u;
+        for (int l = 0; l < 32; ++l) {
+            uint32_t x = st[c * 32 + l];
+            const int64_t end = ptr + lcount[c * 32 + l];
+            for (int64_t p = l; p < len; p += 32) {
+                const uint32_t slot = x & 4095u;
                 const uint32_t s = sym[slot];
-                x[l] = f[s] * (x[l] >> 12) + slot - cum[s];
+                x = f[s] * (x >> 12) + slot - cum[s];
                 const int64_t q = c * CH + p;
                 lat[(q / n) * (int64_t)n_pad + q % n] = (int8_t)((int)s - 128);
-                if (x[l] < (1u << 16)) {
+                if (x < (1u << 16)) {
                     uint16_t w = 0;
-                    if (ptr < off[c + 1] && ptr < nwords) std::memcpy(&w, wbase + 2 * ptr, 2);
+                    if (ptr < end && ptr < nwords) std::memcpy(&w, wbase + 2 * ptr, 2);
                     else err = -3;
                     ++ptr;
-                    x[l] = (x[l] << 16) | w;
+                    x = (x << 16) | w;
                 }
             }
+            if (ptr != end || x != (1u << 16)) err = -3;
+            ptr = end;
+        }
         if (ptr != (int64_t)off[c + 1]) err = -3;
-        for (int l = 0; l < 32; ++l)
-            if (x[l] != (1u << 16)) err = -3;
     }
     return err;
 }

@@ -5,15 +5,18 @@
 // static-model range/ANS coder) cut into independently decodable chunks and 32-way
 // interleaved inside each chunk, so one warp decodes a chunk with one rANS state per lane.
 //
-// Stream format ("QANS"), all little-endian:
-//   u32 magic 'QANS' | u32 n_sym | u32 n_chunks | u32 reserved
+// Stream format ("QAN2"), all little-endian:
+//   u32 magic 'QAN2' | u32 n_sym | u32 n_chunks | u32 reserved
 //   u16 freq[256]                    normalised to sum 4096 (PROB_BITS = 12); symbol = latent + 128
 //   u32 word_off[n_chunks + 1]       chunk word offsets into words[]
 //   u32 state[n_chunks][32]          initial decoder state of each lane
-//   u16 words[]                      renormalisation words in decoding order (padded to 4 bytes)
+//   u16 lane_count[n_chunks][32]     renormalisation words of each lane
+//   u16 words[]                      per chunk: lane 0's words in decoding order, lane 1's, ...
+//                                    (padded to 4 bytes)
 // Symbols are the category's latent matrix flattened row-major (k * n + i, k < L, i < n);
 // chunk j holds symbols [j*CH, (j+1)*CH), CH = 8192; lane l of chunk j decodes symbols
-// j*CH + 32 t + l for t = 0, 1, ...  rANS: 32-bit state in [2^16, 2^32), 16-bit renormalisation.
+// j*CH + 32 t + l for t = 0, 1, ... with its own rANS state (32-bit, in [2^16, 2^32)) and its
+// own word sequence (16-bit renormalisation), so a lane never waits for the others.
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -22,7 +25,7 @@
 
 namespace queen {
 
-constexpr uint32_t ANS_MAGIC = 0x534e4151u;  // 'QANS'
+constexpr uint32_t ANS_MAGIC = 0x324e4151u;  // 'QAN2'
 constexpr int ANS_PROB_BITS = 12;
 constexpr uint32_t ANS_M = 1u << ANS_PROB_BITS;
 constexpr uint32_t ANS_L = 1u << 16;
@@ -65,19 +68,17 @@ static void normalise(const uint64_t cnt[256], uint64_t total, uint16_t f[256]) 
 // ---------------------------------------------------------------- device decoder
 // One launch per frame (every category).  A block builds its category's slot table in shared
 // memory straight from the stream's 256 frequencies: slot -> (f - 1) | (slot - c) << 12 |
-// latent byte << 24, one 32-bit word, so a decode step is ONE shared load + a multiply-add on
-// the state's critical path.  Each warp then decodes chunks with one rANS state per lane; the
-// chunk's renormalisation words pass through a 128-word shared-memory window per warp (refilled
-// 64 words at a time from a register prefetch issued one refill ahead), so a renormalisation is
-// a ballot + one shared load.
+// latent byte << 24, one 32-bit word.  Each warp then decodes one chunk, one rANS state per
+// lane.  A lane's renormalisation words are its own sequence, prefetched 4 deep into
+// registers, so its critical path per symbol is ONE shared load + a multiply-add + a select
+// (no warp vote or shuffle).
 //
 // Bounds (every stream is wire input): the host passes each category's expected symbol and
 // chunk counts (L * n, from the packet shape) and the stream's byte size.  A block whose
 // header does not match (magic, n_sym, n_chunks, frequency sum) raises QUEEN_ERR_INDEX and
-// writes nothing; a chunk whose word range lies outside the stream raises it and writes
-// nothing; every decoded symbol index stays below the host n_sym.
+// writes nothing; a chunk whose word range lies outside the stream, or whose lane counts do
+// not add up to it, raises it and writes nothing; every read stays inside the lane's range.
 constexpr int ANS_WARPS = 8;
-constexpr int ANS_WIN = 128;  // words in a warp's shared-memory window
 
 struct AnsFrame {
     const unsigned char* stream[5];
@@ -94,7 +95,6 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
                                                                DevFlags* fl) {
     __shared__ uint32_t s_tab[ANS_M];
     __shared__ uint32_t s_c[257];
-    __shared__ uint32_t s_win[ANS_WARPS][ANS_WIN];
     int cat = 0;
     while (cat < 4 && (int)blockIdx.x >= fr.block0[cat + 1]) ++cat;
     const unsigned char* stream = fr.stream[cat];
@@ -145,53 +145,42 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
     if (chunk >= n_chunks) return;
     const uint32_t* woff = reinterpret_cast<const uint32_t*>(stream + sizeof(AnsHeader));
     const uint32_t* states = woff + n_chunks + 1;
-    const uint16_t* words = reinterpret_cast<const uint16_t*>(states + (size_t)n_chunks * ANS_LANES);
-    uint32_t ptr = woff[chunk];
-    const uint32_t end = woff[chunk + 1];
-    if (ptr > end || end > fr.n_words[cat]) {  // warp-uniform
+    const uint16_t* lcount = reinterpret_cast<const uint16_t*>(states + (size_t)n_chunks * ANS_LANES);
+    const uint16_t* words = lcount + (size_t)n_chunks * ANS_LANES;
+    const uint32_t c0 = woff[chunk], c1 = woff[chunk + 1];
+    const uint32_t cnt = lcount[(size_t)chunk * ANS_LANES + lane];
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (c0 > c1 || c1 > fr.n_words[cat] || c1 - c0 != tot) {  // warp-uniform
         if (lane == 0) raise_flag(fl, FLAG_INDEX);
         return;
     }
+    uint32_t ptr = c0 + incl - cnt;  // this lane's words: [ptr, end)
+    const uint32_t end = ptr + cnt;
+    auto ld = [&](uint32_t w) -> uint32_t { return w < end ? (uint32_t)__ldg(words + w) : 0u; };
+    uint32_t q0 = ld(ptr), q1 = ld(ptr + 1), q2 = ld(ptr + 2), q3 = ld(ptr + 3);
     int8_t* cout = out + (size_t)fr.row0[cat] * n_pad;
     uint32_t x = states[(size_t)chunk * ANS_LANES + lane];
     const uint32_t base = chunk * ANS_CHUNK;
     const uint32_t len = min((uint32_t)ANS_CHUNK, n_sym - base);
-    const uint32_t lt = (1u << lane) - 1u;
     const uint32_t k = (base + lane) / (uint32_t)n;
     uint32_t i = (base + lane) - k * (uint32_t)n;
     int8_t* op = cout + (size_t)k * n_pad + i;  // this lane's next output byte (row k, column i)
-    uint32_t* win = s_win[wid];
-    auto ld = [&](uint32_t w) -> uint32_t { return w < end ? (uint32_t)__ldg(words + w) : 0u; };
-    uint32_t wbase = ptr;  // window = words [wbase, wbase + 128) at win[(w - wbase0) & 127]
-#pragma unroll
-    for (int q = 0; q < 4; ++q) win[q * 32 + lane] = ld(wbase + q * 32 + lane);
-    uint32_t pre0 = ld(wbase + 128 + lane), pre1 = ld(wbase + 160 + lane);  // next refill
-    uint32_t wpos = 0;  // window slot of word wbase
-    __syncwarp();
-    const uint32_t steps = (len + 31) / 32;
-    for (uint32_t t = 0; t < steps; ++t) {
-        const bool active = t * 32 + lane < len;
+    const uint32_t mine = len > (uint32_t)lane ? (len - lane + 31) / 32 : 0u;  // this lane's symbols
+    for (uint32_t t = 0; t < mine; ++t) {
         const uint32_t e = s_tab[x & (ANS_M - 1)];
-        if (active) {
-            x = ((e & 0xfffu) + 1u) * (x >> ANS_PROB_BITS) + ((e >> 12) & 0xfffu);
-            *op = (int8_t)(e >> 24);
-        }
-        const bool need = active && x < ANS_L;
-        const uint32_t m = __ballot_sync(0xffffffffu, need);
-        if (m) {
-            const uint32_t q = ptr - wbase + __popc(m & lt);  // < 96: inside the window
-            if (need) x = (x << 16) | win[(wpos + q) & (ANS_WIN - 1)];
-            ptr += __popc(m);
-            if (ptr - wbase >= 64) {  // the oldest 64 words are consumed: refill them
-                __syncwarp();
-                win[(wpos + lane) & (ANS_WIN - 1)] = pre0;
-                win[(wpos + 32 + lane) & (ANS_WIN - 1)] = pre1;
-                wpos = (wpos + 64) & (ANS_WIN - 1);
-                wbase += 64;
-                pre0 = ld(wbase + 128 + lane);
-                pre1 = ld(wbase + 160 + lane);
-                __syncwarp();
-            }
+        x = ((e & 0xfffu) + 1u) * (x >> ANS_PROB_BITS) + ((e >> 12) & 0xfffu);
+        *op = (int8_t)(e >> 24);
+        if (x < ANS_L) {
+            x = (x << 16) | q0;
+            q0 = q1; q1 = q2; q2 = q3;
+            ++ptr;
+            q3 = ld(ptr + 3);
         }
         i += 32;  // next symbol of this lane: flat index + 32
         op += 32;
@@ -207,7 +196,7 @@ static bool ans_expect(int L, int n, int64_t bytes, uint32_t& n_sym, uint32_t& n
     if (ns > 0xffffffffull) return false;
     n_sym = (uint32_t)ns;
     n_chunks = (uint32_t)((ns + ANS_CHUNK - 1) / ANS_CHUNK);
-    const int64_t fixed = (int64_t)sizeof(AnsHeader) + 4 * ((int64_t)n_chunks + 1) + 4 * (int64_t)ANS_LANES * n_chunks;
+    const int64_t fixed = (int64_t)sizeof(AnsHeader) + 4 * ((int64_t)n_chunks + 1) + 6 * (int64_t)ANS_LANES * n_chunks;
     if (bytes < fixed) return false;
     const int64_t nw = (bytes - fixed) / 2;
     n_words = (uint32_t)std::min<int64_t>(nw, 0xffffffffll);
@@ -246,9 +235,9 @@ cudaError_t launch_ans_decode(const void* stream_dev, int64_t bytes, int L, int 
 }
 
 // ---------------------------------------------------------------- host encoder
-// Produces exactly the stream the decoder consumes: per chunk, the symbols are encoded in
-// the reverse of decoding order (t descending, lane descending); the words emitted by the
-// pre-encode renormalisations are reversed at the end so the decoder reads them forward.
+// Produces exactly the stream the decoder consumes: per chunk and lane, the lane's symbols
+// are encoded in the reverse of decoding order (t descending); the words its pre-encode
+// renormalisations emit are reversed at the end so the decoder reads them forward.
 size_t ans_encode(const int8_t* lat, int L, int n, int n_pad, std::vector<unsigned char>& out) {
     const uint64_t n_sym = (uint64_t)L * (uint64_t)n;
     const uint32_t n_chunks = (uint32_t)((n_sym + ANS_CHUNK - 1) / ANS_CHUNK);
@@ -264,36 +253,37 @@ size_t ans_encode(const int8_t* lat, int L, int n, int n_pad, std::vector<unsign
     cum[0] = 0;
     for (int s = 0; s < 256; ++s) cum[s + 1] = cum[s] + h.freq[s];
     std::vector<uint32_t> woff(n_chunks + 1, 0), states((size_t)n_chunks * ANS_LANES, ANS_L);
+    std::vector<uint16_t> lcount((size_t)n_chunks * ANS_LANES, 0);
     std::vector<uint16_t> words;
     std::vector<uint16_t> rev;
     for (uint32_t c = 0; c < n_chunks; ++c) {
         const uint64_t base = (uint64_t)c * ANS_CHUNK;
         const uint32_t len = (uint32_t)std::min<uint64_t>(ANS_CHUNK, n_sym - base);
-        const uint32_t steps = (len + 31) / 32;
-        uint32_t x[ANS_LANES];
-        for (int l = 0; l < ANS_LANES; ++l) x[l] = ANS_L;
-        rev.clear();
-        for (int64_t t = (int64_t)steps - 1; t >= 0; --t)
-            for (int l = ANS_LANES - 1; l >= 0; --l) {
-                const uint64_t p = (uint64_t)t * 32 + l;
-                if (p >= len) continue;
-                const uint64_t flat = base + p;
+        woff[c] = (uint32_t)words.size();
+        for (int l = 0; l < ANS_LANES; ++l) {
+            uint32_t x = ANS_L;
+            rev.clear();
+            const uint32_t mine = len > (uint32_t)l ? (len - l + 31) / 32 : 0u;
+            for (int64_t t = (int64_t)mine - 1; t >= 0; --t) {
+                const uint64_t flat = base + (uint64_t)t * 32 + l;
                 const int k = (int)(flat / (uint64_t)n), i = (int)(flat % (uint64_t)n);
                 const uint32_t s = (uint8_t)((int)lat[(size_t)k * n_pad + i] + 128);
                 const uint32_t f = h.freq[s];
                 const uint64_t xmax = (uint64_t)((ANS_L >> ANS_PROB_BITS) << 16) * f;  // f = 4096 -> 2^32
-                if ((uint64_t)x[l] >= xmax) {
-                    rev.push_back((uint16_t)(x[l] & 0xffffu));
-                    x[l] >>= 16;
+                if ((uint64_t)x >= xmax) {
+                    rev.push_back((uint16_t)(x & 0xffffu));
+                    x >>= 16;
                 }
-                x[l] = ((x[l] / f) << ANS_PROB_BITS) + (x[l] % f) + cum[s];
+                x = ((x / f) << ANS_PROB_BITS) + (x % f) + cum[s];
             }
-        woff[c] = (uint32_t)words.size();
-        for (size_t q = rev.size(); q-- > 0;) words.push_back(rev[q]);
-        for (int l = 0; l < ANS_LANES; ++l) states[(size_t)c * ANS_LANES + l] = x[l];
+            states[(size_t)c * ANS_LANES + l] = x;
+            lcount[(size_t)c * ANS_LANES + l] = (uint16_t)rev.size();
+            for (size_t q = rev.size(); q-- > 0;) words.push_back(rev[q]);
+        }
     }
     woff[n_chunks] = (uint32_t)words.size();
-    const size_t bytes = sizeof(AnsHeader) + 4 * woff.size() + 4 * states.size() + ((2 * words.size() + 3) & ~size_t(3));
+    const size_t bytes = sizeof(AnsHeader) + 4 * woff.size() + 4 * states.size() + 2 * lcount.size() +
+                         ((2 * words.size() + 3) & ~size_t(3));
     out.assign(bytes, 0);
     unsigned char* o = out.data();
     std::memcpy(o, &h, sizeof(h));
@@ -302,6 +292,8 @@ size_t ans_encode(const int8_t* lat, int L, int n, int n_pad, std::vector<unsign
     o += 4 * woff.size();
     std::memcpy(o, states.data(), 4 * states.size());
     o += 4 * states.size();
+    std::memcpy(o, lcount.data(), 2 * lcount.size());
+    o += 2 * lcount.size();
     if (!words.empty()) std::memcpy(o, words.data(), 2 * words.size());
     return bytes;
 }

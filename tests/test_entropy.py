@@ -42,7 +42,7 @@ def test_oracle_roundtrip_and_entropy_bound(L, n, n_pad, beta):
     H = float(-(p * np.log2(p)).sum()) if cnt.sum() else 0.0
     nsym = L * n
     nch = (nsym + 8191) // 8192
-    overhead_bits = 8 * (528 + 4 * (nch + 1) + 4 * 32 * nch + 4) + 0.01 * nsym + 16 * 32 * nch
+    overhead_bits = 8 * (528 + 4 * (nch + 1) + 4 * 32 * nch + 2 * 32 * nch + 4) + 0.01 * nsym + 16 * 32 * nch
     assert 8 * s.size <= nsym * H * 1.01 + overhead_bits
 
 
@@ -79,8 +79,13 @@ def test_corrupt_and_mismatched_streams_rejected():
     s = oracle.ans_encode(lat, 5000)
     assert oracle.ans_decode(s, 6, 4999, 5000)[1] == -3        # wrong shape
     assert oracle.ans_decode(s[:600], 6, 5000, 5000)[1] == -3  # truncated
+    nch = (6 * 5000 + 8191) // 8192
     bad = s.copy()
-    bad[528 + 8 + 5] ^= 0x55                                   # a lane's initial state
+    bad[528 + 4 * (nch + 1) + 4 * 7 + 1] ^= 0x55               # lane 7's initial state (chunk 0)
+    assert oracle.ans_decode(bad, 6, 5000, 5000)[1] == -3
+    bad = s.copy()
+    lc = 528 + 4 * (nch + 1) + 4 * 32 * nch                    # lane word counts
+    bad[lc + 2 * 3] ^= 0x01                                    # lane 3's word count (chunk 0)
     assert oracle.ans_decode(bad, 6, 5000, 5000)[1] == -3
     bad = s.copy()
     bad[0] ^= 1                                                # magic

@@ -44,7 +44,8 @@ def test_gpu_ans_corrupt_stream_flags():
     lat = _laplace(6, 20000, 20000, 0.5, seed=2)
     s = Q.queen_entropy_encode(lat, 20000)
     bad = s.copy()
-    bad[528 + 8 + 13] ^= 0x5A  # a lane's initial state
+    nch = (6 * 20000 + 8191) // 8192
+    bad[528 + 4 * (nch + 1) + 4 * 13 + 1] ^= 0x5A  # lane 13's initial state (chunk 0)
     ctx = _ctx()
     out = torch.zeros((6, 20000), dtype=torch.int8, device="cuda")
     Q.queen_entropy_decode(ctx, torch.from_numpy(bad).cuda(), 6, 20000, out)
