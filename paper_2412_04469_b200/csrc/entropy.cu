@@ -79,6 +79,8 @@ static void normalise(const uint64_t cnt[256], uint64_t total, uint16_t f[256]) 
 // writes nothing; a chunk whose word range lies outside the stream, or whose lane counts do
 // not add up to it, raises it and writes nothing; every read stays inside the lane's range.
 constexpr int ANS_WARPS = 8;
+constexpr int ANS_STAGE = 4096;  // renormalisation words staged per warp (4 bits per symbol)
+constexpr size_t ANS_SMEM = sizeof(uint16_t) * ANS_WARPS * ANS_STAGE;  // dynamic shared memory
 
 struct AnsFrame {
     const unsigned char* stream[5];
@@ -95,6 +97,7 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
                                                                DevFlags* fl) {
     __shared__ uint32_t s_tab[ANS_M];
     __shared__ uint32_t s_c[257];
+    extern __shared__ uint16_t s_words_dyn[];  // [ANS_WARPS][ANS_STAGE]
     int cat = 0;
     while (cat < 4 && (int)blockIdx.x >= fr.block0[cat + 1]) ++cat;
     const unsigned char* stream = fr.stream[cat];
@@ -160,10 +163,6 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
         if (lane == 0) raise_flag(fl, FLAG_INDEX);
         return;
     }
-    uint32_t ptr = c0 + incl - cnt;  // this lane's words: [ptr, end)
-    const uint32_t end = ptr + cnt;
-    auto ld = [&](uint32_t w) -> uint32_t { return w < end ? (uint32_t)__ldg(words + w) : 0u; };
-    uint32_t q0 = ld(ptr), q1 = ld(ptr + 1), q2 = ld(ptr + 2), q3 = ld(ptr + 3);
     int8_t* cout = out + (size_t)fr.row0[cat] * n_pad;
     uint32_t x = states[(size_t)chunk * ANS_LANES + lane];
     const uint32_t base = chunk * ANS_CHUNK;
@@ -172,21 +171,51 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
     uint32_t i = (base + lane) - k * (uint32_t)n;
     int8_t* op = cout + (size_t)k * n_pad + i;  // this lane's next output byte (row k, column i)
     const uint32_t mine = len > (uint32_t)lane ? (len - lane + 31) / 32 : 0u;  // this lane's symbols
-    for (uint32_t t = 0; t < mine; ++t) {
-        const uint32_t e = s_tab[x & (ANS_M - 1)];
-        x = ((e & 0xfffu) + 1u) * (x >> ANS_PROB_BITS) + ((e >> 12) & 0xfffu);
-        *op = (int8_t)(e >> 24);
-        if (x < ANS_L) {
-            x = (x << 16) | q0;
-            q0 = q1; q1 = q2; q2 = q3;
-            ++ptr;
-            q3 = ld(ptr + 3);
+    const uint32_t nw = c1 - c0;
+    uint32_t ptr = incl - cnt, end = incl;  // this lane's words, relative to the chunk: [ptr, end)
+    if (nw <= ANS_STAGE) {
+        // common case: the chunk's words staged in shared memory (coalesced), so a
+        // renormalisation is a select on a word loaded beside the table lookup -- no branch
+        uint16_t* sw = s_words_dyn + wid * ANS_STAGE;
+        for (uint32_t q = lane; q < nw; q += 32) sw[q] = __ldg(words + c0 + q);
+        __syncwarp();
+        for (uint32_t t = 0; t < mine; ++t) {
+            const uint32_t w = sw[min(ptr, (uint32_t)ANS_STAGE - 1u)];
+            const uint32_t e = s_tab[x & (ANS_M - 1)];
+            const uint32_t xd = ((e & 0xfffu) + 1u) * (x >> ANS_PROB_BITS) + ((e >> 12) & 0xfffu);
+            const bool need = xd < ANS_L;
+            x = need ? ((xd << 16) | w) : xd;
+            ptr += need ? 1u : 0u;
+            *op = (int8_t)(e >> 24);
+            i += 32;  // next symbol of this lane: flat index + 32
+            op += 32;
+            const bool wrap = i >= (uint32_t)n;
+            i = wrap ? i - (uint32_t)n : i;
+            op = wrap ? op + (n_pad - n) : op;
+            while (i >= (uint32_t)n) { i -= (uint32_t)n; op += n_pad - n; }  // n < 32 only
         }
-        i += 32;  // next symbol of this lane: flat index + 32
-        op += 32;
-        while (i >= (uint32_t)n) { i -= (uint32_t)n; op += n_pad - n; }
+    } else {
+        // more words than the staging area (> 4 bits per symbol): read them from the stream
+        ptr += c0;
+        end += c0;
+        for (uint32_t t = 0; t < mine; ++t) {
+            const uint32_t e = s_tab[x & (ANS_M - 1)];
+            x = ((e & 0xfffu) + 1u) * (x >> ANS_PROB_BITS) + ((e >> 12) & 0xfffu);
+            *op = (int8_t)(e >> 24);
+            if (x < ANS_L) {
+                x = (x << 16) | (ptr < end ? (uint32_t)__ldg(words + ptr) : 0u);
+                ++ptr;
+            }
+            i += 32;
+            op += 32;
+            while (i >= (uint32_t)n) { i -= (uint32_t)n; op += n_pad - n; }
+        }
     }
     if (ptr != end || x != ANS_L) raise_flag(fl, FLAG_INDEX);  // corrupt / mismatched stream
+}
+
+cudaError_t init_entropy_attributes() {
+    return cudaFuncSetAttribute(k_ans_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ANS_SMEM);
 }
 
 // host: expected counts of one category's stream (L * n symbols), and the renormalisation
@@ -222,7 +251,7 @@ cudaError_t launch_ans_decode_frame(const void* const streams[5], const int64_t 
     }
     fr.block0[5] = blk;
     if (blk == 0) return cudaSuccess;
-    k_ans_decode<<<blk, ANS_WARPS * 32, 0, s>>>(fr, out, fl);
+    k_ans_decode<<<blk, ANS_WARPS * 32, ANS_SMEM, s>>>(fr, out, fl);
     return cudaGetLastError();
 }
 

@@ -32,6 +32,7 @@ float host_theta0(float tau, float g0, float g1) {
     return (float)((double)tau * std::log(-(double)g0 / (double)g1));
 }
 cudaError_t init_binning_attributes();
+cudaError_t init_entropy_attributes();
 int key_passes(int64_t gtiles);
 size_t ans_encode(const int8_t* lat, int L, int n, int n_pad, std::vector<unsigned char>& out);
 cudaError_t launch_ans_decode(const void* stream_dev, int64_t bytes, int L, int n, int n_pad, int8_t* out,
@@ -60,7 +61,8 @@ queen_status queen_create(int device, queen_ctx** out) {
     *out = nullptr;
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) return QUEEN_ERR_CUDA;
-    if ((e = init_binning_attributes()) != cudaSuccess) return QUEEN_ERR_CUDA;
+    if ((e = init_binning_attributes()) != cudaSuccess || (e = init_entropy_attributes()) != cudaSuccess)
+        return QUEEN_ERR_CUDA;
     queen_ctx* c = new queen_ctx();
     c->device = device;
     if (cudaEventCreateWithFlags(&c->binned, cudaEventDisableTiming) != cudaSuccess ||

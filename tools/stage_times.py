@@ -18,7 +18,8 @@ frames = int(args[1]) if len(args) > 1 else 10
 cfg = synth.get_config(name)
 sc = synth.make_scene(cfg)
 cams = synth.make_cameras(cfg)
-pl = Player(sc.planes, sc.n, sc.deg, cams)
+vpb = {"stress": 8}.get(name)
+pl = Player(sc.planes, sc.n, sc.deg, cams, views_per_batch=vpb)
 pkt = device_packet(synth.make_packet(sc, 1), pl.dev)
 pl.fit_capacity()
 for _ in range(3):
