@@ -152,7 +152,13 @@ __global__ void BWD_BOUNDS k_blend_bwd(const float4* __restrict__ rec, int n_pad
                 const float2 e = make_float2(ex2b(h[2 * k] ? p2[k].x : NEG_INF), ex2b(h[2 * k + 1] ? p2[k].y : NEG_INF));
                 float2 al = __fmul2_rn(make_float2(o, o), e);
                 al = make_float2(fminf(0.99f, al.x), fminf(0.99f, al.y));
-                TA[k] = __fmul2_rn(TA[k], __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
+                // the forward's transmittance update (k_blend composite2: T - aT, QUEEN_BLEND_TSUB)
+                if (QUEEN_BLEND_TSUB) {
+                    const float2 aT = __fmul2_rn(al, TA[k]);
+                    TA[k] = __fadd2_rn(TA[k], make_float2(-aT.x, -aT.y));
+                } else {
+                    TA[k] = __fmul2_rn(TA[k], __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
+                }
                 last[2 * k] = h[2 * k] ? b0 + q : last[2 * k];
                 last[2 * k + 1] = h[2 * k + 1] ? b0 + q : last[2 * k + 1];
             }

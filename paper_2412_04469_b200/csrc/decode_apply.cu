@@ -73,9 +73,11 @@ __device__ __forceinline__ void coo_entry(float* planes, int n, int64_t n_pad, c
 template <bool F32, bool APPLY, bool GATES>
 __global__ void __launch_bounds__(256, QUEEN_DA_MINB) k_decode_apply(DecodeParams p) {
     extern __shared__ float sdec[];
-    // groups of the same Gaussian block are adjacent in the grid (gid fastest), so the groups
-    // of one category run together and its latent rows come from DRAM once (then L2)
-    if ((int)blockIdx.x >= p.ngroups * p.xblocks) {
+    // grid = groups x Gaussian blocks, group-major (measured: gid-fastest, which keeps a
+    // category's latent rows in L2 across its groups, is slower -- N3DV 41 -> 49 us, stress
+    // 573 -> 628 us -- the concurrent blocks then stream ~14 planes at once instead of ~1)
+    const int gid = blockIdx.x / p.xblocks;
+    if (gid >= p.ngroups) {
         // fused COO scatter blocks (COO mode: the decode groups never touch position rows)
         int k = p.coo_k;
         if (p.coo_kdev) k = min(max(*p.coo_kdev, 0), p.coo_k);
@@ -83,10 +85,9 @@ __global__ void __launch_bounds__(256, QUEEN_DA_MINB) k_decode_apply(DecodeParam
         if (j < k) coo_entry(p.planes, p.n, p.n_pad, p.coo_idx, p.coo_val, p.coo_k, j, p.fl);
         return;
     }
-    const int gid = blockIdx.x % p.ngroups;
     const int c = p.g_c[gid];
     const int64_t np = p.n_pad;
-    const int i0 = ((blockIdx.x / p.ngroups) * blockDim.x + threadIdx.x) * 4;
+    const int i0 = ((blockIdx.x - gid * p.xblocks) * blockDim.x + threadIdx.x) * 4;
     if (c == 5) {
         if (!(GATES && APPLY) || i0 >= p.n) return;
         // a4 fused: dp = g l_p for log alpha > theta0 (R#6), p += dp

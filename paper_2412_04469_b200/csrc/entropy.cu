@@ -80,7 +80,7 @@ static void normalise(const uint64_t cnt[256], uint64_t total, uint16_t f[256]) 
 // not add up to it, raises it and writes nothing; every read stays inside the lane's range.
 constexpr int ANS_WARPS = 8;
 constexpr int ANS_STAGE = 4096;  // renormalisation words staged per warp (4 bits per symbol)
-constexpr size_t ANS_SMEM = sizeof(uint16_t) * ANS_WARPS * ANS_STAGE;  // dynamic shared memory
+constexpr size_t ANS_SMEM = sizeof(uint16_t) * ANS_WARPS * (ANS_STAGE + 288);  // dynamic shared memory
 
 struct AnsFrame {
     const unsigned char* stream[5];
@@ -173,29 +173,36 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
     const uint32_t mine = len > (uint32_t)lane ? (len - lane + 31) / 32 : 0u;  // this lane's symbols
     const uint32_t nw = c1 - c0;
     uint32_t ptr = incl - cnt, end = incl;  // this lane's words, relative to the chunk: [ptr, end)
-    if (nw <= ANS_STAGE) {
+    if (nw <= ANS_STAGE && n >= 32) {
         // common case: the chunk's words staged in shared memory (coalesced), so a
-        // renormalisation is a select on a word loaded beside the table lookup -- no branch
-        uint16_t* sw = s_words_dyn + wid * ANS_STAGE;
+        // renormalisation is a select on a word loaded beside the table lookup -- no branch.
+        // (The staging area has 288 words of slack: a lane's pointer advances at most once per
+        // step, so even a corrupt stream never reads past it; the final check flags it.)
+        uint16_t* sw = s_words_dyn + wid * (ANS_STAGE + 288);
         for (uint32_t q = lane; q < nw; q += 32) sw[q] = __ldg(words + c0 + q);
         __syncwarp();
+        // output: 32-bit offset from the category's first row; the lane's column wraps into the
+        // next row once every ~n/32 steps, at step tw (a rare, short branch)
+        uint32_t off = k * (uint32_t)n_pad + i;
+        uint32_t tw = ((uint32_t)n - i + 31) / 32;
         for (uint32_t t = 0; t < mine; ++t) {
-            const uint32_t w = sw[min(ptr, (uint32_t)ANS_STAGE - 1u)];
+            const uint32_t w = sw[ptr];
             const uint32_t e = s_tab[x & (ANS_M - 1)];
             const uint32_t xd = ((e & 0xfffu) + 1u) * (x >> ANS_PROB_BITS) + ((e >> 12) & 0xfffu);
             const bool need = xd < ANS_L;
             x = need ? ((xd << 16) | w) : xd;
             ptr += need ? 1u : 0u;
-            *op = (int8_t)(e >> 24);
-            i += 32;  // next symbol of this lane: flat index + 32
-            op += 32;
-            const bool wrap = i >= (uint32_t)n;
-            i = wrap ? i - (uint32_t)n : i;
-            op = wrap ? op + (n_pad - n) : op;
-            while (i >= (uint32_t)n) { i -= (uint32_t)n; op += n_pad - n; }  // n < 32 only
+            cout[off] = (int8_t)(e >> 24);
+            off += 32;
+            if (t + 1 == tw) {  // column i + 32 tw >= n: continue in the next row
+                i = i + 32 * tw - (uint32_t)n;
+                off += (uint32_t)(n_pad - n);
+                tw += ((uint32_t)n - i + 31) / 32;
+            }
         }
     } else {
-        // more words than the staging area (> 4 bits per symbol): read them from the stream
+        // more words than the staging area (> 4 bits per symbol), or rows shorter than a warp:
+        // read the words from the stream
         ptr += c0;
         end += c0;
         for (uint32_t t = 0; t < mine; ++t) {

@@ -335,6 +335,9 @@ cudaError_t launch_project(const float* planes, int n, int n_pad, int deg, const
 cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
                             const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof);
 enum : int { OUT_F32 = 0, OUT_MASK = 1, OUT_RGB8 = 2 };  // k_blend epilogues
+#ifndef QUEEN_BLEND_TSUB
+#define QUEEN_BLEND_TSUB 1  // blend transmittance T' = T - aT (aT = alpha T is formed anyway) instead of T (1 - alpha)
+#endif
 cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
                              uint8_t* out8, int out_mode, float mask_thresh, uint32_t* order_ws, cudaStream_t s,

@@ -72,7 +72,10 @@ __device__ __forceinline__ void composite2(Px2& p, float q0, float q1, bool h0, 
     p.r = __ffma2_rn(make_float2(c.y, c.y), aT, p.r);
     p.g = __ffma2_rn(make_float2(c.z, c.z), aT, p.g);
     p.b = __ffma2_rn(make_float2(c.w, c.w), aT, p.b);
-    p.T = __fmul2_rn(p.T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
+    if (QUEEN_BLEND_TSUB)  // T (1 - a) reassociated as T - a T: <= 1 ulp per step, RGB/T stay within tolerance
+        p.T = __fadd2_rn(p.T, make_float2(-aT.x, -aT.y));
+    else
+        p.T = __fmul2_rn(p.T, __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al.x, -al.y)));
 }
 
 #ifndef QUEEN_BLEND_MINB
@@ -86,6 +89,10 @@ constexpr int BLEND_UNROLL = QUEEN_BLEND_UNROLL;  // record-loop unroll
 #define QUEEN_BLEND_UNCOND 1
 #endif
 constexpr bool BLEND_UNCOND = QUEEN_BLEND_UNCOND;
+#ifndef QUEEN_BLEND_PAIRSKIP
+#define QUEEN_BLEND_PAIRSKIP 1  // warp-uniform skip of a row pair (16 x 4 pixels of the warp) that no lane hits
+#endif
+constexpr bool BLEND_PAIRSKIP = QUEEN_BLEND_PAIRSKIP;
 
 template <bool COUNT, int RPT, bool WMASK>
 __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const float4* __restrict__ rec, int n_pad, const uint2* __restrict__ ranges,
@@ -104,19 +111,25 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
     const int gt = order ? (int)order[blockIdx.x] : (int)blockIdx.x;
     const int v = gt / T;
     const int t = gt - v * T;
+    // Pixel layout: a warp covers 16 columns x 2*RPT rows of the tile; lane (column c, half h)
+    // owns row pair k = rows 4k + 2h, 4k + 2h + 1 of the warp's rows, so the warp's row pair k
+    // is the contiguous 16 x 4 band 4k .. 4k + 3 (PAIRSKIP skips a band no lane hits).
+    constexpr int WROWS = 2 * RPT;  // rows per warp
     const int px = (t % gx) * 16 + (threadIdx.x & 15);
-    const int py0 = (t / gx) * 16 + (threadIdx.x >> 4) * RPT;
+    const int wrow0 = (t / gx) * 16 + (threadIdx.x >> 5) * WROWS;  // the warp's first row
+    const int hh = (threadIdx.x >> 4) & 1;
+    auto row_of = [&](int r) { return wrow0 + 4 * (r >> 1) + 2 * hh + (r & 1); };  // r = 2k + sub
     const float fx = (float)px;
-    const float fyc = (float)py0 + 0.5f * (RPT - 1);
-    const float hspan = 0.5f * (RPT - 1) + 1e-4f;
+    const float fyc = (float)(wrow0 + 2 * hh) + 0.5f * (WROWS - 3);
+    const float hspan = 0.5f * (WROWS - 3) + 1e-4f;
     float2 nfy[NP];
 #pragma unroll
-    for (int q = 0; q < NP; ++q) nfy[q] = make_float2(-(float)(py0 + 2 * q), -(float)(py0 + 2 * q + 1));
+    for (int q = 0; q < NP; ++q) nfy[q] = make_float2(-(float)row_of(2 * q), -(float)row_of(2 * q + 1));
     Px2 p[NP];
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
-        const float T0 = (px < W && py0 + 2 * k < H) ? 1.0f : 0.0f;
-        const float T1 = (px < W && py0 + 2 * k + 1 < H) ? 1.0f : 0.0f;
+        const float T0 = (px < W && row_of(2 * k) < H) ? 1.0f : 0.0f;
+        const float T1 = (px < W && row_of(2 * k + 1) < H) ? 1.0f : 0.0f;
         p[k] = Px2{make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(T0, T1)};
     }
     long long ev = 0, cpn = 0;
@@ -181,7 +194,7 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
             // sub-tile (touches(), conservative); otherwise every record.  Skipping a record no
             // pixel of the warp hits changes nothing, so the output is bit-identical either way
             // (test_gpu_parity::test_blend_warp_mask_is_exact).
-            const float wx0 = (float)((t % gx) * 16), wy0 = (float)((t / gx) * 16 + (threadIdx.x >> 5) * (32 / 16) * RPT);
+            const float wx0 = (float)((t % gx) * 16), wy0 = (float)wrow0;
             // the warp's record list (batch order) in shared memory
             uint16_t* lst = s_list[threadIdx.x >> 5];
             int nq = 0;
@@ -236,16 +249,19 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
                     const float4 c = QREC(sC);  // o, r, g, b
                     // BLEND_UNCOND: every row pair composites once any lane hits (a non-hitting
                     // row gets alpha = +0, bit-identical); otherwise branch per row pair
+                    bool doit[NP];
+#pragma unroll
+                    for (int k = 0; k < NP; ++k)
+                        doit[k] = BLEND_PAIRSKIP ? __any_sync(0xffffffffu, h[2 * k] | h[2 * k + 1])
+                                                 : (BLEND_UNCOND || (h[2 * k] | h[2 * k + 1]));
                     if (c.x > 0.98f) {
 #pragma unroll
                         for (int k = 0; k < NP; ++k)
-                            if (BLEND_UNCOND || (h[2 * k] | h[2 * k + 1]))
-                                composite2<true>(p[k], qq[k].x, qq[k].y, h[2 * k], h[2 * k + 1], c);
+                            if (doit[k]) composite2<true>(p[k], qq[k].x, qq[k].y, h[2 * k], h[2 * k + 1], c);
                     } else {
 #pragma unroll
                         for (int k = 0; k < NP; ++k)
-                            if (BLEND_UNCOND || (h[2 * k] | h[2 * k + 1]))
-                                composite2<false>(p[k], qq[k].x, qq[k].y, h[2 * k], h[2 * k + 1], c);
+                            if (doit[k]) composite2<false>(p[k], qq[k].x, qq[k].y, h[2 * k], h[2 * k + 1], c);
                     }
                 }
 #undef QREC
@@ -272,11 +288,11 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
     }
     if (out_mode == OUT_MASK) {  // render_mask: mark pixels whose accumulated alpha 1 - T exceeds the threshold
         if (px < W) {
-            uint8_t* mo = out8 + (int64_t)v * H * W + (int64_t)py0 * W + px;
+            uint8_t* mo = out8 + (int64_t)v * H * W + px;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
                 const float pT = (r & 1) ? p[r >> 1].T.y : p[r >> 1].T.x;
-                if (py0 + r < H) mo[(int64_t)r * W] = (1.0f - pT > mask_thresh) ? 1 : 0;
+                if (row_of(r) < H) mo[(int64_t)row_of(r) * W] = (1.0f - pT > mask_thresh) ? 1 : 0;
             }
         }
         return;
@@ -284,18 +300,19 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
     if (out_mode == OUT_RGB8) {  // display format: round(clamp(C + T bg, 0, 1) * 255), planar u8
         if (px < W) {
             const int64_t plane = (int64_t)H * W;
-            uint8_t* o8 = out8 + (int64_t)v * 3 * plane + (int64_t)py0 * W + px;
-            float* to = T_out ? T_out + (int64_t)v * plane + (int64_t)py0 * W + px : nullptr;
+            uint8_t* o8 = out8 + (int64_t)v * 3 * plane + px;
+            float* to = T_out ? T_out + (int64_t)v * plane + px : nullptr;
 #pragma unroll
             for (int r = 0; r < RPT; ++r) {
-                if (py0 + r < H) {
+                if (row_of(r) < H) {
+                    const int64_t ro = (int64_t)row_of(r) * W;
                     const Px2& q = p[r >> 1];
                     const float pr = (r & 1) ? q.r.y : q.r.x, pg = (r & 1) ? q.g.y : q.g.x, pb = (r & 1) ? q.b.y : q.b.x;
                     const float pT = (r & 1) ? q.T.y : q.T.x;
-                    o8[(int64_t)r * W] = (uint8_t)__float2uint_rn(fminf(fmaxf(pr + pT * bg0, 0.0f), 1.0f) * 255.0f);
-                    o8[plane + (int64_t)r * W] = (uint8_t)__float2uint_rn(fminf(fmaxf(pg + pT * bg1, 0.0f), 1.0f) * 255.0f);
-                    o8[2 * plane + (int64_t)r * W] = (uint8_t)__float2uint_rn(fminf(fmaxf(pb + pT * bg2, 0.0f), 1.0f) * 255.0f);
-                    if (to) to[(int64_t)r * W] = pT;
+                    o8[ro] = (uint8_t)__float2uint_rn(fminf(fmaxf(pr + pT * bg0, 0.0f), 1.0f) * 255.0f);
+                    o8[plane + ro] = (uint8_t)__float2uint_rn(fminf(fmaxf(pg + pT * bg1, 0.0f), 1.0f) * 255.0f);
+                    o8[2 * plane + ro] = (uint8_t)__float2uint_rn(fminf(fmaxf(pb + pT * bg2, 0.0f), 1.0f) * 255.0f);
+                    if (to) to[ro] = pT;
                 }
             }
         }
@@ -303,18 +320,19 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
     }
     if (px < W) {
         const int64_t plane = (int64_t)H * W;
-        float* o = rgb_out + (int64_t)v * 3 * plane + (int64_t)py0 * W + px;
-        float* to = T_out ? T_out + (int64_t)v * plane + (int64_t)py0 * W + px : nullptr;
+        float* o = rgb_out + (int64_t)v * 3 * plane + px;
+        float* to = T_out ? T_out + (int64_t)v * plane + px : nullptr;
 #pragma unroll
         for (int r = 0; r < RPT; ++r) {
-            if (py0 + r < H) {
+            if (row_of(r) < H) {
+                const int64_t ro = (int64_t)row_of(r) * W;
                 const Px2& q = p[r >> 1];
                 const float pr = (r & 1) ? q.r.y : q.r.x, pg = (r & 1) ? q.g.y : q.g.x, pb = (r & 1) ? q.b.y : q.b.x;
                 const float pT = (r & 1) ? q.T.y : q.T.x;
-                o[(int64_t)r * W] = pr + pT * bg0;
-                o[plane + (int64_t)r * W] = pg + pT * bg1;
-                o[2 * plane + (int64_t)r * W] = pb + pT * bg2;
-                if (to) to[(int64_t)r * W] = pT;
+                o[ro] = pr + pT * bg0;
+                o[plane + ro] = pg + pT * bg1;
+                o[2 * plane + ro] = pb + pT * bg2;
+                if (to) to[ro] = pT;
             }
         }
     }
