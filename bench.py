@@ -332,6 +332,7 @@ def main():
 
     import paper_2412_04469_b200 as Q
     from paper_2412_04469_b200 import packet as wire
+    from paper_2412_04469_b200.dist import ShardedStream
     from paper_2412_04469_b200.runtime import EntropyPacket, Player, device_packet, wire_packet
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -393,26 +394,24 @@ def main():
             used_bytes = [b.size for b in host_bufs]
         src_bufs = [torch.from_numpy(b).to(dev) for b in host_bufs]
     nbytes = lay["total"]
-    # every rank decodes from its own copy of the frame packet (the broadcast target)
-    slots = [torch.zeros(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
-    if rank == 0 and world == 1:
-        slots = src_bufs  # N=1: the resident packets are used directly (no collective)
-    mkpkt = (lambda b: EntropyPacket(b, hdr)) if entropy else (lambda b: wire_packet(b, hdr))
-    dps = [mkpkt(s) for s in slots]
-
-    player = Player(sc.planes, sc.n, sc.deg, cams, device=local, views_per_batch=vpb)
+    # dist.ShardedStream (the product's multi-rank path): this rank's views, the Gaussian set
+    # replicated (rank 0's A_0 broadcast once; the other ranks start from zeros), and every rank
+    # decoding from its own copy of the frame packet, broadcast into one of two slots per frame.
+    # N=1: the resident packets are used in place (no collective).
+    ss = ShardedStream(sc.planes if rank == 0 else np.zeros_like(sc.planes), sc.n, sc.deg, cams_all, hdr, nbytes,
+                       entropy=entropy, device=local, views_per_batch=vpb, views=mine,
+                       resident=src_bufs if world == 1 else None)
+    ss.share_scene()
+    player = ss.player
+    dps = ss.packets
+    A0 = player.planes.clone()  # frame-0 set on every rank (after the broadcast)
     stream = torch.cuda.current_stream()
 
+    def src(t):  # packet t on rank 0 ("packet t arrived in HBM"), None elsewhere
+        return src_bufs[t % P] if rank == 0 else None
+
     def step(t):
-        if world > 1:
-            slot = t % 2
-            if rank == 0:
-                slots[slot].copy_(src_bufs[t % P])  # stands for "packet t arrived in HBM on rank 0"
-            dist.broadcast(slots[slot], 0)
-            dp = dps[slot]
-        else:
-            dp = dps[t % P]
-        player.apply(dp)
+        player.apply(ss.receive(t, src(t)))
         player.render()
 
     # size key buffers (host sync once, outside timing), then warm up
@@ -430,9 +429,7 @@ def main():
 
     def bcast(t):  # N > 1: packet t into its slot on every rank (NCCL, outside any graph)
         if world > 1:
-            if rank == 0:
-                slots[t % 2].copy_(src_bufs[t % P])  # stands for "packet t arrived in HBM on rank 0"
-            dist.broadcast(slots[t % 2], 0)
+            ss.receive(t, src(t))
 
     def timed_loop(run_step, sampler=None):
         e0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -474,7 +471,6 @@ def main():
         # N = 1: one graph per resident packet (at most one per timed step, so every graph's
         # profiler events are last recorded inside the timed region); N > 1: one per slot
         ng = len(dps) if world > 1 else max(1, min(len(dps), args.steps))
-        A0 = torch.from_numpy(sc.planes).to(dev)
         if pipeline:
             # pipelined step t (runtime.Player.capture_step): render frame t, and decode + apply
             # packet t+1 under its blend; graph j applies packet slot j.  Frame 0 = A_0 + packet 0
@@ -562,7 +558,7 @@ def main():
         # eager SERIAL launches of the same frames (decode + apply, then render), for comparison;
         # profiled, so each stage's time is also measured with the stage alone on the GPU
         # (pipelined, the side-stream stages share the GPU with the blend)
-        player.planes.copy_(torch.from_numpy(sc.planes).to(dev))
+        player.planes.copy_(A0)
         if not args.no_profile:
             player.profile(True)
             player.profile_read(reset=True)
@@ -810,6 +806,7 @@ def main():
         out_dev = [torch.empty(player.rgb.shape, dtype=odt, device=dev) for _ in range(NB)]
         out_host = [torch.empty(player.rgb.shape, dtype=odt).pin_memory() for _ in range(NB)]
         recv = [torch.zeros(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
+        mkpkt = (lambda b: EntropyPacket(b, hdr)) if entropy else (lambda b: wire_packet(b, hdr))
         dp_recv = [mkpkt(r) for r in recv]
         s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         ev = lambda: torch.cuda.Event(enable_timing=False)  # noqa: E731
@@ -886,7 +883,7 @@ def main():
 
         # restart the sequence from A_0 so the streamed frames are the same ones; W untimed
         # warm-up frames (first launches, lazy module loading), then the K timed frames
-        player.planes.copy_(torch.from_numpy(sc.planes).to(dev))
+        player.planes.copy_(A0)
         stream_frames(0, args.warmup, first=True)
         t0, t1, lat0, lat1 = stream_frames(args.warmup, args.steps, first=False)
         lat_med = statistics.median(a.elapsed_time(b) for a, b in zip(lat0, lat1))

@@ -61,7 +61,10 @@ constexpr int LB_BATCH = QUEEN_LB_BATCH;
 #endif  // onesweep look-back predecessors loaded per round trip
 constexpr int SORT_WARPS = SORT_THREADS / 32;
 
-enum : int { TK_DEPTH = 0, TK_TILE = 4, TK_VIS = 8, TK_DUP = 9 };
+enum : int { TK_DEPTH = 0, TK_TILE = 4, TK_VIS = 8, TK_DUP = 9, TK_EMIT = 10 };
+#ifndef QUEEN_BIN_BUCKETS
+#define QUEEN_BIN_BUCKETS 1  // bucketed emission (k_piece_* + k_emit) instead of duplication + tile radix passes
+#endif
 
 // Block-wide exclusive scan of one u32 per thread (256 threads); returns the exclusive
 // prefix and the block total.
@@ -791,6 +794,368 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
     }
 }
 
+// ---------------------------------------------------------------------------
+// K4'/K5': bucketed emission (replaces duplication + the tile radix passes).
+// A bucket is a BK_W x BK_H block of one view's tiles.  A piece is (pair, bucket) for every
+// bucket a visible pair's tile rect intersects.  With the pairs already in depth order
+// (m = their rank), the final entry list is known position by position:
+//   entry (tile t, pair m) -> ranges[t].first + #{pairs m' < m whose rect covers t}
+// and every such count is local to t's bucket.  So:
+//   k_piece_count   per chunk of PC_CH depth-ordered pairs: pieces per bucket -> pcnt[chunk][b]
+//   k_piece_colscan per bucket: exclusive scan over chunks (in place) -> the bucket's
+//                   (chunk, bucket) segment offsets; totals
+//   k_piece_base    bucket bases (scan of totals) and emit-tile bases (ceil(total / EM_E))
+//   k_piece_scatter per chunk: each piece's m into its (chunk, bucket) segment (order inside a
+//                   segment arbitrary: shared-memory cursors)
+//   k_emit          per emit tile (whole segments of one bucket, ~EM_E pieces): sort the m
+//                   values (unique), count entries per bucket tile, resolve each tile's offset
+//                   among the bucket's earlier emit tiles by decoupled look-back, then write
+//                   every entry's Gaussian index at its final position, ranked stably in m order
+//                   (per-warp match words over the bucket's tiles).
+// The result is bit-identical to the sorted (gt, depth, index) order: a bucket's pieces are
+// emitted in m order, and m order is (depth, view, index) order.
+// ---------------------------------------------------------------------------
+constexpr int PC_THREADS = 512;             // PC_CH / 8 pairs per thread
+constexpr size_t PC_MAX_SMEM = 200 * 1024;  // per-chunk bucket counters: up to 51200 buckets per batch
+constexpr int EM_CAP = 8192;                // sort capacity: EM_E + a whole segment (< PC_CH), power of 2
+static_assert(EM_E + PC_CH <= EM_CAP, "an emit tile holds whole segments");
+constexpr int EM_THREADS = 512;
+constexpr int EM_WARPS = EM_THREADS / 32;
+
+struct BucketGeo {
+    int gx, gy, nbx, nby, NB, VNB;
+    int T, n_pad;
+    int CHS;  // row stride of pcnt ([bucket][chunk]): the chunk capacity
+};
+
+__device__ __forceinline__ const uint32_t* depth_order(const uint32_t* a, const uint32_t* b, const uint32_t* triv,
+                                                       uint32_t M) {
+    // the last depth pass is skipped (identity) when its digit histogram says so: its input holds the order
+    return triv[0] == M ? a : b;
+}
+
+__device__ __forceinline__ uint32_t visible_pairs(const uint32_t* Kd) { return Kd[2] ? 0u : Kd[1]; }
+
+__global__ void __launch_bounds__(PC_THREADS) k_piece_count(const uint32_t* __restrict__ dva,
+                                                            const uint32_t* __restrict__ dvb,
+                                                            const uint32_t* __restrict__ triv,
+                                                            const uint32_t* __restrict__ Kd,
+                                                            const short4* __restrict__ rect, BucketGeo g,
+                                                            uint32_t* __restrict__ pcnt) {
+    extern __shared__ uint32_t sc[];  // [VNB]
+    const uint32_t M = visible_pairs(Kd);
+    const uint32_t c = blockIdx.x;
+    if ((uint64_t)c * PC_CH >= M) return;
+    const uint32_t* __restrict__ dvals = depth_order(dva, dvb, triv, Kd[1]);
+    for (int b = threadIdx.x; b < g.VNB; b += PC_THREADS) sc[b] = 0u;
+    __syncthreads();
+#pragma unroll 2
+    for (int e = 0; e < PC_CH / PC_THREADS; ++e) {
+        const uint32_t m = c * PC_CH + e * PC_THREADS + threadIdx.x;
+        if (m < M) {
+            const uint32_t j = __ldg(dvals + m);
+            const short4 r = __ldg(rect + j);
+            const int vb = (int)(j / (uint32_t)g.n_pad) * g.NB;
+            const int bx0 = r.x / BK_W, bx1 = r.z / BK_W, by0 = r.y / BK_H, by1 = r.w / BK_H;
+            for (int by = by0; by <= by1; ++by)
+                for (int bx = bx0; bx <= bx1; ++bx) atomicAdd(&sc[vb + by * g.nbx + bx], 1u);
+        }
+    }
+    __syncthreads();
+    // pcnt is bucket-major ([bucket][chunk], row stride g.CHS): each bucket's segment offsets are
+    // contiguous for the column scan and the emit tiles' segment search
+    for (int b = threadIdx.x; b < g.VNB; b += PC_THREADS) pcnt[(size_t)b * g.CHS + c] = sc[b];
+}
+
+// per bucket (one warp): exclusive scan of its pieces over the chunks (in place) and the total
+__global__ void __launch_bounds__(256) k_piece_colscan(uint32_t* __restrict__ pcnt, const uint32_t* __restrict__ Kd,
+                                                       BucketGeo g, uint32_t* __restrict__ ptotal) {
+    const int b = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (b >= g.VNB) return;
+    const uint32_t M = visible_pairs(Kd);
+    const uint32_t nch = (M + PC_CH - 1) / PC_CH;
+    uint32_t* row = pcnt + (size_t)b * g.CHS;
+    // exclusive offsets in chunk order, 32 chunks per round (coalesced)
+    uint32_t carry = 0;
+    for (uint32_t c0 = 0; c0 < nch; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        const uint32_t x = c < nch ? row[c] : 0u;
+        uint32_t inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (c < nch) row[c] = carry + inc - x;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) ptotal[b] = carry;
+}
+
+// one block: bucket bases (exclusive scan of the totals) and emit-tile bases; meta[0] = pieces,
+// meta[1] = emit tiles
+__global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict__ ptotal, int VNB,
+                                                     uint32_t* __restrict__ pbase, uint32_t* __restrict__ ebase,
+                                                     uint32_t* __restrict__ meta) {
+    __shared__ uint32_t s_w[32], s_e[32];
+    __shared__ uint32_t s_carry, s_ecarry;
+    if (threadIdx.x == 0) { s_carry = 0; s_ecarry = 0; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int b0 = 0; b0 < VNB; b0 += blockDim.x) {
+        const int b = b0 + threadIdx.x;
+        const uint32_t x = b < VNB ? ptotal[b] : 0u;
+        const uint32_t y = (x + EM_E - 1) / EM_E;
+        uint32_t ix = x, iy = y;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t a = __shfl_up_sync(0xffffffffu, ix, o), c = __shfl_up_sync(0xffffffffu, iy, o);
+            if (lane >= o) { ix += a; iy += c; }
+        }
+        if (lane == 31) { s_w[w] = ix; s_e[w] = iy; }
+        __syncthreads();
+        uint32_t px = 0, py = 0, tx = 0, ty = 0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+            px += q < w ? s_w[q] : 0u;
+            py += q < w ? s_e[q] : 0u;
+            tx += s_w[q];
+            ty += s_e[q];
+        }
+        const uint32_t cx = s_carry, cy = s_ecarry;
+        if (b < VNB) {
+            pbase[b] = cx + px + ix - x;
+            ebase[b] = cy + py + iy - y;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) { s_carry = cx + tx; s_ecarry = cy + ty; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        ebase[VNB] = s_ecarry;
+        meta[0] = s_carry;
+        meta[1] = s_ecarry;
+    }
+}
+
+__global__ void __launch_bounds__(PC_THREADS) k_piece_scatter(const uint32_t* __restrict__ dva,
+                                                              const uint32_t* __restrict__ dvb,
+                                                              const uint32_t* __restrict__ triv,
+                                                              const uint32_t* __restrict__ Kd,
+                                                              const short4* __restrict__ rect, BucketGeo g,
+                                                              const uint32_t* __restrict__ pcnt,
+                                                              const uint32_t* __restrict__ pbase,
+                                                              uint32_t* __restrict__ pieces) {
+    extern __shared__ uint32_t sc[];  // [VNB] cursors
+    const uint32_t M = visible_pairs(Kd);
+    const uint32_t c = blockIdx.x;
+    if ((uint64_t)c * PC_CH >= M) return;
+    const uint32_t* __restrict__ dvals = depth_order(dva, dvb, triv, Kd[1]);
+    for (int b = threadIdx.x; b < g.VNB; b += PC_THREADS) sc[b] = pbase[b] + pcnt[(size_t)b * g.CHS + c];
+    __syncthreads();
+#pragma unroll 2
+    for (int e = 0; e < PC_CH / PC_THREADS; ++e) {
+        const uint32_t m = c * PC_CH + e * PC_THREADS + threadIdx.x;
+        if (m < M) {
+            const uint32_t j = __ldg(dvals + m);
+            const short4 r = __ldg(rect + j);
+            const int vb = (int)(j / (uint32_t)g.n_pad) * g.NB;
+            const int bx0 = r.x / BK_W, bx1 = r.z / BK_W, by0 = r.y / BK_H, by1 = r.w / BK_H;
+            for (int by = by0; by <= by1; ++by)
+                for (int bx = bx0; bx <= bx1; ++bx) pieces[atomicAdd(&sc[vb + by * g.nbx + bx], 1u)] = m;
+        }
+    }
+}
+
+// bucket-local start of emit tile k of bucket b: the first (chunk, bucket) segment that starts
+// at or after k * EM_E (emit tiles hold whole segments), or the bucket total
+__device__ __forceinline__ uint32_t emit_start(const uint32_t* row, uint32_t nch, uint32_t total, uint32_t k) {
+    const uint32_t want = k * (uint32_t)EM_E;
+    if (want == 0) return 0u;
+    if (want >= total) return total;
+    uint32_t lo = 0, hi = nch;  // first c with off[c] >= want (off[nch] := total)
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (row[mid] >= want) hi = mid; else lo = mid + 1;
+    }
+    return lo < nch ? row[lo] : total;
+}
+
+struct EmitSmem {
+    uint32_t key[EM_CAP];                 // m values (sorted), then Gaussian indices
+    uint16_t lr[EM_CAP];                  // piece rect inside the bucket: lx0 | lx1 << 4 | ly0 << 8 | ly1 << 11
+    uint32_t wm[EM_WARPS][BK_T];          // per-warp match words of a round
+    uint32_t wpre[EM_WARPS][BK_T];        // per-warp exclusive prefix of a round
+    int diff[(BK_H + 1) * (BK_W + 1)];    // 2D difference array of the tile's entry counts
+    uint32_t base[BK_T];                  // final position of the tile's next entry
+    uint32_t w_s[EM_WARPS];
+    uint32_t tile, b, k, n, s0;
+};
+
+__global__ void __launch_bounds__(EM_THREADS) k_emit(const uint32_t* __restrict__ pieces,
+                                                     const uint32_t* __restrict__ pcnt,
+                                                     const uint32_t* __restrict__ ptotal,
+                                                     const uint32_t* __restrict__ pbase,
+                                                     const uint32_t* __restrict__ ebase,
+                                                     const uint32_t* __restrict__ meta,
+                                                     const uint32_t* __restrict__ dva, const uint32_t* __restrict__ dvb,
+                                                     const uint32_t* __restrict__ triv, const uint32_t* __restrict__ Kd,
+                                                     const short4* __restrict__ rect, const uint2* __restrict__ ranges,
+                                                     BucketGeo g, uint32_t* __restrict__ vals, uint32_t* lb,
+                                                     uint32_t* ticket, DevFlags* fl) {
+    extern __shared__ __align__(16) unsigned char em_smem[];
+    EmitSmem& S = *reinterpret_cast<EmitSmem*>(em_smem);
+    const uint32_t M = visible_pairs(Kd);
+    if (M == 0) return;
+    const uint32_t NE = meta[1];
+    const uint32_t nch = (M + PC_CH - 1) / PC_CH;
+    const uint32_t* __restrict__ dvals = depth_order(dva, dvb, triv, Kd[1]);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const uint32_t t = atomicAdd(ticket, 1u);
+            S.tile = t;
+            if (t < NE) {
+                int lo = 0, hi = g.VNB;  // bucket: last b with ebase[b] <= t
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (ebase[mid] <= t) lo = mid; else hi = mid;
+                }
+                const uint32_t k = t - ebase[lo];
+                const uint32_t tot = ptotal[lo];
+                const uint32_t* row = pcnt + (size_t)lo * g.CHS;
+                const uint32_t s0 = emit_start(row, nch, tot, k);
+                const uint32_t s1 = emit_start(row, nch, tot, k + 1);
+                S.b = (uint32_t)lo;
+                S.k = k;
+                S.s0 = s0;
+                S.n = s1 - s0;
+            }
+        }
+        for (int q = threadIdx.x; q < (BK_H + 1) * (BK_W + 1); q += EM_THREADS) S.diff[q] = 0;
+        for (int q = threadIdx.x; q < EM_WARPS * BK_T; q += EM_THREADS) (&S.wm[0][0])[q] = 0u;
+        __syncthreads();
+        const uint32_t et = S.tile;
+        if (et >= NE) break;
+        const int b = (int)S.b;
+        const uint32_t n = S.n, k = S.k;
+        if (n > (uint32_t)EM_CAP) {  // cannot happen (EM_E + a segment < EM_CAP); guard the smem
+            if (threadIdx.x == 0) raise_flag(fl, FLAG_CAPACITY);
+        }
+        const uint32_t nn = min(n, (uint32_t)EM_CAP);
+        // load the tile's m values (pad with ~0 to the next power of two) and sort them
+        uint32_t np2 = 1;
+        while (np2 < nn) np2 <<= 1;
+        const uint32_t* src = pieces + pbase[b] + S.s0;
+        for (uint32_t q = threadIdx.x; q < np2; q += EM_THREADS) S.key[q] = q < nn ? __ldg(src + q) : 0xffffffffu;
+        __syncthreads();
+        for (uint32_t kk = 2; kk <= np2; kk <<= 1) {
+            for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
+                for (uint32_t i = threadIdx.x; i < np2; i += EM_THREADS) {
+                    const uint32_t ixj = i ^ jj;
+                    if (ixj > i) {
+                        const uint32_t a = S.key[i], c = S.key[ixj];
+                        const bool up = (i & kk) == 0;
+                        if ((a > c) == up) { S.key[i] = c; S.key[ixj] = a; }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // pieces: Gaussian index (in place of m), rect inside the bucket, entry counts per tile
+        const int v = b / g.NB;
+        const int bl = b - v * g.NB;
+        const int by = bl / g.nbx, bx = bl - by * g.nbx;
+        const int tx0b = bx * BK_W, ty0b = by * BK_H;
+        for (uint32_t q = threadIdx.x; q < nn; q += EM_THREADS) {
+            const uint32_t j = __ldg(dvals + S.key[q]);
+            const short4 r = __ldg(rect + j);
+            const int lx0 = max((int)r.x - tx0b, 0), lx1 = min((int)r.z - tx0b, BK_W - 1);
+            const int ly0 = max((int)r.y - ty0b, 0), ly1 = min((int)r.w - ty0b, BK_H - 1);
+            S.key[q] = j - (uint32_t)v * (uint32_t)g.n_pad;
+            S.lr[q] = (uint16_t)(lx0 | (lx1 << 4) | (ly0 << 8) | (ly1 << 11));
+            atomicAdd(&S.diff[ly0 * (BK_W + 1) + lx0], 1);
+            atomicAdd(&S.diff[ly0 * (BK_W + 1) + lx1 + 1], -1);
+            atomicAdd(&S.diff[(ly1 + 1) * (BK_W + 1) + lx0], -1);
+            atomicAdd(&S.diff[(ly1 + 1) * (BK_W + 1) + lx1 + 1], 1);
+        }
+        __syncthreads();
+        if (threadIdx.x < BK_H) {  // prefix along x
+            int run = 0;
+            for (int x = 0; x < BK_W; ++x) { run += S.diff[threadIdx.x * (BK_W + 1) + x]; S.diff[threadIdx.x * (BK_W + 1) + x] = run; }
+        }
+        __syncthreads();
+        if (threadIdx.x < BK_W) {  // prefix along y
+            int run = 0;
+            for (int y = 0; y < BK_H; ++y) { run += S.diff[y * (BK_W + 1) + threadIdx.x]; S.diff[y * (BK_W + 1) + threadIdx.x] = run; }
+        }
+        __syncthreads();
+        // each tile's offset among the bucket's earlier emit tiles: decoupled look-back
+        if (threadIdx.x < BK_T) {
+            const int lt = threadIdx.x, ly = lt / BK_W, lx = lt - ly * BK_W;
+            const uint32_t cnt = (uint32_t)S.diff[ly * (BK_W + 1) + lx];
+            uint32_t* my = lb + (size_t)et * BK_T + lt;
+            uint32_t prefix = 0;
+            if (k == 0) {
+                st_volatile_u32(my, LB_INC | cnt);
+            } else {
+                st_volatile_u32(my, LB_AGG | cnt);
+                int64_t look = (int64_t)et - 1;
+                long long spins = 0;
+                for (;;) {
+                    const uint32_t x = ld_volatile_u32(lb + (size_t)look * BK_T + lt);
+                    const uint32_t f = x >> 30;
+                    if (f == 0) {
+                        if (++spins > SPIN_LIMIT) { raise_flag(fl, FLAG_TIMEOUT); break; }
+                        continue;
+                    }
+                    prefix += x & LB_MASK;
+                    if (f == 2) break;
+                    --look;
+                }
+                st_volatile_u32(my, LB_INC | (prefix + cnt));
+            }
+            const int ty = ty0b + ly, tx = tx0b + lx;
+            const uint32_t gt = (uint32_t)v * (uint32_t)g.T + (uint32_t)(ty * g.gx + tx);
+            S.base[lt] = (tx < g.gx && ty < g.gy) ? ranges[gt].x + prefix : 0u;
+        }
+        __syncthreads();
+        // rounds of EM_THREADS pieces in m order: stable ranks per tile (warp match words)
+        for (uint32_t q0 = 0; q0 < nn; q0 += EM_THREADS) {
+            const uint32_t q = q0 + threadIdx.x;
+            const bool has = q < nn;
+            const uint32_t lr = has ? S.lr[q] : 0u;
+            const int lx0 = lr & 15, lx1 = (lr >> 4) & 15, ly0 = (lr >> 8) & 7, ly1 = (lr >> 11) & 7;
+            if (has)
+                for (int ly = ly0; ly <= ly1; ++ly)
+                    for (int lx = lx0; lx <= lx1; ++lx) atomicOr(&S.wm[w][ly * BK_W + lx], 1u << lane);
+            __syncthreads();
+            if (threadIdx.x < BK_T) {
+                uint32_t run = S.base[threadIdx.x];
+#pragma unroll
+                for (int ww = 0; ww < EM_WARPS; ++ww) {
+                    S.wpre[ww][threadIdx.x] = run;
+                    run += __popc(S.wm[ww][threadIdx.x]);
+                }
+                S.base[threadIdx.x] = run;
+            }
+            __syncthreads();
+            if (has) {
+                const uint32_t gi = S.key[q];
+                for (int ly = ly0; ly <= ly1; ++ly)
+                    for (int lx = lx0; lx <= lx1; ++lx) {
+                        const int lt = ly * BK_W + lx;
+                        vals[S.wpre[w][lt] + __popc(S.wm[w][lt] & lt_mask)] = gi;
+                    }
+            }
+            __syncthreads();
+            for (int qq = threadIdx.x; qq < EM_WARPS * BK_T; qq += EM_THREADS) (&S.wm[0][0])[qq] = 0u;
+            __syncthreads();
+        }
+    }
+}
+
 // ranges[gt] = view base + local start (view bases = exclusive scan of the <= 64 view
 // totals); [0,0) for empty tiles and everywhere on capacity overflow (already flagged)
 __global__ void __launch_bounds__(256) k_ranges_finalize(const uint32_t* __restrict__ counts,
@@ -842,8 +1207,21 @@ static cudaError_t onesweep_attr() {
                                 (int)Onesweep<BITS>::SMEM);
 }
 
+static int emit_grid() {
+    static int occ = 0;
+    if (!occ) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, EM_THREADS, sizeof(EmitSmem));
+        if (occ <= 0) occ = 1;
+    }
+    return occ * num_sms();
+}
+
 cudaError_t init_binning_attributes() {
     cudaError_t e;
+    if ((e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EmitSmem))) ||
+        (e = cudaFuncSetAttribute(k_piece_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC_MAX_SMEM)) ||
+        (e = cudaFuncSetAttribute(k_piece_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC_MAX_SMEM)))
+        return e;
     if ((e = onesweep_attr<8, OS_KV>()) || (e = onesweep_attr<8, OS_PACK>()) || (e = onesweep_attr<8, OS_PACKED>()) ||
         (e = onesweep_attr<8, OS_V>()) || (e = onesweep_attr<9, OS_KV>()) || (e = onesweep_attr<9, OS_PACK>()) ||
         (e = onesweep_attr<9, OS_PACKED>()) || (e = onesweep_attr<9, OS_V>()))
@@ -907,14 +1285,18 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     prof->begin(ST_COMPACT, s);
     if ((e = cudaMemsetAsync(fl->tickets, 0, sizeof(fl->tickets), s))) return e;
     if ((e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS, s))) return e;
+#if !QUEEN_BIN_BUCKETS
     if ((e = cudaMemsetAsync(dup_lb, 0, sizeof(unsigned long long) * (elem_tiles + 1), s))) return e;
+#endif
     if ((e = cudaMemsetAsync(depth_lb, 0, sizeof(uint32_t) * DEPTH_PASSES * MAX_BINS * (size_t)(os_elem_tiles + 1), s)))
         return e;
     uint32_t* dminmax = reinterpret_cast<uint32_t*>(ws + L.dminmax);
     if ((e = cudaMemsetAsync(dminmax, 0xff, sizeof(uint32_t), s))) return e;       // min <- 0xffffffff
     if ((e = cudaMemsetAsync(dminmax + 1, 0, sizeof(uint32_t), s))) return e;      // max <- 0
+#if !QUEEN_BIN_BUCKETS
     if ((e = cudaMemsetAsync(tile_lb, 0, sizeof(uint32_t) * (size_t)tpasses * (1 << tbits) * (size_t)(os_key_tiles + 1), s)))
         return e;
+#endif
     if ((e = cudaMemsetAsync(bins.K, 0, sizeof(uint32_t) * 4, s))) return e;
     if (bp.slabs > 0) {
         k_slab_count<<<(unsigned)bp.slabs, SLAB_THREADS, sizeof(int) * dplane, s>>>(
@@ -952,6 +1334,57 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
         cur ^= 1;
     }
     prof->end(s, DEPTH_PASSES + 1);
+#if QUEEN_BIN_BUCKETS
+    // per-tile entry counts -> ranges (the emission writes entries at their final positions)
+    prof->begin(ST_RANGES, s);
+    k_ranges_finalize<<<sms * 2, 256, 0, s>>>(tcounts, lstart, view_tot, n_views, (uint32_t)T, cap, Kd,
+                                              reinterpret_cast<uint2*>(bins.ranges));
+    prof->end(s);
+    // pieces (pair, bucket) bucketed in depth order, then emitted tile by tile
+    BucketGeo bg;
+    bg.gx = gx;
+    bg.gy = gy;
+    bg.nbx = (gx + BK_W - 1) / BK_W;
+    bg.nby = (gy + BK_H - 1) / BK_H;
+    bg.NB = bg.nbx * bg.nby;
+    bg.VNB = bg.NB * n_views;
+    bg.T = (int)T;
+    bg.n_pad = proj.n_pad;
+    uint32_t* pcnt = reinterpret_cast<uint32_t*>(ws + L.pcnt);
+    uint32_t* ptotal = reinterpret_cast<uint32_t*>(ws + L.pbuck);
+    uint32_t* pbase = ptotal + bg.VNB;
+    uint32_t* ebase = pbase + bg.VNB;  // [VNB + 1]
+    uint32_t* meta = ebase + bg.VNB + 1;
+    uint32_t* emit_lb = reinterpret_cast<uint32_t*>(ws + L.emit_lb);
+    const int64_t chunks = (count + PC_CH - 1) / PC_CH;
+    bg.CHS = (int)chunks;
+    const int64_t etiles = ((int64_t)cap + EM_E - 1) / EM_E + bg.VNB + 1;
+    const size_t vsm = sizeof(uint32_t) * (size_t)bg.VNB;
+    const uint32_t* dlast_in = dv[cur ^ 1];   // input of the last depth pass
+    const uint32_t* dlast_out = dv[cur];      // its output (unless it was skipped)
+    const uint32_t* triv = hist + (DEPTH_PASSES - 1) * MAX_BINS;
+    const short4* r4 = reinterpret_cast<const short4*>(proj.rect);
+    if (vsm > PC_MAX_SMEM) return cudaErrorInvalidConfiguration;  // > 51200 buckets: not reachable (<= 64 4K views)
+    prof->begin(ST_DUPLICATE, s);
+    if ((e = cudaMemsetAsync(emit_lb, 0, sizeof(uint32_t) * BK_T * (size_t)etiles, s))) return e;
+    if (chunks > 0) {
+        k_piece_count<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt);
+        k_piece_colscan<<<(unsigned)((bg.VNB + 7) / 8), 256, 0, s>>>(pcnt, Kd, bg, ptotal);
+        k_piece_base<<<1, 1024, 0, s>>>(ptotal, bg.VNB, pbase, ebase, meta);
+        k_piece_scatter<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, pbase,
+                                                                  bins.keys_alt);
+    }
+    prof->end(s, chunks > 0 ? 5 : 1);
+    prof->begin(ST_TILE_SORT, s);
+    if (chunks > 0)
+        k_emit<<<emit_grid(), EM_THREADS, sizeof(EmitSmem), s>>>(bins.keys_alt, pcnt, ptotal, pbase, ebase, meta,
+                                                                 dlast_in, dlast_out, triv, Kd, r4,
+                                                                 reinterpret_cast<const uint2*>(bins.ranges), bg,
+                                                                 bins.vals, emit_lb, &fl->tickets[TK_EMIT], fl);
+    prof->end(s, chunks > 0 ? 1 : 0);
+    bins.sorted_in_alt = 0;
+    return cudaGetLastError();
+#else
     // offsets in depth order + duplication
     prof->begin(ST_DUPLICATE, s);
     if (elem_tiles > 0)
@@ -997,6 +1430,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     prof->end(s, tpasses + 1);
     bins.sorted_in_alt = va == bins.vals_alt ? 1 : 0;
     return cudaGetLastError();
+#endif
 }
 
 }  // namespace queen

@@ -111,6 +111,16 @@ inline BinPlan bin_plan(int64_t n_pad, int64_t n_views, int W, int H) {
     return p;
 }
 
+// Bucketed emission (binning.cu K4'/K5'): buckets of BK_W x BK_H tiles of one view; the
+// depth-ordered pairs are counted and scattered in chunks of PC_CH; emit tiles hold ~EM_E pieces.
+constexpr int PC_CH = 4096;
+constexpr int BK_W = 16, BK_H = 8, BK_T = BK_W * BK_H;
+constexpr int EM_E = 2048;
+inline int64_t buckets_per_view(int W, int H) {
+    const int64_t gx = (W + 15) / 16, gy = (H + 15) / 16;
+    return ((gx + BK_W - 1) / BK_W) * ((gy + BK_H - 1) / BK_H);
+}
+
 // Blend schedule (raster.cu): tiles launched longest list first, by list length classes of
 // 32 entries (ORDER_BINS classes, the last open-ended), so the grid's tail holds short tiles.
 constexpr int ORDER_BINS = 64;
@@ -119,7 +129,7 @@ constexpr int ORDER_BINS = 64;
 struct WsLayout {
     // scratch (bin_sort)
     size_t flags, hist, dminmax, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, counts, view_tot, slab_counts,
-        slab_vis, select, order, total_scratch;
+        slab_vis, select, pcnt, pbuck, emit_lb, order, total_scratch;
     // render_views / render_mask buffers
     size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, mask_tmp, total;
     int64_t key_tiles, elem_tiles, os_key_tiles, os_elem_tiles, T, elems;
@@ -153,6 +163,14 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     L.slab_counts = o; o += align256(sizeof(uint32_t) * (size_t)(bp.ok ? bp.slabs : 0) * L.T);
     L.slab_vis = o; o += align256(sizeof(uint32_t) * (size_t)(bp.slabs + 1));
     L.select = o; o += align256((size_t)n_pad);  // render_mask: per-Gaussian subset flags
+    {
+        const int64_t vnb = (int64_t)n_views * buckets_per_view(W, H);
+        const int64_t chunks = (L.elems + PC_CH - 1) / PC_CH;
+        L.pcnt = o; o += align256(sizeof(uint32_t) * (size_t)(chunks * vnb));  // pieces per (chunk, bucket)
+        L.pbuck = o; o += align256(sizeof(uint32_t) * (size_t)(3 * vnb + 8));  // totals | bases | emit-tile bases | meta
+        const int64_t etiles = (keys_cap + EM_E - 1) / EM_E + vnb + 1;
+        L.emit_lb = o; o += align256(sizeof(uint32_t) * BK_T * (size_t)etiles);  // emit-tile look-back
+    }
     L.order = o; o += align256(sizeof(uint32_t) * (2 * ORDER_BINS + (size_t)n_views * L.T));  // blend tile order
     L.total_scratch = o;
     L.rec = o; o += align256(sizeof(float) * REC_WORDS * L.elems);
@@ -177,7 +195,8 @@ inline bool scratch_fits(const WsLayout& need, const WsLayout& have) {
                                    &WsLayout::depth_lb,   &WsLayout::tile_lb,     &WsLayout::dkeys,
                                    &WsLayout::dkeys_alt,  &WsLayout::dvals,       &WsLayout::dvals_alt,
                                    &WsLayout::counts,     &WsLayout::view_tot,    &WsLayout::slab_counts,
-                                   &WsLayout::slab_vis,   &WsLayout::select,      &WsLayout::order,
+                                   &WsLayout::slab_vis,   &WsLayout::select,      &WsLayout::pcnt,
+                                   &WsLayout::pbuck,      &WsLayout::emit_lb,     &WsLayout::order,
                                    &WsLayout::total_scratch};
     for (size_t q = 0; q + 1 < sizeof(r) / sizeof(r[0]); ++q)
         if (need.*r[q + 1] - need.*r[q] > have.*r[q + 1] - have.*r[q]) return false;

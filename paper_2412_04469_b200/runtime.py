@@ -87,7 +87,7 @@ class EntropyPacket:
         ptrs = [base + self.hdr["ans_off"][c] if self.hdr["lat"][c] else None for c in range(5)]
         # bound each stream by its fixed-capacity section (not this frame's used bytes): a captured
         # graph replays the decode on later packets refilled into the same buffer
-        offs = [self.hdr["ans_off"][c] for c in range(5)] + [self.hdr["total"]]
+        offs = [self.hdr["ans_off"][c] for c in range(5)] + [int(self.hdr.get("total", self.buf.numel()))]
         caps = [(min(o for o in offs[c + 1:] if o > offs[c]) - offs[c]) if self.hdr["lat"][c] else 0 for c in range(5)]
         queen_entropy_decode_frame(ctx, ptrs, caps, self.hdr["lat"], self.hdr["n"], self.latents, stream)
 
