@@ -334,6 +334,37 @@ def make_packet(scene: Scene, t: int, *, gates: bool = True, beta: float | None 
                   log_alpha, pregate, (tau, g0, g1))
 
 
+# ----------------------------------------------------------------------------- first frame
+@dataclass
+class FirstFrameSH:
+    """Frame 0's high-frequency SH coefficients in quantised form: integer latents
+    [L][n_pad] int8 (the colour-frequency latent dim of the config) and the decoder [3(B-1)][L]."""
+    n: int
+    n_pad: int
+    deg: int
+    latents: np.ndarray
+    decoder: np.ndarray
+
+
+def make_first_frame_sh(scene: Scene, *, beta: float = 1.5, dyadic: bool = False) -> FirstFrameSH:
+    """Seeded frame-0 SH latents (Laplace, scale beta: absolute coefficients, not residuals) and
+    decoder (U[-1,1]/sqrt(L) x 0.05 -- SH-rest magnitudes of N(0, 0.05^2)); dyadic:
+    |l| <= 8 and D on the 2^-10 grid (|D| <= 1/8), so any accumulation order is exact."""
+    cfg = scene.cfg
+    n, n_pad, deg = scene.n, scene.n_pad, scene.deg
+    L = cfg.lat[4] if cfg.lat[4] > 0 else 4
+    M = 3 * ((deg + 1) ** 2 - 1)
+    rng = np.random.Generator(np.random.PCG64([cfg.seed, 0xF0]))
+    q = np.zeros((L, n_pad), np.int8)
+    if dyadic:
+        q[:, :n] = rng.integers(-8, 9, (L, n)).astype(np.int8)
+        d = rng.integers(-128, 129, (M, L)).astype(np.float32) / 1024.0
+    else:
+        q[:, :n] = np.clip(np.round(rng.laplace(0.0, beta, (L, n))), -127, 127).astype(np.int8)
+        d = (rng.uniform(-1, 1, (M, L)) / math.sqrt(L) * 0.05).astype(np.float32)
+    return FirstFrameSH(n, n_pad, deg, q, np.ascontiguousarray(d, np.float32))
+
+
 # ----------------------------------------------------------------------------- NEXT #2
 @dataclass
 class Delta:

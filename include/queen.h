@@ -177,6 +177,17 @@ queen_status queen_decode_residuals(queen_ctx* ctx, const queen_packet* pkt, flo
 /* queen_apply_frame: FUSED a1-a5: A_{t-1} -> A_t in place (Eq. 4):
  * non-position planes += D_c float(round(l_c)); positions += COO / gated residual. */
 queen_status queen_apply_frame(queen_ctx* ctx, queen_gaussians* scene, const queen_packet* pkt, void* stream);
+
+/* queen_set_sh_rest: first-frame quantisation ("First-frame Quantization": only
+ * frame 0's high-frequency SH coefficients, DC excluded, are learnably quantised).  Decodes them
+ * ONCE and WRITES them (not added) into the scene:
+ *   planes[14 + m][i] = sum_{k<L} decoder[m][k] * (float)latents[k][i]   (fmaf chain over
+ *   ascending k from +0.0f, DESIGN R7), m = 3 (b - 1) + ch, b = 1 .. B-1, for i < n.
+ * latents: device int8 [L][n_pad] (e.g. decoded by queen_entropy_decode); decoder: device fp32
+ * row-major [3(B-1)][L]; scene->sh_degree 1..3; L in 1..16.  Other planes and columns >= n are
+ * untouched.  Enqueue-only; no device-detectable errors. */
+queen_status queen_set_sh_rest(queen_ctx* ctx, queen_gaussians* scene, const int8_t* latents, int32_t L,
+                               const float* decoder, void* stream);
 /* queen_project: a6-a7 for n_views cameras (Eq. 1 + SH colour).
  * `cams` is a HOST array of n_views cameras.  out arrays hold [n_views][n_pad]. */
 queen_status queen_project(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams, int32_t n_views,
@@ -212,6 +223,14 @@ queen_status queen_rasterize_rgb8(queen_ctx* ctx, const queen_proj* proj, const 
                                   float* T_out, void* stream);
 queen_status queen_render_views_rgb8(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
                                      int32_t n_views, const float bg[3], uint8_t* rgb8_out, float* T_out, void* stream);
+/* Half-precision variants (the streaming output that keeps the 2e-3 RGB bar: binary16 is within
+ * 2^-11 of any value in [0, 1]): f16_out IEEE binary16 [n_views][3][H][W] = the fp32 output value
+ * C + T bg rounded to nearest even (unclamped); T_out as above (nullable). */
+queen_status queen_rasterize_f16(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
+                                 const queen_camera* cams, int32_t n_views, const float bg[3], uint16_t* f16_out,
+                                 float* T_out, void* stream);
+queen_status queen_render_views_f16(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
+                                    int32_t n_views, const float bg[3], uint16_t* f16_out, float* T_out, void* stream);
 
 /* Debug / evidence: per-view blend work counters (evaluated and composited
  * (pixel, Gaussian) pairs, int64 device arrays [n_views]); same semantics as the

@@ -46,6 +46,7 @@ def lib():
             "oracle_quantize": (i64, [p, p, i64]),
             "oracle_decode": (None, [i32, i32, i32, p, p, p, p]),
             "oracle_apply": (i32, [i32, i32, i32, p, p, p, p, i32, p, p]),
+            "oracle_set_sh_rest": (None, [i32, i32, i32, i32, p, p, p]),
             "oracle_gate_value": (f32, [f32, f32, f32, f32]),
             "oracle_gate": (i32, [i32, i32, p, p, f32, f32, f32, f32, p, p, i32]),
             "oracle_sh_basis": (None, [i32, f32, f32, f32, p]),
@@ -130,6 +131,18 @@ def gate(pkt):
     k = lib().oracle_gate(pkt.n, pkt.n_pad, _p(np.ascontiguousarray(pkt.log_alpha)), _p(np.ascontiguousarray(pkt.pos_pregate)),
                           float(tau), float(g0), float(g1), float(th0), _p(idx), _p(val), max(cap, 1))
     return idx[:k].copy(), np.ascontiguousarray(val[:, :k])
+
+
+def set_sh_rest(planes: np.ndarray, n: int, deg: int, latents: np.ndarray, decoder: np.ndarray) -> np.ndarray:
+    """First-frame SH "set" decode: a copy of planes with the SH-rest rows
+    (14 .. 11+3B-1) of the first n Gaussians replaced by D . float(l)."""
+    out = np.array(planes, np.float32, copy=True, order="C")
+    lat = np.ascontiguousarray(latents, np.int8)
+    dec = np.ascontiguousarray(decoder, np.float32)
+    L = lat.shape[0]
+    assert lat.shape[1] == out.shape[1] and dec.shape == (3 * ((deg + 1) ** 2 - 1), L)
+    lib().oracle_set_sh_rest(int(n), out.shape[1], int(deg), int(L), _p(lat), _p(dec), _p(out))
+    return out
 
 
 def apply(planes: np.ndarray, pkt, *, use_gates: bool = False, use_f32_latents: bool = False):

@@ -150,6 +150,23 @@ void oracle_decode(int n, int n_pad, int deg, const int* lat, const int8_t* q,
 }
 
 // ---------------------------------------------------------------------------
+// First-frame quantisation ("First-frame Quantization"): only frame 0's
+// high-frequency SH coefficients (DC excluded) are stored as integer latents + a decoder.
+// They are decoded once and written (A_0 is set, not updated): SH-rest coefficient m
+// (m = 3 (b - 1) + ch, plane 14 + m) of Gaussian i = D[m] . float(l_i), same accumulation
+// order as a2 (R#7).  q: int8 [L][n_pad]; dec: [3(B-1)][L]; planes: [11+3B][n_pad].
+// ---------------------------------------------------------------------------
+void oracle_set_sh_rest(int n, int n_pad, int deg, int L, const int8_t* q, const float* dec, float* planes) {
+    const int B = (deg + 1) * (deg + 1);
+    for (int m = 0; m < 3 * (B - 1); ++m)
+        for (int i = 0; i < n; ++i) {
+            float r = +0.0f;
+            for (int k = 0; k < L; ++k) r = std::fma(dec[m * L + k], (float)q[(int64_t)k * n_pad + i], r);
+            planes[(int64_t)(14 + m) * n_pad + i] = r;
+        }
+}
+
+// ---------------------------------------------------------------------------
 // a3 + a5. Apply A_t = A_{t-1} + R_t (Eq. 4) on the raw non-position
 // planes (R#1), then the COO position residual p[I_k] += E_p[k].
 // planes: float [11+3B][n_pad]; non-position plane 3+row receives resid row.

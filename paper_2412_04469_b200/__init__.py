@@ -34,7 +34,8 @@ EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version",
            "queen_wait_rendered", "queen_entropy_encode",
            "queen_entropy_decode", "queen_entropy_decode_frame", "queen_render_mask",
            "queen_densify", "queen_rasterize_rgb8", "queen_render_views_rgb8",
-           "queen_rasterize_backward", "queen_project_backward", "queen_decode_backward", "queen_set_options"]
+           "queen_rasterize_backward", "queen_project_backward", "queen_decode_backward", "queen_set_options",
+           "queen_rasterize_f16", "queen_render_views_f16", "queen_set_sh_rest"]
 STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy", "blend_order"]
 
 
@@ -108,6 +109,7 @@ def lib() -> C.CDLL:
                                          p, p, p]),
             "queen_profile_enable": (i32, [p, i32]),
             "queen_set_options": (i32, [p, i32]),
+            "queen_set_sh_rest": (i32, [p, C.POINTER(QueenGaussians), p, i32, p, p]),
             "queen_decode_backward": (i32, [p, C.POINTER(QueenPacket), p, p, p, p, p, p]),
             "queen_rasterize_backward": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera),
                                                i32, C.POINTER(C.c_float), p, p, p]),
@@ -115,6 +117,10 @@ def lib() -> C.CDLL:
             "queen_rasterize_rgb8": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
                                            C.POINTER(C.c_float), p, p, p]),
             "queen_render_views_rgb8": (i32, [p, C.POINTER(QueenGaussians), C.POINTER(QueenCamera), i32,
+                                              C.POINTER(C.c_float), p, p, p]),
+            "queen_rasterize_f16": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
+                                           C.POINTER(C.c_float), p, p, p]),
+            "queen_render_views_f16": (i32, [p, C.POINTER(QueenGaussians), C.POINTER(QueenCamera), i32,
                                               C.POINTER(C.c_float), p, p, p]),
             "queen_densify": (i32, [p, C.POINTER(QueenGaussians), p, i32, p, i32, C.POINTER(QueenGaussians), p]),
             "queen_render_mask": (i32, [p, C.POINTER(QueenGaussians), p, i32, p, C.POINTER(QueenCamera), i32, C.c_float,
@@ -362,6 +368,24 @@ def queen_render_views_rgb8(ctx: Context, scene: QueenGaussians, cams, rgb8_out,
     ctx._chk(st, "queen_render_views_rgb8")
 
 
+def queen_rasterize_f16(ctx: Context, proj: QueenProj, bins: QueenBins, cams, f16_out, T_out=None,
+                         bg=(0.0, 0.0, 0.0), stream=None):
+    arr = camera_array(cams)
+    bgv = (C.c_float * 3)(*[float(x) for x in bg])
+    st = lib().queen_rasterize_f16(ctx.handle, C.byref(proj), C.byref(bins), arr, len(arr), bgv, _ptr(f16_out),
+                                    _ptr(T_out), C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_rasterize_f16")
+
+
+def queen_render_views_f16(ctx: Context, scene: QueenGaussians, cams, f16_out, T_out=None, bg=(0.0, 0.0, 0.0),
+                            stream=None, cam_array=None):
+    arr = cam_array if cam_array is not None else camera_array(cams)
+    bgv = (C.c_float * 3)(*[float(x) for x in bg])
+    st = lib().queen_render_views_f16(ctx.handle, C.byref(scene), arr, len(arr), bgv, _ptr(f16_out), _ptr(T_out),
+                                       C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_render_views_f16")
+
+
 def queen_rasterize_backward(ctx: Context, proj: QueenProj, bins: QueenBins, cams, dL_drgb, grad_rec,
                              bg=(0.0, 0.0, 0.0), stream=None):
     """NEXT #4: dL/d(record) [V][n_pad][9] from dL/d(image) [V][3][H][W] (queen.h)."""
@@ -401,6 +425,13 @@ def queen_entropy_encode(latents: np.ndarray, n: int) -> np.ndarray:
     if st != QUEEN_OK:
         raise QueenError(st, f"queen_entropy_encode (needs {nb.value} bytes)")
     return out[: nb.value].copy()
+
+
+def queen_set_sh_rest(ctx: Context, scene: QueenGaussians, latents, L: int, decoder, stream=None):
+    """First-frame SH "set" decode: planes[14+m] = D . float(l) for the SH-rest rows."""
+    st = lib().queen_set_sh_rest(ctx.handle, C.byref(scene), _ptr(latents), int(L), _ptr(decoder),
+                                 C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_set_sh_rest")
 
 
 def queen_entropy_decode(ctx: Context, stream_dev, L: int, n: int, latents_out, stream=None, nbytes: int | None = None):

@@ -70,7 +70,7 @@ __device__ __forceinline__ void coo_entry(float* planes, int n, int64_t n_pad, c
     planes[2 * n_pad + i] = planes[2 * n_pad + i] + v2;
 }
 
-template <bool F32, bool APPLY, bool GATES>
+template <bool F32, bool APPLY, bool GATES, bool SET = false>
 __global__ void __launch_bounds__(256, QUEEN_DA_MINB) k_decode_apply(DecodeParams p) {
     extern __shared__ float sdec[];
     // grid = groups x Gaussian blocks, group-major (measured: gid-fastest, which keeps a
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(256, QUEEN_DA_MINB) k_decode_apply(DecodeParam
             if (write_q) *reinterpret_cast<uint32_t*>(p.q_out + off) = q4[k];
         }
     }
-    if (APPLY) {
+    if (APPLY && !SET) {
 #pragma unroll
         for (int u = 0; u < DA_ROWS; ++u)
             if (u < R) av[u] = *reinterpret_cast<const float4*>(p.planes + (int64_t)(3 + row0 + u) * np + i0);
@@ -196,7 +196,17 @@ __global__ void __launch_bounds__(256, QUEEN_DA_MINB) k_decode_apply(DecodeParam
         if (u >= R) break;
         const int row = row0 + u;
         if (p.resid_out) *reinterpret_cast<float4*>(p.resid_out + (int64_t)row * np + i0) = r[u];
-        if (APPLY) {
+        if (SET) {
+            // first-frame "set" decode: A_0 = D . float(l), written, not added
+            float4 v = *reinterpret_cast<const float4*>(&r[u]);
+            if (!l1 || !l2 || !l3) {  // ragged tail: keep the padding columns as they are
+                const float4 o = *reinterpret_cast<const float4*>(p.planes + (int64_t)(3 + row) * np + i0);
+                if (!l1) v.y = o.y;
+                if (!l2) v.z = o.z;
+                if (!l3) v.w = o.w;
+            }
+            *reinterpret_cast<float4*>(p.planes + (int64_t)(3 + row) * np + i0) = v;
+        } else if (APPLY) {
             // a3: A_t = A_{t-1} + r, separate add (R#7)
             float4 v = av[u];
             v.x = v.x + r[u].x;
@@ -413,6 +423,42 @@ cudaError_t launch_decode_apply(const queen_packet& pk, float* planes, float* re
         k_coo_scatter<<<kb, 256, 0, s>>>(planes, pk.n, pk.n_pad, pk.pos_idx, pk.pos_val, pk.k, pk.k_dev, fl, nullptr,
                                          nullptr, nullptr, 0, true);
     }
+    return cudaGetLastError();
+}
+
+// First-frame quantisation: frame 0's high-frequency SH coefficients (SH-rest,
+// excluding DC) are stored as integer latents + a decoder and decoded ONCE, written absolutely:
+// planes[14 + m][i] = sum_k D[m][k] float(l[k][i]) (fmaf chain ascending k from +0, R#7),
+// m = 3 (b - 1) + ch.  Same kernel as the frame residuals (category 4 groups only, SET mode).
+cudaError_t launch_set_sh_rest(float* planes, int n, int n_pad, int deg, const int8_t* latents, int L,
+                               const float* decoder, DevFlags* fl, cudaStream_t s) {
+    queen_packet pk{};
+    pk.n = n;
+    pk.n_pad = n_pad;
+    pk.sh_degree = deg;
+    pk.lat_dim[4] = L;
+    pk.latent_kind = QUEEN_LAT_INT8;
+    pk.latents = latents;
+    pk.decoders = decoder;
+    DecodeParams p{};
+    fill_params(pk, p);
+    p.planes = planes;
+    p.fl = fl;
+    const int M = p.M[4], parts = (M + DA_ROWS - 1) / DA_ROWS;
+    int ng = 0, max_dec = 1;
+    for (int q = 0; q < parts; ++q) {
+        p.g_c[ng] = 4;
+        p.g_m0[ng] = (int)((int64_t)M * q / parts);
+        p.g_m1[ng] = (int)((int64_t)M * (q + 1) / parts);
+        max_dec = max(max_dec, (p.g_m1[ng] - p.g_m0[ng]) * L);
+        ++ng;
+    }
+    p.ngroups = ng;
+    const int threads = 256;
+    p.xblocks = (n + 4 * threads - 1) / (4 * threads);
+    const int64_t blocks = (int64_t)p.xblocks * ng;
+    if (blocks > 0 && M > 0)
+        k_decode_apply<false, true, false, true><<<(unsigned)blocks, threads, sizeof(float) * (size_t)max_dec, s>>>(p);
     return cudaGetLastError();
 }
 

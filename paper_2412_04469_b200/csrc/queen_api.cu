@@ -217,6 +217,21 @@ queen_status queen_apply_frame(queen_ctx* ctx, queen_gaussians* scene, const que
     return QUEEN_OK;
 }
 
+queen_status queen_set_sh_rest(queen_ctx* ctx, queen_gaussians* scene, const int8_t* latents, int32_t L,
+                               const float* decoder, void* stream) {
+    if (!ctx) return QUEEN_ERR_INVALID_ARG;
+    if (!scene || !scene->planes || !latents || !decoder) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
+    if (scene->sh_degree < 1 || scene->sh_degree > 3) return fail(ctx, QUEEN_ERR_INVALID_ARG, "sh_degree must be 1..3 (SH-rest exists)");
+    if (L < 1 || L > 16) return fail(ctx, QUEEN_ERR_INVALID_ARG, "latent dim must be 1..16");
+    if (scene->n < 0 || scene->n > scene->n_pad || scene->n_pad % 4) return fail(ctx, QUEEN_ERR_SHAPE, "n <= n_pad, n_pad % 4 == 0");
+    ctx->prof.begin(ST_APPLY, static_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_set_sh_rest(scene->planes, scene->n, scene->n_pad, scene->sh_degree, latents, L, decoder,
+                                       flags_of(ctx), static_cast<cudaStream_t>(stream));
+    ctx->prof.end(static_cast<cudaStream_t>(stream), 1);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "set_sh_rest");
+    return QUEEN_OK;
+}
+
 static queen_status check_cams(queen_ctx* ctx, const queen_camera* cams, int32_t n_views, bool same_size) {
     if (!cams || n_views < 1) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null cams / n_views < 1");
     for (int v = 0; v < n_views; ++v) {
@@ -294,14 +309,14 @@ static uint32_t* order_scratch(queen_ctx* ctx, int32_t n_views, int W, int H) {
 
 static queen_status rasterize_impl(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
                                    const queen_camera* cams, int32_t n_views, const float bg[3], float* rgb_out,
-                                   float* T_out, uint8_t* rgb8_out, void* stream) {
+                                   float* T_out, uint8_t* rgb8_out, void* stream, int alt_mode = OUT_RGB8) {
     if (!ctx) return QUEEN_ERR_INVALID_ARG;
     if (!proj || !bins || !(rgb_out || rgb8_out) || !bg) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
     if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
     const uint32_t* vals = bins->sorted_in_alt ? bins->vals_alt : bins->vals;
     int nl = 1;
     cudaError_t e = launch_rasterize(proj->rec, proj->n_pad, bins->ranges, vals, n_views, cams[0].width, cams[0].height,
-                                     bg[0], bg[1], bg[2], rgb_out, T_out, rgb8_out, rgb8_out ? OUT_RGB8 : OUT_F32, 0.f,
+                                     bg[0], bg[1], bg[2], rgb_out, T_out, rgb8_out, rgb8_out ? alt_mode : OUT_F32, 0.f,
                                      order_scratch(ctx, n_views, cams[0].width, cams[0].height),
                                      static_cast<cudaStream_t>(stream), &nl, &ctx->prof, ctx->opts);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "rasterize");
@@ -312,6 +327,14 @@ queen_status queen_rasterize(queen_ctx* ctx, const queen_proj* proj, const queen
                              int32_t n_views, const float bg[3], float* rgb_out, float* T_out, void* stream) {
     if (ctx && !rgb_out) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null rgb_out");
     return rasterize_impl(ctx, proj, bins, cams, n_views, bg, rgb_out, T_out, nullptr, stream);
+}
+
+queen_status queen_rasterize_f16(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
+                                 const queen_camera* cams, int32_t n_views, const float bg[3], uint16_t* f16_out,
+                                 float* T_out, void* stream) {
+    if (ctx && !f16_out) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null f16_out");
+    return rasterize_impl(ctx, proj, bins, cams, n_views, bg, nullptr, T_out, reinterpret_cast<uint8_t*>(f16_out), stream,
+                          OUT_F16);
 }
 
 queen_status queen_rasterize_rgb8(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
@@ -423,7 +446,8 @@ queen_status queen_entropy_decode_frame(queen_ctx* ctx, const void* const* strea
 }
 
 static queen_status render_impl(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams, int32_t n_views,
-                                const float bg[3], float* rgb_out, float* T_out, uint8_t* rgb8_out, void* stream) {
+                                const float bg[3], float* rgb_out, float* T_out, uint8_t* rgb8_out, void* stream,
+                                int alt_mode = OUT_RGB8) {
     if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
     if (!scene || !(rgb_out || rgb8_out) || !bg) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
     if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
@@ -457,9 +481,9 @@ static queen_status render_impl(queen_ctx* ctx, const queen_gaussians* scene, co
     if (queen_status st = queen_bin_sort(ctx, &pj, cams, n_views, &b, stream)) return st;
     if (cudaEventRecord(ctx->binned, static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return cuda_fail(ctx, cudaGetLastError(), "record binned event");
-    if (!bs) return rasterize_impl(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, rgb8_out, stream);
+    if (!bs) return rasterize_impl(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, rgb8_out, stream, alt_mode);
     if (cudaStreamWaitEvent(bs, ctx->binned, 0) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "blend wait");
-    queen_status st = rasterize_impl(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, rgb8_out, bs);
+    queen_status st = rasterize_impl(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, rgb8_out, bs, alt_mode);
     if (!st && cudaEventRecord(ctx->rendered, bs) != cudaSuccess)
         return cuda_fail(ctx, cudaGetLastError(), "record rendered event");
     return st;
@@ -469,6 +493,12 @@ queen_status queen_render_views(queen_ctx* ctx, const queen_gaussians* scene, co
                                 const float bg[3], float* rgb_out, float* T_out, void* stream) {
     if (ctx && !rgb_out) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null rgb_out");
     return render_impl(ctx, scene, cams, n_views, bg, rgb_out, T_out, nullptr, stream);
+}
+
+queen_status queen_render_views_f16(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
+                                    int32_t n_views, const float bg[3], uint16_t* f16_out, float* T_out, void* stream) {
+    if (ctx && !f16_out) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null f16_out");
+    return render_impl(ctx, scene, cams, n_views, bg, nullptr, T_out, reinterpret_cast<uint8_t*>(f16_out), stream, OUT_F16);
 }
 
 queen_status queen_render_views_rgb8(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,

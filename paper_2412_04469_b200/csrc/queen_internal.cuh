@@ -351,9 +351,11 @@ cudaError_t launch_coo_copy(const queen_packet& p, uint32_t* idx_out, float* val
 cudaError_t launch_project(const float* planes, int n, int n_pad, int deg, const CamBatch& cams, int n_views,
                            float* rec, uint32_t* depth, uint32_t* tiles, int16_t* rect, const uint8_t* select,
                            DevFlags* fl, cudaStream_t s);
+cudaError_t launch_set_sh_rest(float* planes, int n, int n_pad, int deg, const int8_t* latents, int L,
+                               const float* decoder, DevFlags* fl, cudaStream_t s);
 cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
                             const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof);
-enum : int { OUT_F32 = 0, OUT_MASK = 1, OUT_RGB8 = 2 };  // k_blend epilogues
+enum : int { OUT_F32 = 0, OUT_MASK = 1, OUT_RGB8 = 2, OUT_F16 = 3 };  // k_blend epilogues
 #ifndef QUEEN_BLEND_TSUB
 #define QUEEN_BLEND_TSUB 1  // blend transmittance T' = T - aT (aT = alpha T is formed anyway) instead of T (1 - alpha)
 #endif

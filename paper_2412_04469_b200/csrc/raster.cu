@@ -22,6 +22,8 @@
 //   a = min(0.99, o 2^p2); C = fma(rgb, a T, C); T = T (1 - a); stop after T < 1e-4.
 #include <cstdlib>
 
+#include <cuda_fp16.h>
+
 #include "queen_internal.cuh"
 
 #include <algorithm>
@@ -293,6 +295,27 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
             for (int r = 0; r < RPT; ++r) {
                 const float pT = (r & 1) ? p[r >> 1].T.y : p[r >> 1].T.x;
                 if (row_of(r) < H) mo[(int64_t)row_of(r) * W] = (1.0f - pT > mask_thresh) ? 1 : 0;
+            }
+        }
+        return;
+    }
+    if (out_mode == OUT_F16) {  // half-precision planar: the fp32 output value rounded to nearest binary16
+        if (px < W) {
+            const int64_t plane = (int64_t)H * W;
+            __half* oh = reinterpret_cast<__half*>(out8) + (int64_t)v * 3 * plane + px;
+            float* to = T_out ? T_out + (int64_t)v * plane + px : nullptr;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                if (row_of(r) < H) {
+                    const int64_t ro = (int64_t)row_of(r) * W;
+                    const Px2& q = p[r >> 1];
+                    const float pr = (r & 1) ? q.r.y : q.r.x, pg = (r & 1) ? q.g.y : q.g.x, pb = (r & 1) ? q.b.y : q.b.x;
+                    const float pT = (r & 1) ? q.T.y : q.T.x;
+                    oh[ro] = __float2half_rn(pr + pT * bg0);
+                    oh[plane + ro] = __float2half_rn(pg + pT * bg1);
+                    oh[2 * plane + ro] = __float2half_rn(pb + pT * bg2);
+                    if (to) to[ro] = pT;
+                }
             }
         }
         return;

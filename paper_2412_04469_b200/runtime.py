@@ -11,8 +11,27 @@ import torch
 from . import (QUEEN_LAT_F32, QUEEN_LAT_INT8, QUEEN_MAX_VIEWS, QUEEN_POS_COO, QUEEN_POS_GATES, Context,
                QueenError, camera_array, gaussians_struct, packet_struct, queen_apply_frame,
                queen_densify, queen_entropy_decode_frame, queen_render_mask, queen_render_views,
-               queen_render_views_rgb8, queen_set_blend_stream, queen_wait_binned)
+               queen_render_views_f16, queen_render_views_rgb8, queen_set_blend_stream, queen_wait_binned)
 from . import packet as wire
+
+
+_OUT_FNS = {"f32": (queen_render_views, torch.float32), "rgb8": (queen_render_views_rgb8, torch.uint8),
+            "f16": (queen_render_views_f16, torch.float16)}
+
+
+def _out_fn(rgb8, out):
+    """Output format of a render call: rgb8=True or a uint8 `out` -> u8 display format; a float16
+    `out` -> binary16; else fp32."""
+    if rgb8 is True or rgb8 == "rgb8" or (out is not None and out.dtype == torch.uint8):
+        fmt = "rgb8"
+    elif rgb8 == "f16" or (out is not None and out.dtype == torch.float16):
+        fmt = "f16"
+    else:
+        fmt = "f32"
+    fn, dt = _OUT_FNS[fmt]
+    if fmt != "f32" and (out is None or out.dtype != dt):
+        raise ValueError(f"{fmt} rendering needs an out tensor of dtype {dt} [V][3][H][W]")
+    return fn
 
 
 class DevicePacket:
@@ -153,12 +172,11 @@ class Player:
         queen_apply_frame(self.ctx, self.scene, pkt.struct, stream)
 
     def render(self, stream=None, out=None, rgb8: bool = False):
-        """Render every view into `out` (default self.rgb): fp32 [V][3][H][W], or with rgb8=True the
-        display format u8 [V][3][H][W] (queen_render_views_rgb8; `out` then required)."""
+        """Render every view into `out` (default self.rgb): fp32 [V][3][H][W]; with rgb8=True the
+        display format u8 [V][3][H][W] (queen_render_views_rgb8); with a float16 `out` binary16
+        (queen_render_views_f16)."""
         rgb = self.rgb if out is None else out
-        if rgb8 and (out is None or out.dtype != torch.uint8):
-            raise ValueError("rgb8 rendering needs a uint8 out tensor [V][3][H][W]")
-        fn = queen_render_views_rgb8 if rgb8 else queen_render_views
+        fn = _out_fn(rgb8, out)
         main = stream if stream is not None else torch.cuda.current_stream(self.dev)
         if self.n_lanes > 1:
             start = torch.cuda.Event()
@@ -313,7 +331,7 @@ class Player:
         if self._consumed[lane] is not None:  # the reader of this lane's previous image is done
             bs.wait_event(self._consumed[lane])
         self._consumed[lane] = consumed if out is None else None
-        fn = queen_render_views_rgb8 if rgb8 else queen_render_views
+        fn = _out_fn(rgb8, out)
         queen_set_blend_stream(ctx, bs)  # only for these calls: render() / step() keep one stream
         try:
             for (a, b), arr in zip(self.batches, self.cam_arrays):

@@ -487,6 +487,22 @@ def test_render_views_rgb8_display_format():
     assert np.abs(u8.cpu().numpy().astype(np.int16) - ref8).max() <= 1
 
 
+def test_render_views_f16_output():
+    """queen_render_views_f16 = the fp32 render rounded to nearest binary16 (GPU vs GPU: identical
+    compositing, bit-exact), and within the 2e-3 RGB bar of the oracle (binary16 adds <= 2^-11)."""
+    from paper_2412_04469_b200.runtime import Player
+    cfg, sc, cams = _render_case("n3dv", 20003, 3, width=333, height=250, focal=280.0)
+    pl = Player(sc.planes, sc.n, sc.deg, cams, bg=(0.2, 0.4, 0.6))
+    pl.fit_capacity()
+    f32 = pl.render().clone()
+    h = torch.empty(f32.shape, dtype=torch.float16, device="cuda")
+    pl.render(out=h)
+    assert torch.equal(h, f32.to(torch.float16))  # torch: round to nearest even
+    _, _, ref, _ = oracle.render(sc.planes, sc.n, sc.deg, cams, bg=(0.2, 0.4, 0.6))
+    err = np.abs(np.clip(h.float().cpu().numpy(), 0, 1) - np.clip(ref, 0, 1)).max()
+    assert err <= RGB_TOL, err
+
+
 def test_cuda_graph_frame_equals_eager():
     """A captured frame step (entropy decode + apply + render, Player.capture) replays to the
     same SoA and images, bit for bit, as the eager calls."""

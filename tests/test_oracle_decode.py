@@ -145,3 +145,42 @@ def test_latent_range_error():
     pkt.latents_f32[0, 3] = 127.6
     _, st, _ = oracle.apply(sc.planes, pkt, use_f32_latents=True)
     assert st == -4
+
+
+# ------------------------------------------------------------------ first-frame SH "set" decode
+def test_set_sh_rest_identity_decoder():
+    """P:1380-1381 first-frame quantisation, D = I (L = M = 9 at degree 1): the SH-rest planes
+    become float(l) exactly; every other plane and the padding columns are untouched."""
+    rng = np.random.default_rng(3)
+    n, n_pad, deg = 37, 40, 1
+    planes = rng.standard_normal((11 + 3 * 4, n_pad)).astype(np.float32)
+    lat = rng.integers(-127, 128, (9, n_pad)).astype(np.int8)
+    out = oracle.set_sh_rest(planes, n, deg, lat, np.eye(9, dtype=np.float32))
+    assert np.array_equal(out[14:, :n], lat[:, :n].astype(np.float32))
+    assert np.array_equal(out[:14].view(np.uint32), planes[:14].view(np.uint32))
+    assert np.array_equal(out[:, n:].view(np.uint32), planes[:, n:].view(np.uint32))
+
+
+def test_set_sh_rest_dyadic_exact():
+    """Dyadic family (D on the 2^-10 grid, |l| <= 8, L = 12, degree 3: M = 45): every partial sum
+    is exact in fp32, so the result equals the integer-arithmetic value sum_k D_k l_k exactly,
+    and it REPLACES the old coefficients (set, not add)."""
+    from harness import synth
+    cfg = synth.get_config("immersive")
+    sc = synth.make_scene(cfg, n=3001)
+    ff = synth.make_first_frame_sh(sc, dyadic=True)
+    assert ff.latents.shape[0] == 12 and ff.decoder.shape == (45, 12)
+    out = oracle.set_sh_rest(sc.planes, sc.n, sc.deg, ff.latents, ff.decoder)
+    Di = np.rint(ff.decoder.astype(np.float64) * 1024).astype(np.int64)      # exact integers
+    exact = (Di @ ff.latents[:, :sc.n].astype(np.int64)).astype(np.float64) / 1024.0
+    assert np.array_equal(out[14:, :sc.n].astype(np.float64), exact)
+    assert np.array_equal(out[:14].view(np.uint32), sc.planes[:14].view(np.uint32))
+
+
+def test_set_sh_rest_zero_latents_give_positive_zero():
+    """All-zero latents decode to +0.0 (fmaf chain from +0, R7), whatever the decoder's signs."""
+    n, n_pad, deg = 8, 8, 2
+    planes = np.full((11 + 3 * 9, n_pad), 7.0, np.float32)
+    dec = -np.ones((24, 3), np.float32)
+    out = oracle.set_sh_rest(planes, n, deg, np.zeros((3, n_pad), np.int8), dec)
+    assert np.all(out[14:].view(np.uint32) == 0)
