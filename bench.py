@@ -738,6 +738,35 @@ def main():
                                "frames, L2 flushed between frames (P:1457's definition on this workload)"}
         del pl1
 
+    # ---- NEXT #1 (first frame): frame 0's SH-rest coefficients decoded from their entropy-coded
+    # latents + decoder and written into the set, the stream's one-time load cost
+    first_frame = None
+    if rank == 0 and sc.deg > 0 and not args.no_paper_style:
+        ff = synth.make_first_frame_sh(sc)
+        Lf = ff.latents.shape[0]
+        ff_stream = Q.queen_entropy_encode(ff.latents, sc.n)
+        ff_dev = torch.from_numpy(ff_stream).to(dev)
+        ff_lat = torch.empty((Lf, sc.n_pad), dtype=torch.int8, device=dev)
+        ff_dec = torch.from_numpy(ff.decoder).to(dev)
+        ff_planes = A0.clone()
+        ff_scene = Q.gaussians_struct(ff_planes, sc.n, sc.deg)
+        fe = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        for rep in range(2):  # first launch warms up; the second is timed (L2 flushed before it)
+            flush.zero_()
+            fe[0].record(stream)
+            Q.queen_entropy_decode(player.ctx, ff_dev, Lf, sc.n, ff_lat)
+            fe[1].record(stream)
+            Q.queen_set_sh_rest(player.ctx, ff_scene, ff_lat, Lf, ff_dec)
+            fe[2].record(stream)
+        torch.cuda.synchronize()
+        first_frame = {"ms": fe[0].elapsed_time(fe[2]), "entropy_decode_ms": fe[0].elapsed_time(fe[1]),
+                       "set_ms": fe[1].elapsed_time(fe[2]), "coded_bytes": int(ff_stream.size),
+                       "bits_per_latent": 8.0 * ff_stream.size / (Lf * sc.n), "latent_dim": Lf,
+                       "coefficients": 3 * ((sc.deg + 1) ** 2 - 1),
+                       "note": "frame 0's SH-rest: GPU entropy decode of the latent stream + queen_set_sh_rest "
+                               "(D . float(l) written, P:1380-1381), L2 flushed"}
+        del ff_planes, ff_lat
+
     # ---- NEXT #3: masked / dynamic-subset rendering of the frame's gated set
     masked = None
     if rank == 0 and not args.no_paper_style:
@@ -988,6 +1017,7 @@ def main():
                                           "side stream under the blend", **stages_serial}} if stages_serial else {}),
             "roofline": roof,
             "path_roofline": path, "paper_style": paper, "library_sort": libsort, "masked_render": masked, "densify": densify, "backward": backward,
+            "first_frame": first_frame,
             "eager": eager, "graph_pipelined": graph_pipelined,
             "e2e_f32": e2e_f32, "e2e_u8": e2e_u8, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,

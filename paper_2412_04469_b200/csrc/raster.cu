@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
                 // Without the warp mask: conservative per-thread box cull (a pixel with p2 >= T2
                 // satisfies |dx| <= hx and |dy| <= hy, K7; this thread's rows are
                 // fyc +- hspan).  Skips never change a decision.
-                if (!COUNT && !WMASK && (fabsf(dx) > a.z || fabsf(a.y - fyc) > a.w + hspan)) continue;
+                // (A flag, not a `continue`: the warp votes below need every lane.)
+                const bool cull = !COUNT && !WMASK && (fabsf(dx) > a.z || fabsf(a.y - fyc) > a.w + hspan);
                 const float4 bq = QREC(sB);  // A2, B2, C2, T2
                 const float tAdx = (bq.x * dx) * dx;
                 const float tB = bq.y * dx;
@@ -239,23 +240,27 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
                 for (int k = 0; k < NP; ++k) {
                     const float2 dy = __fadd2_rn(vv, nfy[k]);  // v - y, exactly
                     qq[k] = __ffma2_rn(__ffma2_rn(cc, dy, tb2), dy, ta2);  // Horner in dy
-                    h[2 * k] = hit(p[k].T.x, qq[k].x, bq.w);
-                    h[2 * k + 1] = hit(p[k].T.y, qq[k].y, bq.w);
+                    h[2 * k] = !cull && hit(p[k].T.x, qq[k].x, bq.w);
+                    h[2 * k + 1] = !cull && hit(p[k].T.y, qq[k].y, bq.w);
                     anyh |= h[2 * k] | h[2 * k + 1];
                 }
                 if (COUNT) {
 #pragma unroll
                     for (int r = 0; r < RPT; ++r) cpn += (int)h[r];
                 }
-                if (anyh) {
-                    const float4 c = QREC(sC);  // o, r, g, b
-                    // BLEND_UNCOND: every row pair composites once any lane hits (a non-hitting
-                    // row gets alpha = +0, bit-identical); otherwise branch per row pair
-                    bool doit[NP];
+                // warp-uniform control flow from here: a row pair (16 x 4 band of the warp) is
+                // composited when any lane hits in it (PAIRSKIP); lanes without a hit in it
+                // composite alpha = +0, which leaves C and T bit-identical
+                bool doit[NP];
+                bool any_pair = false;
 #pragma unroll
-                    for (int k = 0; k < NP; ++k)
-                        doit[k] = BLEND_PAIRSKIP ? __any_sync(0xffffffffu, h[2 * k] | h[2 * k + 1])
-                                                 : (BLEND_UNCOND || (h[2 * k] | h[2 * k + 1]));
+                for (int k = 0; k < NP; ++k) {
+                    doit[k] = BLEND_PAIRSKIP ? __any_sync(0xffffffffu, h[2 * k] | h[2 * k + 1])
+                                             : __any_sync(0xffffffffu, anyh);
+                    any_pair |= doit[k];
+                }
+                if (any_pair) {
+                    const float4 c = QREC(sC);  // o, r, g, b
                     if (c.x > 0.98f) {
 #pragma unroll
                         for (int k = 0; k < NP; ++k)
