@@ -821,6 +821,8 @@ constexpr int EM_CAP = 8192;                // sort capacity: EM_E + a whole seg
 static_assert(EM_E + PC_CH <= EM_CAP, "an emit tile holds whole segments");
 constexpr int EM_THREADS = 512;
 constexpr int EM_WARPS = EM_THREADS / 32;
+constexpr int EM_SEGS = 2048;               // segments a tile sorts one by one (else: one bitonic sort)
+constexpr uint32_t EM_SMALL_SEG = 48;       // insertion-sorted by one thread (else: one bitonic sort)
 
 struct BucketGeo {
     int gx, gy, nbx, nby, NB, VNB;
@@ -969,15 +971,16 @@ __global__ void __launch_bounds__(PC_THREADS) k_piece_scatter(const uint32_t* __
 
 // bucket-local start of emit tile k of bucket b: the first (chunk, bucket) segment that starts
 // at or after k * EM_E (emit tiles hold whole segments), or the bucket total
-__device__ __forceinline__ uint32_t emit_start(const uint32_t* row, uint32_t nch, uint32_t total, uint32_t k) {
+// (also returns the chunk c whose segment starts there: off[c] = start, c = nch at the end)
+__device__ __forceinline__ uint32_t emit_start(const uint32_t* row, uint32_t nch, uint32_t total, uint32_t k,
+                                               uint32_t& chunk) {
     const uint32_t want = k * (uint32_t)EM_E;
-    if (want == 0) return 0u;
-    if (want >= total) return total;
     uint32_t lo = 0, hi = nch;  // first c with off[c] >= want (off[nch] := total)
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
         if (row[mid] >= want) hi = mid; else lo = mid + 1;
     }
+    chunk = lo;
     return lo < nch ? row[lo] : total;
 }
 
@@ -988,8 +991,8 @@ struct EmitSmem {
     uint32_t wpre[EM_WARPS][BK_T];        // per-warp exclusive prefix of a round
     int diff[(BK_H + 1) * (BK_W + 1)];    // 2D difference array of the tile's entry counts
     uint32_t base[BK_T];                  // final position of the tile's next entry
-    uint32_t w_s[EM_WARPS];
-    uint32_t tile, b, k, n, s0;
+    uint32_t segoff[EM_SEGS + 1];         // tile-local start of each (chunk, bucket) segment
+    uint32_t tile, b, k, n, s0, c0, nseg;
 };
 
 __global__ void __launch_bounds__(EM_THREADS) k_emit(const uint32_t* __restrict__ pieces,
@@ -1025,12 +1028,15 @@ __global__ void __launch_bounds__(EM_THREADS) k_emit(const uint32_t* __restrict_
                 const uint32_t k = t - ebase[lo];
                 const uint32_t tot = ptotal[lo];
                 const uint32_t* row = pcnt + (size_t)lo * g.CHS;
-                const uint32_t s0 = emit_start(row, nch, tot, k);
-                const uint32_t s1 = emit_start(row, nch, tot, k + 1);
+                uint32_t cA, cB;
+                const uint32_t s0 = emit_start(row, nch, tot, k, cA);
+                const uint32_t s1 = emit_start(row, nch, tot, k + 1, cB);
                 S.b = (uint32_t)lo;
                 S.k = k;
                 S.s0 = s0;
                 S.n = s1 - s0;
+                S.c0 = cA;
+                S.nseg = cB - cA;  // (chunk, bucket) segments in the tile (some empty)
             }
         }
         for (int q = threadIdx.x; q < (BK_H + 1) * (BK_W + 1); q += EM_THREADS) S.diff[q] = 0;
@@ -1044,13 +1050,42 @@ __global__ void __launch_bounds__(EM_THREADS) k_emit(const uint32_t* __restrict_
             if (threadIdx.x == 0) raise_flag(fl, FLAG_CAPACITY);
         }
         const uint32_t nn = min(n, (uint32_t)EM_CAP);
-        // load the tile's m values (pad with ~0 to the next power of two) and sort them
-        uint32_t np2 = 1;
-        while (np2 < nn) np2 <<= 1;
+        // load the tile's m values and sort them.  The tile is a run of whole (chunk, bucket)
+        // segments in chunk order -- already in m order ACROSS segments -- whose pieces are in
+        // arbitrary order inside; segments are short (a chunk's ~4096 pairs spread over all the
+        // buckets), so each thread insertion-sorts whole segments.  Tiles with a long segment or
+        // too many segments fall back to one bitonic sort of the tile.
         const uint32_t* src = pieces + pbase[b] + S.s0;
-        for (uint32_t q = threadIdx.x; q < np2; q += EM_THREADS) S.key[q] = q < nn ? __ldg(src + q) : 0xffffffffu;
+        for (uint32_t q = threadIdx.x; q < nn; q += EM_THREADS) S.key[q] = __ldg(src + q);
+        const uint32_t nseg = S.nseg;
+        bool bitonic = nseg > (uint32_t)EM_SEGS;
+        if (!bitonic) {
+            const uint32_t* row = pcnt + (size_t)b * g.CHS + S.c0;
+            for (uint32_t q = threadIdx.x; q < nseg; q += EM_THREADS) S.segoff[q] = row[q] - S.s0;
+            if (threadIdx.x == 0) S.segoff[nseg] = n;
+        }
         __syncthreads();
-        for (uint32_t kk = 2; kk <= np2; kk <<= 1) {
+        bool big = false;
+        if (!bitonic) {
+            for (uint32_t q = threadIdx.x; q < nseg; q += EM_THREADS) {
+                const uint32_t a = S.segoff[q], e = S.segoff[q + 1];
+                if (e - a > EM_SMALL_SEG) { big = true; continue; }
+                for (uint32_t x = a + 1; x < e; ++x) {  // insertion sort (unique keys)
+                    const uint32_t v = S.key[x];
+                    uint32_t y = x;
+                    while (y > a && S.key[y - 1] > v) { S.key[y] = S.key[y - 1]; --y; }
+                    S.key[y] = v;
+                }
+            }
+        }
+        bitonic = __syncthreads_or(bitonic || big) != 0;
+        uint32_t np2 = 1;
+        while (bitonic && np2 < nn) np2 <<= 1;
+        if (bitonic) {
+            for (uint32_t q = nn + threadIdx.x; q < np2; q += EM_THREADS) S.key[q] = 0xffffffffu;
+            __syncthreads();
+        }
+        for (uint32_t kk = 2; bitonic && kk <= np2; kk <<= 1) {
             for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
                 for (uint32_t i = threadIdx.x; i < np2; i += EM_THREADS) {
                     const uint32_t ixj = i ^ jj;

@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
         // output: 32-bit offset from the category's first row; the lane's column wraps into the
         // next row once every ~n/32 steps, at step tw (a rare, short branch)
         uint32_t off = k * (uint32_t)n_pad + i;
-        uint32_t tw = ((uint32_t)n - i + 31) / 32;
+        uint32_t tw = ((uint32_t)n - i + 31) / 32;  // step after which the column passes n
+        uint32_t t_i = 0;                           // step at which the lane was at column i
         for (uint32_t t = 0; t < mine; ++t) {
             const uint32_t w = sw[ptr];
             const uint32_t e = s_tab[x & (ANS_M - 1)];
@@ -194,9 +195,10 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
             ptr += need ? 1u : 0u;
             cout[off] = (int8_t)(e >> 24);
             off += 32;
-            if (t + 1 == tw) {  // column i + 32 tw >= n: continue in the next row
-                i = i + 32 * tw - (uint32_t)n;
+            if (t + 1 == tw) {  // column i + 32 (tw - t_i) >= n: continue in the next row
+                i = i + 32 * (tw - t_i) - (uint32_t)n;
                 off += (uint32_t)(n_pad - n);
+                t_i = tw;
                 tw += ((uint32_t)n - i + 31) / 32;
             }
         }
