@@ -895,11 +895,26 @@ __global__ void __launch_bounds__(256) k_piece_colscan(uint32_t* __restrict__ pc
     if (lane == 0) ptotal[b] = carry;
 }
 
+// bucket-local start of emit tile k of bucket b: the first (chunk, bucket) segment that starts
+// at or after k * EM_E (emit tiles hold whole segments), or the bucket total
+// (also returns the chunk c whose segment starts there: off[c] = start, c = nch at the end)
+__device__ __forceinline__ uint32_t emit_start(const uint32_t* row, uint32_t nch, uint32_t total, uint32_t k,
+                                               uint32_t& chunk) {
+    const uint32_t want = k * (uint32_t)EM_E;
+    uint32_t lo = 0, hi = nch;  // first c with off[c] >= want (off[nch] := total)
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (row[mid] >= want) hi = mid; else lo = mid + 1;
+    }
+    chunk = lo;
+    return lo < nch ? row[lo] : total;
+}
+
 // one block: bucket bases (exclusive scan of the totals) and emit-tile bases; meta[0] = pieces,
 // meta[1] = emit tiles
 __global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict__ ptotal, int VNB,
                                                      uint32_t* __restrict__ pbase, uint32_t* __restrict__ ebase,
-                                                     uint32_t* __restrict__ meta) {
+                                                     uint32_t* __restrict__ meta, uint32_t* __restrict__ ebucket) {
     __shared__ uint32_t s_w[32], s_e[32];
     __shared__ uint32_t s_carry, s_ecarry;
     if (threadIdx.x == 0) { s_carry = 0; s_ecarry = 0; }
@@ -938,6 +953,32 @@ __global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict_
         meta[0] = s_carry;
         meta[1] = s_ecarry;
     }
+    __syncthreads();
+    for (int b = threadIdx.x; b < VNB; b += blockDim.x) {  // each emit tile's bucket
+        const uint32_t e0 = ebase[b], et = (ptotal[b] + EM_E - 1) / EM_E;
+        for (uint32_t k = 0; k < et; ++k) ebucket[e0 + k] = (uint32_t)b;
+    }
+}
+
+// one thread per emit tile: its bucket, index k, pieces [s0, s0 + n) of the bucket, and its
+// chunk segments [c0, c0 + nseg) -- all the binary searches in flight at once, before k_emit
+__global__ void __launch_bounds__(256) k_emit_plan(const uint32_t* __restrict__ pcnt, const uint32_t* __restrict__ ptotal,
+                                                   const uint32_t* __restrict__ ebase,
+                                                   const uint32_t* __restrict__ ebucket,
+                                                   const uint32_t* __restrict__ meta, const uint32_t* __restrict__ Kd,
+                                                   BucketGeo g, uint4* __restrict__ plan) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= meta[1]) return;
+    const uint32_t nch = (visible_pairs(Kd) + PC_CH - 1) / PC_CH;
+    const uint32_t b = ebucket[t];
+    const uint32_t k = t - ebase[b];
+    const uint32_t tot = ptotal[b];
+    const uint32_t* row = pcnt + (size_t)b * g.CHS;
+    uint32_t cA, cB;
+    const uint32_t s0 = emit_start(row, nch, tot, k, cA);
+    const uint32_t s1 = emit_start(row, nch, tot, k + 1, cB);
+    plan[2 * (size_t)t] = make_uint4(b, k, s0, s1 - s0);
+    plan[2 * (size_t)t + 1] = make_uint4(cA, cB - cA, 0u, 0u);
 }
 
 __global__ void __launch_bounds__(PC_THREADS) k_piece_scatter(const uint32_t* __restrict__ dva,
@@ -969,21 +1010,6 @@ __global__ void __launch_bounds__(PC_THREADS) k_piece_scatter(const uint32_t* __
     }
 }
 
-// bucket-local start of emit tile k of bucket b: the first (chunk, bucket) segment that starts
-// at or after k * EM_E (emit tiles hold whole segments), or the bucket total
-// (also returns the chunk c whose segment starts there: off[c] = start, c = nch at the end)
-__device__ __forceinline__ uint32_t emit_start(const uint32_t* row, uint32_t nch, uint32_t total, uint32_t k,
-                                               uint32_t& chunk) {
-    const uint32_t want = k * (uint32_t)EM_E;
-    uint32_t lo = 0, hi = nch;  // first c with off[c] >= want (off[nch] := total)
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (row[mid] >= want) hi = mid; else lo = mid + 1;
-    }
-    chunk = lo;
-    return lo < nch ? row[lo] : total;
-}
-
 struct EmitSmem {
     uint32_t key[EM_CAP];                 // m values (sorted), then Gaussian indices
     uint16_t lr[EM_CAP];                  // piece rect inside the bucket: lx0 | lx1 << 4 | ly0 << 8 | ly1 << 11
@@ -997,9 +1023,8 @@ struct EmitSmem {
 
 __global__ void __launch_bounds__(EM_THREADS) k_emit(const uint32_t* __restrict__ pieces,
                                                      const uint32_t* __restrict__ pcnt,
-                                                     const uint32_t* __restrict__ ptotal,
+                                                     const uint4* __restrict__ plan,
                                                      const uint32_t* __restrict__ pbase,
-                                                     const uint32_t* __restrict__ ebase,
                                                      const uint32_t* __restrict__ meta,
                                                      const uint32_t* __restrict__ dva, const uint32_t* __restrict__ dvb,
                                                      const uint32_t* __restrict__ triv, const uint32_t* __restrict__ Kd,
@@ -1020,23 +1045,13 @@ __global__ void __launch_bounds__(EM_THREADS) k_emit(const uint32_t* __restrict_
             const uint32_t t = atomicAdd(ticket, 1u);
             S.tile = t;
             if (t < NE) {
-                int lo = 0, hi = g.VNB;  // bucket: last b with ebase[b] <= t
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (ebase[mid] <= t) lo = mid; else hi = mid;
-                }
-                const uint32_t k = t - ebase[lo];
-                const uint32_t tot = ptotal[lo];
-                const uint32_t* row = pcnt + (size_t)lo * g.CHS;
-                uint32_t cA, cB;
-                const uint32_t s0 = emit_start(row, nch, tot, k, cA);
-                const uint32_t s1 = emit_start(row, nch, tot, k + 1, cB);
-                S.b = (uint32_t)lo;
-                S.k = k;
-                S.s0 = s0;
-                S.n = s1 - s0;
-                S.c0 = cA;
-                S.nseg = cB - cA;  // (chunk, bucket) segments in the tile (some empty)
+                const uint4 a = plan[2 * (size_t)t], c = plan[2 * (size_t)t + 1];
+                S.b = a.x;
+                S.k = a.y;
+                S.s0 = a.z;
+                S.n = a.w;
+                S.c0 = c.x;
+                S.nseg = c.y;  // (chunk, bucket) segments in the tile (some empty)
             }
         }
         for (int q = threadIdx.x; q < (BK_H + 1) * (BK_W + 1); q += EM_THREADS) S.diff[q] = 0;
@@ -1391,9 +1406,12 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     uint32_t* ebase = pbase + bg.VNB;  // [VNB + 1]
     uint32_t* meta = ebase + bg.VNB + 1;
     uint32_t* emit_lb = reinterpret_cast<uint32_t*>(ws + L.emit_lb);
+    uint4* plan = reinterpret_cast<uint4*>(ws + L.eplan);                      // [etiles][2]
+    uint32_t* ebucket = nullptr;  // after the plans: [etiles] (set below)
     const int64_t chunks = (count + PC_CH - 1) / PC_CH;
     bg.CHS = (int)chunks;
     const int64_t etiles = ((int64_t)cap + EM_E - 1) / EM_E + bg.VNB + 1;
+    ebucket = reinterpret_cast<uint32_t*>(plan + 2 * (size_t)etiles);
     const size_t vsm = sizeof(uint32_t) * (size_t)bg.VNB;
     const uint32_t* dlast_in = dv[cur ^ 1];   // input of the last depth pass
     const uint32_t* dlast_out = dv[cur];      // its output (unless it was skipped)
@@ -1405,18 +1423,20 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     if (chunks > 0) {
         k_piece_count<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt);
         k_piece_colscan<<<(unsigned)((bg.VNB + 7) / 8), 256, 0, s>>>(pcnt, Kd, bg, ptotal);
-        k_piece_base<<<1, 1024, 0, s>>>(ptotal, bg.VNB, pbase, ebase, meta);
+        k_piece_base<<<1, 1024, 0, s>>>(ptotal, bg.VNB, pbase, ebase, meta, ebucket);
         k_piece_scatter<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, pbase,
                                                                   bins.keys_alt);
     }
     prof->end(s, chunks > 0 ? 5 : 1);
     prof->begin(ST_TILE_SORT, s);
     if (chunks > 0)
-        k_emit<<<emit_grid(), EM_THREADS, sizeof(EmitSmem), s>>>(bins.keys_alt, pcnt, ptotal, pbase, ebase, meta,
+        k_emit_plan<<<(unsigned)((etiles + 255) / 256), 256, 0, s>>>(pcnt, ptotal, ebase, ebucket, meta, Kd, bg, plan);
+    if (chunks > 0)
+        k_emit<<<emit_grid(), EM_THREADS, sizeof(EmitSmem), s>>>(bins.keys_alt, pcnt, plan, pbase, meta,
                                                                  dlast_in, dlast_out, triv, Kd, r4,
                                                                  reinterpret_cast<const uint2*>(bins.ranges), bg,
                                                                  bins.vals, emit_lb, &fl->tickets[TK_EMIT], fl);
-    prof->end(s, chunks > 0 ? 1 : 0);
+    prof->end(s, chunks > 0 ? 2 : 0);
     bins.sorted_in_alt = 0;
     return cudaGetLastError();
 #else

@@ -129,7 +129,7 @@ constexpr int ORDER_BINS = 64;
 struct WsLayout {
     // scratch (bin_sort)
     size_t flags, hist, dminmax, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, counts, view_tot, slab_counts,
-        slab_vis, select, pcnt, pbuck, emit_lb, order, total_scratch;
+        slab_vis, select, pcnt, pbuck, emit_lb, eplan, order, total_scratch;
     // render_views / render_mask buffers
     size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, mask_tmp, total;
     int64_t key_tiles, elem_tiles, os_key_tiles, os_elem_tiles, T, elems;
@@ -170,6 +170,7 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
         L.pbuck = o; o += align256(sizeof(uint32_t) * (size_t)(3 * vnb + 8));  // totals | bases | emit-tile bases | meta
         const int64_t etiles = (keys_cap + EM_E - 1) / EM_E + vnb + 1;
         L.emit_lb = o; o += align256(sizeof(uint32_t) * BK_T * (size_t)etiles);  // emit-tile look-back
+        L.eplan = o; o += align256(sizeof(uint32_t) * 9 * (size_t)etiles);       // emit-tile plans + buckets
     }
     L.order = o; o += align256(sizeof(uint32_t) * (2 * ORDER_BINS + (size_t)n_views * L.T));  // blend tile order
     L.total_scratch = o;
@@ -196,7 +197,8 @@ inline bool scratch_fits(const WsLayout& need, const WsLayout& have) {
                                    &WsLayout::dkeys_alt,  &WsLayout::dvals,       &WsLayout::dvals_alt,
                                    &WsLayout::counts,     &WsLayout::view_tot,    &WsLayout::slab_counts,
                                    &WsLayout::slab_vis,   &WsLayout::select,      &WsLayout::pcnt,
-                                   &WsLayout::pbuck,      &WsLayout::emit_lb,     &WsLayout::order,
+                                   &WsLayout::pbuck,      &WsLayout::emit_lb,     &WsLayout::eplan,
+                                   &WsLayout::order,
                                    &WsLayout::total_scratch};
     for (size_t q = 0; q + 1 < sizeof(r) / sizeof(r[0]); ++q)
         if (need.*r[q + 1] - need.*r[q] > have.*r[q + 1] - have.*r[q]) return false;
