@@ -28,6 +28,8 @@
 // progress for the look-back), rank keys with warp match_any multisplit in key order
 // (stable), publish per-digit tile counts, resolve global digit offsets by decoupled
 // look-back, stage the tile in shared memory in digit order and write it out coalesced.
+#include <algorithm>
+
 #include "queen_internal.cuh"
 
 namespace queen {
@@ -817,12 +819,12 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
 // ---------------------------------------------------------------------------
 constexpr int PC_THREADS = 512;             // PC_CH / 8 pairs per thread
 constexpr size_t PC_MAX_SMEM = 200 * 1024;  // per-chunk bucket counters: up to 51200 buckets per batch
-constexpr int EM_CAP = 8192;                // sort capacity: EM_E + a whole segment (< PC_CH), power of 2
+constexpr int PS_MAX_WARPS = 8;             // k_piece_scatter: chunks (warps) per CTA, fewer when VNB is large
+constexpr int EM_CAP = EM_E + PC_CH;         // pieces an emit tile can hold: EM_E + one whole segment
 static_assert(EM_E + PC_CH <= EM_CAP, "an emit tile holds whole segments");
 constexpr int EM_THREADS = 512;
 constexpr int EM_WARPS = EM_THREADS / 32;
-constexpr int EM_SEGS = 2048;               // segments a tile sorts one by one (else: one bitonic sort)
-constexpr uint32_t EM_SMALL_SEG = 48;       // insertion-sorted by one thread (else: one bitonic sort)
+
 
 struct BucketGeo {
     int gx, gy, nbx, nby, NB, VNB;
@@ -981,32 +983,74 @@ __global__ void __launch_bounds__(256) k_emit_plan(const uint32_t* __restrict__ 
     plan[2 * (size_t)t + 1] = make_uint4(cA, cB - cA, 0u, 0u);
 }
 
-__global__ void __launch_bounds__(PC_THREADS) k_piece_scatter(const uint32_t* __restrict__ dva,
-                                                              const uint32_t* __restrict__ dvb,
-                                                              const uint32_t* __restrict__ triv,
-                                                              const uint32_t* __restrict__ Kd,
-                                                              const short4* __restrict__ rect, BucketGeo g,
-                                                              const uint32_t* __restrict__ pcnt,
-                                                              const uint32_t* __restrict__ pbase,
-                                                              uint32_t* __restrict__ pieces) {
-    extern __shared__ uint32_t sc[];  // [VNB] cursors
+// One WARP per chunk, in m order (rounds of 32 pairs): a piece's position in its (chunk, bucket)
+// segment is the bucket's running cursor + the number of lower lanes with a piece in the same
+// bucket (per-warp shared-memory match words: each lane ORs its bit into the word of each of its
+// buckets -- a pair has at most one piece per bucket), so every segment comes out in m order and
+// the emission needs no sort.  The next round's pair index and rect are loaded one round ahead.
+__global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint32_t* __restrict__ dva,
+                                                                     const uint32_t* __restrict__ dvb,
+                                                                     const uint32_t* __restrict__ triv,
+                                                                     const uint32_t* __restrict__ Kd,
+                                                                     const short4* __restrict__ rect, BucketGeo g,
+                                                                     const uint32_t* __restrict__ pcnt,
+                                                                     const uint32_t* __restrict__ pbase,
+                                                                     uint32_t* __restrict__ pieces) {
+    extern __shared__ uint32_t ps_smem[];  // per warp: [VNB] cursors | [VNB] match words
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t M = visible_pairs(Kd);
-    const uint32_t c = blockIdx.x;
-    if ((uint64_t)c * PC_CH >= M) return;
+    const uint32_t c = blockIdx.x * (blockDim.x >> 5) + w;
+    if ((uint64_t)c * PC_CH >= M) return;  // warp-uniform
+    uint32_t* cur = ps_smem + (size_t)w * 2 * g.VNB;
+    uint32_t* wm = cur + g.VNB;
     const uint32_t* __restrict__ dvals = depth_order(dva, dvb, triv, Kd[1]);
-    for (int b = threadIdx.x; b < g.VNB; b += PC_THREADS) sc[b] = pbase[b] + pcnt[(size_t)b * g.CHS + c];
-    __syncthreads();
-#pragma unroll 2
-    for (int e = 0; e < PC_CH / PC_THREADS; ++e) {
-        const uint32_t m = c * PC_CH + e * PC_THREADS + threadIdx.x;
-        if (m < M) {
-            const uint32_t j = __ldg(dvals + m);
-            const short4 r = __ldg(rect + j);
-            const int vb = (int)(j / (uint32_t)g.n_pad) * g.NB;
-            const int bx0 = r.x / BK_W, bx1 = r.z / BK_W, by0 = r.y / BK_H, by1 = r.w / BK_H;
-            for (int by = by0; by <= by1; ++by)
-                for (int bx = bx0; bx <= bx1; ++bx) pieces[atomicAdd(&sc[vb + by * g.nbx + bx], 1u)] = m;
+    for (int b = lane; b < g.VNB; b += 32) {
+        cur[b] = pbase[b] + pcnt[(size_t)b * g.CHS + c];
+        wm[b] = 0u;
+    }
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t m0 = c * PC_CH;
+    const uint32_t mend = min(M, m0 + PC_CH);
+    const int rounds = (int)((mend - m0 + 31) / 32);
+    auto ldj = [&](int r) -> uint32_t {
+        const uint32_t m = m0 + (uint32_t)r * 32 + lane;
+        return (r < rounds && m < mend) ? __ldg(dvals + m) : 0xffffffffu;
+    };
+    uint32_t j_c = ldj(0), j_n = ldj(1);
+    short4 r_c = j_c != 0xffffffffu ? __ldg(rect + j_c) : make_short4(1, 1, 0, 0);
+    __syncwarp();
+    for (int r = 0; r < rounds; ++r) {
+        const uint32_t j_nn = ldj(r + 2);
+        const short4 r_n = j_n != 0xffffffffu ? __ldg(rect + j_n) : make_short4(1, 1, 0, 0);
+        const uint32_t m = m0 + (uint32_t)r * 32 + lane;
+        const bool has = j_c != 0xffffffffu;
+        int vb = 0, bx0 = 1, bx1 = 0, by0 = 1, by1 = 0;  // empty unless has
+        if (has) {
+            vb = (int)(j_c / (uint32_t)g.n_pad) * g.NB;
+            bx0 = r_c.x / BK_W; bx1 = r_c.z / BK_W; by0 = r_c.y / BK_H; by1 = r_c.w / BK_H;
         }
+        for (int by = by0; by <= by1; ++by)
+            for (int bx = bx0; bx <= bx1; ++bx) atomicOr(&wm[vb + by * g.nbx + bx], 1u << lane);
+        __syncwarp();
+        for (int by = by0; by <= by1; ++by)
+            for (int bx = bx0; bx <= bx1; ++bx) {
+                const int bk = vb + by * g.nbx + bx;
+                pieces[cur[bk] + __popc(wm[bk] & lt)] = m;
+            }
+        __syncwarp();
+        for (int by = by0; by <= by1; ++by)
+            for (int bx = bx0; bx <= bx1; ++bx) {
+                const int bk = vb + by * g.nbx + bx;
+                const uint32_t x = wm[bk];
+                if ((x & lt) == 0) {  // the bucket's lowest lane advances its cursor and clears its word
+                    cur[bk] += __popc(x);
+                    wm[bk] = 0u;
+                }
+            }
+        __syncwarp();
+        j_c = j_n;
+        r_c = r_n;
+        j_n = j_nn;
     }
 }
 
@@ -1017,7 +1061,6 @@ struct EmitSmem {
     uint32_t wpre[EM_WARPS][BK_T];        // per-warp exclusive prefix of a round
     int diff[(BK_H + 1) * (BK_W + 1)];    // 2D difference array of the tile's entry counts
     uint32_t base[BK_T];                  // final position of the tile's next entry
-    uint32_t segoff[EM_SEGS + 1];         // tile-local start of each (chunk, bucket) segment
     uint32_t tile, b, k, n, s0, c0, nseg;
 };
 
@@ -1065,54 +1108,11 @@ __global__ void __launch_bounds__(EM_THREADS) k_emit(const uint32_t* __restrict_
             if (threadIdx.x == 0) raise_flag(fl, FLAG_CAPACITY);
         }
         const uint32_t nn = min(n, (uint32_t)EM_CAP);
-        // load the tile's m values and sort them.  The tile is a run of whole (chunk, bucket)
-        // segments in chunk order -- already in m order ACROSS segments -- whose pieces are in
-        // arbitrary order inside; segments are short (a chunk's ~4096 pairs spread over all the
-        // buckets), so each thread insertion-sorts whole segments.  Tiles with a long segment or
-        // too many segments fall back to one bitonic sort of the tile.
+        // the tile's m values: a run of whole (chunk, bucket) segments in chunk order, each in m
+        // order (k_piece_scatter), so the tile is already sorted
         const uint32_t* src = pieces + pbase[b] + S.s0;
         for (uint32_t q = threadIdx.x; q < nn; q += EM_THREADS) S.key[q] = __ldg(src + q);
-        const uint32_t nseg = S.nseg;
-        bool bitonic = nseg > (uint32_t)EM_SEGS;
-        if (!bitonic) {
-            const uint32_t* row = pcnt + (size_t)b * g.CHS + S.c0;
-            for (uint32_t q = threadIdx.x; q < nseg; q += EM_THREADS) S.segoff[q] = row[q] - S.s0;
-            if (threadIdx.x == 0) S.segoff[nseg] = n;
-        }
         __syncthreads();
-        bool big = false;
-        if (!bitonic) {
-            for (uint32_t q = threadIdx.x; q < nseg; q += EM_THREADS) {
-                const uint32_t a = S.segoff[q], e = S.segoff[q + 1];
-                if (e - a > EM_SMALL_SEG) { big = true; continue; }
-                for (uint32_t x = a + 1; x < e; ++x) {  // insertion sort (unique keys)
-                    const uint32_t v = S.key[x];
-                    uint32_t y = x;
-                    while (y > a && S.key[y - 1] > v) { S.key[y] = S.key[y - 1]; --y; }
-                    S.key[y] = v;
-                }
-            }
-        }
-        bitonic = __syncthreads_or(bitonic || big) != 0;
-        uint32_t np2 = 1;
-        while (bitonic && np2 < nn) np2 <<= 1;
-        if (bitonic) {
-            for (uint32_t q = nn + threadIdx.x; q < np2; q += EM_THREADS) S.key[q] = 0xffffffffu;
-            __syncthreads();
-        }
-        for (uint32_t kk = 2; bitonic && kk <= np2; kk <<= 1) {
-            for (uint32_t jj = kk >> 1; jj > 0; jj >>= 1) {
-                for (uint32_t i = threadIdx.x; i < np2; i += EM_THREADS) {
-                    const uint32_t ixj = i ^ jj;
-                    if (ixj > i) {
-                        const uint32_t a = S.key[i], c = S.key[ixj];
-                        const bool up = (i & kk) == 0;
-                        if ((a > c) == up) { S.key[i] = c; S.key[ixj] = a; }
-                    }
-                }
-                __syncthreads();
-            }
-        }
         // pieces: Gaussian index (in place of m), rect inside the bucket, entry counts per tile
         const int v = b / g.NB;
         const int bl = b - v * g.NB;
@@ -1417,15 +1417,17 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     const uint32_t* dlast_out = dv[cur];      // its output (unless it was skipped)
     const uint32_t* triv = hist + (DEPTH_PASSES - 1) * MAX_BINS;
     const short4* r4 = reinterpret_cast<const short4*>(proj.rect);
-    if (vsm > PC_MAX_SMEM) return cudaErrorInvalidConfiguration;  // > 51200 buckets: not reachable (<= 64 4K views)
+    if (8 * (size_t)bg.VNB > PC_MAX_SMEM) return cudaErrorInvalidConfiguration;  // > 25600 buckets: not reachable (<= 64 4K views)
     prof->begin(ST_DUPLICATE, s);
     if ((e = cudaMemsetAsync(emit_lb, 0, sizeof(uint32_t) * BK_T * (size_t)etiles, s))) return e;
     if (chunks > 0) {
         k_piece_count<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt);
         k_piece_colscan<<<(unsigned)((bg.VNB + 7) / 8), 256, 0, s>>>(pcnt, Kd, bg, ptotal);
         k_piece_base<<<1, 1024, 0, s>>>(ptotal, bg.VNB, pbase, ebase, meta, ebucket);
-        k_piece_scatter<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, pbase,
-                                                                  bins.keys_alt);
+        // warps per CTA: each holds 2 x VNB words (cursors, match words)
+        const int wpc = (int)std::max<int64_t>(1, std::min<int64_t>(PS_MAX_WARPS, (int64_t)PC_MAX_SMEM / (8 * (int64_t)bg.VNB)));
+        k_piece_scatter<<<(unsigned)((chunks + wpc - 1) / wpc), 32 * wpc, (size_t)wpc * 8 * bg.VNB, s>>>(
+            dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, pbase, bins.keys_alt);
     }
     prof->end(s, chunks > 0 ? 5 : 1);
     prof->begin(ST_TILE_SORT, s);
