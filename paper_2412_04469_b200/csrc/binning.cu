@@ -819,11 +819,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
 // ---------------------------------------------------------------------------
 constexpr int PC_THREADS = 512;             // PC_CH / 8 pairs per thread
 constexpr size_t PC_MAX_SMEM = 200 * 1024;  // per-chunk bucket counters: up to 51200 buckets per batch
-constexpr int PS_MAX_WARPS = 8;             // k_piece_scatter: chunks (warps) per CTA, fewer when VNB is large
-constexpr int EM_CAP = EM_E + PC_CH;         // pieces an emit tile can hold: EM_E + one whole segment
-static_assert(EM_E + PC_CH <= EM_CAP, "an emit tile holds whole segments");
-constexpr int EM_THREADS = 512;
-constexpr int EM_WARPS = EM_THREADS / 32;
+constexpr int PS_MAX_WARPS = 4;             // k_piece_scatter: chunks (warps) per CTA, fewer when VNB is large
 
 
 struct BucketGeo {
@@ -987,7 +983,9 @@ __global__ void __launch_bounds__(256) k_emit_plan(const uint32_t* __restrict__ 
 // segment is the bucket's running cursor + the number of lower lanes with a piece in the same
 // bucket (per-warp shared-memory match words: each lane ORs its bit into the word of each of its
 // buckets -- a pair has at most one piece per bucket), so every segment comes out in m order and
-// the emission needs no sort.  The next round's pair index and rect are loaded one round ahead.
+// the emission needs no sort.  A piece is stored as its Gaussian index (piece_gi) and its rect
+// inside the bucket (piece_lr), so the emission streams them without gathers.  The next
+// rounds' pair indices and rects are loaded ahead.
 __global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint32_t* __restrict__ dva,
                                                                      const uint32_t* __restrict__ dvb,
                                                                      const uint32_t* __restrict__ triv,
@@ -995,7 +993,8 @@ __global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint3
                                                                      const short4* __restrict__ rect, BucketGeo g,
                                                                      const uint32_t* __restrict__ pcnt,
                                                                      const uint32_t* __restrict__ pbase,
-                                                                     uint32_t* __restrict__ pieces) {
+                                                                     uint32_t* __restrict__ piece_gi,
+                                                                     uint32_t* __restrict__ piece_lr) {
     extern __shared__ uint32_t ps_smem[];  // per warp: [VNB] cursors | [VNB] match words
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t M = visible_pairs(Kd);
@@ -1022,7 +1021,6 @@ __global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint3
     for (int r = 0; r < rounds; ++r) {
         const uint32_t j_nn = ldj(r + 2);
         const short4 r_n = j_n != 0xffffffffu ? __ldg(rect + j_n) : make_short4(1, 1, 0, 0);
-        const uint32_t m = m0 + (uint32_t)r * 32 + lane;
         const bool has = j_c != 0xffffffffu;
         int vb = 0, bx0 = 1, bx1 = 0, by0 = 1, by1 = 0;  // empty unless has
         if (has) {
@@ -1032,10 +1030,17 @@ __global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint3
         for (int by = by0; by <= by1; ++by)
             for (int bx = bx0; bx <= bx1; ++bx) atomicOr(&wm[vb + by * g.nbx + bx], 1u << lane);
         __syncwarp();
+        const uint32_t gi = has ? j_c - (uint32_t)(vb / g.NB) * (uint32_t)g.n_pad : 0u;
         for (int by = by0; by <= by1; ++by)
             for (int bx = bx0; bx <= bx1; ++bx) {
                 const int bk = vb + by * g.nbx + bx;
-                pieces[cur[bk] + __popc(wm[bk] & lt)] = m;
+                const uint32_t pos = cur[bk] + __popc(wm[bk] & lt);
+                // the piece: Gaussian index and its rect inside the bucket (lx0 | lx1 << 4 | ly0 << 8 | ly1 << 11)
+                const int tx0b = bx * BK_W, ty0b = by * BK_H;
+                const int lx0 = max((int)r_c.x - tx0b, 0), lx1 = min((int)r_c.z - tx0b, BK_W - 1);
+                const int ly0 = max((int)r_c.y - ty0b, 0), ly1 = min((int)r_c.w - ty0b, BK_H - 1);
+                piece_gi[pos] = gi;
+                piece_lr[pos] = (uint32_t)(lx0 | (lx1 << 4) | (ly0 << 8) | (ly1 << 11));
             }
         __syncwarp();
         for (int by = by0; by <= by1; ++by)
@@ -1054,104 +1059,89 @@ __global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint3
     }
 }
 
-struct EmitSmem {
-    uint32_t key[EM_CAP];                 // m values (sorted), then Gaussian indices
-    uint16_t lr[EM_CAP];                  // piece rect inside the bucket: lx0 | lx1 << 4 | ly0 << 8 | ly1 << 11
-    uint32_t wm[EM_WARPS][BK_T];          // per-warp match words of a round
-    uint32_t wpre[EM_WARPS][BK_T];        // per-warp exclusive prefix of a round
-    int diff[(BK_H + 1) * (BK_W + 1)];    // 2D difference array of the tile's entry counts
-    uint32_t base[BK_T];                  // final position of the tile's next entry
-    uint32_t tile, b, k, n, s0, c0, nseg;
+// Emission, one WARP per emit tile (its pieces: whole (chunk, bucket) segments in m order,
+// streamed from piece_gi / piece_lr; no sort, no block barriers):
+//   pass 1  entry counts per bucket tile (2D difference array over the 16 x 8 tiles);
+//   then    each tile's offset among the bucket's earlier emit tiles by decoupled look-back
+//           (4 tiles per lane), base = ranges[gt].first + offset;
+//   pass 2  the entries, flattened 32 at a time in (piece, row, column) order: lane i takes entry
+//           e0 + i, finds its piece among the round's 32 by one redux.or over the piece starts,
+//           and ranks it among the chunk's entries of the same tile by match words (lower lanes
+//           = earlier pieces), so each tile's entries are written in m order.
+constexpr int EW_WARPS = 4;  // independent emit workers per CTA
+struct EwSmem {
+    int diff[(BK_H + 1) * (BK_W + 1)];
+    uint32_t base[BK_T];   // final position of each bucket tile's next entry
+    uint32_t wm[BK_T];     // match words of the current 32-entry chunk
+    uint32_t pstart[33];   // entry offsets of the round's 32 pieces (+ total)
+    uint32_t pgi[32], plr[32];
 };
 
-__global__ void __launch_bounds__(EM_THREADS) k_emit(const uint32_t* __restrict__ pieces,
-                                                     const uint32_t* __restrict__ pcnt,
-                                                     const uint4* __restrict__ plan,
-                                                     const uint32_t* __restrict__ pbase,
-                                                     const uint32_t* __restrict__ meta,
-                                                     const uint32_t* __restrict__ dva, const uint32_t* __restrict__ dvb,
-                                                     const uint32_t* __restrict__ triv, const uint32_t* __restrict__ Kd,
-                                                     const short4* __restrict__ rect, const uint2* __restrict__ ranges,
-                                                     BucketGeo g, uint32_t* __restrict__ vals, uint32_t* lb,
-                                                     uint32_t* ticket, DevFlags* fl) {
-    extern __shared__ __align__(16) unsigned char em_smem[];
-    EmitSmem& S = *reinterpret_cast<EmitSmem*>(em_smem);
-    const uint32_t M = visible_pairs(Kd);
-    if (M == 0) return;
+__global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restrict__ piece_gi,
+                                                        const uint32_t* __restrict__ piece_lr,
+                                                        const uint4* __restrict__ plan,
+                                                        const uint32_t* __restrict__ pbase,
+                                                        const uint32_t* __restrict__ meta,
+                                                        const uint32_t* __restrict__ Kd,
+                                                        const uint2* __restrict__ ranges, BucketGeo g,
+                                                        uint32_t* __restrict__ vals, uint32_t* lb, uint32_t* ticket,
+                                                        DevFlags* fl) {
+    __shared__ EwSmem sm[EW_WARPS];
+    const int lane = threadIdx.x & 31;
+    EwSmem& S = sm[threadIdx.x >> 5];
+    if (visible_pairs(Kd) == 0) return;
     const uint32_t NE = meta[1];
-    const uint32_t nch = (M + PC_CH - 1) / PC_CH;
-    const uint32_t* __restrict__ dvals = depth_order(dva, dvb, triv, Kd[1]);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    const uint32_t le_mask = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;
     for (;;) {
-        if (threadIdx.x == 0) {
-            const uint32_t t = atomicAdd(ticket, 1u);
-            S.tile = t;
-            if (t < NE) {
-                const uint4 a = plan[2 * (size_t)t], c = plan[2 * (size_t)t + 1];
-                S.b = a.x;
-                S.k = a.y;
-                S.s0 = a.z;
-                S.n = a.w;
-                S.c0 = c.x;
-                S.nseg = c.y;  // (chunk, bucket) segments in the tile (some empty)
-            }
-        }
-        for (int q = threadIdx.x; q < (BK_H + 1) * (BK_W + 1); q += EM_THREADS) S.diff[q] = 0;
-        for (int q = threadIdx.x; q < EM_WARPS * BK_T; q += EM_THREADS) (&S.wm[0][0])[q] = 0u;
-        __syncthreads();
-        const uint32_t et = S.tile;
-        if (et >= NE) break;
-        const int b = (int)S.b;
-        const uint32_t n = S.n, k = S.k;
-        if (n > (uint32_t)EM_CAP) {  // cannot happen (EM_E + a segment < EM_CAP); guard the smem
-            if (threadIdx.x == 0) raise_flag(fl, FLAG_CAPACITY);
-        }
-        const uint32_t nn = min(n, (uint32_t)EM_CAP);
-        // the tile's m values: a run of whole (chunk, bucket) segments in chunk order, each in m
-        // order (k_piece_scatter), so the tile is already sorted
-        const uint32_t* src = pieces + pbase[b] + S.s0;
-        for (uint32_t q = threadIdx.x; q < nn; q += EM_THREADS) S.key[q] = __ldg(src + q);
-        __syncthreads();
-        // pieces: Gaussian index (in place of m), rect inside the bucket, entry counts per tile
-        const int v = b / g.NB;
-        const int bl = b - v * g.NB;
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(ticket, 1u);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= NE) break;
+        const uint4 pa = plan[2 * (size_t)t];
+        const uint32_t b = pa.x, k = pa.y, s0 = pa.z, n = pa.w;
+        const int v = (int)b / g.NB;
+        const int bl = (int)b - v * g.NB;
         const int by = bl / g.nbx, bx = bl - by * g.nbx;
         const int tx0b = bx * BK_W, ty0b = by * BK_H;
-        for (uint32_t q = threadIdx.x; q < nn; q += EM_THREADS) {
-            const uint32_t j = __ldg(dvals + S.key[q]);
-            const short4 r = __ldg(rect + j);
-            const int lx0 = max((int)r.x - tx0b, 0), lx1 = min((int)r.z - tx0b, BK_W - 1);
-            const int ly0 = max((int)r.y - ty0b, 0), ly1 = min((int)r.w - ty0b, BK_H - 1);
-            S.key[q] = j - (uint32_t)v * (uint32_t)g.n_pad;
-            S.lr[q] = (uint16_t)(lx0 | (lx1 << 4) | (ly0 << 8) | (ly1 << 11));
+        const uint32_t* __restrict__ lrp = piece_lr + pbase[b] + s0;
+        const uint32_t* __restrict__ gip = piece_gi + pbase[b] + s0;
+        for (int q = lane; q < (BK_H + 1) * (BK_W + 1); q += 32) S.diff[q] = 0;
+        __syncwarp();
+        // pass 1: entries per bucket tile
+        for (uint32_t q = lane; q < n; q += 32) {
+            const uint32_t lr = __ldg(lrp + q);
+            const int lx0 = lr & 15, lx1 = (lr >> 4) & 15, ly0 = (lr >> 8) & 7, ly1 = (lr >> 11) & 7;
             atomicAdd(&S.diff[ly0 * (BK_W + 1) + lx0], 1);
             atomicAdd(&S.diff[ly0 * (BK_W + 1) + lx1 + 1], -1);
             atomicAdd(&S.diff[(ly1 + 1) * (BK_W + 1) + lx0], -1);
             atomicAdd(&S.diff[(ly1 + 1) * (BK_W + 1) + lx1 + 1], 1);
         }
-        __syncthreads();
-        if (threadIdx.x < BK_H) {  // prefix along x
+        __syncwarp();
+        if (lane < BK_H) {
             int run = 0;
-            for (int x = 0; x < BK_W; ++x) { run += S.diff[threadIdx.x * (BK_W + 1) + x]; S.diff[threadIdx.x * (BK_W + 1) + x] = run; }
+            for (int x = 0; x < BK_W; ++x) { run += S.diff[lane * (BK_W + 1) + x]; S.diff[lane * (BK_W + 1) + x] = run; }
         }
-        __syncthreads();
-        if (threadIdx.x < BK_W) {  // prefix along y
+        __syncwarp();
+        if (lane < BK_W) {
             int run = 0;
-            for (int y = 0; y < BK_H; ++y) { run += S.diff[y * (BK_W + 1) + threadIdx.x]; S.diff[y * (BK_W + 1) + threadIdx.x] = run; }
+            for (int y = 0; y < BK_H; ++y) { run += S.diff[y * (BK_W + 1) + lane]; S.diff[y * (BK_W + 1) + lane] = run; }
         }
-        __syncthreads();
-        // each tile's offset among the bucket's earlier emit tiles: decoupled look-back
-        if (threadIdx.x < BK_T) {
-            const int lt = threadIdx.x, ly = lt / BK_W, lx = lt - ly * BK_W;
-            const uint32_t cnt = (uint32_t)S.diff[ly * (BK_W + 1) + lx];
-            uint32_t* my = lb + (size_t)et * BK_T + lt;
-            uint32_t prefix = 0;
-            if (k == 0) {
-                st_volatile_u32(my, LB_INC | cnt);
-            } else {
-                st_volatile_u32(my, LB_AGG | cnt);
-                int64_t look = (int64_t)et - 1;
+        __syncwarp();
+        // look-back: tile lt = lane + 32 i (4 per lane); publish all four first
+        uint32_t cnt[BK_T / 32], prefix[BK_T / 32];
+#pragma unroll
+        for (int i = 0; i < BK_T / 32; ++i) {
+            const int lt = lane + 32 * i, ly = lt / BK_W, lx = lt - ly * BK_W;
+            cnt[i] = (uint32_t)S.diff[ly * (BK_W + 1) + lx];
+            prefix[i] = 0;
+            st_volatile_u32(lb + (size_t)t * BK_T + lt, (k == 0 ? LB_INC : LB_AGG) | cnt[i]);
+        }
+        if (k > 0) {
+#pragma unroll
+            for (int i = 0; i < BK_T / 32; ++i) {
+                const int lt = lane + 32 * i;
+                int64_t look = (int64_t)t - 1;
                 long long spins = 0;
                 for (;;) {
                     const uint32_t x = ld_volatile_u32(lb + (size_t)look * BK_T + lt);
@@ -1160,48 +1150,79 @@ __global__ void __launch_bounds__(EM_THREADS) k_emit(const uint32_t* __restrict_
                         if (++spins > SPIN_LIMIT) { raise_flag(fl, FLAG_TIMEOUT); break; }
                         continue;
                     }
-                    prefix += x & LB_MASK;
+                    prefix[i] += x & LB_MASK;
                     if (f == 2) break;
                     --look;
                 }
-                st_volatile_u32(my, LB_INC | (prefix + cnt));
+                st_volatile_u32(lb + (size_t)t * BK_T + lt, LB_INC | (prefix[i] + cnt[i]));
             }
+        }
+#pragma unroll
+        for (int i = 0; i < BK_T / 32; ++i) {
+            const int lt = lane + 32 * i, ly = lt / BK_W, lx = lt - ly * BK_W;
             const int ty = ty0b + ly, tx = tx0b + lx;
             const uint32_t gt = (uint32_t)v * (uint32_t)g.T + (uint32_t)(ty * g.gx + tx);
-            S.base[lt] = (tx < g.gx && ty < g.gy) ? ranges[gt].x + prefix : 0u;
+            S.base[lt] = (tx < g.gx && ty < g.gy) ? __ldg(&ranges[gt].x) + prefix[i] : 0u;
+            S.wm[lt] = 0u;
         }
-        __syncthreads();
-        // rounds of EM_THREADS pieces in m order: stable ranks per tile (warp match words)
-        for (uint32_t q0 = 0; q0 < nn; q0 += EM_THREADS) {
-            const uint32_t q = q0 + threadIdx.x;
-            const bool has = q < nn;
-            const uint32_t lr = has ? S.lr[q] : 0u;
-            const int lx0 = lr & 15, lx1 = (lr >> 4) & 15, ly0 = (lr >> 8) & 7, ly1 = (lr >> 11) & 7;
-            if (has)
-                for (int ly = ly0; ly <= ly1; ++ly)
-                    for (int lx = lx0; lx <= lx1; ++lx) atomicOr(&S.wm[w][ly * BK_W + lx], 1u << lane);
-            __syncthreads();
-            if (threadIdx.x < BK_T) {
-                uint32_t run = S.base[threadIdx.x];
+        __syncwarp();
+        // pass 2: the entries in (piece, row, column) order, 32 per step
+        for (uint32_t q0 = 0; q0 < n; q0 += 32) {
+            const uint32_t q = q0 + lane;
+            const bool has = q < n;
+            const uint32_t lr = has ? __ldg(lrp + q) : 0u;
+            const uint32_t gi = has ? __ldg(gip + q) : 0u;
+            const uint32_t ne = has ? (((lr >> 4) & 15) - (lr & 15) + 1) * (((lr >> 11) & 7) - ((lr >> 8) & 7) + 1) : 0u;
+            uint32_t incl = ne;
 #pragma unroll
-                for (int ww = 0; ww < EM_WARPS; ++ww) {
-                    S.wpre[ww][threadIdx.x] = run;
-                    run += __popc(S.wm[ww][threadIdx.x]);
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t E = __shfl_sync(0xffffffffu, incl, 31);
+            S.pstart[lane] = incl - ne;
+            S.plr[lane] = lr;
+            S.pgi[lane] = gi;
+            if (lane == 31) S.pstart[32] = E;
+            __syncwarp();
+            int pp = 0;  // piece of entry e0 (lanes agree); every piece of the round has >= 1 entry
+            for (uint32_t e0 = 0; e0 < E; e0 += 32) {
+                const uint32_t e = e0 + lane;
+                const int cand = pp + lane + 1;
+                const uint32_t st = cand <= 32 ? S.pstart[cand] : 0xffffffffu;
+                const uint32_t d = st - e0;  // start of piece cand relative to e0
+                const uint32_t bit = (st > e0 && d < 32u) ? (1u << d) : 0u;
+                const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
+                const int p = pp + __popc(starts & le_mask);
+                const bool valid = e < E;
+                int lt = 0;
+                uint32_t gpi = 0;
+                if (valid) {
+                    const uint32_t plr = S.plr[p];
+                    const uint32_t lx0 = plr & 15, lx1 = (plr >> 4) & 15, ly0 = (plr >> 8) & 7;
+                    const uint32_t wdt = lx1 - lx0 + 1;
+                    const uint32_t o = e - S.pstart[p];
+                    const uint32_t row = (o * ((65536u + wdt - 1) / wdt)) >> 16;  // exact: o < 128
+                    lt = (int)((ly0 + row) * BK_W + lx0 + (o - row * wdt));
+                    gpi = S.pgi[p];
+                    atomicOr(&S.wm[lt], 1u << lane);
                 }
-                S.base[threadIdx.x] = run;
+                __syncwarp();
+                uint32_t x = 0;
+                if (valid) {
+                    x = S.wm[lt];
+                    vals[S.base[lt] + __popc(x & lt_mask)] = gpi;
+                }
+                __syncwarp();
+                if (valid && (x & lt_mask) == 0) {  // lowest lane of the tile: advance, clear
+                    S.base[lt] += __popc(x);
+                    S.wm[lt] = 0u;
+                }
+                __syncwarp();
+                const int p31 = __shfl_sync(0xffffffffu, p, 31);
+                pp = p31 + ((p31 + 1 <= 32 && S.pstart[p31 + 1] == e0 + 32) ? 1 : 0);
             }
-            __syncthreads();
-            if (has) {
-                const uint32_t gi = S.key[q];
-                for (int ly = ly0; ly <= ly1; ++ly)
-                    for (int lx = lx0; lx <= lx1; ++lx) {
-                        const int lt = ly * BK_W + lx;
-                        vals[S.wpre[w][lt] + __popc(S.wm[w][lt] & lt_mask)] = gi;
-                    }
-            }
-            __syncthreads();
-            for (int qq = threadIdx.x; qq < EM_WARPS * BK_T; qq += EM_THREADS) (&S.wm[0][0])[qq] = 0u;
-            __syncthreads();
+            __syncwarp();
         }
     }
 }
@@ -1260,7 +1281,7 @@ static cudaError_t onesweep_attr() {
 static int emit_grid() {
     static int occ = 0;
     if (!occ) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, EM_THREADS, sizeof(EmitSmem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_emit, EW_WARPS * 32, 0);
         if (occ <= 0) occ = 1;
     }
     return occ * num_sms();
@@ -1268,8 +1289,7 @@ static int emit_grid() {
 
 cudaError_t init_binning_attributes() {
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EmitSmem))) ||
-        (e = cudaFuncSetAttribute(k_piece_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC_MAX_SMEM)) ||
+    if ((e = cudaFuncSetAttribute(k_piece_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC_MAX_SMEM)) ||
         (e = cudaFuncSetAttribute(k_piece_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC_MAX_SMEM)))
         return e;
     if ((e = onesweep_attr<8, OS_KV>()) || (e = onesweep_attr<8, OS_PACK>()) || (e = onesweep_attr<8, OS_PACKED>()) ||
@@ -1427,17 +1447,16 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
         // warps per CTA: each holds 2 x VNB words (cursors, match words)
         const int wpc = (int)std::max<int64_t>(1, std::min<int64_t>(PS_MAX_WARPS, (int64_t)PC_MAX_SMEM / (8 * (int64_t)bg.VNB)));
         k_piece_scatter<<<(unsigned)((chunks + wpc - 1) / wpc), 32 * wpc, (size_t)wpc * 8 * bg.VNB, s>>>(
-            dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, pbase, bins.keys_alt);
+            dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, pbase, bins.keys_alt, bins.keys);
     }
     prof->end(s, chunks > 0 ? 5 : 1);
     prof->begin(ST_TILE_SORT, s);
     if (chunks > 0)
         k_emit_plan<<<(unsigned)((etiles + 255) / 256), 256, 0, s>>>(pcnt, ptotal, ebase, ebucket, meta, Kd, bg, plan);
     if (chunks > 0)
-        k_emit<<<emit_grid(), EM_THREADS, sizeof(EmitSmem), s>>>(bins.keys_alt, pcnt, plan, pbase, meta,
-                                                                 dlast_in, dlast_out, triv, Kd, r4,
-                                                                 reinterpret_cast<const uint2*>(bins.ranges), bg,
-                                                                 bins.vals, emit_lb, &fl->tickets[TK_EMIT], fl);
+        k_emit<<<emit_grid(), EW_WARPS * 32, 0, s>>>(bins.keys_alt, bins.keys, plan, pbase, meta, Kd,
+                                                     reinterpret_cast<const uint2*>(bins.ranges), bg, bins.vals,
+                                                     emit_lb, &fl->tickets[TK_EMIT], fl);
     prof->end(s, chunks > 0 ? 2 : 0);
     bins.sorted_in_alt = 0;
     return cudaGetLastError();

@@ -113,7 +113,7 @@ inline BinPlan bin_plan(int64_t n_pad, int64_t n_views, int W, int H) {
 
 // Bucketed emission (binning.cu K4'/K5'): buckets of BK_W x BK_H tiles of one view; the
 // depth-ordered pairs are counted and scattered in chunks of PC_CH; emit tiles hold ~EM_E pieces.
-constexpr int PC_CH = 4096;
+constexpr int PC_CH = 2048;
 constexpr int BK_W = 16, BK_H = 8, BK_T = BK_W * BK_H;
 constexpr int EM_E = 2048;
 inline int64_t buckets_per_view(int W, int H) {
