@@ -1015,47 +1015,62 @@ __global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint3
         const uint32_t m = m0 + (uint32_t)r * 32 + lane;
         return (r < rounds && m < mend) ? __ldg(dvals + m) : 0xffffffffu;
     };
-    uint32_t j_c = ldj(0), j_n = ldj(1);
-    short4 r_c = j_c != 0xffffffffu ? __ldg(rect + j_c) : make_short4(1, 1, 0, 0);
+    auto ldr = [&](uint32_t j) -> short4 { return j != 0xffffffffu ? __ldg(rect + j) : make_short4(1, 1, 0, 0); };
+    // rounds in groups of PSG: pair indices are loaded two groups ahead, rects one group ahead
+    constexpr int PSG = 4;
+    uint32_t jc[PSG], jn[PSG];
+    short4 rc[PSG];
+#pragma unroll
+    for (int u = 0; u < PSG; ++u) { jc[u] = ldj(u); jn[u] = ldj(PSG + u); }
+#pragma unroll
+    for (int u = 0; u < PSG; ++u) rc[u] = ldr(jc[u]);
     __syncwarp();
-    for (int r = 0; r < rounds; ++r) {
-        const uint32_t j_nn = ldj(r + 2);
-        const short4 r_n = j_n != 0xffffffffu ? __ldg(rect + j_n) : make_short4(1, 1, 0, 0);
-        const bool has = j_c != 0xffffffffu;
-        int vb = 0, bx0 = 1, bx1 = 0, by0 = 1, by1 = 0;  // empty unless has
-        if (has) {
-            vb = (int)(j_c / (uint32_t)g.n_pad) * g.NB;
-            bx0 = r_c.x / BK_W; bx1 = r_c.z / BK_W; by0 = r_c.y / BK_H; by1 = r_c.w / BK_H;
-        }
-        for (int by = by0; by <= by1; ++by)
-            for (int bx = bx0; bx <= bx1; ++bx) atomicOr(&wm[vb + by * g.nbx + bx], 1u << lane);
-        __syncwarp();
-        const uint32_t gi = has ? j_c - (uint32_t)(vb / g.NB) * (uint32_t)g.n_pad : 0u;
-        for (int by = by0; by <= by1; ++by)
-            for (int bx = bx0; bx <= bx1; ++bx) {
-                const int bk = vb + by * g.nbx + bx;
-                const uint32_t pos = cur[bk] + __popc(wm[bk] & lt);
-                // the piece: Gaussian index and its rect inside the bucket (lx0 | lx1 << 4 | ly0 << 8 | ly1 << 11)
-                const int tx0b = bx * BK_W, ty0b = by * BK_H;
-                const int lx0 = max((int)r_c.x - tx0b, 0), lx1 = min((int)r_c.z - tx0b, BK_W - 1);
-                const int ly0 = max((int)r_c.y - ty0b, 0), ly1 = min((int)r_c.w - ty0b, BK_H - 1);
-                piece_gi[pos] = gi;
-                piece_lr[pos] = (uint32_t)(lx0 | (lx1 << 4) | (ly0 << 8) | (ly1 << 11));
+    for (int r0 = 0; r0 < rounds; r0 += PSG) {
+        uint32_t jnn[PSG];
+        short4 rn[PSG];
+#pragma unroll
+        for (int u = 0; u < PSG; ++u) jnn[u] = ldj(r0 + 2 * PSG + u);
+#pragma unroll
+        for (int u = 0; u < PSG; ++u) rn[u] = ldr(jn[u]);
+#pragma unroll
+        for (int u = 0; u < PSG; ++u) {
+            const uint32_t j_c = jc[u];
+            const short4 r_c = rc[u];
+            const bool has = j_c != 0xffffffffu;
+            int vb = 0, bx0 = 1, bx1 = 0, by0 = 1, by1 = 0;  // empty unless has
+            if (has) {
+                vb = (int)(j_c / (uint32_t)g.n_pad) * g.NB;
+                bx0 = r_c.x / BK_W; bx1 = r_c.z / BK_W; by0 = r_c.y / BK_H; by1 = r_c.w / BK_H;
             }
-        __syncwarp();
-        for (int by = by0; by <= by1; ++by)
-            for (int bx = bx0; bx <= bx1; ++bx) {
-                const int bk = vb + by * g.nbx + bx;
-                const uint32_t x = wm[bk];
-                if ((x & lt) == 0) {  // the bucket's lowest lane advances its cursor and clears its word
-                    cur[bk] += __popc(x);
-                    wm[bk] = 0u;
+            for (int by = by0; by <= by1; ++by)
+                for (int bx = bx0; bx <= bx1; ++bx) atomicOr(&wm[vb + by * g.nbx + bx], 1u << lane);
+            __syncwarp();
+            const uint32_t gi = has ? j_c - (uint32_t)(vb / g.NB) * (uint32_t)g.n_pad : 0u;
+            for (int by = by0; by <= by1; ++by)
+                for (int bx = bx0; bx <= bx1; ++bx) {
+                    const int bk = vb + by * g.nbx + bx;
+                    const uint32_t pos = cur[bk] + __popc(wm[bk] & lt);
+                    // the piece: Gaussian index and its rect inside the bucket (lx0 | lx1 << 4 | ly0 << 8 | ly1 << 11)
+                    const int tx0b = bx * BK_W, ty0b = by * BK_H;
+                    const int lx0 = max((int)r_c.x - tx0b, 0), lx1 = min((int)r_c.z - tx0b, BK_W - 1);
+                    const int ly0 = max((int)r_c.y - ty0b, 0), ly1 = min((int)r_c.w - ty0b, BK_H - 1);
+                    piece_gi[pos] = gi;
+                    piece_lr[pos] = (uint32_t)(lx0 | (lx1 << 4) | (ly0 << 8) | (ly1 << 11));
                 }
-            }
-        __syncwarp();
-        j_c = j_n;
-        r_c = r_n;
-        j_n = j_nn;
+            __syncwarp();
+            for (int by = by0; by <= by1; ++by)
+                for (int bx = bx0; bx <= bx1; ++bx) {
+                    const int bk = vb + by * g.nbx + bx;
+                    const uint32_t x = wm[bk];
+                    if ((x & lt) == 0) {  // the bucket's lowest lane advances its cursor and clears its word
+                        cur[bk] += __popc(x);
+                        wm[bk] = 0u;
+                    }
+                }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int u = 0; u < PSG; ++u) { jc[u] = jn[u]; rc[u] = rn[u]; jn[u] = jnn[u]; }
     }
 }
 
@@ -1087,6 +1102,9 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                                                         uint32_t* __restrict__ vals, uint32_t* lb, uint32_t* ticket,
                                                         DevFlags* fl) {
     __shared__ EwSmem sm[EW_WARPS];
+    __shared__ uint32_t s_rcp[BK_W + 1];  // ceil(2^16 / w): row = (o * s_rcp[w]) >> 16 = o / w for o < 128
+    if (threadIdx.x <= BK_W) s_rcp[threadIdx.x] = threadIdx.x ? (65536u + threadIdx.x - 1) / threadIdx.x : 0u;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     EwSmem& S = sm[threadIdx.x >> 5];
     if (visible_pairs(Kd) == 0) return;
@@ -1109,13 +1127,23 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
         for (int q = lane; q < (BK_H + 1) * (BK_W + 1); q += 32) S.diff[q] = 0;
         __syncwarp();
         // pass 1: entries per bucket tile
-        for (uint32_t q = lane; q < n; q += 32) {
-            const uint32_t lr = __ldg(lrp + q);
-            const int lx0 = lr & 15, lx1 = (lr >> 4) & 15, ly0 = (lr >> 8) & 7, ly1 = (lr >> 11) & 7;
-            atomicAdd(&S.diff[ly0 * (BK_W + 1) + lx0], 1);
-            atomicAdd(&S.diff[ly0 * (BK_W + 1) + lx1 + 1], -1);
-            atomicAdd(&S.diff[(ly1 + 1) * (BK_W + 1) + lx0], -1);
-            atomicAdd(&S.diff[(ly1 + 1) * (BK_W + 1) + lx1 + 1], 1);
+        for (uint32_t q0 = 0; q0 < n; q0 += 32 * 8) {  // 8 loads in flight per lane
+            uint32_t lrv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t q = q0 + 32 * u + lane;
+                lrv[u] = q < n ? __ldg(lrp + q) : 0xffffffffu;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t lr = lrv[u];
+                if (lr == 0xffffffffu) continue;
+                const int lx0 = lr & 15, lx1 = (lr >> 4) & 15, ly0 = (lr >> 8) & 7, ly1 = (lr >> 11) & 7;
+                atomicAdd(&S.diff[ly0 * (BK_W + 1) + lx0], 1);
+                atomicAdd(&S.diff[ly0 * (BK_W + 1) + lx1 + 1], -1);
+                atomicAdd(&S.diff[(ly1 + 1) * (BK_W + 1) + lx0], -1);
+                atomicAdd(&S.diff[(ly1 + 1) * (BK_W + 1) + lx1 + 1], 1);
+            }
         }
         __syncwarp();
         if (lane < BK_H) {
@@ -1167,11 +1195,13 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
         }
         __syncwarp();
         // pass 2: the entries in (piece, row, column) order, 32 per step
+        uint32_t lr_n = lane < n ? __ldg(lrp + lane) : 0u, gi_n = lane < n ? __ldg(gip + lane) : 0u;
         for (uint32_t q0 = 0; q0 < n; q0 += 32) {
             const uint32_t q = q0 + lane;
             const bool has = q < n;
-            const uint32_t lr = has ? __ldg(lrp + q) : 0u;
-            const uint32_t gi = has ? __ldg(gip + q) : 0u;
+            const uint32_t lr = lr_n, gi = gi_n;
+            lr_n = q + 32 < n ? __ldg(lrp + q + 32) : 0u;  // next round's pieces, in flight meanwhile
+            gi_n = q + 32 < n ? __ldg(gip + q + 32) : 0u;
             const uint32_t ne = has ? (((lr >> 4) & 15) - (lr & 15) + 1) * (((lr >> 11) & 7) - ((lr >> 8) & 7) + 1) : 0u;
             uint32_t incl = ne;
 #pragma unroll
@@ -1202,7 +1232,7 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                     const uint32_t lx0 = plr & 15, lx1 = (plr >> 4) & 15, ly0 = (plr >> 8) & 7;
                     const uint32_t wdt = lx1 - lx0 + 1;
                     const uint32_t o = e - S.pstart[p];
-                    const uint32_t row = (o * ((65536u + wdt - 1) / wdt)) >> 16;  // exact: o < 128
+                    const uint32_t row = (o * s_rcp[wdt]) >> 16;  // exact: o < 128
                     lt = (int)((ly0 + row) * BK_W + lx0 + (o - row * wdt));
                     gpi = S.pgi[p];
                     atomicOr(&S.wm[lt], 1u << lane);
