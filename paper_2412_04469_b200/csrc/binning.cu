@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __res
 // ---------------------------------------------------------------------------
 constexpr int PC_THREADS = 512;             // PC_CH / 8 pairs per thread
 constexpr size_t PC_MAX_SMEM = 200 * 1024;  // per-chunk bucket counters: up to 51200 buckets per batch
-constexpr int PS_MAX_WARPS = 4;             // k_piece_scatter: chunks (warps) per CTA, fewer when VNB is large
+constexpr int PS_MAX_WARPS = 8;             // k_piece_scatter: chunks (warps) per CTA, fewer when VNB is large
 
 
 struct BucketGeo {
@@ -841,7 +841,8 @@ __global__ void __launch_bounds__(PC_THREADS) k_piece_count(const uint32_t* __re
                                                             const uint32_t* __restrict__ triv,
                                                             const uint32_t* __restrict__ Kd,
                                                             const short4* __restrict__ rect, BucketGeo g,
-                                                            uint32_t* __restrict__ pcnt) {
+                                                            uint32_t* __restrict__ pcnt, uint32_t* __restrict__ rlo,
+                                                            uint32_t* __restrict__ rhi) {
     extern __shared__ uint32_t sc[];  // [VNB]
     const uint32_t M = visible_pairs(Kd);
     const uint32_t c = blockIdx.x;
@@ -855,6 +856,9 @@ __global__ void __launch_bounds__(PC_THREADS) k_piece_count(const uint32_t* __re
         if (m < M) {
             const uint32_t j = __ldg(dvals + m);
             const short4 r = __ldg(rect + j);
+            // the pair's tile rect in m order, for the scatter's coalesced reads
+            rlo[m] = (uint32_t)(uint16_t)r.x | ((uint32_t)(uint16_t)r.y << 16);
+            rhi[m] = (uint32_t)(uint16_t)r.z | ((uint32_t)(uint16_t)r.w << 16);
             const int vb = (int)(j / (uint32_t)g.n_pad) * g.NB;
             const int bx0 = r.x / BK_W, bx1 = r.z / BK_W, by0 = r.y / BK_H, by1 = r.w / BK_H;
             for (int by = by0; by <= by1; ++by)
@@ -979,98 +983,144 @@ __global__ void __launch_bounds__(256) k_emit_plan(const uint32_t* __restrict__ 
     plan[2 * (size_t)t + 1] = make_uint4(cA, cB - cA, 0u, 0u);
 }
 
-// One WARP per chunk, in m order (rounds of 32 pairs): a piece's position in its (chunk, bucket)
-// segment is the bucket's running cursor + the number of lower lanes with a piece in the same
-// bucket (per-warp shared-memory match words: each lane ORs its bit into the word of each of its
-// buckets -- a pair has at most one piece per bucket), so every segment comes out in m order and
-// the emission needs no sort.  A piece is stored as its Gaussian index (piece_gi) and its rect
-// inside the bucket (piece_lr), so the emission streams them without gathers.  The next
-// rounds' pair indices and rects are loaded ahead.
+// One CTA per chunk, its pairs split into wpc contiguous warp ranges.  Phase 1: each warp counts
+// its pieces per bucket; the counts become per-warp cursors (chunk offset + earlier warps).
+// Phase 2: each warp walks its pairs in m order with the pieces flattened 32 at a time
+// ((pair, bucket row, bucket column) order); the pieces of one bucket in such a step come from
+// distinct pairs in lane order, so match.any on the bucket gives each its rank.  Every (chunk,
+// bucket) segment thus comes out in m order and the emission needs no sort.  A piece is stored as
+// its Gaussian index (piece_gi) and its rect inside the bucket (piece_lr), so the emission streams
+// them without gathers; the pairs' indices and rects are read in m order (k_piece_count wrote the
+// rects there), 8 rounds of loads in flight per lane.
+constexpr int PS_ROUNDS = 8;
 __global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint32_t* __restrict__ dva,
                                                                      const uint32_t* __restrict__ dvb,
                                                                      const uint32_t* __restrict__ triv,
                                                                      const uint32_t* __restrict__ Kd,
-                                                                     const short4* __restrict__ rect, BucketGeo g,
+                                                                     const uint32_t* __restrict__ rlo,
+                                                                     const uint32_t* __restrict__ rhi, BucketGeo g,
                                                                      const uint32_t* __restrict__ pcnt,
                                                                      const uint32_t* __restrict__ pbase,
                                                                      uint32_t* __restrict__ piece_gi,
                                                                      uint32_t* __restrict__ piece_lr) {
-    extern __shared__ uint32_t ps_smem[];  // per warp: [VNB] cursors | [VNB] match words
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    extern __shared__ uint32_t ps_smem[];  // [wpc][VNB] counts, then cursors
+    __shared__ uint32_t s_rcp[BK_W + 1];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpc = blockDim.x >> 5;
     const uint32_t M = visible_pairs(Kd);
-    const uint32_t c = blockIdx.x * (blockDim.x >> 5) + w;
-    if ((uint64_t)c * PC_CH >= M) return;  // warp-uniform
-    uint32_t* cur = ps_smem + (size_t)w * 2 * g.VNB;
-    uint32_t* wm = cur + g.VNB;
+    const uint32_t c = blockIdx.x;
+    if ((uint64_t)c * PC_CH >= M) return;  // block-uniform
     const uint32_t* __restrict__ dvals = depth_order(dva, dvb, triv, Kd[1]);
-    for (int b = lane; b < g.VNB; b += 32) {
-        cur[b] = pbase[b] + pcnt[(size_t)b * g.CHS + c];
-        wm[b] = 0u;
-    }
-    const uint32_t lt = (1u << lane) - 1u;
-    const uint32_t m0 = c * PC_CH;
-    const uint32_t mend = min(M, m0 + PC_CH);
-    const int rounds = (int)((mend - m0 + 31) / 32);
-    auto ldj = [&](int r) -> uint32_t {
-        const uint32_t m = m0 + (uint32_t)r * 32 + lane;
-        return (r < rounds && m < mend) ? __ldg(dvals + m) : 0xffffffffu;
-    };
-    auto ldr = [&](uint32_t j) -> short4 { return j != 0xffffffffu ? __ldg(rect + j) : make_short4(1, 1, 0, 0); };
-    // rounds in groups of PSG: pair indices are loaded two groups ahead, rects one group ahead
-    constexpr int PSG = 4;
-    uint32_t jc[PSG], jn[PSG];
-    short4 rc[PSG];
+    uint32_t* cur = ps_smem + (size_t)w * g.VNB;
+    for (int b = lane; b < g.VNB; b += 32) cur[b] = 0u;
+    if (threadIdx.x <= BK_W) s_rcp[threadIdx.x] = threadIdx.x ? (65536u + threadIdx.x - 1) / threadIdx.x : 0u;
+    const uint32_t span = PC_CH / wpc;  // pairs per warp (multiple of 32 * PS_ROUNDS)
+    const uint32_t m0 = c * PC_CH + w * span;
+    const uint32_t mend = min(M, m0 + span);
+    __syncthreads();
+    // phase 1: pieces per (warp, bucket)
+    for (uint32_t mb = m0; mb < mend; mb += 32 * PS_ROUNDS) {
+        uint32_t jv[PS_ROUNDS], lo[PS_ROUNDS], hi[PS_ROUNDS];
 #pragma unroll
-    for (int u = 0; u < PSG; ++u) { jc[u] = ldj(u); jn[u] = ldj(PSG + u); }
-#pragma unroll
-    for (int u = 0; u < PSG; ++u) rc[u] = ldr(jc[u]);
-    __syncwarp();
-    for (int r0 = 0; r0 < rounds; r0 += PSG) {
-        uint32_t jnn[PSG];
-        short4 rn[PSG];
-#pragma unroll
-        for (int u = 0; u < PSG; ++u) jnn[u] = ldj(r0 + 2 * PSG + u);
-#pragma unroll
-        for (int u = 0; u < PSG; ++u) rn[u] = ldr(jn[u]);
-#pragma unroll
-        for (int u = 0; u < PSG; ++u) {
-            const uint32_t j_c = jc[u];
-            const short4 r_c = rc[u];
-            const bool has = j_c != 0xffffffffu;
-            int vb = 0, bx0 = 1, bx1 = 0, by0 = 1, by1 = 0;  // empty unless has
-            if (has) {
-                vb = (int)(j_c / (uint32_t)g.n_pad) * g.NB;
-                bx0 = r_c.x / BK_W; bx1 = r_c.z / BK_W; by0 = r_c.y / BK_H; by1 = r_c.w / BK_H;
-            }
-            for (int by = by0; by <= by1; ++by)
-                for (int bx = bx0; bx <= bx1; ++bx) atomicOr(&wm[vb + by * g.nbx + bx], 1u << lane);
-            __syncwarp();
-            const uint32_t gi = has ? j_c - (uint32_t)(vb / g.NB) * (uint32_t)g.n_pad : 0u;
-            for (int by = by0; by <= by1; ++by)
-                for (int bx = bx0; bx <= bx1; ++bx) {
-                    const int bk = vb + by * g.nbx + bx;
-                    const uint32_t pos = cur[bk] + __popc(wm[bk] & lt);
-                    // the piece: Gaussian index and its rect inside the bucket (lx0 | lx1 << 4 | ly0 << 8 | ly1 << 11)
-                    const int tx0b = bx * BK_W, ty0b = by * BK_H;
-                    const int lx0 = max((int)r_c.x - tx0b, 0), lx1 = min((int)r_c.z - tx0b, BK_W - 1);
-                    const int ly0 = max((int)r_c.y - ty0b, 0), ly1 = min((int)r_c.w - ty0b, BK_H - 1);
-                    piece_gi[pos] = gi;
-                    piece_lr[pos] = (uint32_t)(lx0 | (lx1 << 4) | (ly0 << 8) | (ly1 << 11));
-                }
-            __syncwarp();
-            for (int by = by0; by <= by1; ++by)
-                for (int bx = bx0; bx <= bx1; ++bx) {
-                    const int bk = vb + by * g.nbx + bx;
-                    const uint32_t x = wm[bk];
-                    if ((x & lt) == 0) {  // the bucket's lowest lane advances its cursor and clears its word
-                        cur[bk] += __popc(x);
-                        wm[bk] = 0u;
-                    }
-                }
-            __syncwarp();
+        for (int u = 0; u < PS_ROUNDS; ++u) {
+            const uint32_t m = mb + 32 * u + lane;
+            jv[u] = m < mend ? __ldg(dvals + m) : 0xffffffffu;
+            lo[u] = m < mend ? __ldg(rlo + m) : 0u;
+            hi[u] = m < mend ? __ldg(rhi + m) : 0u;
         }
 #pragma unroll
-        for (int u = 0; u < PSG; ++u) { jc[u] = jn[u]; rc[u] = rn[u]; jn[u] = jnn[u]; }
+        for (int u = 0; u < PS_ROUNDS; ++u) {
+            if (jv[u] == 0xffffffffu) continue;
+            const int vb = (int)(jv[u] / (uint32_t)g.n_pad) * g.NB;
+            const int bx0 = (int)(lo[u] & 0xffffu) / BK_W, by0 = (int)(lo[u] >> 16) / BK_H;
+            const int bx1 = (int)(hi[u] & 0xffffu) / BK_W, by1 = (int)(hi[u] >> 16) / BK_H;
+            for (int by = by0; by <= by1; ++by)
+                for (int bx = bx0; bx <= bx1; ++bx) atomicAdd(&cur[vb + by * g.nbx + bx], 1u);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < g.VNB; b += blockDim.x) {  // cursors: chunk offset + earlier warps
+        uint32_t run = pbase[b] + pcnt[(size_t)b * g.CHS + c];
+        for (int ww = 0; ww < wpc; ++ww) {
+            const uint32_t x = ps_smem[(size_t)ww * g.VNB + b];
+            ps_smem[(size_t)ww * g.VNB + b] = run;
+            run += x;
+        }
+    }
+    __syncthreads();
+    // phase 2: the pieces in m order, flattened 32 at a time
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t le = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;
+    for (uint32_t mb = m0; mb < mend; mb += 32 * PS_ROUNDS) {
+        uint32_t jv[PS_ROUNDS], lo[PS_ROUNDS], hi[PS_ROUNDS];
+#pragma unroll
+        for (int u = 0; u < PS_ROUNDS; ++u) {
+            const uint32_t m = mb + 32 * u + lane;
+            jv[u] = m < mend ? __ldg(dvals + m) : 0xffffffffu;
+            lo[u] = m < mend ? __ldg(rlo + m) : 0u;
+            hi[u] = m < mend ? __ldg(rhi + m) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < PS_ROUNDS; ++u) {
+            const bool has = jv[u] != 0xffffffffu;
+            const int bx0 = (int)(lo[u] & 0xffffu) / BK_W, by0 = (int)(lo[u] >> 16) / BK_H;
+            const int bx1 = (int)(hi[u] & 0xffffu) / BK_W, by1 = (int)(hi[u] >> 16) / BK_H;
+            const uint32_t np = has ? (uint32_t)((bx1 - bx0 + 1) * (by1 - by0 + 1)) : 0u;
+            uint32_t incl = np;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t excl = incl - np;
+            const uint32_t NP = __shfl_sync(0xffffffffu, incl, 31);
+            int pp = 0;  // pair of the step's first piece (lanes agree); pairs with pieces come first
+            for (uint32_t e0 = 0; e0 < NP; e0 += 32) {
+                // piece starts of pairs pp+1 .. inside (e0, e0 + 32): one redux.or
+                const int cand = pp + lane + 1;
+                const uint32_t st = __shfl_sync(0xffffffffu, excl, cand & 31);
+                const uint32_t d = st - e0;
+                const uint32_t bit = (cand < 32 && st > e0 && d < 32u) ? (1u << d) : 0u;
+                const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
+                const int p = pp + __popc(starts & le);
+                const uint32_t e = e0 + lane;
+                const bool valid = e < NP;
+                // the pair's data from its lane
+                const uint32_t pj = __shfl_sync(0xffffffffu, jv[u], p & 31);
+                const uint32_t plo = __shfl_sync(0xffffffffu, lo[u], p & 31);
+                const uint32_t phi = __shfl_sync(0xffffffffu, hi[u], p & 31);
+                const uint32_t pst = __shfl_sync(0xffffffffu, excl, p & 31);
+                int bk = -1 - lane;  // invalid lanes: keys no valid lane has
+                uint32_t gi = 0, lrw = 0;
+                if (valid) {
+                    const int v = (int)(pj / (uint32_t)g.n_pad);
+                    const int tx0 = (int)(plo & 0xffffu), ty0 = (int)(plo >> 16);
+                    const int tx1 = (int)(phi & 0xffffu), ty1 = (int)(phi >> 16);
+                    const int qbx0 = tx0 / BK_W, qby0 = ty0 / BK_H, qbx1 = tx1 / BK_W;
+                    const uint32_t bw = (uint32_t)(qbx1 - qbx0 + 1);
+                    const uint32_t o = e - pst;
+                    const uint32_t orow = (o * s_rcp[bw]) >> 16;  // exact: o < 4096
+                    const int bx = qbx0 + (int)(o - orow * bw), by = qby0 + (int)orow;
+                    bk = v * g.NB + by * g.nbx + bx;
+                    gi = pj - (uint32_t)v * (uint32_t)g.n_pad;
+                    const int tx0b = bx * BK_W, ty0b = by * BK_H;
+                    const int lx0 = max(tx0 - tx0b, 0), lx1 = min(tx1 - tx0b, BK_W - 1);
+                    const int ly0 = max(ty0 - ty0b, 0), ly1 = min(ty1 - ty0b, BK_H - 1);
+                    lrw = (uint32_t)(lx0 | (lx1 << 4) | (ly0 << 8) | (ly1 << 11));
+                }
+                const uint32_t peers = __match_any_sync(0xffffffffu, bk);
+                const uint32_t pos = valid ? cur[bk] + __popc(peers & lt) : 0u;
+                __syncwarp();
+                if (valid) {
+                    piece_gi[pos] = gi;
+                    piece_lr[pos] = lrw;
+                    if ((peers & lt) == 0) cur[bk] += __popc(peers);  // the bucket's lowest lane
+                }
+                __syncwarp();
+                const int p31 = __shfl_sync(0xffffffffu, p, 31);
+                const uint32_t nst = __shfl_sync(0xffffffffu, excl, (p31 + 1) & 31);
+                pp = p31 + ((p31 + 1 < 32 && nst == e0 + 32) ? 1 : 0);
+            }
+        }
     }
 }
 
@@ -1087,7 +1137,6 @@ constexpr int EW_WARPS = 4;  // independent emit workers per CTA
 struct EwSmem {
     int diff[(BK_H + 1) * (BK_W + 1)];
     uint32_t base[BK_T];   // final position of each bucket tile's next entry
-    uint32_t wm[BK_T];     // match words of the current 32-entry chunk
     uint32_t pstart[33];   // entry offsets of the round's 32 pieces (+ total)
     uint32_t pgi[32], plr[32];
 };
@@ -1191,7 +1240,6 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
             const int ty = ty0b + ly, tx = tx0b + lx;
             const uint32_t gt = (uint32_t)v * (uint32_t)g.T + (uint32_t)(ty * g.gx + tx);
             S.base[lt] = (tx < g.gx && ty < g.gy) ? __ldg(&ranges[gt].x) + prefix[i] : 0u;
-            S.wm[lt] = 0u;
         }
         __syncwarp();
         // pass 2: the entries in (piece, row, column) order, 32 per step
@@ -1225,7 +1273,7 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                 const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
                 const int p = pp + __popc(starts & le_mask);
                 const bool valid = e < E;
-                int lt = 0;
+                int lt = -1 - lane;  // invalid lanes: a key no valid lane has
                 uint32_t gpi = 0;
                 if (valid) {
                     const uint32_t plr = S.plr[p];
@@ -1235,18 +1283,14 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                     const uint32_t row = (o * s_rcp[wdt]) >> 16;  // exact: o < 128
                     lt = (int)((ly0 + row) * BK_W + lx0 + (o - row * wdt));
                     gpi = S.pgi[p];
-                    atomicOr(&S.wm[lt], 1u << lane);
                 }
+                // the chunk's entries of one tile come from distinct pieces in lane order
+                const uint32_t peers = __match_any_sync(0xffffffffu, lt);
+                const uint32_t pos = valid ? S.base[lt] + __popc(peers & lt_mask) : 0u;
                 __syncwarp();
-                uint32_t x = 0;
                 if (valid) {
-                    x = S.wm[lt];
-                    vals[S.base[lt] + __popc(x & lt_mask)] = gpi;
-                }
-                __syncwarp();
-                if (valid && (x & lt_mask) == 0) {  // lowest lane of the tile: advance, clear
-                    S.base[lt] += __popc(x);
-                    S.wm[lt] = 0u;
+                    vals[pos] = gpi;
+                    if ((peers & lt_mask) == 0) S.base[lt] += __popc(peers);  // the tile's lowest lane
                 }
                 __syncwarp();
                 const int p31 = __shfl_sync(0xffffffffu, p, 31);
@@ -1466,18 +1510,22 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     const uint32_t* dlast_in = dv[cur ^ 1];   // input of the last depth pass
     const uint32_t* dlast_out = dv[cur];      // its output (unless it was skipped)
     const uint32_t* triv = hist + (DEPTH_PASSES - 1) * MAX_BINS;
+    // the depth-key buffers are free after the depth sort: the pairs' rects in m order
+    uint32_t* rlo = dk[0];
+    uint32_t* rhi = dk[1];
     const short4* r4 = reinterpret_cast<const short4*>(proj.rect);
     if (8 * (size_t)bg.VNB > PC_MAX_SMEM) return cudaErrorInvalidConfiguration;  // > 25600 buckets: not reachable (<= 64 4K views)
     prof->begin(ST_DUPLICATE, s);
     if ((e = cudaMemsetAsync(emit_lb, 0, sizeof(uint32_t) * BK_T * (size_t)etiles, s))) return e;
     if (chunks > 0) {
-        k_piece_count<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt);
+        k_piece_count<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, rlo, rhi);
         k_piece_colscan<<<(unsigned)((bg.VNB + 7) / 8), 256, 0, s>>>(pcnt, Kd, bg, ptotal);
         k_piece_base<<<1, 1024, 0, s>>>(ptotal, bg.VNB, pbase, ebase, meta, ebucket);
-        // warps per CTA: each holds 2 x VNB words (cursors, match words)
-        const int wpc = (int)std::max<int64_t>(1, std::min<int64_t>(PS_MAX_WARPS, (int64_t)PC_MAX_SMEM / (8 * (int64_t)bg.VNB)));
-        k_piece_scatter<<<(unsigned)((chunks + wpc - 1) / wpc), 32 * wpc, (size_t)wpc * 8 * bg.VNB, s>>>(
-            dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, pbase, bins.keys_alt, bins.keys);
+        // warps per chunk: each holds VNB cursors in shared memory
+        int wpc = (int)std::max<int64_t>(1, std::min<int64_t>(PS_MAX_WARPS, (int64_t)PC_MAX_SMEM / (4 * (int64_t)bg.VNB)));
+        while (wpc > 1 && (PC_CH / wpc) % (32 * PS_ROUNDS)) --wpc;
+        k_piece_scatter<<<(unsigned)chunks, 32 * wpc, (size_t)wpc * 4 * bg.VNB, s>>>(
+            dlast_in, dlast_out, triv, Kd, rlo, rhi, bg, pcnt, pbase, bins.keys_alt, bins.keys);
     }
     prof->end(s, chunks > 0 ? 5 : 1);
     prof->begin(ST_TILE_SORT, s);
