@@ -1137,6 +1137,7 @@ constexpr int EW_WARPS = 4;  // independent emit workers per CTA
 struct EwSmem {
     int diff[(BK_H + 1) * (BK_W + 1)];
     uint32_t base[BK_T];   // final position of each bucket tile's next entry
+    uint32_t wm[BK_T];     // match words of the current 32-entry step
     uint32_t pstart[33];   // entry offsets of the round's 32 pieces (+ total)
     uint32_t pgi[32], plr[32];
 };
@@ -1240,6 +1241,7 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
             const int ty = ty0b + ly, tx = tx0b + lx;
             const uint32_t gt = (uint32_t)v * (uint32_t)g.T + (uint32_t)(ty * g.gx + tx);
             S.base[lt] = (tx < g.gx && ty < g.gy) ? __ldg(&ranges[gt].x) + prefix[i] : 0u;
+            S.wm[lt] = 0u;
         }
         __syncwarp();
         // pass 2: the entries in (piece, row, column) order, 32 per step
@@ -1273,7 +1275,7 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                 const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
                 const int p = pp + __popc(starts & le_mask);
                 const bool valid = e < E;
-                int lt = -1 - lane;  // invalid lanes: a key no valid lane has
+                int lt = 0;
                 uint32_t gpi = 0;
                 if (valid) {
                     const uint32_t plr = S.plr[p];
@@ -1283,14 +1285,20 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                     const uint32_t row = (o * s_rcp[wdt]) >> 16;  // exact: o < 128
                     lt = (int)((ly0 + row) * BK_W + lx0 + (o - row * wdt));
                     gpi = S.pgi[p];
+                    atomicOr(&S.wm[lt], 1u << lane);
                 }
-                // the chunk's entries of one tile come from distinct pieces in lane order
-                const uint32_t peers = __match_any_sync(0xffffffffu, lt);
-                const uint32_t pos = valid ? S.base[lt] + __popc(peers & lt_mask) : 0u;
+                // the step's entries of one tile come from distinct pieces in lane order: match words
+                // (measured faster than match.any here: 289 vs 422 us per N3DV frame)
                 __syncwarp();
+                uint32_t x = 0;
                 if (valid) {
-                    vals[pos] = gpi;
-                    if ((peers & lt_mask) == 0) S.base[lt] += __popc(peers);  // the tile's lowest lane
+                    x = S.wm[lt];
+                    vals[S.base[lt] + __popc(x & lt_mask)] = gpi;
+                }
+                __syncwarp();
+                if (valid && (x & lt_mask) == 0) {  // lowest lane of the tile: advance, clear
+                    S.base[lt] += __popc(x);
+                    S.wm[lt] = 0u;
                 }
                 __syncwarp();
                 const int p31 = __shfl_sync(0xffffffffu, p, 31);

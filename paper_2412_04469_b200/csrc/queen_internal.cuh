@@ -115,7 +115,7 @@ inline BinPlan bin_plan(int64_t n_pad, int64_t n_views, int W, int H) {
 // depth-ordered pairs are counted and scattered in chunks of PC_CH; emit tiles hold ~EM_E pieces.
 constexpr int PC_CH = 2048;
 constexpr int BK_W = 16, BK_H = 8, BK_T = BK_W * BK_H;
-constexpr int EM_E = 2048;
+constexpr int EM_E = 512;
 inline int64_t buckets_per_view(int W, int H) {
     const int64_t gx = (W + 15) / 16, gy = (H + 15) / 16;
     return ((gx + BK_W - 1) / BK_W) * ((gy + BK_H - 1) / BK_H);
