@@ -1134,12 +1134,13 @@ __global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint3
 //           and ranks it among the chunk's entries of the same tile by match words (lower lanes
 //           = earlier pieces), so each tile's entries are written in m order.
 constexpr int EW_WARPS = 4;  // independent emit workers per CTA
+constexpr int EW_ENT = 512;  // entries staged per round and warp
 struct EwSmem {
     int diff[(BK_H + 1) * (BK_W + 1)];
     uint32_t base[BK_T];   // final position of each bucket tile's next entry
     uint32_t wm[BK_T];     // match words of the current 32-entry step
-    uint32_t pstart[33];   // entry offsets of the round's 32 pieces (+ total)
-    uint32_t pgi[32], plr[32];
+    uint8_t elt[EW_ENT];   // staged entries of a round: bucket tile, Gaussian index
+    uint32_t egi[EW_ENT];
 };
 
 __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restrict__ piece_gi,
@@ -1152,15 +1153,11 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                                                         uint32_t* __restrict__ vals, uint32_t* lb, uint32_t* ticket,
                                                         DevFlags* fl) {
     __shared__ EwSmem sm[EW_WARPS];
-    __shared__ uint32_t s_rcp[BK_W + 1];  // ceil(2^16 / w): row = (o * s_rcp[w]) >> 16 = o / w for o < 128
-    if (threadIdx.x <= BK_W) s_rcp[threadIdx.x] = threadIdx.x ? (65536u + threadIdx.x - 1) / threadIdx.x : 0u;
-    __syncthreads();
     const int lane = threadIdx.x & 31;
     EwSmem& S = sm[threadIdx.x >> 5];
     if (visible_pairs(Kd) == 0) return;
     const uint32_t NE = meta[1];
     const uint32_t lt_mask = (1u << lane) - 1u;
-    const uint32_t le_mask = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;
     for (;;) {
         uint32_t t = 0;
         if (lane == 0) t = atomicAdd(ticket, 1u);
@@ -1244,14 +1241,15 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
             S.wm[lt] = 0u;
         }
         __syncwarp();
-        // pass 2: the entries in (piece, row, column) order, 32 per step
+        // pass 2: the entries in (piece, row, column) order.  A round takes the next <= 32 pieces
+        // whose entries fit the staging area; each piece's lane writes its entries' bucket tiles
+        // and Gaussian index there, then the warp ranks them 32 at a time (match words).
+        uint32_t q0 = 0;
         uint32_t lr_n = lane < n ? __ldg(lrp + lane) : 0u, gi_n = lane < n ? __ldg(gip + lane) : 0u;
-        for (uint32_t q0 = 0; q0 < n; q0 += 32) {
+        while (q0 < n) {
             const uint32_t q = q0 + lane;
             const bool has = q < n;
             const uint32_t lr = lr_n, gi = gi_n;
-            lr_n = q + 32 < n ? __ldg(lrp + q + 32) : 0u;  // next round's pieces, in flight meanwhile
-            gi_n = q + 32 < n ? __ldg(gip + q + 32) : 0u;
             const uint32_t ne = has ? (((lr >> 4) & 15) - (lr & 15) + 1) * (((lr >> 11) & 7) - ((lr >> 8) & 7) + 1) : 0u;
             uint32_t incl = ne;
 #pragma unroll
@@ -1259,36 +1257,31 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                 const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            const uint32_t E = __shfl_sync(0xffffffffu, incl, 31);
-            S.pstart[lane] = incl - ne;
-            S.plr[lane] = lr;
-            S.pgi[lane] = gi;
-            if (lane == 31) S.pstart[32] = E;
+            const uint32_t fit = __ballot_sync(0xffffffffu, incl <= (uint32_t)EW_ENT);  // a prefix of the lanes
+            const int kk = __popc(fit);  // >= 1: a piece has <= 128 entries
+            const uint32_t E = __shfl_sync(0xffffffffu, incl, kk - 1);
+            // next round's pieces, in flight meanwhile (reloaded below when this round took < 32)
+            const uint32_t qn = q0 + (uint32_t)kk + lane;
+            lr_n = qn < n ? __ldg(lrp + qn) : 0u;
+            gi_n = qn < n ? __ldg(gip + qn) : 0u;
+            if (lane < kk && has) {
+                const uint32_t lx0 = lr & 15, lx1 = (lr >> 4) & 15, ly0 = (lr >> 8) & 7, ly1 = (lr >> 11) & 7;
+                uint32_t o = incl - ne;
+                for (uint32_t ly = ly0; ly <= ly1; ++ly)
+                    for (uint32_t lx = lx0; lx <= lx1; ++lx, ++o) {
+                        S.elt[o] = (uint8_t)(ly * BK_W + lx);
+                        S.egi[o] = gi;
+                    }
+            }
             __syncwarp();
-            int pp = 0;  // piece of entry e0 (lanes agree); every piece of the round has >= 1 entry
             for (uint32_t e0 = 0; e0 < E; e0 += 32) {
                 const uint32_t e = e0 + lane;
-                const int cand = pp + lane + 1;
-                const uint32_t st = cand <= 32 ? S.pstart[cand] : 0xffffffffu;
-                const uint32_t d = st - e0;  // start of piece cand relative to e0
-                const uint32_t bit = (st > e0 && d < 32u) ? (1u << d) : 0u;
-                const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
-                const int p = pp + __popc(starts & le_mask);
                 const bool valid = e < E;
-                int lt = 0;
-                uint32_t gpi = 0;
-                if (valid) {
-                    const uint32_t plr = S.plr[p];
-                    const uint32_t lx0 = plr & 15, lx1 = (plr >> 4) & 15, ly0 = (plr >> 8) & 7;
-                    const uint32_t wdt = lx1 - lx0 + 1;
-                    const uint32_t o = e - S.pstart[p];
-                    const uint32_t row = (o * s_rcp[wdt]) >> 16;  // exact: o < 128
-                    lt = (int)((ly0 + row) * BK_W + lx0 + (o - row * wdt));
-                    gpi = S.pgi[p];
-                    atomicOr(&S.wm[lt], 1u << lane);
-                }
-                // the step's entries of one tile come from distinct pieces in lane order: match words
-                // (measured faster than match.any here: 289 vs 422 us per N3DV frame)
+                const int lt = valid ? S.elt[e] : 0;
+                const uint32_t gpi = valid ? S.egi[e] : 0u;
+                // the step's entries of one tile come from distinct pieces in lane order: match
+                // words (measured faster than match.any here: 289 vs 422 us per N3DV frame)
+                if (valid) atomicOr(&S.wm[lt], 1u << lane);
                 __syncwarp();
                 uint32_t x = 0;
                 if (valid) {
@@ -1301,10 +1294,8 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                     S.wm[lt] = 0u;
                 }
                 __syncwarp();
-                const int p31 = __shfl_sync(0xffffffffu, p, 31);
-                pp = p31 + ((p31 + 1 <= 32 && S.pstart[p31 + 1] == e0 + 32) ? 1 : 0);
             }
-            __syncwarp();
+            q0 += (uint32_t)kk;
         }
     }
 }
