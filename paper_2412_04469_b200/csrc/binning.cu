@@ -1129,18 +1129,14 @@ __global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint3
 //   pass 1  entry counts per bucket tile (2D difference array over the 16 x 8 tiles);
 //   then    each tile's offset among the bucket's earlier emit tiles by decoupled look-back
 //           (4 tiles per lane), base = ranges[gt].first + offset;
-//   pass 2  the entries, flattened 32 at a time in (piece, row, column) order: lane i takes entry
-//           e0 + i, finds its piece among the round's 32 by one redux.or over the piece starts,
-//           and ranks it among the chunk's entries of the same tile by match words (lower lanes
-//           = earlier pieces), so each tile's entries are written in m order.
+//   pass 2  rounds of 32 pieces: an entry's rank among the round's earlier pieces on its tile is
+//           popc(R[row] & C[column] & lower lanes) (row / column coverage ballots), so each tile's
+//           entries are written in m order.
 constexpr int EW_WARPS = 4;  // independent emit workers per CTA
-constexpr int EW_ENT = 512;  // entries staged per round and warp
 struct EwSmem {
     int diff[(BK_H + 1) * (BK_W + 1)];
     uint32_t base[BK_T];   // final position of each bucket tile's next entry
-    uint32_t wm[BK_T];     // match words of the current 32-entry step
-    uint8_t elt[EW_ENT];   // staged entries of a round: bucket tile, Gaussian index
-    uint32_t egi[EW_ENT];
+    uint32_t R[BK_H], C[BK_W];  // the round's pieces covering each bucket row / column
 };
 
 __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restrict__ piece_gi,
@@ -1238,64 +1234,48 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
             const int ty = ty0b + ly, tx = tx0b + lx;
             const uint32_t gt = (uint32_t)v * (uint32_t)g.T + (uint32_t)(ty * g.gx + tx);
             S.base[lt] = (tx < g.gx && ty < g.gy) ? __ldg(&ranges[gt].x) + prefix[i] : 0u;
-            S.wm[lt] = 0u;
         }
         __syncwarp();
-        // pass 2: the entries in (piece, row, column) order.  A round takes the next <= 32 pieces
-        // whose entries fit the staging area; each piece's lane writes its entries' bucket tiles
-        // and Gaussian index there, then the warp ranks them 32 at a time (match words).
-        uint32_t q0 = 0;
+        // pass 2: rounds of 32 pieces in m order (lane = piece).  A piece covers the bucket tiles
+        // rows x columns of its rect, so the round's pieces covering tile (ly, lx) are
+        // R[ly] & C[lx] with R[ly] = ballot(piece covers row ly), C[lx] = ballot(covers column lx):
+        // 24 ballots give every entry's rank among the round's earlier pieces -- popc(R & C & lower
+        // lanes) -- with no atomics and no per-entry synchronisation.
         uint32_t lr_n = lane < n ? __ldg(lrp + lane) : 0u, gi_n = lane < n ? __ldg(gip + lane) : 0u;
-        while (q0 < n) {
+        for (uint32_t q0 = 0; q0 < n; q0 += 32) {
             const uint32_t q = q0 + lane;
             const bool has = q < n;
             const uint32_t lr = lr_n, gi = gi_n;
-            const uint32_t ne = has ? (((lr >> 4) & 15) - (lr & 15) + 1) * (((lr >> 11) & 7) - ((lr >> 8) & 7) + 1) : 0u;
-            uint32_t incl = ne;
+            lr_n = q + 32 < n ? __ldg(lrp + q + 32) : 0u;  // next round's pieces, in flight meanwhile
+            gi_n = q + 32 < n ? __ldg(gip + q + 32) : 0u;
+            const uint32_t lx0 = lr & 15, lx1 = (lr >> 4) & 15, ly0 = (lr >> 8) & 7, ly1 = (lr >> 11) & 7;
+            const uint32_t rm = has ? ((2u << ly1) - 1u) & ~((1u << ly0) - 1u) : 0u;  // rows covered
+            const uint32_t cm = has ? ((2u << lx1) - 1u) & ~((1u << lx0) - 1u) : 0u;  // columns covered
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
+            for (int y = 0; y < BK_H; ++y) {
+                const uint32_t r = __ballot_sync(0xffffffffu, (rm >> y) & 1u);
+                if (lane == 0) S.R[y] = r;
             }
-            const uint32_t fit = __ballot_sync(0xffffffffu, incl <= (uint32_t)EW_ENT);  // a prefix of the lanes
-            const int kk = __popc(fit);  // >= 1: a piece has <= 128 entries
-            const uint32_t E = __shfl_sync(0xffffffffu, incl, kk - 1);
-            // next round's pieces, in flight meanwhile (reloaded below when this round took < 32)
-            const uint32_t qn = q0 + (uint32_t)kk + lane;
-            lr_n = qn < n ? __ldg(lrp + qn) : 0u;
-            gi_n = qn < n ? __ldg(gip + qn) : 0u;
-            if (lane < kk && has) {
-                const uint32_t lx0 = lr & 15, lx1 = (lr >> 4) & 15, ly0 = (lr >> 8) & 7, ly1 = (lr >> 11) & 7;
-                uint32_t o = incl - ne;
-                for (uint32_t ly = ly0; ly <= ly1; ++ly)
-                    for (uint32_t lx = lx0; lx <= lx1; ++lx, ++o) {
-                        S.elt[o] = (uint8_t)(ly * BK_W + lx);
-                        S.egi[o] = gi;
-                    }
+#pragma unroll
+            for (int x = 0; x < BK_W; ++x) {
+                const uint32_t c = __ballot_sync(0xffffffffu, (cm >> x) & 1u);
+                if (lane == 0) S.C[x] = c;
             }
             __syncwarp();
-            for (uint32_t e0 = 0; e0 < E; e0 += 32) {
-                const uint32_t e = e0 + lane;
-                const bool valid = e < E;
-                const int lt = valid ? S.elt[e] : 0;
-                const uint32_t gpi = valid ? S.egi[e] : 0u;
-                // the step's entries of one tile come from distinct pieces in lane order: match
-                // words (measured faster than match.any here: 289 vs 422 us per N3DV frame)
-                if (valid) atomicOr(&S.wm[lt], 1u << lane);
-                __syncwarp();
-                uint32_t x = 0;
-                if (valid) {
-                    x = S.wm[lt];
-                    vals[S.base[lt] + __popc(x & lt_mask)] = gpi;
+            if (has) {
+                for (uint32_t ly = ly0; ly <= ly1; ++ly) {
+                    const uint32_t rr = S.R[ly] & lt_mask;
+                    for (uint32_t lx = lx0; lx <= lx1; ++lx)
+                        vals[S.base[ly * BK_W + lx] + __popc(rr & S.C[lx])] = gi;
                 }
-                __syncwarp();
-                if (valid && (x & lt_mask) == 0) {  // lowest lane of the tile: advance, clear
-                    S.base[lt] += __popc(x);
-                    S.wm[lt] = 0u;
-                }
-                __syncwarp();
             }
-            q0 += (uint32_t)kk;
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < BK_T / 32; ++i) {  // the round's entries per tile
+                const int lt = lane + 32 * i;
+                S.base[lt] += __popc(S.R[lt / BK_W] & S.C[lt % BK_W]);
+            }
+            __syncwarp();
         }
     }
 }
