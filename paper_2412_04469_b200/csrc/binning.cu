@@ -826,7 +826,13 @@ struct BucketGeo {
     int gx, gy, nbx, nby, NB, VNB;
     int T, n_pad;
     int CHS;  // row stride of pcnt ([bucket][chunk]): the chunk capacity
+    unsigned long long npad_magic;  // ceil(2^64 / n_pad): j / n_pad = umulhi64(j, magic), exact for j < 2^32
 };
+
+// view of a flat pair index j = v n_pad + i, without an integer division
+__device__ __forceinline__ uint32_t view_of(uint32_t j, const BucketGeo& g) {
+    return (uint32_t)__umul64hi((unsigned long long)j, g.npad_magic);
+}
 
 __device__ __forceinline__ const uint32_t* depth_order(const uint32_t* a, const uint32_t* b, const uint32_t* triv,
                                                        uint32_t M) {
@@ -859,7 +865,7 @@ __global__ void __launch_bounds__(PC_THREADS) k_piece_count(const uint32_t* __re
             // the pair's tile rect in m order, for the scatter's coalesced reads
             rlo[m] = (uint32_t)(uint16_t)r.x | ((uint32_t)(uint16_t)r.y << 16);
             rhi[m] = (uint32_t)(uint16_t)r.z | ((uint32_t)(uint16_t)r.w << 16);
-            const int vb = (int)(j / (uint32_t)g.n_pad) * g.NB;
+            const int vb = (int)view_of(j, g) * g.NB;
             const int bx0 = r.x / BK_W, bx1 = r.z / BK_W, by0 = r.y / BK_H, by1 = r.w / BK_H;
             for (int by = by0; by <= by1; ++by)
                 for (int bx = bx0; bx <= bx1; ++bx) atomicAdd(&sc[vb + by * g.nbx + bx], 1u);
@@ -1030,7 +1036,7 @@ __global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint3
 #pragma unroll
         for (int u = 0; u < PS_ROUNDS; ++u) {
             if (jv[u] == 0xffffffffu) continue;
-            const int vb = (int)(jv[u] / (uint32_t)g.n_pad) * g.NB;
+            const int vb = (int)view_of(jv[u], g) * g.NB;
             const int bx0 = (int)(lo[u] & 0xffffu) / BK_W, by0 = (int)(lo[u] >> 16) / BK_H;
             const int bx1 = (int)(hi[u] & 0xffffu) / BK_W, by1 = (int)(hi[u] >> 16) / BK_H;
             for (int by = by0; by <= by1; ++by)
@@ -1092,7 +1098,7 @@ __global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint3
                 int bk = -1 - lane;  // invalid lanes: keys no valid lane has
                 uint32_t gi = 0, lrw = 0;
                 if (valid) {
-                    const int v = (int)(pj / (uint32_t)g.n_pad);
+                    const int v = (int)view_of(pj, g);
                     const int tx0 = (int)(plo & 0xffffu), ty0 = (int)(plo >> 16);
                     const int tx1 = (int)(phi & 0xffffu), ty1 = (int)(phi >> 16);
                     const int qbx0 = tx0 / BK_W, qby0 = ty0 / BK_H, qbx1 = tx1 / BK_W;
@@ -1137,6 +1143,8 @@ struct EwSmem {
     int diff[(BK_H + 1) * (BK_W + 1)];
     uint32_t base[BK_T];   // final position of each bucket tile's next entry
     uint32_t R[BK_H], C[BK_W];  // the round's pieces covering each bucket row / column
+    uint32_t pstart[33];        // entry offsets of the round's pieces (+ total)
+    uint32_t plr[32], pgi[32];
 };
 
 __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restrict__ piece_gi,
@@ -1149,11 +1157,14 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                                                         uint32_t* __restrict__ vals, uint32_t* lb, uint32_t* ticket,
                                                         DevFlags* fl) {
     __shared__ EwSmem sm[EW_WARPS];
+    __shared__ uint32_t s_rcp[BK_W + 1];  // ceil(2^16 / w): row = (o * s_rcp[w]) >> 16 = o / w for o < 128
+    if (threadIdx.x <= BK_W) s_rcp[threadIdx.x] = threadIdx.x ? (65536u + threadIdx.x - 1) / threadIdx.x : 0u;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     EwSmem& S = sm[threadIdx.x >> 5];
     if (visible_pairs(Kd) == 0) return;
     const uint32_t NE = meta[1];
-    const uint32_t lt_mask = (1u << lane) - 1u;
+    const uint32_t le_mask = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;
     for (;;) {
         uint32_t t = 0;
         if (lane == 0) t = atomicAdd(ticket, 1u);
@@ -1261,13 +1272,43 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                 const uint32_t c = __ballot_sync(0xffffffffu, (cm >> x) & 1u);
                 if (lane == 0) S.C[x] = c;
             }
+            // the round's entries flattened 32 per step over the lanes, in (piece, row, column)
+            // order: lane i takes entry e0 + i and finds its piece by one redux.or over the piece
+            // starts in the step (every piece has >= 1 entry)
+            const uint32_t ne = has ? (lx1 - lx0 + 1) * (ly1 - ly0 + 1) : 0u;
+            uint32_t incl = ne;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t E = __shfl_sync(0xffffffffu, incl, 31);
+            S.pstart[lane] = incl - ne;
+            S.plr[lane] = lr;
+            S.pgi[lane] = gi;
+            if (lane == 31) S.pstart[32] = E;
             __syncwarp();
-            if (has) {
-                for (uint32_t ly = ly0; ly <= ly1; ++ly) {
-                    const uint32_t rr = S.R[ly] & lt_mask;
-                    for (uint32_t lx = lx0; lx <= lx1; ++lx)
-                        vals[S.base[ly * BK_W + lx] + __popc(rr & S.C[lx])] = gi;
+            int pp = 0;  // piece of entry e0 (lanes agree)
+            for (uint32_t e0 = 0; e0 < E; e0 += 32) {
+                const uint32_t e = e0 + lane;
+                const int cand = pp + lane + 1;
+                const uint32_t st = cand <= 32 ? S.pstart[cand] : 0xffffffffu;
+                const uint32_t d = st - e0;  // start of piece cand relative to e0
+                const uint32_t bit = (st > e0 && d < 32u) ? (1u << d) : 0u;
+                const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
+                const int p = pp + __popc(starts & le_mask);
+                if (e < E) {
+                    const uint32_t plr = S.plr[p];
+                    const uint32_t px0 = plr & 15, px1 = (plr >> 4) & 15, py0 = (plr >> 8) & 7;
+                    const uint32_t wdt = px1 - px0 + 1;
+                    const uint32_t o = e - S.pstart[p];
+                    const uint32_t row = (o * s_rcp[wdt]) >> 16;  // exact: o < 128
+                    const uint32_t ly = py0 + row, lx = px0 + (o - row * wdt);
+                    const uint32_t rank = __popc(S.R[ly] & S.C[lx] & ((1u << p) - 1u));
+                    vals[S.base[ly * BK_W + lx] + rank] = S.pgi[p];
                 }
+                const int p31 = __shfl_sync(0xffffffffu, p, 31);
+                pp = p31 + ((p31 + 1 <= 32 && S.pstart[p31 + 1] == e0 + 32) ? 1 : 0);
             }
             __syncwarp();
 #pragma unroll
@@ -1473,6 +1514,8 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     bg.VNB = bg.NB * n_views;
     bg.T = (int)T;
     bg.n_pad = proj.n_pad;
+    // ceil(2^64 / n_pad) (n_pad >= 4): floor(j / n_pad) = umulhi64(j, magic) for every j < 2^32
+    bg.npad_magic = ~0ull / (unsigned long long)proj.n_pad + 1ull;
     uint32_t* pcnt = reinterpret_cast<uint32_t*>(ws + L.pcnt);
     uint32_t* ptotal = reinterpret_cast<uint32_t*>(ws + L.pbuck);
     uint32_t* pbase = ptotal + bg.VNB;
