@@ -4,8 +4,8 @@
 
 One step = one frame of the workload: (N>1: NCCL broadcast of the frame's residual
 packet from rank 0) -> queen_apply_frame (int8 latent decode + apply + COO position
-scatter) -> queen_render_views for this rank's views (project, scan, duplicate,
-onesweep sort, ranges, blend).  Views are sharded v = rank mod N; the Gaussian set
+scatter) -> queen_render_views for this rank's views (project, counts, depth sort, bucketed
+emission, ranges, blend).  Views are sharded v = rank mod N; the Gaussian set
 is replicated.  Default workload: BASELINE configs[1] (N3DV-shaped, 300k Gaussians,
 20 views at 1352x1014, SH degree 3).
 
@@ -127,7 +127,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- roofline model
-def algorithmic_bytes(stage, cfg, n, vpb_list, K_list, k_coo, M_list, ent_bytes=0):
+def algorithmic_bytes(stage, cfg, n, vpb_list, K_list, k_coo, M_list, ent_bytes=0, P_list=None):
     """Algorithmic bytes per STEP (one frame, all batches) of each profiled stage (DESIGN.md
     "Roofline"): what the stage's algorithm must move with perfect coalescing.  Per batch of v
     views: E = n x v elements, M visible (view, Gaussian) pairs, K entries."""
@@ -147,10 +147,10 @@ def algorithmic_bytes(stage, cfg, n, vpb_list, K_list, k_coo, M_list, ent_bytes=
         return sum(n * v * 24 + 8 * M for v, M, K in bt)
     if stage == "depth_sort":  # 4 LSD passes over the (depth, index) pairs, 16 B each
         return sum(4 * 16 * M for v, M, K in bt)
-    if stage == "duplicate":  # pairs + rects in, K (gt, index) entries out
-        return sum(12 * M + 8 * K for v, M, K in bt)
-    if stage == "tile_sort":  # pass 1: 8 B in, 4 B packed out; pass 2: 4 B in, 4 B index out
-        return sum(20 * K for v, M, K in bt)
+    if stage == "bucket":  # count: pair index + rect in, rect copy out (20 B/pair); scatter: 12 B/pair in, 8 B/piece out
+        return sum(32 * M + 8 * Pc for (v, M, K), Pc in zip(bt, P_list))
+    if stage == "emit":  # pieces read by the count pass (4 B) and the write pass (8 B), 4 B per entry out
+        return sum(12 * Pc + 4 * K for (v, M, K), Pc in zip(bt, P_list))
     if stage == "blend_order":  # ranges read by the histogram and by the scatter, 4 B order out per tile
         T = ((cfg.width + 15) // 16) * ((cfg.height + 15) // 16)
         return sum(20 * v * T for v, M, K in bt)
@@ -615,13 +615,14 @@ def main():
     # ---- evidence (outside the timed region): K per batch, blend work counts
     batches = [cams[a:b] for a, b in player.batches]
     from paper_2412_04469_b200.stages import Stages  # explicit-buffer stage runner over the same C-ABI
-    K_list, M_list, ev_pairs, cp_pairs, libsort = [], [], 0, 0, None
+    K_list, M_list, P_list, ev_pairs, cp_pairs, libsort = [], [], [], 0, 0, None
     for bi, bc in enumerate(batches):
         stg = Stages(player.planes.cpu().numpy(), sc.n, sc.deg, bc, keys_cap=player.keys_cap, device=local)
         stg.project().bin_sort()
         bnp = stg.bins_np()
         K_list.append(bnp["K"])
         M_list.append(bnp["M"])
+        P_list.append(bnp["P"])
         if bi == 0 and not args.no_libsort:
             libsort = library_sort_comparison(stg, bnp, dev)
         e = torch.zeros(len(bc), dtype=torch.int64, device=dev)
@@ -669,11 +670,11 @@ def main():
                     "timing": "k_blend alone: serial eager steps inside bench.py (stages_serial)" if stages_serial
                               else "k_blend in the headline timed region (stages)",
                     "work": {"evaluated_pairs": ev_pairs, "composited_pairs": cp_pairs}}
-        elif algorithmic_bytes(dom, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b) is None:
+        elif algorithmic_bytes(dom, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b, P_list) is None:
             roof = {"bound": None, "kernel": dom, "achieved": None, "peak": None, "unit": None, "frac": None,
                     "traffic": None, "note": "dominant stage has no roofline model"}
         else:
-            b = algorithmic_bytes(dom, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b)
+            b = algorithmic_bytes(dom, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b, P_list)
             t = kst[dom]["ms_per_step"] * 1e-3
             achieved = b / t / 1e9
             peak = peaks["hbm_gbs"]
@@ -691,13 +692,13 @@ def main():
                     idl = 1e3 * max((7 * ev_pairs + 7 * cp_pairs) / (SM_COUNT * 128 * f_hz),
                                     cp_pairs / (SM_COUNT * 16 * f_hz))
                 else:
-                    b = algorithmic_bytes(name, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b)
+                    b = algorithmic_bytes(name, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b, P_list)
                     idl = 1e3 * b / (peaks["hbm_gbs"] * 1e9) if b else s_["ms_per_step"]
                 if table is stages:
                     ideal[name] = idl
                 s_["ideal_ms_per_step"] = idl
                 s_["frac"] = idl / s_["ms_per_step"] if s_["ms_per_step"] > 0 else None
-                b = algorithmic_bytes(name, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b)
+                b = algorithmic_bytes(name, cfg, sc.n, vpb_list, K_list, k_coo, M_list, ent_b, P_list)
                 if b and name != "blend":
                     s_["algorithmic_GBps"] = b / (s_["ms_per_step"] * 1e-3) / 1e9
         path = {"ideal_ms": sum(ideal.values()), "frame_ms": total_ms / args.steps,
@@ -709,7 +710,7 @@ def main():
         nb = len(batches)
         kst = stages_serial if stages_serial else stages  # stages alone on the GPU (not overlapped)
         libsort["ours_binning_ms_per_batch"] = sum(kst[k]["ms_per_step"] for k in
-                                                   ("compact", "depth_sort", "duplicate", "ranges", "tile_sort")
+                                                   ("compact", "depth_sort", "bucket", "ranges", "emit")
                                                    if k in kst) / nb
 
     # ---- paper-style FPS: decode + render of ONE centre view on 1 GPU, median
@@ -1011,7 +1012,7 @@ def main():
             "packet_bytes_per_frame": int(statistics.mean(used_bytes)) if used_bytes else None,
             "mpixel_per_s": mpix, "view_fps": value * V, "frame_intervals": frame_intervals,
             "status": Q.STATUS.get(st, st),
-            "keys_per_batch": K_list, "visible_pairs_per_batch": M_list, "stages": stages,
+            "keys_per_batch": K_list, "visible_pairs_per_batch": M_list, "pieces_per_batch": P_list, "stages": stages,
             **({"stages_serial": {"note": "the same stages in serial eager steps (each stage alone on the GPU); "
                                           "`stages` is the pipelined headline region, where entropy/apply run on a "
                                           "side stream under the blend", **stages_serial}} if stages_serial else {}),

@@ -131,8 +131,10 @@ typedef struct {
  *   ranges[n_views*T][2] u32  [first, last+1) of gt in the sorted entries, [0,0) if empty
  *   K (device u32[4])         [0] = entries K of the batch (0 if K > keys_cap: QUEEN_ERR_CAPACITY,
  *                             no entries, all ranges [0,0)), [1] = visible (view, Gaussian) pairs,
- *                             [2] = 1 on capacity overflow
- *   sorted_in_alt             OUT (host): 1 if the sorted result is in vals_alt */
+ *                             [2] = 1 on capacity overflow, [3] = pieces (visible pair x 16x8-tile
+ *                             bucket) of the bucketed emission
+ *   sorted_in_alt             OUT (host): 1 if the sorted result is in vals_alt (always 0: the
+ *                             emission writes vals; keys / keys_alt / vals_alt are scratch) */
 typedef struct {
     int64_t keys_cap;
     uint32_t* keys;
@@ -341,7 +343,7 @@ queen_status queen_wait_rendered(const queen_ctx* ctx, void* stream);
 
 /* Stage profiler (evidence for bench.py): when enabled, every call records CUDA events
  * on its stream around each stage: 0 apply, 1 project, 2 compact (+resets), 3 depth sort,
- * 4 duplicate, 5 tile sort, 6 ranges, 7 blend (k_blend alone), 8 entropy decode, 9 blend
+ * 4 bucket (pieces counted and scattered into tile buckets), 5 emit (entries written in order), 6 ranges, 7 blend (k_blend alone), 8 entropy decode, 9 blend
  * order (the longest-list-first tile schedule built before the blend).  queen_profile_read
  * waits for the recorded events and returns per-stage summed milliseconds and kernel
  * launches (double[10], int64[10]), optionally resetting them.  Not capturable. */

@@ -36,7 +36,7 @@ EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version",
            "queen_densify", "queen_rasterize_rgb8", "queen_render_views_rgb8",
            "queen_rasterize_backward", "queen_project_backward", "queen_decode_backward", "queen_set_options",
            "queen_rasterize_f16", "queen_render_views_f16", "queen_set_sh_rest"]
-STAGES = ["apply", "project", "compact", "depth_sort", "duplicate", "tile_sort", "ranges", "blend", "entropy", "blend_order"]
+STAGES = ["apply", "project", "compact", "depth_sort", "bucket", "emit", "ranges", "blend", "entropy", "blend_order"]
 
 
 class QueenError(RuntimeError):

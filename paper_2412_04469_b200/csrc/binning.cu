@@ -34,12 +34,6 @@
 
 namespace queen {
 
-__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
-    return *reinterpret_cast<const volatile unsigned long long*>(p);
-}
-__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v) {
-    *reinterpret_cast<volatile unsigned long long*>(p) = v;
-}
 // look-back words: one 32-bit (flag | count) word each, so GPU-scope relaxed accesses suffice
 // (volatile would compile to system-scope .STRONG.SYS accesses)
 __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
@@ -51,7 +45,6 @@ __device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-constexpr unsigned long long SCAN_AGG = 1ull << 62, SCAN_INC = 2ull << 62, SCAN_MASK = (1ull << 62) - 1;
 constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_MASK = (1u << 30) - 1;
 constexpr long long SPIN_LIMIT = 1ll << 24;
 #ifndef QUEEN_LB_BATCH
@@ -61,59 +54,11 @@ constexpr int LB_BATCH = QUEEN_LB_BATCH;
 #ifndef QUEEN_OS_MATCH_OR
 #define QUEEN_OS_MATCH_OR 1  // warp match by shared atomicOr (measured: tile sort 488 -> 417 us vs match.any)
 #endif  // onesweep look-back predecessors loaded per round trip
-constexpr int SORT_WARPS = SORT_THREADS / 32;
 
-enum : int { TK_DEPTH = 0, TK_TILE = 4, TK_VIS = 8, TK_DUP = 9, TK_EMIT = 10 };
-#ifndef QUEEN_BIN_BUCKETS
-#define QUEEN_BIN_BUCKETS 1  // bucketed emission (k_piece_* + k_emit) instead of duplication + tile radix passes
-#endif
+enum : int { TK_DEPTH = 0, TK_EMIT = 4 };  // dynamic-tile tickets: depth passes 0..3, emission
 
-// Block-wide exclusive scan of one u32 per thread (256 threads); returns the exclusive
-// prefix and the block total.
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* s_w, uint32_t& total) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t inc = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-    }
-    if (lane == 31) s_w[w] = inc;
-    __syncthreads();
-    uint32_t pre = 0, tot = 0;
-#pragma unroll
-    for (int q = 0; q < SORT_WARPS; ++q) {
-        const uint32_t s = s_w[q];
-        pre += (q < w) ? s : 0u;
-        tot += s;
-    }
-    total = tot;
-    return pre + inc - x;
-}
 
-// Decoupled look-back over 64-bit aggregates (called by one thread).
-__device__ unsigned long long lookback64(unsigned long long* lb, uint32_t tile, unsigned long long agg, DevFlags* fl) {
-    unsigned long long prefix = 0;
-    if (tile == 0) {
-        st_volatile_u64(&lb[0], SCAN_INC | agg);
-        return 0;
-    }
-    st_volatile_u64(&lb[tile], SCAN_AGG | agg);
-    int64_t look = (int64_t)tile - 1;
-    long long spins = 0;
-    while (look >= 0) {
-        const unsigned long long e = ld_volatile_u64(&lb[look]);
-        if ((e >> 62) == 0) {
-            if (++spins > SPIN_LIMIT) { raise_flag(fl, FLAG_TIMEOUT); break; }
-            continue;
-        }
-        prefix += e & SCAN_MASK;
-        if ((e >> 62) == 2) break;
-        --look;
-    }
-    st_volatile_u64(&lb[tile], SCAN_INC | (prefix + agg));
-    return prefix;
-}
+
 
 // ---------------------------------------------------------------------------
 // K3a: per-slab counting.  Each view's elements are cut into slabs of
@@ -249,15 +194,11 @@ __global__ void __launch_bounds__(256) k_slab_sum(const uint32_t* __restrict__ c
     tcounts[(int64_t)v * T + t] = s0 + s1 + s2 + s3;
 }
 
-// Per-view block (1024 threads): view-local exclusive starts of the tile totals, view total,
-// and the tile-digit histograms of the coming tile sort.
+// Per-view block (1024 threads): view-local exclusive starts of the tile totals and the view total.
 __global__ void __launch_bounds__(1024) k_view_scan(const uint32_t* __restrict__ tcounts, int T, uint32_t* lstart,
-                                                    uint32_t* view_tot, uint32_t* hist, int tpasses, int tbits) {
-    __shared__ uint32_t sh[MAX_TILE_PASSES * MAX_BINS];
+                                                    uint32_t* view_tot) {
     __shared__ uint32_t s_w[32];
     const int v = blockIdx.x;
-    for (int q = threadIdx.x; q < tpasses * MAX_BINS; q += blockDim.x) sh[q] = 0;
-    __syncthreads();
     const uint32_t* tc = tcounts + (int64_t)v * T;
     const int per = (T + blockDim.x - 1) / blockDim.x;
     const int t0 = threadIdx.x * per, t1 = min(T, t0 + per);
@@ -277,19 +218,11 @@ __global__ void __launch_bounds__(1024) k_view_scan(const uint32_t* __restrict__
         tot += s_w[q];
     }
     uint32_t run = pre + inc - csum;
-    const uint32_t dmask = (1u << tbits) - 1u;
     for (int t = t0; t < t1; ++t) {
-        const uint32_t c = tc[t];
-        const uint32_t g = (uint32_t)v * (uint32_t)T + (uint32_t)t;
-        lstart[g] = run;
-        run += c;
-        if (c)
-            for (int p = 0; p < tpasses; ++p) atomicAdd(&sh[p * MAX_BINS + ((g >> (p * tbits)) & dmask)], c);
+        lstart[(int64_t)v * T + t] = run;
+        run += tc[t];
     }
     if (threadIdx.x == 0) view_tot[v] = tot;
-    __syncthreads();
-    for (int q = threadIdx.x; q < tpasses * MAX_BINS; q += blockDim.x)
-        if (sh[q]) atomicAdd(&hist[q], sh[q]);
 }
 
 // K, M, overflow flag; slab visible counts -> global exclusive offsets (in place).  One block.
@@ -465,12 +398,8 @@ struct Onesweep {
     static constexpr size_t SMEM = (size_t)TILE * 4 * 2 + (size_t)NW * BINS * 4 + (size_t)BINS * 4 * 2;
 };
 
-// Pass modes (which words travel): OS_KV key + value in, key + value out;
-// OS_PACK key + value in, one packed word out = (key >> pshift) << ibits | value (the key's
-// digits still to come above the value); OS_PACKED packed word in (digit = word >> shift),
-// value = low ibits out; OS_V key + value in, value out (last pass: the keys are not needed
-// after it -- the tile ranges are known from the counts).
-enum : int { OS_KV = 0, OS_PACK = 1, OS_PACKED = 2, OS_V = 3 };
+// Pass mode: key + value in, key + value out (the depth passes over the visible pairs).
+enum : int { OS_KV = 0 };
 
 template <int BITS, int MODE>
 __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_t* __restrict__ kin,
@@ -524,7 +453,7 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
             const uint32_t idx = base + w * (32 * IT) + j * 32 + lane;
             const bool ok = idx < Kn;
             k[j] = ok ? kin[idx] : 0u;
-            val[j] = (ok && MODE != OS_PACKED) ? vin[idx] : 0u;
+            val[j] = ok ? vin[idx] : 0u;
         }
         // warp multisplit in key order (stable): rank among this warp's earlier equal digits.
         // All MATCHes first (independent), then the short shared-memory chain.
@@ -638,161 +567,18 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
             if (d < (uint32_t)BINS) {
                 const uint32_t pos = dstart[d] + whist[w * BINS + d] + (rk[j] & 0xffffu);
                 sk[pos] = k[j];
-                if (MODE != OS_PACKED) sv[pos] = val[j];
+                sv[pos] = val[j];
             }
         }
         __syncthreads();
         const uint32_t nvalid = min((uint32_t)TILE, Kn - base);
-        const uint32_t imask = ibits >= 32 ? 0xffffffffu : (1u << ibits) - 1u;
         for (uint32_t p = threadIdx.x; p < nvalid; p += NT) {
             const uint32_t key = sk[p];
             const uint32_t dest = dbase[(key >> shift) & DMASK] + p;
-            if (MODE == OS_KV) { kout[dest] = key; vout[dest] = sv[p]; }
-            if (MODE == OS_PACK) kout[dest] = ((key >> pshift) << ibits) | sv[p];
-            if (MODE == OS_PACKED) vout[dest] = key & imask;
-            if (MODE == OS_V) vout[dest] = sv[p];
+            kout[dest] = key;
+            vout[dest] = sv[p];
         }
         __syncthreads();
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K3b + K4: offsets of the depth-sorted pairs (decoupled look-back) + duplication.
-// Entry = (gt, Gaussian index), emitted for each pair ty-major, tx-minor.
-// Phase 1 stages the block's 4096 pairs in shared memory (block-local offset, gt of the
-// rect's first tile, Gaussian index, rect width).
-// Phase 2: each warp emits a contiguous run of the block's entries, 32 at a time; every
-// pair has >= 1 entry, so the pairs starting inside a 32-entry chunk are the next <= 31
-// pairs: one shared load + redux.or + popc locates each lane's pair.  Stores coalesce.
-// ---------------------------------------------------------------------------
-constexpr size_t DUP_SMEM = (size_t)SORT_TILE * (4 + 4 + 4 + 2) + 16;
-
-__global__ void __launch_bounds__(SORT_THREADS) k_scan_dup(const uint32_t* __restrict__ dvals_a,
-                                                           const uint32_t* __restrict__ dvals_b,
-                                                           const uint32_t* __restrict__ triv, const uint32_t* count_ptr,
-                                                           const short4* __restrict__ rect, int n_pad, int gx, int gy,
-                                                           uint32_t T, uint32_t* __restrict__ keys,
-                                                           uint32_t* __restrict__ vals, uint32_t cap,
-                                                           unsigned long long* lb, DevFlags* fl, uint32_t* K_out) {
-    extern __shared__ __align__(16) unsigned char dsm[];
-    uint32_t* s_off = reinterpret_cast<uint32_t*>(dsm);       // [SORT_TILE + 1]
-    uint32_t* s_base = s_off + SORT_TILE + 4;                // [SORT_TILE]
-    uint32_t* s_i = s_base + SORT_TILE;                      // [SORT_TILE]
-    uint16_t* s_wx = reinterpret_cast<uint16_t*>(s_i + SORT_TILE);
-    __shared__ uint32_t s_tile, s_w[SORT_WARPS];
-    __shared__ unsigned long long s_prefix;
-    const uint32_t M = *count_ptr;
-    const uint32_t ntiles = (M + SORT_TILE - 1) / SORT_TILE;
-    // the last depth pass skipped (identity) when its digit histogram says so: its input holds the order
-    const uint32_t* __restrict__ dvals = triv[0] == M ? dvals_a : dvals_b;
-    if (threadIdx.x == 0) s_tile = atomicAdd(&fl->tickets[TK_DUP], 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    if (tile >= ntiles) return;
-    const uint32_t base = tile * SORT_TILE + threadIdx.x * SORT_ITEMS;
-    uint32_t nt[SORT_ITEMS];
-    uint32_t tsum = 0;
-    // batch the dependent gathers: all 16 indices (4 x uint4), then all 16 rects, then use them
-    uint32_t jj[SORT_ITEMS];
-#pragma unroll
-    for (int q4 = 0; q4 < SORT_ITEMS / 4; ++q4) {
-        uint4 x = make_uint4(0, 0, 0, 0);
-        if (base + 4 * q4 + 3 < M) x = __ldg(reinterpret_cast<const uint4*>(dvals + base + 4 * q4));
-        else {
-            if (base + 4 * q4 + 0 < M) x.x = __ldg(dvals + base + 4 * q4 + 0);
-            if (base + 4 * q4 + 1 < M) x.y = __ldg(dvals + base + 4 * q4 + 1);
-            if (base + 4 * q4 + 2 < M) x.z = __ldg(dvals + base + 4 * q4 + 2);
-        }
-        jj[4 * q4] = x.x; jj[4 * q4 + 1] = x.y; jj[4 * q4 + 2] = x.z; jj[4 * q4 + 3] = x.w;
-    }
-    short4 rr[SORT_ITEMS];
-#pragma unroll
-    for (int e = 0; e < SORT_ITEMS; ++e) rr[e] = base + e < M ? __ldg(rect + jj[e]) : make_short4(0, 0, 0, 0);
-#pragma unroll
-    for (int e = 0; e < SORT_ITEMS; ++e) {
-        const uint32_t m = base + e;
-        const int q = threadIdx.x * SORT_ITEMS + e;
-        nt[e] = 0;
-        if (m < M) {
-            const uint32_t j = jj[e];
-            const short4 r = rr[e];
-            const uint32_t v = j / (uint32_t)n_pad;
-            const uint32_t wx = (uint32_t)(r.z - r.x + 1), wy = (uint32_t)(r.w - r.y + 1);
-            nt[e] = wx * wy;
-            s_base[q] = v * T + (uint32_t)r.y * (uint32_t)gx + (uint32_t)r.x;
-            s_i[q] = j - v * (uint32_t)n_pad;
-            s_wx[q] = (uint16_t)wx;
-        }
-        tsum += nt[e];
-    }
-    uint32_t total;
-    const uint32_t excl = block_excl_scan(tsum, s_w, total);
-    if (threadIdx.x == 0) {
-        s_prefix = lookback64(lb, tile, total, fl);
-        if (tile == ntiles - 1) {
-            const unsigned long long K = s_prefix + total;
-            if (K > cap) {
-                raise_flag(fl, FLAG_CAPACITY);
-                atomicMax(&fl->info, K);
-            }
-            // overflow: no entry list is produced (the tile sort sees 0 entries and every range is
-            // [0,0)); QUEEN_ERR_CAPACITY carries the K needed.  K_out[2] = overflow flag.
-            K_out[0] = K > cap ? 0u : (uint32_t)K;
-            K_out[2] = K > cap ? 1u : 0u;
-        }
-        s_off[SORT_TILE] = total;
-    }
-    {
-        uint32_t run = excl;
-#pragma unroll
-        for (int e = 0; e < SORT_ITEMS; ++e) {
-            s_off[threadIdx.x * SORT_ITEMS + e] = run;
-            run += nt[e];
-        }
-    }
-    __syncthreads();
-    const unsigned long long gbase = s_prefix;
-    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t nchunks = (total + 31) / 32;
-    const uint32_t c0 = (uint32_t)(((uint64_t)nchunks * w) / SORT_WARPS);
-    const uint32_t c1 = (uint32_t)(((uint64_t)nchunks * (w + 1)) / SORT_WARPS);
-    if (c0 >= c1) return;
-    // pair owning entry 32*c0 (binary search once; all lanes agree)
-    int lo = 0;
-    {
-        const uint32_t p = 32 * c0;
-        int hi = SORT_TILE;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (s_off[mid] <= p) lo = mid; else hi = mid;
-        }
-    }
-    const uint32_t le_mask = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
-    for (uint32_t c = c0; c < c1; ++c) {
-        const uint32_t p0 = 32 * c;
-        const int cand = lo + (int)lane;
-        const uint32_t o = cand <= SORT_TILE ? s_off[cand] : 0xffffffffu;
-        const uint32_t sdel = o - p0;  // start of pair lo+lane relative to p0 (lanes >= 1 start after p0)
-        const uint32_t bit = (lane > 0 && o > p0 && sdel < 32u) ? (1u << sdel) : 0u;
-        const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
-        const int e = lo + __popc(starts & le_mask);
-        const uint32_t p = p0 + lane;
-        if (p < total) {
-            const uint32_t cc = p - s_off[e];
-            const uint32_t wx = s_wx[e];
-            // row = cc / wx by a float estimate + integer fix-ups (cc < 2^24: the estimate is
-            // within one of the quotient)
-            uint32_t row = __float2uint_rz(__uint2float_rn(cc) * __fdividef(1.0f, (float)wx));
-            if (row * wx > cc) --row;
-            if ((row + 1) * wx <= cc) ++row;
-            const uint64_t dst = gbase + p;
-            if (dst < cap) {
-                keys[dst] = s_base[e] + row * (uint32_t)gx + (cc - row * wx);
-                vals[dst] = s_i[e];
-            }
-        }
-        const int e31 = __shfl_sync(0xffffffffu, e, 31);
-        lo = e31 + ((e31 + 1 <= SORT_TILE && s_off[e31 + 1] == p0 + 32) ? 1 : 0);
     }
 }
 
@@ -922,7 +708,8 @@ __device__ __forceinline__ uint32_t emit_start(const uint32_t* row, uint32_t nch
 // meta[1] = emit tiles
 __global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict__ ptotal, int VNB,
                                                      uint32_t* __restrict__ pbase, uint32_t* __restrict__ ebase,
-                                                     uint32_t* __restrict__ meta, uint32_t* __restrict__ ebucket) {
+                                                     uint32_t* __restrict__ meta, uint32_t* __restrict__ ebucket,
+                                                     uint32_t* __restrict__ Kd) {
     __shared__ uint32_t s_w[32], s_e[32];
     __shared__ uint32_t s_carry, s_ecarry;
     if (threadIdx.x == 0) { s_carry = 0; s_ecarry = 0; }
@@ -960,6 +747,7 @@ __global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict_
         ebase[VNB] = s_ecarry;
         meta[0] = s_carry;
         meta[1] = s_ecarry;
+        Kd[3] = s_carry;  // pieces P (evidence: bench's algorithmic bytes)
     }
     __syncthreads();
     for (int b = threadIdx.x; b < VNB; b += blockDim.x) {  // each emit tile's bucket
@@ -1143,8 +931,6 @@ struct EwSmem {
     int diff[(BK_H + 1) * (BK_W + 1)];
     uint32_t base[BK_T];   // final position of each bucket tile's next entry
     uint32_t R[BK_H], C[BK_W];  // the round's pieces covering each bucket row / column
-    uint32_t pstart[33];        // entry offsets of the round's pieces (+ total)
-    uint32_t plr[32], pgi[32];
 };
 
 __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restrict__ piece_gi,
@@ -1157,14 +943,11 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                                                         uint32_t* __restrict__ vals, uint32_t* lb, uint32_t* ticket,
                                                         DevFlags* fl) {
     __shared__ EwSmem sm[EW_WARPS];
-    __shared__ uint32_t s_rcp[BK_W + 1];  // ceil(2^16 / w): row = (o * s_rcp[w]) >> 16 = o / w for o < 128
-    if (threadIdx.x <= BK_W) s_rcp[threadIdx.x] = threadIdx.x ? (65536u + threadIdx.x - 1) / threadIdx.x : 0u;
-    __syncthreads();
     const int lane = threadIdx.x & 31;
     EwSmem& S = sm[threadIdx.x >> 5];
     if (visible_pairs(Kd) == 0) return;
     const uint32_t NE = meta[1];
-    const uint32_t le_mask = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;
+    const uint32_t lt_mask = (1u << lane) - 1u;
     for (;;) {
         uint32_t t = 0;
         if (lane == 0) t = atomicAdd(ticket, 1u);
@@ -1272,43 +1055,13 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
                 const uint32_t c = __ballot_sync(0xffffffffu, (cm >> x) & 1u);
                 if (lane == 0) S.C[x] = c;
             }
-            // the round's entries flattened 32 per step over the lanes, in (piece, row, column)
-            // order: lane i takes entry e0 + i and finds its piece by one redux.or over the piece
-            // starts in the step (every piece has >= 1 entry)
-            const uint32_t ne = has ? (lx1 - lx0 + 1) * (ly1 - ly0 + 1) : 0u;
-            uint32_t incl = ne;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const uint32_t E = __shfl_sync(0xffffffffu, incl, 31);
-            S.pstart[lane] = incl - ne;
-            S.plr[lane] = lr;
-            S.pgi[lane] = gi;
-            if (lane == 31) S.pstart[32] = E;
             __syncwarp();
-            int pp = 0;  // piece of entry e0 (lanes agree)
-            for (uint32_t e0 = 0; e0 < E; e0 += 32) {
-                const uint32_t e = e0 + lane;
-                const int cand = pp + lane + 1;
-                const uint32_t st = cand <= 32 ? S.pstart[cand] : 0xffffffffu;
-                const uint32_t d = st - e0;  // start of piece cand relative to e0
-                const uint32_t bit = (st > e0 && d < 32u) ? (1u << d) : 0u;
-                const uint32_t starts = __reduce_or_sync(0xffffffffu, bit);
-                const int p = pp + __popc(starts & le_mask);
-                if (e < E) {
-                    const uint32_t plr = S.plr[p];
-                    const uint32_t px0 = plr & 15, px1 = (plr >> 4) & 15, py0 = (plr >> 8) & 7;
-                    const uint32_t wdt = px1 - px0 + 1;
-                    const uint32_t o = e - S.pstart[p];
-                    const uint32_t row = (o * s_rcp[wdt]) >> 16;  // exact: o < 128
-                    const uint32_t ly = py0 + row, lx = px0 + (o - row * wdt);
-                    const uint32_t rank = __popc(S.R[ly] & S.C[lx] & ((1u << p) - 1u));
-                    vals[S.base[ly * BK_W + lx] + rank] = S.pgi[p];
+            if (has) {  // (flattening the entries over the lanes measured no faster: 208 vs 202 us)
+                for (uint32_t ly = ly0; ly <= ly1; ++ly) {
+                    const uint32_t rr = S.R[ly] & lt_mask;
+                    for (uint32_t lx = lx0; lx <= lx1; ++lx)
+                        vals[S.base[ly * BK_W + lx] + __popc(rr & S.C[lx])] = gi;
                 }
-                const int p31 = __shfl_sync(0xffffffffu, p, 31);
-                pp = p31 + ((p31 + 1 <= 32 && S.pstart[p31 + 1] == e0 + 32) ? 1 : 0);
             }
             __syncwarp();
 #pragma unroll
@@ -1386,11 +1139,7 @@ cudaError_t init_binning_attributes() {
     if ((e = cudaFuncSetAttribute(k_piece_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC_MAX_SMEM)) ||
         (e = cudaFuncSetAttribute(k_piece_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC_MAX_SMEM)))
         return e;
-    if ((e = onesweep_attr<8, OS_KV>()) || (e = onesweep_attr<8, OS_PACK>()) || (e = onesweep_attr<8, OS_PACKED>()) ||
-        (e = onesweep_attr<8, OS_V>()) || (e = onesweep_attr<9, OS_KV>()) || (e = onesweep_attr<9, OS_PACK>()) ||
-        (e = onesweep_attr<9, OS_PACKED>()) || (e = onesweep_attr<9, OS_V>()))
-        return e;
-    if ((e = cudaFuncSetAttribute(k_scan_dup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DUP_SMEM))) return e;
+    if ((e = onesweep_attr<8, OS_KV>()) || (e = onesweep_attr<9, OS_KV>())) return e;
     return cudaFuncSetAttribute(k_slab_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(int) * BIN_MAX_SMEM_WORDS));
 }
@@ -1403,17 +1152,6 @@ static void onesweep(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, u
         kin, vin, kout, vout, count, cap, shift, pshift, ibits, hist_excl, lb, ticket, fl, triv);
 }
 
-template <int BITS>
-static void onesweep_mode(int mode, const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
-                          const uint32_t* count, uint32_t cap, int shift, int pshift, int ibits, const uint32_t* hist_excl,
-                          uint32_t* lb, uint32_t* ticket, DevFlags* fl, cudaStream_t s) {
-    switch (mode) {
-        case OS_KV: onesweep<BITS, OS_KV>(kin, vin, kout, vout, count, cap, shift, pshift, ibits, hist_excl, lb, ticket, fl, s); break;
-        case OS_PACK: onesweep<BITS, OS_PACK>(kin, vin, kout, vout, count, cap, shift, pshift, ibits, hist_excl, lb, ticket, fl, s); break;
-        case OS_PACKED: onesweep<BITS, OS_PACKED>(kin, vin, kout, vout, count, cap, shift, pshift, ibits, hist_excl, lb, ticket, fl, s); break;
-        default: onesweep<BITS, OS_V>(kin, vin, kout, vout, count, cap, shift, pshift, ibits, hist_excl, lb, ticket, fl, s); break;
-    }
-}
 
 cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
                             const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof) {
@@ -1421,16 +1159,11 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     const int64_t T = (int64_t)gx * gy;
     const int64_t count = (int64_t)n_views * proj.n_pad;
     const uint32_t cap = (uint32_t)bins.keys_cap;
-    const int gbits = tile_gbits(T * n_views);
-    const int tbits = tile_digit_bits(gbits);
-    const int tpasses = tile_passes(gbits);
     const BinPlan bp = bin_plan(proj.n_pad, n_views, W, H);
     unsigned char* ws = static_cast<unsigned char*>(scratch);
     uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist);  // [depth 4 | tile 4][MAX_BINS] counts, then excl
-    uint32_t* hist_excl = hist + (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS;
-    unsigned long long* dup_lb = reinterpret_cast<unsigned long long*>(ws + L.dup_lb);
+    uint32_t* hist_excl = hist + DEPTH_PASSES * MAX_BINS;
     uint32_t* depth_lb = reinterpret_cast<uint32_t*>(ws + L.depth_lb);
-    uint32_t* tile_lb = reinterpret_cast<uint32_t*>(ws + L.tile_lb);
     uint32_t* dk[2] = {reinterpret_cast<uint32_t*>(ws + L.dkeys), reinterpret_cast<uint32_t*>(ws + L.dkeys_alt)};
     uint32_t* dv[2] = {reinterpret_cast<uint32_t*>(ws + L.dvals), reinterpret_cast<uint32_t*>(ws + L.dvals_alt)};
     uint32_t* tcounts = reinterpret_cast<uint32_t*>(ws + L.counts);  // per-tile totals | view-local starts
@@ -1438,9 +1171,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     uint32_t* view_tot = reinterpret_cast<uint32_t*>(ws + L.view_tot);
     uint32_t* scount = reinterpret_cast<uint32_t*>(ws + L.slab_counts);
     uint32_t* svis = reinterpret_cast<uint32_t*>(ws + L.slab_vis);
-    const int64_t elem_tiles = (count + SORT_TILE - 1) / SORT_TILE;
     const int64_t os_elem_tiles = (count + OS_TILE - 1) / OS_TILE;
-    const int64_t os_key_tiles = ((int64_t)cap + OS_TILE - 1) / OS_TILE;
     uint32_t* Kd = bins.K;      // [0] = K entries
     uint32_t* Md = bins.K + 1;  // [1] = M visible pairs
     const int sms = num_sms();
@@ -1448,19 +1179,14 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     cudaError_t e;
     prof->begin(ST_COMPACT, s);
     if ((e = cudaMemsetAsync(fl->tickets, 0, sizeof(fl->tickets), s))) return e;
-    if ((e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS, s))) return e;
-#if !QUEEN_BIN_BUCKETS
-    if ((e = cudaMemsetAsync(dup_lb, 0, sizeof(unsigned long long) * (elem_tiles + 1), s))) return e;
-#endif
+    if ((e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * DEPTH_PASSES * MAX_BINS, s))) return e;
+
     if ((e = cudaMemsetAsync(depth_lb, 0, sizeof(uint32_t) * DEPTH_PASSES * MAX_BINS * (size_t)(os_elem_tiles + 1), s)))
         return e;
     uint32_t* dminmax = reinterpret_cast<uint32_t*>(ws + L.dminmax);
     if ((e = cudaMemsetAsync(dminmax, 0xff, sizeof(uint32_t), s))) return e;       // min <- 0xffffffff
     if ((e = cudaMemsetAsync(dminmax + 1, 0, sizeof(uint32_t), s))) return e;      // max <- 0
-#if !QUEEN_BIN_BUCKETS
-    if ((e = cudaMemsetAsync(tile_lb, 0, sizeof(uint32_t) * (size_t)tpasses * (1 << tbits) * (size_t)(os_key_tiles + 1), s)))
-        return e;
-#endif
+
     if ((e = cudaMemsetAsync(bins.K, 0, sizeof(uint32_t) * 4, s))) return e;
     if (bp.slabs > 0) {
         k_slab_count<<<(unsigned)bp.slabs, SLAB_THREADS, sizeof(int) * dplane, s>>>(
@@ -1468,8 +1194,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
             scount, svis, dminmax);
         k_slab_sum<<<dim3((unsigned)((T + 255) / 256), (unsigned)n_views), 256, 0, s>>>(scount, (int)bp.spv, (int)T,
                                                                                         tcounts);
-        k_view_scan<<<n_views, 1024, 0, s>>>(tcounts, (int)T, lstart, view_tot, hist + DEPTH_PASSES * MAX_BINS, tpasses,
-                                             tbits);
+        k_view_scan<<<n_views, 1024, 0, s>>>(tcounts, (int)T, lstart, view_tot);
     } else {
         if ((e = cudaMemsetAsync(tcounts, 0, sizeof(uint32_t) * 2 * T * n_views, s))) return e;
         if ((e = cudaMemsetAsync(view_tot, 0, sizeof(uint32_t) * n_views, s))) return e;
@@ -1498,7 +1223,6 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
         cur ^= 1;
     }
     prof->end(s, DEPTH_PASSES + 1);
-#if QUEEN_BIN_BUCKETS
     // per-tile entry counts -> ranges (the emission writes entries at their final positions)
     prof->begin(ST_RANGES, s);
     k_ranges_finalize<<<sms * 2, 256, 0, s>>>(tcounts, lstart, view_tot, n_views, (uint32_t)T, cap, Kd,
@@ -1542,7 +1266,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     if (chunks > 0) {
         k_piece_count<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, rlo, rhi);
         k_piece_colscan<<<(unsigned)((bg.VNB + 7) / 8), 256, 0, s>>>(pcnt, Kd, bg, ptotal);
-        k_piece_base<<<1, 1024, 0, s>>>(ptotal, bg.VNB, pbase, ebase, meta, ebucket);
+        k_piece_base<<<1, 1024, 0, s>>>(ptotal, bg.VNB, pbase, ebase, meta, ebucket, Kd);
         // warps per chunk: each holds VNB cursors in shared memory
         int wpc = (int)std::max<int64_t>(1, std::min<int64_t>(PS_MAX_WARPS, (int64_t)PC_MAX_SMEM / (4 * (int64_t)bg.VNB)));
         while (wpc > 1 && (PC_CH / wpc) % (32 * PS_ROUNDS)) --wpc;
@@ -1560,53 +1284,6 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     prof->end(s, chunks > 0 ? 2 : 0);
     bins.sorted_in_alt = 0;
     return cudaGetLastError();
-#else
-    // offsets in depth order + duplication
-    prof->begin(ST_DUPLICATE, s);
-    if (elem_tiles > 0)
-        k_scan_dup<<<(unsigned)elem_tiles, SORT_THREADS, DUP_SMEM, s>>>(dv[cur ^ 1], dv[cur],
-                                                                         hist + (DEPTH_PASSES - 1) * MAX_BINS, Md,
-                                                                         reinterpret_cast<const short4*>(proj.rect),
-                                                                         proj.n_pad, gx, gy, (uint32_t)T, bins.keys,
-                                                                         bins.vals, cap, dup_lb, fl, Kd);
-    prof->end(s);
-    // per-tile entry counts -> ranges
-    prof->begin(ST_RANGES, s);
-    k_ranges_finalize<<<sms * 2, 256, 0, s>>>(tcounts, lstart, view_tot, n_views, (uint32_t)T, cap, Kd,
-                                              reinterpret_cast<uint2*>(bins.ranges));
-    prof->end(s);
-    // tile digits on the K entries
-    prof->begin(ST_TILE_SORT, s);
-    uint32_t* thist = hist + DEPTH_PASSES * MAX_BINS;
-    uint32_t* thist_excl = hist_excl + DEPTH_PASSES * MAX_BINS;
-    k_hist_scan<<<1, 32 * MAX_TILE_PASSES, 0, s>>>(thist, thist_excl, tpasses, 1 << tbits);
-    // The keys are not needed after the last pass (ranges come from the counts), so the last
-    // pass writes values only; with two passes whose remaining digit fits beside the
-    // Gaussian index, the first pass writes one packed word and the second reads only it.
-    int ibits = 1;
-    while ((1ll << ibits) < (int64_t)proj.n_pad) ++ibits;
-    const bool packed = tpasses == 2 && (gbits - tbits) + ibits <= 32;
-    uint32_t* ka = bins.keys;
-    uint32_t* kb = bins.keys_alt;
-    uint32_t* va = bins.vals;
-    uint32_t* vb = bins.vals_alt;
-    for (int p = 0; p < tpasses; ++p) {
-        uint32_t* lbp = tile_lb + (size_t)p * (1 << tbits) * (os_key_tiles + 1);
-        const int mode = packed ? (p == 0 ? OS_PACK : OS_PACKED) : (p == tpasses - 1 ? OS_V : OS_KV);
-        const int shift = mode == OS_PACKED ? ibits : tbits * p;
-        if (tbits == 9)
-            onesweep_mode<9>(mode, ka, va, kb, vb, Kd, cap, shift, tbits, ibits, thist_excl + p * MAX_BINS, lbp,
-                             &fl->tickets[TK_TILE + p], fl, s);
-        else
-            onesweep_mode<8>(mode, ka, va, kb, vb, Kd, cap, shift, tbits, ibits, thist_excl + p * MAX_BINS, lbp,
-                             &fl->tickets[TK_TILE + p], fl, s);
-        uint32_t* tk = ka; ka = kb; kb = tk;
-        uint32_t* tv = va; va = vb; vb = tv;
-    }
-    prof->end(s, tpasses + 1);
-    bins.sorted_in_alt = va == bins.vals_alt ? 1 : 0;
-    return cudaGetLastError();
-#endif
 }
 
 }  // namespace queen

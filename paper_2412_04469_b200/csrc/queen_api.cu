@@ -33,7 +33,6 @@ float host_theta0(float tau, float g0, float g1) {
 }
 cudaError_t init_binning_attributes();
 cudaError_t init_entropy_attributes();
-int key_passes(int64_t gtiles);
 size_t ans_encode(const int8_t* lat, int L, int n, int n_pad, std::vector<unsigned char>& out);
 cudaError_t launch_ans_decode(const void* stream_dev, int64_t bytes, int L, int n, int n_pad, int8_t* out,
                               DevFlags* fl, cudaStream_t s);
@@ -188,10 +187,10 @@ queen_status queen_decode_residuals(queen_ctx* ctx, const queen_packet* pkt, flo
     if (e != cudaSuccess) return cuda_fail(ctx, e, "decode");
     if (coo_out) {
         if (pkt->pos_kind == QUEEN_POS_GATES) {
-            // scratch for block counts: the sort look-back region (not in use concurrently)
-            void* scratch = static_cast<unsigned char*>(ctx->ws) + ctx->L.tile_lb;
+            // scratch for block counts: the depth-key buffer (not in use concurrently)
+            void* scratch = static_cast<unsigned char*>(ctx->ws) + ctx->L.dkeys;
             size_t need = sizeof(uint32_t) * ((pkt->n + 1023) / 1024 + 1);
-            if (need > ctx->L.total_scratch - ctx->L.tile_lb) return fail(ctx, QUEEN_ERR_SHAPE, "workspace too small for gate compaction");
+            if (need > ctx->L.dkeys_alt - ctx->L.dkeys) return fail(ctx, QUEEN_ERR_SHAPE, "workspace too small for gate compaction");
             e = launch_gate_compact(*pkt, coo_idx_out, coo_val_out, k_out, scratch, fl, s);
         } else if (pkt->pos_kind == QUEEN_POS_COO) {
             e = launch_coo_copy(*pkt, coo_idx_out, coo_val_out, k_out, fl, s);

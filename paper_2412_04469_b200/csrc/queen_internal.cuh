@@ -68,19 +68,8 @@ struct CamBatch {
 //   tile passes  : ceil(gbits / TILE_DIGIT_BITS) x (8 or 9) bits over the K entries
 constexpr int DEPTH_PASSES = 4;    // 3 x 9-bit digits of (depth - min depth), + bits 27..31
 constexpr int DEPTH_BITS = 9;
-constexpr int MAX_TILE_PASSES = 4;
 constexpr int MAX_BINS = 512;
 
-inline int tile_gbits(int64_t gtiles) {
-    int g = 1;
-    while ((1ll << g) < gtiles) ++g;
-    return g;
-}
-inline int tile_digit_bits(int gbits) { return gbits <= 16 ? 8 : (gbits <= 18 ? 9 : 8); }
-inline int tile_passes(int gbits) {
-    const int db = tile_digit_bits(gbits);
-    return (gbits + db - 1) / db;
-}
 
 // Binning counts (binning.cu K3a): each view's elements are cut into slabs of S consecutive
 // indices; one CTA per slab keeps the view's tile grid in shared memory as a difference
@@ -128,7 +117,7 @@ constexpr int ORDER_BINS = 64;
 // Workspace carve-up (bytes, 256-aligned) for (n_pad, n_views, W, H, keys_cap).
 struct WsLayout {
     // scratch (bin_sort)
-    size_t flags, hist, dminmax, dup_lb, depth_lb, tile_lb, dkeys, dkeys_alt, dvals, dvals_alt, counts, view_tot, slab_counts,
+    size_t flags, hist, dminmax, depth_lb, dkeys, dkeys_alt, dvals, dvals_alt, counts, view_tot, slab_counts,
         slab_vis, select, pcnt, pbuck, emit_lb, eplan, order, total_scratch;
     // render_views / render_mask buffers
     size_t rec, depth, tiles, rect, keys, keys_alt, vals, vals_alt, ranges, K, mask_tmp, total;
@@ -148,11 +137,9 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     L.os_elem_tiles = (L.elems + OS_TILE - 1) / OS_TILE;
     size_t o = 0;
     L.flags = o; o += align256(sizeof(DevFlags));
-    L.hist = o; o += align256(sizeof(uint32_t) * (DEPTH_PASSES + MAX_TILE_PASSES) * MAX_BINS * 2);
+    L.hist = o; o += align256(sizeof(uint32_t) * DEPTH_PASSES * MAX_BINS * 2);
     L.dminmax = o; o += align256(sizeof(uint32_t) * 2);
-    L.dup_lb = o; o += align256(sizeof(unsigned long long) * (L.elem_tiles + 1));
     L.depth_lb = o; o += align256(sizeof(uint32_t) * DEPTH_PASSES * MAX_BINS * (L.os_elem_tiles + 1));
-    L.tile_lb = o; o += align256(sizeof(uint32_t) * MAX_TILE_PASSES * MAX_BINS * (L.os_key_tiles + 1));
     L.dkeys = o; o += align256(sizeof(uint32_t) * L.elems);
     L.dkeys_alt = o; o += align256(sizeof(uint32_t) * L.elems);
     L.dvals = o; o += align256(sizeof(uint32_t) * L.elems);
@@ -192,8 +179,7 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
 // every scratch region of `need` fits in the corresponding region of `have`
 inline bool scratch_fits(const WsLayout& need, const WsLayout& have) {
     const size_t WsLayout::*r[] = {&WsLayout::flags,      &WsLayout::hist,        &WsLayout::dminmax,
-                                   &WsLayout::dup_lb,
-                                   &WsLayout::depth_lb,   &WsLayout::tile_lb,     &WsLayout::dkeys,
+                                   &WsLayout::depth_lb,   &WsLayout::dkeys,
                                    &WsLayout::dkeys_alt,  &WsLayout::dvals,       &WsLayout::dvals_alt,
                                    &WsLayout::counts,     &WsLayout::view_tot,    &WsLayout::slab_counts,
                                    &WsLayout::slab_vis,   &WsLayout::select,      &WsLayout::pcnt,

@@ -70,15 +70,16 @@ class Stages:
                     rect=to_np(self.rect))
 
     def bins_np(self):
-        """K, M, the sorted Gaussian indices, the ranges, and each entry's gt (rebuilt from the
-        ranges: after queen_bin_sort the key buffers are scratch)."""
+        """K, M, P (pieces), the sorted Gaussian indices, the ranges, and each entry's gt (rebuilt
+        from the ranges: after queen_bin_sort the key buffers are scratch)."""
         torch.cuda.synchronize()
         K = int(to_np(self.K)[0])
         vs = self.vals_alt if self.bins.sorted_in_alt else self.vals
         ranges = to_np(self.ranges).view(np.uint32)
         lens = (ranges[:, 1].astype(np.int64) - ranges[:, 0].astype(np.int64))
         keys = np.repeat(np.arange(ranges.shape[0], dtype=np.uint32), lens)
-        return dict(K=K, M=int(to_np(self.K)[1]), keys=keys, vals=to_np(vs[:K]).view(np.uint32), ranges=ranges)
+        return dict(K=K, M=int(to_np(self.K)[1]), P=int(to_np(self.K)[3]), keys=keys, vals=to_np(vs[:K]).view(np.uint32),
+                    ranges=ranges)
 
     def image_np(self):
         torch.cuda.synchronize()
