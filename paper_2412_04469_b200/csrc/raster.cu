@@ -203,27 +203,17 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
 #pragma unroll
             for (int e = 0; e < BATCH / 32; ++e) {
                 const int q = (threadIdx.x & 31) + 32 * e;
-                // band flags (bit k: the record can reach a pixel centre of the warp's 16 x 4 band k)
-                // ride in the low bits of the entry's byte offset (a multiple of 16)
-                uint32_t bands = q < cnt ? (1u << NP) - 1u : 0u;
-                if (WMASK && bands) {
-                    bands = 0;
-#pragma unroll
-                    for (int k = 0; k < NP; ++k)
-                        if (touches(sA[s][q], sB[s][q], wx0, wx0 + 15.0f, wy0 + 4.0f * k, wy0 + 4.0f * k + 3.0f))
-                            bands |= 1u << k;
-                }
-                const bool want = bands != 0;
+                bool want = q < cnt;
+                if (WMASK && want) want = touches(sA[s][q], sB[s][q], wx0, wx0 + 15.0f, wy0, wy0 + (float)((32 / 16) * RPT - 1));
                 const uint32_t bal = __ballot_sync(0xffffffffu, want);
-                if (want) lst[nq + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = (uint16_t)(q * 16 + bands);
+                if (want) lst[nq + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = (uint16_t)(q * 16);
                 nq += __popc(bal);
             }
             __syncwarp();
 #pragma unroll BLEND_UNROLL
             for (int i = 0; i < nq; ++i) {
                 // records addressed by byte offset (no per-record index scaling)
-                const uint32_t ent = lst[i];
-                const uint32_t qo = ent & ~15u, bands = ent & 15u;
+                const uint32_t qo = lst[i];
 #define QREC(arr) (*reinterpret_cast<const float4*>(reinterpret_cast<const char*>(arr[s]) + qo))
                 const float4 a = QREC(sA);  // u, v, hx, hy
                 const float dx = a.x - fx;
@@ -248,15 +238,11 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
                 bool anyh = false;
 #pragma unroll
                 for (int k = 0; k < NP; ++k) {
-                    h[2 * k] = h[2 * k + 1] = false;
-                    qq[k] = make_float2(0.f, 0.f);
-                    if ((bands >> k) & 1u) {  // warp-uniform: a band the record cannot reach is not evaluated
-                        const float2 dy = __fadd2_rn(vv, nfy[k]);  // v - y, exactly
-                        qq[k] = __ffma2_rn(__ffma2_rn(cc, dy, tb2), dy, ta2);  // Horner in dy
-                        h[2 * k] = !cull && hit(p[k].T.x, qq[k].x, bq.w);
-                        h[2 * k + 1] = !cull && hit(p[k].T.y, qq[k].y, bq.w);
-                        anyh |= h[2 * k] | h[2 * k + 1];
-                    }
+                    const float2 dy = __fadd2_rn(vv, nfy[k]);  // v - y, exactly
+                    qq[k] = __ffma2_rn(__ffma2_rn(cc, dy, tb2), dy, ta2);  // Horner in dy
+                    h[2 * k] = !cull && hit(p[k].T.x, qq[k].x, bq.w);
+                    h[2 * k + 1] = !cull && hit(p[k].T.y, qq[k].y, bq.w);
+                    anyh |= h[2 * k] | h[2 * k + 1];
                 }
                 if (COUNT) {
 #pragma unroll
@@ -269,8 +255,8 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
                 bool any_pair = false;
 #pragma unroll
                 for (int k = 0; k < NP; ++k) {
-                    doit[k] = ((bands >> k) & 1u) && (BLEND_PAIRSKIP ? __any_sync(0xffffffffu, h[2 * k] | h[2 * k + 1])
-                                                                      : __any_sync(0xffffffffu, anyh));
+                    doit[k] = BLEND_PAIRSKIP ? __any_sync(0xffffffffu, h[2 * k] | h[2 * k + 1])
+                                             : __any_sync(0xffffffffu, anyh);
                     any_pair |= doit[k];
                 }
                 if (any_pair) {
