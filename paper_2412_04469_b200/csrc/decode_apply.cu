@@ -15,6 +15,10 @@ namespace queen {
 #ifndef QUEEN_DA_ROWS
 #define QUEEN_DA_ROWS 4  // measured N3DV apply (L2 flushed): 8 rows x 2 blocks 57 us, 6 x 3 45 us, 4 x 4 41 us
 #endif
+#ifndef QUEEN_DA_SX
+#define QUEEN_DA_SX 32
+#endif
+constexpr int DA_SX = QUEEN_DA_SX;  // Gaussian blocks per grid super-tile
 constexpr int DA_ROWS = QUEEN_DA_ROWS;      // attribute rows per work group (all loads in flight at once)
 constexpr int DA_MAX_GROUPS = 5 + (4 + 3 + 1 + 3 + 45 + DA_ROWS - 1) / DA_ROWS + 1;  // worst case at degree 3, + gates
 
@@ -73,11 +77,11 @@ __device__ __forceinline__ void coo_entry(float* planes, int n, int64_t n_pad, c
 template <bool F32, bool APPLY, bool GATES, bool SET = false>
 __global__ void __launch_bounds__(256, QUEEN_DA_MINB) k_decode_apply(DecodeParams p) {
     extern __shared__ float sdec[];
-    // grid = groups x Gaussian blocks, group-major (measured: gid-fastest, which keeps a
-    // category's latent rows in L2 across its groups, is slower -- N3DV 41 -> 49 us, stress
-    // 573 -> 628 us -- the concurrent blocks then stream ~14 planes at once instead of ~1)
-    const int gid = blockIdx.x / p.xblocks;
-    if (gid >= p.ngroups) {
+    // grid: super-tiles of DA_SX Gaussian blocks; inside one, group-major.  Every group of a
+    // category re-reads the category's latent rows, which then come from L2 (a super-tile's
+    // latents are <= DA_SX * 1024 * 16 B), while the concurrent blocks still stream one plane
+    // at a time.  (Fully gid-fastest was slower: N3DV 41 -> 49 us, stress 573 -> 628 us.)
+    if ((int)blockIdx.x >= p.ngroups * p.xblocks) {
         // fused COO scatter blocks (COO mode: the decode groups never touch position rows)
         int k = p.coo_k;
         if (p.coo_kdev) k = min(max(*p.coo_kdev, 0), p.coo_k);
@@ -85,9 +89,14 @@ __global__ void __launch_bounds__(256, QUEEN_DA_MINB) k_decode_apply(DecodeParam
         if (j < k) coo_entry(p.planes, p.n, p.n_pad, p.coo_idx, p.coo_val, p.coo_k, j, p.fl);
         return;
     }
+    const int sup = (int)blockIdx.x / (p.ngroups * DA_SX);
+    const int rem = (int)blockIdx.x - sup * p.ngroups * DA_SX;
+    const int width = min(DA_SX, p.xblocks - sup * DA_SX);  // Gaussian blocks in this super-tile
+    const int gid = rem / width;
+    const int xb = sup * DA_SX + (rem - gid * width);
     const int c = p.g_c[gid];
     const int64_t np = p.n_pad;
-    const int i0 = ((blockIdx.x - gid * p.xblocks) * blockDim.x + threadIdx.x) * 4;
+    const int i0 = (xb * blockDim.x + threadIdx.x) * 4;
     if (c == 5) {
         if (!(GATES && APPLY) || i0 >= p.n) return;
         // a4 fused: dp = g l_p for log alpha > theta0 (R#6), p += dp
