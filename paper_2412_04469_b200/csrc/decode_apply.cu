@@ -15,10 +15,10 @@ namespace queen {
 #ifndef QUEEN_DA_ROWS
 #define QUEEN_DA_ROWS 4  // measured N3DV apply (L2 flushed): 8 rows x 2 blocks 57 us, 6 x 3 45 us, 4 x 4 41 us
 #endif
-#ifndef QUEEN_DA_SX
-#define QUEEN_DA_SX 32
-#endif
-constexpr int DA_SX = QUEEN_DA_SX;  // Gaussian blocks per grid super-tile
+// Gaussian blocks per grid super-tile: group-major over all blocks while a category's latent rows
+// stay in L2 anyway; super-tiles of 128 blocks once they do not (measured, apply stage with L2
+// flushed: stress 590 -> 516 us with 128; N3DV 42.8 us group-major vs 44.1 with 128, 47.4 with 32)
+inline int da_super(int n) { return n > (1 << 20) ? 128 : 1 << 30; }
 constexpr int DA_ROWS = QUEEN_DA_ROWS;      // attribute rows per work group (all loads in flight at once)
 constexpr int DA_MAX_GROUPS = 5 + (4 + 3 + 1 + 3 + 45 + DA_ROWS - 1) / DA_ROWS + 1;  // worst case at degree 3, + gates
 
@@ -37,6 +37,7 @@ struct DecodeParams {
     int ngroups;
     int g_c[DA_MAX_GROUPS], g_m0[DA_MAX_GROUPS], g_m1[DA_MAX_GROUPS];
     int xblocks;                 // Gaussian blocks per group
+    int sx;                      // Gaussian blocks per grid super-tile
     int coo_k;                   // COO capacity (entries); 0 = no fused scatter
     const int32_t* coo_kdev;
     const uint32_t* coo_idx;
@@ -77,10 +78,10 @@ __device__ __forceinline__ void coo_entry(float* planes, int n, int64_t n_pad, c
 template <bool F32, bool APPLY, bool GATES, bool SET = false>
 __global__ void __launch_bounds__(256, QUEEN_DA_MINB) k_decode_apply(DecodeParams p) {
     extern __shared__ float sdec[];
-    // grid: super-tiles of DA_SX Gaussian blocks; inside one, group-major.  Every group of a
-    // category re-reads the category's latent rows, which then come from L2 (a super-tile's
-    // latents are <= DA_SX * 1024 * 16 B), while the concurrent blocks still stream one plane
-    // at a time.  (Fully gid-fastest was slower: N3DV 41 -> 49 us, stress 573 -> 628 us.)
+    // grid: super-tiles of p.sx Gaussian blocks (da_super); inside one, group-major.  Every group
+    // of a category re-reads the category's latent rows, which then come from L2 (a super-tile's
+    // latents are <= sx * 1024 * 16 B), while the concurrent blocks still stream one plane at a
+    // time.  (Fully gid-fastest was slower: N3DV 41 -> 49 us, stress 573 -> 628 us.)
     if ((int)blockIdx.x >= p.ngroups * p.xblocks) {
         // fused COO scatter blocks (COO mode: the decode groups never touch position rows)
         int k = p.coo_k;
@@ -89,11 +90,12 @@ __global__ void __launch_bounds__(256, QUEEN_DA_MINB) k_decode_apply(DecodeParam
         if (j < k) coo_entry(p.planes, p.n, p.n_pad, p.coo_idx, p.coo_val, p.coo_k, j, p.fl);
         return;
     }
-    const int sup = (int)blockIdx.x / (p.ngroups * DA_SX);
-    const int rem = (int)blockIdx.x - sup * p.ngroups * DA_SX;
-    const int width = min(DA_SX, p.xblocks - sup * DA_SX);  // Gaussian blocks in this super-tile
+    const int sx = min(p.sx, p.xblocks);
+    const int sup = (int)blockIdx.x / (p.ngroups * sx);
+    const int rem = (int)blockIdx.x - sup * p.ngroups * sx;
+    const int width = min(sx, p.xblocks - sup * sx);  // Gaussian blocks in this super-tile
     const int gid = rem / width;
-    const int xb = sup * DA_SX + (rem - gid * width);
+    const int xb = sup * sx + (rem - gid * width);
     const int c = p.g_c[gid];
     const int64_t np = p.n_pad;
     const int i0 = (xb * blockDim.x + threadIdx.x) * 4;
@@ -402,6 +404,7 @@ cudaError_t launch_decode_apply(const queen_packet& pk, float* planes, float* re
     p.ngroups = ng;
     const int threads = 256;
     p.xblocks = (pk.n + 4 * threads - 1) / (4 * threads);
+    p.sx = da_super(pk.n);
     const bool coo = apply_attrs && apply_pos && pk.pos_kind == QUEEN_POS_COO && pk.k > 0;
     int coo_blocks = 0;
     if (coo) {
@@ -465,6 +468,7 @@ cudaError_t launch_set_sh_rest(float* planes, int n, int n_pad, int deg, const i
     p.ngroups = ng;
     const int threads = 256;
     p.xblocks = (n + 4 * threads - 1) / (4 * threads);
+    p.sx = da_super(n);
     const int64_t blocks = (int64_t)p.xblocks * ng;
     if (blocks > 0 && M > 0)
         k_decode_apply<false, true, false, true><<<(unsigned)blocks, threads, sizeof(float) * (size_t)max_dec, s>>>(p);
