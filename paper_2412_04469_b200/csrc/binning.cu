@@ -1278,7 +1278,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     if (chunks > 0)
         k_emit_plan<<<(unsigned)((etiles + 255) / 256), 256, 0, s>>>(pcnt, ptotal, ebase, ebucket, meta, Kd, bg, plan);
     if (chunks > 0)
-        k_emit<<<emit_grid(), EW_WARPS * 32, 0, s>>>(bins.keys_alt, bins.keys, plan, pbase, meta, Kd,
+        k_emit<<<(unsigned)std::min<int64_t>(emit_grid(), (etiles + EW_WARPS - 1) / EW_WARPS), EW_WARPS * 32, 0, s>>>(bins.keys_alt, bins.keys, plan, pbase, meta, Kd,
                                                      reinterpret_cast<const uint2*>(bins.ranges), bg, bins.vals,
                                                      emit_lb, &fl->tickets[TK_EMIT], fl);
     prof->end(s, chunks > 0 ? 2 : 0);
