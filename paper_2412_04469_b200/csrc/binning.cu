@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
 // (m = their rank), the final entry list is known position by position:
 //   entry (tile t, pair m) -> ranges[t].first + #{pairs m' < m whose rect covers t}
 // and every such count is local to t's bucket.  So:
-//   k_piece_count   per chunk of PC_CH depth-ordered pairs: pieces per bucket -> pcnt[chunk][b]
+//   k_piece_count   per chunk of g.ch depth-ordered pairs: pieces per bucket -> pcnt[b][chunk]
 //   k_piece_colscan per bucket: exclusive scan over chunks (in place) -> the bucket's
 //                   (chunk, bucket) segment offsets; totals
 //   k_piece_base    bucket bases (scan of totals) and emit-tile bases (ceil(total / EM_E))
@@ -612,6 +612,7 @@ struct BucketGeo {
     int gx, gy, nbx, nby, NB, VNB;
     int T, n_pad;
     int CHS;  // row stride of pcnt ([bucket][chunk]): the chunk capacity
+    int ch;   // depth-ordered pairs per chunk (a power-of-two multiple of PC_CH)
     unsigned long long npad_magic;  // ceil(2^64 / n_pad): j / n_pad = umulhi64(j, magic), exact for j < 2^32
 };
 
@@ -638,13 +639,13 @@ __global__ void __launch_bounds__(PC_THREADS) k_piece_count(const uint32_t* __re
     extern __shared__ uint32_t sc[];  // [VNB]
     const uint32_t M = visible_pairs(Kd);
     const uint32_t c = blockIdx.x;
-    if ((uint64_t)c * PC_CH >= M) return;
+    if ((uint64_t)c * g.ch >= M) return;
     const uint32_t* __restrict__ dvals = depth_order(dva, dvb, triv, Kd[1]);
     for (int b = threadIdx.x; b < g.VNB; b += PC_THREADS) sc[b] = 0u;
     __syncthreads();
 #pragma unroll 2
-    for (int e = 0; e < PC_CH / PC_THREADS; ++e) {
-        const uint32_t m = c * PC_CH + e * PC_THREADS + threadIdx.x;
+    for (int e = 0; e < g.ch / PC_THREADS; ++e) {
+        const uint32_t m = c * g.ch + e * PC_THREADS + threadIdx.x;
         if (m < M) {
             const uint32_t j = __ldg(dvals + m);
             const short4 r = __ldg(rect + j);
@@ -670,7 +671,7 @@ __global__ void __launch_bounds__(256) k_piece_colscan(uint32_t* __restrict__ pc
     const int lane = threadIdx.x & 31;
     if (b >= g.VNB) return;
     const uint32_t M = visible_pairs(Kd);
-    const uint32_t nch = (M + PC_CH - 1) / PC_CH;
+    const uint32_t nch = (M + g.ch - 1) / g.ch;
     uint32_t* row = pcnt + (size_t)b * g.CHS;
     // exclusive offsets in chunk order, 32 chunks per round (coalesced)
     uint32_t carry = 0;
@@ -757,15 +758,16 @@ __global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict_
 }
 
 // one thread per emit tile: its bucket, index k, pieces [s0, s0 + n) of the bucket, and its
-// chunk segments [c0, c0 + nseg) -- all the binary searches in flight at once, before k_emit
+// chunk segments [c0, c0 + nseg) -- all the binary searches in flight at once, before k_emit;
+// also clears the tile's look-back words (only the NE tiles in use, not the capacity)
 __global__ void __launch_bounds__(256) k_emit_plan(const uint32_t* __restrict__ pcnt, const uint32_t* __restrict__ ptotal,
                                                    const uint32_t* __restrict__ ebase,
                                                    const uint32_t* __restrict__ ebucket,
                                                    const uint32_t* __restrict__ meta, const uint32_t* __restrict__ Kd,
-                                                   BucketGeo g, uint4* __restrict__ plan) {
+                                                   BucketGeo g, uint4* __restrict__ plan, uint32_t* __restrict__ lb) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= meta[1]) return;
-    const uint32_t nch = (visible_pairs(Kd) + PC_CH - 1) / PC_CH;
+    const uint32_t nch = (visible_pairs(Kd) + g.ch - 1) / g.ch;
     const uint32_t b = ebucket[t];
     const uint32_t k = t - ebase[b];
     const uint32_t tot = ptotal[b];
@@ -775,6 +777,9 @@ __global__ void __launch_bounds__(256) k_emit_plan(const uint32_t* __restrict__ 
     const uint32_t s1 = emit_start(row, nch, tot, k + 1, cB);
     plan[2 * (size_t)t] = make_uint4(b, k, s0, s1 - s0);
     plan[2 * (size_t)t + 1] = make_uint4(cA, cB - cA, 0u, 0u);
+    uint4* lbt = reinterpret_cast<uint4*>(lb + (size_t)t * BK_T);  // the tile's look-back words, unpublished
+#pragma unroll 8
+    for (int q = 0; q < BK_T / 4; ++q) lbt[q] = make_uint4(0u, 0u, 0u, 0u);
 }
 
 // One CTA per chunk, its pairs split into wpc contiguous warp ranges.  Phase 1: each warp counts
@@ -802,13 +807,13 @@ __global__ void __launch_bounds__(PS_MAX_WARPS * 32) k_piece_scatter(const uint3
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, wpc = blockDim.x >> 5;
     const uint32_t M = visible_pairs(Kd);
     const uint32_t c = blockIdx.x;
-    if ((uint64_t)c * PC_CH >= M) return;  // block-uniform
+    if ((uint64_t)c * g.ch >= M) return;  // block-uniform
     const uint32_t* __restrict__ dvals = depth_order(dva, dvb, triv, Kd[1]);
     uint32_t* cur = ps_smem + (size_t)w * g.VNB;
     for (int b = lane; b < g.VNB; b += 32) cur[b] = 0u;
     if (threadIdx.x <= BK_W) s_rcp[threadIdx.x] = threadIdx.x ? (65536u + threadIdx.x - 1) / threadIdx.x : 0u;
-    const uint32_t span = PC_CH / wpc;  // pairs per warp (multiple of 32 * PS_ROUNDS)
-    const uint32_t m0 = c * PC_CH + w * span;
+    const uint32_t span = g.ch / wpc;  // pairs per warp (multiple of 32 * PS_ROUNDS)
+    const uint32_t m0 = c * g.ch + w * span;
     const uint32_t mend = min(M, m0 + span);
     __syncthreads();
     // phase 1: pieces per (warp, bucket)
@@ -1248,7 +1253,11 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     uint32_t* emit_lb = reinterpret_cast<uint32_t*>(ws + L.emit_lb);
     uint4* plan = reinterpret_cast<uint4*>(ws + L.eplan);                      // [etiles][2]
     uint32_t* ebucket = nullptr;  // after the plans: [etiles] (set below)
-    const int64_t chunks = (count + PC_CH - 1) / PC_CH;
+    // chunk size: 2048 pairs, doubled while the dense per-(bucket, chunk) counts would exceed
+    // ~4 M words (batches of many views: Immersive's 46 views x 40 buckets)
+    bg.ch = PC_CH;
+    while (bg.ch < 8 * PC_CH && (int64_t)bg.VNB * ((count + bg.ch - 1) / bg.ch) > (4 << 20)) bg.ch *= 2;
+    const int64_t chunks = (count + bg.ch - 1) / bg.ch;
     bg.CHS = (int)chunks;
     const int64_t etiles = ((int64_t)cap + EM_E - 1) / EM_E + bg.VNB + 1;
     ebucket = reinterpret_cast<uint32_t*>(plan + 2 * (size_t)etiles);
@@ -1262,21 +1271,21 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     const short4* r4 = reinterpret_cast<const short4*>(proj.rect);
     if (8 * (size_t)bg.VNB > PC_MAX_SMEM) return cudaErrorInvalidConfiguration;  // > 25600 buckets: not reachable (<= 64 4K views)
     prof->begin(ST_DUPLICATE, s);
-    if ((e = cudaMemsetAsync(emit_lb, 0, sizeof(uint32_t) * BK_T * (size_t)etiles, s))) return e;
     if (chunks > 0) {
         k_piece_count<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, rlo, rhi);
         k_piece_colscan<<<(unsigned)((bg.VNB + 7) / 8), 256, 0, s>>>(pcnt, Kd, bg, ptotal);
         k_piece_base<<<1, 1024, 0, s>>>(ptotal, bg.VNB, pbase, ebase, meta, ebucket, Kd);
         // warps per chunk: each holds VNB cursors in shared memory
         int wpc = (int)std::max<int64_t>(1, std::min<int64_t>(PS_MAX_WARPS, (int64_t)PC_MAX_SMEM / (4 * (int64_t)bg.VNB)));
-        while (wpc > 1 && (PC_CH / wpc) % (32 * PS_ROUNDS)) --wpc;
+        while (wpc > 1 && (bg.ch / wpc) % (32 * PS_ROUNDS)) --wpc;
         k_piece_scatter<<<(unsigned)chunks, 32 * wpc, (size_t)wpc * 4 * bg.VNB, s>>>(
             dlast_in, dlast_out, triv, Kd, rlo, rhi, bg, pcnt, pbase, bins.keys_alt, bins.keys);
     }
     prof->end(s, chunks > 0 ? 5 : 1);
     prof->begin(ST_TILE_SORT, s);
     if (chunks > 0)
-        k_emit_plan<<<(unsigned)((etiles + 255) / 256), 256, 0, s>>>(pcnt, ptotal, ebase, ebucket, meta, Kd, bg, plan);
+        k_emit_plan<<<(unsigned)((etiles + 255) / 256), 256, 0, s>>>(pcnt, ptotal, ebase, ebucket, meta, Kd, bg, plan,
+                                                                     emit_lb);
     if (chunks > 0)
         k_emit<<<(unsigned)std::min<int64_t>(emit_grid(), (etiles + EW_WARPS - 1) / EW_WARPS), EW_WARPS * 32, 0, s>>>(bins.keys_alt, bins.keys, plan, pbase, meta, Kd,
                                                      reinterpret_cast<const uint2*>(bins.ranges), bg, bins.vals,
