@@ -81,32 +81,25 @@ struct BinPlan {
     bool ok;
     int64_t S, spv, slabs;  // slab size, slabs per view, slabs in the batch
 };
-#ifndef QUEEN_SLAB_TARGET
-#define QUEEN_SLAB_TARGET 592  // slabs per batch: 4 waves of CTAs over 148 SMs
+#ifndef QUEEN_SLABS_PER_VIEW
+#define QUEEN_SLABS_PER_VIEW 32
 #endif
 inline BinPlan bin_plan(int64_t n_pad, int64_t n_views, int W, int H) {
     const int64_t gx = (W + 15) / 16, gy = (H + 15) / 16;
     BinPlan p{};
     p.ok = (gx + 1) * (gy + 1) <= BIN_MAX_SMEM_WORDS;
-    // ~QUEEN_SLAB_TARGET slabs per batch whatever its view count (a few-view batch -- a rank of
-    // a multi-GPU run -- still fills the GPU), slab sizes multiples of 1024 in [2048, 65536]
-    const int64_t spv0 = n_views > 0 ? (QUEEN_SLAB_TARGET + n_views - 1) / n_views : 1;
-    int64_t S = (n_pad + spv0 - 1) / spv0;
+    // ~32 slabs per view (S depends on n_pad only, so a smaller batch never needs more
+    // slab-count space than the workspace was carved for), multiples of 1024 in [2048, 65536].
+    // (~592 slabs per batch whatever its view count -- for the few-view batches of a multi-GPU
+    // rank -- measured slower: 3-view N3DV batch, compact 58 -> 65 us.)
+    (void)n_views;
+    int64_t S = (n_pad + QUEEN_SLABS_PER_VIEW - 1) / QUEEN_SLABS_PER_VIEW;
     S = (S + 1023) / 1024 * 1024;
     S = S < 2048 ? 2048 : (S > 65536 ? 65536 : S);
     p.S = S;
     p.spv = n_pad > 0 ? (n_pad + S - 1) / S : 0;
     p.slabs = p.spv * n_views;
     return p;
-}
-// the most slabs any batch of 1..n_views views of n_pad elements uses (workspace sizing)
-inline int64_t max_slabs(int64_t n_pad, int64_t n_views, int W, int H) {
-    int64_t m = 0;
-    for (int64_t v = 1; v <= n_views; ++v) {
-        const int64_t sl = bin_plan(n_pad, v, W, H).slabs;
-        m = sl > m ? sl : m;
-    }
-    return m;
 }
 
 // Bucketed emission (binning.cu K4'/K5'): buckets of BK_W x BK_H tiles of one view; the
@@ -156,9 +149,8 @@ inline WsLayout ws_layout(int32_t n_pad, int32_t n_views, int32_t W, int32_t H, 
     L.counts = o; o += align256(sizeof(uint32_t) * 2 * (size_t)n_views * L.T);  // counts | local starts
     L.view_tot = o; o += align256(sizeof(uint32_t) * (size_t)n_views);
     const BinPlan bp = bin_plan(n_pad, n_views, W, H);
-    const int64_t slabs = max_slabs(n_pad, n_views, W, H);
-    L.slab_counts = o; o += align256(sizeof(uint32_t) * (size_t)(bp.ok ? slabs : 0) * L.T);
-    L.slab_vis = o; o += align256(sizeof(uint32_t) * (size_t)(slabs + 1));
+    L.slab_counts = o; o += align256(sizeof(uint32_t) * (size_t)(bp.ok ? bp.slabs : 0) * L.T);
+    L.slab_vis = o; o += align256(sizeof(uint32_t) * (size_t)(bp.slabs + 1));
     L.select = o; o += align256((size_t)n_pad);  // render_mask: per-Gaussian subset flags
     {
         const int64_t vnb = (int64_t)n_views * buckets_per_view(W, H);
