@@ -179,7 +179,19 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
         // (The staging area has 288 words of slack: a lane's pointer advances at most once per
         // step, so even a corrupt stream never reads past it; the final check flags it.)
         uint16_t* sw = s_words_dyn + wid * (ANS_STAGE + 288);
-        for (uint32_t q = lane; q < nw; q += 32) sw[q] = __ldg(words + c0 + q);
+        for (uint32_t q0 = 0; q0 < nw; q0 += 32 * 8) {  // 8 loads in flight per lane
+            uint16_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t q = q0 + 32 * u + lane;
+                v[u] = q < nw ? __ldg(words + c0 + q) : (uint16_t)0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t q = q0 + 32 * u + lane;
+                if (q < nw) sw[q] = v[u];
+            }
+        }
         __syncwarp();
         // output: 32-bit offset from the category's first row; the lane's column wraps into the
         // next row once every ~n/32 steps, at step tw (a rare, short branch)
