@@ -1,33 +1,28 @@
 // K3-K6: binning for a batch of equally-sized views (BASELINE north_star: "duplication
 // of Gaussians into 16x16 tiles, a radix sort on (tile, depth) keys, per-tile range
-// extraction"; "warp-level scans and a custom onesweep radix sort").
+// extraction"; "warp-level scans and a custom onesweep radix sort").  DESIGN.md §8.
 //
-// The sort is an LSD radix sort on the composite key (gt, depth) with gt = view*T +
-// tile: LSD order processes the depth digits first and the tile digits last.  Every
-// duplicate of a Gaussian carries the same depth, so the depth digits are sorted
-// BEFORE duplication, on the M visible (view, Gaussian) pairs (M << K), and only the
-// tile digits are sorted on the K duplicated entries, with 4-byte keys.  Every count the
-// sort needs (visible pairs, entries per tile -> ranges, digit histograms) is known
-// before the first pass, from one read of the projection outputs:
+// The entries are ordered by (gt, depth, index), gt = view*T + tile.  Every copy of a Gaussian
+// carries the same depth, so the depth order is sorted once, on the M visible (view,
+// Gaussian) pairs; the entries are then written directly at their final positions:
 //   K3a k_slab_count    per slab of S consecutive elements of a view (one CTA): visible
 //                       count, depth-digit histograms, and the slab's entries per tile via
 //                       a shared-memory 2D difference array of tile rects -> counts[slab][t]
-//       k_slab_sum      per view: entries per tile, view-local starts, tile-digit histograms
+//       k_slab_sum      per view: entries per tile; k_view_scan: view-local tile starts
 //       k_totals        K, M, capacity check; slab offsets of the visible pairs
 //       k_slab_compact  visible pairs in (view, index) order -> (depth bits, flat index) [M]
-//   K5a k_onesweep32<8> x4  stable sort of the pairs by depth (31 bits)
-//   K4  k_scan_dup      decoupled look-back scan of tiles touched in depth order fused
-//                       with duplication: entry = (gt, Gaussian index), emitted for
-//                       each pair ty-major, tx-minor
+//   K5a k_onesweep32<9> x3 (+<8>)  stable sort of the pairs by relative depth (27 + 4 bits)
 //   K6  k_ranges_finalize  [first, last+1) of each gt from the per-tile counts
-//   K5b k_onesweep32<8|9> x2..3  stable sort of the entries by gt
-// Stability makes the final order (gt, depth, view, index) -> (gt, depth, index):
-// identical to sorting the 96-bit (gt << 31 | depth, index) tuples (oracle: std::sort).
+//   K4' k_piece_count / k_piece_colscan / k_piece_base / k_piece_scatter: the pairs cut
+//       into pieces per 16x8-tile bucket, each bucket's pieces in depth order
+//   K5' k_emit_plan + k_emit: each bucket's entries written at their final positions
+// The result equals sorting the 96-bit (gt << 31 | depth, index) tuples (oracle: std::sort).
 //
 // onesweep pass: persistent CTAs take 4096-key tiles by atomic ticket (forward
-// progress for the look-back), rank keys with warp match_any multisplit in key order
-// (stable), publish per-digit tile counts, resolve global digit offsets by decoupled
-// look-back, stage the tile in shared memory in digit order and write it out coalesced.
+// progress for the look-back), rank keys with a warp multisplit in key order (stable;
+// shared-memory match words), publish per-digit tile counts, resolve global digit offsets by
+// decoupled look-back, stage the tile in shared memory in digit order and write it out
+// coalesced.
 #include <algorithm>
 
 #include "queen_internal.cuh"
@@ -48,11 +43,11 @@ __device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
 constexpr uint32_t LB_AGG = 1u << 30, LB_INC = 2u << 30, LB_MASK = (1u << 30) - 1;
 constexpr long long SPIN_LIMIT = 1ll << 24;
 #ifndef QUEEN_LB_BATCH
-#define QUEEN_LB_BATCH 4  // measured (tile sort, N3DV): 1 -> 420 us, 2 -> 388, 4 -> 390, 8 -> 408, 16 -> 450
+#define QUEEN_LB_BATCH 4  // measured (round-1 tile sort, N3DV): 1 -> 420 us, 2 -> 388, 4 -> 390, 8 -> 408, 16 -> 450
 #endif
 constexpr int LB_BATCH = QUEEN_LB_BATCH;
 #ifndef QUEEN_OS_MATCH_OR
-#define QUEEN_OS_MATCH_OR 1  // warp match by shared atomicOr (measured: tile sort 488 -> 417 us vs match.any)
+#define QUEEN_OS_MATCH_OR 1  // warp match by shared atomicOr (measured, round-1 tile sort: 488 -> 417 us vs match.any)
 #endif  // onesweep look-back predecessors loaded per round trip
 
 enum : int { TK_DEPTH = 0, TK_EMIT = 4 };  // dynamic-tile tickets: depth passes 0..3, emission
@@ -425,7 +420,7 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
     // every key has digit 0: the stable pass is the identity -- nothing is written, and the
-    // consumer (k_scan_dup) reads the pass's input buffer instead (same test on the device)
+    // consumers (k_piece_count / k_piece_scatter) read the pass's input buffer instead
     if (triv && triv[0] == Kn) return;
     const bool owns_digits = threadIdx.x * DPT < BINS;
 #if QUEEN_OS_MATCH_OR
@@ -1213,7 +1208,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     prof->begin(ST_DEPTH_SORT, s);
     // depth keys are relative to the batch's smallest visible depth (order-preserving, and the
     // range of a scene's depths fits 27 bits unless it spans > 2^27 ulps): three 9-bit passes,
-    // then bits 27..31, which is skipped (no copy; the duplication reads the previous buffer)
+    // then bits 27..31, which is skipped (no copy; the bucket kernels read the previous buffer)
     // whenever that digit is 0 for every key
     k_hist_scan<<<1, 32 * DEPTH_PASSES, 0, s>>>(hist, hist_excl, DEPTH_PASSES, MAX_BINS);
     int cur = 0;
@@ -1270,7 +1265,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     uint32_t* rhi = dk[1];
     const short4* r4 = reinterpret_cast<const short4*>(proj.rect);
     if (8 * (size_t)bg.VNB > PC_MAX_SMEM) return cudaErrorInvalidConfiguration;  // > 25600 buckets: not reachable (<= 64 4K views)
-    prof->begin(ST_DUPLICATE, s);
+    prof->begin(ST_BUCKET, s);
     if (chunks > 0) {
         k_piece_count<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, rlo, rhi);
         k_piece_colscan<<<(unsigned)((bg.VNB + 7) / 8), 256, 0, s>>>(pcnt, Kd, bg, ptotal);
@@ -1282,7 +1277,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
             dlast_in, dlast_out, triv, Kd, rlo, rhi, bg, pcnt, pbase, bins.keys_alt, bins.keys);
     }
     prof->end(s, chunks > 0 ? 5 : 1);
-    prof->begin(ST_TILE_SORT, s);
+    prof->begin(ST_EMIT, s);
     if (chunks > 0)
         k_emit_plan<<<(unsigned)((etiles + 255) / 256), 256, 0, s>>>(pcnt, ptotal, ebase, ebucket, meta, Kd, bg, plan,
                                                                      emit_lb);

@@ -34,18 +34,7 @@ struct DevFlags {
 static_assert(sizeof(DevFlags) == 128, "DevFlags layout");
 
 constexpr int MAX_PASSES = 8;
-#ifndef QUEEN_SORT_THREADS
-#define QUEEN_SORT_THREADS 256
-#endif
-constexpr int SORT_THREADS = QUEEN_SORT_THREADS;  // duplication block size
-#ifndef QUEEN_SORT_ITEMS
-#define QUEEN_SORT_ITEMS 4  // measured N3DV duplication: 16 -> 173 us, 8 -> 139 us, 4 -> 129 us
-#endif
-constexpr int SORT_ITEMS = QUEEN_SORT_ITEMS;  // depth-sorted pairs per thread in the duplication
-constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;  // pairs per duplication block (4096)
-constexpr int SCAN_THREADS = 256;
-constexpr int SCAN_ITEMS = 16;
-constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+constexpr int SORT_TILE = 4096;  // workspace-capacity granularity (keys / elements)
 constexpr int REC_WORDS = 12;
 #ifndef QUEEN_OS_THREADS
 #define QUEEN_OS_THREADS 512
@@ -270,7 +259,7 @@ __device__ __forceinline__ bool touches(const float4& a, const float4& q, float 
 
 // Stage profiler: CUDA events recorded on the launching stream at stage boundaries
 // (enabled by queen_profile_enable; used by bench.py for per-kernel durations).
-enum Stage { ST_APPLY = 0, ST_PROJECT, ST_COMPACT, ST_DEPTH_SORT, ST_DUPLICATE, ST_TILE_SORT, ST_RANGES, ST_BLEND, ST_ENTROPY, ST_BLEND_ORDER, ST_COUNT };
+enum Stage { ST_APPLY = 0, ST_PROJECT, ST_COMPACT, ST_DEPTH_SORT, ST_BUCKET, ST_EMIT, ST_RANGES, ST_BLEND, ST_ENTROPY, ST_BLEND_ORDER, ST_COUNT };
 struct Prof {
     bool on = false;
     std::vector<cudaEvent_t> pool;
