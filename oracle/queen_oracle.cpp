@@ -482,8 +482,10 @@ int64_t oracle_bin(int n_pad, int V, int W, int H, const uint32_t* tiles, const 
 // ---------------------------------------------------------------------------
 // a12. Front-to-back compositing, Eq. 2: c = sum c_i a_i prod_{j<i}(1-a_j),
 // a_i = o_i exp(-1/2 d^T S'^-1 d), over the pixel's tile list in depth order.
-// 3D-GS cut-offs as read in R#14: skip when a_i < 1/255 (exact test p2 < T2, or
-// p2 > 0), a_i clamped at 0.99, composite-then-stop when T < 1e-4.  Pixel (x, y)
+// 3D-GS cut-offs as read in R#14: skip when a_i < 1/255 (exact test p2 < T2), a_i
+// clamped at 0.99, composite-then-stop when T < 1e-4.  p2 is mathematically <= 0 (the conic
+// is positive definite); a positive computed p2 is rounding at the ellipse's centre and is
+// composited like the centre (R#14; 3D-GS's "power > 0" skip is not kept).  Pixel (x, y)
 // is sampled at ((float)x, (float)y) (R#12).  Output C + T*bg and T (R#16).
 // ---------------------------------------------------------------------------
 // record words: 0 u, 1 v, 4 A2, 5 B2, 6 C2, 7 T2, 8 o, 9-11 rgb (hx, hy unused here)
@@ -495,7 +497,7 @@ static inline float rec_p2(const float* rc, float fx, float fy) {
 
 static inline bool blend_step(const float* rc, float fx, float fy, float C[3], float& T) {
     float p2 = rec_p2(rc, fx, fy);
-    if (p2 > 0.0f || p2 < rc[7]) return false;
+    if (p2 < rc[7]) return false;
     float alpha = std::fmin(0.99f, rc[8] * std::exp2(p2));
     float aT = alpha * T;
     C[0] = std::fma(rc[9], aT, C[0]);
@@ -591,7 +593,7 @@ void oracle_blend_counts(int n_pad, int V, int W, int H, const float* rec, const
                     const float* rc = rec + ((int64_t)v * n_pad + vals_sorted[j]) * 12;
                     ++ev;
                     float p2 = rec_p2(rc, (float)x, (float)y);
-                    if (!(p2 > 0.0f || p2 < rc[7])) ++cp;
+                    if (!(p2 < rc[7])) ++cp;
                     if (blend_step(rc, (float)x, (float)y, C, Tr)) break;
                 }
             }
@@ -654,7 +656,7 @@ void oracle_contrib(int n_pad, int V, int W, int H, const float* rec, const uint
                 for (uint32_t j = ranges[2 * gt]; j < ranges[2 * gt + 1]; ++j) {
                     const float* rc = rec + ((int64_t)v * n_pad + vals_sorted[j]) * 12;
                     const float p2 = rec_p2(rc, (float)x, (float)y);
-                    if (p2 > 0.0f || p2 < rc[7]) continue;
+                    if (p2 < rc[7]) continue;
                     if (offsets) {
                         gid_out[offsets[pix] + c] = (int32_t)vals_sorted[j];
                         clamp_out[offsets[pix] + c] = rc[8] * std::exp2(p2) > 0.99f ? 1 : 0;

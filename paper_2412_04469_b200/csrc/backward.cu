@@ -140,8 +140,8 @@ __global__ void BWD_BOUNDS k_blend_bwd(const float4* __restrict__ rec, int n_pad
             for (int k = 0; k < NP; ++k) {
                 const float2 dy = __fadd2_rn(vv, nfy[k]);
                 p2[k] = __ffma2_rn(__ffma2_rn(cc, dy, tb2), dy, ta2);
-                h[2 * k] = !(TA[k].x < 1e-4f) && !(p2[k].x > 0.0f) && !(p2[k].x < bq.w);
-                h[2 * k + 1] = !(TA[k].y < 1e-4f) && !(p2[k].y > 0.0f) && !(p2[k].y < bq.w);
+                h[2 * k] = !(TA[k].x < 1e-4f) && !(p2[k].x < bq.w);
+                h[2 * k + 1] = !(TA[k].y < 1e-4f) && !(p2[k].y < bq.w);
                 anyh |= h[2 * k] | h[2 * k + 1];
             }
             if (!anyh) continue;
@@ -248,8 +248,8 @@ __global__ void BWD_BOUNDS k_blend_bwd(const float4* __restrict__ rec, int n_pad
                 if (!(l0 | l1)) continue;
                 const float2 dy = __fadd2_rn(vv, nfy[k]);
                 const float2 p2 = __ffma2_rn(__ffma2_rn(cc, dy, tb2), dy, ta2);
-                const bool h0 = l0 && !(p2.x > 0.0f || p2.x < bq.w);
-                const bool h1 = l1 && !(p2.y > 0.0f || p2.y < bq.w);
+                const bool h0 = l0 && !(p2.x < bq.w);
+                const bool h1 = l1 && !(p2.y < bq.w);
                 if (!(h0 | h1)) continue;
                 any = true;
                 // a non-hit lane of the pair runs with a = 0: T, Sb and every sum stay unchanged

@@ -18,7 +18,7 @@
 //    different rows issues one short straight-line block instead of four divergent ones
 //    (SASS: 62 instructions for a fully hit record, was ~100).
 // Per-pixel arithmetic is exactly the oracle's (oracle/queen_oracle.cpp blend_step):
-//   p2 = fma(fma(C2, dy, B2 dx), dy, (A2 dx) dx);  skip if p2 > 0 or p2 < T2;
+//   p2 = fma(fma(C2, dy, B2 dx), dy, (A2 dx) dx);  skip if p2 < T2 (R14: no p2 > 0 skip);
 //   a = min(0.99, o 2^p2); C = fma(rgb, a T, C); T = T (1 - a); stop after T < 1e-4.
 #include <cstdlib>
 
@@ -53,7 +53,8 @@ struct Px2 {
     float2 r, g, b, T;
 };
 
-__device__ __forceinline__ bool hit(float T, float p2, float T2) { return !(T < 1e-4f) && !(p2 > 0.0f) && !(p2 < T2); }
+// a pixel hits a record when it is alive (T >= 1e-4) and alpha >= 1/255 (p2 >= T2; R14)
+__device__ __forceinline__ bool hit(float T, float p2, float T2) { return !(T < 1e-4f) && !(p2 < T2); }
 
 // Branch-free compositing of one record into a row pair: a row that does not hit gets
 // exponent -inf, i.e. alpha = min(0.99, o * 2^-inf) = +0, and then C = fma(c, +0, C) = C and
