@@ -82,10 +82,10 @@ __device__ __forceinline__ void composite2(Px2& p, float q0, float q1, bool h0, 
 }
 
 #ifndef QUEEN_BLEND_MINB
-#define QUEEN_BLEND_MINB 20  // 48 registers: 20 CTAs (40 warps) per SM; measured n3dv blend 64 regs 1.399 ms, 48 regs 1.378, 40 regs (spills) 1.401
+#define QUEEN_BLEND_MINB 24  // 40 registers (a few spill): 24 CTAs (48 warps) per SM; measured (round 2, N3DV blend) 56 regs 1.305 ms, 48 regs 1.310, 40 regs 1.288 (+ unroll 8: 1.284; MeetRoom / Immersive -1.5 %)
 #endif
 #ifndef QUEEN_BLEND_UNROLL
-#define QUEEN_BLEND_UNROLL 4  // measured n3dv blend: 1 -> 1.423 ms, 2 -> 1.410, 4 -> 1.399
+#define QUEEN_BLEND_UNROLL 8  // measured n3dv blend: 1 -> 1.423 ms, 2 -> 1.410, 4 -> 1.399 (round 1); 2 -> 1.328, 4 -> 1.310, 8 -> 1.302 (round 2)
 #endif
 constexpr int BLEND_UNROLL = QUEEN_BLEND_UNROLL;  // record-loop unroll
 #ifndef QUEEN_BLEND_UNCOND
