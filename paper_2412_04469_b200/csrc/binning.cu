@@ -587,10 +587,10 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
 //   k_piece_count   per chunk of g.ch depth-ordered pairs: pieces per bucket -> pcnt[b][chunk]
 //   k_piece_colscan per bucket: exclusive scan over chunks (in place) -> the bucket's
 //                   (chunk, bucket) segment offsets; totals
-//   k_piece_base    bucket bases (scan of totals) and emit-tile bases (ceil(total / EM_E))
+//   k_piece_base    bucket bases (scan of totals) and emit-tile bases (ceil(total / em_e))
 //   k_piece_scatter per chunk: each piece's m into its (chunk, bucket) segment (order inside a
 //                   segment arbitrary: shared-memory cursors)
-//   k_emit          per emit tile (whole segments of one bucket, ~EM_E pieces): sort the m
+//   k_emit          per emit tile (whole segments of one bucket, ~em_e pieces): sort the m
 //                   values (unique), count entries per bucket tile, resolve each tile's offset
 //                   among the bucket's earlier emit tiles by decoupled look-back, then write
 //                   every entry's Gaussian index at its final position, ranked stably in m order
@@ -608,6 +608,7 @@ struct BucketGeo {
     int T, n_pad;
     int CHS;  // row stride of pcnt ([bucket][chunk]): the chunk capacity
     int ch;   // depth-ordered pairs per chunk (a power-of-two multiple of PC_CH)
+    int em_e; // nominal pieces per emit tile
     unsigned long long npad_magic;  // ceil(2^64 / n_pad): j / n_pad = umulhi64(j, magic), exact for j < 2^32
 };
 
@@ -686,11 +687,11 @@ __global__ void __launch_bounds__(256) k_piece_colscan(uint32_t* __restrict__ pc
 }
 
 // bucket-local start of emit tile k of bucket b: the first (chunk, bucket) segment that starts
-// at or after k * EM_E (emit tiles hold whole segments), or the bucket total
+// at or after k * em_e (emit tiles hold whole segments), or the bucket total
 // (also returns the chunk c whose segment starts there: off[c] = start, c = nch at the end)
 __device__ __forceinline__ uint32_t emit_start(const uint32_t* row, uint32_t nch, uint32_t total, uint32_t k,
-                                               uint32_t& chunk) {
-    const uint32_t want = k * (uint32_t)EM_E;
+                                               uint32_t em_e, uint32_t& chunk) {
+    const uint32_t want = k * em_e;
     uint32_t lo = 0, hi = nch;  // first c with off[c] >= want (off[nch] := total)
     while (lo < hi) {
         const uint32_t mid = (lo + hi) >> 1;
@@ -702,7 +703,7 @@ __device__ __forceinline__ uint32_t emit_start(const uint32_t* row, uint32_t nch
 
 // one block: bucket bases (exclusive scan of the totals) and emit-tile bases; meta[0] = pieces,
 // meta[1] = emit tiles
-__global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict__ ptotal, int VNB,
+__global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict__ ptotal, int VNB, uint32_t em_e,
                                                      uint32_t* __restrict__ pbase, uint32_t* __restrict__ ebase,
                                                      uint32_t* __restrict__ meta, uint32_t* __restrict__ ebucket,
                                                      uint32_t* __restrict__ Kd) {
@@ -714,7 +715,7 @@ __global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict_
     for (int b0 = 0; b0 < VNB; b0 += blockDim.x) {
         const int b = b0 + threadIdx.x;
         const uint32_t x = b < VNB ? ptotal[b] : 0u;
-        const uint32_t y = (x + EM_E - 1) / EM_E;
+        const uint32_t y = (x + em_e - 1) / em_e;
         uint32_t ix = x, iy = y;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -747,7 +748,7 @@ __global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict_
     }
     __syncthreads();
     for (int b = threadIdx.x; b < VNB; b += blockDim.x) {  // each emit tile's bucket
-        const uint32_t e0 = ebase[b], et = (ptotal[b] + EM_E - 1) / EM_E;
+        const uint32_t e0 = ebase[b], et = (ptotal[b] + em_e - 1) / em_e;
         for (uint32_t k = 0; k < et; ++k) ebucket[e0 + k] = (uint32_t)b;
     }
 }
@@ -768,8 +769,8 @@ __global__ void __launch_bounds__(256) k_emit_plan(const uint32_t* __restrict__ 
     const uint32_t tot = ptotal[b];
     const uint32_t* row = pcnt + (size_t)b * g.CHS;
     uint32_t cA, cB;
-    const uint32_t s0 = emit_start(row, nch, tot, k, cA);
-    const uint32_t s1 = emit_start(row, nch, tot, k + 1, cB);
+    const uint32_t s0 = emit_start(row, nch, tot, k, (uint32_t)g.em_e, cA);
+    const uint32_t s1 = emit_start(row, nch, tot, k + 1, (uint32_t)g.em_e, cB);
     plan[2 * (size_t)t] = make_uint4(b, k, s0, s1 - s0);
     plan[2 * (size_t)t + 1] = make_uint4(cA, cB - cA, 0u, 0u);
     uint4* lbt = reinterpret_cast<uint4*>(lb + (size_t)t * BK_T);  // the tile's look-back words, unpublished
@@ -1254,7 +1255,8 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     while (bg.ch < 8 * PC_CH && (int64_t)bg.VNB * ((count + bg.ch - 1) / bg.ch) > (4 << 20)) bg.ch *= 2;
     const int64_t chunks = (count + bg.ch - 1) / bg.ch;
     bg.CHS = (int)chunks;
-    const int64_t etiles = ((int64_t)cap + EM_E - 1) / EM_E + bg.VNB + 1;
+    bg.em_e = count > (12 << 20) ? 128 : 256;
+    const int64_t etiles = ((int64_t)cap + bg.em_e - 1) / bg.em_e + bg.VNB + 1;
     ebucket = reinterpret_cast<uint32_t*>(plan + 2 * (size_t)etiles);
     const size_t vsm = sizeof(uint32_t) * (size_t)bg.VNB;
     const uint32_t* dlast_in = dv[cur ^ 1];   // input of the last depth pass
@@ -1269,7 +1271,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     if (chunks > 0) {
         k_piece_count<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, rlo, rhi);
         k_piece_colscan<<<(unsigned)((bg.VNB + 7) / 8), 256, 0, s>>>(pcnt, Kd, bg, ptotal);
-        k_piece_base<<<1, 1024, 0, s>>>(ptotal, bg.VNB, pbase, ebase, meta, ebucket, Kd);
+        k_piece_base<<<1, 1024, 0, s>>>(ptotal, bg.VNB, (uint32_t)bg.em_e, pbase, ebase, meta, ebucket, Kd);
         // warps per chunk: each holds VNB cursors in shared memory
         int wpc = (int)std::max<int64_t>(1, std::min<int64_t>(PS_MAX_WARPS, (int64_t)PC_MAX_SMEM / (4 * (int64_t)bg.VNB)));
         while (wpc > 1 && (bg.ch / wpc) % (32 * PS_ROUNDS)) --wpc;
