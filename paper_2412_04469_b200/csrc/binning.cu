@@ -1255,7 +1255,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     while (bg.ch < 8 * PC_CH && (int64_t)bg.VNB * ((count + bg.ch - 1) / bg.ch) > (4 << 20)) bg.ch *= 2;
     const int64_t chunks = (count + bg.ch - 1) / bg.ch;
     bg.CHS = (int)chunks;
-    bg.em_e = count > (12 << 20) ? 128 : 256;
+    bg.em_e = proj.n_pad > (1 << 20) ? 128 : 256;  // measured: stress (3 M) 128, N3DV / Immersive 256
     const int64_t etiles = ((int64_t)cap + bg.em_e - 1) / bg.em_e + bg.VNB + 1;
     ebucket = reinterpret_cast<uint32_t*>(plan + 2 * (size_t)etiles);
     const size_t vsm = sizeof(uint32_t) * (size_t)bg.VNB;

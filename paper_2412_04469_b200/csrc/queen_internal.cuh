@@ -96,8 +96,8 @@ inline BinPlan bin_plan(int64_t n_pad, int64_t n_views, int W, int H) {
 // ~g.em_e pieces.
 constexpr int PC_CH = 2048;
 constexpr int BK_W = 16, BK_H = 8, BK_T = BK_W * BK_H;
-// emit-tile size: pieces per tile, chosen per batch (binning.cu: 256, or 128 for batches of
-// > 12 M (view, Gaussian) elements); EM_E_MIN sizes the workspace.  Measured emit: N3DV 2048 ->
+// emit-tile size: pieces per tile, chosen per batch (binning.cu: 256, or 128 above 1 M
+// Gaussians); EM_E_MIN sizes the workspace.  Measured emit: N3DV 2048 ->
 // 289 us, 512 -> 233 us, 256 -> 187 us, 128 -> 199 us; stress 512 -> 11.75 ms, 256 -> 9.75, 128 -> 8.23
 constexpr int EM_E_MIN = 128;
 inline int64_t buckets_per_view(int W, int H) {
