@@ -600,7 +600,10 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
 // ---------------------------------------------------------------------------
 constexpr int PC_THREADS = 512;             // PC_CH / 8 pairs per thread
 constexpr size_t PC_MAX_SMEM = 200 * 1024;  // per-chunk bucket counters: up to 51200 buckets per batch
-constexpr int PS_MAX_WARPS = 8;             // k_piece_scatter: chunks (warps) per CTA, fewer when VNB is large
+constexpr int PS_MAX_WARPS = 8;
+#ifndef QUEEN_PC_BUDGET
+#define QUEEN_PC_BUDGET 16  // M words of per-(bucket, chunk) counts before the chunk size doubles (measured 4 / 16 / 64: Immersive bucket 0.53 / 0.41 / 0.46 ms, stress 7.2 / 6.1 / 6.6 ms)
+#endif             // k_piece_scatter: chunks (warps) per CTA, fewer when VNB is large
 
 
 struct BucketGeo {
@@ -1252,7 +1255,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     // chunk size: 2048 pairs, doubled while the dense per-(bucket, chunk) counts would exceed
     // ~4 M words (batches of many views: Immersive's 46 views x 40 buckets)
     bg.ch = PC_CH;
-    while (bg.ch < 8 * PC_CH && (int64_t)bg.VNB * ((count + bg.ch - 1) / bg.ch) > (4 << 20)) bg.ch *= 2;
+    while (bg.ch < 8 * PC_CH && (int64_t)bg.VNB * ((count + bg.ch - 1) / bg.ch) > ((int64_t)QUEEN_PC_BUDGET << 20)) bg.ch *= 2;
     const int64_t chunks = (count + bg.ch - 1) / bg.ch;
     bg.CHS = (int)chunks;
     bg.em_e = proj.n_pad > (1 << 20) ? 128 : 256;  // measured: stress (3 M) 128, N3DV / Immersive 256
