@@ -67,11 +67,10 @@ static void normalise(const uint64_t cnt[256], uint64_t total, uint16_t f[256]) 
 
 // ---------------------------------------------------------------- device decoder
 // One launch per frame (every category).  A block builds its category's slot table in shared
-// memory straight from the stream's 256 frequencies: slot -> (f - 1) | (slot - c) << 12 |
-// latent byte << 24, one 32-bit word.  Each warp then decodes one chunk, one rANS state per
-// lane.  A lane's renormalisation words are its own sequence, prefetched 4 deep into
-// registers, so its critical path per symbol is ONE shared load + a multiply-add + a select
-// (no warp vote or shuffle).
+// memory straight from the stream's 256 frequencies: slot -> (f - 1) | latent byte << 12 |
+// (slot - c) << 20, one 32-bit word.  Each warp then decodes one chunk, one rANS state per lane, from the
+// chunk's words staged in shared memory; a lane's critical path per symbol is ONE shared load,
+// one multiply-add, a compare and a select (no warp vote or shuffle).
 //
 // Bounds (every stream is wire input): the host passes each category's expected symbol and
 // chunk counts (L * n, from the packet shape) and the stream's byte size.  A block whose
@@ -93,26 +92,75 @@ struct AnsFrame {
     int n, n_pad;
 };
 
+// Setup is two global round trips: (1) the header, the frequencies and the chunk's offsets,
+// lane counts and states (all addressed by the host-expected counts, so in bounds whatever the
+// header says); (2) the chunk's words, staged in shared memory while warp 0 scans the
+// frequencies.  A slot's entry packs (f - 1) | byte << 12 | (slot - c) << 20, so a decode
+// step is x' = (f - 1) * xs + (xs + (slot - c)): an AND and a LEA.HI side by side, then one IMAD.
 __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr, int8_t* __restrict__ out,
                                                                DevFlags* fl) {
-    __shared__ uint32_t s_tab[ANS_M];
+    __shared__ uint32_t s_tab[ANS_M];  // slot -> (f - 1) | latent byte << 12 | (slot - c) << 20
     __shared__ uint32_t s_c[257];
-    extern __shared__ uint16_t s_words_dyn[];  // [ANS_WARPS][ANS_STAGE]
+    extern __shared__ uint16_t s_words_dyn[];  // [ANS_WARPS][ANS_STAGE + 288]
     int cat = 0;
     while (cat < 4 && (int)blockIdx.x >= fr.block0[cat + 1]) ++cat;
     const unsigned char* stream = fr.stream[cat];
     const int n = fr.n, n_pad = fr.n_pad;
     const AnsHeader* h = reinterpret_cast<const AnsHeader*>(stream);
     const uint32_t n_sym = fr.n_sym[cat], n_chunks = fr.n_chunks[cat];
-    if (h->magic != ANS_MAGIC || h->n_sym != n_sym || h->n_chunks != n_chunks) {  // block-uniform
-        if (threadIdx.x == 0) raise_flag(fl, FLAG_INDEX);
-        return;
-    }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (wid == 0) {  // exclusive scan of the 256 frequencies by one warp
-        uint32_t v[8], sum = 0;
+    // round trip 1: header, frequencies (warp 0), this warp's chunk record
+    const uint32_t chunk = (blockIdx.x - fr.block0[cat]) * ANS_WARPS + wid;
+    const bool live = chunk < n_chunks;  // warp-uniform
+    const uint32_t* woff = reinterpret_cast<const uint32_t*>(stream + sizeof(AnsHeader));
+    const uint32_t* states = woff + n_chunks + 1;
+    const uint16_t* lcount = reinterpret_cast<const uint16_t*>(states + (size_t)n_chunks * ANS_LANES);
+    const uint16_t* words = lcount + (size_t)n_chunks * ANS_LANES;
+    const bool hdr_ok = h->magic == ANS_MAGIC && h->n_sym == n_sym && h->n_chunks == n_chunks;
+    uint32_t v[8];
+    if (wid == 0) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) { v[q] = h->freq[lane * 8 + q]; sum += v[q]; }
+        for (int q = 0; q < 8; ++q) v[q] = h->freq[lane * 8 + q];
+    }
+    uint32_t c0 = 0, c1 = 0, cnt = 0, x = ANS_L;
+    if (live) {
+        c0 = woff[chunk];
+        c1 = woff[chunk + 1];
+        cnt = lcount[(size_t)chunk * ANS_LANES + lane];
+        x = states[(size_t)chunk * ANS_LANES + lane];
+    }
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t nw = c1 - c0;
+    const bool chunk_ok = live && hdr_ok && c0 <= c1 && c1 <= fr.n_words[cat] && nw == tot;  // warp-uniform
+    if (live && hdr_ok && !chunk_ok && lane == 0) raise_flag(fl, FLAG_INDEX);
+    const bool staged = chunk_ok && nw <= ANS_STAGE && n >= 32;
+    uint16_t* sw = s_words_dyn + wid * (ANS_STAGE + 288);
+    // round trip 2: the chunk's words into shared memory (coalesced, 8 loads in flight per lane)
+    if (staged) {
+        for (uint32_t q0 = 0; q0 < nw; q0 += 32 * 8) {
+            uint16_t wv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t q = q0 + 32 * u + lane;
+                wv[u] = q < nw ? __ldg(words + c0 + q) : (uint16_t)0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t q = q0 + 32 * u + lane;
+                if (q < nw) sw[q] = wv[u];
+            }
+        }
+    }
+    if (wid == 0) {  // exclusive scan of the 256 frequencies
+        uint32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sum += v[q];
         uint32_t inc = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -125,7 +173,7 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
         if (lane == 31) s_c[256] = run;
     }
     __syncthreads();
-    if (s_c[256] != ANS_M) {  // corrupt frequency table (block-uniform)
+    if (!hdr_ok || s_c[256] != ANS_M) {  // bad header or corrupt frequency table (block-uniform)
         if (threadIdx.x == 0) raise_flag(fl, FLAG_INDEX);
         return;
     }
@@ -140,85 +188,66 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
         uint32_t c_lo = s_c[lo], c_hi = s_c[lo + 1];
         for (uint32_t slot = s0; slot < s0 + SPT; ++slot) {
             while (slot >= c_hi) { ++lo; c_lo = c_hi; c_hi = s_c[lo + 1]; }
-            s_tab[slot] = (c_hi - c_lo - 1u) | ((slot - c_lo) << 12) | ((uint32_t)(uint8_t)(lo - 128) << 24);
+            s_tab[slot] = (c_hi - c_lo - 1u) | ((uint32_t)(uint8_t)(lo - 128) << 12) | ((slot - c_lo) << 20);
         }
     }
     __syncthreads();
-    const uint32_t chunk = (blockIdx.x - fr.block0[cat]) * ANS_WARPS + wid;
-    if (chunk >= n_chunks) return;
-    const uint32_t* woff = reinterpret_cast<const uint32_t*>(stream + sizeof(AnsHeader));
-    const uint32_t* states = woff + n_chunks + 1;
-    const uint16_t* lcount = reinterpret_cast<const uint16_t*>(states + (size_t)n_chunks * ANS_LANES);
-    const uint16_t* words = lcount + (size_t)n_chunks * ANS_LANES;
-    const uint32_t c0 = woff[chunk], c1 = woff[chunk + 1];
-    const uint32_t cnt = lcount[(size_t)chunk * ANS_LANES + lane];
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-    if (c0 > c1 || c1 > fr.n_words[cat] || c1 - c0 != tot) {  // warp-uniform
-        if (lane == 0) raise_flag(fl, FLAG_INDEX);
-        return;
-    }
+    if (!chunk_ok) return;
     int8_t* cout = out + (size_t)fr.row0[cat] * n_pad;
-    uint32_t x = states[(size_t)chunk * ANS_LANES + lane];
     const uint32_t base = chunk * ANS_CHUNK;
     const uint32_t len = min((uint32_t)ANS_CHUNK, n_sym - base);
     const uint32_t k = (base + lane) / (uint32_t)n;
     uint32_t i = (base + lane) - k * (uint32_t)n;
     int8_t* op = cout + (size_t)k * n_pad + i;  // this lane's next output byte (row k, column i)
     const uint32_t mine = len > (uint32_t)lane ? (len - lane + 31) / 32 : 0u;  // this lane's symbols
-    const uint32_t nw = c1 - c0;
     uint32_t ptr = incl - cnt, end = incl;  // this lane's words, relative to the chunk: [ptr, end)
-    if (nw <= ANS_STAGE && n >= 32) {
-        // common case: the chunk's words staged in shared memory (coalesced), so a
-        // renormalisation is a select on a word loaded beside the table lookup -- no branch.
-        // (The staging area has 288 words of slack: a lane's pointer advances at most once per
-        // step, so even a corrupt stream never reads past it; the final check flags it.)
-        uint16_t* sw = s_words_dyn + wid * (ANS_STAGE + 288);
-        for (uint32_t q0 = 0; q0 < nw; q0 += 32 * 8) {  // 8 loads in flight per lane
-            uint16_t v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint32_t q = q0 + 32 * u + lane;
-                v[u] = q < nw ? __ldg(words + c0 + q) : (uint16_t)0;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint32_t q = q0 + 32 * u + lane;
-                if (q < nw) sw[q] = v[u];
-            }
-        }
-        __syncwarp();
-        // output: 32-bit offset from the category's first row; the lane's column wraps into the
-        // next row once every ~n/32 steps, at step tw (a rare, short branch)
-        uint32_t off = k * (uint32_t)n_pad + i;
+    if (staged) {
+        // common case: a renormalisation is a select on a word already in a register -- no
+        // branch.  (The staging area has 288 words of slack: a lane's pointer advances at
+        // most once per step, so even a corrupt stream never reads past it; the final check
+        // flags it.)  The lane's column wraps into the next row once every ~n/32 steps, at step
+        // tw: steps run in segments that end there, so the hot loop has no row-wrap test.
+        const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(sw);
+        uint32_t wa = wbase + 2u * ptr;             // shared address of the lane's next word
         uint32_t tw = ((uint32_t)n - i + 31) / 32;  // step after which the column passes n
         uint32_t t_i = 0;                           // step at which the lane was at column i
-        // steps run in segments that end where the lane's column passes n, so the hot loop has
-        // no row-wrap test (it compiled to ~8 predicated instructions per step)
+        // the lane's next word waits in a register and is reloaded only after a renormalisation
+        // consumed it (predicated, a step ahead of its use): one shared load per renormalisation,
+        // not one per step.  (Lanes of high-entropy chunks advance in lockstep through regions
+        // spaced by multiples of 32 banks, so per-step word loads were 10-way bank conflicts.)
+        uint16_t wn;
+        asm("ld.shared.u16 %0, [%1];" : "=h"(wn) : "r"(wa));
+        auto step = [&](int u) {
+            const uint32_t e = s_tab[x & (ANS_M - 1)];
+            const uint32_t xs = x >> ANS_PROB_BITS;
+            const uint32_t xd = (e & 0xfffu) * xs + (xs + (e >> 20));  // f * xs + slot - c
+            const bool need = xd < ANS_L;
+            x = need ? ((xd << 16) | (uint32_t)wn) : xd;
+            wa += need ? 2u : 0u;
+            if (need) asm("ld.shared.u16 %0, [%1];" : "=h"(wn) : "r"(wa));
+            op[32 * u] = (int8_t)(e >> 12);
+        };
         for (uint32_t t = 0; t < mine;) {
             const uint32_t tend = min(mine, tw);
+            for (; t + 4 <= tend; t += 4) {
+                step(0);
+                step(1);
+                step(2);
+                step(3);
+                op += 128;
+            }
             for (; t < tend; ++t) {
-                const uint32_t w = sw[ptr];
-                const uint32_t e = s_tab[x & (ANS_M - 1)];
-                const uint32_t xd = ((e & 0xfffu) + 1u) * (x >> ANS_PROB_BITS) + ((e >> 12) & 0xfffu);
-                const bool need = xd < ANS_L;
-                x = need ? ((xd << 16) | w) : xd;
-                ptr += need ? 1u : 0u;
-                cout[off] = (int8_t)(e >> 24);
-                off += 32;
+                step(0);
+                op += 32;
             }
             if (t == tw) {  // column i + 32 (tw - t_i) >= n: continue in the next row
                 i = i + 32 * (tw - t_i) - (uint32_t)n;
-                off += (uint32_t)(n_pad - n);
+                op += n_pad - n;
                 t_i = tw;
                 tw += ((uint32_t)n - i + 31) / 32;
             }
         }
+        ptr = (wa - wbase) >> 1;
     } else {
         // more words than the staging area (> 4 bits per symbol), or rows shorter than a warp:
         // read the words from the stream
@@ -226,8 +255,9 @@ __global__ void __launch_bounds__(ANS_WARPS * 32) k_ans_decode(const AnsFrame fr
         end += c0;
         for (uint32_t t = 0; t < mine; ++t) {
             const uint32_t e = s_tab[x & (ANS_M - 1)];
-            x = ((e & 0xfffu) + 1u) * (x >> ANS_PROB_BITS) + ((e >> 12) & 0xfffu);
-            *op = (int8_t)(e >> 24);
+            const uint32_t xs = x >> ANS_PROB_BITS;
+            x = (e & 0xfffu) * xs + (xs + (e >> 20));
+            *op = (int8_t)(e >> 12);
             if (x < ANS_L) {
                 x = (x << 16) | (ptr < end ? (uint32_t)__ldg(words + ptr) : 0u);
                 ++ptr;
