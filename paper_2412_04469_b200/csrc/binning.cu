@@ -604,6 +604,9 @@ constexpr int PS_MAX_WARPS = 8;
 #ifndef QUEEN_PC_BUDGET
 #define QUEEN_PC_BUDGET 16  // M words of per-(bucket, chunk) counts before the chunk size doubles (measured 4 / 16 / 64: Immersive bucket 0.53 / 0.41 / 0.46 ms, stress 7.2 / 6.1 / 6.6 ms)
 #endif             // k_piece_scatter: chunks (warps) per CTA, fewer when VNB is large
+#ifndef QUEEN_PC_CH0
+#define QUEEN_PC_CH0 PC_CH  // starting chunk size (pairs), doubled up to 8 PC_CH by the budget rule
+#endif
 
 
 struct BucketGeo {
@@ -1254,7 +1257,7 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     uint32_t* ebucket = nullptr;  // after the plans: [etiles] (set below)
     // chunk size: 2048 pairs, doubled while the dense per-(bucket, chunk) counts would exceed
     // ~4 M words (batches of many views: Immersive's 46 views x 40 buckets)
-    bg.ch = PC_CH;
+    bg.ch = QUEEN_PC_CH0;
     while (bg.ch < 8 * PC_CH && (int64_t)bg.VNB * ((count + bg.ch - 1) / bg.ch) > ((int64_t)QUEEN_PC_BUDGET << 20)) bg.ch *= 2;
     const int64_t chunks = (count + bg.ch - 1) / bg.ch;
     bg.CHS = (int)chunks;

@@ -367,7 +367,10 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
     }
 }
 
-constexpr int BLEND_RPT = 4;
+#ifndef QUEEN_BLEND_RPT
+#define QUEEN_BLEND_RPT 4  // rows per thread: a warp covers 16 x 2*RPT pixels
+#endif
+constexpr int BLEND_RPT = QUEEN_BLEND_RPT;
 
 // Blend schedule: a permutation of the gt tiles, longest list first (list-length classes of
 // 32 entries; order inside a class arbitrary).  Tiles are independent, so the schedule never
