@@ -60,6 +60,9 @@ def parse():
                          "t+1 under the blend of frame t")
     ap.add_argument("--no-paper-style", action="store_true", help="skip the decode + 1 centre view timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--apply-after", choices=("projected", "binned"), default="projected",
+                    help="two-lane steps: the next packet's apply waits for the frame's projection "
+                         "(default) or for its whole binning")
     ap.add_argument("--no-profile", action="store_true")
     return ap.parse_args()
 
@@ -425,6 +428,7 @@ def main():
                        resident=src_bufs if world == 1 else None)
     ss.share_scene()
     player = ss.player
+    player.apply_after = args.apply_after
     dps = ss.packets
     A0 = player.planes.clone()  # frame-0 set on every rank (after the broadcast)
     stream = torch.cuda.current_stream()
@@ -534,8 +538,8 @@ def main():
         if two_lane:
             # Headline: two-lane eager steps (runtime.Player.step2): frame t renders on lane t % 2
             # (own context; binning on a high-priority stream, blend on a normal-priority one), so
-            # frame t+1's projection + binning overlap frame t's blend, and packet t+1 is decoded +
-            # applied on a side stream after frame t's binning.  Cross-step overlap means the K
+            # frame t+1's projection + binning overlap frame t's blend, and packet t+1 is decoded
+            # at once and applied on a side stream after frame t's projection (--apply-after).  Cross-step overlap means the K
             # steps are timed as ONE interval (barrier + sync on both sides, max over ranks) and L2
             # is not flushed between steps: a frame's working set (SoA, records, keys, images;
             # ~0.9 GB at N3DV) is several times the 126 MB L2.
@@ -1001,6 +1005,7 @@ def main():
                                    f"{W}x{H}, SH {cfg.deg}, latents {tuple(cfg.lat)}, {cfg.rho:.0%} gates)",
                        "gaussians": cfg.n, "views": V, "width": W, "height": H, "views_per_batch": player.vpb, "render_lanes": player.n_lanes,
                        "frame_lanes": 2 if (use_graph and two_lane) else 1,
+                       "apply_after": args.apply_after if (use_graph and two_lane) else "binned",
                        "parallelism": f"views sharded v mod {world}, Gaussians replicated, packet NCCL-broadcast",
                        "packet_format": args.packet_format,
                        "launch": ("eager two-lane steps: frame t+1's binning (own context, high-priority "

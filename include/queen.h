@@ -331,6 +331,13 @@ queen_status queen_render_mask(queen_ctx* ctx, const queen_gaussians* scene, con
  * bound).  Capturable; no host sync. */
 queen_status queen_wait_binned(const queen_ctx* ctx, void* stream);
 
+/* Makes `stream` wait until the projection of the most recent queen_render_views call on `ctx`
+ * has completed.  The projection is the render's only read of the Gaussian SoA (the binning and
+ * the blend read the projected records in the workspace), so the next frame's
+ * queen_apply_frame (A_t -> A_{t+1}) may overwrite the SoA from then on while this
+ * frame's binning and blend continue.  Capturable; no host sync. */
+queen_status queen_wait_projected(const queen_ctx* ctx, void* stream);
+
 /* Optional separate stream for the blend of queen_render_views[_rgb8] on `ctx` (NULL: the
  * call's stream, the default).  When set, the projection + binning run on the call's stream
  * and the blend on `stream` after them, so a renderer can give the (latency-bound) binning a

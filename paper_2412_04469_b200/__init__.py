@@ -30,7 +30,7 @@ QUEEN_OPT_BLEND_NOMASK, QUEEN_OPT_BLEND_GRID_ORDER = 1, 2
 EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version", "queen_workspace_size",
            "queen_set_workspace", "queen_check", "queen_decode_residuals", "queen_apply_frame", "queen_project",
            "queen_bin_sort", "queen_rasterize", "queen_render_views", "queen_blend_counts",
-           "queen_profile_enable", "queen_profile_read", "queen_wait_binned", "queen_set_blend_stream",
+           "queen_profile_enable", "queen_profile_read", "queen_wait_binned", "queen_wait_projected", "queen_set_blend_stream",
            "queen_wait_rendered", "queen_entropy_encode",
            "queen_entropy_decode", "queen_entropy_decode_frame", "queen_render_mask",
            "queen_densify", "queen_rasterize_rgb8", "queen_render_views_rgb8",
@@ -126,6 +126,7 @@ def lib() -> C.CDLL:
             "queen_render_mask": (i32, [p, C.POINTER(QueenGaussians), p, i32, p, C.POINTER(QueenCamera), i32, C.c_float,
                                         i32, p, p]),
             "queen_wait_binned": (i32, [p, p]),
+            "queen_wait_projected": (i32, [p, p]),
             "queen_set_blend_stream": (i32, [p, p]),
             "queen_wait_rendered": (i32, [p, p]),
             "queen_entropy_encode": (i32, [p, i32, i32, i32, p, C.c_size_t, C.POINTER(C.c_size_t)]),
@@ -456,6 +457,11 @@ def queen_entropy_decode_frame(ctx: Context, stream_ptrs, stream_bytes, lat_dim,
 def queen_wait_binned(ctx: Context, stream=None):
     st = lib().queen_wait_binned(ctx.handle, C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_wait_binned")
+
+
+def queen_wait_projected(ctx: Context, stream=None):
+    st = lib().queen_wait_projected(ctx.handle, C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_wait_projected")
 
 
 def queen_set_blend_stream(ctx: Context, stream=None):

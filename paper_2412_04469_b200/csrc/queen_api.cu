@@ -18,7 +18,8 @@ struct queen_ctx {
     int64_t ws_keys = 0;
     queen::WsLayout L{};
     queen::Prof prof;
-    cudaEvent_t binned = nullptr;  // recorded by queen_render_views after binning (queen_wait_binned)
+    cudaEvent_t binned = nullptr;     // recorded by queen_render_views after binning (queen_wait_binned)
+    cudaEvent_t projected = nullptr;  // recorded after the projection: the last read of the SoA (queen_wait_projected)
     cudaEvent_t rendered = nullptr;     // recorded by queen_render_views after the blend
     cudaStream_t blend_stream = nullptr;  // queen_set_blend_stream: the blend's own stream
     bool blend_elsewhere = false;         // the most recent blend ran on blend_stream
@@ -65,6 +66,7 @@ queen_status queen_create(int device, queen_ctx** out) {
     queen_ctx* c = new queen_ctx();
     c->device = device;
     if (cudaEventCreateWithFlags(&c->binned, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->projected, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->rendered, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
         return QUEEN_ERR_CUDA;
@@ -76,6 +78,7 @@ queen_status queen_create(int device, queen_ctx** out) {
 void queen_destroy(queen_ctx* ctx) {
     if (!ctx) return;
     if (ctx->binned) cudaEventDestroy(ctx->binned);
+    if (ctx->projected) cudaEventDestroy(ctx->projected);
     if (ctx->rendered) cudaEventDestroy(ctx->rendered);
     for (cudaEvent_t e : ctx->prof.pool) cudaEventDestroy(e);
     delete ctx;
@@ -85,6 +88,12 @@ queen_status queen_wait_binned(const queen_ctx* ctx, void* stream) {
     if (!ctx) return QUEEN_ERR_INVALID_ARG;
     return cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->binned, 0) == cudaSuccess ? QUEEN_OK
                                                                                                  : QUEEN_ERR_CUDA;
+}
+
+queen_status queen_wait_projected(const queen_ctx* ctx, void* stream) {
+    if (!ctx) return QUEEN_ERR_INVALID_ARG;
+    return cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), ctx->projected, 0) == cudaSuccess ? QUEEN_OK
+                                                                                                    : QUEEN_ERR_CUDA;
 }
 
 queen_status queen_set_blend_stream(queen_ctx* ctx, void* stream) {
@@ -477,6 +486,8 @@ static queen_status render_impl(queen_ctx* ctx, const queen_gaussians* scene, co
         return cuda_fail(ctx, cudaGetLastError(), "wait rendered event");
     ctx->blend_elsewhere = bs != nullptr;
     if (queen_status st = queen_project(ctx, scene, cams, n_views, &pj, stream)) return st;
+    if (cudaEventRecord(ctx->projected, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return cuda_fail(ctx, cudaGetLastError(), "record projected event");
     if (queen_status st = queen_bin_sort(ctx, &pj, cams, n_views, &b, stream)) return st;
     if (cudaEventRecord(ctx->binned, static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return cuda_fail(ctx, cudaGetLastError(), "record binned event");

@@ -11,7 +11,8 @@ import torch
 from . import (QUEEN_LAT_F32, QUEEN_LAT_INT8, QUEEN_MAX_VIEWS, QUEEN_POS_COO, QUEEN_POS_GATES, Context,
                QueenError, camera_array, gaussians_struct, packet_struct, queen_apply_frame,
                queen_densify, queen_entropy_decode_frame, queen_render_mask, queen_render_views,
-               queen_render_views_f16, queen_render_views_rgb8, queen_set_blend_stream, queen_wait_binned)
+               queen_render_views_f16, queen_render_views_rgb8, queen_set_blend_stream, queen_wait_binned,
+               queen_wait_projected)
 from . import packet as wire
 
 
@@ -153,6 +154,9 @@ class Player:
         self.ctx = self.ctxs[0]
         self.streams = [None] + [torch.cuda.Stream(device=self.dev) for _ in range(self.n_lanes - 1)]
         self.bg = bg
+        # step2: the next packet's apply waits for this frame's projection ("projected", its
+        # last read of the SoA) or for its whole binning ("binned")
+        self.apply_after = "projected"
         self.rgb = torch.empty((V, 3, H, W), dtype=torch.float32, device=self.dev)
         self.T = torch.empty((V, H, W), dtype=torch.float32, device=self.dev) if with_T else None
         self.scene = gaussians_struct(self.planes, n, deg)
@@ -346,9 +350,18 @@ class Player:
             with torch.cuda.stream(side):
                 if ready is not None:
                     side.wait_event(ready)
-                queen_wait_binned(ctx, side)
-                if isinstance(next_pkt, EntropyPacket):
-                    next_pkt.decode(ctx, side)
+                if self.apply_after == "projected":
+                    # the projection is the render's only read of A_t (binning and blend read
+                    # the lane's projected records), so the packet decodes at once and A_{t+1}
+                    # is applied under this frame's binning: the next frame's projection no
+                    # longer waits for this frame's binning chain
+                    if isinstance(next_pkt, EntropyPacket):
+                        next_pkt.decode(ctx, side)
+                    queen_wait_projected(ctx, side)
+                else:
+                    queen_wait_binned(ctx, side)
+                    if isinstance(next_pkt, EntropyPacket):
+                        next_pkt.decode(ctx, side)
                 queen_apply_frame(ctx, self.scene, next_pkt.struct, side)
             main.wait_stream(side)
         return rgb

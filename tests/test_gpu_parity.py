@@ -537,7 +537,8 @@ def test_cuda_graph_frame_equals_eager():
 def test_pipelined_steps_equal_serial_frames():
     """Pipelined steps (Player.step / capture_step: frame t rendered while packet t+1 is decoded
     and applied on a side stream after the render's binning; Player.step2: in addition frame t+1
-    binned on a second context under frame t's blend) give, frame by frame, the same images and
+    binned on a second context under frame t's blend, packet t+1 applied after frame t's
+    projection or binning) give, frame by frame, the same images and
     final SoA, bit for bit, as serial apply-then-render; also with two view batches (the apply
     waits for the LAST batch's binning)."""
     import paper_2412_04469_b200 as Q
@@ -580,18 +581,21 @@ def test_pipelined_steps_equal_serial_frames():
         torch.cuda.synchronize()
         assert torch.equal(gp.rgb, refs[-1])
         assert gp.check_status()[0] == 0
-        # two-lane steps (Player.step2): frame t+1's binning under frame t's blend, 2 contexts
-        tl = Player(sc.planes, sc.n, sc.deg, cams, keys_cap=serial.keys_cap, views_per_batch=vpb)
-        tl.apply(eps[0])
-        outs = [torch.empty_like(tl.rgb) for _ in range(len(eps))]
-        evs = [torch.cuda.Event() for _ in range(len(eps))]
-        for t in range(len(eps)):
-            tl.step2(eps[t + 1] if t + 1 < len(eps) else None, out=outs[t], rendered=evs[t])
-        tl.sync_lanes()
-        torch.cuda.synchronize()
-        for t in range(len(eps)):
-            assert torch.equal(outs[t], refs[t]), ("two-lane", vpb, t)
-        assert torch.equal(tl.planes, serial.planes)
+        # two-lane steps (Player.step2): frame t+1's binning under frame t's blend, 2 contexts;
+        # the next packet applied after the frame's projection (default) or after its binning
+        for after in ("binned", "projected"):
+            tl = Player(sc.planes, sc.n, sc.deg, cams, keys_cap=serial.keys_cap, views_per_batch=vpb)
+            tl.apply_after = after
+            tl.apply(eps[0])
+            outs = [torch.empty_like(tl.rgb) for _ in range(len(eps))]
+            evs = [torch.cuda.Event() for _ in range(len(eps))]
+            for t in range(len(eps)):
+                tl.step2(eps[t + 1] if t + 1 < len(eps) else None, out=outs[t], rendered=evs[t])
+            tl.sync_lanes()
+            torch.cuda.synchronize()
+            for t in range(len(eps)):
+                assert torch.equal(outs[t], refs[t]), ("two-lane", after, vpb, t)
+            assert torch.equal(tl.planes, serial.planes)
         # out=None: the per-lane image buffers (frame t's is valid once `rendered` fires)
         tl2 = Player(sc.planes, sc.n, sc.deg, cams, keys_cap=serial.keys_cap, views_per_batch=vpb)
         tl2.apply(eps[0])
