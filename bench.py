@@ -60,6 +60,10 @@ def parse():
                          "t+1 under the blend of frame t")
     ap.add_argument("--no-paper-style", action="store_true", help="skip the decode + 1 centre view timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--frame-lanes", type=int, default=0,
+                    help="two-lane steps: frames in flight (one libqueen context each); 0 = auto: 4 when "
+                         "this rank renders <= 8 Mpixel per frame (short frames: later frames' binning runs "
+                         "ahead), else 2")
     ap.add_argument("--apply-after", choices=("projected", "binned"), default="projected",
                     help="two-lane steps: the next packet's apply waits for the frame's projection "
                          "(default) or for its whole binning")
@@ -429,6 +433,8 @@ def main():
     ss.share_scene()
     player = ss.player
     player.apply_after = args.apply_after
+    rank_px = len(mine) * W * H
+    player.frame_lanes = max(2, args.frame_lanes) if args.frame_lanes else (4 if rank_px <= (8 << 20) else 2)
     dps = ss.packets
     A0 = player.planes.clone()  # frame-0 set on every rank (after the broadcast)
     stream = torch.cuda.current_stream()
@@ -546,13 +552,14 @@ def main():
             graph_pipelined = {"value": args.steps / (total_ms / 1e3), "unit": UNIT,
                                "ms_per_step": total_ms / args.steps,
                                "note": "one-lane pipelined steps replayed from CUDA graphs, L2 flushed between steps"}
-            outs = [torch.empty_like(player.rgb) for _ in range(2)]
+            nl = player.frame_lanes
+            outs = [torch.empty_like(player.rgb) for _ in range(nl)]
             player.planes.copy_(A0)
             bcast(0)
             player.apply(dps[0])
             for t in range(args.warmup):
                 bcast(t + 1)
-                player.step2(dps[(t + 1) % ng], out=outs[t & 1])
+                player.step2(dps[(t + 1) % ng], out=outs[t % nl])
             player.sync_lanes()
             if not args.no_profile:
                 player.profile(True)
@@ -566,7 +573,7 @@ def main():
             e0.record(stream)
             for k, t in enumerate(range(args.warmup, args.warmup + args.steps)):
                 bcast(t + 1)
-                player.step2(dps[(t + 1) % ng], out=outs[t & 1], rendered=done[k])
+                player.step2(dps[(t + 1) % ng], out=outs[t % nl], rendered=done[k])
             player.sync_lanes()
             e1.record(stream)
             torch.cuda.synchronize()
@@ -580,15 +587,17 @@ def main():
             if world > 1:
                 dist.all_reduce(tot, op=dist.ReduceOp.MAX)
             total_ms = float(tot[0])
-            done_ms = [float(x) for x in tot[1:]]
+            # display order: frame t can be shown once frames 0..t are rendered (step2 keeps
+            # completions in order, so this is the identity there)
+            done_ms = list(np.maximum.accumulate([float(x) for x in tot[1:]]))
             dts = [b - a for a, b in zip(done_ms, done_ms[1:])]
             med_ms = statistics.median(dts) if dts else total_ms / args.steps
             frame_intervals = {"median_ms": med_ms, "mean_ms": total_ms / args.steps,
                                "p10_ms": float(np.percentile(dts, 10)) if dts else None,
                                "p90_ms": float(np.percentile(dts, 90)) if dts else None,
                                "fps_median": 1e3 / med_ms if med_ms > 0 else None,
-                               "definition": "dt = done(t) - done(t-1), done(t) = frame t's last view rendered, "
-                                             "max over ranks; median over the timed frames (P:1457)"}
+                               "definition": "dt = done(t) - done(t-1), done(t) = frames 0..t's last view rendered "
+                                             "(display order), max over ranks; median over the timed frames (P:1457)"}
             if not args.no_profile:
                 prof = player.profile_read(reset=True)
                 n_prof_frames = args.steps
@@ -872,9 +881,9 @@ def main():
         # the copies of frame k overlap the compute of frames k +- 1 like a real player.
         pin_pk = [torch.from_numpy(b).pin_memory() for b in host_bufs] if rank == 0 else None
         odt = {"rgb8": torch.uint8, "f16": torch.float16, "f32": torch.float32}[fmt]
-        # three image slots: with two-lane steps frame k+2's binning may start while frame k's D2H
-        # is still running, so a slot is reused three frames later
-        NB = 3
+        # frame_lanes + 1 image slots: with two-lane steps frame k+frame_lanes' binning may start
+        # while frame k's D2H is still running, so a slot is reused frame_lanes + 1 frames later
+        NB = player.frame_lanes + 1
         out_dev = [torch.empty(player.rgb.shape, dtype=odt, device=dev) for _ in range(NB)]
         out_host = [torch.empty(player.rgb.shape, dtype=odt).pin_memory() for _ in range(NB)]
         recv = [torch.zeros(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
@@ -1004,7 +1013,7 @@ def main():
             "config": {"workload": f"{cfg.name}: BASELINE configs[{cfg.index}] ({cfg.n} Gaussians, {V} views "
                                    f"{W}x{H}, SH {cfg.deg}, latents {tuple(cfg.lat)}, {cfg.rho:.0%} gates)",
                        "gaussians": cfg.n, "views": V, "width": W, "height": H, "views_per_batch": player.vpb, "render_lanes": player.n_lanes,
-                       "frame_lanes": 2 if (use_graph and two_lane) else 1,
+                       "frame_lanes": player.frame_lanes if (use_graph and two_lane) else 1,
                        "apply_after": args.apply_after if (use_graph and two_lane) else "binned",
                        "parallelism": f"views sharded v mod {world}, Gaussians replicated, packet NCCL-broadcast",
                        "packet_format": args.packet_format,

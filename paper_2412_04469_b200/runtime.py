@@ -157,6 +157,7 @@ class Player:
         # step2: the next packet's apply waits for this frame's projection ("projected", its
         # last read of the SoA) or for its whole binning ("binned")
         self.apply_after = "projected"
+        self.frame_lanes = 2  # step2: frames in flight, one libqueen context (workspace) each
         self.rgb = torch.empty((V, 3, H, W), dtype=torch.float32, device=self.dev)
         self.T = torch.empty((V, H, W), dtype=torch.float32, device=self.dev) if with_T else None
         self.scene = gaussians_struct(self.planes, n, deg)
@@ -292,7 +293,8 @@ class Player:
 
     def step2(self, next_pkt, out=None, rgb8: bool = False, rendered: torch.cuda.Event | None = None,
               ready: torch.cuda.Event | None = None, consumed: torch.cuda.Event | None = None):
-        """Two-lane pipelined frame step (eager): like step(), but frame t renders on lane t % 2 --
+        """Two-lane pipelined frame step (eager): like step(), but frame t renders on lane
+        t % frame_lanes (2 by default) --
         its own libqueen context (workspace), a high-priority stream for projection + binning and
         a normal-priority stream for the blend (queen_set_blend_stream) -- and the current stream
         does NOT wait for it, so frame t+1's projection and binning (on the other lane) run under
@@ -300,10 +302,10 @@ class Player:
         `rendered` is recorded on the blend stream when frame t's image is complete; `out` must
         not be reused before that (out=None: one of two per-lane image buffers, returned; with_T:
         per-lane T buffers, self.T_lanes).  With out=None the returned buffer is rendered into
-        again two frames later: a caller that reads it on another stream passes `consumed`, an
-        event it records after its last read of THIS call's image (before the step two frames
-        on); that later step's blend waits for it before overwriting the buffer.  Call
-        sync_lanes() before reading results on the current stream."""
+        again frame_lanes frames later: a caller that reads it on another stream passes
+        `consumed`, an event it records after its last read of THIS call's image (before the step
+        frame_lanes frames on); that later step's blend waits for it before overwriting the
+        buffer.  Call sync_lanes() before reading results on the current stream."""
         if self.n_lanes != 1:
             raise ValueError("two-lane frame steps need a single view-batch lane")
         main = torch.cuda.current_stream(self.dev)
@@ -311,7 +313,7 @@ class Player:
             # per lane: context, high-priority binning stream, normal-priority blend stream
             lo, hi = torch.cuda.Stream.priority_range()  # (lowest, highest) priority
             self._lanes2 = []
-            for k in range(2):
+            for k in range(max(2, int(self.frame_lanes))):
                 ctx = self.ctx if k == 0 else Context(self.device)
                 if k:  # joins self.ctxs: profiled, status-checked and re-carved with the others
                     ctx.set_workspace(self.planes.shape[1], self.vpb, self.W, self.H, self.keys_cap)
@@ -320,28 +322,39 @@ class Player:
                 self._lanes2.append((ctx, torch.cuda.Stream(device=self.dev, priority=hi), bs))
             self._lane_t = 0
             self._side = getattr(self, "_side", None) or torch.cuda.Stream(device=self.dev, priority=hi)
-        lane = self._lane_t & 1
+        lane = self._lane_t % len(self._lanes2)
         ctx, ls, bs = self._lanes2[lane]
         self._lane_t += 1
         ls.wait_stream(main)  # the frame's apply (and the caller's ordering) first
         if out is None or self.T is not None:  # the two lanes' blends overlap: per-lane buffers
             if not hasattr(self, "rgb_lanes"):
-                self.rgb_lanes = [self.rgb, torch.empty_like(self.rgb)]
-                self.T_lanes = [self.T, torch.empty_like(self.T)] if self.T is not None else [None, None]
+                nl = len(self._lanes2)
+                self.rgb_lanes = [self.rgb] + [torch.empty_like(self.rgb) for _ in range(nl - 1)]
+                self.T_lanes = ([self.T] + [torch.empty_like(self.T) for _ in range(nl - 1)] if self.T is not None
+                                else [None] * nl)
         rgb = self.rgb_lanes[lane] if out is None else out
         T = self.T_lanes[lane] if self.T is not None else None
         if not hasattr(self, "_consumed"):
-            self._consumed = [None, None]
+            self._consumed = [None] * len(self._lanes2)
         if self._consumed[lane] is not None:  # the reader of this lane's previous image is done
             bs.wait_event(self._consumed[lane])
         self._consumed[lane] = consumed if out is None else None
         fn = _out_fn(rgb8, out)
+        # frames complete in order: with more than two lanes this frame's blend starts after the
+        # previous frame's (a later frame could otherwise finish first; measured at 3-4 lanes);
+        # the binning of later frames still runs ahead on their own lanes.  Two lanes complete
+        # in order anyway, and there the blends' tails may overlap.
+        if len(self._lanes2) > 2 and getattr(self, "_blend_done", None) is not None:
+            bs.wait_event(self._blend_done)
         queen_set_blend_stream(ctx, bs)  # only for these calls: render() / step() keep one stream
         try:
             for (a, b), arr in zip(self.batches, self.cam_arrays):
                 fn(ctx, self.scene, None, rgb[a:b], None if T is None else T[a:b], self.bg, ls, cam_array=arr)
         finally:
             queen_set_blend_stream(ctx, None)
+        if len(self._lanes2) > 2:
+            self._blend_done = torch.cuda.Event()
+            self._blend_done.record(bs)
         if rendered is not None:
             rendered.record(bs)
         if next_pkt is not None:

@@ -583,9 +583,9 @@ def test_pipelined_steps_equal_serial_frames():
         assert gp.check_status()[0] == 0
         # two-lane steps (Player.step2): frame t+1's binning under frame t's blend, 2 contexts;
         # the next packet applied after the frame's projection (default) or after its binning
-        for after in ("binned", "projected"):
+        for after, nl in (("binned", 2), ("projected", 2), ("projected", 3)):
             tl = Player(sc.planes, sc.n, sc.deg, cams, keys_cap=serial.keys_cap, views_per_batch=vpb)
-            tl.apply_after = after
+            tl.apply_after, tl.frame_lanes = after, nl
             tl.apply(eps[0])
             outs = [torch.empty_like(tl.rgb) for _ in range(len(eps))]
             evs = [torch.cuda.Event() for _ in range(len(eps))]
@@ -594,7 +594,7 @@ def test_pipelined_steps_equal_serial_frames():
             tl.sync_lanes()
             torch.cuda.synchronize()
             for t in range(len(eps)):
-                assert torch.equal(outs[t], refs[t]), ("two-lane", after, vpb, t)
+                assert torch.equal(outs[t], refs[t]), ("two-lane", after, nl, vpb, t)
             assert torch.equal(tl.planes, serial.planes)
         # out=None: the per-lane image buffers (frame t's is valid once `rendered` fires)
         tl2 = Player(sc.planes, sc.n, sc.deg, cams, keys_cap=serial.keys_cap, views_per_batch=vpb)
