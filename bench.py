@@ -87,16 +87,61 @@ def rank_views(V, rank, world):
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock and clock-event reasons sampled DURING the timed region: NVML (nvidia_ml_py) polled
+    from a thread every 5 ms, one sample taken as the region starts (a short region -- N3DV's 20
+    frames are ~40 ms -- is over before `nvidia-smi -lms` has started); nvidia-smi as fallback."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
+        cvd = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [x for x in cvd.split(",") if x.strip()]
+        if ids and gpu_index < len(ids) and ids[gpu_index].strip().isdigit():
+            self.idx = int(ids[gpu_index])  # NVML / nvidia-smi index of this rank's device
         self.p = None
+        self.nv = None
         self.path = f"/tmp/queen_clocks_{os.getpid()}.csv"
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.bits = (pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                         pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap)
+        except Exception:
+            self.nv = None
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        smax = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.samples.append((float(sm), float(smax), int(r)))
+
+    def _loop(self):
+        while not self.halt.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            self.halt.wait(0.005)
 
     def start(self):
+        if self.nv is not None:
+            import threading
+            self.samples = []
+            self.halt = threading.Event()
+            try:
+                self._sample()
+            except Exception:
+                self.nv = None
+            if self.nv is not None:
+                self.th = threading.Thread(target=self._loop, daemon=True)
+                self.th.start()
+                return
         try:
             self.f = open(self.path, "w")
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -105,6 +150,15 @@ class ClockSampler:
             self.p = None
 
     def stop(self):
+        """Call right after the region's closing synchronize."""
+        if self.nv is not None:
+            self.halt.set()
+            self.th.join(timeout=2)
+            sm = [a for a, _, _ in self.samples]
+            smax = self.samples[-1][1] if self.samples else None
+            reasons = {nm for _, _, r in self.samples for nm, bit in zip(self.NAMES, self.bits) if r & bit}
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                    "samples": len(sm), "source": "nvml, 5 ms"}
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
@@ -115,7 +169,6 @@ class ClockSampler:
             self.p.kill()
         self.f.close()
         sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 9:
@@ -125,12 +178,12 @@ class ClockSampler:
                 smax = float(parts[2])
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[5:9]):
+            for nm, val in zip(self.NAMES, parts[5:9]):
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         os.unlink(self.path)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi -lms 100"}
 
 
 # ----------------------------------------------------------------------------- roofline model
