@@ -624,9 +624,11 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             done = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]  # frame t rendered
             e0.record(stream)
+            h0 = time.perf_counter()
             for k, t in enumerate(range(args.warmup, args.warmup + args.steps)):
                 bcast(t + 1)
                 player.step2(dps[(t + 1) % ng], out=outs[t % nl], rendered=done[k])
+            host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # host enqueue time per step
             player.sync_lanes()
             e1.record(stream)
             torch.cuda.synchronize()
@@ -645,7 +647,7 @@ def main():
             done_ms = list(np.maximum.accumulate([float(x) for x in tot[1:]]))
             dts = [b - a for a, b in zip(done_ms, done_ms[1:])]
             med_ms = statistics.median(dts) if dts else total_ms / args.steps
-            frame_intervals = {"median_ms": med_ms, "mean_ms": total_ms / args.steps,
+            frame_intervals = {"median_ms": med_ms, "mean_ms": total_ms / args.steps, "host_enqueue_ms": host_ms,
                                "p10_ms": float(np.percentile(dts, 10)) if dts else None,
                                "p90_ms": float(np.percentile(dts, 90)) if dts else None,
                                "fps_median": 1e3 / med_ms if med_ms > 0 else None,
