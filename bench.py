@@ -203,8 +203,10 @@ def algorithmic_bytes(stage, cfg, n, vpb_list, K_list, k_coo, M_list, ent_bytes=
         return ent_bytes + n * SL
     if stage == "project":  # read the attributes once per batch, write 64 B per (view, Gaussian)
         return sum(n * 4 * P + n * v * 64 for v, M, K in bt)
-    if stage == "compact":  # count: tiles + rect + depth (16 B/elem); compact: tiles + depth (8 B), pairs out
-        return sum(n * v * 24 + 8 * M for v, M, K in bt)
+    if stage == "compact":  # count: tiles + rect + depth (16 B/elem); compact: tiles + depth (8 B), pairs out;
+        # tile ranges finalised here too (counts + local starts in, (first, last) out: 16 B per tile)
+        T = ((cfg.width + 15) // 16) * ((cfg.height + 15) // 16)
+        return sum(n * v * 24 + 8 * M + 16 * v * T for v, M, K in bt)
     if stage == "depth_sort":  # 4 LSD passes over the (depth, index) pairs, 16 B each
         return sum(4 * 16 * M for v, M, K in bt)
     if stage == "bucket":  # count: pair index + rect in, rect copy out (20 B/pair); scatter: 12 B/pair in, 8 B/piece out

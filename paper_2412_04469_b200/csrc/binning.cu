@@ -5,14 +5,17 @@
 // The entries are ordered by (gt, depth, index), gt = view*T + tile.  Every copy of a Gaussian
 // carries the same depth, so the depth order is sorted once, on the M visible (view,
 // Gaussian) pairs; the entries are then written directly at their final positions:
+//       k_bin_init      the batch's tickets, histograms, look-back words, depth min/max
 //   K3a k_slab_count    per slab of S consecutive elements of a view (one CTA): visible
 //                       count, depth-digit histograms, and the slab's entries per tile via
 //                       a shared-memory 2D difference array of tile rects -> counts[slab][t]
-//       k_slab_sum      per view: entries per tile; k_view_scan: view-local tile starts
-//       k_totals        K, M, capacity check; slab offsets of the visible pairs
-//       k_slab_compact  visible pairs in (view, index) order -> (depth bits, flat index) [M]
+//       k_slab_sum      per view: entries per tile
+//       k_view_scan_totals  per view: view-local tile starts; its last block: K, M, capacity
+//                       check, slab offsets of the visible pairs
+//       k_slab_compact  visible pairs in (view, index) order -> (depth bits, flat index) [M];
+//                       also (K6) [first, last+1) of each gt from the per-tile counts, and its
+//                       last block scans the depth-digit histograms
 //   K5a k_onesweep32<9> x3 (+<8>)  stable sort of the pairs by relative depth (27 + 4 bits)
-//   K6  k_ranges_finalize  [first, last+1) of each gt from the per-tile counts
 //   K4' k_piece_count / k_piece_colscan / k_piece_base / k_piece_scatter: the pairs cut
 //       into pieces per 16x8-tile bucket, each bucket's pieces in depth order
 //   K5' k_emit_plan + k_emit: each bucket's entries written at their final positions
@@ -50,7 +53,9 @@ constexpr int LB_BATCH = QUEEN_LB_BATCH;
 #define QUEEN_OS_MATCH_OR 1  // warp match by shared atomicOr (measured, round-1 tile sort: 488 -> 417 us vs match.any)
 #endif  // onesweep look-back predecessors loaded per round trip
 
-enum : int { TK_DEPTH = 0, TK_EMIT = 4 };  // dynamic-tile tickets: depth passes 0..3, emission
+// dynamic-tile tickets: depth passes 0..3, emission; last-block counters of k_view_scan_totals
+// and k_slab_compact
+enum : int { TK_DEPTH = 0, TK_EMIT = 4, TK_VSCAN = 5, TK_COMPACT = 6 };
 
 
 
@@ -190,8 +195,7 @@ __global__ void __launch_bounds__(256) k_slab_sum(const uint32_t* __restrict__ c
 }
 
 // Per-view block (1024 threads): view-local exclusive starts of the tile totals and the view total.
-__global__ void __launch_bounds__(1024) k_view_scan(const uint32_t* __restrict__ tcounts, int T, uint32_t* lstart,
-                                                    uint32_t* view_tot) {
+__device__ void view_scan_body(const uint32_t* __restrict__ tcounts, int T, uint32_t* lstart, uint32_t* view_tot) {
     __shared__ uint32_t s_w[32];
     const int v = blockIdx.x;
     const uint32_t* tc = tcounts + (int64_t)v * T;
@@ -220,14 +224,21 @@ __global__ void __launch_bounds__(1024) k_view_scan(const uint32_t* __restrict__
     if (threadIdx.x == 0) view_tot[v] = tot;
 }
 
-// K, M, overflow flag; slab visible counts -> global exclusive offsets (in place).  One block.
-__global__ void __launch_bounds__(1024) k_totals(const uint32_t* __restrict__ view_tot, int n_views, uint32_t* svis,
-                                                 int slabs, uint32_t cap, uint32_t* Kd, DevFlags* fl) {
+__global__ void __launch_bounds__(1024) k_view_scan(const uint32_t* __restrict__ tcounts, int T, uint32_t* lstart,
+                                                    uint32_t* view_tot) {
+    view_scan_body(tcounts, T, lstart, view_tot);
+}
+
+// K, M, overflow flag; slab visible counts -> global exclusive offsets (in place).  Run by one
+// block of 1024 threads: the last view block of k_view_scan, or k_totals.  view_tot is read
+// through L2 (other blocks of the same launch wrote it).
+__device__ void totals_body(const uint32_t* view_tot, int n_views, uint32_t* svis, int slabs, uint32_t cap,
+                            uint32_t* Kd, DevFlags* fl) {
     __shared__ uint32_t s_w[32];
     __shared__ uint32_t s_carry;
     if (threadIdx.x == 0) {
         unsigned long long K = 0;
-        for (int v = 0; v < n_views; ++v) K += view_tot[v];
+        for (int v = 0; v < n_views; ++v) K += __ldcg(view_tot + v);
         const bool over = K > cap;
         if (over) {
             raise_flag(fl, FLAG_CAPACITY);
@@ -265,16 +276,56 @@ __global__ void __launch_bounds__(1024) k_totals(const uint32_t* __restrict__ vi
     if (threadIdx.x == 0) Kd[1] = s_carry;  // M visible pairs
 }
 
+__global__ void __launch_bounds__(1024) k_totals(const uint32_t* __restrict__ view_tot, int n_views, uint32_t* svis,
+                                                 int slabs, uint32_t cap, uint32_t* Kd, DevFlags* fl) {
+    totals_body(view_tot, n_views, svis, slabs, cap, Kd, fl);
+}
+
+// k_view_scan, whose last block to finish then runs totals_body (one launch instead of two)
+__global__ void __launch_bounds__(1024) k_view_scan_totals(const uint32_t* __restrict__ tcounts, int T,
+                                                           uint32_t* lstart, uint32_t* view_tot, int n_views,
+                                                           uint32_t* svis, int slabs, uint32_t cap, uint32_t* Kd,
+                                                           DevFlags* fl, uint32_t* ticket) {
+    view_scan_body(tcounts, T, lstart, view_tot);
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    totals_body(view_tot, n_views, svis, slabs, cap, Kd, fl);
+}
+
 // K3b: per slab, its visible elements in index order -> (depth bits, flat index) pairs at the
 // slab's global offset.  Rounds of 4096 elements, 8 consecutive per thread (vector loads);
 // block scan of the per-thread visible counts; pairs staged in shared memory in order and
 // written out coalesced.
+// (ranges_slice, hist_scan_body: defined below)
+__device__ void ranges_slice(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ lstart,
+                             const uint32_t* __restrict__ view_tot, int n_views, uint32_t T, uint32_t cap,
+                             const uint32_t* Kd, uint2* __restrict__ ranges);
+__device__ void hist_scan_body(const uint32_t* hist, uint32_t* excl, int passes, int bins);
+
+struct RangesArgs {  // k_ranges_finalize's work, done by k_slab_compact's blocks (grid-stride)
+    const uint32_t* counts;
+    const uint32_t* lstart;
+    const uint32_t* view_tot;
+    int n_views;
+    uint32_t T, cap;
+    const uint32_t* Kd;
+    uint2* ranges;
+};
+
+// Also: every block finalises a slice of the tile ranges, and the last block to finish scans
+// the depth digit histograms (k_ranges_finalize and k_hist_scan folded in: two launches fewer)
 __global__ void __launch_bounds__(SLAB_THREADS) k_slab_compact(const uint32_t* __restrict__ tiles,
                                                                const uint32_t* __restrict__ depth, int n_pad, int S,
                                                                int spv, const uint32_t* __restrict__ soff,
                                                                const uint32_t* __restrict__ dminmax,
                                                                uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dvals,
-                                                               uint32_t* __restrict__ hist) {
+                                                               uint32_t* __restrict__ hist, uint32_t* __restrict__ hist_excl,
+                                                               uint32_t* ticket, RangesArgs ra) {
     constexpr int NW = SLAB_THREADS / 32;
     __shared__ uint32_t s_w[NW];
     __shared__ uint32_t s_k[SLAB_ROUND], s_j[SLAB_ROUND];
@@ -333,15 +384,24 @@ __global__ void __launch_bounds__(SLAB_THREADS) k_slab_compact(const uint32_t* _
     }
     for (int q = threadIdx.x; q < DEPTH_PASSES * MAX_BINS; q += SLAB_THREADS)
         if (sh[q]) atomicAdd(&hist[q], sh[q]);
+    ranges_slice(ra.counts, ra.lstart, ra.view_tot, ra.n_views, ra.T, ra.cap, ra.Kd, ra.ranges);
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    hist_scan_body(hist, hist_excl, DEPTH_PASSES, MAX_BINS);
 }
 
-// exclusive scan of each pass's digit counts (one warp per pass)
-__global__ void k_hist_scan(const uint32_t* hist, uint32_t* excl, int passes, int bins) {
+// exclusive scan of each pass's digit counts (one warp per pass; threads past 32 * passes idle)
+__device__ void hist_scan_body(const uint32_t* hist, uint32_t* excl, int passes, int bins) {
     const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (p >= passes) return;
     const int per = bins / 32;
     uint32_t s = 0;
-    for (int q = 0; q < per; ++q) s += hist[p * MAX_BINS + lane * per + q];
+    for (int q = 0; q < per; ++q) s += __ldcg(hist + p * MAX_BINS + lane * per + q);
     uint32_t x = s;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -350,10 +410,14 @@ __global__ void k_hist_scan(const uint32_t* hist, uint32_t* excl, int passes, in
     }
     uint32_t run = x - s;
     for (int q = 0; q < per; ++q) {
-        const uint32_t c = hist[p * MAX_BINS + lane * per + q];
+        const uint32_t c = __ldcg(hist + p * MAX_BINS + lane * per + q);
         excl[p * MAX_BINS + lane * per + q] = run;
         run += c;
     }
+}
+
+__global__ void k_hist_scan(const uint32_t* hist, uint32_t* excl, int passes, int bins) {
+    hist_scan_body(hist, excl, passes, bins);
 }
 
 // ---------------------------------------------------------------------------
@@ -1082,11 +1146,11 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
 }
 
 // ranges[gt] = view base + local start (view bases = exclusive scan of the <= 64 view
-// totals); [0,0) for empty tiles and everywhere on capacity overflow (already flagged)
-__global__ void __launch_bounds__(256) k_ranges_finalize(const uint32_t* __restrict__ counts,
-                                                         const uint32_t* __restrict__ lstart,
-                                                         const uint32_t* __restrict__ view_tot, int n_views, uint32_t T,
-                                                         uint32_t cap, const uint32_t* Kd, uint2* __restrict__ ranges) {
+// totals); [0,0) for empty tiles and everywhere on capacity overflow (already flagged).  Every
+// block of the calling grid takes a grid-stride slice of the tiles.
+__device__ void ranges_slice(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ lstart,
+                             const uint32_t* __restrict__ view_tot, int n_views, uint32_t T, uint32_t cap,
+                             const uint32_t* Kd, uint2* __restrict__ ranges) {
     __shared__ unsigned long long s_base[QUEEN_MAX_VIEWS + 1];
     if (threadIdx.x == 0) {
         unsigned long long r = 0;
@@ -1103,6 +1167,24 @@ __global__ void __launch_bounds__(256) k_ranges_finalize(const uint32_t* __restr
     }
 }
 
+__global__ void __launch_bounds__(256) k_ranges_finalize(const uint32_t* __restrict__ counts,
+                                                         const uint32_t* __restrict__ lstart,
+                                                         const uint32_t* __restrict__ view_tot, int n_views, uint32_t T,
+                                                         uint32_t cap, const uint32_t* Kd, uint2* __restrict__ ranges) {
+    ranges_slice(counts, lstart, view_tot, n_views, T, cap, Kd, ranges);
+}
+
+// one launch zeroing the binning's per-batch state: tickets, digit histograms, the depth
+// passes' look-back words (uint4 stores), the depth min/max and the key counts
+__global__ void __launch_bounds__(256) k_bin_init(DevFlags* fl, uint32_t* hist, int hist_words, uint4* lb,
+                                                  size_t lb_vec, uint32_t* dminmax, uint32_t* K) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < 16) fl->tickets[t] = 0u;
+    if (t < 4) K[t] = 0u;
+    if (t == 0) { dminmax[0] = 0xffffffffu; dminmax[1] = 0u; }
+    for (size_t q = t; q < (size_t)hist_words; q += (size_t)gridDim.x * blockDim.x) hist[q] = 0u;
+    for (size_t q = t; q < lb_vec; q += (size_t)gridDim.x * blockDim.x) lb[q] = make_uint4(0u, 0u, 0u, 0u);
+}
 
 static int num_sms() {
     static int sms = 0;
@@ -1185,39 +1267,43 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     const size_t dplane = (size_t)(gx + 1) * (gy + 1);
     cudaError_t e;
     prof->begin(ST_COMPACT, s);
-    if ((e = cudaMemsetAsync(fl->tickets, 0, sizeof(fl->tickets), s))) return e;
-    if ((e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * DEPTH_PASSES * MAX_BINS, s))) return e;
-
-    if ((e = cudaMemsetAsync(depth_lb, 0, sizeof(uint32_t) * DEPTH_PASSES * MAX_BINS * (size_t)(os_elem_tiles + 1), s)))
-        return e;
     uint32_t* dminmax = reinterpret_cast<uint32_t*>(ws + L.dminmax);
-    if ((e = cudaMemsetAsync(dminmax, 0xff, sizeof(uint32_t), s))) return e;       // min <- 0xffffffff
-    if ((e = cudaMemsetAsync(dminmax + 1, 0, sizeof(uint32_t), s))) return e;      // max <- 0
-
-    if ((e = cudaMemsetAsync(bins.K, 0, sizeof(uint32_t) * 4, s))) return e;
+    {  // one launch for the per-batch state (was six memsets)
+        const size_t lb_vec = (size_t)DEPTH_PASSES * MAX_BINS * (size_t)(os_elem_tiles + 1) / 4;
+        const unsigned blocks = (unsigned)std::max<size_t>(1, std::min<size_t>((size_t)sms * 4, (lb_vec + 255) / 256));
+        k_bin_init<<<blocks, 256, 0, s>>>(fl, hist, DEPTH_PASSES * MAX_BINS, reinterpret_cast<uint4*>(depth_lb), lb_vec,
+                                          dminmax, bins.K);
+    }
+    // ranges: view base + local start per tile (the emission writes entries at their final
+    // positions); finalised inside k_slab_compact
+    RangesArgs ra{tcounts, lstart, view_tot, n_views, (uint32_t)T, cap, Kd, reinterpret_cast<uint2*>(bins.ranges)};
     if (bp.slabs > 0) {
         k_slab_count<<<(unsigned)bp.slabs, SLAB_THREADS, sizeof(int) * dplane, s>>>(
             proj.tiles, reinterpret_cast<const short4*>(proj.rect), proj.depth, proj.n_pad, (int)bp.S, (int)bp.spv, gx, gy,
             scount, svis, dminmax);
         k_slab_sum<<<dim3((unsigned)((T + 255) / 256), (unsigned)n_views), 256, 0, s>>>(scount, (int)bp.spv, (int)T,
                                                                                         tcounts);
-        k_view_scan<<<n_views, 1024, 0, s>>>(tcounts, (int)T, lstart, view_tot);
+        k_view_scan_totals<<<n_views, 1024, 0, s>>>(tcounts, (int)T, lstart, view_tot, n_views, svis, (int)bp.slabs, cap,
+                                                    Kd, fl, &fl->tickets[TK_VSCAN]);
+        k_slab_compact<<<(unsigned)bp.slabs, SLAB_THREADS, 0, s>>>(proj.tiles, proj.depth, proj.n_pad, (int)bp.S,
+                                                                  (int)bp.spv, svis, dminmax, dk[0], dv[0], hist,
+                                                                  hist_excl, &fl->tickets[TK_COMPACT], ra);
     } else {
         if ((e = cudaMemsetAsync(tcounts, 0, sizeof(uint32_t) * 2 * T * n_views, s))) return e;
         if ((e = cudaMemsetAsync(view_tot, 0, sizeof(uint32_t) * n_views, s))) return e;
+        k_totals<<<1, 1024, 0, s>>>(view_tot, n_views, svis, 0, cap, Kd, fl);
+        k_hist_scan<<<1, 32 * DEPTH_PASSES, 0, s>>>(hist, hist_excl, DEPTH_PASSES, MAX_BINS);
+        k_ranges_finalize<<<sms * 2, 256, 0, s>>>(ra.counts, ra.lstart, ra.view_tot, n_views, (uint32_t)T, cap, Kd,
+                                                  ra.ranges);
     }
-    k_totals<<<1, 1024, 0, s>>>(view_tot, n_views, svis, (int)bp.slabs, cap, Kd, fl);
-    if (bp.slabs > 0)
-        k_slab_compact<<<(unsigned)bp.slabs, SLAB_THREADS, 0, s>>>(proj.tiles, proj.depth, proj.n_pad, (int)bp.S,
-                                                                  (int)bp.spv, svis, dminmax, dk[0], dv[0], hist);
-    prof->end(s, bp.slabs > 0 ? 5 : 1);
+    prof->end(s, bp.slabs > 0 ? 5 : 4);
     // depth digits (LSD: least significant first) on the visible pairs
     prof->begin(ST_DEPTH_SORT, s);
     // depth keys are relative to the batch's smallest visible depth (order-preserving, and the
     // range of a scene's depths fits 27 bits unless it spans > 2^27 ulps): three 9-bit passes,
     // then bits 27..31, which is skipped (no copy; the bucket kernels read the previous buffer)
-    // whenever that digit is 0 for every key
-    k_hist_scan<<<1, 32 * DEPTH_PASSES, 0, s>>>(hist, hist_excl, DEPTH_PASSES, MAX_BINS);
+    // whenever that digit is 0 for every key.  (The digit histograms' exclusive scans were done
+    // by k_slab_compact's last block.)
     int cur = 0;
     for (int p = 0; p < DEPTH_PASSES; ++p) {
         uint32_t* lbp = depth_lb + (size_t)p * MAX_BINS * (os_elem_tiles + 1);
@@ -1229,12 +1315,9 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
                                hist_excl + p * MAX_BINS, lbp, &fl->tickets[TK_DEPTH + p], fl, s, hist + p * MAX_BINS);
         cur ^= 1;
     }
-    prof->end(s, DEPTH_PASSES + 1);
-    // per-tile entry counts -> ranges (the emission writes entries at their final positions)
-    prof->begin(ST_RANGES, s);
-    k_ranges_finalize<<<sms * 2, 256, 0, s>>>(tcounts, lstart, view_tot, n_views, (uint32_t)T, cap, Kd,
-                                              reinterpret_cast<uint2*>(bins.ranges));
-    prof->end(s);
+    prof->end(s, DEPTH_PASSES);
+    prof->begin(ST_RANGES, s);  // (folded into k_slab_compact: kept as an empty stage)
+    prof->end(s, 0);
     // pieces (pair, bucket) bucketed in depth order, then emitted tile by tile
     BucketGeo bg;
     bg.gx = gx;
