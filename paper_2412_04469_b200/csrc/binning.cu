@@ -53,9 +53,9 @@ constexpr int LB_BATCH = QUEEN_LB_BATCH;
 #define QUEEN_OS_MATCH_OR 1  // warp match by shared atomicOr (measured, round-1 tile sort: 488 -> 417 us vs match.any)
 #endif  // onesweep look-back predecessors loaded per round trip
 
-// dynamic-tile tickets: depth passes 0..3, emission; last-block counters of k_view_scan_totals
-// and k_slab_compact
-enum : int { TK_DEPTH = 0, TK_EMIT = 4, TK_VSCAN = 5, TK_COMPACT = 6 };
+// dynamic-tile tickets: depth passes 0..3, emission; last-block counters of k_view_scan_totals,
+// k_slab_compact and k_piece_colscan
+enum : int { TK_DEPTH = 0, TK_EMIT = 4, TK_VSCAN = 5, TK_COMPACT = 6, TK_COLSCAN = 7 };
 
 
 
@@ -730,61 +730,19 @@ __global__ void __launch_bounds__(PC_THREADS) k_piece_count(const uint32_t* __re
     for (int b = threadIdx.x; b < g.VNB; b += PC_THREADS) pcnt[(size_t)b * g.CHS + c] = sc[b];
 }
 
-// per bucket (one warp): exclusive scan of its pieces over the chunks (in place) and the total
-__global__ void __launch_bounds__(256) k_piece_colscan(uint32_t* __restrict__ pcnt, const uint32_t* __restrict__ Kd,
-                                                       BucketGeo g, uint32_t* __restrict__ ptotal) {
-    const int b = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (b >= g.VNB) return;
-    const uint32_t M = visible_pairs(Kd);
-    const uint32_t nch = (M + g.ch - 1) / g.ch;
-    uint32_t* row = pcnt + (size_t)b * g.CHS;
-    // exclusive offsets in chunk order, 32 chunks per round (coalesced)
-    uint32_t carry = 0;
-    for (uint32_t c0 = 0; c0 < nch; c0 += 32) {
-        const uint32_t c = c0 + lane;
-        const uint32_t x = c < nch ? row[c] : 0u;
-        uint32_t inc = x;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        if (c < nch) row[c] = carry + inc - x;
-        carry += __shfl_sync(0xffffffffu, inc, 31);
-    }
-    if (lane == 0) ptotal[b] = carry;
-}
-
-// bucket-local start of emit tile k of bucket b: the first (chunk, bucket) segment that starts
-// at or after k * em_e (emit tiles hold whole segments), or the bucket total
-// (also returns the chunk c whose segment starts there: off[c] = start, c = nch at the end)
-__device__ __forceinline__ uint32_t emit_start(const uint32_t* row, uint32_t nch, uint32_t total, uint32_t k,
-                                               uint32_t em_e, uint32_t& chunk) {
-    const uint32_t want = k * em_e;
-    uint32_t lo = 0, hi = nch;  // first c with off[c] >= want (off[nch] := total)
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (row[mid] >= want) hi = mid; else lo = mid + 1;
-    }
-    chunk = lo;
-    return lo < nch ? row[lo] : total;
-}
-
 // one block: bucket bases (exclusive scan of the totals) and emit-tile bases; meta[0] = pieces,
-// meta[1] = emit tiles
-__global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict__ ptotal, int VNB, uint32_t em_e,
-                                                     uint32_t* __restrict__ pbase, uint32_t* __restrict__ ebase,
-                                                     uint32_t* __restrict__ meta, uint32_t* __restrict__ ebucket,
-                                                     uint32_t* __restrict__ Kd) {
-    __shared__ uint32_t s_w[32], s_e[32];
+// meta[1] = emit tiles.  Run by the last block of k_piece_colscan (256 threads).
+__device__ void piece_base_body(const uint32_t* ptotal, int VNB, uint32_t em_e, uint32_t* __restrict__ pbase,
+                                uint32_t* __restrict__ ebase, uint32_t* __restrict__ meta, uint32_t* __restrict__ Kd) {
+    constexpr int NWB = 8;  // warps of the 256-thread block
+    __shared__ uint32_t s_w[NWB], s_e[NWB];
     __shared__ uint32_t s_carry, s_ecarry;
     if (threadIdx.x == 0) { s_carry = 0; s_ecarry = 0; }
     __syncthreads();
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int b0 = 0; b0 < VNB; b0 += blockDim.x) {
         const int b = b0 + threadIdx.x;
-        const uint32_t x = b < VNB ? ptotal[b] : 0u;
+        const uint32_t x = b < VNB ? __ldcg(ptotal + b) : 0u;
         const uint32_t y = (x + em_e - 1) / em_e;
         uint32_t ix = x, iy = y;
 #pragma unroll
@@ -795,7 +753,8 @@ __global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict_
         if (lane == 31) { s_w[w] = ix; s_e[w] = iy; }
         __syncthreads();
         uint32_t px = 0, py = 0, tx = 0, ty = 0;
-        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+#pragma unroll
+        for (int q = 0; q < NWB; ++q) {
             px += q < w ? s_w[q] : 0u;
             py += q < w ? s_e[q] : 0u;
             tx += s_w[q];
@@ -816,31 +775,98 @@ __global__ void __launch_bounds__(1024) k_piece_base(const uint32_t* __restrict_
         meta[1] = s_ecarry;
         Kd[3] = s_carry;  // pieces P (evidence: bench's algorithmic bytes)
     }
-    __syncthreads();
-    for (int b = threadIdx.x; b < VNB; b += blockDim.x) {  // each emit tile's bucket
-        const uint32_t e0 = ebase[b], et = (ptotal[b] + em_e - 1) / em_e;
-        for (uint32_t k = 0; k < et; ++k) ebucket[e0 + k] = (uint32_t)b;
-    }
 }
 
-// one thread per emit tile: its bucket, index k, pieces [s0, s0 + n) of the bucket, and its
-// chunk segments [c0, c0 + nseg) -- all the binary searches in flight at once, before k_emit;
-// also clears the tile's look-back words (only the NE tiles in use, not the capacity)
+// per bucket (one warp): exclusive scan of its pieces over the chunks (in place) and the total,
+// 8 rounds of 32 chunks loaded at once; the last block to finish then computes the bucket and
+// emit-tile bases (piece_base_body: one launch fewer)
+constexpr int CS_ROUNDS = 8;
+__global__ void __launch_bounds__(256) k_piece_colscan(uint32_t* __restrict__ pcnt, const uint32_t* __restrict__ Kd_in,
+                                                       BucketGeo g, uint32_t* __restrict__ ptotal,
+                                                       uint32_t* __restrict__ pbase, uint32_t* __restrict__ ebase,
+                                                       uint32_t* __restrict__ meta, uint32_t* __restrict__ Kd,
+                                                       uint32_t* ticket) {
+    const int b = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (b < g.VNB) {  // warp-uniform
+        const uint32_t M = visible_pairs(Kd_in);
+        const uint32_t nch = (M + g.ch - 1) / g.ch;
+        uint32_t* row = pcnt + (size_t)b * g.CHS;
+        uint32_t carry = 0;
+        for (uint32_t c0 = 0; c0 < nch; c0 += 32 * CS_ROUNDS) {
+            uint32_t xs[CS_ROUNDS];
+#pragma unroll
+            for (int u = 0; u < CS_ROUNDS; ++u) {
+                const uint32_t c = c0 + 32 * u + lane;
+                xs[u] = c < nch ? row[c] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < CS_ROUNDS; ++u) {
+                const uint32_t c = c0 + 32 * u + lane;
+                uint32_t inc = xs[u];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                if (c < nch) row[c] = carry + inc - xs[u];
+                carry += __shfl_sync(0xffffffffu, inc, 31);
+            }
+        }
+        if (lane == 0) ptotal[b] = carry;
+    }
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    piece_base_body(ptotal, g.VNB, (uint32_t)g.em_e, pbase, ebase, meta, Kd);
+}
+
+// bucket-local start of emit tile k of bucket b: the first (chunk, bucket) segment that starts
+// at or after k * em_e (emit tiles hold whole segments), or the bucket total
+// (also returns the chunk c whose segment starts there: off[c] = start, c = nch at the end).
+// Both ends of a tile are searched in lockstep (independent loads in flight together).
+__device__ __forceinline__ void emit_range(const uint32_t* row, uint32_t nch, uint32_t total, uint32_t k,
+                                           uint32_t em_e, uint32_t& s0, uint32_t& c0, uint32_t& s1, uint32_t& c1) {
+    const uint32_t wa = k * em_e, wb = (k + 1) * em_e;
+    uint32_t la = 0, ha = nch, lb = 0, hb = nch;  // first c with off[c] >= want (off[nch] := total)
+    while (la < ha || lb < hb) {
+        const uint32_t ma = (la + ha) >> 1, mb = (lb + hb) >> 1;
+        const uint32_t va = la < ha ? row[ma] : 0u, vb = lb < hb ? row[mb] : 0u;
+        if (la < ha) { if (va >= wa) ha = ma; else la = ma + 1; }
+        if (lb < hb) { if (vb >= wb) hb = mb; else lb = mb + 1; }
+    }
+    c0 = la;
+    c1 = lb;
+    s0 = la < nch ? row[la] : total;
+    s1 = lb < nch ? row[lb] : total;
+}
+
+// one thread per emit tile: its bucket (binary search of the emit-tile bases), index k, pieces
+// [s0, s0 + n) of the bucket, and its chunk segments [c0, c0 + nseg) -- all the searches in
+// flight at once, before k_emit; also clears the tile's look-back words (only the NE tiles in
+// use, not the capacity)
 __global__ void __launch_bounds__(256) k_emit_plan(const uint32_t* __restrict__ pcnt, const uint32_t* __restrict__ ptotal,
                                                    const uint32_t* __restrict__ ebase,
-                                                   const uint32_t* __restrict__ ebucket,
                                                    const uint32_t* __restrict__ meta, const uint32_t* __restrict__ Kd,
                                                    BucketGeo g, uint4* __restrict__ plan, uint32_t* __restrict__ lb) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= meta[1]) return;
     const uint32_t nch = (visible_pairs(Kd) + g.ch - 1) / g.ch;
-    const uint32_t b = ebucket[t];
-    const uint32_t k = t - ebase[b];
+    uint32_t lo = 0, hi = (uint32_t)g.VNB;  // the last bucket b with ebase[b] <= t (non-empty: ebase[b+1] > t)
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(ebase + mid) <= t) lo = mid; else hi = mid;
+    }
+    const uint32_t b = lo;
+    const uint32_t k = t - __ldg(ebase + b);
     const uint32_t tot = ptotal[b];
     const uint32_t* row = pcnt + (size_t)b * g.CHS;
-    uint32_t cA, cB;
-    const uint32_t s0 = emit_start(row, nch, tot, k, (uint32_t)g.em_e, cA);
-    const uint32_t s1 = emit_start(row, nch, tot, k + 1, (uint32_t)g.em_e, cB);
+    uint32_t s0, cA, s1, cB;
+    emit_range(row, nch, tot, k, (uint32_t)g.em_e, s0, cA, s1, cB);
     plan[2 * (size_t)t] = make_uint4(b, k, s0, s1 - s0);
     plan[2 * (size_t)t + 1] = make_uint4(cA, cB - cA, 0u, 0u);
     uint4* lbt = reinterpret_cast<uint4*>(lb + (size_t)t * BK_T);  // the tile's look-back words, unpublished
@@ -1337,7 +1363,6 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     uint32_t* meta = ebase + bg.VNB + 1;
     uint32_t* emit_lb = reinterpret_cast<uint32_t*>(ws + L.emit_lb);
     uint4* plan = reinterpret_cast<uint4*>(ws + L.eplan);                      // [etiles][2]
-    uint32_t* ebucket = nullptr;  // after the plans: [etiles] (set below)
     // chunk size: 2048 pairs, doubled while the dense per-(bucket, chunk) counts would exceed
     // ~4 M words (batches of many views: Immersive's 46 views x 40 buckets)
     bg.ch = QUEEN_PC_CH0;
@@ -1346,7 +1371,6 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     bg.CHS = (int)chunks;
     bg.em_e = proj.n_pad > (1 << 20) ? 128 : 256;  // measured: stress (3 M) 128, N3DV / Immersive 256
     const int64_t etiles = ((int64_t)cap + bg.em_e - 1) / bg.em_e + bg.VNB + 1;
-    ebucket = reinterpret_cast<uint32_t*>(plan + 2 * (size_t)etiles);
     const size_t vsm = sizeof(uint32_t) * (size_t)bg.VNB;
     const uint32_t* dlast_in = dv[cur ^ 1];   // input of the last depth pass
     const uint32_t* dlast_out = dv[cur];      // its output (unless it was skipped)
@@ -1359,18 +1383,18 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     prof->begin(ST_BUCKET, s);
     if (chunks > 0) {
         k_piece_count<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, rlo, rhi);
-        k_piece_colscan<<<(unsigned)((bg.VNB + 7) / 8), 256, 0, s>>>(pcnt, Kd, bg, ptotal);
-        k_piece_base<<<1, 1024, 0, s>>>(ptotal, bg.VNB, (uint32_t)bg.em_e, pbase, ebase, meta, ebucket, Kd);
+        k_piece_colscan<<<(unsigned)((bg.VNB + 7) / 8), 256, 0, s>>>(pcnt, Kd, bg, ptotal, pbase, ebase, meta, Kd,
+                                                                     &fl->tickets[TK_COLSCAN]);
         // warps per chunk: each holds VNB cursors in shared memory
         int wpc = (int)std::max<int64_t>(1, std::min<int64_t>(PS_MAX_WARPS, (int64_t)PC_MAX_SMEM / (4 * (int64_t)bg.VNB)));
         while (wpc > 1 && (bg.ch / wpc) % (32 * PS_ROUNDS)) --wpc;
         k_piece_scatter<<<(unsigned)chunks, 32 * wpc, (size_t)wpc * 4 * bg.VNB, s>>>(
             dlast_in, dlast_out, triv, Kd, rlo, rhi, bg, pcnt, pbase, bins.keys_alt, bins.keys);
     }
-    prof->end(s, chunks > 0 ? 5 : 1);
+    prof->end(s, chunks > 0 ? 3 : 0);
     prof->begin(ST_EMIT, s);
     if (chunks > 0)
-        k_emit_plan<<<(unsigned)((etiles + 255) / 256), 256, 0, s>>>(pcnt, ptotal, ebase, ebucket, meta, Kd, bg, plan,
+        k_emit_plan<<<(unsigned)((etiles + 255) / 256), 256, 0, s>>>(pcnt, ptotal, ebase, meta, Kd, bg, plan,
                                                                      emit_lb);
     if (chunks > 0)
         k_emit<<<(unsigned)std::min<int64_t>(emit_grid(), (etiles + EW_WARPS - 1) / EW_WARPS), EW_WARPS * 32, 0, s>>>(bins.keys_alt, bins.keys, plan, pbase, meta, Kd,
