@@ -16,7 +16,7 @@
 //                       also (K6) [first, last+1) of each gt from the per-tile counts, and its
 //                       last block scans the depth-digit histograms
 //   K5a k_onesweep32<9> x3 (+<8>)  stable sort of the pairs by relative depth (27 + 4 bits)
-//   K4' k_piece_count / k_piece_colscan / k_piece_base / k_piece_scatter: the pairs cut
+//   K4' k_piece_count / k_piece_colscan (+ bases) / k_piece_scatter: the pairs cut
 //       into pieces per 16x8-tile bucket, each bucket's pieces in depth order
 //   K5' k_emit_plan + k_emit: each bucket's entries written at their final positions
 // The result equals sorting the 96-bit (gt << 31 | depth, index) tuples (oracle: std::sort).
@@ -648,17 +648,19 @@ __global__ void __launch_bounds__(Onesweep<BITS>::NT) k_onesweep32(const uint32_
 // (m = their rank), the final entry list is known position by position:
 //   entry (tile t, pair m) -> ranges[t].first + #{pairs m' < m whose rect covers t}
 // and every such count is local to t's bucket.  So:
-//   k_piece_count   per chunk of g.ch depth-ordered pairs: pieces per bucket -> pcnt[b][chunk]
+//   k_piece_count   per chunk of g.ch depth-ordered pairs: pieces per bucket -> pcnt[b][chunk];
+//                   the pairs' tile rects copied into m order for the scatter
 //   k_piece_colscan per bucket: exclusive scan over chunks (in place) -> the bucket's
-//                   (chunk, bucket) segment offsets; totals
-//   k_piece_base    bucket bases (scan of totals) and emit-tile bases (ceil(total / em_e))
-//   k_piece_scatter per chunk: each piece's m into its (chunk, bucket) segment (order inside a
-//                   segment arbitrary: shared-memory cursors)
-//   k_emit          per emit tile (whole segments of one bucket, ~em_e pieces): sort the m
-//                   values (unique), count entries per bucket tile, resolve each tile's offset
-//                   among the bucket's earlier emit tiles by decoupled look-back, then write
-//                   every entry's Gaussian index at its final position, ranked stably in m order
-//                   (per-warp match words over the bucket's tiles).
+//                   (chunk, bucket) segment offsets and totals; its last block: bucket bases
+//                   and emit-tile bases (ceil(total / em_e) tiles per bucket)
+//   k_piece_scatter per chunk: each piece (Gaussian index, rect inside the bucket) into its
+//                   (chunk, bucket) segment, in m order (per-warp cursors, match.any ranks)
+//   k_emit_plan     per emit tile (whole segments of one bucket, ~em_e pieces): its bucket,
+//                   piece range and segment range (binary searches); clears its look-back words
+//   k_emit          per emit tile (one warp): entries per bucket tile, each tile's offset among
+//                   the bucket's earlier emit tiles by decoupled look-back, then every entry's
+//                   Gaussian index written at its final position -- rank among the round's
+//                   earlier pieces = popc(R[ly] & C[lx] & lower lanes) from 24 coverage ballots
 // The result is bit-identical to the sorted (gt, depth, index) order: a bucket's pieces are
 // emitted in m order, and m order is (depth, view, index) order.
 // ---------------------------------------------------------------------------
