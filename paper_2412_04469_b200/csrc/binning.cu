@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(1024) k_view_scan_totals(const uint32_t* __res
 // (ranges_slice, hist_scan_body: defined below)
 __device__ void ranges_slice(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ lstart,
                              const uint32_t* __restrict__ view_tot, int n_views, uint32_t T, uint32_t cap,
-                             const uint32_t* Kd, uint2* __restrict__ ranges);
+                             const uint32_t* Kd, uint2* __restrict__ ranges, uint32_t* ohist);
 __device__ void hist_scan_body(const uint32_t* hist, uint32_t* excl, int passes, int bins);
 
 struct RangesArgs {  // k_ranges_finalize's work, done by k_slab_compact's blocks (grid-stride)
@@ -315,6 +315,7 @@ struct RangesArgs {  // k_ranges_finalize's work, done by k_slab_compact's block
     uint32_t T, cap;
     const uint32_t* Kd;
     uint2* ranges;
+    uint32_t* ocnt;  // blend-schedule class counts [ORDER_BINS] | cursors [ORDER_BINS]
 };
 
 // Also: every block finalises a slice of the tile ranges, and the last block to finish scans
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(SLAB_THREADS) k_slab_compact(const uint32_t* _
     }
     for (int q = threadIdx.x; q < DEPTH_PASSES * MAX_BINS; q += SLAB_THREADS)
         if (sh[q]) atomicAdd(&hist[q], sh[q]);
-    ranges_slice(ra.counts, ra.lstart, ra.view_tot, ra.n_views, ra.T, ra.cap, ra.Kd, ra.ranges);
+    ranges_slice(ra.counts, ra.lstart, ra.view_tot, ra.n_views, ra.T, ra.cap, ra.Kd, ra.ranges, ra.ocnt);
     __shared__ bool s_last;
     __threadfence();
     __syncthreads();
@@ -393,6 +394,19 @@ __global__ void __launch_bounds__(SLAB_THREADS) k_slab_compact(const uint32_t* _
     if (!s_last) return;
     __threadfence();
     hist_scan_body(hist, hist_excl, DEPTH_PASSES, MAX_BINS);
+    if (threadIdx.x >= 32 * DEPTH_PASSES && threadIdx.x < 32 * DEPTH_PASSES + 32) {
+        // blend schedule: each class's first position (exclusive scan, two classes per lane)
+        const int l = threadIdx.x & 31;
+        const uint32_t a = __ldcg(ra.ocnt + 2 * l), b = __ldcg(ra.ocnt + 2 * l + 1);
+        uint32_t x = a + b;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (l >= o) x += y;
+        }
+        ra.ocnt[ORDER_BINS + 2 * l] = x - a - b;
+        ra.ocnt[ORDER_BINS + 2 * l + 1] = x - b;
+    }
 }
 
 // exclusive scan of each pass's digit counts (one warp per pass; threads past 32 * passes idle)
@@ -697,14 +711,41 @@ __device__ __forceinline__ const uint32_t* depth_order(const uint32_t* a, const 
 
 __device__ __forceinline__ uint32_t visible_pairs(const uint32_t* Kd) { return Kd[2] ? 0u : Kd[1]; }
 
+struct OrderSched {  // the blend schedule built by k_piece_count (see launch_rasterize's order_pre)
+    const uint2* ranges;
+    uint32_t* cursor;  // per class: next position (starts from k_slab_compact's last block)
+    uint32_t* order;   // [n_views * T] tile permutation
+};
+
 __global__ void __launch_bounds__(PC_THREADS) k_piece_count(const uint32_t* __restrict__ dva,
                                                             const uint32_t* __restrict__ dvb,
                                                             const uint32_t* __restrict__ triv,
                                                             const uint32_t* __restrict__ Kd,
                                                             const short4* __restrict__ rect, BucketGeo g,
                                                             uint32_t* __restrict__ pcnt, uint32_t* __restrict__ rlo,
-                                                            uint32_t* __restrict__ rhi) {
+                                                            uint32_t* __restrict__ rhi, OrderSched osched) {
     extern __shared__ uint32_t sc[];  // [VNB]
+    {  // the blend schedule (tiles longest list first): slices of PC_THREADS tiles, grid-stride
+        __shared__ uint32_t s_cnt[ORDER_BINS], s_at[ORDER_BINS];
+        const uint32_t G = (uint32_t)g.VNB / (uint32_t)g.NB * (uint32_t)g.T;  // n_views * T
+        for (uint32_t c0 = blockIdx.x * PC_THREADS; c0 < G; c0 += gridDim.x * PC_THREADS) {
+            for (int q = threadIdx.x; q < ORDER_BINS; q += PC_THREADS) s_cnt[q] = 0u;
+            __syncthreads();
+            const uint32_t i = c0 + threadIdx.x;
+            int cl = 0;
+            uint32_t rank = 0;
+            if (i < G) {
+                cl = order_class(osched.ranges[i]);
+                rank = atomicAdd(&s_cnt[cl], 1u);
+            }
+            __syncthreads();
+            for (int q = threadIdx.x; q < ORDER_BINS; q += PC_THREADS)
+                if (s_cnt[q]) s_at[q] = atomicAdd(&osched.cursor[q], s_cnt[q]);
+            __syncthreads();
+            if (i < G) osched.order[s_at[cl] + rank] = i;
+            __syncthreads();
+        }
+    }
     const uint32_t M = visible_pairs(Kd);
     const uint32_t c = blockIdx.x;
     if ((uint64_t)c * g.ch >= M) return;
@@ -1178,20 +1219,29 @@ __global__ void __launch_bounds__(EW_WARPS * 32) k_emit(const uint32_t* __restri
 // block of the calling grid takes a grid-stride slice of the tiles.
 __device__ void ranges_slice(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ lstart,
                              const uint32_t* __restrict__ view_tot, int n_views, uint32_t T, uint32_t cap,
-                             const uint32_t* Kd, uint2* __restrict__ ranges) {
+                             const uint32_t* Kd, uint2* __restrict__ ranges, uint32_t* ohist) {
     __shared__ unsigned long long s_base[QUEEN_MAX_VIEWS + 1];
+    __shared__ uint32_t s_oh[ORDER_BINS];
     if (threadIdx.x == 0) {
         unsigned long long r = 0;
         for (int q = 0; q < n_views; ++q) { s_base[q] = r; r += view_tot[q]; }
     }
+    for (int q = threadIdx.x; q < ORDER_BINS; q += blockDim.x) s_oh[q] = 0u;
     __syncthreads();
     const bool overflow = Kd[2] != 0u;
     const uint64_t G = (uint64_t)n_views * T;
     for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G; g += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t c = counts[g];
         const unsigned long long st = s_base[g / T] + lstart[g], en = st + c;
-        ranges[g] = (c && !overflow) ? make_uint2((uint32_t)(st < cap ? st : cap), (uint32_t)(en < cap ? en : cap))
-                                     : make_uint2(0u, 0u);
+        const uint2 r = (c && !overflow) ? make_uint2((uint32_t)(st < cap ? st : cap), (uint32_t)(en < cap ? en : cap))
+                                         : make_uint2(0u, 0u);
+        ranges[g] = r;
+        if (ohist) atomicAdd(&s_oh[order_class(r)], 1u);  // the blend schedule's class counts
+    }
+    if (ohist) {
+        __syncthreads();
+        for (int q = threadIdx.x; q < ORDER_BINS; q += blockDim.x)
+            if (s_oh[q]) atomicAdd(&ohist[q], s_oh[q]);
     }
 }
 
@@ -1199,15 +1249,16 @@ __global__ void __launch_bounds__(256) k_ranges_finalize(const uint32_t* __restr
                                                          const uint32_t* __restrict__ lstart,
                                                          const uint32_t* __restrict__ view_tot, int n_views, uint32_t T,
                                                          uint32_t cap, const uint32_t* Kd, uint2* __restrict__ ranges) {
-    ranges_slice(counts, lstart, view_tot, n_views, T, cap, Kd, ranges);
+    ranges_slice(counts, lstart, view_tot, n_views, T, cap, Kd, ranges, nullptr);
 }
 
 // one launch zeroing the binning's per-batch state: tickets, digit histograms, the depth
 // passes' look-back words (uint4 stores), the depth min/max and the key counts
 __global__ void __launch_bounds__(256) k_bin_init(DevFlags* fl, uint32_t* hist, int hist_words, uint4* lb,
-                                                  size_t lb_vec, uint32_t* dminmax, uint32_t* K) {
+                                                  size_t lb_vec, uint32_t* dminmax, uint32_t* K, uint32_t* ocnt) {
     const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < 16) fl->tickets[t] = 0u;
+    if (ocnt && t < 2 * ORDER_BINS) ocnt[t] = 0u;  // blend-schedule class counts | cursors
     if (t < 4) K[t] = 0u;
     if (t == 0) { dminmax[0] = 0xffffffffu; dminmax[1] = 0u; }
     for (size_t q = t; q < (size_t)hist_words; q += (size_t)gridDim.x * blockDim.x) hist[q] = 0u;
@@ -1271,7 +1322,8 @@ static void onesweep(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, u
 
 
 cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
-                            const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof) {
+                            const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof, bool* order_ready) {
+    if (order_ready) *order_ready = false;
     const int gx = (W + 15) / 16, gy = (H + 15) / 16;
     const int64_t T = (int64_t)gx * gy;
     const int64_t count = (int64_t)n_views * proj.n_pad;
@@ -1296,15 +1348,18 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     cudaError_t e;
     prof->begin(ST_COMPACT, s);
     uint32_t* dminmax = reinterpret_cast<uint32_t*>(ws + L.dminmax);
+    // the blend schedule (class counts | cursors | tile permutation) in the workspace's order
+    // region: built by k_slab_compact (counts, cursors) and k_piece_count (permutation)
+    uint32_t* ocnt = reinterpret_cast<uint32_t*>(ws + L.order);
     {  // one launch for the per-batch state (was six memsets)
         const size_t lb_vec = (size_t)DEPTH_PASSES * MAX_BINS * (size_t)(os_elem_tiles + 1) / 4;
         const unsigned blocks = (unsigned)std::max<size_t>(1, std::min<size_t>((size_t)sms * 4, (lb_vec + 255) / 256));
         k_bin_init<<<blocks, 256, 0, s>>>(fl, hist, DEPTH_PASSES * MAX_BINS, reinterpret_cast<uint4*>(depth_lb), lb_vec,
-                                          dminmax, bins.K);
+                                          dminmax, bins.K, ocnt);
     }
     // ranges: view base + local start per tile (the emission writes entries at their final
     // positions); finalised inside k_slab_compact
-    RangesArgs ra{tcounts, lstart, view_tot, n_views, (uint32_t)T, cap, Kd, reinterpret_cast<uint2*>(bins.ranges)};
+    RangesArgs ra{tcounts, lstart, view_tot, n_views, (uint32_t)T, cap, Kd, reinterpret_cast<uint2*>(bins.ranges), ocnt};
     if (bp.slabs > 0) {
         k_slab_count<<<(unsigned)bp.slabs, SLAB_THREADS, sizeof(int) * dplane, s>>>(
             proj.tiles, reinterpret_cast<const short4*>(proj.rect), proj.depth, proj.n_pad, (int)bp.S, (int)bp.spv, gx, gy,
@@ -1384,7 +1439,9 @@ cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, q
     if (8 * (size_t)bg.VNB > PC_MAX_SMEM) return cudaErrorInvalidConfiguration;  // > 25600 buckets: not reachable (<= 64 4K views)
     prof->begin(ST_BUCKET, s);
     if (chunks > 0) {
-        k_piece_count<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, rlo, rhi);
+        const OrderSched os{reinterpret_cast<const uint2*>(bins.ranges), ocnt + ORDER_BINS, ocnt + 2 * ORDER_BINS};
+        k_piece_count<<<(unsigned)chunks, PC_THREADS, vsm, s>>>(dlast_in, dlast_out, triv, Kd, r4, bg, pcnt, rlo, rhi, os);
+        if (order_ready) *order_ready = bp.slabs > 0;
         k_piece_colscan<<<(unsigned)((bg.VNB + 7) / 8), 256, 0, s>>>(pcnt, Kd, bg, ptotal, pbase, ebase, meta, Kd,
                                                                      &fl->tickets[TK_COLSCAN]);
         // warps per chunk: each holds VNB cursors in shared memory

@@ -284,8 +284,10 @@ queen_status queen_project(queen_ctx* ctx, const queen_gaussians* scene, const q
     return QUEEN_OK;
 }
 
-queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_camera* cams, int32_t n_views,
-                            queen_bins* bins, void* stream) {
+// order_ready (render paths): set when the binning also built the blend's tile schedule
+static queen_status bin_sort_impl(queen_ctx* ctx, const queen_proj* proj, const queen_camera* cams, int32_t n_views,
+                                  queen_bins* bins, void* stream, bool* order_ready) {
+    if (order_ready) *order_ready = false;
     if (!ctx || !ctx->ws) return fail(ctx, QUEEN_ERR_INVALID_ARG, "no ctx/workspace");
     if (!proj || !bins || !bins->keys || !bins->keys_alt || !bins->vals || !bins->vals_alt || !bins->ranges || !bins->K)
         return fail(ctx, QUEEN_ERR_INVALID_ARG, "null proj/bins");
@@ -302,9 +304,14 @@ queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_
         !scratch_fits(need, ctx->L))
         return fail(ctx, QUEEN_ERR_SHAPE, "workspace scratch too small for this batch");
     cudaError_t e = launch_bin_sort(*proj, n_views, W, H, *bins, ctx->ws, ctx->L, flags_of(ctx),
-                                    static_cast<cudaStream_t>(stream), &ctx->prof);
+                                    static_cast<cudaStream_t>(stream), &ctx->prof, order_ready);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "bin_sort");
     return QUEEN_OK;
+}
+
+queen_status queen_bin_sort(queen_ctx* ctx, const queen_proj* proj, const queen_camera* cams, int32_t n_views,
+                            queen_bins* bins, void* stream) {
+    return bin_sort_impl(ctx, proj, cams, n_views, bins, stream, nullptr);
 }
 
 // workspace scratch for the blend schedule (tile order), if the workspace covers this call
@@ -317,16 +324,18 @@ static uint32_t* order_scratch(queen_ctx* ctx, int32_t n_views, int W, int H) {
 
 static queen_status rasterize_impl(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
                                    const queen_camera* cams, int32_t n_views, const float bg[3], float* rgb_out,
-                                   float* T_out, uint8_t* rgb8_out, void* stream, int alt_mode = OUT_RGB8) {
+                                   float* T_out, uint8_t* rgb8_out, void* stream, int alt_mode = OUT_RGB8,
+                                   bool order_ready = false) {
     if (!ctx) return QUEEN_ERR_INVALID_ARG;
     if (!proj || !bins || !(rgb_out || rgb8_out) || !bg) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null args");
     if (queen_status st = check_cams(ctx, cams, n_views, true)) return st;
     const uint32_t* vals = bins->sorted_in_alt ? bins->vals_alt : bins->vals;
     int nl = 1;
+    uint32_t* ows = order_scratch(ctx, n_views, cams[0].width, cams[0].height);
     cudaError_t e = launch_rasterize(proj->rec, proj->n_pad, bins->ranges, vals, n_views, cams[0].width, cams[0].height,
                                      bg[0], bg[1], bg[2], rgb_out, T_out, rgb8_out, rgb8_out ? alt_mode : OUT_F32, 0.f,
-                                     order_scratch(ctx, n_views, cams[0].width, cams[0].height),
-                                     static_cast<cudaStream_t>(stream), &nl, &ctx->prof, ctx->opts);
+                                     ows, static_cast<cudaStream_t>(stream), &nl, &ctx->prof, ctx->opts,
+                                     (order_ready && ows) ? ows + 2 * ORDER_BINS : nullptr);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "rasterize");
     return QUEEN_OK;
 }
@@ -488,12 +497,13 @@ static queen_status render_impl(queen_ctx* ctx, const queen_gaussians* scene, co
     if (queen_status st = queen_project(ctx, scene, cams, n_views, &pj, stream)) return st;
     if (cudaEventRecord(ctx->projected, static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return cuda_fail(ctx, cudaGetLastError(), "record projected event");
-    if (queen_status st = queen_bin_sort(ctx, &pj, cams, n_views, &b, stream)) return st;
+    bool ord = false;
+    if (queen_status st = bin_sort_impl(ctx, &pj, cams, n_views, &b, stream, &ord)) return st;
     if (cudaEventRecord(ctx->binned, static_cast<cudaStream_t>(stream)) != cudaSuccess)
         return cuda_fail(ctx, cudaGetLastError(), "record binned event");
-    if (!bs) return rasterize_impl(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, rgb8_out, stream, alt_mode);
+    if (!bs) return rasterize_impl(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, rgb8_out, stream, alt_mode, ord);
     if (cudaStreamWaitEvent(bs, ctx->binned, 0) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "blend wait");
-    queen_status st = rasterize_impl(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, rgb8_out, bs, alt_mode);
+    queen_status st = rasterize_impl(ctx, &pj, &b, cams, n_views, bg, rgb_out, T_out, rgb8_out, bs, alt_mode, ord);
     if (!st && cudaEventRecord(ctx->rendered, bs) != cudaSuccess)
         return cuda_fail(ctx, cudaGetLastError(), "record rendered event");
     return st;

@@ -108,6 +108,11 @@ inline int64_t buckets_per_view(int W, int H) {
 // Blend schedule (raster.cu): tiles launched longest list first, by list length classes of
 // 32 entries (ORDER_BINS classes, the last open-ended), so the grid's tail holds short tiles.
 constexpr int ORDER_BINS = 64;
+// list-length class of a tile's range (0 = the longest lists)
+__device__ __forceinline__ int order_class(uint2 r) {
+    const uint32_t c = (r.y - r.x) >> 5;
+    return ORDER_BINS - 1 - (int)(c < (uint32_t)(ORDER_BINS - 1) ? c : (uint32_t)(ORDER_BINS - 1));
+}
 
 // Workspace carve-up (bytes, 256-aligned) for (n_pad, n_views, W, H, keys_cap).
 struct WsLayout {
@@ -336,8 +341,10 @@ cudaError_t launch_project(const float* planes, int n, int n_pad, int deg, const
                            DevFlags* fl, cudaStream_t s);
 cudaError_t launch_set_sh_rest(float* planes, int n, int n_pad, int deg, const int8_t* latents, int L,
                                const float* decoder, DevFlags* fl, cudaStream_t s);
+// order_ready (optional out): true when the binning also wrote the blend's tile schedule into
+// the workspace's order region (ws + L.order + 2 ORDER_BINS), for launch_rasterize's order_pre
 cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
-                            const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof);
+                            const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof, bool* order_ready = nullptr);
 enum : int { OUT_F32 = 0, OUT_MASK = 1, OUT_RGB8 = 2, OUT_F16 = 3 };  // k_blend epilogues
 #ifndef QUEEN_BLEND_TSUB
 #define QUEEN_BLEND_TSUB 1  // blend transmittance T' = T - aT (aT = alpha T is formed anyway) instead of T (1 - alpha)
@@ -345,7 +352,8 @@ enum : int { OUT_F32 = 0, OUT_MASK = 1, OUT_RGB8 = 2, OUT_F16 = 3 };  // k_blend
 cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
                              uint8_t* out8, int out_mode, float mask_thresh, uint32_t* order_ws, cudaStream_t s,
-                             int* n_launch = nullptr, Prof* prof = nullptr, int opts = 0);
+                             int* n_launch = nullptr, Prof* prof = nullptr, int opts = 0,
+                             const uint32_t* order_pre = nullptr);
 // blend schedule: *order = longest-list-first permutation of the blocks gt tiles (in order_ws),
 // or nullptr (grid order) when there is no scratch
 cudaError_t launch_tile_order(const uint32_t* ranges, int64_t blocks, uint32_t* order_ws, cudaStream_t s,

@@ -375,10 +375,7 @@ constexpr int BLEND_RPT = QUEEN_BLEND_RPT;
 // Blend schedule: a permutation of the gt tiles, longest list first (list-length classes of
 // 32 entries; order inside a class arbitrary).  Tiles are independent, so the schedule never
 // changes a pixel; it only moves the long tiles away from the grid's tail.
-__device__ __forceinline__ int order_class(uint2 r) {
-    const uint32_t c = (r.y - r.x) >> 5;
-    return ORDER_BINS - 1 - (int)(c < (uint32_t)(ORDER_BINS - 1) ? c : (uint32_t)(ORDER_BINS - 1));
-}
+// (order_class: queen_internal.cuh; the render path builds the schedule inside the binning)
 
 __global__ void __launch_bounds__(256) k_order_hist(const uint2* __restrict__ ranges, int n, uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[ORDER_BINS];
@@ -445,7 +442,7 @@ cudaError_t launch_tile_order(const uint32_t* ranges, int64_t blocks, uint32_t* 
 cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges, const uint32_t* vals, int n_views,
                              int W, int H, float bg0, float bg1, float bg2, float* rgb_out, float* T_out,
                              uint8_t* out8, int out_mode, float mask_thresh, uint32_t* order_ws, cudaStream_t s,
-                             int* n_launch, Prof* prof, int opts) {
+                             int* n_launch, Prof* prof, int opts, const uint32_t* order_pre) {
     const int gx = (W + 15) / 16, gy = (H + 15) / 16;
     const int T = gx * gy;
     const int64_t blocks = (int64_t)T * n_views;
@@ -454,12 +451,19 @@ cudaError_t launch_rasterize(const float* rec, int n_pad, const uint32_t* ranges
     // stage profiler (when given): the tile schedule and the blend are separate stages, so the
     // blend stage times k_blend alone (bench.py's roofline divides its work by that time)
     if (prof) prof->begin(ST_BLEND_ORDER, s);
-    if (cudaError_t e = launch_tile_order(ranges, blocks, order_ws, s, &order, opts)) return e;
-    if (prof) {
+    if (order_pre && !(opts & QUEEN_OPT_BLEND_GRID_ORDER)) {
+        order = order_pre;  // built by the binning (launch_bin_sort's order_ready)
+        if (prof) {
+            prof->end(s, 0);
+            prof->begin(ST_BLEND, s);
+        }
+    } else if (cudaError_t e = launch_tile_order(ranges, blocks, order_ws, s, &order, opts)) {
+        return e;
+    } else if (prof) {
         prof->end(s, order ? 2 : 0);
         prof->begin(ST_BLEND, s);
     }
-    if (n_launch) *n_launch = order ? 3 : 1;
+    if (n_launch) *n_launch = (order && order != order_pre) ? 3 : 1;
     if (opts & QUEEN_OPT_BLEND_NOMASK)  // test option: per-thread box cull only (no warp record lists)
         k_blend<false, BLEND_RPT, false><<<(unsigned)blocks, 256 / BLEND_RPT, 0, s>>>(
             reinterpret_cast<const float4*>(rec), n_pad, reinterpret_cast<const uint2*>(ranges), vals, W, H, gx, T, bg0, bg1,

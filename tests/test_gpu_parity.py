@@ -434,6 +434,42 @@ def test_blend_warp_mask_is_exact():
     _check_image(rgb_a, T_a, rgb, T)
 
 
+def test_render_tile_schedule_from_binning_is_exact():
+    """queen_render_views blends with the tile schedule the binning built (k_slab_compact class
+    counts + k_piece_count permutation): into NaN-filled outputs, the image equals the
+    grid-order render bit for bit (so the schedule covers every tile exactly once) and the
+    oracle's, for one and two view batches."""
+    import paper_2412_04469_b200 as Q
+    from paper_2412_04469_b200.runtime import Player
+    cfg, sc, cams = _render_case("n3dv", 20003, 4, width=333, height=250, focal=280.0)
+    ref_rgb, ref_T = None, None
+    for vpb in (None, 2):
+        pl = Player(sc.planes, sc.n, sc.deg, cams, views_per_batch=vpb, with_T=True)
+        pl.fit_capacity()
+        outs = []
+        for opts in (0, Q.QUEEN_OPT_BLEND_GRID_ORDER):
+            for c in pl.ctxs:
+                c.set_options(opts)
+            pl.rgb.fill_(float("nan"))
+            pl.T.fill_(float("nan"))
+            pl.render()
+            torch.cuda.synchronize()
+            outs.append((pl.rgb.clone(), pl.T.clone()))
+        for c in pl.ctxs:
+            c.set_options(0)
+        (a_rgb, a_T), (b_rgb, b_T) = outs
+        assert not torch.isnan(a_rgb).any() and not torch.isnan(a_T).any(), vpb
+        assert torch.equal(a_rgb.view(torch.int32), b_rgb.view(torch.int32)), vpb
+        assert torch.equal(a_T.view(torch.int32), b_T.view(torch.int32)), vpb
+        if ref_rgb is None:
+            ref_rgb, ref_T = a_rgb, a_T
+        else:
+            assert torch.equal(a_rgb.view(torch.int32), ref_rgb.view(torch.int32))
+        assert pl.check_status()[0] == 0
+    proj, bins, rgb, T = oracle.render(sc.planes, sc.n, sc.deg, cams)
+    _check_image(ref_rgb.cpu().numpy(), ref_T.cpu().numpy(), rgb, T)
+
+
 def test_blend_counts_match_oracle():
     """queen_blend_counts (the bench's roofline work counters) == the oracle's counts: evaluated
     (alive pixel x record) and composited pairs; equal up to the rare pixel whose T crosses 1e-4
