@@ -937,12 +937,13 @@ def main():
         # stream, and a D2H of the images of this rank's views (own stream, double-buffered), so
         # the copies of frame k overlap the compute of frames k +- 1 like a real player.
         pin_pk = [torch.from_numpy(b).pin_memory() for b in host_bufs] if rank == 0 else None
-        odt = {"rgb8": torch.uint8, "f16": torch.float16, "f32": torch.float32}[fmt]
+        odt = {"rgb8": torch.uint8, "f16": torch.float16, "f32": torch.float32, "rgb10": torch.int32}[fmt]
+        oshape = (player.rgb.shape[0],) + tuple(player.rgb.shape[2:]) if fmt == "rgb10" else player.rgb.shape
         # frame_lanes + 1 image slots: with two-lane steps frame k+frame_lanes' binning may start
         # while frame k's D2H is still running, so a slot is reused frame_lanes + 1 frames later
         NB = player.frame_lanes + 1
-        out_dev = [torch.empty(player.rgb.shape, dtype=odt, device=dev) for _ in range(NB)]
-        out_host = [torch.empty(player.rgb.shape, dtype=odt).pin_memory() for _ in range(NB)]
+        out_dev = [torch.empty(oshape, dtype=odt, device=dev) for _ in range(NB)]
+        out_host = [torch.empty(oshape, dtype=odt).pin_memory() for _ in range(NB)]
         recv = [torch.zeros(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
         mkpkt = (lambda b: EntropyPacket(b, hdr)) if entropy else (lambda b: wire_packet(b, hdr))
         dp_recv = [mkpkt(r) for r in recv]
@@ -1036,16 +1037,20 @@ def main():
                                    "of the oracle, above the 2e-3 RGB bar)",
                            "f16": "f16: binary16 [V][3][H][W] (queen_render_views_f16; within 2^-11 of the fp32 "
                                   "image, inside the 2e-3 RGB bar)",
-                           "f32": "fp32 [V][3][H][W] (queen_render_views)"}[fmt],
+                           "f32": "fp32 [V][3][H][W] (queen_render_views)",
+                           "rgb10": "rgb10: packed R10G10B10A2 u32 [V][H][W] display format (queen_render_views_rgb10; "
+                                    "round(clamp(x) * 1023): within 4.9e-4 of the fp32 image, inside the 2e-3 RGB "
+                                    "bar; 4 B per pixel vs 6 for f16)"}[fmt],
                 "note": "runtime.Player public API: pinned H2D of each frame's wire packet + entropy decode + apply + "
                         "render + D2H of this rank's images, copies on their own streams (double-buffered), timed "
                         "from the first H2D to the last D2H; working set per frame >> L2; frame_latency_ms = median "
                         "of (packet H2D start -> frame rendered on the device), max over ranks"}
 
-    e2e = e2e_f32 = None
+    e2e = e2e_f32 = e2e_f16 = None
     e2e_u8 = None
     if not args.no_e2e:
-        e2e = run_e2e("f16")  # headline: an output that keeps the 2e-3 RGB bar
+        e2e = run_e2e("rgb10")  # headline: the most compact output that keeps the 2e-3 RGB bar
+        e2e_f16 = run_e2e("f16")
         e2e_u8 = run_e2e("rgb8")
         e2e_f32 = run_e2e("f32")
 
@@ -1096,7 +1101,7 @@ def main():
             "path_roofline": path, "paper_style": paper, "library_sort": libsort, "masked_render": masked, "densify": densify, "backward": backward,
             "first_frame": first_frame,
             "eager": eager, "graph_pipelined": graph_pipelined,
-            "e2e_f32": e2e_f32, "e2e_u8": e2e_u8, "cpu_baseline": cpu, "e2e": e2e,
+            "e2e_f32": e2e_f32, "e2e_u8": e2e_u8, "e2e_f16": e2e_f16, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": gpu_launches, "clocks": clk,
         }
         print(json.dumps(line))

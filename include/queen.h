@@ -233,6 +233,16 @@ queen_status queen_rasterize_f16(queen_ctx* ctx, const queen_proj* proj, const q
                                  float* T_out, void* stream);
 queen_status queen_render_views_f16(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
                                     int32_t n_views, const float bg[3], uint16_t* f16_out, float* T_out, void* stream);
+/* Packed 10-bit display variants (R10G10B10A2, the compact streaming output that keeps the 2e-3
+ * RGB bar: 1/2 LSB = 4.9e-4): rgb10_out u32 [n_views][H][W], one word per pixel,
+ * r | g << 10 | b << 20 | 3 << 30 with each channel round-half-even(clamp(C + T bg, 0, 1) * 1023)
+ * in fp32 -- 4 bytes per pixel vs 6 for binary16 planar; T_out as above (nullable). */
+queen_status queen_rasterize_rgb10(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
+                                   const queen_camera* cams, int32_t n_views, const float bg[3], uint32_t* rgb10_out,
+                                   float* T_out, void* stream);
+queen_status queen_render_views_rgb10(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
+                                      int32_t n_views, const float bg[3], uint32_t* rgb10_out, float* T_out,
+                                      void* stream);
 
 /* Debug / evidence: per-view blend work counters (evaluated and composited
  * (pixel, Gaussian) pairs, int64 device arrays [n_views]); same semantics as the

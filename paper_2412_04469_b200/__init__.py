@@ -35,7 +35,8 @@ EXPORTS = ["queen_create", "queen_destroy", "queen_last_error", "queen_version",
            "queen_entropy_decode", "queen_entropy_decode_frame", "queen_render_mask",
            "queen_densify", "queen_rasterize_rgb8", "queen_render_views_rgb8",
            "queen_rasterize_backward", "queen_project_backward", "queen_decode_backward", "queen_set_options",
-           "queen_rasterize_f16", "queen_render_views_f16", "queen_set_sh_rest"]
+           "queen_rasterize_f16", "queen_render_views_f16", "queen_set_sh_rest",
+           "queen_rasterize_rgb10", "queen_render_views_rgb10"]
 STAGES = ["apply", "project", "compact", "depth_sort", "bucket", "emit", "ranges", "blend", "entropy", "blend_order"]
 
 
@@ -121,6 +122,10 @@ def lib() -> C.CDLL:
             "queen_rasterize_f16": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
                                            C.POINTER(C.c_float), p, p, p]),
             "queen_render_views_f16": (i32, [p, C.POINTER(QueenGaussians), C.POINTER(QueenCamera), i32,
+                                              C.POINTER(C.c_float), p, p, p]),
+            "queen_rasterize_rgb10": (i32, [p, C.POINTER(QueenProj), C.POINTER(QueenBins), C.POINTER(QueenCamera), i32,
+                                           C.POINTER(C.c_float), p, p, p]),
+            "queen_render_views_rgb10": (i32, [p, C.POINTER(QueenGaussians), C.POINTER(QueenCamera), i32,
                                               C.POINTER(C.c_float), p, p, p]),
             "queen_densify": (i32, [p, C.POINTER(QueenGaussians), p, i32, p, i32, C.POINTER(QueenGaussians), p]),
             "queen_render_mask": (i32, [p, C.POINTER(QueenGaussians), p, i32, p, C.POINTER(QueenCamera), i32, C.c_float,
@@ -385,6 +390,24 @@ def queen_render_views_f16(ctx: Context, scene: QueenGaussians, cams, f16_out, T
     st = lib().queen_render_views_f16(ctx.handle, C.byref(scene), arr, len(arr), bgv, _ptr(f16_out), _ptr(T_out),
                                        C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_render_views_f16")
+
+
+def queen_rasterize_rgb10(ctx: Context, proj: QueenProj, bins: QueenBins, cams, rgb10_out, T_out=None,
+                         bg=(0.0, 0.0, 0.0), stream=None):
+    arr = camera_array(cams)
+    bgv = (C.c_float * 3)(*[float(x) for x in bg])
+    st = lib().queen_rasterize_rgb10(ctx.handle, C.byref(proj), C.byref(bins), arr, len(arr), bgv, _ptr(rgb10_out),
+                                    _ptr(T_out), C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_rasterize_rgb10")
+
+
+def queen_render_views_rgb10(ctx: Context, scene: QueenGaussians, cams, rgb10_out, T_out=None, bg=(0.0, 0.0, 0.0),
+                            stream=None, cam_array=None):
+    arr = cam_array if cam_array is not None else camera_array(cams)
+    bgv = (C.c_float * 3)(*[float(x) for x in bg])
+    st = lib().queen_render_views_rgb10(ctx.handle, C.byref(scene), arr, len(arr), bgv, _ptr(rgb10_out), _ptr(T_out),
+                                       C.c_void_p(_stream(stream)))
+    ctx._chk(st, "queen_render_views_rgb10")
 
 
 def queen_rasterize_backward(ctx: Context, proj: QueenProj, bins: QueenBins, cams, dL_drgb, grad_rec,

@@ -354,6 +354,14 @@ queen_status queen_rasterize_f16(queen_ctx* ctx, const queen_proj* proj, const q
                           OUT_F16);
 }
 
+queen_status queen_rasterize_rgb10(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
+                                 const queen_camera* cams, int32_t n_views, const float bg[3], uint32_t* rgb10_out,
+                                 float* T_out, void* stream) {
+    if (ctx && !rgb10_out) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null rgb10_out");
+    return rasterize_impl(ctx, proj, bins, cams, n_views, bg, nullptr, T_out, reinterpret_cast<uint8_t*>(rgb10_out), stream,
+                          OUT_RGB10);
+}
+
 queen_status queen_rasterize_rgb8(queen_ctx* ctx, const queen_proj* proj, const queen_bins* bins,
                                   const queen_camera* cams, int32_t n_views, const float bg[3], uint8_t* rgb8_out,
                                   float* T_out, void* stream) {
@@ -519,6 +527,12 @@ queen_status queen_render_views_f16(queen_ctx* ctx, const queen_gaussians* scene
                                     int32_t n_views, const float bg[3], uint16_t* f16_out, float* T_out, void* stream) {
     if (ctx && !f16_out) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null f16_out");
     return render_impl(ctx, scene, cams, n_views, bg, nullptr, T_out, reinterpret_cast<uint8_t*>(f16_out), stream, OUT_F16);
+}
+
+queen_status queen_render_views_rgb10(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,
+                                    int32_t n_views, const float bg[3], uint32_t* rgb10_out, float* T_out, void* stream) {
+    if (ctx && !rgb10_out) return fail(ctx, QUEEN_ERR_INVALID_ARG, "null rgb10_out");
+    return render_impl(ctx, scene, cams, n_views, bg, nullptr, T_out, reinterpret_cast<uint8_t*>(rgb10_out), stream, OUT_RGB10);
 }
 
 queen_status queen_render_views_rgb8(queen_ctx* ctx, const queen_gaussians* scene, const queen_camera* cams,

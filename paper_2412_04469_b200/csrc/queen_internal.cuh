@@ -345,7 +345,7 @@ cudaError_t launch_set_sh_rest(float* planes, int n, int n_pad, int deg, const i
 // the workspace's order region (ws + L.order + 2 ORDER_BINS), for launch_rasterize's order_pre
 cudaError_t launch_bin_sort(const queen_proj& proj, int n_views, int W, int H, queen_bins& bins, void* scratch,
                             const WsLayout& L, DevFlags* fl, cudaStream_t s, Prof* prof, bool* order_ready = nullptr);
-enum : int { OUT_F32 = 0, OUT_MASK = 1, OUT_RGB8 = 2, OUT_F16 = 3 };  // k_blend epilogues
+enum : int { OUT_F32 = 0, OUT_MASK = 1, OUT_RGB8 = 2, OUT_F16 = 3, OUT_RGB10 = 4 };  // k_blend epilogues
 #ifndef QUEEN_BLEND_TSUB
 #define QUEEN_BLEND_TSUB 1  // blend transmittance T' = T - aT (aT = alpha T is formed anyway) instead of T (1 - alpha)
 #endif

@@ -326,6 +326,28 @@ __global__ void __launch_bounds__(256 / RPT, QUEEN_BLEND_MINB) k_blend(const flo
         }
         return;
     }
+    if (out_mode == OUT_RGB10) {  // packed 10-bit display format (R10G10B10A2): one u32 per pixel
+        if (px < W) {
+            const int64_t plane = (int64_t)H * W;
+            uint32_t* o10 = reinterpret_cast<uint32_t*>(out8) + (int64_t)v * plane + px;
+            float* to = T_out ? T_out + (int64_t)v * plane + px : nullptr;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                if (row_of(r) < H) {
+                    const int64_t ro = (int64_t)row_of(r) * W;
+                    const Px2& q = p[r >> 1];
+                    const float pr = (r & 1) ? q.r.y : q.r.x, pg = (r & 1) ? q.g.y : q.g.x, pb = (r & 1) ? q.b.y : q.b.x;
+                    const float pT = (r & 1) ? q.T.y : q.T.x;
+                    const uint32_t r10 = __float2uint_rn(fminf(fmaxf(pr + pT * bg0, 0.0f), 1.0f) * 1023.0f);
+                    const uint32_t g10 = __float2uint_rn(fminf(fmaxf(pg + pT * bg1, 0.0f), 1.0f) * 1023.0f);
+                    const uint32_t b10 = __float2uint_rn(fminf(fmaxf(pb + pT * bg2, 0.0f), 1.0f) * 1023.0f);
+                    o10[ro] = r10 | (g10 << 10) | (b10 << 20) | (3u << 30);
+                    if (to) to[ro] = pT;
+                }
+            }
+        }
+        return;
+    }
     if (out_mode == OUT_RGB8) {  // display format: round(clamp(C + T bg, 0, 1) * 255), planar u8
         if (px < W) {
             const int64_t plane = (int64_t)H * W;

@@ -11,27 +11,32 @@ import torch
 from . import (QUEEN_LAT_F32, QUEEN_LAT_INT8, QUEEN_MAX_VIEWS, QUEEN_POS_COO, QUEEN_POS_GATES, Context,
                QueenError, camera_array, gaussians_struct, packet_struct, queen_apply_frame,
                queen_densify, queen_entropy_decode_frame, queen_render_mask, queen_render_views,
-               queen_render_views_f16, queen_render_views_rgb8, queen_set_blend_stream, queen_wait_binned,
+               queen_render_views_f16, queen_render_views_rgb8, queen_render_views_rgb10, queen_set_blend_stream,
+               queen_wait_binned,
                queen_wait_projected)
 from . import packet as wire
 
 
 _OUT_FNS = {"f32": (queen_render_views, torch.float32), "rgb8": (queen_render_views_rgb8, torch.uint8),
-            "f16": (queen_render_views_f16, torch.float16)}
+            "f16": (queen_render_views_f16, torch.float16),
+            "rgb10": (queen_render_views_rgb10, torch.int32)}
 
 
 def _out_fn(rgb8, out):
     """Output format of a render call: rgb8=True or a uint8 `out` -> u8 display format; a float16
-    `out` -> binary16; else fp32."""
+    `out` -> binary16; an int32 `out` ([V][H][W]) -> packed 10-bit R10G10B10A2; else fp32."""
     if rgb8 is True or rgb8 == "rgb8" or (out is not None and out.dtype == torch.uint8):
         fmt = "rgb8"
     elif rgb8 == "f16" or (out is not None and out.dtype == torch.float16):
         fmt = "f16"
+    elif rgb8 == "rgb10" or (out is not None and out.dtype == torch.int32):
+        fmt = "rgb10"
     else:
         fmt = "f32"
     fn, dt = _OUT_FNS[fmt]
     if fmt != "f32" and (out is None or out.dtype != dt):
-        raise ValueError(f"{fmt} rendering needs an out tensor of dtype {dt} [V][3][H][W]")
+        shape = "[V][H][W]" if fmt == "rgb10" else "[V][3][H][W]"
+        raise ValueError(f"{fmt} rendering needs an out tensor of dtype {dt} {shape}")
     return fn
 
 

@@ -539,6 +539,36 @@ def test_render_views_f16_output():
     assert err <= RGB_TOL, err
 
 
+def test_render_views_rgb10_output():
+    """queen_render_views_rgb10 = the fp32 render packed as R10G10B10A2 (each channel
+    round-half-even(clamp(x, 0, 1) * 1023) in fp32: GPU vs GPU bit-exact, also through the
+    Player's two-lane step), and within the 2e-3 RGB bar of the oracle (1/2 LSB = 4.9e-4)."""
+    from paper_2412_04469_b200.runtime import Player
+    cfg, sc, cams = _render_case("n3dv", 20003, 3, width=333, height=250, focal=280.0)
+    bg = (0.2, 0.4, 0.6)
+    pl = Player(sc.planes, sc.n, sc.deg, cams, bg=bg)
+    pl.fit_capacity()
+    f32 = pl.render().clone()
+    V, _, H, W = f32.shape
+    p10 = torch.empty((V, H, W), dtype=torch.int32, device="cuda")
+    pl.render(out=p10)
+    torch.cuda.synchronize()
+    q = torch.round(torch.clamp(f32, 0.0, 1.0) * 1023.0).to(torch.int64)  # torch.round: half to even
+    want = q[:, 0] | (q[:, 1] << 10) | (q[:, 2] << 20) | (3 << 30)
+    got = p10.to(torch.int64) & 0xffffffff
+    assert torch.equal(got, want)
+    dec = torch.stack([(got >> (10 * c)) & 1023 for c in range(3)], 1).double() / 1023.0
+    _, _, ref, _ = oracle.render(sc.planes, sc.n, sc.deg, cams, bg=bg)
+    err = np.abs(dec.cpu().numpy() - np.clip(ref, 0, 1)).max()
+    assert err <= RGB_TOL, err
+    # the two-lane step into per-frame rgb10 buffers
+    out2 = torch.empty_like(p10)
+    pl.step2(None, out=out2)
+    pl.sync_lanes()
+    torch.cuda.synchronize()
+    assert torch.equal(out2, p10)
+
+
 def test_cuda_graph_frame_equals_eager():
     """A captured frame step (entropy decode + apply + render, Player.capture) replays to the
     same SoA and images, bit for bit, as the eager calls."""
