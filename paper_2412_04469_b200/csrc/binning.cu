@@ -827,8 +827,8 @@ constexpr int CS_ROUNDS = 8;
 __global__ void __launch_bounds__(256) k_piece_colscan(uint32_t* __restrict__ pcnt, const uint32_t* __restrict__ Kd_in,
                                                        BucketGeo g, uint32_t* __restrict__ ptotal,
                                                        uint32_t* __restrict__ pbase, uint32_t* __restrict__ ebase,
-                                                       uint32_t* __restrict__ meta, uint32_t* __restrict__ Kd,
-                                                       uint32_t* ticket) {
+                                                       uint32_t* __restrict__ meta, uint32_t* Kd,
+                                                       uint32_t* ticket) {  // (Kd aliases Kd_in: [3] written, [1..2] read)
     const int b = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (b < g.VNB) {  // warp-uniform

@@ -327,41 +327,50 @@ class Player:
                 self._lanes2.append((ctx, torch.cuda.Stream(device=self.dev, priority=hi), bs))
             self._lane_t = 0
             self._side = getattr(self, "_side", None) or torch.cuda.Stream(device=self.dev, priority=hi)
-        lane = self._lane_t % len(self._lanes2)
-        ctx, ls, bs = self._lanes2[lane]
-        self._lane_t += 1
-        ls.wait_stream(main)  # the frame's apply (and the caller's ordering) first
-        if out is None or self.T is not None:  # the two lanes' blends overlap: per-lane buffers
+        nl = len(self._lanes2)
+        fb = getattr(self, "_frame_t", 0) % nl  # this frame's image buffer (out=None) / consumer fence
+        self._frame_t = getattr(self, "_frame_t", 0) + 1
+        if out is None or self.T is not None:  # the lanes' blends overlap: per-frame-slot buffers
             if not hasattr(self, "rgb_lanes"):
-                nl = len(self._lanes2)
                 self.rgb_lanes = [self.rgb] + [torch.empty_like(self.rgb) for _ in range(nl - 1)]
                 self.T_lanes = ([self.T] + [torch.empty_like(self.T) for _ in range(nl - 1)] if self.T is not None
                                 else [None] * nl)
-        rgb = self.rgb_lanes[lane] if out is None else out
-        T = self.T_lanes[lane] if self.T is not None else None
+        rgb = self.rgb_lanes[fb] if out is None else out
+        T = self.T_lanes[fb] if self.T is not None else None
         if not hasattr(self, "_consumed"):
-            self._consumed = [None] * len(self._lanes2)
-        if self._consumed[lane] is not None:  # the reader of this lane's previous image is done
-            bs.wait_event(self._consumed[lane])
-        self._consumed[lane] = consumed if out is None else None
+            self._consumed = [None] * nl
+        wait_consumed = self._consumed[fb]  # the reader of this slot's previous image is done
+        self._consumed[fb] = consumed if out is None else None
         fn = _out_fn(rgb8, out)
-        # frames complete in order: with more than two lanes this frame's blend starts after the
-        # previous frame's (a later frame could otherwise finish first; measured at 3-4 lanes);
-        # the binning of later frames still runs ahead on their own lanes.  Two lanes complete
-        # in order anyway, and there the blends' tails may overlap.
-        if len(self._lanes2) > 2 and getattr(self, "_blend_done", None) is not None:
-            bs.wait_event(self._blend_done)
-        queen_set_blend_stream(ctx, bs)  # only for these calls: render() / step() keep one stream
-        try:
-            for (a, b), arr in zip(self.batches, self.cam_arrays):
+        # The lanes rotate per view BATCH (one batch per frame: per frame), so in a multi-batch
+        # frame batch b+1's projection + binning run under batch b's blend on another lane.
+        # Blends complete in order when there is more than one batch or more than two lanes (each
+        # waits for the previous blend; a later, shorter one could otherwise finish first): the
+        # last batch's blend then marks the frame complete.  Two lanes with one batch per frame
+        # complete in order anyway, and there the blends' tails may overlap.
+        ordered = nl > 2 or len(self.batches) > 1
+        used = []
+        for (a, b), arr in zip(self.batches, self.cam_arrays):
+            lane = self._lane_t % nl
+            self._lane_t += 1
+            ctx, ls, bs = self._lanes2[lane]
+            ls.wait_stream(main)  # the frame's apply (and the caller's ordering) first
+            if wait_consumed is not None:
+                bs.wait_event(wait_consumed)
+            if ordered and getattr(self, "_blend_done", None) is not None:
+                bs.wait_event(self._blend_done)
+            queen_set_blend_stream(ctx, bs)  # only for these calls: render() / step() keep one stream
+            try:
                 fn(ctx, self.scene, None, rgb[a:b], None if T is None else T[a:b], self.bg, ls, cam_array=arr)
-        finally:
-            queen_set_blend_stream(ctx, None)
-        if len(self._lanes2) > 2:
-            self._blend_done = torch.cuda.Event()
-            self._blend_done.record(bs)
+            finally:
+                queen_set_blend_stream(ctx, None)
+            if ordered:
+                self._blend_done = torch.cuda.Event()
+                self._blend_done.record(bs)
+            if ctx not in [u for u, _ in used]:
+                used.append((ctx, bs))
         if rendered is not None:
-            rendered.record(bs)
+            rendered.record(bs)  # the last batch's blend (ordered: after every earlier one)
         if next_pkt is not None:
             side = self._side
             side.wait_stream(main)
@@ -372,12 +381,15 @@ class Player:
                     # the projection is the render's only read of A_t (binning and blend read
                     # the lane's projected records), so the packet decodes at once and A_{t+1}
                     # is applied under this frame's binning: the next frame's projection no
-                    # longer waits for this frame's binning chain
+                    # longer waits for this frame's binning chain (every lane this frame used:
+                    # the latest projection on each is this frame's)
                     if isinstance(next_pkt, EntropyPacket):
                         next_pkt.decode(ctx, side)
-                    queen_wait_projected(ctx, side)
+                    for c, _ in used:
+                        queen_wait_projected(c, side)
                 else:
-                    queen_wait_binned(ctx, side)
+                    for c, _ in used:
+                        queen_wait_binned(c, side)
                     if isinstance(next_pkt, EntropyPacket):
                         next_pkt.decode(ctx, side)
                 queen_apply_frame(ctx, self.scene, next_pkt.struct, side)
