@@ -72,10 +72,12 @@ def parse():
 
 
 def default_vpb(cfg):
-    """Views per batch: as many as fit (a) two 9-bit tile-sort passes (batch tiles <= 2^18: a
-    third pass costs more than a second batch; measured stress 8 -> 14 views: 14.4 -> 12.9
-    frames/s) and (b) ~12 GB of key buffers (~24 B/key x ~8 keys/Gaussian/view).  Immersive's 46
-    views then render as one batch (298 vs 278 frames/s as 23 + 23)."""
+    """Views per batch: as many as keep (a) the batch within 2^18 tiles -- round 1's tile-sort
+    passes set this; with the bucketed emission the bucket stage's per-(bucket, chunk) counters
+    grow with the batch's buckets instead (measured round 2, stress 8 / 11 / 13 / 16 / 32 views
+    per batch: 19.4 / 19.3 / 19.1 / 18.7 / 16.9 frames/s), so the cap stays -- and (b) ~12 GB of
+    key buffers (~24 B/key x ~8 keys/Gaussian/view).  Immersive's 46 views then render as one
+    batch (298 vs 278 frames/s as 23 + 23)."""
     tiles = ((cfg.width + 15) // 16) * ((cfg.height + 15) // 16)
     per_view = 8 * cfg.n * 24 * 1.5
     return int(max(1, min(cfg.views, 64, (12 << 30) // per_view, (1 << 18) // tiles)))
