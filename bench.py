@@ -1081,8 +1081,9 @@ def main():
                        "apply_after": args.apply_after if (use_graph and two_lane) else "binned",
                        "parallelism": f"views sharded v mod {world}, Gaussians replicated, packet NCCL-broadcast",
                        "packet_format": args.packet_format,
-                       "launch": ("eager two-lane steps: frame t+1's binning (own context, high-priority "
-                                  "stream) and decode + apply under frame t's blend"
+                       "launch": ("eager pipelined steps over frame_lanes contexts: frame t+1's binning (own "
+                                  "context, high-priority stream) under frame t's blend; packet t+1 decoded at "
+                                  "once and applied after frame t's projection (apply_after)"
                                   if (use_graph and two_lane) else
                                   ("CUDA-graph replay (one graph per packet slot)" if use_graph else "eager") +
                                   ("; pipelined: decode + apply of frame t+1 under the blend of frame t"
