@@ -427,10 +427,19 @@ def main():
     if world != args.gpus and world == 1 and args.gpus > 1:
         print(json.dumps({"error": "for --gpus N>1 launch with torchrun (one process per GPU)"}))
         return 2
+    # QUEEN_BENCH_ONE_GPU=1 / QUEEN_BENCH_BACKEND=gloo: validation of the N > 1 code path on one
+    # GPU (every rank on cuda:0, host-side collectives, so no rank's kernel waits on another's);
+    # its timings mean nothing.  The driver's multi-GPU run uses neither.
+    if os.environ.get("QUEEN_BENCH_ONE_GPU"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("QUEEN_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     cfg = synth.get_config(args.config)
     sc = synth.make_scene(cfg)
