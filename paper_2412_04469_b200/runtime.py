@@ -327,6 +327,12 @@ class Player:
                 self._lanes2.append((ctx, torch.cuda.Stream(device=self.dev, priority=hi), bs))
             self._lane_t = 0
             self._side = getattr(self, "_side", None) or torch.cuda.Stream(device=self.dev, priority=hi)
+            # reused events (a stream wait takes the event's latest record at enqueue time, and
+            # each is re-recorded only after its waits are enqueued): cheaper on the host than
+            # wait_stream's fresh event per call -- the host cost bounds short multi-GPU frames
+            self._ev_main, self._ev_side = torch.cuda.Event(), torch.cuda.Event()
+            self._ev_blend = [torch.cuda.Event() for _ in self._lanes2]
+            self._last_blend = None  # the previous batch's blend event (ordered completion)
         nl = len(self._lanes2)
         fb = getattr(self, "_frame_t", 0) % nl  # this frame's image buffer (out=None) / consumer fence
         self._frame_t = getattr(self, "_frame_t", 0) + 1
@@ -350,50 +356,51 @@ class Player:
         # complete in order anyway, and there the blends' tails may overlap.
         ordered = nl > 2 or len(self.batches) > 1
         used = []
+        self._ev_main.record(main)  # the frame's apply (and the caller's ordering) first
         for (a, b), arr in zip(self.batches, self.cam_arrays):
             lane = self._lane_t % nl
             self._lane_t += 1
             ctx, ls, bs = self._lanes2[lane]
-            ls.wait_stream(main)  # the frame's apply (and the caller's ordering) first
+            ls.wait_event(self._ev_main)
             if wait_consumed is not None:
                 bs.wait_event(wait_consumed)
-            if ordered and getattr(self, "_blend_done", None) is not None:
-                bs.wait_event(self._blend_done)
+            if ordered and self._last_blend is not None:
+                bs.wait_event(self._last_blend)
             queen_set_blend_stream(ctx, bs)  # only for these calls: render() / step() keep one stream
             try:
                 fn(ctx, self.scene, None, rgb[a:b], None if T is None else T[a:b], self.bg, ls, cam_array=arr)
             finally:
                 queen_set_blend_stream(ctx, None)
             if ordered:
-                self._blend_done = torch.cuda.Event()
-                self._blend_done.record(bs)
+                self._last_blend = self._ev_blend[lane]
+                self._last_blend.record(bs)
             if ctx not in [u for u, _ in used]:
                 used.append((ctx, bs))
         if rendered is not None:
             rendered.record(bs)  # the last batch's blend (ordered: after every earlier one)
         if next_pkt is not None:
             side = self._side
-            side.wait_stream(main)
-            with torch.cuda.stream(side):
-                if ready is not None:
-                    side.wait_event(ready)
-                if self.apply_after == "projected":
-                    # the projection is the render's only read of A_t (binning and blend read
-                    # the lane's projected records), so the packet decodes at once and A_{t+1}
-                    # is applied under this frame's binning: the next frame's projection no
-                    # longer waits for this frame's binning chain (every lane this frame used:
-                    # the latest projection on each is this frame's)
-                    if isinstance(next_pkt, EntropyPacket):
-                        next_pkt.decode(ctx, side)
-                    for c, _ in used:
-                        queen_wait_projected(c, side)
-                else:
-                    for c, _ in used:
-                        queen_wait_binned(c, side)
-                    if isinstance(next_pkt, EntropyPacket):
-                        next_pkt.decode(ctx, side)
-                queen_apply_frame(ctx, self.scene, next_pkt.struct, side)
-            main.wait_stream(side)
+            side.wait_event(self._ev_main)
+            if ready is not None:
+                side.wait_event(ready)
+            if self.apply_after == "projected":
+                # the projection is the render's only read of A_t (binning and blend read the
+                # lane's projected records), so the packet decodes at once and A_{t+1} is applied
+                # under this frame's binning: the next frame's projection no longer waits for
+                # this frame's binning chain (every lane this frame used: the latest projection
+                # on each is this frame's)
+                if isinstance(next_pkt, EntropyPacket):
+                    next_pkt.decode(ctx, side)
+                for c, _ in used:
+                    queen_wait_projected(c, side)
+            else:
+                for c, _ in used:
+                    queen_wait_binned(c, side)
+                if isinstance(next_pkt, EntropyPacket):
+                    next_pkt.decode(ctx, side)
+            queen_apply_frame(ctx, self.scene, next_pkt.struct, side)
+            self._ev_side.record(side)
+            main.wait_event(self._ev_side)
         return rgb
 
     def sync_lanes(self):
