@@ -469,9 +469,11 @@ def queen_entropy_decode(ctx: Context, stream_dev, L: int, n: int, latents_out, 
 def queen_entropy_decode_frame(ctx: Context, stream_ptrs, stream_bytes, lat_dim, n: int, latents_out, stream=None):
     """Decode every category of a frame in one launch (stream_ptrs: 5 device addresses or None;
     stream_bytes: the 5 stream sizes)."""
-    ptrs = (C.c_void_p * 5)(*[C.c_void_p(int(p)) if p else None for p in stream_ptrs])
-    nbs = (C.c_int64 * 5)(*[int(x) for x in stream_bytes])
-    dims = (C.c_int32 * 5)(*[int(x) for x in lat_dim])
+    # (ctypes arrays are passed through: a caller decoding the same buffer every frame builds them once)
+    ptrs = stream_ptrs if isinstance(stream_ptrs, C.Array) else \
+        (C.c_void_p * 5)(*[C.c_void_p(int(p)) if p else None for p in stream_ptrs])
+    nbs = stream_bytes if isinstance(stream_bytes, C.Array) else (C.c_int64 * 5)(*[int(x) for x in stream_bytes])
+    dims = lat_dim if isinstance(lat_dim, C.Array) else (C.c_int32 * 5)(*[int(x) for x in lat_dim])
     st = lib().queen_entropy_decode_frame(ctx.handle, ptrs, nbs, dims, n, latents_out.shape[-1], _ptr(latents_out),
                                           C.c_void_p(_stream(stream)))
     ctx._chk(st, "queen_entropy_decode_frame")

@@ -108,13 +108,20 @@ class EntropyPacket:
             self.struct.pos_val = None
 
     def decode(self, ctx: Context, stream=None):
-        base = self.buf.data_ptr()
-        ptrs = [base + self.hdr["ans_off"][c] if self.hdr["lat"][c] else None for c in range(5)]
-        # bound each stream by its fixed-capacity section (not this frame's used bytes): a captured
-        # graph replays the decode on later packets refilled into the same buffer
-        offs = [self.hdr["ans_off"][c] for c in range(5)] + [int(self.hdr.get("total", self.buf.numel()))]
-        caps = [(min(o for o in offs[c + 1:] if o > offs[c]) - offs[c]) if self.hdr["lat"][c] else 0 for c in range(5)]
-        queen_entropy_decode_frame(ctx, ptrs, caps, self.hdr["lat"], self.hdr["n"], self.latents, stream)
+        if getattr(self, "_dec_args", None) is None:  # the buffer is fixed: marshal once
+            import ctypes as C
+            base = self.buf.data_ptr()
+            ptrs = [base + self.hdr["ans_off"][c] if self.hdr["lat"][c] else None for c in range(5)]
+            # bound each stream by its fixed-capacity section (not this frame's used bytes): a
+            # captured graph replays the decode on later packets refilled into the same buffer
+            offs = [self.hdr["ans_off"][c] for c in range(5)] + [int(self.hdr.get("total", self.buf.numel()))]
+            caps = [(min(o for o in offs[c + 1:] if o > offs[c]) - offs[c]) if self.hdr["lat"][c] else 0
+                    for c in range(5)]
+            self._dec_args = ((C.c_void_p * 5)(*[C.c_void_p(int(p)) if p else None for p in ptrs]),
+                              (C.c_int64 * 5)(*[int(x) for x in caps]),
+                              (C.c_int32 * 5)(*[int(x) for x in self.hdr["lat"]]))
+        ptrs, caps, dims = self._dec_args
+        queen_entropy_decode_frame(ctx, ptrs, caps, dims, self.hdr["n"], self.latents, stream)
 
 
 class Player:
