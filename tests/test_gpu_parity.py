@@ -611,7 +611,7 @@ def test_pipelined_steps_equal_serial_frames():
     from paper_2412_04469_b200 import packet as wire
     from paper_2412_04469_b200.runtime import EntropyPacket, Player
     cfg, sc, cams = _render_case("n3dv", 20003, 3, width=333, height=250, focal=280.0)
-    pkts = [synth.make_packet(sc, t) for t in (1, 2, 3, 4)]
+    pkts = [synth.make_packet(sc, t) for t in range(1, 7)]  # 6 frames: 4 lanes reuse a slot
     streams = [wire.ans_streams(p, Q.queen_entropy_encode) for p in pkts]
     cap = [max(s[c].size for s in streams) for c in range(5)]
     kc = max(p.k for p in pkts)
@@ -673,21 +673,23 @@ def test_pipelined_steps_equal_serial_frames():
         tl2.sync_lanes()
         # out=None read on a consumer stream without host syncs: `consumed` fences the reuse of
         # each lane's buffer two frames later
-        tl3 = Player(sc.planes, sc.n, sc.deg, cams, keys_cap=serial.keys_cap, views_per_batch=vpb)
-        tl3.apply(eps[0])
-        reader = torch.cuda.Stream()
-        copies = []
-        for t in range(len(eps)):
-            ev, done = torch.cuda.Event(), torch.cuda.Event()
-            img = tl3.step2(eps[t + 1] if t + 1 < len(eps) else None, rendered=ev, consumed=done)
-            reader.wait_event(ev)
-            with torch.cuda.stream(reader):
-                copies.append(img.clone())
-                done.record(reader)
-        tl3.sync_lanes()
-        torch.cuda.synchronize()
-        for t in range(len(eps)):
-            assert torch.equal(copies[t], refs[t]), ("two-lane, consumer stream", vpb, t)
+        for nl in (2, 4):  # per-frame-slot image buffers, reused nl frames later
+            tl3 = Player(sc.planes, sc.n, sc.deg, cams, keys_cap=serial.keys_cap, views_per_batch=vpb)
+            tl3.frame_lanes = nl
+            tl3.apply(eps[0])
+            reader = torch.cuda.Stream()
+            copies = []
+            for t in range(len(eps)):
+                ev, done = torch.cuda.Event(), torch.cuda.Event()
+                img = tl3.step2(eps[t + 1] if t + 1 < len(eps) else None, rendered=ev, consumed=done)
+                reader.wait_event(ev)
+                with torch.cuda.stream(reader):
+                    copies.append(img.clone())
+                    done.record(reader)
+            tl3.sync_lanes()
+            torch.cuda.synchronize()
+            for t in range(len(eps)):
+                assert torch.equal(copies[t], refs[t]), ("two-lane, consumer stream", nl, vpb, t)
         # a plain render after two-lane steps (the lane-0 blend ran on its own stream)
         again = tl.render().clone()
         torch.cuda.synchronize()
