@@ -11,15 +11,19 @@
 //  * the tile's sorted records are staged in shared memory in batches of 64 with
 //    cp.async (LDGSTS), double-buffered: batch b+1 is in flight while batch b blends,
 //    and the record indices run one batch further ahead;
-//  * all lanes read the same record (LDS.128 broadcast), and the CTA retires as soon
-//    as all 256 pixels have terminated (__syncthreads_count);
-//  * compositing is branch-free per row pair (composite2: a non-hitting row gets alpha = +0,
-//    which leaves C and T bit-identical) and paired as well, so a warp whose lanes hit in
-//    different rows issues one short straight-line block instead of four divergent ones
-//    (SASS: 62 instructions for a fully hit record, was ~100).
-// Per-pixel arithmetic is exactly the oracle's (oracle/queen_oracle.cpp blend_step):
+//  * per batch, each warp keeps a list of the records whose alpha >= 1/255 ellipse can reach
+//    its 16 x 8 sub-tile (touches(), exact-safe), and all its lanes read the same record
+//    (LDS.128 broadcast); the CTA retires as soon as all 256 pixels have terminated
+//    (__syncthreads_count);
+//  * compositing is warp-uniform per row-pair band (one vote per 16 x 4 band) and
+//    branch-free inside it (composite2: a non-hitting row gets alpha = +0, which leaves C and
+//    T bit-identical), paired as well.
+// Per-pixel arithmetic (oracle/queen_oracle.cpp blend_step):
 //   p2 = fma(fma(C2, dy, B2 dx), dy, (A2 dx) dx);  skip if p2 < T2 (R14: no p2 > 0 skip);
-//   a = min(0.99, o 2^p2); C = fma(rgb, a T, C); T = T (1 - a); stop after T < 1e-4.
+//   a = min(0.99, o 2^p2); C = fma(rgb, a T, C); stop after T < 1e-4 -- the skip decisions are
+//   the oracle's bit for bit; the transmittance update is T - aT (QUEEN_BLEND_TSUB, one FADD2
+//   on the aT already formed) where the oracle computes T (1 - a): within 1 ulp per step, and
+//   RGB / T are checked against the oracle within the 2e-3 bar.
 #include <cstdlib>
 
 #include <cuda_fp16.h>
