@@ -16,9 +16,13 @@ namespace queen {
 #define QUEEN_DA_ROWS 4  // measured N3DV apply (L2 flushed): 8 rows x 2 blocks 57 us, 6 x 3 45 us, 4 x 4 41 us
 #endif
 // Gaussian blocks per grid super-tile: group-major over all blocks while a category's latent rows
-// stay in L2 anyway; super-tiles of 128 blocks once they do not (measured, apply stage with L2
-// flushed: stress 590 -> 516 us with 128; N3DV 42.8 us group-major vs 44.1 with 128, 47.4 with 32)
-inline int da_super(int n) { return n > (1 << 20) ? 128 : 1 << 30; }
+// stay in L2 anyway; super-tiles of 512 blocks once they do not (measured, apply stage with L2
+// flushed: stress 590 -> 516 us with 128, 506 us with 512; N3DV 42.8 us group-major vs 44.1
+// with 128, 47.4 with 32)
+#ifndef QUEEN_DA_SUPER
+#define QUEEN_DA_SUPER 512  // measured (round 2, stress apply): 64 0.533, 128 0.516, 256 0.510, 512 0.506, 1024 0.510, 1536 0.522 ms
+#endif
+inline int da_super(int n) { return n > (1 << 20) ? QUEEN_DA_SUPER : 1 << 30; }
 constexpr int DA_ROWS = QUEEN_DA_ROWS;      // attribute rows per work group (all loads in flight at once)
 constexpr int DA_MAX_GROUPS = 5 + (4 + 3 + 1 + 3 + 45 + DA_ROWS - 1) / DA_ROWS + 1;  // worst case at degree 3, + gates
 
